@@ -1,0 +1,107 @@
+// Shared device helpers for the piecy B200 kernels (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <math.h>
+
+#define PCY_FULL 0xffffffffu
+
+// ---------------------------------------------------------------------------
+// Error plumbing (host side).  Every C-ABI entry point returns 0 or a negative
+// code and leaves a message in a thread-local buffer (pcy_last_error()).
+// ---------------------------------------------------------------------------
+enum PcyStatus {
+  PCY_OK = 0,
+  PCY_EINVAL = -1,
+  PCY_ENONFINITE = -2,
+  PCY_EOVERFLOW = -3,
+  PCY_EWEIGHT = -4,
+  PCY_ECUDA = -5,
+  PCY_ENOMEM = -6,
+  PCY_ENCCL = -7,
+  PCY_ESTATE = -8,
+};
+
+void pcy_set_error(const char* fmt, ...);
+
+#define PCY_CUDA(call)                                                        \
+  do {                                                                        \
+    cudaError_t _e = (call);                                                  \
+    if (_e != cudaSuccess) {                                                  \
+      pcy_set_error("%s:%d: %s: %s", __FILE__, __LINE__, #call,              \
+                    cudaGetErrorString(_e));                                  \
+      return PCY_ECUDA;                                                       \
+    }                                                                         \
+  } while (0)
+
+#define PCY_LAUNCH_CHECK()                                                    \
+  do {                                                                        \
+    cudaError_t _e = cudaGetLastError();                                      \
+    if (_e != cudaSuccess) {                                                  \
+      pcy_set_error("%s:%d: launch: %s", __FILE__, __LINE__,                  \
+                    cudaGetErrorString(_e));                                  \
+      return PCY_ECUDA;                                                       \
+    }                                                                         \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// Explicitly rounded fp64 arithmetic.  The reference evaluates every scalar
+// decision expression as separately rounded IEEE operations (Python floats /
+// numpy, no FMA); these wrappers keep nvcc from contracting them.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double rmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double radd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double rsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double rdiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// ---------------------------------------------------------------------------
+// Warp reductions.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(PCY_FULL, v, o);
+  return v;
+}
+
+// min of (value, position); ties resolve to the lower position.
+__device__ __forceinline__ void warp_argmin(double& v, int& pos) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    double ov = __shfl_xor_sync(PCY_FULL, v, o);
+    int op = __shfl_xor_sync(PCY_FULL, pos, o);
+    if (ov < v || (ov == v && op < pos)) { v = ov; pos = op; }
+  }
+}
+
+// Lane-strided fp64 dot of two length-d vectors, all lanes get the total.
+__device__ __forceinline__ double warp_dot(const double* __restrict__ a,
+                                           const double* __restrict__ b, int d, int lane) {
+  double acc = 0.0;
+  for (int e = lane; e < d; e += 32) acc = fma(a[e], b[e], acc);
+  return warp_sum(acc);
+}
+
+// Transpose-reduce: lane l holds 32 partial sums acc[0..31] (one per member);
+// afterwards acc[0] on lane l is the full sum for member l.  31 shuffles.
+__device__ __forceinline__ double warp_transpose_reduce(double (&acc)[32], int lane) {
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const bool upper = (lane & s) != 0;
+#pragma unroll
+    for (int k = 0; k < s; ++k) {
+      double send = upper ? acc[k] : acc[k + s];
+      double keep = upper ? acc[k + s] : acc[k];
+      acc[k] = keep + __shfl_xor_sync(PCY_FULL, send, s);
+    }
+  }
+  return acc[0];
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z ^= z >> 30; z *= 0xBF58476D1CE4E5B9ULL;
+  z ^= z >> 27; z *= 0x94D049BB133111EBULL;
+  z ^= z >> 31;
+  return z;
+}
+
+static inline int64_t pcy_round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }

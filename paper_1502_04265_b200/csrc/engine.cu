@@ -1,0 +1,935 @@
+// BICO clustering-feature engine on B200 (sm_100a).
+//
+// Reference semantics: /root/reference/pkg/src/piecy/coreset.py (BicoEngine).
+// Layout and kernel roles are described in DESIGN.md §3-§4:
+//   k_stage    -- upcast/copy a block, x_sq, validation, exact-bytes hash
+//   k_boot     -- bootstrap buffering (coreset.py:283-295), one warp, in order
+//   k_mp_*     -- T0 = min positive pairwise sq. distance * m / 16 (:297-299, :479-489)
+//   k_snapshot -- freeze group counts for the chain kernel
+//   k_chain    -- K1: every item's capacity-free nearest-reference chain against
+//                 the snapshot, all items in parallel (warp per item)
+//   k_resolve  -- K3: in-order resolve (:307-377): re-tests members opened since
+//                 the snapshot, closed-form capacity, CF update (K2), open
+//   k_rb_*     -- K4: rebuild (:381-421): T*=2, order (-w, index), reattach
+//   k_dfs/k_gather_* -- features()/extract_coreset() (:425-451)
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+#include "engine.cuh"
+
+static thread_local char g_err[512];
+void pcy_set_error(const char* fmt, ...) {
+  va_list ap; va_start(ap, fmt); vsnprintf(g_err, sizeof(g_err), fmt, ap); va_end(ap);
+}
+extern "C" const char* pcy_last_error(void) { return g_err; }
+
+// ----------------------------------------------------------------- helpers
+__device__ __forceinline__ bool rows_equal(const double* a, const double* b, int d, int lane) {
+  bool eq = true;
+  for (int e = lane; e < d; e += 32)
+    eq &= (__double_as_longlong(a[e]) == __double_as_longlong(b[e]));
+  return __all_sync(PCY_FULL, eq);
+}
+
+__device__ __forceinline__ unsigned long long row_hash(const double* x, int d, int lane) {
+  unsigned long long h = 0;
+  for (int e = lane; e < d; e += 32)
+    h += mix64((unsigned long long)__double_as_longlong(x[e]) + 0x9E3779B97F4A7C15ULL * (unsigned long long)(e + 1));
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) h += __shfl_xor_sync(PCY_FULL, h, o);
+  return mix64(h);
+}
+
+// Append `node` to group g (warp-uniform call).  Returns false on arena overflow.
+__device__ bool grp_append(const EngDev& E, int g, int node, long long& A_alloc, int lane) {
+  int cnt = E.g_count[g], cap = E.g_cap[g], base = E.g_base[g];
+  if (cnt == cap) {
+    int ncap = cap ? 2 * cap : PCY_GROUP_MIN_CAP;
+    long long nb = A_alloc;
+    if (nb + ncap > E.AC) return false;
+    A_alloc += ncap;
+    for (int p = lane; p < cnt; p += 32) E.arena[nb + p] = E.arena[base + p];
+    base = (int)nb; cap = ncap;
+    if (lane == 0) { E.g_base[g] = base; E.g_cap[g] = cap; }
+  }
+  if (lane == 0) { E.arena[base + cnt] = node; E.g_count[g] = cnt + 1; }
+  __syncwarp();
+  return true;
+}
+
+// Nearest among members [lo, hi) of the arena segment `mem`, against vector xv
+// (shared memory).  Lane-per-member transposed dots.  Returns the part
+// |r|^2 - 2 r.x and the position (lowest position wins ties), on all lanes.
+__device__ __forceinline__ void scan_members(const EngDev& E, const int* __restrict__ mem,
+                                             int lo, int hi, const double* __restrict__ xv,
+                                             int lane, double& bp, int& bpos) {
+  const int d = E.d, ld = E.ld;
+  bp = INFINITY; bpos = 0x7fffffff;
+  for (int c0 = lo; c0 < hi; c0 += 32) {
+    const int nm = min(32, hi - c0);
+    const int myid = lane < nm ? mem[c0 + lane] : -1;
+    double acc[32];
+#pragma unroll
+    for (int mm = 0; mm < 32; ++mm) {
+      const int id = __shfl_sync(PCY_FULL, myid, mm);
+      double a = 0.0;
+      if (id >= 0) {
+        const double* __restrict__ rr = E.r + (long long)id * ld;
+        for (int e = lane; e < d; e += 32) a = fma(rr[e], xv[e], a);
+      }
+      acc[mm] = a;
+    }
+    const double dt = warp_transpose_reduce(acc, lane);
+    double part = INFINITY; int pos = 0x7fffffff;
+    if (lane < nm) { part = radd(E.rn[myid], rmul(dt, -2.0)); pos = c0 + lane; }
+    warp_argmin(part, pos);
+    if (part < bp) { bp = part; bpos = pos; }
+  }
+}
+
+// ------------------------------------------------------------------ stage
+// One warp per row: fp32/fp64 -> fp64 padded row, x_sq, validation, hash.
+__global__ void k_stage(EngDev E, const void* __restrict__ src, int dtype, long long stride,
+                        const long long* __restrict__ wsrc, long long n, int dohash) {
+  const int lane = threadIdx.x & 31;
+  const long long i = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= n) return;
+  const int d = E.d, ld = E.ld;
+  double* __restrict__ dst = E.xb + i * ld;
+  double acc = 0.0; bool fin = true;
+  for (int e = lane; e < ld; e += 32) {
+    double v = 0.0;
+    if (e < d) {
+      v = dtype == 1 ? (double)((const float*)src)[i * stride + e] : ((const double*)src)[i * stride + e];
+      fin &= isfinite(v);
+      acc = fma(v, v, acc);
+    }
+    dst[e] = v;
+  }
+  const double xs = warp_sum(acc);
+  const bool allfin = __all_sync(PCY_FULL, fin);
+  __syncwarp();
+  unsigned long long h = dohash ? row_hash(dst, d, lane) : 0ULL;
+  if (lane == 0) {
+    const long long wv = wsrc ? wsrc[i] : 1LL;
+    int code = 0;
+    if (wv < 1) code = 3;
+    else if (!isfinite(xs)) code = allfin ? 2 : 1;
+    E.xsq[i] = xs; E.wb[i] = wv; E.bad[i] = code;
+    if (dohash) E.hsh[i] = h;
+  }
+}
+
+// x_sq for rows already in engine layout (pending replay).
+__global__ void k_rowsq(const double* __restrict__ X, int d, int ld, long long n, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const long long i = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= n) return;
+  const double* x = X + i * ld;
+  double acc = 0.0;
+  for (int e = lane; e < d; e += 32) acc = fma(x[e], x[e], acc);
+  acc = warp_sum(acc);
+  if (lane == 0) out[i] = acc;
+}
+
+// --------------------------------------------------------------- bootstrap
+// coreset.py:283-295, one warp, strictly in stream order.
+__global__ void k_boot(EngDev E, long long start, long long n) {
+  const int lane = threadIdx.x;
+  EngCtl* C = E.ctl;
+  const int d = E.d, ld = E.ld;
+  long long npend = C->npend, ndist = C->ndist, totw = C->total_w;
+  const unsigned long long mask = (unsigned long long)E.hcap - 1ULL;
+  int status = ST_DONE, err = 0; long long stop = n;
+  for (long long i = start; i < n; ++i) {
+    if (E.bad[i]) { status = ST_INVALID; err = E.bad[i]; stop = i; break; }
+    const double* x = E.xb + i * ld;
+    const long long wv = E.wb[i];
+    bool dup = npend > 0 && rows_equal(E.pend_x + (npend - 1) * ld, x, d, lane);
+    if (!dup && npend == E.pend_cap) { status = ST_GROW; stop = i; break; }
+    totw += wv;
+    if (dup) {
+      if (lane == 0) E.pend_w[npend - 1] += wv;
+    } else {
+      double* pr = E.pend_x + npend * ld;
+      for (int e = lane; e < ld; e += 32) pr[e] = x[e];
+      if (lane == 0) { E.pend_w[npend] = wv; E.pend_xsq[npend] = E.xsq[i]; }
+      ++npend;
+    }
+    unsigned long long slot = E.hsh[i] & mask;
+    bool found = false;
+    for (;;) {
+      const int k = E.htab[slot];
+      if (k < 0) break;
+      if (rows_equal(E.dist_x + (long long)k * ld, x, d, lane)) { found = true; break; }
+      slot = (slot + 1) & mask;
+    }
+    if (!found) {
+      double* dr = E.dist_x + ndist * ld;
+      for (int e = lane; e < ld; e += 32) dr[e] = x[e];
+      if (lane == 0) E.htab[slot] = (int)ndist;
+      ++ndist;
+      __syncwarp();
+      if (ndist > E.m) { status = ST_BUILD; stop = i; break; }
+    }
+    __syncwarp();
+  }
+  __syncwarp();
+  if (lane == 0) {
+    C->npend = npend; C->ndist = ndist; C->total_w = totw;
+    C->status = status; C->err = err; C->stop = stop;
+  }
+}
+
+// ---------------------------------------------- min pairwise (threshold T0)
+__global__ void k_mp_norms(EngDev E, long long ns, double* __restrict__ nrm) {
+  const int lane = threadIdx.x & 31;
+  const long long i = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= ns) return;
+  const double* x = E.dist_x + i * E.ld;
+  double v = warp_dot(x, x, E.d, lane);
+  if (lane == 0) {
+    nrm[i] = v;
+    atomicMax(E.minbits + 1, (unsigned long long)__double_as_longlong(v));
+  }
+}
+
+// 32x32 tile of the sample Gram; v = (n_i + n_j) - 2 G_ij, min over v > 0, i < j.
+__global__ void k_mp_tiles(EngDev E, long long ns, const double* __restrict__ nrm) {
+  __shared__ double As[32][33], Bs[32][33];
+  const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
+  const long long i0 = (long long)blockIdx.y * 32, j0 = (long long)blockIdx.x * 32;
+  if (j0 + 31 < i0) return;
+  const int d = E.d, ld = E.ld;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int e0 = 0; e0 < d; e0 += 32) {
+    for (int r = ty; r < 32; r += 8) {
+      const long long ia = i0 + r, jb = j0 + r;
+      As[r][tx] = (ia < ns && e0 + tx < d) ? E.dist_x[ia * ld + e0 + tx] : 0.0;
+      Bs[r][tx] = (jb < ns && e0 + tx < d) ? E.dist_x[jb * ld + e0 + tx] : 0.0;
+    }
+    __syncthreads();
+    const int ne = min(32, d - e0);
+    for (int e = 0; e < ne; ++e) {
+      const double b = Bs[tx][e];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc[k] = fma(As[ty + 8 * k][e], b, acc[k]);
+    }
+    __syncthreads();
+  }
+  unsigned long long best = 0x7ff0000000000000ULL;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const long long i = i0 + ty + 8 * k, j = j0 + tx;
+    if (i < ns && j < ns && i < j) {
+      const double v = rsub(radd(nrm[i], nrm[j]), rmul(2.0, acc[k]));
+      if (v > 0.0) best = min(best, (unsigned long long)__double_as_longlong(v));
+    }
+  }
+  if (best != 0x7ff0000000000000ULL) atomicMin(E.minbits, best);
+}
+
+__global__ void k_mp_finish(EngDev E, long long ns) {
+  if (threadIdx.x || blockIdx.x) return;
+  double mn;
+  if (ns < 2) mn = 1.0;
+  else if (E.minbits[0] == 0x7ff0000000000000ULL) {
+    const double nmax = __longlong_as_double((long long)E.minbits[1]);
+    mn = rmul(1e-12, nmax > 1.0 ? nmax : 1.0);
+  } else mn = __longlong_as_double((long long)E.minbits[0]);
+  E.ctl->T = rdiv(rmul(mn, (double)E.m), 16.0);
+}
+
+// ------------------------------------------------------------- tree reset
+__global__ void k_tree_reset(EngDev E) {
+  if (threadIdx.x || blockIdx.x) return;
+  EngCtl* C = E.ctl;
+  C->G_alloc = 1; C->A_alloc = 0; C->F = 0;
+  E.g_count[0] = 0; E.g_cap[0] = 0; E.g_base[0] = 0;
+}
+
+__global__ void k_snapshot(EngDev E) {
+  const long long G = E.ctl->G_alloc;
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < G; g += (long long)gridDim.x * blockDim.x) {
+    E.g_bs[g] = E.g_count[g];
+    E.g_bsbase[g] = E.g_base[g];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) E.ctl->G_snap = G;
+}
+
+// ------------------------------------------------------------- K1: chains
+// One warp per item: walk the snapshot tree along nearest references while
+// the admission radius holds (coreset.py:325-329, :369-372), ignoring
+// capacity.  Records (node, part) per level; the final recorded level is the
+// one where the chain leaves (outside radius or empty group).
+__global__ void k_chain(EngDev E, const double* __restrict__ X, const double* __restrict__ XS,
+                        long long n) {
+  extern __shared__ double sm_x[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const long long i = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
+  if (i >= n) return;
+  const int d = E.d, ld = E.ld;
+  double* xv = sm_x + (long long)wib * ld;
+  const double xs = XS[i];
+  if (!isfinite(xs)) { if (lane == 0) E.ch_len[i] = 0; return; }   // rejected by k_resolve
+  for (int e = lane; e < d; e += 32) xv[e] = X[i * ld + e];
+  __syncwarp();
+  const long long Gsnap = E.ctl->G_snap;
+  double radius = E.ctl->T;
+  int g = 0, L = 0;
+  int* cn = E.ch_node + i * PCY_MAXL;
+  double* cp = E.ch_part + i * PCY_MAXL;
+  for (;;) {
+    const int cnt = g < Gsnap ? E.g_bs[g] : 0;
+    double bp; int bpos;
+    scan_members(E, E.arena + (cnt ? E.g_bsbase[g] : 0), 0, cnt, xv, lane, bp, bpos);
+    const int bj = (cnt && bpos < cnt) ? E.arena[E.g_bsbase[g] + bpos] : -1;
+    if (lane == 0) { cn[L] = bj; cp[L] = bp; }
+    ++L;
+    if (bj < 0 || radd(bp, xs) > radius) break;
+    const int c = E.child[bj];
+    if (c < 0 || c >= Gsnap) {
+      if (L < PCY_MAXL) { if (lane == 0) { cn[L] = -1; cp[L] = INFINITY; } ++L; }
+      break;
+    }
+    if (L >= PCY_MAXL) break;   // truncated: k_resolve scans directly below
+    g = c;
+    radius = rmul(radius, 0.25);
+  }
+  if (lane == 0) E.ch_len[i] = L;
+}
+
+// ------------------------------------------------------------- K3: resolve
+// One warp, items in stream order.  Per level: the chain's snapshot winner is
+// compared with members appended after the snapshot (or all members in
+// direct mode), then the closed-form capacity (coreset.py:336-356) decides
+// how many copies stay; CF statistics update in place (:357-368).
+__global__ void k_resolve(EngDev E, const double* __restrict__ X, const double* __restrict__ XS,
+                          const long long* __restrict__ W, const int* __restrict__ BAD,
+                          long long n, long long start, long long first_rem, int countw) {
+  extern __shared__ double xv[];
+  const int lane = threadIdx.x;
+  EngCtl* C = E.ctl;
+  const int d = E.d, ld = E.ld;
+  const long long m = E.m;
+  const double T = C->T;
+  long long F = C->F, Falloc = C->F_alloc, freen = C->free_n, Galloc = C->G_alloc;
+  long long Aalloc = C->A_alloc, nidx = C->next_index, totw = C->total_w, maxdepth = C->max_depth;
+  const long long Gsnap = C->G_snap;
+  int status = ST_DONE, err = 0; long long stop = n, remaining = 0;
+
+  for (long long i = start; i < n; ++i) {
+    if (BAD && BAD[i]) { status = ST_INVALID; err = BAD[i]; stop = i; break; }
+    const bool resume = (i == start && first_rem >= 0);
+    const long long wi = W ? W[i] : 1LL;
+    long long rem = resume ? first_rem : wi;
+    if (countw && !resume) totw += wi;
+    for (int e = lane; e < d; e += 32) xv[e] = X[i * ld + e];
+    __syncwarp();
+    const double xs = XS[i];
+    const int len = E.ch_len[i];
+    const int* cn = E.ch_node + i * PCY_MAXL;
+    const double* cp = E.ch_part + i * PCY_MAXL;
+    int g = 0, L = 0;
+    double radius = T;
+    bool direct = false;
+    for (;;) {
+      int bj = -1; double bp = INFINITY;
+      if (!direct) {
+        if (L < len) { bj = cn[L]; bp = cp[L]; }
+        else direct = true;
+      }
+      const int cnt = E.g_count[g];
+      const int lo = direct ? 0 : (g < Gsnap ? E.g_bs[g] : 0);
+      bool newwin = false;
+      if (cnt > lo) {
+        double np_; int npos;
+        const int* mem = E.arena + E.g_base[g];
+        scan_members(E, mem, lo, cnt, xv, lane, np_, npos);
+        if (npos < cnt && (np_ < bp || bj < 0)) {
+          bp = np_; bj = mem[npos]; newwin = true;
+        }
+      }
+      if (bj < 0 || radd(bp, xs) > radius) {
+        // _open (coreset.py:329-335, :374-377)
+        const bool full = F >= m;
+        const long long wopen = full ? 1LL : rem;
+        long long slot;
+        if (freen > 0) slot = E.free_ids[--freen];
+        else slot = Falloc++;
+        double* rr = E.r + slot * ld;
+        double* ss = E.s + slot * ld;
+        const double fw = (double)wopen;
+        for (int e = lane; e < d; e += 32) { rr[e] = xv[e]; ss[e] = rmul(fw, xv[e]); }
+        if (lane == 0) {
+          E.w[slot] = wopen;
+          E.q[slot] = rmul(fw, xs);
+          E.sn[slot] = rmul((double)(wopen * wopen), xs);
+          E.rn[slot] = xs;
+          E.idx[slot] = nidx;
+          E.child[slot] = -1;
+          E.alive[slot] = 1;
+        }
+        ++nidx;
+        __syncwarp();
+        if (!grp_append(E, g, (int)slot, Aalloc, lane)) { status = ST_ARENA; stop = i; break; }
+        ++F;
+        if (L + 1 > maxdepth) maxdepth = L + 1;
+        rem -= wopen;
+        if (full) { status = ST_REBUILD; stop = i; remaining = rem; }
+        break;
+      }
+      // capacity on the winner (coreset.py:336-356)
+      const long long nn = E.w[bj];
+      const double fn = (double)nn;
+      const double nrm = rdiv(E.sn[bj], fn);
+      double errv = rsub(E.q[bj], nrm);
+      if (errv < 0.0) errv = 0.0;
+      double* ss = E.s + (long long)bj * ld;
+      const double dt = warp_dot(ss, xv, d, lane);
+      double dist = rsub(xs, rdiv(rsub(rmul(2.0, dt), nrm), fn));
+      if (dist < 0.0) dist = 0.0;
+      const double slack = radd(rsub(rmul(fn, dist), T), errv);
+      long long take;
+      if (slack <= 0.0) take = rem;
+      else {
+        const double limit = rdiv(rsub(rmul(fn, T), rmul(fn, errv)), slack);
+        if (limit >= (double)rem) take = rem;
+        else if (limit > 0.0) take = (long long)limit;
+        else take = 0;
+      }
+      if (take > 0) {
+        const double ft = (double)take;
+        if (take == 1) { for (int e = lane; e < d; e += 32) ss[e] = radd(ss[e], xv[e]); }
+        else { for (int e = lane; e < d; e += 32) ss[e] = radd(ss[e], rmul(ft, xv[e])); }
+        if (lane == 0) {
+          E.w[bj] = nn + take;
+          E.q[bj] = radd(E.q[bj], rmul(ft, xs));
+          E.sn[bj] = radd(E.sn[bj], radd(rmul(rmul(2.0, ft), dt), rmul((double)(take * take), xs)));
+        }
+        __syncwarp();
+        rem -= take;
+        if (rem == 0) { if (L + 1 > maxdepth) maxdepth = L + 1; break; }
+      }
+      if (newwin) direct = true;
+      int c = E.child[bj];
+      if (c < 0) {
+        c = (int)Galloc++;
+        if (lane == 0) { E.g_count[c] = 0; E.g_cap[c] = 0; E.g_base[c] = 0; E.child[bj] = c; }
+        __syncwarp();
+      }
+      g = c;
+      radius = rmul(radius, 0.25);
+      ++L;
+    }
+    __syncwarp();
+    if (status != ST_DONE) break;
+  }
+  if (lane == 0) {
+    C->F = F; C->F_alloc = Falloc; C->free_n = freen; C->G_alloc = Galloc;
+    C->A_alloc = Aalloc; C->next_index = nidx; C->total_w = totw; C->max_depth = maxdepth;
+    C->status = status; C->err = err; C->stop = stop; C->remaining = remaining;
+  }
+}
+
+// ------------------------------------------------------------ K4: rebuild
+// Order live slots by (-weight, creation index) (coreset.py:454-455).
+__global__ void k_rb_rank(EngDev E, long long nslots) {
+  __shared__ long long sw[256], si[256];
+  __shared__ int sa[256];
+  const long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool mine = u < nslots && E.alive[u];
+  const long long wu = mine ? E.w[u] : 0, iu = mine ? E.idx[u] : 0;
+  long long rank = 0;
+  for (long long t0 = 0; t0 < nslots; t0 += 256) {
+    const long long v = t0 + threadIdx.x;
+    sa[threadIdx.x] = v < nslots ? E.alive[v] : 0;
+    sw[threadIdx.x] = v < nslots ? E.w[v] : 0;
+    si[threadIdx.x] = v < nslots ? E.idx[v] : 0;
+    __syncthreads();
+    if (mine) {
+      const int nt = (int)min(256LL, nslots - t0);
+      for (int k = 0; k < nt; ++k)
+        rank += sa[k] && (sw[k] > wu || (sw[k] == wu && si[k] < iu));
+    }
+    __syncthreads();
+  }
+  if (mine) E.order[rank] = (int)u;
+}
+
+// T *= 2; detach every subtree; fresh roots (coreset.py:386-391).
+__global__ void k_rb_reset(EngDev E, long long nslots) {
+  const long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (u < nslots) E.child[u] = -1;
+  if (u == 0) {
+    EngCtl* C = E.ctl;
+    C->T = rmul(C->T, 2.0);
+    C->G_alloc = 1; C->A_alloc = 0; C->F = 0;
+    E.g_count[0] = 0; E.g_cap[0] = 0; E.g_base[0] = 0;
+  }
+}
+
+// Reattach nodes in rank order (coreset.py:395-421).  One CTA of 32 warps;
+// the member scan of each level is split across warps.
+__global__ void __launch_bounds__(512) k_rb_reattach(EngDev E, long long nodes) {
+  extern __shared__ double refv[];
+  __shared__ double red_p[32];
+  __shared__ int red_pos[32];
+  __shared__ int s_dec, s_host;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  EngCtl* C = E.ctl;
+  const int d = E.d, ld = E.ld;
+  const double T = C->T;
+  long long F = 0, Galloc = 1, Aalloc = 0, freen = C->free_n;
+  for (long long k = 0; k < nodes; ++k) {
+    const int u = E.order[k];
+    for (int e = threadIdx.x; e < d; e += blockDim.x) refv[e] = E.r[(long long)u * ld + e];
+    __syncthreads();
+    const double rsq = E.rn[u];
+    int g = 0;
+    double radius = T;
+    for (;;) {
+      const int cnt = E.g_count[g];
+      const int* mem = E.arena + E.g_base[g];
+      double bp = INFINITY; int bpos = 0x7fffffff;
+      for (int c0 = wid * 32; c0 < cnt; c0 += nw * 32) {
+        double p; int ps;
+        scan_members(E, mem, c0, min(cnt, c0 + 32), refv, lane, p, ps);
+        if (p < bp) { bp = p; bpos = ps; }
+      }
+      if (lane == 0) { red_p[wid] = bp; red_pos[wid] = bpos; }
+      __syncthreads();
+      if (wid == 0) {
+        double p = lane < nw ? red_p[lane] : INFINITY;
+        int ps = lane < nw ? red_pos[lane] : 0x7fffffff;
+        warp_argmin(p, ps);
+        int dec;   // 0 add, 1 merged, 2 descend
+        int h = -1;
+        if (cnt == 0 || radd(p, rsq) > radius) {
+          dec = 0;
+          if (!grp_append(E, g, u, Aalloc, lane)) dec = 3;
+          ++F;
+        } else {
+          h = mem[ps];
+          const long long mw = E.w[h] + E.w[u];
+          const double* sh = E.s + (long long)h * ld;
+          const double* su = E.s + (long long)u * ld;
+          double acc = 0.0;
+          for (int e = lane; e < d; e += 32) { const double v = radd(sh[e], su[e]); acc = fma(v, v, acc); }
+          const double mnorm = warp_sum(acc);
+          const double mq = radd(E.q[h], E.q[u]);
+          if (rsub(mq, rdiv(mnorm, (double)mw)) <= T) {
+            double* shw = E.s + (long long)h * ld;
+            for (int e = lane; e < d; e += 32) shw[e] = radd(shw[e], su[e]);
+            if (lane == 0) {
+              E.w[h] = mw; E.q[h] = mq; E.sn[h] = mnorm;
+              E.alive[u] = 0; E.free_ids[freen] = u;
+            }
+            ++freen;
+            dec = 1;
+          } else {
+            dec = 2;
+            int c = E.child[h];
+            if (c < 0) {
+              c = (int)Galloc++;
+              if (lane == 0) { E.g_count[c] = 0; E.g_cap[c] = 0; E.g_base[c] = 0; E.child[h] = c; }
+            }
+            h = c;
+          }
+        }
+        if (lane == 0) { s_dec = dec; s_host = h; }
+      }
+      __syncthreads();
+      const int dec = s_dec;
+      if (dec != 2) break;
+      g = s_host;
+      radius = rmul(radius, 0.25);
+      __syncthreads();
+    }
+    __syncthreads();
+    if (s_dec == 3) break;
+  }
+  if (threadIdx.x == 0) {
+    C->F = F; C->G_alloc = Galloc; C->A_alloc = Aalloc; C->free_n = freen;
+    C->status = s_dec == 3 ? ST_ARENA : ST_DONE;
+  }
+}
+
+// ------------------------------------------------------------- extraction
+// DFS pre-order over groups (coreset.py:433-440).  Single thread; the output
+// order drives the parallel gathers below.
+__global__ void k_dfs(EngDev E) {
+  if (threadIdx.x || blockIdx.x) return;
+  long long cnt = 0; int depth = 0;
+  E.stk_g[0] = 0; E.stk_p[0] = 0;
+  while (depth >= 0) {
+    const int g = E.stk_g[depth], p = E.stk_p[depth];
+    if (p >= E.g_count[g]) { --depth; continue; }
+    E.stk_p[depth] = p + 1;
+    const int u = E.arena[E.g_base[g] + p];
+    E.order[cnt] = u; E.lvl[cnt] = depth + 1; ++cnt;
+    const int c = E.child[u];
+    if (c >= 0 && E.g_count[c] > 0) { ++depth; E.stk_g[depth] = c; E.stk_p[depth] = 0; }
+  }
+  E.ctl->stop = cnt;
+}
+
+// features(): level, weight, linear sum, square sum, reference.
+__global__ void k_gather_features(EngDev E, long long cnt, int* __restrict__ lv, long long* __restrict__ wo,
+                                  double* __restrict__ so, double* __restrict__ qo, double* __restrict__ ro) {
+  const int lane = threadIdx.x & 31;
+  const long long k = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (k >= cnt) return;
+  const int u = E.order[k], d = E.d, ld = E.ld;
+  if (so) for (int e = lane; e < d; e += 32) so[k * d + e] = E.s[(long long)u * ld + e];
+  if (ro) for (int e = lane; e < d; e += 32) ro[k * d + e] = E.r[(long long)u * ld + e];
+  if (lane == 0) {
+    if (lv) lv[k] = E.lvl[k];
+    if (wo) wo[k] = E.w[u];
+    if (qo) qo[k] = E.q[u];
+  }
+}
+
+// extract_coreset(): row = s / n (coreset.py:449).
+__global__ void k_gather_points(EngDev E, long long cnt, double* __restrict__ po, long long* __restrict__ wo) {
+  const int lane = threadIdx.x & 31;
+  const long long k = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (k >= cnt) return;
+  const int u = E.order[k], d = E.d, ld = E.ld;
+  const double fw = (double)E.w[u];
+  for (int e = lane; e < d; e += 32) po[k * d + e] = rdiv(E.s[(long long)u * ld + e], fw);
+  if (lane == 0 && wo) wo[k] = E.w[u];
+}
+
+// Bootstrap-time features: pending aggregated per exact location in
+// first-occurrence order (coreset.py:429-432, :466-476).  The distinct table
+// is in first-seen order, so aggregation is a keyed weight sum.
+__global__ void k_boot_aggregate(EngDev E, long long* __restrict__ aggw) {
+  const int lane = threadIdx.x & 31;
+  const long long i = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= E.ctl->npend) return;
+  const double* x = E.pend_x + i * E.ld;
+  const unsigned long long mask = (unsigned long long)E.hcap - 1ULL;
+  unsigned long long slot = row_hash(x, E.d, lane) & mask;
+  for (;;) {
+    const int k = E.htab[slot];
+    if (k < 0) return;   // unreachable: every pending row was registered
+    if (rows_equal(E.dist_x + (long long)k * E.ld, x, E.d, lane)) {
+      if (lane == 0) atomicAdd((unsigned long long*)&aggw[k], (unsigned long long)E.pend_w[i]);
+      return;
+    }
+    slot = (slot + 1) & mask;
+  }
+}
+
+__global__ void k_boot_gather(EngDev E, long long cnt, const long long* __restrict__ aggw, int* __restrict__ lv,
+                              long long* __restrict__ wo, double* __restrict__ so, double* __restrict__ qo,
+                              double* __restrict__ ro, double* __restrict__ po) {
+  const int lane = threadIdx.x & 31;
+  const long long k = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (k >= cnt) return;
+  const int d = E.d;
+  const double* x = E.dist_x + k * E.ld;
+  const long long wk = aggw[k];
+  const double fw = (double)wk;
+  double acc = 0.0;
+  for (int e = lane; e < d; e += 32) {
+    const double sv = rmul(fw, x[e]);
+    if (so) so[k * d + e] = sv;
+    if (ro) ro[k * d + e] = x[e];
+    if (po) po[k * d + e] = rdiv(sv, fw);
+    acc = fma(x[e], x[e], acc);
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) {
+    if (lv) lv[k] = 1;
+    if (wo) wo[k] = wk;
+    if (qo) qo[k] = rmul(fw, acc);
+  }
+}
+
+// ====================================================================== host
+namespace {
+
+struct Engine {
+  int dev = 0, d = 0, ld = 0;
+  long long m = 0, sample_cap = 0, NC = 0, GC = 0, AC = 0, Bmax = 0;
+  bool built = false;
+  EngDev E{};
+  EngCtl* ctl_h = nullptr;   // pinned mirror
+  long long* aggw = nullptr;
+  double* mp_nrm = nullptr;
+  std::vector<void*> allocs;
+
+  template <class T> int alloc(T*& p, long long count) {
+    void* q = nullptr;
+    cudaError_t e = cudaMalloc(&q, sizeof(T) * (size_t)(count > 0 ? count : 1));
+    if (e != cudaSuccess) { pcy_set_error("cudaMalloc(%lld x %zu): %s", count, sizeof(T), cudaGetErrorString(e)); return PCY_ENOMEM; }
+    allocs.push_back(q);
+    p = (T*)q;
+    return PCY_OK;
+  }
+  void release(void* p) {
+    for (auto& a : allocs) if (a == p) { cudaFree(a); a = nullptr; }
+  }
+  ~Engine() {
+    for (void* a : allocs) if (a) cudaFree(a);
+    if (ctl_h) cudaFreeHost(ctl_h);
+  }
+
+  int sync_ctl(cudaStream_t st) {
+    PCY_CUDA(cudaMemcpyAsync(ctl_h, E.ctl, sizeof(EngCtl), cudaMemcpyDeviceToHost, st));
+    PCY_CUDA(cudaStreamSynchronize(st));
+    return PCY_OK;
+  }
+
+  int init(int device, int dim, long long budget, long long bootstrap_cap, long long block_rows) {
+    dev = device; d = dim; m = budget;
+    ld = (int)pcy_round_up(d, 4);
+    sample_cap = budget + 1 < bootstrap_cap ? budget + 1 : bootstrap_cap;
+    NC = m + 2; GC = NC + 2; AC = 24 * NC + 4096;
+    Bmax = block_rows > 0 ? block_rows : 4096;
+    PCY_CUDA(cudaSetDevice(dev));
+    PCY_CUDA(cudaFuncSetAttribute(k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    PCY_CUDA(cudaFuncSetAttribute(k_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    PCY_CUDA(cudaFuncSetAttribute(k_rb_reattach, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    E.d = d; E.ld = ld; E.m = m; E.NC = NC; E.GC = GC; E.AC = AC;
+    int rc;
+#define A_(p, n) if ((rc = alloc(p, n))) return rc
+    A_(E.w, NC); A_(E.q, NC); A_(E.sn, NC); A_(E.rn, NC); A_(E.idx, NC);
+    A_(E.child, NC); A_(E.alive, NC); A_(E.free_ids, NC);
+    A_(E.s, NC * ld); A_(E.r, NC * ld);
+    A_(E.g_base, GC); A_(E.g_count, GC); A_(E.g_cap, GC); A_(E.g_bs, GC); A_(E.g_bsbase, GC);
+    A_(E.arena, AC);
+    A_(E.ctl, 1);
+    A_(E.xb, Bmax * ld); A_(E.xsq, Bmax); A_(E.wb, Bmax); A_(E.hsh, Bmax); A_(E.bad, Bmax);
+    A_(E.ch_node, Bmax * PCY_MAXL); A_(E.ch_part, Bmax * PCY_MAXL); A_(E.ch_len, Bmax);
+    E.pend_cap = m + 2;
+    A_(E.pend_x, E.pend_cap * ld); A_(E.pend_w, E.pend_cap); A_(E.pend_xsq, E.pend_cap);
+    A_(E.dist_x, (m + 2) * ld);
+    E.hcap = 1; while (E.hcap < 2 * (m + 2)) E.hcap <<= 1;
+    A_(E.htab, E.hcap);
+    A_(E.order, NC); A_(E.lvl, NC); A_(E.stk_g, NC + 1); A_(E.stk_p, NC + 1);
+    A_(E.minbits, 2);
+    A_(aggw, m + 2); A_(mp_nrm, sample_cap + 1);
+#undef A_
+    PCY_CUDA(cudaMallocHost(&ctl_h, sizeof(EngCtl)));
+    memset(ctl_h, 0, sizeof(EngCtl));
+    PCY_CUDA(cudaMemcpy(E.ctl, ctl_h, sizeof(EngCtl), cudaMemcpyHostToDevice));
+    PCY_CUDA(cudaMemset(E.htab, 0xff, sizeof(int) * E.hcap));
+    PCY_CUDA(cudaMemset(E.alive, 0, sizeof(int) * NC));
+    PCY_CUDA(cudaMemset(E.s, 0, sizeof(double) * NC * ld));
+    PCY_CUDA(cudaMemset(E.r, 0, sizeof(double) * NC * ld));
+    return PCY_OK;
+  }
+
+  int grow_pending(cudaStream_t st) {
+    const long long nc = E.pend_cap * 2;
+    double *nx = nullptr, *nq = nullptr; long long* nw = nullptr;
+    int rc;
+    if ((rc = alloc(nx, nc * ld)) || (rc = alloc(nw, nc)) || (rc = alloc(nq, nc))) return rc;
+    PCY_CUDA(cudaMemcpyAsync(nx, E.pend_x, sizeof(double) * E.pend_cap * ld, cudaMemcpyDeviceToDevice, st));
+    PCY_CUDA(cudaMemcpyAsync(nw, E.pend_w, sizeof(long long) * E.pend_cap, cudaMemcpyDeviceToDevice, st));
+    PCY_CUDA(cudaMemcpyAsync(nq, E.pend_xsq, sizeof(double) * E.pend_cap, cudaMemcpyDeviceToDevice, st));
+    PCY_CUDA(cudaStreamSynchronize(st));
+    release(E.pend_x); release(E.pend_w); release(E.pend_xsq);
+    E.pend_x = nx; E.pend_w = nw; E.pend_xsq = nq; E.pend_cap = nc;
+    return PCY_OK;
+  }
+
+  int rebuild(cudaStream_t st) {
+    // precondition: ctl_h mirrors the device counters
+    while (ctl_h->F > m) {
+      const long long nslots = ctl_h->F_alloc;
+      const long long nodes = ctl_h->F;
+      k_rb_rank<<<(unsigned)((nslots + 255) / 256), 256, 0, st>>>(E, nslots);
+      k_rb_reset<<<(unsigned)((nslots + 255) / 256), 256, 0, st>>>(E, nslots);
+      k_rb_reattach<<<1, 512, sizeof(double) * ld, st>>>(E, nodes);
+      PCY_LAUNCH_CHECK();
+      int rc = sync_ctl(st); if (rc) return rc;
+      if (ctl_h->status == ST_ARENA) { pcy_set_error("member arena exhausted in rebuild"); return PCY_ESTATE; }
+    }
+    return PCY_OK;
+  }
+
+  // Live insertion of rows X (engine layout, stride ld) with x_sq XS, weights W
+  // (nullable = unit), validation codes BAD (nullable).  Returns PCY_OK and
+  // sets *bad_at = -1, or the index of the first invalid row.
+  int live(const double* X, const double* XS, const long long* W, const int* BAD, long long n,
+           int countw, cudaStream_t st, long long* bad_at, int* bad_code) {
+    *bad_at = -1;
+    long long off = 0;
+    while (off < n) {
+      const long long nb = n - off < Bmax ? n - off : Bmax;
+      long long start = 0, first_rem = -1;
+      while (start < nb) {
+        const double* Xs = X + (off + start) * ld;
+        const double* XSs = XS + off + start;
+        k_snapshot<<<64, 256, 0, st>>>(E);
+        const int wpc = ld <= 512 ? 8 : (ld <= 2048 ? 4 : 2);
+        k_chain<<<(unsigned)((nb - start + wpc - 1) / wpc), wpc * 32, sizeof(double) * wpc * ld, st>>>(
+            E, Xs, XSs, nb - start);
+        k_resolve<<<1, 32, sizeof(double) * ld, st>>>(
+            E, Xs, XSs, W ? W + off + start : nullptr, BAD ? BAD + off + start : nullptr,
+            nb - start, 0, first_rem, countw);
+        PCY_LAUNCH_CHECK();
+        int rc = sync_ctl(st); if (rc) return rc;
+        const int status = ctl_h->status;
+        if (status == ST_DONE) break;
+        if (status == ST_INVALID) { *bad_at = off + start + ctl_h->stop; *bad_code = ctl_h->err; return PCY_OK; }
+        if (status == ST_ARENA) { pcy_set_error("member arena exhausted"); return PCY_ESTATE; }
+        if (status == ST_REBUILD) {
+          const long long at = start + ctl_h->stop;
+          const long long r = ctl_h->remaining;
+          rc = rebuild(st); if (rc) return rc;
+          if (r > 0) { start = at; first_rem = r; }
+          else { start = at + 1; first_rem = -1; }
+          continue;
+        }
+        pcy_set_error("unexpected resolve status %d", status);
+        return PCY_ESTATE;
+      }
+      off += nb;
+    }
+    return PCY_OK;
+  }
+
+  int build(cudaStream_t st) {
+    const long long ns = ctl_h->ndist < sample_cap ? ctl_h->ndist : sample_cap;
+    unsigned long long init[2] = {0x7ff0000000000000ULL, 0ULL};
+    PCY_CUDA(cudaMemcpyAsync(E.minbits, init, sizeof(init), cudaMemcpyHostToDevice, st));
+    k_mp_norms<<<(unsigned)((ns + 7) / 8), 256, 0, st>>>(E, ns, mp_nrm);
+    dim3 grid((unsigned)((ns + 31) / 32), (unsigned)((ns + 31) / 32));
+    if (ns >= 2) k_mp_tiles<<<grid, dim3(32, 8), 0, st>>>(E, ns, mp_nrm);
+    k_mp_finish<<<1, 1, 0, st>>>(E, ns);
+    k_tree_reset<<<1, 1, 0, st>>>(E);
+    PCY_LAUNCH_CHECK();
+    int rc = sync_ctl(st); if (rc) return rc;
+    built = true;
+    const long long np = ctl_h->npend;
+    long long bad_at; int code;
+    rc = live(E.pend_x, E.pend_xsq, E.pend_w, nullptr, np, 0, st, &bad_at, &code);
+    return rc;
+  }
+
+  int insert(const void* x, int dtype, long long stride, const long long* w, long long n,
+             cudaStream_t st, long long* consumed, int* bad_code) {
+    *consumed = n; *bad_code = 0;
+    if (dtype != 0 && dtype != 1) { pcy_set_error("dtype must be 0 (f64) or 1 (f32)"); return PCY_EINVAL; }
+    const size_t esz = dtype == 1 ? 4 : 8;
+    long long pos = 0;
+    while (pos < n) {
+      const long long nb = n - pos < Bmax ? n - pos : Bmax;
+      k_stage<<<(unsigned)((nb + 7) / 8), 256, 0, st>>>(E, (const char*)x + (size_t)pos * stride * esz,
+                                                         dtype, stride, w ? w + pos : nullptr, nb, built ? 0 : 1);
+      PCY_LAUNCH_CHECK();
+      long long i = 0;
+      while (i < nb) {
+        if (!built) {
+          k_boot<<<1, 32, 0, st>>>(E, i, nb);
+          PCY_LAUNCH_CHECK();
+          int rc = sync_ctl(st); if (rc) return rc;
+          const int status = ctl_h->status;
+          if (status == ST_DONE) { i = nb; break; }
+          if (status == ST_INVALID) { *consumed = pos + ctl_h->stop; *bad_code = ctl_h->err; return PCY_OK; }
+          if (status == ST_GROW) { i = ctl_h->stop; rc = grow_pending(st); if (rc) return rc; continue; }
+          if (status == ST_BUILD) { i = ctl_h->stop + 1; rc = build(st); if (rc) return rc; continue; }
+          pcy_set_error("unexpected bootstrap status %d", status);
+          return PCY_ESTATE;
+        } else {
+          long long bad_at; int code = 0;
+          int rc = live(E.xb + i * ld, E.xsq + i, E.wb + i, E.bad + i, nb - i, 1, st, &bad_at, &code);
+          if (rc) return rc;
+          if (bad_at >= 0) { *consumed = pos + i + bad_at; *bad_code = code; return PCY_OK; }
+          i = nb;
+        }
+      }
+      pos += nb;
+    }
+    return PCY_OK;
+  }
+
+  int count(cudaStream_t st, long long* cnt) {
+    int rc = sync_ctl(st); if (rc) return rc;
+    if (!built) { *cnt = ctl_h->ndist; return PCY_OK; }
+    k_dfs<<<1, 1, 0, st>>>(E);
+    PCY_LAUNCH_CHECK();
+    rc = sync_ctl(st); if (rc) return rc;
+    *cnt = ctl_h->stop;
+    return PCY_OK;
+  }
+
+  int features(int* lv, long long* wo, double* so, double* qo, double* ro, double* po,
+               long long cap, long long* cnt, cudaStream_t st) {
+    int rc = count(st, cnt); if (rc) return rc;
+    const long long n = *cnt < cap ? *cnt : cap;
+    if (n <= 0) return PCY_OK;
+    if (!built) {
+      PCY_CUDA(cudaMemsetAsync(aggw, 0, sizeof(long long) * (ctl_h->ndist + 1), st));
+      k_boot_aggregate<<<(unsigned)((ctl_h->npend + 7) / 8), 256, 0, st>>>(E, aggw);
+      k_boot_gather<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(E, n, aggw, lv, wo, so, qo, ro, po);
+    } else {
+      if (po) k_gather_points<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(E, n, po, wo);
+      if (lv || so || qo || ro || (wo && !po))
+        k_gather_features<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(E, n, lv, wo, so, qo, ro);
+    }
+    PCY_LAUNCH_CHECK();
+    return PCY_OK;
+  }
+};
+
+}  // namespace
+
+// ==================================================================== C-ABI
+extern "C" {
+
+int pcy_engine_create(int device, int dim, long long budget, long long bootstrap_cap,
+                      long long block_rows, void** out) {
+  *out = nullptr;
+  if (dim < 1) { pcy_set_error("dim must be >= 1"); return PCY_EINVAL; }
+  if (budget < 1) { pcy_set_error("budget must be >= 1"); return PCY_EINVAL; }
+  if (budget > (1LL << 28)) { pcy_set_error("budget too large"); return PCY_EINVAL; }
+  Engine* e = new Engine();
+  int rc = e->init(device, dim, budget, bootstrap_cap, block_rows);
+  if (rc) { delete e; return rc; }
+  *out = e;
+  return PCY_OK;
+}
+
+int pcy_engine_destroy(void* h) {
+  delete (Engine*)h;
+  return PCY_OK;
+}
+
+int pcy_engine_insert(void* h, const void* x, int dtype, long long stride, const long long* w,
+                      long long n, void* stream, long long* consumed, int* bad_code) {
+  Engine* e = (Engine*)h;
+  if (!e) { pcy_set_error("null engine"); return PCY_EINVAL; }
+  if (n <= 0) { *consumed = 0; *bad_code = 0; return PCY_OK; }
+  return e->insert(x, dtype, stride, w, n, (cudaStream_t)stream, consumed, bad_code);
+}
+
+int pcy_engine_stats(void* h, long long* num_features, double* threshold, long long* total_weight,
+                     int* built, void* stream) {
+  Engine* e = (Engine*)h;
+  int rc = e->sync_ctl((cudaStream_t)stream); if (rc) return rc;
+  *num_features = e->built ? e->ctl_h->F : e->ctl_h->ndist;
+  *threshold = e->ctl_h->T;
+  *total_weight = e->ctl_h->total_w;
+  *built = e->built ? 1 : 0;
+  return PCY_OK;
+}
+
+int pcy_engine_features(void* h, int* level, long long* weight, double* lsum, double* sqsum,
+                        double* ref, long long cap, long long* count, void* stream) {
+  return ((Engine*)h)->features(level, weight, lsum, sqsum, ref, nullptr, cap, count, (cudaStream_t)stream);
+}
+
+int pcy_engine_extract(void* h, double* points, long long* weights, long long cap, long long* count,
+                       void* stream) {
+  return ((Engine*)h)->features(nullptr, weights, nullptr, nullptr, nullptr, points, cap, count,
+                                (cudaStream_t)stream);
+}
+
+}  // extern "C"

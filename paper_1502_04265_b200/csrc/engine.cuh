@@ -1,0 +1,55 @@
+// Device-resident BICO clustering-feature engine: data layout shared by the
+// kernels in engine.cu (see DESIGN.md §3 for the HBM layout).
+#pragma once
+#include "common.cuh"
+
+#define PCY_MAXL 24          // chain levels recorded per item by k_chain
+#define PCY_GROUP_MIN_CAP 4  // first arena extent of a group
+
+// Status codes written by the sequential kernels into EngCtl::status.
+enum {
+  ST_DONE = 0,
+  ST_REBUILD = 1,   // open-one-copy at full budget: rebuild, then resume item `stop`
+  ST_INVALID = 2,   // item `stop` failed validation (err holds the code)
+  ST_BUILD = 3,     // bootstrap saw budget+1 distinct locations at item `stop`
+  ST_GROW = 4,      // bootstrap pending buffer full before item `stop`
+  ST_ARENA = 5,     // member arena exhausted (internal error)
+};
+
+struct EngCtl {
+  long long F;            // live features (_num_features)
+  long long F_alloc;      // node slots ever handed out (<= NC)
+  long long free_n;       // free-slot stack depth
+  long long G_alloc;      // groups in use (group 0 = roots)
+  long long A_alloc;      // member-arena bump pointer
+  long long next_index;   // creation counter (_next_index)
+  long long G_snap;       // groups that existed at the chain snapshot
+  long long total_w;      // total weight consumed
+  double T;               // threshold
+  long long npend, ndist; // bootstrap pending entries / distinct keys
+  int status, err;
+  long long stop, remaining;
+  long long max_depth;
+};
+
+struct EngDev {
+  int d, ld;
+  long long m, NC, GC, AC;
+  // nodes (slot-indexed)
+  long long* w; double* q; double* sn; double* rn; long long* idx;
+  int* child; int* alive; int* free_ids;
+  double* s; double* r;            // NC x ld, row-major
+  // groups: members live in arena[g_base .. g_base + g_count)
+  int* g_base; int* g_count; int* g_cap; int* g_bs; int* g_bsbase;
+  int* arena;
+  EngCtl* ctl;
+  // staged batch
+  double* xb; double* xsq; long long* wb; unsigned long long* hsh; int* bad;
+  int* ch_node; double* ch_part; int* ch_len;
+  // bootstrap
+  double* pend_x; long long* pend_w; double* pend_xsq; long long pend_cap;
+  double* dist_x; int* htab; long long hcap;
+  // rebuild / extraction scratch
+  int* order; int* lvl; int* stk_g; int* stk_p;
+  unsigned long long* minbits;
+};

@@ -1,0 +1,232 @@
+"""Weighted k-means++ seeding, weighted Lloyd and costs on the GPU.
+
+Drop-in for ``piecy.evaluation`` (/root/reference/pkg/src/piecy/evaluation.py).
+The random stream is the reference's: repetition ``rep`` draws exactly k
+uniforms from ``numpy.random.default_rng(mix_seed(seed, rep))`` (one per
+center, :49-53, :72-78); they are generated on the host and uploaded, and the
+seeding / Lloyd / cost arithmetic runs in csrc/kmeans.cu.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as nat
+from .util import mix_seed
+
+DEFAULT_REPETITIONS = 5
+DEFAULT_MAX_ITERS = 100
+DEFAULT_TOL = 1e-4
+
+c_i32, c_i64, c_f64, c_vp = ctypes.c_int, ctypes.c_longlong, ctypes.c_double, ctypes.c_void_p
+nat.register("pcy_kmeanspp", c_i32, [c_vp, c_vp, c_i64, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp])
+nat.register("pcy_lloyd", c_i32, [c_vp, c_vp, c_i64, c_i32, c_i32, c_i32, c_vp, c_i32, c_f64, c_vp, c_vp, c_vp])
+nat.register("pcy_weighted_cost", c_i32, [c_vp, c_vp, c_i64, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp])
+
+
+def _as_points(points) -> np.ndarray:
+    pts = np.asarray(points, dtype=np.float64)
+    if pts.ndim != 2:
+        raise ValueError("points must be a 2-d array (one point per row)")
+    return pts
+
+
+def _as_weights(weights, count: int) -> np.ndarray:
+    if weights is None:
+        return np.ones(count)
+    w = np.asarray(weights, dtype=np.float64)
+    if w.shape != (count,):
+        raise ValueError("weights must be one per point")
+    if not np.all(w > 0):
+        raise ValueError("weights must be positive")
+    return w
+
+
+def _dev_points(points, weights, device=None):
+    """(P, w) as contiguous float64 CUDA tensors; accepts numpy or torch."""
+    import torch
+    if isinstance(points, torch.Tensor):
+        P = points.to(device or points.device, dtype=torch.float64).contiguous()
+        if P.dim() != 2:
+            raise ValueError("points must be a 2-d array (one point per row)")
+        if weights is None:
+            w = torch.ones(P.shape[0], dtype=torch.float64, device=P.device)
+        else:
+            w = (weights if isinstance(weights, torch.Tensor) else torch.as_tensor(np.asarray(weights)))
+            w = w.to(P.device, dtype=torch.float64).contiguous()
+            if w.shape != (P.shape[0],):
+                raise ValueError("weights must be one per point")
+        return P, w
+    pts = _as_points(points)
+    wts = _as_weights(weights, pts.shape[0])
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    return (torch.from_numpy(np.ascontiguousarray(pts)).to(dev),
+            torch.from_numpy(np.ascontiguousarray(wts)).to(dev))
+
+
+def _uniforms(seed: int, reps: int, k: int) -> np.ndarray:
+    return np.stack([np.random.default_rng(mix_seed(seed, r)).random(k) for r in range(reps)])
+
+
+def seed_device(P, w, k: int, U: np.ndarray):
+    """k-means++ for every row of U (reps x k uniforms) -> (reps, k, d) tensor."""
+    import torch
+    reps = U.shape[0]
+    n, d = P.shape
+    Ud = torch.from_numpy(np.ascontiguousarray(U, dtype=np.float64)).to(P.device)
+    C = torch.empty((reps, k, d), dtype=torch.float64, device=P.device)
+    nat.check(nat.lib().pcy_kmeanspp(nat.ptr(P), nat.ptr(w), n, d, k, reps, nat.ptr(Ud), nat.ptr(C), None,
+                                     nat.stream_ptr()), "pcy_kmeanspp")
+    return C
+
+
+def lloyd_device(P, w, C, max_iters: int, tol: float):
+    """Lloyd in place on C (reps, k, d); returns per-rep cost logs."""
+    reps, k, d = C.shape
+    n = P.shape[0]
+    logs = np.zeros((reps, max(1, max_iters)))
+    iters = np.zeros(reps, dtype=np.int32)
+    if max_iters > 0:
+        nat.check(nat.lib().pcy_lloyd(nat.ptr(P), nat.ptr(w), n, d, k, reps, nat.ptr(C), int(max_iters),
+                                      float(tol), logs.ctypes.data, iters.ctypes.data, nat.stream_ptr()),
+                  "pcy_lloyd")
+    return [list(logs[r, :iters[r]]) for r in range(reps)]
+
+
+def cost_device(P, w, C) -> np.ndarray:
+    reps, k, d = C.shape
+    out = np.zeros(reps)
+    nat.check(nat.lib().pcy_weighted_cost(nat.ptr(P), nat.ptr(w), P.shape[0], d, k, reps, nat.ptr(C),
+                                          out.ctypes.data, nat.stream_ptr()), "pcy_weighted_cost")
+    return out
+
+
+def kmeanspp_seed(points, weights, k: int, rng: np.random.Generator) -> np.ndarray:
+    """Draw ``k`` centers by the weighted D^2 rule (evaluation.py:56-82)."""
+    pts = _as_points(points) if not _is_tensor(points) else points
+    n = pts.shape[0]
+    if n == 0:
+        raise ValueError("cannot seed centers from an empty point set")
+    if k < 1:
+        raise ValueError("k must be >= 1")
+    P, w = _dev_points(points, weights)
+    U = rng.random(k)[None, :]
+    return seed_device(P, w, k, U)[0].cpu().numpy()
+
+
+def lloyd_iterate(points, weights, centers, max_iters: int = DEFAULT_MAX_ITERS,
+                  tol: float = DEFAULT_TOL, cost_log: list | None = None) -> np.ndarray:
+    """Weighted Lloyd with empty-cluster repair (evaluation.py:85-139)."""
+    import torch
+    P, w = _dev_points(points, weights)
+    ctr = np.array(centers, dtype=np.float64, copy=True)
+    if ctr.ndim != 2 or ctr.shape[1] != P.shape[1]:
+        raise ValueError("centers must match the point dimension")
+    if P.shape[0] == 0:
+        return ctr
+    C = torch.from_numpy(ctr).to(P.device)[None].contiguous()
+    logs = lloyd_device(P, w, C, int(max_iters), float(tol))
+    if cost_log is not None:
+        cost_log.extend(float(c) for c in logs[0])
+    return C[0].cpu().numpy()
+
+
+def weighted_cost(points, weights, centers) -> float:
+    """Weighted SSE of points against their nearest center (evaluation.py:142-149)."""
+    import torch
+    if not _is_tensor(points):
+        pts = _as_points(points)
+        _as_weights(weights, pts.shape[0])
+        if pts.shape[0] == 0:
+            return 0.0
+    P, w = _dev_points(points, weights)
+    ctr = np.asarray(centers, dtype=np.float64)
+    C = torch.from_numpy(np.ascontiguousarray(ctr)).to(P.device)[None].contiguous()
+    return float(cost_device(P, w, C)[0])
+
+
+def kmeans_repetitions(points, weights, k: int, reps: int = DEFAULT_REPETITIONS,
+                       seed: int = 0, max_iters: int = DEFAULT_MAX_ITERS,
+                       tol: float = DEFAULT_TOL):
+    """Seeding + Lloyd ``reps`` times, repetition rng = PCG64(mix_seed(seed, rep))
+    (evaluation.py:199-210).  All repetitions run concurrently on the device.
+    Returns [(centers, cost), ...]."""
+    runs = kmeans_repetitions_device(points, weights, k, reps, seed, max_iters, tol)
+    C, costs = runs
+    Ch = C.cpu().numpy()
+    return [(Ch[r], float(costs[r])) for r in range(reps)]
+
+
+def kmeans_repetitions_device(points, weights, k: int, reps: int = DEFAULT_REPETITIONS,
+                              seed: int = 0, max_iters: int = DEFAULT_MAX_ITERS,
+                              tol: float = DEFAULT_TOL, cost_logs: list | None = None):
+    """Device form: returns (centers (reps, k, d) CUDA tensor, costs ndarray)."""
+    P, w = _dev_points(points, weights)
+    if P.shape[0] == 0:
+        raise ValueError("cannot seed centers from an empty point set")
+    if k < 1:
+        raise ValueError("k must be >= 1")
+    U = _uniforms(seed, reps, k)
+    C = seed_device(P, w, k, U)
+    logs = lloyd_device(P, w, C, int(max_iters), float(tol))
+    if cost_logs is not None:
+        cost_logs.extend(logs)
+    return C, cost_device(P, w, C)
+
+
+def _is_tensor(x) -> bool:
+    try:
+        import torch
+        return isinstance(x, torch.Tensor)
+    except Exception:
+        return False
+
+
+@dataclass(frozen=True)
+class CostSummary:
+    minimum: float
+    maximum: float
+    average: float
+    median: float
+
+    @classmethod
+    def of(cls, costs) -> "CostSummary":
+        arr = np.asarray(list(costs), dtype=np.float64)
+        if arr.size == 0:
+            raise ValueError("no costs to summarize")
+        return cls(float(arr.min()), float(arr.max()), float(arr.mean()), float(np.median(arr)))
+
+
+def evaluate_cost_multi(center_sets, point_stream, chunk: int = 8192) -> list:
+    """One streaming pass; unweighted SSE of the stream against each center
+    set (evaluation.py:157-180).  Chunks are costed on the device."""
+    import torch
+    sets = [np.asarray(c, dtype=np.float64) for c in center_sets]
+    totals = [0.0] * len(sets)
+    buf = []
+    dev = torch.device("cuda", torch.cuda.current_device())
+    Cs = [torch.from_numpy(np.ascontiguousarray(c)).to(dev)[None].contiguous() for c in sets]
+
+    def _flush(rows):
+        P = torch.from_numpy(np.ascontiguousarray(np.stack(rows))).to(dev)
+        w = torch.ones(P.shape[0], dtype=torch.float64, device=dev)
+        for i, C in enumerate(Cs):
+            totals[i] += float(cost_device(P, w, C)[0])
+
+    for x in point_stream:
+        buf.append(np.asarray(x, dtype=np.float64))
+        if len(buf) == chunk:
+            _flush(buf)
+            buf = []
+    if buf:
+        _flush(buf)
+    return [float(t) for t in totals]
+
+
+def evaluate_cost(centers, point_stream, chunk: int = 8192) -> float:
+    """Unweighted SSE of a stream against its nearest center (evaluation.py:152-154)."""
+    return evaluate_cost_multi([centers], point_stream, chunk=chunk)[0]
