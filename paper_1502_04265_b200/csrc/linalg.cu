@@ -1,0 +1,457 @@
+// Randomized best-fit projection on B200 (sm_100a), all fp64.
+//
+// Reference: /root/reference/pkg/src/piecy/linalg.py
+//   randomized_truncated_svd :167-206   (sketch, q power iterations with QR,
+//                                         two-sided core when rows > 4r)
+//   _fix_signs / _clip_small :77-94
+//   project                  :209-221   A V V^T
+//   weighted_best_fit        :231-250   rows scaled by sqrt(w)
+// Building blocks:
+//   k_dgemm   -- tiled GEMM on the fp64 tensor pipe (mma.sync m8n8k4 -> DMMA)
+//   CholeskyQR2 (k_chol_inv): orthonormal basis of the same span as
+//                LAPACK's Householder Q (only the span reaches the result;
+//                SURVEY.md §7 hard part 5)
+//   k_jacobi  -- one-sided (Hestenes) Jacobi SVD, tournament ordering
+#include <cmath>
+#include <algorithm>
+#include <vector>
+#include "common.cuh"
+
+namespace {
+
+// ------------------------------------------------------------------- GEMM
+// C[M x N] = alpha * op(A) * op(B) + beta * C, row-major with leading dims.
+// op(A) is M x K: A[m*lda + k] (ta=0) or A[k*lda + m] (ta=1).
+// op(B) is K x N: B[k*ldb + n] (tb=0) or B[n*ldb + k] (tb=1).
+constexpr int GBM = 64, GBN = 64, GBK = 16;
+
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(128) k_dgemm(int M, int N, int K, double alpha,
+                                               const double* __restrict__ A, long long lda, int ta,
+                                               const double* __restrict__ B, long long ldb, int tb,
+                                               double beta, double* __restrict__ C, long long ldc) {
+  __shared__ double As[GBM][GBK + 4];
+  __shared__ double Bs[GBK][GBN + 4];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const long long m0 = (long long)blockIdx.y * GBM, n0 = (long long)blockIdx.x * GBN;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) { acc[i][j][0] = 0.0; acc[i][j][1] = 0.0; }
+
+  for (int k0 = 0; k0 < K; k0 += GBK) {
+    // A tile (64 x 16): 1024 elements, 8 per thread
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int e = tid + r * 128;
+      int mm, kk;
+      if (!ta) { mm = e / GBK; kk = e % GBK; } else { kk = e / GBM; mm = e % GBM; }
+      const long long gm = m0 + mm; const int gk = k0 + kk;
+      double v = 0.0;
+      if (gm < M && gk < K) v = ta ? A[(long long)gk * lda + gm] : A[gm * lda + gk];
+      As[mm][kk] = v;
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int e = tid + r * 128;
+      int nn, kk;
+      if (!tb) { kk = e / GBN; nn = e % GBN; } else { nn = e / GBK; kk = e % GBK; }
+      const long long gn = n0 + nn; const int gk = k0 + kk;
+      double v = 0.0;
+      if (gn < N && gk < K) v = tb ? B[gn * ldb + gk] : B[(long long)gk * ldb + gn];
+      Bs[kk][nn] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ks = 0; ks < GBK; ks += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = As[wm + i * 8 + g][ks + t4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = Bs[ks + t4][wn + j * 8 + g];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const long long gm = m0 + wm + i * 8 + g, gn = n0 + wn + j * 8 + 2 * t4 + h;
+        if (gm < M && gn < N) {
+          double v = alpha * acc[i][j][h];
+          if (beta != 0.0) v += beta * C[gm * ldc + gn];
+          C[gm * ldc + gn] = v;
+        }
+      }
+}
+
+// ------------------------------------------------------- Cholesky inverse
+// G (r x r, row-major, SPD) = L L^T.  Writes Linv (row-major lower) so that
+// Y * Linv^T has orthonormal columns.  status[0] = 0 ok, 1 breakdown.
+__global__ void __launch_bounds__(1024) k_chol_inv(const double* __restrict__ G, int r, double shift,
+                                                  double* __restrict__ L, double* __restrict__ Linv,
+                                                  int* __restrict__ status) {
+  __shared__ double s_piv;
+  __shared__ int s_bad;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  if (tid == 0) s_bad = 0;
+  for (long long e = tid; e < (long long)r * r; e += blockDim.x) L[e] = 0.0;
+  __syncthreads();
+  for (int j = 0; j < r; ++j) {
+    if (warp == 0) {
+      double acc = 0.0;
+      for (int k = lane; k < j; k += 32) acc = fma(L[(long long)j * r + k], L[(long long)j * r + k], acc);
+      acc = warp_sum(acc);
+      if (lane == 0) {
+        const double t = G[(long long)j * r + j] + shift - acc;
+        if (!(t > 0.0) || !isfinite(t)) s_bad = 1;
+        s_piv = sqrt(fmax(t, 1e-300));
+        L[(long long)j * r + j] = s_piv;
+      }
+    }
+    __syncthreads();
+    if (s_bad) break;
+    const double piv = s_piv;
+    for (int i = j + 1 + warp; i < r; i += nw) {
+      double acc = 0.0;
+      for (int k = lane; k < j; k += 32) acc = fma(L[(long long)i * r + k], L[(long long)j * r + k], acc);
+      acc = warp_sum(acc);
+      if (lane == 0) L[(long long)i * r + j] = (G[(long long)i * r + j] - acc) / piv;
+    }
+    __syncthreads();
+  }
+  if (s_bad) { if (tid == 0) status[0] = 1; return; }
+  // Linv: forward substitution, one thread per column c.
+  for (int c = tid; c < r; c += blockDim.x) {
+    for (int i = 0; i < c; ++i) Linv[(long long)i * r + c] = 0.0;
+    for (int i = c; i < r; ++i) {
+      double acc = (i == c) ? 1.0 : 0.0;
+      for (int k = c; k < i; ++k) acc -= L[(long long)i * r + k] * Linv[(long long)k * r + c];
+      Linv[(long long)i * r + c] = acc / L[(long long)i * r + i];
+    }
+  }
+  if (tid == 0) status[0] = 0;
+}
+
+// ---------------------------------------------------------- Jacobi SVD
+// One-sided Jacobi on G (m rows x n cols, column j at G + j*m).  On exit
+// sig[j] (descending) and U (m x n, row-major with leading dim ldu) hold the
+// normalised columns of G*J; these are the right singular vectors of G^T.
+// perm scratch (n ints).
+__global__ void __launch_bounds__(1024) k_jacobi(double* __restrict__ G, int m, int n, double tol, int max_sweeps,
+                                                double* __restrict__ sig, double* __restrict__ U, int ldu,
+                                                int* __restrict__ perm, int* __restrict__ sweeps_out) {
+  __shared__ int s_rot;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int np = (n + 1) & ~1;   // even count (one dummy when n is odd)
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    if (tid == 0) s_rot = 0;
+    __syncthreads();
+    for (int round = 0; round < np - 1; ++round) {
+      // tournament pairing: position 0 fixed, others rotate
+      for (int pr = warp; pr < np / 2; pr += nw) {
+        int a = (pr == 0) ? 0 : 1 + (pr - 1 + round) % (np - 1);
+        int b = 1 + (np - 2 - pr + round) % (np - 1);
+        if (a >= n || b >= n) continue;
+        if (a > b) { const int t = a; a = b; b = t; }
+        double* gp = G + (long long)a * m;
+        double* gq = G + (long long)b * m;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int i = lane; i < m; i += 32) {
+          const double x = gp[i], y = gq[i];
+          al = fma(x, x, al); be = fma(y, y, be); ga = fma(x, y, ga);
+        }
+        al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
+        if (fabs(ga) > tol * sqrt(al * be) && ga != 0.0) {
+          const double zeta = (be - al) / (2.0 * ga);
+          const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+          for (int i = lane; i < m; i += 32) {
+            const double x = gp[i], y = gq[i];
+            gp[i] = c * x - s * y;
+            gq[i] = s * x + c * y;
+          }
+          if (lane == 0) s_rot = 1;
+        }
+      }
+      __syncthreads();
+    }
+    if (!s_rot) break;
+    __syncthreads();
+  }
+  // column norms
+  for (int j = warp; j < n; j += nw) {
+    const double* gj = G + (long long)j * m;
+    double acc = 0.0;
+    for (int i = lane; i < m; i += 32) acc = fma(gj[i], gj[i], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) sig[j] = sqrt(acc);
+  }
+  __syncthreads();
+  // order by sigma descending (stable on ties), rank by counting
+  for (int j = tid; j < n; j += blockDim.x) {
+    const double sj = sig[j];
+    int rank = 0;
+    for (int k = 0; k < n; ++k) rank += (sig[k] > sj) || (sig[k] == sj && k < j);
+    perm[rank] = j;
+  }
+  __syncthreads();
+  for (int jj = warp; jj < n; jj += nw) {
+    const int j = perm[jj];
+    const double* gj = G + (long long)j * m;
+    const double sj = sig[j];
+    const double inv = sj > 0.0 ? 1.0 / sj : 0.0;
+    for (int i = lane; i < m; i += 32) U[(long long)i * ldu + jj] = gj[i] * inv;
+  }
+  __syncthreads();
+  if (tid == 0) *sweeps_out = sweep;
+}
+
+// Sorted singular values: sorted[jj] = sig[perm[jj]] computed by rank again
+// (same ranking rule as k_jacobi's column order).
+__global__ void k_sorted_sigma(const double* __restrict__ sig, int n, double* __restrict__ out) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const double sj = sig[j];
+    int rank = 0;
+    for (int k = 0; k < n; ++k) rank += (sig[k] > sj) || (sig[k] == sj && k < j);
+    out[rank] = sj;
+  }
+}
+
+// _fix_signs: first entry with |v| > 1e-12 * max|v| made nonnegative, per
+// column of V (rows x cols row-major, leading dim ldv).  One warp per column.
+__global__ void k_fix_signs(double* __restrict__ V, int rows, int cols, int ldv) {
+  const int lane = threadIdx.x & 31;
+  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (j >= cols) return;
+  double pk = 0.0;
+  for (int i = lane; i < rows; i += 32) pk = fmax(pk, fabs(V[(long long)i * ldv + j]));
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) pk = fmax(pk, __shfl_xor_sync(PCY_FULL, pk, o));
+  if (pk == 0.0) return;
+  const double thr = 1e-12 * pk;
+  int first = 0x7fffffff;
+  for (int i = lane; i < rows; i += 32)
+    if (fabs(V[(long long)i * ldv + j]) > thr) { first = i; break; }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) first = min(first, __shfl_xor_sync(PCY_FULL, first, o));
+  if (first == 0x7fffffff) return;
+  const bool neg = V[(long long)first * ldv + j] < 0.0;
+  if (neg) for (int i = lane; i < rows; i += 32) V[(long long)i * ldv + j] = -V[(long long)i * ldv + j];
+}
+
+__global__ void k_cast_f32(const float* __restrict__ src, long long n, double* __restrict__ dst) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    dst[i] = (double)src[i];
+}
+
+// rows scaled by sqrt(w) (linalg.py:247)
+__global__ void k_scale_rows(const double* __restrict__ A, const long long* __restrict__ w, long long rows, int cols,
+                             double* __restrict__ out) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < rows * cols; e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e / cols;
+    out[e] = A[e] * sqrt((double)w[i]);
+  }
+}
+
+__global__ void k_all_finite(const void* __restrict__ p, long long n, int dt, int* __restrict__ flag) {
+  bool ok = true;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    ok &= dt ? isfinite(((const float*)p)[i]) : isfinite(((const double*)p)[i]);
+  if (!__all_sync(PCY_FULL, ok) && (threadIdx.x & 31) == 0) *flag = 0;
+}
+
+}  // namespace
+
+// ==================================================================== host
+static int gemm(cudaStream_t st, int M, int N, int K, double alpha, const double* A, long long lda, int ta,
+                const double* B, long long ldb, int tb, double beta, double* C, long long ldc) {
+  if (M <= 0 || N <= 0) return PCY_OK;
+  dim3 grid((unsigned)((N + GBN - 1) / GBN), (unsigned)((M + GBM - 1) / GBM));
+  k_dgemm<<<grid, 128, 0, st>>>(M, N, K, alpha, A, lda, ta, B, ldb, tb, beta, C, ldc);
+  PCY_LAUNCH_CHECK();
+  return PCY_OK;
+}
+
+// Orthonormalise Y (rows x r, row-major) in place: CholeskyQR2, falling back
+// to shifted CholeskyQR3 when the Gram factorisation breaks down.
+static int cholqr(cudaStream_t st, double* Y, long long rows, int r, double* Gs, double* Ls, double* Li,
+                  double* T, int* status) {
+  int hs = 0;
+  auto pass = [&](double shift, int* ok) -> int {
+    int rc;
+    if ((rc = gemm(st, r, r, (int)rows, 1.0, Y, r, 1, Y, r, 0, 0.0, Gs, r))) return rc;
+    k_chol_inv<<<1, 1024, 0, st>>>(Gs, r, shift, Ls, Li, status);
+    PCY_LAUNCH_CHECK();
+    PCY_CUDA(cudaMemcpyAsync(&hs, status, sizeof(int), cudaMemcpyDeviceToHost, st));
+    PCY_CUDA(cudaStreamSynchronize(st));
+    *ok = hs == 0;
+    if (!*ok) return PCY_OK;
+    // Y <- Y * Linv^T
+    if ((rc = gemm(st, (int)rows, r, r, 1.0, Y, r, 0, Li, r, 1, 0.0, T, r))) return rc;
+    PCY_CUDA(cudaMemcpyAsync(Y, T, sizeof(double) * rows * r, cudaMemcpyDeviceToDevice, st));
+    return PCY_OK;
+  };
+  int ok = 0, rc;
+  if ((rc = pass(0.0, &ok))) return rc;
+  if (ok) {
+    if ((rc = pass(0.0, &ok))) return rc;
+    if (ok) return PCY_OK;
+  }
+  // shifted CholeskyQR3: shift = 11 (m n + n (n+1)) u ||Y||_2^2, ||Y||_2^2 <= trace(G)
+  std::vector<double> g((size_t)r * r);
+  if ((rc = gemm(st, r, r, (int)rows, 1.0, Y, r, 1, Y, r, 0, 0.0, Gs, r))) return rc;
+  PCY_CUDA(cudaMemcpyAsync(g.data(), Gs, sizeof(double) * r * r, cudaMemcpyDeviceToHost, st));
+  PCY_CUDA(cudaStreamSynchronize(st));
+  double tr = 0.0;
+  for (int i = 0; i < r; ++i) tr += g[(size_t)i * r + i];
+  const double shift = 11.0 * ((double)rows * r + (double)r * (r + 1)) * 1.1102230246251565e-16 * tr;
+  if ((rc = pass(shift, &ok))) return rc;
+  if (!ok) { pcy_set_error("CholeskyQR breakdown even with shift"); return PCY_ESTATE; }
+  for (int it = 0; it < 2; ++it) {
+    if ((rc = pass(0.0, &ok))) return rc;
+    if (!ok) { pcy_set_error("CholeskyQR breakdown after shifted pass"); return PCY_ESTATE; }
+  }
+  return PCY_OK;
+}
+
+extern "C" {
+
+int pcy_all_finite(const void* p, long long n, int dtype, int* out_host, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  int* flag;
+  PCY_CUDA(cudaMallocAsync(&flag, sizeof(int), st));
+  const int one = 1;
+  PCY_CUDA(cudaMemcpyAsync(flag, &one, sizeof(int), cudaMemcpyHostToDevice, st));
+  if (n > 0) k_all_finite<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 8), 256, 0, st>>>(p, n, dtype, flag);
+  PCY_LAUNCH_CHECK();
+  PCY_CUDA(cudaMemcpyAsync(out_host, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  PCY_CUDA(cudaStreamSynchronize(st));
+  cudaFreeAsync(flag, st);
+  return PCY_OK;
+}
+
+int pcy_dgemm(int M, int N, int K, double alpha, const double* A, long long lda, int ta, const double* B,
+              long long ldb, int tb, double beta, double* C, long long ldc, void* stream) {
+  return gemm((cudaStream_t)stream, M, N, K, alpha, A, lda, ta, B, ldb, tb, beta, C, ldc);
+}
+
+int pcy_cast_f32_f64(const float* src, long long n, double* dst, void* stream) {
+  if (n <= 0) return PCY_OK;
+  k_cast_f32<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 16), 256, 0, (cudaStream_t)stream>>>(src, n, dst);
+  PCY_LAUNCH_CHECK();
+  return PCY_OK;
+}
+
+int pcy_scale_rows_sqrtw(const double* A, const long long* w, long long rows, int cols, double* out, void* stream) {
+  if (rows <= 0) return PCY_OK;
+  const long long n = rows * cols;
+  k_scale_rows<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 16), 256, 0, (cudaStream_t)stream>>>(A, w, rows, cols, out);
+  PCY_LAUNCH_CHECK();
+  return PCY_OK;
+}
+
+// Randomized truncated SVD (linalg.py:167-206) of A (rows x cols, fp64,
+// row-major).  omega (cols x r) and omega2 (r x r, used when rows > 4r) are
+// the host-drawn standard normals of the reference's rng.  Outputs V
+// (cols x ell, row-major, signs fixed) and sigma (ell, host, clipped).
+int pcy_rsvd(const double* A, long long rows, int cols, int ell, int r, int power, const double* omega,
+             const double* omega2, double* V, double* sigma_host, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (r > rows || r > cols || ell > r || ell < 1) { pcy_set_error("rsvd: bad rank"); return PCY_EINVAL; }
+  const bool two = rows > 4LL * r;
+  double *Q, *Z, *Bm, *Gs, *Ls, *Li, *T, *Wm, *core, *Uj, *sig, *Vfull;
+  int *status, *perm, *sweeps;
+  const long long big = std::max<long long>(rows, cols);
+  PCY_CUDA(cudaMallocAsync(&Q, sizeof(double) * rows * r, st));
+  PCY_CUDA(cudaMallocAsync(&Z, sizeof(double) * cols * r, st));
+  PCY_CUDA(cudaMallocAsync(&Bm, sizeof(double) * (long long)r * cols, st));
+  PCY_CUDA(cudaMallocAsync(&Gs, sizeof(double) * r * r, st));
+  PCY_CUDA(cudaMallocAsync(&Ls, sizeof(double) * r * r, st));
+  PCY_CUDA(cudaMallocAsync(&Li, sizeof(double) * r * r, st));
+  PCY_CUDA(cudaMallocAsync(&T, sizeof(double) * big * r, st));
+  PCY_CUDA(cudaMallocAsync(&Wm, sizeof(double) * cols * r, st));
+  PCY_CUDA(cudaMallocAsync(&core, sizeof(double) * r * r, st));
+  PCY_CUDA(cudaMallocAsync(&Uj, sizeof(double) * cols * r, st));
+  PCY_CUDA(cudaMallocAsync(&sig, sizeof(double) * 2 * r, st));
+  PCY_CUDA(cudaMallocAsync(&Vfull, sizeof(double) * cols * r, st));
+  PCY_CUDA(cudaMallocAsync(&status, sizeof(int) * 4, st));
+  PCY_CUDA(cudaMallocAsync(&perm, sizeof(int) * r, st));
+  PCY_CUDA(cudaMallocAsync(&sweeps, sizeof(int), st));
+  int rc = PCY_OK;
+  do {
+    // Q = qr(A omega)
+    if ((rc = gemm(st, (int)rows, r, cols, 1.0, A, cols, 0, omega, r, 0, 0.0, Q, r))) break;
+    if ((rc = cholqr(st, Q, rows, r, Gs, Ls, Li, T, status))) break;
+    for (int it = 0; it < power; ++it) {
+      // Z = qr(A^T Q); Q = qr(A Z)
+      if ((rc = gemm(st, cols, r, (int)rows, 1.0, A, cols, 1, Q, r, 0, 0.0, Z, r))) break;
+      if ((rc = cholqr(st, Z, cols, r, Gs, Ls, Li, T, status))) break;
+      if ((rc = gemm(st, (int)rows, r, cols, 1.0, A, cols, 0, Z, r, 0, 0.0, Q, r))) break;
+      if ((rc = cholqr(st, Q, rows, r, Gs, Ls, Li, T, status))) break;
+    }
+    if (rc) break;
+    // small = Q^T A  (r x cols)
+    if ((rc = gemm(st, r, cols, (int)rows, 1.0, Q, r, 1, A, cols, 0, 0.0, Bm, cols))) break;
+    const double tol = 2.220446049250313e-16 * (double)std::max(r, 8);
+    if (two) {
+      // W = qr(small^T omega2) (cols x r); core = small W (r x r)
+      if ((rc = gemm(st, cols, r, r, 1.0, Bm, cols, 1, omega2, r, 0, 0.0, Wm, r))) break;
+      if ((rc = cholqr(st, Wm, cols, r, Gs, Ls, Li, T, status))) break;
+      if ((rc = gemm(st, r, r, cols, 1.0, Bm, cols, 0, Wm, r, 0, 0.0, core, r))) break;
+      // Jacobi on core^T: column j of core^T = row j of core (contiguous)
+      k_jacobi<<<1, 1024, 0, st>>>(core, r, r, tol, 60, sig, Uj, r, perm, sweeps);
+      PCY_LAUNCH_CHECK();
+      // Uj (r x r row-major) columns = right singular vectors of core: V = W Uj
+      if ((rc = gemm(st, cols, r, r, 1.0, Wm, r, 0, Uj, r, 0, 0.0, Vfull, r))) break;
+    } else {
+      // Jacobi on small^T: column j of small^T = row j of small (contiguous)
+      k_jacobi<<<1, 1024, 0, st>>>(Bm, cols, r, tol, 60, sig, Vfull, r, perm, sweeps);
+      PCY_LAUNCH_CHECK();
+    }
+    k_sorted_sigma<<<1, 256, 0, st>>>(sig, r, sig + r);
+    // keep the first ell columns
+    PCY_CUDA(cudaMemcpy2DAsync(V, sizeof(double) * ell, Vfull, sizeof(double) * r, sizeof(double) * ell, cols,
+                               cudaMemcpyDeviceToDevice, st));
+    k_fix_signs<<<(ell + 7) / 8, 256, 0, st>>>(V, cols, ell, ell);
+    PCY_LAUNCH_CHECK();
+    std::vector<double> hs(r);
+    PCY_CUDA(cudaMemcpyAsync(hs.data(), sig + r, sizeof(double) * r, cudaMemcpyDeviceToHost, st));
+    PCY_CUDA(cudaStreamSynchronize(st));
+    for (int j = 0; j < ell; ++j) sigma_host[j] = hs[j];
+    if (ell > 0 && sigma_host[0] > 0.0)
+      for (int j = 0; j < ell; ++j) if (sigma_host[j] < 1e-12 * sigma_host[0]) sigma_host[j] = 0.0;
+  } while (0);
+  cudaFreeAsync(Q, st); cudaFreeAsync(Z, st); cudaFreeAsync(Bm, st); cudaFreeAsync(Gs, st);
+  cudaFreeAsync(Ls, st); cudaFreeAsync(Li, st); cudaFreeAsync(T, st); cudaFreeAsync(Wm, st);
+  cudaFreeAsync(core, st); cudaFreeAsync(Uj, st); cudaFreeAsync(sig, st); cudaFreeAsync(Vfull, st);
+  cudaFreeAsync(status, st); cudaFreeAsync(perm, st); cudaFreeAsync(sweeps, st);
+  return rc;
+}
+
+// project (linalg.py:209-221): out = (A V) V^T, A rows x cols, V cols x ell.
+int pcy_project(const double* A, long long rows, int cols, const double* V, int ell, double* out, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  double* P;
+  PCY_CUDA(cudaMallocAsync(&P, sizeof(double) * rows * ell, st));
+  int rc = gemm(st, (int)rows, ell, cols, 1.0, A, cols, 0, V, ell, 0, 0.0, P, ell);
+  if (!rc) rc = gemm(st, (int)rows, cols, ell, 1.0, P, ell, 0, V, ell, 1, 0.0, out, cols);
+  cudaFreeAsync(P, st);
+  return rc;
+}
+
+}  // extern "C"
