@@ -1,0 +1,320 @@
+#!/usr/bin/env python
+"""Benchmark of the piecy hot path on B200: stream -> BICO coreset -> k-means.
+
+One "step" = one full pass of the hot path over the configured synthetic
+stream: ``run_piecy`` (piece projection when active, BICO insertion) ->
+extract the coreset -> ``kmeans_repetitions`` (5 reps of weighted k-means++
+and Lloyd).  Metric: stream points per second (BASELINE.json).
+
+Default workload: cfg2 (BASELINE.json configs[1], the config the metric is
+quoted on; fits one GPU).  piecy is a single sequential engine, so with
+``--gpus N`` every rank runs an independent replica on its own GPU
+("replicas only") and ``value`` is the aggregate.
+
+Arms:
+  (default)         this framework on the GPU(s).
+  --impl reference  the reference algorithm's CPU path on the host cores:
+                    the CPU restatement in oracle/ (C BICO engine + numpy
+                    clustering); rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "stream points/sec (BICO+piecy, 1-8 GPU)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--rows", type=int, default=None, help="override stream length (smaller same-family stream)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ncu", action="store_true", help="one short step for profiler capture, no JSON")
+    return ap.parse_args()
+
+
+def workload(args):
+    from paper_1502_04265_b200 import workloads as W
+    cfg = W.CONFIGS[args.config]
+    X = W.generate(args.config, args.rows)
+    return cfg, X
+
+
+def config_json(cfg, X, N):
+    return {
+        "workload": (f"{cfg.name}: {cfg.entry} n={X.shape[0]} d={cfg.d} {cfg.dtype} k={cfg.k} m={cfg.m} "
+                     f"svd_dim={cfg.svd_dim} piece={cfg.piece_size}"
+                     + (f" num_pieces={cfg.num_pieces}" if cfg.num_pieces else "")
+                     + f" + kmeans_repetitions(reps={cfg.reps}, max_iters={cfg.max_iters}, tol=1e-4)"),
+        "n": int(X.shape[0]), "d": cfg.d, "k": cfg.k, "coreset_size": cfg.m, "svd_dim": cfg.svd_dim,
+        "piece_size": cfg.piece_size, "reps": cfg.reps, "seed": cfg.seed,
+        "parallelism": "replicas" if N > 1 else "single-engine",
+        "l2": "256 MiB buffer written between timed steps (input is ~L2-sized)",
+    }
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------- reference
+def cpu_run(cfg, X):
+    """One pass of the CPU restatement (oracle/) over X; returns seconds."""
+    from oracle import piecy_oracle as O
+    t0 = time.perf_counter()
+    if cfg.entry == "piecy":
+        P, w = O.piecy(X, cfg.k, cfg.piece_size, cfg.svd_dim, cfg.m, seed=cfg.seed)
+    else:
+        P, w = O.piecy_mr(X, cfg.k, cfg.piece_size, cfg.num_pieces, cfg.svd_dim, cfg.m, seed=cfg.seed)
+    O.kmeans_reps(P, w.astype(np.float64), cfg.k, reps=cfg.reps, seed=cfg.seed, max_iters=cfg.max_iters)
+    return time.perf_counter() - t0
+
+
+def cpu_sample(cfg, X, budget_s=20.0):
+    """Bounded CPU sample: the whole stream when it fits ~budget, else a prefix."""
+    n = X.shape[0]
+    rows = n
+    probe = min(n, 50_000)
+    t = cpu_run(cfg, X[:probe])
+    est = t * n / probe
+    if est > budget_s:
+        rows = max(probe, int(n * budget_s / est))
+    if rows != probe:
+        t = cpu_run(cfg, X[:rows])
+    return rows, t
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    cfg, X = workload(args)
+    rows, t = cpu_sample(cfg, X, budget_s=max(5.0, 150.0 / max(1, args.steps)))
+    Xs = X[:rows]
+    for _ in range(min(args.warmup, 1)):
+        cpu_run(cfg, Xs)
+    times = [cpu_run(cfg, Xs) for _ in range(args.steps)]
+    ms = 1000.0 * float(np.mean(times))
+    val = rows / (ms / 1000.0)
+    cores = os.cpu_count() or 1
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "points/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": min(args.warmup, 1), "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_json(cfg, X, 1),
+        "cpu_baseline": {"value": val, "unit": "points/s", "cores": cores, "kind": "port",
+                         "sample": f"first {rows} of {X.shape[0]} rows of {cfg.name}; BICO engine in C "
+                                   f"(1 thread), clustering numpy/OpenBLAS ({cores} threads)"},
+        "e2e": {"value": val, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------- ours
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return 0
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_1502_04265_b200 import _native as nat
+    from paper_1502_04265_b200.evaluation import kmeans_repetitions, kmeans_repetitions_device
+    from paper_1502_04265_b200.pipeline import PiecyConfig, run_piecy, run_piecy_device
+
+    cfg, X = workload(args)
+    n, d = X.shape
+    pcfg = PiecyConfig(k=cfg.k, piece_size=cfg.piece_size, svd_dim=cfg.svd_dim, coreset_size=cfg.m, seed=cfg.seed)
+    Xd = torch.from_numpy(X).to(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step_device():
+        eng = run_piecy_device(Xd, d, pcfg)
+        P, w = eng.extract_device()
+        C, costs = kmeans_repetitions_device(P, w, cfg.k, cfg.reps, cfg.seed, cfg.max_iters, 1e-4)
+        return P.shape[0], costs
+
+    if args.ncu:
+        step_device()
+        torch.cuda.synchronize()
+        return 0
+
+    for _ in range(args.warmup):
+        step_device()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    nat.prof_reset()
+    nat.prof_enable(True)
+    l0 = nat.launch_count()
+    st = torch.cuda.current_stream()
+    evs = []
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        F, costs = step_device()
+        e1.record(st)
+        evs.append((e0, e1))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = nat.launch_count() - l0
+    nat.prof_enable(False)
+    ms_steps = [a.elapsed_time(b) for a, b in evs]
+    ms = float(np.sum(ms_steps))
+    prof = {k: nat.prof_read(k) for k in ("resolve", "chain", "reattach")}
+    clk = clocks.stop()
+
+    # e2e: public API with host buffers (H2D of the stream, D2H of coreset + centers + costs)
+    e2e_times = []
+    h2d = d2h = 0
+    for it in range(max(1, min(args.steps, 3))):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        cs = run_piecy(X, d, pcfg)
+        runs = kmeans_repetitions(cs.points, cs.weights.astype(np.float64), cfg.k, reps=cfg.reps, seed=cfg.seed,
+                                  max_iters=cfg.max_iters, tol=1e-4)
+        torch.cuda.synchronize()
+        e2e_times.append(time.perf_counter() - t0)
+        h2d = X.nbytes + cs.points.nbytes + cs.weights.size * 8 + cfg.reps * cfg.k * 8
+        d2h = cs.points.nbytes + cs.weights.nbytes + sum(c.nbytes + 8 for c, _ in runs)
+
+    t_local = torch.tensor([ms / args.steps, float(np.mean(e2e_times))], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    ms_step, e2e_s = float(t_local[0]), float(t_local[1])
+
+    if rank == 0:
+        peaks = {}
+        try:
+            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+                peaks = json.load(f)
+        except Exception:
+            pass
+        hbm = float(peaks.get("hbm_gbs", 6650.0))
+        peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+        # dominant kernel by device time share
+        dom = max(prof, key=lambda k: prof[k][0])
+        r_ms, r_cnt, r_units = prof["resolve"]
+        # K3 algorithmic bytes per point: x row read, s row read+write (fp64),
+        # node scalars (w, q, sn) read+write, chain entry (id + part)
+        bytes_per_pt = 8 * d * 3 + 48 + 12
+        achieved = (r_units * bytes_per_pt) / (r_ms / 1e3) / 1e9 if r_ms > 0 else 0.0
+        roof = {"kernel": "k_resolve (K3 in-order resolve + CF update)", "bound": "hbm",
+                "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "traffic": None, "peak_source": peak_src,
+                "note": "latency-bound sequential scan (one warp); algorithmic bytes = 24*d+60 per point",
+                "ns_per_point": (r_ms * 1e6 / r_units) if r_units else None,
+                "share_of_step": r_ms / ms if ms > 0 else None}
+        kernel_ms = {k: {"ms": v[0] / args.steps, "launches": v[1] / args.steps, "units": v[2] / args.steps}
+                     for k, v in prof.items()}
+        cpu = None
+        if not args.no_cpu_baseline:
+            rows, t = cpu_sample(cfg, X)
+            cpu = {"value": rows / t, "unit": "points/s", "cores": os.cpu_count() or 1, "kind": "port",
+                   "sample": f"first {rows} of {n} rows of {cfg.name}, one pass; BICO in C (1 thread), "
+                             f"clustering numpy/OpenBLAS"}
+        line = {
+            "metric": METRIC, "value": n * world / (ms_step / 1e3), "unit": "points/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_json(cfg, X, world),
+            "e2e": {"value": n * world / e2e_s, "unit": "points/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": int(launches),
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "clocks": clk,
+            "kernel_ms_per_step": kernel_ms,
+            "dominant_kernel": dom,
+            "coreset_size": int(F),
+            "step_ms": ms_steps,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -28,7 +28,33 @@ _SIGS = {
     "pcy_engine_stats": (c_i32, [c_vp, P_i64, P_f64, P_i64, P_i32, c_vp]),
     "pcy_engine_features": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, P_i64, c_vp]),
     "pcy_engine_extract": (c_i32, [c_vp, c_vp, c_vp, c_i64, P_i64, c_vp]),
+    # instrumentation
+    "pcy_launch_count": (c_i64, []),
+    "pcy_prof_enable": (c_i32, [c_i32]),
+    "pcy_prof_reset": (c_i32, []),
+    "pcy_prof_read": (c_i32, [c_i32, P_f64, P_i64, P_i64]),
 }
+
+PROF_SLOTS = {"resolve": 0, "chain": 1, "reattach": 2, "seed": 3, "lloyd": 4, "gemm": 5}
+
+
+def launch_count() -> int:
+    return int(lib().pcy_launch_count())
+
+
+def prof_enable(on: bool = True) -> None:
+    lib().pcy_prof_enable(1 if on else 0)
+
+
+def prof_reset() -> None:
+    lib().pcy_prof_reset()
+
+
+def prof_read(name: str):
+    """(total ms, launches, units) accumulated for a profiled kernel."""
+    ms, cnt, units = c_f64(), c_i64(), c_i64()
+    lib().pcy_prof_read(PROF_SLOTS[name], ctypes.byref(ms), ctypes.byref(cnt), ctypes.byref(units))
+    return ms.value, cnt.value, units.value
 
 _OPTIONAL = set()
 

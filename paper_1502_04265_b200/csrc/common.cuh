@@ -23,6 +23,14 @@ enum PcyStatus {
 };
 
 void pcy_set_error(const char* fmt, ...);
+void pcy_count_launch();
+
+// Per-kernel event timing (enabled by pcy_prof_enable).
+enum { PCY_PROF_RESOLVE = 0, PCY_PROF_CHAIN = 1, PCY_PROF_REATTACH = 2, PCY_PROF_SEED = 3,
+       PCY_PROF_LLOYD = 4, PCY_PROF_GEMM = 5, PCY_PROF_SLOTS = 8 };
+struct PcyProfSlot { double ms = 0.0; long long count = 0; long long units = 0; };
+bool pcy_prof_enabled();
+void pcy_prof_add(int slot, double ms, long long units);
 
 #define PCY_CUDA(call)                                                        \
   do {                                                                        \

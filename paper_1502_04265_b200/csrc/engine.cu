@@ -15,6 +15,9 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
+#include <mutex>
+#include <cstdlib>
 #include <vector>
 #include "engine.cuh"
 
@@ -23,6 +26,32 @@ void pcy_set_error(const char* fmt, ...) {
   va_list ap; va_start(ap, fmt); vsnprintf(g_err, sizeof(g_err), fmt, ap); va_end(ap);
 }
 extern "C" const char* pcy_last_error(void) { return g_err; }
+
+// Launch counter (bench.py's gpu_launches) and optional per-kernel event
+// timing of the engine's sequential kernels (bench.py's roofline).
+static std::atomic<long long> g_launches{0};
+void pcy_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+static std::atomic<int> g_prof_on{0};
+static std::mutex g_prof_mu;
+static PcyProfSlot g_prof[PCY_PROF_SLOTS];
+bool pcy_prof_enabled() { return g_prof_on.load(std::memory_order_relaxed) != 0; }
+void pcy_prof_add(int slot, double ms, long long units) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof[slot].ms += ms; g_prof[slot].count += 1; g_prof[slot].units += units;
+}
+extern "C" long long pcy_launch_count(void) { return g_launches.load(); }
+extern "C" int pcy_prof_enable(int on) { g_prof_on.store(on); return 0; }
+extern "C" int pcy_prof_reset(void) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (auto& p : g_prof) p = PcyProfSlot{};
+  return 0;
+}
+extern "C" int pcy_prof_read(int slot, double* ms, long long* count, long long* units) {
+  if (slot < 0 || slot >= PCY_PROF_SLOTS) return PCY_EINVAL;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  *ms = g_prof[slot].ms; *count = g_prof[slot].count; *units = g_prof[slot].units;
+  return 0;
+}
 
 // ----------------------------------------------------------------- helpers
 __device__ __forceinline__ bool rows_equal(const double* a, const double* b, int d, int lane) {
@@ -87,6 +116,9 @@ __device__ __forceinline__ void scan_members(const EngDev& E, const int* __restr
     if (part < bp) { bp = part; bpos = pos; }
   }
 }
+
+#include "resolve_fast.cuh"
+#include "reattach_fast.cuh"
 
 // ------------------------------------------------------------------ stage
 // One warp per row: fp32/fp64 -> fp64 padded row, x_sq, validation, hash.
@@ -660,6 +692,12 @@ struct Engine {
   EngCtl* ctl_h = nullptr;   // pinned mirror
   long long* aggw = nullptr;
   double* mp_nrm = nullptr;
+  cudaEvent_t ev[6] = {};
+  ChainHdr* chh = nullptr;
+  ChainLvl* chr = nullptr;
+  int nper = 0;          // fast path registers per lane (0 = generic path)
+  int nnew_cap = 0;
+  size_t res_smem = 0;
   std::vector<void*> allocs;
 
   template <class T> int alloc(T*& p, long long count) {
@@ -674,6 +712,7 @@ struct Engine {
     for (auto& a : allocs) if (a == p) { cudaFree(a); a = nullptr; }
   }
   ~Engine() {
+    for (auto& e : ev) if (e) cudaEventDestroy(e);
     for (void* a : allocs) if (a) cudaFree(a);
     if (ctl_h) cudaFreeHost(ctl_h);
   }
@@ -705,6 +744,7 @@ struct Engine {
     A_(E.ctl, 1);
     A_(E.xb, Bmax * ld); A_(E.xsq, Bmax); A_(E.wb, Bmax); A_(E.hsh, Bmax); A_(E.bad, Bmax);
     A_(E.ch_node, Bmax * PCY_MAXL); A_(E.ch_part, Bmax * PCY_MAXL); A_(E.ch_len, Bmax);
+    A_(chh, Bmax); A_(chr, Bmax * PCY_FMAXL);
     E.pend_cap = m + 2;
     A_(E.pend_x, E.pend_cap * ld); A_(E.pend_w, E.pend_cap); A_(E.pend_xsq, E.pend_cap);
     A_(E.dist_x, (m + 2) * ld);
@@ -714,6 +754,30 @@ struct Engine {
     A_(E.minbits, 2);
     A_(aggw, m + 2); A_(mp_nrm, sample_cap + 1);
 #undef A_
+    for (auto& e : ev) PCY_CUDA(cudaEventCreate(&e));
+    if (ld <= 256) {
+      nper = ld <= 32 ? 1 : ld <= 64 ? 2 : ld <= 128 ? 4 : 8;
+      const size_t base = resolve_smem_bytes(ld, 0, NC, GC);
+      const size_t maxsm = 227 * 1024;
+      long long cap = maxsm > base ? (long long)((maxsm - base) / (2 * sizeof(double) * ld)) : 0;
+      if (cap > PCY_NNEW_MAX) cap = PCY_NNEW_MAX;
+      nnew_cap = (int)cap;
+      res_smem = resolve_smem_bytes(ld, nnew_cap, NC, GC);
+      if (nnew_cap < 8) nper = 0;   // budget too large for the shared-memory tables
+      PCY_CUDA(cudaFuncSetAttribute(k_chain2, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+      PCY_CUDA(cudaFuncSetAttribute(k_rchain, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+      switch (nper) {
+        case 1: PCY_CUDA(cudaFuncSetAttribute(k_resolve2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
+                  PCY_CUDA(cudaFuncSetAttribute(k_reattach2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem)); break;
+        case 2: PCY_CUDA(cudaFuncSetAttribute(k_resolve2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
+                  PCY_CUDA(cudaFuncSetAttribute(k_reattach2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem)); break;
+        case 4: PCY_CUDA(cudaFuncSetAttribute(k_resolve2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
+                  PCY_CUDA(cudaFuncSetAttribute(k_reattach2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem)); break;
+        default: PCY_CUDA(cudaFuncSetAttribute(k_resolve2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
+                 PCY_CUDA(cudaFuncSetAttribute(k_reattach2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem)); break;
+      }
+      if (getenv("PCY_GENERIC_RESOLVE")) nper = 0;
+    }
     PCY_CUDA(cudaMallocHost(&ctl_h, sizeof(EngCtl)));
     memset(ctl_h, 0, sizeof(EngCtl));
     PCY_CUDA(cudaMemcpy(E.ctl, ctl_h, sizeof(EngCtl), cudaMemcpyHostToDevice));
@@ -743,11 +807,43 @@ struct Engine {
     while (ctl_h->F > m) {
       const long long nslots = ctl_h->F_alloc;
       const long long nodes = ctl_h->F;
-      k_rb_rank<<<(unsigned)((nslots + 255) / 256), 256, 0, st>>>(E, nslots);
-      k_rb_reset<<<(unsigned)((nslots + 255) / 256), 256, 0, st>>>(E, nslots);
-      k_rb_reattach<<<1, 512, sizeof(double) * ld, st>>>(E, nodes);
+      k_rb_rank<<<(unsigned)((nslots + 255) / 256), 256, 0, st>>>(E, nslots); pcy_count_launch();
+      k_rb_reset<<<(unsigned)((nslots + 255) / 256), 256, 0, st>>>(E, nslots); pcy_count_launch();
+      const bool prof = pcy_prof_enabled();
+      if (prof) PCY_CUDA(cudaEventRecord(ev[3], st));
+      int rc;
+      if (nper) {
+        long long off = 0;
+        const int wpc = ld <= 512 ? 8 : (ld <= 2048 ? 4 : 2);
+        while (off < nodes) {
+          const long long nb = nodes - off < 1024 ? nodes - off : 1024;
+          k_rchain<<<(unsigned)((nb + wpc - 1) / wpc), wpc * 32, sizeof(double) * wpc * ld, st>>>(E, E.order + off, nb, chh, chr); pcy_count_launch();
+          switch (nper) {
+            case 1: k_reattach2<1><<<1, 32, res_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr); pcy_count_launch(); break;
+            case 2: k_reattach2<2><<<1, 32, res_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr); pcy_count_launch(); break;
+            case 4: k_reattach2<4><<<1, 32, res_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr); pcy_count_launch(); break;
+            default: k_reattach2<8><<<1, 32, res_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr); pcy_count_launch(); break;
+          }
+          PCY_LAUNCH_CHECK();
+          rc = sync_ctl(st); if (rc) return rc;
+          if (ctl_h->status == ST_ARENA) { pcy_set_error("member arena exhausted in rebuild"); return PCY_ESTATE; }
+          if (ctl_h->status == ST_FULL) {
+            if (ctl_h->stop == 0) { pcy_set_error("reattach made no progress"); return PCY_ESTATE; }
+            off += ctl_h->stop;
+          } else off += nb;
+        }
+      } else {
+        k_rb_reattach<<<1, 512, sizeof(double) * ld, st>>>(E, nodes); pcy_count_launch();
+      }
+      if (prof) PCY_CUDA(cudaEventRecord(ev[4], st));
       PCY_LAUNCH_CHECK();
-      int rc = sync_ctl(st); if (rc) return rc;
+      rc = sync_ctl(st); if (rc) return rc;
+      if (ctl_h->status == ST_ARENA) { pcy_set_error("member arena exhausted in rebuild"); return PCY_ESTATE; }
+      if (prof) {
+        float t = 0.f;
+        PCY_CUDA(cudaEventElapsedTime(&t, ev[3], ev[4]));
+        pcy_prof_add(PCY_PROF_REATTACH, t, nodes);
+      }
       if (ctl_h->status == ST_ARENA) { pcy_set_error("member arena exhausted in rebuild"); return PCY_ESTATE; }
     }
     return PCY_OK;
@@ -761,24 +857,53 @@ struct Engine {
     *bad_at = -1;
     long long off = 0;
     while (off < n) {
-      const long long nb = n - off < Bmax ? n - off : Bmax;
+      const long long sub = nper ? (long long)1024 : Bmax;   // items one K3 launch can usually absorb
+      const long long nb = n - off < sub ? n - off : sub;
       long long start = 0, first_rem = -1;
       while (start < nb) {
         const double* Xs = X + (off + start) * ld;
         const double* XSs = XS + off + start;
-        k_snapshot<<<64, 256, 0, st>>>(E);
+        const bool prof = pcy_prof_enabled();
+        const long long* Ws = W ? W + off + start : nullptr;
+        const int* Bs = BAD ? BAD + off + start : nullptr;
         const int wpc = ld <= 512 ? 8 : (ld <= 2048 ? 4 : 2);
-        k_chain<<<(unsigned)((nb - start + wpc - 1) / wpc), wpc * 32, sizeof(double) * wpc * ld, st>>>(
-            E, Xs, XSs, nb - start);
-        k_resolve<<<1, 32, sizeof(double) * ld, st>>>(
-            E, Xs, XSs, W ? W + off + start : nullptr, BAD ? BAD + off + start : nullptr,
-            nb - start, 0, first_rem, countw);
+        const unsigned nblk = (unsigned)((nb - start + wpc - 1) / wpc);
+        if (!nper) { k_snapshot<<<64, 256, 0, st>>>(E); pcy_count_launch(); }
+        if (prof) PCY_CUDA(cudaEventRecord(ev[0], st));
+        if (nper) {
+          k_chain2<<<nblk, wpc * 32, sizeof(double) * wpc * ld, st>>>(E, Xs, XSs, Ws, nb - start, chh, chr); pcy_count_launch();
+        } else {
+          k_chain<<<nblk, wpc * 32, sizeof(double) * wpc * ld, st>>>(E, Xs, XSs, nb - start); pcy_count_launch();
+        }
+        if (prof) PCY_CUDA(cudaEventRecord(ev[1], st));
+        switch (nper) {
+          case 1: k_resolve2<1><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
+          case 2: k_resolve2<2><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
+          case 4: k_resolve2<4><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
+          case 8: k_resolve2<8><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
+          default:
+            k_resolve<<<1, 32, sizeof(double) * ld, st>>>(E, Xs, XSs, Ws, Bs, nb - start, 0, first_rem, countw); pcy_count_launch();
+        }
+        if (prof) PCY_CUDA(cudaEventRecord(ev[2], st));
         PCY_LAUNCH_CHECK();
         int rc = sync_ctl(st); if (rc) return rc;
+        if (prof) {
+          float t1 = 0.f, t2 = 0.f;
+          PCY_CUDA(cudaEventElapsedTime(&t1, ev[0], ev[1]));
+          PCY_CUDA(cudaEventElapsedTime(&t2, ev[1], ev[2]));
+          const long long done = ctl_h->status == ST_DONE ? nb - start : ctl_h->stop + (ctl_h->status == ST_FULL ? 0 : 1);
+          pcy_prof_add(PCY_PROF_CHAIN, t1, nb - start);
+          pcy_prof_add(PCY_PROF_RESOLVE, t2, done);
+        }
         const int status = ctl_h->status;
         if (status == ST_DONE) break;
         if (status == ST_INVALID) { *bad_at = off + start + ctl_h->stop; *bad_code = ctl_h->err; return PCY_OK; }
         if (status == ST_ARENA) { pcy_set_error("member arena exhausted"); return PCY_ESTATE; }
+        if (status == ST_FULL) {
+          if (ctl_h->stop == 0) { pcy_set_error("resolve made no progress"); return PCY_ESTATE; }
+          start += ctl_h->stop; first_rem = -1;
+          continue;
+        }
         if (status == ST_REBUILD) {
           const long long at = start + ctl_h->stop;
           const long long r = ctl_h->remaining;
@@ -799,11 +924,11 @@ struct Engine {
     const long long ns = ctl_h->ndist < sample_cap ? ctl_h->ndist : sample_cap;
     unsigned long long init[2] = {0x7ff0000000000000ULL, 0ULL};
     PCY_CUDA(cudaMemcpyAsync(E.minbits, init, sizeof(init), cudaMemcpyHostToDevice, st));
-    k_mp_norms<<<(unsigned)((ns + 7) / 8), 256, 0, st>>>(E, ns, mp_nrm);
+    k_mp_norms<<<(unsigned)((ns + 7) / 8), 256, 0, st>>>(E, ns, mp_nrm); pcy_count_launch();
     dim3 grid((unsigned)((ns + 31) / 32), (unsigned)((ns + 31) / 32));
-    if (ns >= 2) k_mp_tiles<<<grid, dim3(32, 8), 0, st>>>(E, ns, mp_nrm);
-    k_mp_finish<<<1, 1, 0, st>>>(E, ns);
-    k_tree_reset<<<1, 1, 0, st>>>(E);
+    if (ns >= 2) { k_mp_tiles<<<grid, dim3(32, 8), 0, st>>>(E, ns, mp_nrm); pcy_count_launch(); }
+    k_mp_finish<<<1, 1, 0, st>>>(E, ns); pcy_count_launch();
+    k_tree_reset<<<1, 1, 0, st>>>(E); pcy_count_launch();
     PCY_LAUNCH_CHECK();
     int rc = sync_ctl(st); if (rc) return rc;
     built = true;
@@ -822,12 +947,12 @@ struct Engine {
     while (pos < n) {
       const long long nb = n - pos < Bmax ? n - pos : Bmax;
       k_stage<<<(unsigned)((nb + 7) / 8), 256, 0, st>>>(E, (const char*)x + (size_t)pos * stride * esz,
-                                                         dtype, stride, w ? w + pos : nullptr, nb, built ? 0 : 1);
+                                                         dtype, stride, w ? w + pos : nullptr, nb, built ? 0 : 1); pcy_count_launch();
       PCY_LAUNCH_CHECK();
       long long i = 0;
       while (i < nb) {
         if (!built) {
-          k_boot<<<1, 32, 0, st>>>(E, i, nb);
+          k_boot<<<1, 32, 0, st>>>(E, i, nb); pcy_count_launch();
           PCY_LAUNCH_CHECK();
           int rc = sync_ctl(st); if (rc) return rc;
           const int status = ctl_h->status;
@@ -853,7 +978,7 @@ struct Engine {
   int count(cudaStream_t st, long long* cnt) {
     int rc = sync_ctl(st); if (rc) return rc;
     if (!built) { *cnt = ctl_h->ndist; return PCY_OK; }
-    k_dfs<<<1, 1, 0, st>>>(E);
+    k_dfs<<<1, 1, 0, st>>>(E); pcy_count_launch();
     PCY_LAUNCH_CHECK();
     rc = sync_ctl(st); if (rc) return rc;
     *cnt = ctl_h->stop;
@@ -867,12 +992,13 @@ struct Engine {
     if (n <= 0) return PCY_OK;
     if (!built) {
       PCY_CUDA(cudaMemsetAsync(aggw, 0, sizeof(long long) * (ctl_h->ndist + 1), st));
-      k_boot_aggregate<<<(unsigned)((ctl_h->npend + 7) / 8), 256, 0, st>>>(E, aggw);
-      k_boot_gather<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(E, n, aggw, lv, wo, so, qo, ro, po);
+      k_boot_aggregate<<<(unsigned)((ctl_h->npend + 7) / 8), 256, 0, st>>>(E, aggw); pcy_count_launch();
+      k_boot_gather<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(E, n, aggw, lv, wo, so, qo, ro, po); pcy_count_launch();
     } else {
-      if (po) k_gather_points<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(E, n, po, wo);
-      if (lv || so || qo || ro || (wo && !po))
-        k_gather_features<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(E, n, lv, wo, so, qo, ro);
+      if (po) { k_gather_points<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(E, n, po, wo); pcy_count_launch(); }
+      if (lv || so || qo || ro || (wo && !po)) {
+        k_gather_features<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(E, n, lv, wo, so, qo, ro); pcy_count_launch();
+      }
     }
     PCY_LAUNCH_CHECK();
     return PCY_OK;

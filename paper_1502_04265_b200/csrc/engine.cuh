@@ -14,6 +14,7 @@ enum {
   ST_BUILD = 3,     // bootstrap saw budget+1 distinct locations at item `stop`
   ST_GROW = 4,      // bootstrap pending buffer full before item `stop`
   ST_ARENA = 5,     // member arena exhausted (internal error)
+  ST_FULL = 6,      // resolve tables full before item `stop`: relaunch from there
 };
 
 struct EngCtl {

@@ -308,7 +308,7 @@ int pcy_kmeanspp(const double* P, const double* w, long long n, int d, int k, in
   PCY_CUDA(cudaMallocAsync(&picks, sizeof(int) * k * reps, st));
   const size_t sm = sizeof(double) * d;
   if (sm > 48 * 1024) PCY_CUDA(cudaFuncSetAttribute(k_seed, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  k_seed<<<reps, KM_THREADS, sm, st>>>(P, w, n, d, k, U, centers, best, mass, picks);
+  k_seed<<<reps, KM_THREADS, sm, st>>>(P, w, n, d, k, U, centers, best, mass, picks); pcy_count_launch();
   PCY_LAUNCH_CHECK();
   if (picks_out) {
     std::vector<int> h((size_t)k * reps);
@@ -340,7 +340,7 @@ int pcy_lloyd(const double* P, const double* w, long long n, int d, int k, int r
   std::vector<int> act(reps, 1);
   std::vector<double> prev(reps, INFINITY), hc(reps);
   for (int r = 0; r < reps; ++r) iters_out[r] = 0;
-  k_rownorm<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(P, n, d, pn);
+  k_rownorm<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(P, n, d, pn); pcy_count_launch();
   const size_t usm = sizeof(double) * d;
   if (usm > 48 * 1024) PCY_CUDA(cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usm));
   for (int it = 0; it < max_iters; ++it) {
@@ -348,9 +348,9 @@ int pcy_lloyd(const double* P, const double* w, long long n, int d, int k, int r
     for (int r = 0; r < reps; ++r) nact += act[r];
     if (!nact) break;
     PCY_CUDA(cudaMemcpyAsync(active, act.data(), sizeof(int) * reps, cudaMemcpyHostToDevice, st));
-    k_rownorm<<<(unsigned)((k * reps + 7) / 8), 256, 0, st>>>(centers, (long long)k * reps, d, cn);
-    k_assign<<<dim3((unsigned)((n + 7) / 8), reps), 256, 0, st>>>(P, pn, n, d, k, centers, cn, active, assign, best);
-    k_finish<<<reps, KM_THREADS, 0, st>>>(P, w, n, d, k, centers, active, assign, best, counts, cost, 1);
+    k_rownorm<<<(unsigned)((k * reps + 7) / 8), 256, 0, st>>>(centers, (long long)k * reps, d, cn); pcy_count_launch();
+    k_assign<<<dim3((unsigned)((n + 7) / 8), reps), 256, 0, st>>>(P, pn, n, d, k, centers, cn, active, assign, best); pcy_count_launch();
+    k_finish<<<reps, KM_THREADS, 0, st>>>(P, w, n, d, k, centers, active, assign, best, counts, cost, 1); pcy_count_launch();
     PCY_LAUNCH_CHECK();
     PCY_CUDA(cudaMemcpyAsync(hc.data(), cost, sizeof(double) * reps, cudaMemcpyDeviceToHost, st));
     PCY_CUDA(cudaStreamSynchronize(st));
@@ -365,7 +365,7 @@ int pcy_lloyd(const double* P, const double* w, long long n, int d, int k, int r
     }
     if (!any_update) break;
     PCY_CUDA(cudaMemcpyAsync(active, act.data(), sizeof(int) * reps, cudaMemcpyHostToDevice, st));
-    k_update<<<dim3(k, reps), 256, usm, st>>>(P, w, n, d, k, active, assign, centers);
+    k_update<<<dim3(k, reps), 256, usm, st>>>(P, w, n, d, k, active, assign, centers); pcy_count_launch();
     PCY_LAUNCH_CHECK();
   }
   PCY_CUDA(cudaStreamSynchronize(st));
@@ -385,10 +385,10 @@ int pcy_weighted_cost(const double* P, const double* w, long long n, int d, int 
   PCY_CUDA(cudaMallocAsync(&best, sizeof(double) * n * reps, st));
   PCY_CUDA(cudaMallocAsync(&assign, sizeof(int) * n * reps, st));
   PCY_CUDA(cudaMallocAsync(&cost, sizeof(double) * reps, st));
-  k_rownorm<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(P, n, d, pn);
-  k_rownorm<<<(unsigned)((k * reps + 7) / 8), 256, 0, st>>>(centers, (long long)k * reps, d, cn);
-  k_assign<<<dim3((unsigned)((n + 7) / 8), reps), 256, 0, st>>>(P, pn, n, d, k, centers, cn, nullptr, assign, best);
-  k_finish<<<reps, KM_THREADS, 0, st>>>(P, w, n, d, k, (double*)centers, nullptr, assign, best, nullptr, cost, 0);
+  k_rownorm<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(P, n, d, pn); pcy_count_launch();
+  k_rownorm<<<(unsigned)((k * reps + 7) / 8), 256, 0, st>>>(centers, (long long)k * reps, d, cn); pcy_count_launch();
+  k_assign<<<dim3((unsigned)((n + 7) / 8), reps), 256, 0, st>>>(P, pn, n, d, k, centers, cn, nullptr, assign, best); pcy_count_launch();
+  k_finish<<<reps, KM_THREADS, 0, st>>>(P, w, n, d, k, (double*)centers, nullptr, assign, best, nullptr, cost, 0); pcy_count_launch();
   PCY_LAUNCH_CHECK();
   PCY_CUDA(cudaMemcpyAsync(costs, cost, sizeof(double) * reps, cudaMemcpyDeviceToHost, st));
   PCY_CUDA(cudaStreamSynchronize(st));

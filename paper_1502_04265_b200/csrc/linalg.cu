@@ -268,6 +268,11 @@ __global__ void k_scale_rows(const double* __restrict__ A, const long long* __re
   }
 }
 
+__global__ void k_cast_i64(const long long* __restrict__ src, long long n, double* __restrict__ dst) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    dst[i] = (double)src[i];
+}
+
 __global__ void k_all_finite(const void* __restrict__ p, long long n, int dt, int* __restrict__ flag) {
   bool ok = true;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
@@ -282,7 +287,7 @@ static int gemm(cudaStream_t st, int M, int N, int K, double alpha, const double
                 const double* B, long long ldb, int tb, double beta, double* C, long long ldc) {
   if (M <= 0 || N <= 0) return PCY_OK;
   dim3 grid((unsigned)((N + GBN - 1) / GBN), (unsigned)((M + GBM - 1) / GBM));
-  k_dgemm<<<grid, 128, 0, st>>>(M, N, K, alpha, A, lda, ta, B, ldb, tb, beta, C, ldc);
+  k_dgemm<<<grid, 128, 0, st>>>(M, N, K, alpha, A, lda, ta, B, ldb, tb, beta, C, ldc); pcy_count_launch();
   PCY_LAUNCH_CHECK();
   return PCY_OK;
 }
@@ -295,7 +300,7 @@ static int cholqr(cudaStream_t st, double* Y, long long rows, int r, double* Gs,
   auto pass = [&](double shift, int* ok) -> int {
     int rc;
     if ((rc = gemm(st, r, r, (int)rows, 1.0, Y, r, 1, Y, r, 0, 0.0, Gs, r))) return rc;
-    k_chol_inv<<<1, 1024, 0, st>>>(Gs, r, shift, Ls, Li, status);
+    k_chol_inv<<<1, 1024, 0, st>>>(Gs, r, shift, Ls, Li, status); pcy_count_launch();
     PCY_LAUNCH_CHECK();
     PCY_CUDA(cudaMemcpyAsync(&hs, status, sizeof(int), cudaMemcpyDeviceToHost, st));
     PCY_CUDA(cudaStreamSynchronize(st));
@@ -337,7 +342,7 @@ int pcy_all_finite(const void* p, long long n, int dtype, int* out_host, void* s
   PCY_CUDA(cudaMallocAsync(&flag, sizeof(int), st));
   const int one = 1;
   PCY_CUDA(cudaMemcpyAsync(flag, &one, sizeof(int), cudaMemcpyHostToDevice, st));
-  if (n > 0) k_all_finite<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 8), 256, 0, st>>>(p, n, dtype, flag);
+  if (n > 0) { k_all_finite<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 8), 256, 0, st>>>(p, n, dtype, flag); pcy_count_launch(); }
   PCY_LAUNCH_CHECK();
   PCY_CUDA(cudaMemcpyAsync(out_host, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
   PCY_CUDA(cudaStreamSynchronize(st));
@@ -352,7 +357,14 @@ int pcy_dgemm(int M, int N, int K, double alpha, const double* A, long long lda,
 
 int pcy_cast_f32_f64(const float* src, long long n, double* dst, void* stream) {
   if (n <= 0) return PCY_OK;
-  k_cast_f32<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 16), 256, 0, (cudaStream_t)stream>>>(src, n, dst);
+  k_cast_f32<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 16), 256, 0, (cudaStream_t)stream>>>(src, n, dst); pcy_count_launch();
+  PCY_LAUNCH_CHECK();
+  return PCY_OK;
+}
+
+int pcy_cast_i64_f64(const long long* src, long long n, double* dst, void* stream) {
+  if (n <= 0) return PCY_OK;
+  k_cast_i64<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 16), 256, 0, (cudaStream_t)stream>>>(src, n, dst); pcy_count_launch();
   PCY_LAUNCH_CHECK();
   return PCY_OK;
 }
@@ -360,7 +372,7 @@ int pcy_cast_f32_f64(const float* src, long long n, double* dst, void* stream) {
 int pcy_scale_rows_sqrtw(const double* A, const long long* w, long long rows, int cols, double* out, void* stream) {
   if (rows <= 0) return PCY_OK;
   const long long n = rows * cols;
-  k_scale_rows<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 16), 256, 0, (cudaStream_t)stream>>>(A, w, rows, cols, out);
+  k_scale_rows<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 16), 256, 0, (cudaStream_t)stream>>>(A, w, rows, cols, out); pcy_count_launch();
   PCY_LAUNCH_CHECK();
   return PCY_OK;
 }
@@ -414,20 +426,20 @@ int pcy_rsvd(const double* A, long long rows, int cols, int ell, int r, int powe
       if ((rc = cholqr(st, Wm, cols, r, Gs, Ls, Li, T, status))) break;
       if ((rc = gemm(st, r, r, cols, 1.0, Bm, cols, 0, Wm, r, 0, 0.0, core, r))) break;
       // Jacobi on core^T: column j of core^T = row j of core (contiguous)
-      k_jacobi<<<1, 1024, 0, st>>>(core, r, r, tol, 60, sig, Uj, r, perm, sweeps);
+      k_jacobi<<<1, 1024, 0, st>>>(core, r, r, tol, 60, sig, Uj, r, perm, sweeps); pcy_count_launch();
       PCY_LAUNCH_CHECK();
       // Uj (r x r row-major) columns = right singular vectors of core: V = W Uj
       if ((rc = gemm(st, cols, r, r, 1.0, Wm, r, 0, Uj, r, 0, 0.0, Vfull, r))) break;
     } else {
       // Jacobi on small^T: column j of small^T = row j of small (contiguous)
-      k_jacobi<<<1, 1024, 0, st>>>(Bm, cols, r, tol, 60, sig, Vfull, r, perm, sweeps);
+      k_jacobi<<<1, 1024, 0, st>>>(Bm, cols, r, tol, 60, sig, Vfull, r, perm, sweeps); pcy_count_launch();
       PCY_LAUNCH_CHECK();
     }
-    k_sorted_sigma<<<1, 256, 0, st>>>(sig, r, sig + r);
+    k_sorted_sigma<<<1, 256, 0, st>>>(sig, r, sig + r); pcy_count_launch();
     // keep the first ell columns
     PCY_CUDA(cudaMemcpy2DAsync(V, sizeof(double) * ell, Vfull, sizeof(double) * r, sizeof(double) * ell, cols,
                                cudaMemcpyDeviceToDevice, st));
-    k_fix_signs<<<(ell + 7) / 8, 256, 0, st>>>(V, cols, ell, ell);
+    k_fix_signs<<<(ell + 7) / 8, 256, 0, st>>>(V, cols, ell, ell); pcy_count_launch();
     PCY_LAUNCH_CHECK();
     std::vector<double> hs(r);
     PCY_CUDA(cudaMemcpyAsync(hs.data(), sig + r, sizeof(double) * r, cudaMemcpyDeviceToHost, st));

@@ -1,0 +1,333 @@
+// K4 rebuild reattach, batched (included by engine.cu after resolve_fast.cuh).
+//
+// _reattach (coreset.py:395-421) re-inserts the collected nodes in (-weight,
+// index) order.  Like insertion, a node's nearest-reference chain depends only
+// on the references already placed, so it is computed for a whole batch in
+// parallel against the partially rebuilt tree (k_rchain, one warp per node),
+// together with the merge test under the snapshot statistics.  k_reattach2
+// then walks the batch in order on one warp, re-testing only against nodes
+// placed earlier in the same launch (shared-memory table) and recomputing the
+// merge test for hosts touched in the launch.
+
+__global__ void k_rchain(EngDev E, const int* __restrict__ order, long long n, ChainHdr* __restrict__ H,
+                         ChainLvl* __restrict__ R) {
+  extern __shared__ double sm_x[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const long long i = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
+  if (i >= n) return;
+  const int d = E.d, ld = E.ld;
+  const int u = order[i];
+  double* xv = sm_x + (long long)wib * ld;
+  for (int e = lane; e < d; e += 32) xv[e] = E.r[(long long)u * ld + e];
+  __syncwarp();
+  const double rsq = E.rn[u];
+  const long long wu = E.w[u];
+  const double qu = E.q[u];
+  const double* su = E.s + (long long)u * ld;
+  const double T = E.ctl->T;
+  ChainLvl* rec = R + i * PCY_FMAXL;
+  double radius = T;
+  int g = 0, L = 0, pred = -1, predj = -1, trunc = 0;
+  for (;;) {
+    const int cnt = E.g_count[g], base = E.g_base[g];
+    double bp; int bpos;
+    scan_members(E, E.arena + base, 0, cnt, xv, lane, bp, bpos);
+    const int j = bpos < cnt ? E.arena[base + bpos] : -1;
+    ChainLvl c = empty_level();
+    c.part = bp; c.j = j; c.g = g;
+    ++L;
+    const bool outside = j < 0 || radd(bp, rsq) > radius;
+    if (!outside) {
+      c.w = E.w[j]; c.q = E.q[j]; c.sn = E.sn[j]; c.child = E.child[j];
+      const double* sh = E.s + (long long)j * ld;
+      double acc = 0.0;
+      for (int e = lane; e < d; e += 32) { const double v = radd(sh[e], su[e]); acc = fma(v, v, acc); }
+      const double mnorm = warp_sum(acc);
+      const long long mw = c.w + wu;
+      const double mq = radd(c.q, qu);
+      c.nq = mq; c.nsn = mnorm;
+      c.take = rsub(mq, rdiv(mnorm, (double)mw)) <= T ? 1 : 0;
+      if (c.take && pred < 0) { pred = L - 1; predj = j; }
+    }
+    if (lane == 0) rec[L - 1] = c;
+    if (outside) { if (pred < 0) pred = L - 1; break; }
+    if (c.child < 0) {
+      if (L < PCY_FMAXL) {
+        if (lane == 0) rec[L] = empty_level();
+        ++L;
+        if (pred < 0) pred = L - 1;
+      } else trunc = 1;
+      break;
+    }
+    if (L >= PCY_FMAXL) { trunc = 1; break; }
+    g = c.child;
+    radius = rmul(radius, 0.25);
+  }
+  if (pred < 0) pred = L - 1;
+  if (lane == 0) H[i] = ChainHdr{L, pred, predj, trunc};
+}
+
+template <int NPER>
+__global__ void __launch_bounds__(32, 1) k_reattach2(EngDev E, const int* __restrict__ order, long long n,
+                                                     int nnew_cap, const ChainHdr* __restrict__ H,
+                                                     const ChainLvl* __restrict__ R) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  ResolveSmem& S = *reinterpret_cast<ResolveSmem*>(smraw);
+  const int lane = threadIdx.x;
+  const int d = E.d, ld = E.ld;
+  double* xsm = reinterpret_cast<double*>(smraw + ((sizeof(ResolveSmem) + 15) & ~size_t(15)));
+  double* tref = xsm + ld;
+  double* ts_unused = tref + (long long)nnew_cap * ld;
+  unsigned* mbits = reinterpret_cast<unsigned*>(ts_unused + (long long)nnew_cap * ld);
+  const int mwords = (int)(E.NC / 32 + 1);
+  unsigned* gbits = mbits + mwords;
+  const int gwords = (int)(E.GC / 32 + 1);
+  EngCtl* C = E.ctl;
+  const double T = C->T;
+  long long F = C->F, freen = C->free_n, Galloc = C->G_alloc, Aalloc = C->A_alloc;
+  const long long G0 = Galloc;
+  int status = ST_DONE; long long stop = n;
+
+  for (int s2 = lane; s2 < PCY_MOD_SLOTS; s2 += 32) S.mkey[s2] = -1;
+  for (int s2 = lane; s2 < PCY_GMAP_SLOTS; s2 += 32) S.gkey[s2] = -1;
+  for (int s2 = lane; s2 < mwords; s2 += 32) mbits[s2] = 0u;
+  for (int s2 = lane; s2 < gwords; s2 += 32) gbits[s2] = 0u;
+  if (lane == 0) S.modcount = 0;
+  int nnew = 0;
+
+  // ---- prologue: item 0
+  double xr[NPER], su[NPER], pr[NPER];
+  int u_c = n > 0 ? order[0] : 0;
+  int u_n = n > 1 ? order[1] : 0;
+  ChainHdr hc = n > 0 ? H[0] : ChainHdr{0, 0, -1, 0};
+  ChainHdr hn = n > 1 ? H[1] : ChainHdr{0, 0, -1, 0};
+  long long wu_c = 0; double qu_c = 0.0, snu_c = 0.0, rsq_c = 0.0;
+  if (n > 0) {
+    load_row<NPER>(xr, E.r + (long long)u_c * ld, d, lane);
+    load_row<NPER>(su, E.s + (long long)u_c * ld, d, lane);
+    if (hc.predj >= 0) load_row<NPER>(pr, E.s + (long long)hc.predj * ld, d, lane);
+    wu_c = E.w[u_c]; qu_c = E.q[u_c]; snu_c = E.sn[u_c]; rsq_c = E.rn[u_c];
+    const uint4* src = reinterpret_cast<const uint4*>(R);
+    uint4* dst = reinterpret_cast<uint4*>(&S.rb[0][0]);
+    for (int c = lane; c < REC_CHUNKS; c += 32) dst[c] = src[c];
+  }
+  __syncwarp();
+  int cur = 0;
+  int prnode = hc.predj;
+
+  for (long long i = 0; i < n; ++i) {
+    if (nnew >= nnew_cap || S.modcount >= PCY_MOD_SLOTS / 2) { status = ST_FULL; stop = i; break; }
+    // ---- prefetch item i+1
+    double xn[NPER], sun[NPER], pn[NPER];
+    uint4 rpf[(REC_CHUNKS + 31) / 32];
+    const bool has_next = i + 1 < n;
+    ChainHdr h2 = ChainHdr{0, 0, -1, 0};
+    int u2 = 0;
+    long long wu_n = 0; double qu_n = 0.0, snu_n = 0.0, rsq_n = 0.0;
+    if (has_next) {
+      load_row<NPER>(xn, E.r + (long long)u_n * ld, d, lane);
+      load_row<NPER>(sun, E.s + (long long)u_n * ld, d, lane);
+      wu_n = E.w[u_n]; qu_n = E.q[u_n]; snu_n = E.sn[u_n]; rsq_n = E.rn[u_n];
+      const uint4* src = reinterpret_cast<const uint4*>(R + (i + 1) * PCY_FMAXL);
+#pragma unroll
+      for (int q = 0; q < (REC_CHUNKS + 31) / 32; ++q) { const int c = lane + 32 * q; if (c < REC_CHUNKS) rpf[q] = src[c]; }
+      if (hn.predj >= 0) load_row<NPER>(pn, E.s + (long long)hn.predj * ld, d, lane);
+      if (i + 2 < n) { h2 = H[i + 2]; u2 = order[i + 2]; }
+    }
+    // ---- item i: node u
+    const int u = u_c;
+    const int len = hc.len;
+    int g = 0, L = 0;
+    double radius = T;
+    bool direct = false, xs_stored = false;
+    int lastmod = -1;
+    for (;;) {
+      int bj = -1, li = -1;
+      double bp = INFINITY;
+      if (!direct) {
+        if (L < len) { li = L; bj = S.rb[cur][L].j; bp = S.rb[cur][L].part; }
+        else direct = true;
+      }
+      if (direct && g < G0) {
+        if (!xs_stored) {
+#pragma unroll
+          for (int k = 0; k < NPER; ++k) { const int e = lane + 32 * k; if (e < ld) xsm[e] = xr[k]; }
+          __syncwarp();
+          xs_stored = true;
+        }
+        const int cnt = E.g_count[g];
+        if (cnt > 0) {
+          double p; int ps;
+          const int* mem = E.arena + E.g_base[g];
+          scan_members(E, mem, 0, cnt, xsm, lane, p, ps);
+          if (ps < cnt) { bj = mem[ps]; bp = p; }
+        }
+      }
+      int bt = -1;
+      if ((gbits[g >> 5] >> (g & 31)) & 1u) {
+        for (int tt = S.ghead[gmap_find(S, g)]; tt >= 0; tt = S.tnext[tt]) {
+          const double part = radd(S.trn[tt], rmul(smem_dot<NPER>(tref + (long long)tt * ld, xr, d, lane), -2.0));
+          if (part < bp || bj < 0) { bp = part; bt = tt; bj = S.tid[tt]; }
+        }
+      }
+      if (bj < 0 || radd(bp, rsq_c) > radius) {
+        // group.add(node): u keeps its statistics (coreset.py:403-406)
+        const int t = nnew++;
+        double* rr = tref + (long long)t * ld;
+#pragma unroll
+        for (int k = 0; k < NPER; ++k) { const int e = lane + 32 * k; if (e < ld) rr[e] = xr[k]; }
+        const bool had = ((gbits[g >> 5] >> (g & 31)) & 1u) != 0;
+        int gs;
+        if (had) gs = gmap_find(S, g);
+        else {
+          gs = (int)(((unsigned)g * 2654435761u) >> 24) & (PCY_GMAP_SLOTS - 1);
+          while (S.gkey[gs] >= 0) gs = (gs + 1) & (PCY_GMAP_SLOTS - 1);
+        }
+        if (lane == 0) {
+          S.tid[t] = u; S.tgrp[t] = g; S.tchild[t] = -1; S.tnext[t] = -1;
+          S.tw[t] = wu_c; S.tq[t] = qu_c; S.tsn[t] = snu_c; S.trn[t] = rsq_c;
+          if (had) { S.tnext[S.gtail[gs]] = t; S.gtail[gs] = t; }
+          else { S.gkey[gs] = g; S.ghead[gs] = t; S.gtail[gs] = t; gbits[g >> 5] |= 1u << (g & 31); }
+        }
+        ++F;
+        __syncwarp();
+        break;
+      }
+      // merge test with the host (coreset.py:407-417)
+      const bool touched = bt < 0 && ((mbits[bj >> 5] >> (bj & 31)) & 1u);
+      int ms = -1;
+      bool merge;
+      long long mw; double mq, mnorm;
+      long long hw; double hq, hsn;
+      if (bt < 0 && li >= 0 && !touched) {
+        const ChainLvl& rc = S.rb[cur][li];
+        hw = rc.w; hq = rc.q; hsn = rc.sn;
+        merge = rc.take != 0; mw = rc.w + wu_c; mq = rc.nq; mnorm = rc.nsn;
+      } else {
+        if (bt >= 0) { hw = S.tw[bt]; hq = S.tq[bt]; hsn = S.tsn[bt]; }
+        else if (touched) { ms = map_find(S, bj); hw = S.mw[ms]; hq = S.mq[ms]; hsn = S.msn[ms]; }
+        else { hw = E.w[bj]; hq = E.q[bj]; hsn = E.sn[bj]; }
+        if (bj != prnode) { load_row<NPER>(pr, E.s + (long long)bj * ld, d, lane); prnode = bj; }
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < NPER; ++k) { const double v = radd(pr[k], su[k]); acc = fma(v, v, acc); }
+        mnorm = warp_sum(acc);
+        mw = hw + wu_c; mq = radd(hq, qu_c);
+        merge = rsub(mq, rdiv(mnorm, (double)mw)) <= T;
+      }
+      if (merge) {
+        if (bj != prnode) { load_row<NPER>(pr, E.s + (long long)bj * ld, d, lane); prnode = bj; }
+#pragma unroll
+        for (int k = 0; k < NPER; ++k) pr[k] = radd(pr[k], su[k]);
+        store_row<NPER>(E.s + (long long)bj * ld, pr, d, lane);
+        if (bt >= 0) {
+          if (lane == 0) { S.tw[bt] = mw; S.tq[bt] = mq; S.tsn[bt] = mnorm; }
+          __syncwarp();
+        } else {
+          int child_now;
+          if (touched) { if (ms < 0) ms = map_find(S, bj); child_now = S.mchild[ms]; }
+          else child_now = li >= 0 ? S.rb[cur][li].child : E.child[bj];
+          ms = map_put(S, mbits, bj, mw, mq, mnorm, child_now, lane);
+          if (lane == 0) { E.w[bj] = mw; E.q[bj] = mq; E.sn[bj] = mnorm; }
+        }
+        if (lane == 0) { E.alive[u] = 0; E.free_ids[freen] = u; }
+        ++freen;
+        lastmod = bj;
+        __syncwarp();
+        break;
+      }
+      int c;
+      if (bt >= 0) {
+        c = S.tchild[bt];
+        if (c < 0) {
+          c = (int)Galloc++;
+          if (lane == 0) { S.tchild[bt] = c; E.g_count[c] = 0; E.g_cap[c] = 0; E.g_base[c] = 0; }
+          __syncwarp();
+        }
+        direct = true;
+      } else {
+        const bool tnow = ((mbits[bj >> 5] >> (bj & 31)) & 1u) != 0;
+        if (tnow && ms < 0) ms = map_find(S, bj);
+        c = tnow ? S.mchild[ms] : (li >= 0 ? S.rb[cur][li].child : E.child[bj]);
+        if (c < 0) {
+          c = (int)Galloc++;
+          if (lane == 0) { E.g_count[c] = 0; E.g_cap[c] = 0; E.g_base[c] = 0; E.child[bj] = c; }
+          if (tnow) { if (lane == 0) S.mchild[ms] = c; __syncwarp(); }
+          else ms = map_put(S, mbits, bj, hw, hq, hsn, c, lane);
+        }
+      }
+      g = c;
+      radius = rmul(radius, 0.25);
+      ++L;
+    }
+    __syncwarp();
+    if (has_next) {
+      uint4* dst = reinterpret_cast<uint4*>(&S.rb[cur ^ 1][0]);
+#pragma unroll
+      for (int q = 0; q < (REC_CHUNKS + 31) / 32; ++q) { const int c = lane + 32 * q; if (c < REC_CHUNKS) dst[c] = rpf[q]; }
+#pragma unroll
+      for (int k = 0; k < NPER; ++k) { xr[k] = xn[k]; su[k] = sun[k]; }
+      int nextnode = hn.predj;
+      if (nextnode >= 0 && nextnode == lastmod) {
+        if (prnode == lastmod) {
+#pragma unroll
+          for (int k = 0; k < NPER; ++k) pn[k] = pr[k];
+        } else nextnode = -1;
+      }
+#pragma unroll
+      for (int k = 0; k < NPER; ++k) pr[k] = pn[k];
+      prnode = nextnode;
+      hc = hn; hn = h2;
+      u_c = u_n; u_n = u2;
+      wu_c = wu_n; qu_c = qu_n; snu_c = snu_n; rsq_c = rsq_n;
+      cur ^= 1;
+    }
+    __syncwarp();
+  }
+
+  // ---- cleanup: statistics of placed nodes, memberships in position order
+  __syncwarp();
+  for (int t = lane; t < nnew; t += 32) {
+    const int node = S.tid[t];
+    E.w[node] = S.tw[t]; E.q[node] = S.tq[t]; E.sn[node] = S.tsn[t];
+    E.child[node] = S.tchild[t];
+    const int g = S.tgrp[t];
+    int k = 0, f = t;
+    for (int v = t - 1; v >= 0; --v) if (S.tgrp[v] == g) { ++k; f = v; }
+    S.tk[t] = k; S.tfirst[t] = f;
+    S.tcnt[t] = E.g_count[g]; S.tcap[t] = E.g_cap[g]; S.tbase[t] = E.g_base[g];
+  }
+  __syncwarp();
+  bool arena_ok = true;
+  for (int t = 0; t < nnew; ++t) {
+    if (S.tfirst[t] != t) continue;
+    const int g = S.tgrp[t];
+    int total = 0;
+    for (int v = t; v < nnew; ++v) total += (S.tgrp[v] == g);
+    const int cnt = S.tcnt[t], cap = S.tcap[t], base = S.tbase[t];
+    int nb = base, ncap = cap;
+    if (cnt + total > cap) {
+      ncap = cap ? 2 * cap : PCY_GROUP_MIN_CAP;
+      while (ncap < cnt + total) ncap *= 2;
+      if (Aalloc + ncap > E.AC) { arena_ok = false; break; }
+      nb = (int)Aalloc; Aalloc += ncap;
+      for (int p = lane; p < cnt; p += 32) E.arena[nb + p] = E.arena[base + p];
+    }
+    if (lane == 0) {
+      S.tbase[t] = nb; S.tcap[t] = ncap;
+      E.g_base[g] = nb; E.g_cap[g] = ncap; E.g_count[g] = cnt + total;
+    }
+    __syncwarp();
+  }
+  if (arena_ok) {
+    for (int t = lane; t < nnew; t += 32) {
+      const int f = S.tfirst[t];
+      E.arena[S.tbase[f] + S.tcnt[f] + S.tk[t]] = S.tid[t];
+    }
+  } else status = ST_ARENA;
+  __syncwarp();
+  if (lane == 0) {
+    C->F = F; C->free_n = freen; C->G_alloc = Galloc; C->A_alloc = Aalloc;
+    C->status = status; C->stop = stop;
+  }
+}

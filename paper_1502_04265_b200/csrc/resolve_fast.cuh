@@ -1,0 +1,527 @@
+// K1/K3 fast path for ld <= 256 (included by engine.cu after its helpers).
+//
+// k_chain2 (K1, warp per item, all items in parallel) records for every level
+// of an item's capacity-free chain the snapshot winner, its part, the snapshot
+// scalars (w, q, sn) of that node and the direct dot <s_j, x>, plus the level
+// at which the snapshot statistics say the item would stop (pred).
+//
+// k_resolve2 (K3, one warp, items in order) re-decides every level with the
+// *current* state.  State changed inside the launch lives in shared memory:
+//   * new-node table: nodes opened in this launch (ref row, s row, scalars,
+//     group, child) -- these are the only members appended since the snapshot;
+//   * modified map:   current (w, q, sn, child) of snapshot nodes touched in
+//     this launch (their s rows are written through to HBM).
+// Snapshot values from K1 are used whenever a node is untouched, so the common
+// item needs no HBM round trip on its critical path: its x row, chain record
+// and the s row of its predicted node are prefetched one item ahead.
+// <s, x> is always the same lane-strided fp64 dot (warp_dot order), whether
+// K1 or K3 evaluates it, so both produce identical values.
+#pragma once
+
+#define PCY_FMAXL 16
+#define PCY_MOD_SLOTS 2048
+#define PCY_NNEW_MAX 96
+#define PCY_GMAP_SLOTS 256
+
+struct __align__(16) ChainLvl {
+  double part, dot, q, sn;   // snapshot winner: part, <s_j, x>, q_j, sn_j
+  double nq, nsn;            // post-update q / sn when take > 0 (snapshot statistics)
+  long long w, take;         // snapshot weight; copies taken at this level (rem = W[i])
+  int j, g, child, pad;      // winner node, group of the level, snapshot child group
+};
+struct __align__(16) ChainHdr { int len, pred, predj, trunc; };
+
+__device__ __forceinline__ ChainLvl empty_level() {
+  ChainLvl t;
+  t.part = INFINITY; t.dot = 0.0; t.q = 0.0; t.sn = 0.0; t.nq = 0.0; t.nsn = 0.0;
+  t.w = 0; t.take = 0; t.j = -1; t.g = -1; t.child = -1; t.pad = 0;
+  return t;
+}
+
+// Closed-form capacity (coreset.py:336-356, inlined max_insertable_copies).
+__device__ __forceinline__ long long capacity(long long nn, double qv, double snv, double dt, double xs,
+                                              double T, long long rem) {
+  const double fn = (double)nn;
+  const double nrm = rdiv(snv, fn);
+  double errv = rsub(qv, nrm);
+  if (errv < 0.0) errv = 0.0;
+  double dist = rsub(xs, rdiv(rsub(rmul(2.0, dt), nrm), fn));
+  if (dist < 0.0) dist = 0.0;
+  const double slack = radd(rsub(rmul(fn, dist), T), errv);
+  if (slack <= 0.0) return rem;
+  const double limit = rdiv(rsub(rmul(fn, T), rmul(fn, errv)), slack);
+  if (limit >= (double)rem) return rem;
+  if (limit > 0.0) return (long long)limit;
+  return 0;
+}
+
+// ------------------------------------------------------------------- K1
+__global__ void k_chain2(EngDev E, const double* __restrict__ X, const double* __restrict__ XS,
+                         const long long* __restrict__ W, long long n, ChainHdr* __restrict__ H,
+                         ChainLvl* __restrict__ R) {
+  extern __shared__ double sm_x[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const long long i = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
+  if (i >= n) return;
+  const int d = E.d, ld = E.ld;
+  double* xv = sm_x + (long long)wib * ld;
+  const double xs = XS[i];
+  ChainLvl* rec = R + i * PCY_FMAXL;
+  if (!isfinite(xs)) { if (lane == 0) H[i] = ChainHdr{0, 0, -1, 0}; return; }
+  for (int e = lane; e < d; e += 32) xv[e] = X[i * ld + e];
+  __syncwarp();
+  const double T = E.ctl->T;
+  const long long rem = W ? W[i] : 1LL;
+  double radius = T;
+  int g = 0, L = 0, pred = -1, predj = -1, trunc = 0;
+  for (;;) {
+    const int cnt = E.g_count[g], base = E.g_base[g];
+    double bp; int bpos;
+    scan_members(E, E.arena + base, 0, cnt, xv, lane, bp, bpos);
+    const int j = bpos < cnt ? E.arena[base + bpos] : -1;
+    ChainLvl c = empty_level();
+    c.part = bp; c.j = j; c.g = g;
+    if (j >= 0) {
+      c.dot = warp_dot(E.s + (long long)j * ld, xv, d, lane);
+      c.w = E.w[j]; c.q = E.q[j]; c.sn = E.sn[j]; c.child = E.child[j];
+    }
+    ++L;
+    const bool outside = j < 0 || radd(bp, xs) > radius;
+    if (!outside) {
+      c.take = capacity(c.w, c.q, c.sn, c.dot, xs, T, rem);
+      if (c.take > 0) {
+        const double ft = (double)c.take;
+        c.nq = radd(c.q, rmul(ft, xs));
+        c.nsn = radd(c.sn, radd(rmul(rmul(2.0, ft), c.dot), rmul((double)(c.take * c.take), xs)));
+        if (pred < 0) { pred = L - 1; predj = j; }
+      }
+    }
+    if (lane == 0) rec[L - 1] = c;
+    if (outside) { if (pred < 0) pred = L - 1; break; }
+    if (c.child < 0) {
+      if (L < PCY_FMAXL) {
+        if (lane == 0) rec[L] = empty_level();
+        ++L;
+        if (pred < 0) pred = L - 1;
+      } else trunc = 1;
+      break;
+    }
+    if (L >= PCY_FMAXL) { trunc = 1; break; }
+    g = c.child;
+    radius = rmul(radius, 0.25);
+  }
+  if (pred < 0) pred = L - 1;
+  if (lane == 0) H[i] = ChainHdr{L, pred, predj, trunc};
+}
+
+// ------------------------------------------------------------------- K3
+struct ResolveSmem {
+  ChainLvl rb[2][PCY_FMAXL];                 // chain records, double buffered
+  int mkey[PCY_MOD_SLOTS], mchild[PCY_MOD_SLOTS];   // touched snapshot nodes
+  long long mw[PCY_MOD_SLOTS];
+  double mq[PCY_MOD_SLOTS], msn[PCY_MOD_SLOTS];
+  int gkey[PCY_GMAP_SLOTS], ghead[PCY_GMAP_SLOTS], gtail[PCY_GMAP_SLOTS];  // groups with new members
+  int tid[PCY_NNEW_MAX], tgrp[PCY_NNEW_MAX], tchild[PCY_NNEW_MAX], tnext[PCY_NNEW_MAX];
+  int tk[PCY_NNEW_MAX], tfirst[PCY_NNEW_MAX], tcnt[PCY_NNEW_MAX], tbase[PCY_NNEW_MAX], tcap[PCY_NNEW_MAX];
+  long long tw[PCY_NNEW_MAX];
+  double trn[PCY_NNEW_MAX], tq[PCY_NNEW_MAX], tsn[PCY_NNEW_MAX];
+  int modcount;
+};
+// dynamic tail: double xsm[ld]; double tref[nnew][ld]; double ts[nnew][ld];
+//               unsigned mbits[NC/32+1]; unsigned gbits[GC/32+1]
+
+__host__ __device__ inline size_t resolve_smem_bytes(int ld, int nnew, long long NC, long long GC) {
+  return ((sizeof(ResolveSmem) + 15) & ~size_t(15)) + sizeof(double) * (size_t)ld * (1 + 2 * (size_t)nnew) +
+         sizeof(unsigned) * (size_t)(NC / 32 + 1 + GC / 32 + 1);
+}
+
+__device__ __forceinline__ int map_slot(int id) { return (int)(((unsigned)id * 2654435761u) >> 21) & (PCY_MOD_SLOTS - 1); }
+
+__device__ __forceinline__ int map_find(const ResolveSmem& S, int id) {
+  int s = map_slot(id);
+  for (;;) {
+    const int k = S.mkey[s];
+    if (k == id) return s;
+    if (k < 0) return -1;
+    s = (s + 1) & (PCY_MOD_SLOTS - 1);
+  }
+}
+
+// insert-or-update; lane 0 writes; caller syncs
+__device__ __forceinline__ int map_put(ResolveSmem& S, unsigned* mbits, int id, long long w, double q, double sn,
+                                       int child, int lane) {
+  int s = map_slot(id);
+  while (S.mkey[s] >= 0 && S.mkey[s] != id) s = (s + 1) & (PCY_MOD_SLOTS - 1);
+  if (lane == 0) {
+    if (S.mkey[s] < 0) { S.modcount++; mbits[id >> 5] |= 1u << (id & 31); }
+    S.mkey[s] = id; S.mw[s] = w; S.mq[s] = q; S.msn[s] = sn; S.mchild[s] = child;
+  }
+  __syncwarp();
+  return s;
+}
+
+__device__ __forceinline__ int gmap_find(const ResolveSmem& S, int g) {
+  int s = (int)(((unsigned)g * 2654435761u) >> 24) & (PCY_GMAP_SLOTS - 1);
+  for (;;) {
+    const int k = S.gkey[s];
+    if (k == g) return s;
+    if (k < 0) return -1;
+    s = (s + 1) & (PCY_GMAP_SLOTS - 1);
+  }
+}
+
+template <int NPER>
+__device__ __forceinline__ double reg_dot(const double (&a)[NPER], const double (&b)[NPER]) {
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < NPER; ++k) acc = fma(a[k], b[k], acc);
+  return warp_sum(acc);
+}
+
+template <int NPER>
+__device__ __forceinline__ double smem_dot(const double* __restrict__ row, const double (&x)[NPER], int d, int lane) {
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < NPER; ++k) { const int e = lane + 32 * k; if (e < d) acc = fma(row[e], x[k], acc); }
+  return warp_sum(acc);
+}
+
+template <int NPER>
+__device__ __forceinline__ void load_row(double (&r)[NPER], const double* __restrict__ src, int d, int lane) {
+#pragma unroll
+  for (int k = 0; k < NPER; ++k) { const int e = lane + 32 * k; r[k] = e < d ? src[e] : 0.0; }
+}
+
+template <int NPER>
+__device__ __forceinline__ void store_row(double* __restrict__ dst, const double (&r)[NPER], int d, int lane) {
+#pragma unroll
+  for (int k = 0; k < NPER; ++k) { const int e = lane + 32 * k; if (e < d) dst[e] = r[k]; }
+}
+
+constexpr int REC_CHUNKS = PCY_FMAXL * (int)sizeof(ChainLvl) / 16;   // uint4 per record
+
+template <int NPER>
+__global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __restrict__ X,
+                                                    const double* __restrict__ XS, const long long* __restrict__ W,
+                                                    const int* __restrict__ BAD, long long n, long long first_rem,
+                                                    int countw, int nnew_cap, const ChainHdr* __restrict__ H,
+                                                    const ChainLvl* __restrict__ R) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  ResolveSmem& S = *reinterpret_cast<ResolveSmem*>(smraw);
+  const int lane = threadIdx.x;
+  const int d = E.d, ld = E.ld;
+  double* xsm = reinterpret_cast<double*>(smraw + ((sizeof(ResolveSmem) + 15) & ~size_t(15)));
+  double* tref = xsm + ld;
+  double* ts = tref + (long long)nnew_cap * ld;
+  unsigned* mbits = reinterpret_cast<unsigned*>(ts + (long long)nnew_cap * ld);
+  const int mwords = (int)(E.NC / 32 + 1);
+  unsigned* gbits = mbits + mwords;
+  const int gwords = (int)(E.GC / 32 + 1);
+  EngCtl* C = E.ctl;
+  const long long m = E.m;
+  const double T = C->T;
+  long long F = C->F, Falloc = C->F_alloc, freen = C->free_n, Galloc = C->G_alloc;
+  long long Aalloc = C->A_alloc, nidx = C->next_index, totw = C->total_w, maxdepth = C->max_depth;
+  const long long G0 = Galloc;
+  int status = ST_DONE, err = 0; long long stop = n, remaining = 0;
+
+  for (int s2 = lane; s2 < PCY_MOD_SLOTS; s2 += 32) S.mkey[s2] = -1;
+  for (int s2 = lane; s2 < PCY_GMAP_SLOTS; s2 += 32) S.gkey[s2] = -1;
+  for (int s2 = lane; s2 < mwords; s2 += 32) mbits[s2] = 0u;
+  for (int s2 = lane; s2 < gwords; s2 += 32) gbits[s2] = 0u;
+  if (lane == 0) S.modcount = 0;
+  int nnew = 0;
+  int free_top = freen > 0 ? E.free_ids[freen - 1] : -1;
+
+  // ---- prologue: item 0
+  double xr[NPER], pr[NPER];
+  int bad_c = (n > 0 && BAD) ? BAD[0] : 0;
+  long long w_c = (n > 0 && W) ? W[0] : 1LL;
+  double xs_c = n > 0 ? XS[0] : 0.0;
+  ChainHdr hc = n > 0 ? H[0] : ChainHdr{0, 0, -1, 0};
+  ChainHdr hn = n > 1 ? H[1] : ChainHdr{0, 0, -1, 0};
+  if (n > 0) {
+    load_row<NPER>(xr, X, d, lane);
+    if (hc.predj >= 0) load_row<NPER>(pr, E.s + (long long)hc.predj * ld, d, lane);
+    const uint4* src = reinterpret_cast<const uint4*>(R);
+    uint4* dst = reinterpret_cast<uint4*>(&S.rb[0][0]);
+    for (int c = lane; c < REC_CHUNKS; c += 32) dst[c] = src[c];
+  }
+  __syncwarp();
+  int cur = 0;
+  int prnode = hc.predj;   // node whose current s row is held in pr[]
+
+  for (long long i = 0; i < n; ++i) {
+    if (bad_c) { status = ST_INVALID; err = bad_c; stop = i; break; }
+    if (nnew >= nnew_cap || S.modcount >= PCY_MOD_SLOTS / 2) { status = ST_FULL; stop = i; break; }
+    // ---- prefetch item i+1 (scalars, x row, chain record, predicted row) and header of i+2
+    double xn[NPER], pn[NPER];
+    uint4 rpf[(REC_CHUNKS + 31) / 32];
+    const bool has_next = i + 1 < n;
+    ChainHdr h2 = ChainHdr{0, 0, -1, 0};
+    int bad_n = 0; long long w_n = 1; double xs_n = 0.0;
+    if (has_next) {
+      bad_n = BAD ? BAD[i + 1] : 0;
+      w_n = W ? W[i + 1] : 1LL;
+      xs_n = XS[i + 1];
+      load_row<NPER>(xn, X + (i + 1) * ld, d, lane);
+      const uint4* src = reinterpret_cast<const uint4*>(R + (i + 1) * PCY_FMAXL);
+#pragma unroll
+      for (int q = 0; q < (REC_CHUNKS + 31) / 32; ++q) { const int c = lane + 32 * q; if (c < REC_CHUNKS) rpf[q] = src[c]; }
+      if (hn.predj >= 0) load_row<NPER>(pn, E.s + (long long)hn.predj * ld, d, lane);
+      if (i + 2 < n) h2 = H[i + 2];
+    }
+    // ---- item i
+    const bool resume = (i == 0 && first_rem >= 0);
+    const long long wi = w_c;
+    long long rem = resume ? first_rem : wi;
+    if (countw && !resume) totw += wi;
+    const double xs = xs_c;
+    const int len = hc.len;
+    int g = 0, L = 0;
+    double radius = T;
+    bool direct = false, xs_stored = false;
+    int lastmod = -1, nmod = 0;
+    int modl[4] = {-1, -1, -1, -1};   // snapshot nodes rewritten by this item
+    for (;;) {
+      int bj = -1, li = -1;
+      double bp = INFINITY;
+      if (!direct) {
+        if (L < len) { li = L; bj = S.rb[cur][L].j; bp = S.rb[cur][L].part; }
+        else direct = true;   // truncated chain
+      }
+      if (direct && g < G0) {
+        // members present at launch start, scanned directly (truncated chains only)
+        if (!xs_stored) {
+#pragma unroll
+          for (int k = 0; k < NPER; ++k) { const int e = lane + 32 * k; if (e < ld) xsm[e] = xr[k]; }
+          __syncwarp();
+          xs_stored = true;
+        }
+        const int cnt = E.g_count[g];
+        if (cnt > 0) {
+          double p; int ps;
+          const int* mem = E.arena + E.g_base[g];
+          scan_members(E, mem, 0, cnt, xsm, lane, p, ps);
+          if (ps < cnt) { bj = mem[ps]; bp = p; }
+        }
+      }
+      // members opened in this launch, in position order
+      int bt = -1;
+      if ((gbits[g >> 5] >> (g & 31)) & 1u) {
+        for (int tt = S.ghead[gmap_find(S, g)]; tt >= 0; tt = S.tnext[tt]) {
+          const double part = radd(S.trn[tt], rmul(smem_dot<NPER>(tref + (long long)tt * ld, xr, d, lane), -2.0));
+          if (part < bp || bj < 0) { bp = part; bt = tt; bj = S.tid[tt]; }
+        }
+      }
+      // admission radius (coreset.py:329)
+      if (bj < 0 || radd(bp, xs) > radius) {
+        const bool full = F >= m;
+        const long long wopen = full ? 1LL : rem;
+        long long slot;
+        if (freen > 0) { slot = free_top; --freen; free_top = freen > 0 ? E.free_ids[freen - 1] : -1; }
+        else slot = Falloc++;
+        const int t = nnew++;
+        const double fw = (double)wopen;
+        double* rr = tref + (long long)t * ld;
+        double* sr = ts + (long long)t * ld;
+#pragma unroll
+        for (int k = 0; k < NPER; ++k) {
+          const int e = lane + 32 * k;
+          if (e < ld) { rr[e] = xr[k]; sr[e] = rmul(fw, xr[k]); }
+        }
+        const bool had = ((gbits[g >> 5] >> (g & 31)) & 1u) != 0;
+        int gs = -1;
+        if (had) gs = gmap_find(S, g);
+        else {
+          gs = (int)(((unsigned)g * 2654435761u) >> 24) & (PCY_GMAP_SLOTS - 1);
+          while (S.gkey[gs] >= 0) gs = (gs + 1) & (PCY_GMAP_SLOTS - 1);
+        }
+        if (lane == 0) {
+          S.tid[t] = (int)slot; S.tgrp[t] = g; S.tchild[t] = -1; S.tnext[t] = -1; S.tw[t] = wopen;
+          S.tq[t] = rmul(fw, xs); S.tsn[t] = rmul((double)(wopen * wopen), xs); S.trn[t] = xs;
+          if (had) { S.tnext[S.gtail[gs]] = t; S.gtail[gs] = t; }
+          else { S.gkey[gs] = g; S.ghead[gs] = t; S.gtail[gs] = t; gbits[g >> 5] |= 1u << (g & 31); }
+          E.idx[slot] = nidx; E.alive[slot] = 1; E.child[slot] = -1;
+        }
+        ++nidx; ++F;
+        if (L + 1 > maxdepth) maxdepth = L + 1;
+        rem -= wopen;
+        __syncwarp();
+        if (full) { status = ST_REBUILD; stop = i; remaining = rem; }
+        break;
+      }
+      // capacity on the winner (coreset.py:336-356)
+      long long nn, take, nw2 = 0;
+      double qv, snv, nq = 0.0, nsn = 0.0;
+      int ms = -1;
+      const bool touched = bt < 0 && ((mbits[bj >> 5] >> (bj & 31)) & 1u);
+      if (bt < 0 && li >= 0 && !touched && rem == wi && !resume) {
+        // untouched snapshot node on the first descent: K1's decision is exact
+        const ChainLvl& rc = S.rb[cur][li];
+        nn = rc.w; qv = rc.q; snv = rc.sn; take = rc.take;
+        if (take > 0) { nw2 = nn + take; nq = rc.nq; nsn = rc.nsn; }
+      } else {
+        double dt;
+        if (bt >= 0) {
+          nn = S.tw[bt]; qv = S.tq[bt]; snv = S.tsn[bt];
+          dt = smem_dot<NPER>(ts + (long long)bt * ld, xr, d, lane);
+        } else {
+          if (touched) { ms = map_find(S, bj); nn = S.mw[ms]; qv = S.mq[ms]; snv = S.msn[ms]; }
+          else if (li >= 0) { const ChainLvl& rc = S.rb[cur][li]; nn = rc.w; qv = rc.q; snv = rc.sn; }
+          else { nn = E.w[bj]; qv = E.q[bj]; snv = E.sn[bj]; }
+          if (!touched && li >= 0) dt = S.rb[cur][li].dot;
+          else {
+            if (bj != prnode) { load_row<NPER>(pr, E.s + (long long)bj * ld, d, lane); prnode = bj; }
+            dt = reg_dot<NPER>(pr, xr);
+          }
+        }
+        take = capacity(nn, qv, snv, dt, xs, T, rem);
+        if (take > 0) {
+          const double ft = (double)take;
+          nw2 = nn + take;
+          nq = radd(qv, rmul(ft, xs));
+          nsn = radd(snv, radd(rmul(rmul(2.0, ft), dt), rmul((double)(take * take), xs)));
+        }
+      }
+      if (take > 0) {
+        const double ft = (double)take;
+        if (bt >= 0) {
+          double* srow = ts + (long long)bt * ld;
+#pragma unroll
+          for (int k = 0; k < NPER; ++k) {
+            const int e = lane + 32 * k;
+            if (e < d) srow[e] = take == 1 ? radd(srow[e], xr[k]) : radd(srow[e], rmul(ft, xr[k]));
+          }
+          if (lane == 0) { S.tw[bt] = nw2; S.tq[bt] = nq; S.tsn[bt] = nsn; }
+          __syncwarp();
+        } else {
+          if (bj != prnode) { load_row<NPER>(pr, E.s + (long long)bj * ld, d, lane); prnode = bj; }
+#pragma unroll
+          for (int k = 0; k < NPER; ++k) pr[k] = take == 1 ? radd(pr[k], xr[k]) : radd(pr[k], rmul(ft, xr[k]));
+          store_row<NPER>(E.s + (long long)bj * ld, pr, d, lane);
+          int child_now;
+          if (touched) { if (ms < 0) ms = map_find(S, bj); child_now = S.mchild[ms]; }
+          else child_now = li >= 0 ? S.rb[cur][li].child : E.child[bj];
+          ms = map_put(S, mbits, bj, nw2, nq, nsn, child_now, lane);
+          if (lane == 0) { E.w[bj] = nw2; E.q[bj] = nq; E.sn[bj] = nsn; }
+          if (nmod < 4) modl[nmod] = bj;
+          ++nmod;
+          lastmod = bj;
+        }
+        rem -= take;
+        if (rem == 0) { if (L + 1 > maxdepth) maxdepth = L + 1; break; }
+      }
+      // descend (coreset.py:369-372)
+      int c;
+      if (bt >= 0) {
+        c = S.tchild[bt];
+        if (c < 0) {
+          c = (int)Galloc++;
+          if (lane == 0) { S.tchild[bt] = c; E.g_count[c] = 0; E.g_cap[c] = 0; E.g_base[c] = 0; }
+          __syncwarp();
+        }
+        direct = true;
+      } else {
+        const bool tnow = ((mbits[bj >> 5] >> (bj & 31)) & 1u) != 0;
+        if (tnow && ms < 0) ms = map_find(S, bj);
+        c = tnow ? S.mchild[ms] : (li >= 0 ? S.rb[cur][li].child : E.child[bj]);
+        if (c < 0) {
+          c = (int)Galloc++;
+          if (lane == 0) { E.g_count[c] = 0; E.g_cap[c] = 0; E.g_base[c] = 0; E.child[bj] = c; }
+          if (tnow) { if (lane == 0) S.mchild[ms] = c; __syncwarp(); }
+          else ms = map_put(S, mbits, bj, nn, qv, snv, c, lane);   // untouched: current stats
+        }
+      }
+      g = c;
+      radius = rmul(radius, 0.25);
+      ++L;
+    }
+    __syncwarp();
+    if (status != ST_DONE) break;
+    // ---- rotate prefetched data into place
+    if (has_next) {
+      uint4* dst = reinterpret_cast<uint4*>(&S.rb[cur ^ 1][0]);
+#pragma unroll
+      for (int q = 0; q < (REC_CHUNKS + 31) / 32; ++q) { const int c = lane + 32 * q; if (c < REC_CHUNKS) dst[c] = rpf[q]; }
+#pragma unroll
+      for (int k = 0; k < NPER; ++k) xr[k] = xn[k];
+      int nextnode = hn.predj;
+      bool hit = nmod > 4 || nextnode == lastmod;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) hit |= (modl[q] >= 0 && modl[q] == nextnode);
+      if (nextnode >= 0 && hit) {
+        // a node sits in one group, so an item rewrites it at most once: pr is
+        // its current row exactly when it was the item's last rewrite
+        if (nextnode == lastmod && prnode == lastmod) {
+#pragma unroll
+          for (int k = 0; k < NPER; ++k) pn[k] = pr[k];   // the row this item just rewrote
+        } else {
+          nextnode = -1;                                   // stale prefetch: demand-load later
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < NPER; ++k) pr[k] = pn[k];
+      prnode = nextnode;
+      hc = hn; hn = h2;
+      bad_c = bad_n; w_c = w_n; xs_c = xs_n;
+      cur ^= 1;
+    }
+    __syncwarp();
+  }
+
+  // ---- cleanup: new nodes and their memberships to HBM (position order per group)
+  __syncwarp();
+  for (int t = 0; t < nnew; ++t) {
+    const int node = S.tid[t];
+    const double* rr = tref + (long long)t * ld;
+    const double* sr = ts + (long long)t * ld;
+    for (int e = lane; e < ld; e += 32) { E.r[(long long)node * ld + e] = rr[e]; E.s[(long long)node * ld + e] = sr[e]; }
+  }
+  for (int t = lane; t < nnew; t += 32) {
+    const int node = S.tid[t];
+    E.w[node] = S.tw[t]; E.q[node] = S.tq[t]; E.sn[node] = S.tsn[t]; E.rn[node] = S.trn[t];
+    E.child[node] = S.tchild[t];
+    const int g = S.tgrp[t];
+    int k = 0, f = t;
+    for (int u = t - 1; u >= 0; --u) if (S.tgrp[u] == g) { ++k; f = u; }
+    S.tk[t] = k; S.tfirst[t] = f;
+    S.tcnt[t] = E.g_count[g]; S.tcap[t] = E.g_cap[g]; S.tbase[t] = E.g_base[g];
+  }
+  __syncwarp();
+  bool arena_ok = true;
+  for (int t = 0; t < nnew; ++t) {
+    if (S.tfirst[t] != t) continue;
+    const int g = S.tgrp[t];
+    int total = 0;
+    for (int u = t; u < nnew; ++u) total += (S.tgrp[u] == g);
+    const int cnt = S.tcnt[t], cap = S.tcap[t], base = S.tbase[t];
+    int nb = base, ncap = cap;
+    if (cnt + total > cap) {
+      ncap = cap ? 2 * cap : PCY_GROUP_MIN_CAP;
+      while (ncap < cnt + total) ncap *= 2;
+      if (Aalloc + ncap > E.AC) { arena_ok = false; break; }
+      nb = (int)Aalloc; Aalloc += ncap;
+      for (int p = lane; p < cnt; p += 32) E.arena[nb + p] = E.arena[base + p];
+    }
+    if (lane == 0) {
+      S.tbase[t] = nb; S.tcap[t] = ncap;
+      E.g_base[g] = nb; E.g_cap[g] = ncap; E.g_count[g] = cnt + total;
+    }
+    __syncwarp();
+  }
+  if (arena_ok) {
+    for (int t = lane; t < nnew; t += 32) {
+      const int f = S.tfirst[t];
+      E.arena[S.tbase[f] + S.tcnt[f] + S.tk[t]] = S.tid[t];
+    }
+  } else {
+    status = ST_ARENA;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    C->F = F; C->F_alloc = Falloc; C->free_n = freen; C->G_alloc = Galloc;
+    C->A_alloc = Aalloc; C->next_index = nidx; C->total_w = totw; C->max_depth = maxdepth;
+    C->status = status; C->err = err; C->stop = stop; C->remaining = remaining;
+  }
+}

@@ -25,6 +25,7 @@ DEFAULT_TOL = 1e-4
 c_i32, c_i64, c_f64, c_vp = ctypes.c_int, ctypes.c_longlong, ctypes.c_double, ctypes.c_void_p
 nat.register("pcy_kmeanspp", c_i32, [c_vp, c_vp, c_i64, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp])
 nat.register("pcy_lloyd", c_i32, [c_vp, c_vp, c_i64, c_i32, c_i32, c_i32, c_vp, c_i32, c_f64, c_vp, c_vp, c_vp])
+nat.register("pcy_cast_i64_f64", c_i32, [c_vp, c_i64, c_vp, c_vp])
 nat.register("pcy_weighted_cost", c_i32, [c_vp, c_vp, c_i64, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp])
 
 
@@ -57,7 +58,13 @@ def _dev_points(points, weights, device=None):
             w = torch.ones(P.shape[0], dtype=torch.float64, device=P.device)
         else:
             w = (weights if isinstance(weights, torch.Tensor) else torch.as_tensor(np.asarray(weights)))
-            w = w.to(P.device, dtype=torch.float64).contiguous()
+            w = w.to(P.device).contiguous()
+            if w.dtype == torch.int64:
+                wf = torch.empty(w.shape, dtype=torch.float64, device=P.device)
+                nat.check(nat.lib().pcy_cast_i64_f64(nat.ptr(w), w.numel(), nat.ptr(wf), nat.stream_ptr()), "cast")
+                w = wf
+            elif w.dtype != torch.float64:
+                w = w.to(torch.float64)
             if w.shape != (P.shape[0],):
                 raise ValueError("weights must be one per point")
         return P, w
