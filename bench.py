@@ -199,11 +199,22 @@ def main():
     Xd = torch.from_numpy(X).to(dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
+    phase_ms = {"coreset": 0.0, "kmeans": 0.0}
+
     def step_device():
+        st0 = torch.cuda.current_stream()
+        a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        a.record(st0)
         eng = run_piecy_device(Xd, d, pcfg)
         P, w = eng.extract_device()
+        b.record(st0)
         C, costs = kmeans_repetitions_device(P, w, cfg.k, cfg.reps, cfg.seed, cfg.max_iters, 1e-4)
+        c.record(st0)
+        c.synchronize()
+        step_device.phases.append((a.elapsed_time(b), b.elapsed_time(c)))
+        step_device.engine = eng
         return P.shape[0], costs
+    step_device.phases = []
 
     if args.ncu:
         step_device()
@@ -307,7 +318,9 @@ def main():
             "kernel_ms_per_step": kernel_ms,
             "dominant_kernel": dom,
             "coreset_size": int(F),
+            "engine_counters": step_device.engine.counters(),
             "step_ms": ms_steps,
+            "phase_ms": [{"coreset": round(p[0], 2), "kmeans": round(p[1], 2)} for p in step_device.phases[-args.steps:]],
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -270,6 +270,15 @@ class BicoEngine:
             raise ValueError(_BAD_MESSAGES.get(bad.value, "invalid point"))
         return consumed.value
 
+    def counters(self) -> dict:
+        """K3 instrumentation: levels walked, direct scans, demand row loads,
+        full capacity evaluations, items resolved, deepest level."""
+        self._flush()
+        out = np.zeros(6, dtype=np.int64)
+        nat.check(nat.lib().pcy_engine_counters(self._h, out.ctypes.data), "pcy_engine_counters")
+        keys = ("levels", "direct_scans", "demand_loads", "slow_capacity", "items", "max_depth")
+        return {k: int(v) for k, v in zip(keys, out)}
+
     # -- extraction ---------------------------------------------------------
     def features_device(self):
         """(levels, weights, linear sums, square sums, references) as CUDA tensors, DFS order."""

@@ -24,6 +24,12 @@ enum PcyStatus {
 
 void pcy_set_error(const char* fmt, ...);
 void pcy_count_launch();
+// Wait for all work queued on `st` by spinning on an event (no blocking-sync
+// wake-up latency on the host thread).
+cudaError_t pcy_spin_sync(cudaStream_t st);
+// Device -> host copy of a small result through a thread-local pinned
+// staging buffer, completed with pcy_spin_sync.
+cudaError_t pcy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t st);
 
 // Per-kernel event timing (enabled by pcy_prof_enable).
 enum { PCY_PROF_RESOLVE = 0, PCY_PROF_CHAIN = 1, PCY_PROF_REATTACH = 2, PCY_PROF_SEED = 3,

@@ -17,6 +17,7 @@
 #include <cstring>
 #include <atomic>
 #include <mutex>
+#include <cstddef>
 #include <cstdlib>
 #include <vector>
 #include "engine.cuh"
@@ -38,6 +39,31 @@ bool pcy_prof_enabled() { return g_prof_on.load(std::memory_order_relaxed) != 0;
 void pcy_prof_add(int slot, double ms, long long units) {
   std::lock_guard<std::mutex> lk(g_prof_mu);
   g_prof[slot].ms += ms; g_prof[slot].count += 1; g_prof[slot].units += units;
+}
+cudaError_t pcy_spin_sync(cudaStream_t st) {
+  static thread_local cudaEvent_t ev = nullptr;
+  cudaError_t e;
+  if (!ev && (e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return e;
+  if ((e = cudaEventRecord(ev, st)) != cudaSuccess) return e;
+  for (;;) {
+    e = cudaEventQuery(ev);
+    if (e != cudaErrorNotReady) return e;
+  }
+}
+cudaError_t pcy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  static thread_local void* buf = nullptr;
+  static thread_local size_t cap = 0;
+  cudaError_t e;
+  if (bytes > cap) {
+    if (buf) cudaFreeHost(buf);
+    size_t c = 4096; while (c < bytes) c *= 2;
+    if ((e = cudaMallocHost(&buf, c)) != cudaSuccess) { buf = nullptr; cap = 0; return e; }
+    cap = c;
+  }
+  if ((e = cudaMemcpyAsync(buf, src, bytes, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
+  if ((e = pcy_spin_sync(st)) != cudaSuccess) return e;
+  memcpy(dst, buf, bytes);
+  return cudaSuccess;
 }
 extern "C" long long pcy_launch_count(void) { return g_launches.load(); }
 extern "C" int pcy_prof_enable(int on) { g_prof_on.store(on); return 0; }
@@ -271,6 +297,18 @@ __global__ void k_mp_finish(EngDev E, long long ns) {
     mn = rmul(1e-12, nmax > 1.0 ? nmax : 1.0);
   } else mn = __longlong_as_double((long long)E.minbits[0]);
   E.ctl->T = rdiv(rmul(mn, (double)E.m), 16.0);
+}
+
+// ------------------------------------------------------- host publication
+__global__ void k_publish(const EngCtl* __restrict__ src, EngCtl* dst, long long seq) {
+  const int lane = threadIdx.x;
+  const int words = (int)(offsetof(EngCtl, seq) / sizeof(long long));
+  const long long* s = reinterpret_cast<const long long*>(src);
+  volatile long long* t = reinterpret_cast<volatile long long*>(dst);
+  for (int k = lane; k < words; k += 32) t[k] = s[k];
+  __threadfence_system();
+  __syncwarp();
+  if (lane == 0) t[words] = seq;
 }
 
 // ------------------------------------------------------------- tree reset
@@ -689,7 +727,9 @@ struct Engine {
   long long m = 0, sample_cap = 0, NC = 0, GC = 0, AC = 0, Bmax = 0;
   bool built = false;
   EngDev E{};
-  EngCtl* ctl_h = nullptr;   // pinned mirror
+  EngCtl* ctl_h = nullptr;   // mapped pinned mirror (host view)
+  EngCtl* ctl_map_d = nullptr;   // device view of the mirror
+  long long seq = 0;
   long long* aggw = nullptr;
   double* mp_nrm = nullptr;
   cudaEvent_t ev[6] = {};
@@ -717,9 +757,23 @@ struct Engine {
     if (ctl_h) cudaFreeHost(ctl_h);
   }
 
+  // Publish the device counters into the mapped host mirror and spin on its
+  // sequence number: no stream synchronisation, no wake-up latency.
   int sync_ctl(cudaStream_t st) {
-    PCY_CUDA(cudaMemcpyAsync(ctl_h, E.ctl, sizeof(EngCtl), cudaMemcpyDeviceToHost, st));
-    PCY_CUDA(cudaStreamSynchronize(st));
+    const long long want = ++seq;
+    k_publish<<<1, 32, 0, st>>>(E.ctl, ctl_map_d, want); pcy_count_launch();
+    PCY_LAUNCH_CHECK();
+    volatile long long* sp = &ctl_h->seq;
+    for (long long spins = 0; *sp != want; ++spins) {
+      if ((spins & 1023) == 1023) {
+        const cudaError_t e = cudaStreamQuery(st);
+        if (e != cudaSuccess && e != cudaErrorNotReady) {
+          pcy_set_error("engine kernel failed: %s", cudaGetErrorString(e));
+          return PCY_ECUDA;
+        }
+      }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
     return PCY_OK;
   }
 
@@ -759,7 +813,7 @@ struct Engine {
       nper = ld <= 32 ? 1 : ld <= 64 ? 2 : ld <= 128 ? 4 : 8;
       const size_t base = resolve_smem_bytes(ld, 0, NC, GC);
       const size_t maxsm = 227 * 1024;
-      long long cap = maxsm > base ? (long long)((maxsm - base) / (2 * sizeof(double) * ld)) : 0;
+      long long cap = maxsm > base ? (long long)((maxsm - base) / (sizeof(double) * (2 * ld + 1))) : 0;
       if (cap > PCY_NNEW_MAX) cap = PCY_NNEW_MAX;
       nnew_cap = (int)cap;
       res_smem = resolve_smem_bytes(ld, nnew_cap, NC, GC);
@@ -778,8 +832,9 @@ struct Engine {
       }
       if (getenv("PCY_GENERIC_RESOLVE")) nper = 0;
     }
-    PCY_CUDA(cudaMallocHost(&ctl_h, sizeof(EngCtl)));
+    PCY_CUDA(cudaHostAlloc(&ctl_h, sizeof(EngCtl), cudaHostAllocMapped));
     memset(ctl_h, 0, sizeof(EngCtl));
+    PCY_CUDA(cudaHostGetDevicePointer((void**)&ctl_map_d, ctl_h, 0));
     PCY_CUDA(cudaMemcpy(E.ctl, ctl_h, sizeof(EngCtl), cudaMemcpyHostToDevice));
     PCY_CUDA(cudaMemset(E.htab, 0xff, sizeof(int) * E.hcap));
     PCY_CUDA(cudaMemset(E.alive, 0, sizeof(int) * NC));
@@ -796,7 +851,7 @@ struct Engine {
     PCY_CUDA(cudaMemcpyAsync(nx, E.pend_x, sizeof(double) * E.pend_cap * ld, cudaMemcpyDeviceToDevice, st));
     PCY_CUDA(cudaMemcpyAsync(nw, E.pend_w, sizeof(long long) * E.pend_cap, cudaMemcpyDeviceToDevice, st));
     PCY_CUDA(cudaMemcpyAsync(nq, E.pend_xsq, sizeof(double) * E.pend_cap, cudaMemcpyDeviceToDevice, st));
-    PCY_CUDA(cudaStreamSynchronize(st));
+    PCY_CUDA(pcy_spin_sync(st));
     release(E.pend_x); release(E.pend_w); release(E.pend_xsq);
     E.pend_x = nx; E.pend_w = nw; E.pend_xsq = nq; E.pend_cap = nc;
     return PCY_OK;
@@ -1044,6 +1099,15 @@ int pcy_engine_stats(void* h, long long* num_features, double* threshold, long l
   *threshold = e->ctl_h->T;
   *total_weight = e->ctl_h->total_w;
   *built = e->built ? 1 : 0;
+  return PCY_OK;
+}
+
+// Engine instrumentation counters: [levels, direct scans, demand loads,
+// full capacity evaluations, items, max depth].
+int pcy_engine_counters(void* h, long long* out6) {
+  Engine* e = (Engine*)h;
+  out6[0] = e->ctl_h->cnt_levels; out6[1] = e->ctl_h->cnt_direct; out6[2] = e->ctl_h->cnt_demand;
+  out6[3] = e->ctl_h->cnt_slow; out6[4] = e->ctl_h->cnt_items; out6[5] = e->ctl_h->max_depth;
   return PCY_OK;
 }
 

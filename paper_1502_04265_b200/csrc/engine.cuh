@@ -31,6 +31,10 @@ struct EngCtl {
   int status, err;
   long long stop, remaining;
   long long max_depth;
+  // instrumentation (k_resolve2): levels walked, direct scans, demand row
+  // loads, full capacity evaluations, items resolved
+  long long cnt_levels, cnt_direct, cnt_demand, cnt_slow, cnt_items;
+  long long seq;          // publication sequence number (mapped host mirror)
 };
 
 struct EngDev {

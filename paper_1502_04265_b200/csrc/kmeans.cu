@@ -312,8 +312,7 @@ int pcy_kmeanspp(const double* P, const double* w, long long n, int d, int k, in
   PCY_LAUNCH_CHECK();
   if (picks_out) {
     std::vector<int> h((size_t)k * reps);
-    PCY_CUDA(cudaMemcpyAsync(h.data(), picks, sizeof(int) * k * reps, cudaMemcpyDeviceToHost, st));
-    PCY_CUDA(cudaStreamSynchronize(st));
+    PCY_CUDA(pcy_d2h(h.data(), picks, sizeof(int) * k * reps, st));
     for (size_t i = 0; i < h.size(); ++i) picks_out[i] = h[i];
   }
   PCY_CUDA(cudaFreeAsync(best, st));
@@ -352,8 +351,7 @@ int pcy_lloyd(const double* P, const double* w, long long n, int d, int k, int r
     k_assign<<<dim3((unsigned)((n + 7) / 8), reps), 256, 0, st>>>(P, pn, n, d, k, centers, cn, active, assign, best); pcy_count_launch();
     k_finish<<<reps, KM_THREADS, 0, st>>>(P, w, n, d, k, centers, active, assign, best, counts, cost, 1); pcy_count_launch();
     PCY_LAUNCH_CHECK();
-    PCY_CUDA(cudaMemcpyAsync(hc.data(), cost, sizeof(double) * reps, cudaMemcpyDeviceToHost, st));
-    PCY_CUDA(cudaStreamSynchronize(st));
+    PCY_CUDA(pcy_d2h(hc.data(), cost, sizeof(double) * reps, st));
     bool any_update = false;
     for (int r = 0; r < reps; ++r) {
       if (!act[r]) continue;
@@ -368,7 +366,7 @@ int pcy_lloyd(const double* P, const double* w, long long n, int d, int k, int r
     k_update<<<dim3(k, reps), 256, usm, st>>>(P, w, n, d, k, active, assign, centers); pcy_count_launch();
     PCY_LAUNCH_CHECK();
   }
-  PCY_CUDA(cudaStreamSynchronize(st));
+  PCY_CUDA(pcy_spin_sync(st));
   cudaFreeAsync(pn, st); cudaFreeAsync(cn, st); cudaFreeAsync(best, st); cudaFreeAsync(assign, st);
   cudaFreeAsync(counts, st); cudaFreeAsync(cost, st); cudaFreeAsync(active, st);
   return PCY_OK;
@@ -390,8 +388,7 @@ int pcy_weighted_cost(const double* P, const double* w, long long n, int d, int 
   k_assign<<<dim3((unsigned)((n + 7) / 8), reps), 256, 0, st>>>(P, pn, n, d, k, centers, cn, nullptr, assign, best); pcy_count_launch();
   k_finish<<<reps, KM_THREADS, 0, st>>>(P, w, n, d, k, (double*)centers, nullptr, assign, best, nullptr, cost, 0); pcy_count_launch();
   PCY_LAUNCH_CHECK();
-  PCY_CUDA(cudaMemcpyAsync(costs, cost, sizeof(double) * reps, cudaMemcpyDeviceToHost, st));
-  PCY_CUDA(cudaStreamSynchronize(st));
+  PCY_CUDA(pcy_d2h(costs, cost, sizeof(double) * reps, st));
   cudaFreeAsync(pn, st); cudaFreeAsync(cn, st); cudaFreeAsync(best, st); cudaFreeAsync(assign, st);
   cudaFreeAsync(cost, st);
   return PCY_OK;

@@ -302,8 +302,7 @@ static int cholqr(cudaStream_t st, double* Y, long long rows, int r, double* Gs,
     if ((rc = gemm(st, r, r, (int)rows, 1.0, Y, r, 1, Y, r, 0, 0.0, Gs, r))) return rc;
     k_chol_inv<<<1, 1024, 0, st>>>(Gs, r, shift, Ls, Li, status); pcy_count_launch();
     PCY_LAUNCH_CHECK();
-    PCY_CUDA(cudaMemcpyAsync(&hs, status, sizeof(int), cudaMemcpyDeviceToHost, st));
-    PCY_CUDA(cudaStreamSynchronize(st));
+    PCY_CUDA(pcy_d2h(&hs, status, sizeof(int), st));
     *ok = hs == 0;
     if (!*ok) return PCY_OK;
     // Y <- Y * Linv^T
@@ -320,8 +319,7 @@ static int cholqr(cudaStream_t st, double* Y, long long rows, int r, double* Gs,
   // shifted CholeskyQR3: shift = 11 (m n + n (n+1)) u ||Y||_2^2, ||Y||_2^2 <= trace(G)
   std::vector<double> g((size_t)r * r);
   if ((rc = gemm(st, r, r, (int)rows, 1.0, Y, r, 1, Y, r, 0, 0.0, Gs, r))) return rc;
-  PCY_CUDA(cudaMemcpyAsync(g.data(), Gs, sizeof(double) * r * r, cudaMemcpyDeviceToHost, st));
-  PCY_CUDA(cudaStreamSynchronize(st));
+  PCY_CUDA(pcy_d2h(g.data(), Gs, sizeof(double) * r * r, st));
   double tr = 0.0;
   for (int i = 0; i < r; ++i) tr += g[(size_t)i * r + i];
   const double shift = 11.0 * ((double)rows * r + (double)r * (r + 1)) * 1.1102230246251565e-16 * tr;
@@ -344,8 +342,7 @@ int pcy_all_finite(const void* p, long long n, int dtype, int* out_host, void* s
   PCY_CUDA(cudaMemcpyAsync(flag, &one, sizeof(int), cudaMemcpyHostToDevice, st));
   if (n > 0) { k_all_finite<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 8), 256, 0, st>>>(p, n, dtype, flag); pcy_count_launch(); }
   PCY_LAUNCH_CHECK();
-  PCY_CUDA(cudaMemcpyAsync(out_host, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
-  PCY_CUDA(cudaStreamSynchronize(st));
+  PCY_CUDA(pcy_d2h(out_host, flag, sizeof(int), st));
   cudaFreeAsync(flag, st);
   return PCY_OK;
 }
@@ -442,8 +439,7 @@ int pcy_rsvd(const double* A, long long rows, int cols, int ell, int r, int powe
     k_fix_signs<<<(ell + 7) / 8, 256, 0, st>>>(V, cols, ell, ell); pcy_count_launch();
     PCY_LAUNCH_CHECK();
     std::vector<double> hs(r);
-    PCY_CUDA(cudaMemcpyAsync(hs.data(), sig + r, sizeof(double) * r, cudaMemcpyDeviceToHost, st));
-    PCY_CUDA(cudaStreamSynchronize(st));
+    PCY_CUDA(pcy_d2h(hs.data(), sig + r, sizeof(double) * r, st));
     for (int j = 0; j < ell; ++j) sigma_host[j] = hs[j];
     if (ell > 0 && sigma_host[0] > 0.0)
       for (int j = 0; j < ell; ++j) if (sigma_host[j] < 1e-12 * sigma_host[0]) sigma_host[j] = 0.0;

@@ -76,8 +76,9 @@ __global__ void __launch_bounds__(32, 1) k_reattach2(EngDev E, const int* __rest
   const int lane = threadIdx.x;
   const int d = E.d, ld = E.ld;
   double* xsm = reinterpret_cast<double*>(smraw + ((sizeof(ResolveSmem) + 15) & ~size_t(15)));
+  const int lds = ld | 1;   // odd stride: conflict-free lane-per-row reads
   double* tref = xsm + ld;
-  double* ts_unused = tref + (long long)nnew_cap * ld;
+  double* ts_unused = tref + (long long)nnew_cap * lds;
   unsigned* mbits = reinterpret_cast<unsigned*>(ts_unused + (long long)nnew_cap * ld);
   const int mwords = (int)(E.NC / 32 + 1);
   unsigned* gbits = mbits + mwords;
@@ -139,7 +140,10 @@ __global__ void __launch_bounds__(32, 1) k_reattach2(EngDev E, const int* __rest
     const int len = hc.len;
     int g = 0, L = 0;
     double radius = T;
-    bool direct = false, xs_stored = false;
+    bool direct = false;
+#pragma unroll
+    for (int k = 0; k < NPER; ++k) { const int e = lane + 32 * k; if (e < ld) xsm[e] = xr[k]; }
+    __syncwarp();
     int lastmod = -1;
     for (;;) {
       int bj = -1, li = -1;
@@ -149,12 +153,6 @@ __global__ void __launch_bounds__(32, 1) k_reattach2(EngDev E, const int* __rest
         else direct = true;
       }
       if (direct && g < G0) {
-        if (!xs_stored) {
-#pragma unroll
-          for (int k = 0; k < NPER; ++k) { const int e = lane + 32 * k; if (e < ld) xsm[e] = xr[k]; }
-          __syncwarp();
-          xs_stored = true;
-        }
         const int cnt = E.g_count[g];
         if (cnt > 0) {
           double p; int ps;
@@ -165,15 +163,25 @@ __global__ void __launch_bounds__(32, 1) k_reattach2(EngDev E, const int* __rest
       }
       int bt = -1;
       if ((gbits[g >> 5] >> (g & 31)) & 1u) {
-        for (int tt = S.ghead[gmap_find(S, g)]; tt >= 0; tt = S.tnext[tt]) {
-          const double part = radd(S.trn[tt], rmul(smem_dot<NPER>(tref + (long long)tt * ld, xr, d, lane), -2.0));
-          if (part < bp || bj < 0) { bp = part; bt = tt; bj = S.tid[tt]; }
+        // one new member per lane: sequential dot over the padded smem row
+        double np_ = INFINITY; int nt = 0x7fffffff;
+        for (int c0 = 0; c0 < nnew; c0 += 32) {
+          const int t = c0 + lane;
+          if (t < nnew && S.tgrp[t] == g) {
+            const double* rr = tref + (long long)t * lds;
+            double acc = 0.0;
+            for (int e = 0; e < d; ++e) acc = fma(rr[e], xsm[e], acc);
+            const double part = radd(S.trn[t], rmul(acc, -2.0));
+            if (part < np_) { np_ = part; nt = t; }
+          }
         }
+        warp_argmin(np_, nt);
+        if (nt != 0x7fffffff && (np_ < bp || bj < 0)) { bp = np_; bt = nt; bj = S.tid[nt]; }
       }
       if (bj < 0 || radd(bp, rsq_c) > radius) {
         // group.add(node): u keeps its statistics (coreset.py:403-406)
         const int t = nnew++;
-        double* rr = tref + (long long)t * ld;
+        double* rr = tref + (long long)t * lds;
 #pragma unroll
         for (int k = 0; k < NPER; ++k) { const int e = lane + 32 * k; if (e < ld) rr[e] = xr[k]; }
         const bool had = ((gbits[g >> 5] >> (g & 31)) & 1u) != 0;

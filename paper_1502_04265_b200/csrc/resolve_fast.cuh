@@ -127,11 +127,11 @@ struct ResolveSmem {
   double trn[PCY_NNEW_MAX], tq[PCY_NNEW_MAX], tsn[PCY_NNEW_MAX];
   int modcount;
 };
-// dynamic tail: double xsm[ld]; double tref[nnew][ld]; double ts[nnew][ld];
+// dynamic tail: double xsm[ld]; double tref[nnew][ld|1]; double ts[nnew][ld];
 //               unsigned mbits[NC/32+1]; unsigned gbits[GC/32+1]
 
 __host__ __device__ inline size_t resolve_smem_bytes(int ld, int nnew, long long NC, long long GC) {
-  return ((sizeof(ResolveSmem) + 15) & ~size_t(15)) + sizeof(double) * (size_t)ld * (1 + 2 * (size_t)nnew) +
+  return ((sizeof(ResolveSmem) + 15) & ~size_t(15)) + sizeof(double) * ((size_t)ld + (size_t)nnew * ((size_t)(ld | 1) + ld)) +
          sizeof(unsigned) * (size_t)(NC / 32 + 1 + GC / 32 + 1);
 }
 
@@ -211,8 +211,9 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
   const int lane = threadIdx.x;
   const int d = E.d, ld = E.ld;
   double* xsm = reinterpret_cast<double*>(smraw + ((sizeof(ResolveSmem) + 15) & ~size_t(15)));
+  const int lds = ld | 1;   // odd stride: conflict-free lane-per-row reads
   double* tref = xsm + ld;
-  double* ts = tref + (long long)nnew_cap * ld;
+  double* ts = tref + (long long)nnew_cap * lds;
   unsigned* mbits = reinterpret_cast<unsigned*>(ts + (long long)nnew_cap * ld);
   const int mwords = (int)(E.NC / 32 + 1);
   unsigned* gbits = mbits + mwords;
@@ -222,6 +223,7 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
   const double T = C->T;
   long long F = C->F, Falloc = C->F_alloc, freen = C->free_n, Galloc = C->G_alloc;
   long long Aalloc = C->A_alloc, nidx = C->next_index, totw = C->total_w, maxdepth = C->max_depth;
+  long long c_lv = 0, c_dir = 0, c_dem = 0, c_slow = 0, c_it = 0;
   const long long G0 = Galloc;
   int status = ST_DONE, err = 0; long long stop = n, remaining = 0;
 
@@ -280,42 +282,14 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
     const int len = hc.len;
     int g = 0, L = 0;
     double radius = T;
-    bool direct = false, xs_stored = false;
+    bool direct = false;
+#pragma unroll
+    for (int k = 0; k < NPER; ++k) { const int e = lane + 32 * k; if (e < ld) xsm[e] = xr[k]; }
+    __syncwarp();
     int lastmod = -1, nmod = 0;
     int modl[4] = {-1, -1, -1, -1};   // snapshot nodes rewritten by this item
-    for (;;) {
-      int bj = -1, li = -1;
-      double bp = INFINITY;
-      if (!direct) {
-        if (L < len) { li = L; bj = S.rb[cur][L].j; bp = S.rb[cur][L].part; }
-        else direct = true;   // truncated chain
-      }
-      if (direct && g < G0) {
-        // members present at launch start, scanned directly (truncated chains only)
-        if (!xs_stored) {
-#pragma unroll
-          for (int k = 0; k < NPER; ++k) { const int e = lane + 32 * k; if (e < ld) xsm[e] = xr[k]; }
-          __syncwarp();
-          xs_stored = true;
-        }
-        const int cnt = E.g_count[g];
-        if (cnt > 0) {
-          double p; int ps;
-          const int* mem = E.arena + E.g_base[g];
-          scan_members(E, mem, 0, cnt, xsm, lane, p, ps);
-          if (ps < cnt) { bj = mem[ps]; bp = p; }
-        }
-      }
-      // members opened in this launch, in position order
-      int bt = -1;
-      if ((gbits[g >> 5] >> (g & 31)) & 1u) {
-        for (int tt = S.ghead[gmap_find(S, g)]; tt >= 0; tt = S.tnext[tt]) {
-          const double part = radd(S.trn[tt], rmul(smem_dot<NPER>(tref + (long long)tt * ld, xr, d, lane), -2.0));
-          if (part < bp || bj < 0) { bp = part; bt = tt; bj = S.tid[tt]; }
-        }
-      }
-      // admission radius (coreset.py:329)
-      if (bj < 0 || radd(bp, xs) > radius) {
+    // _open (coreset.py:329-335, :374-377) into group g at level L; returns true when full (rebuild)
+    auto do_open = [&](int g, int L) -> bool {
         const bool full = F >= m;
         const long long wopen = full ? 1LL : rem;
         long long slot;
@@ -323,7 +297,7 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
         else slot = Falloc++;
         const int t = nnew++;
         const double fw = (double)wopen;
-        double* rr = tref + (long long)t * ld;
+        double* rr = tref + (long long)t * lds;
         double* sr = ts + (long long)t * ld;
 #pragma unroll
         for (int k = 0; k < NPER; ++k) {
@@ -348,7 +322,92 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
         if (L + 1 > maxdepth) maxdepth = L + 1;
         rem -= wopen;
         __syncwarp();
-        if (full) { status = ST_REBUILD; stop = i; remaining = rem; }
+        return full;
+    };
+    // ---- verified fast path: nothing on K1's path changed in this launch, so
+    // every decision along it is K1's (same statistics, dots, members).
+    bool done_fast = false;
+    if (!resume && len > 0 && !hc.trunc) {
+      const int pl = hc.pred;
+      bool ok = pl >= 0 && pl < len;
+      for (int L2 = 0; ok && L2 <= pl; ++L2) {
+        const int g2 = S.rb[cur][L2].g, j2 = S.rb[cur][L2].j;
+        if (g2 >= 0 && ((gbits[g2 >> 5] >> (g2 & 31)) & 1u)) ok = false;
+        if (j2 >= 0 && ((mbits[j2 >> 5] >> (j2 & 31)) & 1u)) ok = false;
+      }
+      if (ok) {
+        const ChainLvl& rp = S.rb[cur][pl];
+        if (rp.take > 0 && rp.take == rem) {
+          const int bj = rp.j;
+          const long long take = rp.take;
+          const double ft = (double)take;
+          if (bj != prnode) { load_row<NPER>(pr, E.s + (long long)bj * ld, d, lane); prnode = bj; ++c_dem; }
+#pragma unroll
+          for (int k = 0; k < NPER; ++k) pr[k] = take == 1 ? radd(pr[k], xr[k]) : radd(pr[k], rmul(ft, xr[k]));
+          store_row<NPER>(E.s + (long long)bj * ld, pr, d, lane);
+          const long long nw2 = rp.w + take;
+          map_put(S, mbits, bj, nw2, rp.nq, rp.nsn, rp.child, lane);
+          if (lane == 0) { E.w[bj] = nw2; E.q[bj] = rp.nq; E.sn[bj] = rp.nsn; }
+          modl[0] = bj; nmod = 1; lastmod = bj;
+          rem = 0;
+          if (pl + 1 > maxdepth) maxdepth = pl + 1;
+          c_lv += pl + 1;
+          done_fast = true;
+        } else if (rp.take == 0) {
+          int g = rp.g;
+          if (g < 0) {
+            // the snapshot parent had no child group: create it (coreset.py:369-371)
+            const ChainLvl& pp = S.rb[cur][pl - 1];
+            g = (int)Galloc++;
+            if (lane == 0) { E.g_count[g] = 0; E.g_cap[g] = 0; E.g_base[g] = 0; E.child[pp.j] = g; }
+            map_put(S, mbits, pp.j, pp.w, pp.q, pp.sn, g, lane);
+          }
+          if (do_open(g, pl)) { status = ST_REBUILD; stop = i; remaining = rem; }
+          c_lv += pl + 1;
+          done_fast = true;
+        }
+      }
+    }
+    if (!done_fast) for (;;) {
+      int bj = -1, li = -1;
+      double bp = INFINITY;
+      if (!direct) {
+        if (L < len) { li = L; bj = S.rb[cur][L].j; bp = S.rb[cur][L].part; }
+        else direct = true;   // truncated chain
+      }
+      ++c_lv;
+      if (direct && g < G0) {
+        // members present at launch start, scanned directly (truncated chains only)
+        ++c_dir;
+        const int cnt = E.g_count[g];
+        if (cnt > 0) {
+          double p; int ps;
+          const int* mem = E.arena + E.g_base[g];
+          scan_members(E, mem, 0, cnt, xsm, lane, p, ps);
+          if (ps < cnt) { bj = mem[ps]; bp = p; }
+        }
+      }
+      // members opened in this launch, in position order
+      int bt = -1;
+      if ((gbits[g >> 5] >> (g & 31)) & 1u) {
+        // one new member per lane: sequential dot over the padded smem row
+        double np_ = INFINITY; int nt = 0x7fffffff;
+        for (int c0 = 0; c0 < nnew; c0 += 32) {
+          const int t = c0 + lane;
+          if (t < nnew && S.tgrp[t] == g) {
+            const double* rr = tref + (long long)t * lds;
+            double acc = 0.0;
+            for (int e = 0; e < d; ++e) acc = fma(rr[e], xsm[e], acc);
+            const double part = radd(S.trn[t], rmul(acc, -2.0));
+            if (part < np_) { np_ = part; nt = t; }
+          }
+        }
+        warp_argmin(np_, nt);
+        if (nt != 0x7fffffff && (np_ < bp || bj < 0)) { bp = np_; bt = nt; bj = S.tid[nt]; }
+      }
+      // admission radius (coreset.py:329)
+      if (bj < 0 || radd(bp, xs) > radius) {
+        if (do_open(g, L)) { status = ST_REBUILD; stop = i; remaining = rem; }
         break;
       }
       // capacity on the winner (coreset.py:336-356)
@@ -363,6 +422,7 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
         if (take > 0) { nw2 = nn + take; nq = rc.nq; nsn = rc.nsn; }
       } else {
         double dt;
+        ++c_slow;
         if (bt >= 0) {
           nn = S.tw[bt]; qv = S.tq[bt]; snv = S.tsn[bt];
           dt = smem_dot<NPER>(ts + (long long)bt * ld, xr, d, lane);
@@ -372,7 +432,7 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
           else { nn = E.w[bj]; qv = E.q[bj]; snv = E.sn[bj]; }
           if (!touched && li >= 0) dt = S.rb[cur][li].dot;
           else {
-            if (bj != prnode) { load_row<NPER>(pr, E.s + (long long)bj * ld, d, lane); prnode = bj; }
+            if (bj != prnode) { load_row<NPER>(pr, E.s + (long long)bj * ld, d, lane); prnode = bj; ++c_dem; }
             dt = reg_dot<NPER>(pr, xr);
           }
         }
@@ -396,7 +456,7 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
           if (lane == 0) { S.tw[bt] = nw2; S.tq[bt] = nq; S.tsn[bt] = nsn; }
           __syncwarp();
         } else {
-          if (bj != prnode) { load_row<NPER>(pr, E.s + (long long)bj * ld, d, lane); prnode = bj; }
+          if (bj != prnode) { load_row<NPER>(pr, E.s + (long long)bj * ld, d, lane); prnode = bj; ++c_dem; }
 #pragma unroll
           for (int k = 0; k < NPER; ++k) pr[k] = take == 1 ? radd(pr[k], xr[k]) : radd(pr[k], rmul(ft, xr[k]));
           store_row<NPER>(E.s + (long long)bj * ld, pr, d, lane);
@@ -438,6 +498,7 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
       ++L;
     }
     __syncwarp();
+    ++c_it;
     if (status != ST_DONE) break;
     // ---- rotate prefetched data into place
     if (has_next) {
@@ -474,7 +535,7 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
   __syncwarp();
   for (int t = 0; t < nnew; ++t) {
     const int node = S.tid[t];
-    const double* rr = tref + (long long)t * ld;
+    const double* rr = tref + (long long)t * lds;
     const double* sr = ts + (long long)t * ld;
     for (int e = lane; e < ld; e += 32) { E.r[(long long)node * ld + e] = rr[e]; E.s[(long long)node * ld + e] = sr[e]; }
   }
@@ -523,5 +584,7 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
     C->F = F; C->F_alloc = Falloc; C->free_n = freen; C->G_alloc = Galloc;
     C->A_alloc = Aalloc; C->next_index = nidx; C->total_w = totw; C->max_depth = maxdepth;
     C->status = status; C->err = err; C->stop = stop; C->remaining = remaining;
+    C->cnt_levels += c_lv; C->cnt_direct += c_dir; C->cnt_demand += c_dem; C->cnt_slow += c_slow;
+    C->cnt_items += c_it;
   }
 }
