@@ -10,17 +10,7 @@
 // Error plumbing (host side).  Every C-ABI entry point returns 0 or a negative
 // code and leaves a message in a thread-local buffer (pcy_last_error()).
 // ---------------------------------------------------------------------------
-enum PcyStatus {
-  PCY_OK = 0,
-  PCY_EINVAL = -1,
-  PCY_ENONFINITE = -2,
-  PCY_EOVERFLOW = -3,
-  PCY_EWEIGHT = -4,
-  PCY_ECUDA = -5,
-  PCY_ENOMEM = -6,
-  PCY_ENCCL = -7,
-  PCY_ESTATE = -8,
-};
+#include "../../include/piecy_b200.h"   // C-ABI declarations and PCY_E* codes
 
 void pcy_set_error(const char* fmt, ...);
 void pcy_count_launch();
