@@ -103,12 +103,18 @@ __global__ void __launch_bounds__(128) k_dgemm(int M, int N, int K, double alpha
 // Y * Linv^T has orthonormal columns.  status[0] = 0 ok, 1 breakdown.
 __global__ void __launch_bounds__(1024) k_chol_inv(const double* __restrict__ G, int r, double shift,
                                                   double* __restrict__ L, double* __restrict__ Linv,
-                                                  int* __restrict__ status) {
+                                                  int* __restrict__ status, int expect_identity) {
   __shared__ double s_piv;
   __shared__ int s_bad;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   if (tid == 0) s_bad = 0;
-  for (long long e = tid; e < (long long)r * r; e += blockDim.x) L[e] = 0.0;
+  __syncthreads();
+  for (long long e = tid; e < (long long)r * r; e += blockDim.x) {
+    L[e] = 0.0;
+    // second CholeskyQR pass: the Gram of an already orthonormalised basis
+    // must be close to I, otherwise the first pass lost orthogonality
+    if (expect_identity && fabs(G[e] - ((e / r) == (e % r) ? 1.0 : 0.0)) > 1e-3) s_bad = 1;
+  }
   __syncthreads();
   for (int j = 0; j < r; ++j) {
     if (warp == 0) {
@@ -142,6 +148,73 @@ __global__ void __launch_bounds__(1024) k_chol_inv(const double* __restrict__ G,
       for (int k = c; k < i; ++k) acc -= L[(long long)i * r + k] * Linv[(long long)k * r + c];
       Linv[(long long)i * r + c] = acc / L[(long long)i * r + i];
     }
+  }
+  if (tid == 0) status[0] = 0;
+}
+
+
+// Rank-robust orthonormalisation (fallback when CholeskyQR breaks down on a
+// rank-deficient sketch, where LAPACK's Householder QR still returns an
+// orthonormal Q).  Classical Gram-Schmidt with re-orthogonalisation; a column
+// that vanishes is replaced by the next standard basis vector orthogonalised
+// against the accepted ones (the completion rule of linalg.py:97-117).  Only
+// the span reaches the projection, so any orthonormal completion is valid.
+__global__ void __launch_bounds__(1024) k_cgs2(double* __restrict__ Y, long long rows, int r,
+                                              double* __restrict__ coef, int* __restrict__ status) {
+  __shared__ double red[32];
+  __shared__ double s_val;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  auto block_sum = [&](double v) -> double {
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    if (warp == 0) { double t = lane < nw ? red[lane] : 0.0; t = warp_sum(t); if (lane == 0) s_val = t; }
+    __syncthreads();
+    return s_val;
+  };
+  auto orthogonalise = [&](int j) {
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int k = warp; k < j; k += nw) {
+        double acc = 0.0;
+        for (long long i = lane; i < rows; i += 32) acc = fma(Y[i * r + k], Y[i * r + j], acc);
+        acc = warp_sum(acc);
+        if (lane == 0) coef[k] = acc;
+      }
+      __syncthreads();
+      for (long long i = tid; i < rows; i += blockDim.x) {
+        double v = Y[i * r + j];
+        for (int k = 0; k < j; ++k) v = fma(-Y[i * r + k], coef[k], v);
+        Y[i * r + j] = v;
+      }
+      __syncthreads();
+    }
+  };
+  long long basis = 0;
+  for (int j = 0; j < r; ++j) {
+    double acc = 0.0;
+    for (long long i = tid; i < rows; i += blockDim.x) acc = fma(Y[i * r + j], Y[i * r + j], acc);
+    const double orig = sqrt(block_sum(acc));
+    orthogonalise(j);
+    acc = 0.0;
+    for (long long i = tid; i < rows; i += blockDim.x) acc = fma(Y[i * r + j], Y[i * r + j], acc);
+    double nrm = sqrt(block_sum(acc));
+    if (!(nrm > 1e-10 * orig) || orig == 0.0) {
+      for (;;) {
+        if (basis >= rows) { if (tid == 0) status[0] = 2; return; }
+        for (long long i = tid; i < rows; i += blockDim.x) Y[i * r + j] = (i == basis) ? 1.0 : 0.0;
+        ++basis;
+        __syncthreads();
+        orthogonalise(j);
+        acc = 0.0;
+        for (long long i = tid; i < rows; i += blockDim.x) acc = fma(Y[i * r + j], Y[i * r + j], acc);
+        nrm = sqrt(block_sum(acc));
+        if (nrm > 0.5) break;
+      }
+    }
+    const double inv = 1.0 / nrm;
+    for (long long i = tid; i < rows; i += blockDim.x) Y[i * r + j] *= inv;
+    __syncthreads();
   }
   if (tid == 0) status[0] = 0;
 }
@@ -297,10 +370,10 @@ static int gemm(cudaStream_t st, int M, int N, int K, double alpha, const double
 static int cholqr(cudaStream_t st, double* Y, long long rows, int r, double* Gs, double* Ls, double* Li,
                   double* T, int* status) {
   int hs = 0;
-  auto pass = [&](double shift, int* ok) -> int {
+  auto pass = [&](double shift, int* ok, int check) -> int {
     int rc;
     if ((rc = gemm(st, r, r, (int)rows, 1.0, Y, r, 1, Y, r, 0, 0.0, Gs, r))) return rc;
-    k_chol_inv<<<1, 1024, 0, st>>>(Gs, r, shift, Ls, Li, status); pcy_count_launch();
+    k_chol_inv<<<1, 1024, 0, st>>>(Gs, r, shift, Ls, Li, status, check); pcy_count_launch();
     PCY_LAUNCH_CHECK();
     PCY_CUDA(pcy_d2h(&hs, status, sizeof(int), st));
     *ok = hs == 0;
@@ -311,23 +384,20 @@ static int cholqr(cudaStream_t st, double* Y, long long rows, int r, double* Gs,
     return PCY_OK;
   };
   int ok = 0, rc;
-  if ((rc = pass(0.0, &ok))) return rc;
+  if ((rc = pass(0.0, &ok, 0))) return rc;
   if (ok) {
-    if ((rc = pass(0.0, &ok))) return rc;
+    if ((rc = pass(0.0, &ok, 1))) return rc;
     if (ok) return PCY_OK;
   }
-  // shifted CholeskyQR3: shift = 11 (m n + n (n+1)) u ||Y||_2^2, ||Y||_2^2 <= trace(G)
-  std::vector<double> g((size_t)r * r);
-  if ((rc = gemm(st, r, r, (int)rows, 1.0, Y, r, 1, Y, r, 0, 0.0, Gs, r))) return rc;
-  PCY_CUDA(pcy_d2h(g.data(), Gs, sizeof(double) * r * r, st));
-  double tr = 0.0;
-  for (int i = 0; i < r; ++i) tr += g[(size_t)i * r + i];
-  const double shift = 11.0 * ((double)rows * r + (double)r * (r + 1)) * 1.1102230246251565e-16 * tr;
-  if ((rc = pass(shift, &ok))) return rc;
-  if (!ok) { pcy_set_error("CholeskyQR breakdown even with shift"); return PCY_ESTATE; }
-  for (int it = 0; it < 2; ++it) {
-    if ((rc = pass(0.0, &ok))) return rc;
-    if (!ok) { pcy_set_error("CholeskyQR breakdown after shifted pass"); return PCY_ESTATE; }
+  // rank-deficient sketch: Gram-Schmidt with completion
+  {
+    double* coef = nullptr;
+    PCY_CUDA(cudaMallocAsync(&coef, sizeof(double) * r, st));
+    k_cgs2<<<1, 1024, 0, st>>>(Y, rows, r, coef, status); pcy_count_launch();
+    PCY_LAUNCH_CHECK();
+    PCY_CUDA(pcy_d2h(&hs, status, sizeof(int), st));
+    cudaFreeAsync(coef, st);
+    if (hs != 0) { pcy_set_error("orthonormal completion failed"); return PCY_ESTATE; }
   }
   return PCY_OK;
 }

@@ -54,3 +54,18 @@ def test_weighted_best_fit_matches_oracle():
     V, sig = O.weighted_fit(A, w, 12, 10, 2, 99)
     np.testing.assert_allclose(pr.singular_values, sig, rtol=1e-10)
     np.testing.assert_allclose(pr.vectors, V, atol=1e-9)
+
+
+@pytest.mark.parametrize("rows,cols,rank_true,ell,ov", [(4, 3, 1, 1, 2), (60, 30, 3, 8, 10), (500, 80, 5, 12, 10)])
+def test_rank_deficient_sketch_projects_like_reference(rows, cols, rank_true, ell, ov):
+    """LAPACK QR stays orthonormal on rank-deficient sketches; the device
+    CholeskyQR2 falls back to Gram-Schmidt with completion.  Only the span
+    reaches the projection, which must match the oracle."""
+    from paper_1502_04265_b200 import linalg
+    rng = np.random.default_rng(rows)
+    A = rng.normal(size=(rows, rank_true)) @ rng.normal(size=(rank_true, cols))
+    pr = linalg.randomized_truncated_svd(A, linalg.SvdTruncation(ell, ov, 2, 5))
+    V, sig = O.rsvd(A, ell, ov, 2, 5)
+    np.testing.assert_allclose(pr.singular_values[:rank_true], sig[:rank_true], rtol=1e-9)
+    np.testing.assert_allclose(linalg.project(A, pr), O.project(A, V), atol=1e-9 * np.abs(A).max())
+    np.testing.assert_allclose(pr.vectors.T @ pr.vectors, np.eye(ell), atol=1e-9)
