@@ -145,6 +145,7 @@ __device__ __forceinline__ void scan_members(const EngDev& E, const int* __restr
 
 #include "resolve_fast.cuh"
 #include "reattach_fast.cuh"
+#include "resolve_smem.cuh"
 
 // ------------------------------------------------------------------ stage
 // One warp per row: fp32/fp64 -> fp64 padded row, x_sq, validation, hash.
@@ -735,9 +736,9 @@ struct Engine {
   cudaEvent_t ev[6] = {};
   ChainHdr* chh = nullptr;
   ChainLvl* chr = nullptr;
-  int nper = 0;          // fast path registers per lane (0 = generic path)
+  int nper = 0;          // resolve kernel: 1..8 register rows, 100/101 shared-memory rows, 0 generic
   int nnew_cap = 0;
-  size_t res_smem = 0;
+  size_t res_smem = 0, rea_smem = 0;
   std::vector<void*> allocs;
 
   template <class T> int alloc(T*& p, long long count) {
@@ -809,29 +810,49 @@ struct Engine {
     A_(aggw, m + 2); A_(mp_nrm, sample_cap + 1);
 #undef A_
     for (auto& e : ev) PCY_CUDA(cudaEventCreate(&e));
-    if (ld <= 256) {
+    const size_t maxsm = 227 * 1024;
+    PCY_CUDA(cudaFuncSetAttribute(k_chain2, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    PCY_CUDA(cudaFuncSetAttribute(k_rchain, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    if (ld <= 256 && !getenv("PCY_SMEM_RESOLVE")) {
       nper = ld <= 32 ? 1 : ld <= 64 ? 2 : ld <= 128 ? 4 : 8;
       const size_t base = resolve_smem_bytes(ld, 0, NC, GC);
-      const size_t maxsm = 227 * 1024;
       long long cap = maxsm > base ? (long long)((maxsm - base) / (sizeof(double) * (2 * ld + 1))) : 0;
       if (cap > PCY_NNEW_MAX) cap = PCY_NNEW_MAX;
       nnew_cap = (int)cap;
-      res_smem = resolve_smem_bytes(ld, nnew_cap, NC, GC);
-      if (nnew_cap < 8) nper = 0;   // budget too large for the shared-memory tables
-      PCY_CUDA(cudaFuncSetAttribute(k_chain2, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-      PCY_CUDA(cudaFuncSetAttribute(k_rchain, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+      res_smem = rea_smem = resolve_smem_bytes(ld, nnew_cap, NC, GC);
+      if (nnew_cap < 8) nper = 0;
       switch (nper) {
         case 1: PCY_CUDA(cudaFuncSetAttribute(k_resolve2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
-                  PCY_CUDA(cudaFuncSetAttribute(k_reattach2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem)); break;
+                PCY_CUDA(cudaFuncSetAttribute(k_reattach2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem)); break;
         case 2: PCY_CUDA(cudaFuncSetAttribute(k_resolve2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
-                  PCY_CUDA(cudaFuncSetAttribute(k_reattach2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem)); break;
+                PCY_CUDA(cudaFuncSetAttribute(k_reattach2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem)); break;
         case 4: PCY_CUDA(cudaFuncSetAttribute(k_resolve2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
-                  PCY_CUDA(cudaFuncSetAttribute(k_reattach2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem)); break;
-        default: PCY_CUDA(cudaFuncSetAttribute(k_resolve2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
-                 PCY_CUDA(cudaFuncSetAttribute(k_reattach2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem)); break;
+                PCY_CUDA(cudaFuncSetAttribute(k_reattach2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem)); break;
+        case 8: PCY_CUDA(cudaFuncSetAttribute(k_resolve2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
+                PCY_CUDA(cudaFuncSetAttribute(k_reattach2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem)); break;
+        default: break;
       }
-      if (getenv("PCY_GENERIC_RESOLVE")) nper = 0;
     }
+    if (!nper) {
+      // rows in shared memory, any dimension
+      const size_t base_t = resolve3_smem_bytes<2048>(ld, 0, true, NC, GC, 2);
+      long long cap = maxsm > base_t ? (long long)((maxsm - base_t) / (sizeof(double) * (2 * ld + 1))) : 0;
+      if (cap > PCY_NNEW_MAX) cap = PCY_NNEW_MAX;
+      if (cap >= 16) {
+        nper = 100; nnew_cap = (int)cap;
+        res_smem = resolve3_smem_bytes<2048>(ld, nnew_cap, true, NC, GC, 0);
+        rea_smem = resolve3_smem_bytes<2048>(ld, nnew_cap, true, NC, GC, 2);
+        PCY_CUDA(cudaFuncSetAttribute(k_resolve3<true, 2048>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
+        PCY_CUDA(cudaFuncSetAttribute(k_reattach3<true, 2048>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem));
+      } else if (resolve3_smem_bytes<1024>(ld, 0, false, NC, GC, 2) <= maxsm) {
+        nper = 101; nnew_cap = PCY_NNEW_MAX;
+        res_smem = resolve3_smem_bytes<1024>(ld, 0, false, NC, GC, 0);
+        rea_smem = resolve3_smem_bytes<1024>(ld, 0, false, NC, GC, 2);
+        PCY_CUDA(cudaFuncSetAttribute(k_resolve3<false, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
+        PCY_CUDA(cudaFuncSetAttribute(k_reattach3<false, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem));
+      }
+    }
+    if (getenv("PCY_GENERIC_RESOLVE")) nper = 0;
     PCY_CUDA(cudaHostAlloc(&ctl_h, sizeof(EngCtl), cudaHostAllocMapped));
     memset(ctl_h, 0, sizeof(EngCtl));
     PCY_CUDA(cudaHostGetDevicePointer((void**)&ctl_map_d, ctl_h, 0));
@@ -877,7 +898,9 @@ struct Engine {
             case 1: k_reattach2<1><<<1, 32, res_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr); pcy_count_launch(); break;
             case 2: k_reattach2<2><<<1, 32, res_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr); pcy_count_launch(); break;
             case 4: k_reattach2<4><<<1, 32, res_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr); pcy_count_launch(); break;
-            default: k_reattach2<8><<<1, 32, res_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr); pcy_count_launch(); break;
+            case 8: k_reattach2<8><<<1, 32, res_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr); pcy_count_launch(); break;
+            case 100: k_reattach3<true, 2048><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr); pcy_count_launch(); break;
+            default: k_reattach3<false, 1024><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr); pcy_count_launch(); break;
           }
           PCY_LAUNCH_CHECK();
           rc = sync_ctl(st); if (rc) return rc;
@@ -936,6 +959,8 @@ struct Engine {
           case 2: k_resolve2<2><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
           case 4: k_resolve2<4><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
           case 8: k_resolve2<8><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
+          case 100: k_resolve3<true, 2048><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
+          case 101: k_resolve3<false, 1024><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
           default:
             k_resolve<<<1, 32, sizeof(double) * ld, st>>>(E, Xs, XSs, Ws, Bs, nb - start, 0, first_rem, countw); pcy_count_launch();
         }
