@@ -49,22 +49,16 @@ def parse():
     return ap.parse_args()
 
 
-def workload(args):
-    from paper_1502_04265_b200 import workloads as W
-    cfg = W.CONFIGS[args.config]
-    X = W.generate(args.config, args.rows)
-    return cfg, X
-
-
-def config_json(cfg, X, N):
+def config_json(cfg, n, N):
     return {
-        "workload": (f"{cfg.name}: {cfg.entry} n={X.shape[0]} d={cfg.d} {cfg.dtype} k={cfg.k} m={cfg.m} "
+        "workload": (f"{cfg.name}: {cfg.entry} n={n} d={cfg.d} {cfg.dtype} k={cfg.k} m={cfg.m} "
                      f"svd_dim={cfg.svd_dim} piece={cfg.piece_size}"
                      + (f" num_pieces={cfg.num_pieces}" if cfg.num_pieces else "")
                      + f" + kmeans_repetitions(reps={cfg.reps}, max_iters={cfg.max_iters}, tol=1e-4)"),
-        "n": int(X.shape[0]), "d": cfg.d, "k": cfg.k, "coreset_size": cfg.m, "svd_dim": cfg.svd_dim,
+        "n": int(n), "d": cfg.d, "k": cfg.k, "coreset_size": cfg.m, "svd_dim": cfg.svd_dim,
         "piece_size": cfg.piece_size, "reps": cfg.reps, "seed": cfg.seed,
-        "parallelism": "replicas" if N > 1 else "single-engine",
+        "parallelism": (("replicas" if N > 1 else "single-engine") if cfg.entry == "piecy"
+                        else f"level-0 groups sharded over {N} GPU(s), NCCL gather to rank 0"),
         "l2": "256 MiB buffer written between timed steps (input is ~L2-sized)",
     }
 
@@ -133,26 +127,33 @@ def cpu_run(cfg, X):
     return time.perf_counter() - t0
 
 
-def cpu_sample(cfg, X, budget_s=20.0):
-    """Bounded CPU sample: the whole stream when it fits ~budget, else a prefix."""
-    n = X.shape[0]
-    rows = n
-    probe = min(n, 50_000)
-    t = cpu_run(cfg, X[:probe])
-    est = t * n / probe
-    if est > budget_s:
-        rows = max(probe, int(n * budget_s / est))
+def stream_prefix(cfg, rows, n_total=None):
+    from paper_1502_04265_b200 import workloads as W
+    if cfg.entry == "piecy":
+        return W.generate(cfg.name, n_total)[:rows]
+    return W.generate_rows(cfg.name, 0, rows, n=n_total)
+
+
+def cpu_sample(cfg, n_total, budget_s=20.0):
+    """Bounded CPU sample: the whole stream when it fits ~budget, else a prefix.
+    Returns (rows, seconds, prefix array)."""
+    probe = min(n_total, 50_000 if cfg.d <= 256 else 10_000)
+    Xp = stream_prefix(cfg, probe, n_total)
+    t = cpu_run(cfg, Xp)
+    rows = n_total if t * n_total / probe <= budget_s else max(probe, int(n_total * budget_s / (t * n_total / probe)))
     if rows != probe:
-        t = cpu_run(cfg, X[:rows])
-    return rows, t
+        Xp = stream_prefix(cfg, rows, n_total)
+        t = cpu_run(cfg, Xp)
+    return rows, t, Xp
 
 
 def run_reference(args, rank):
     if rank != 0:
         return
-    cfg, X = workload(args)
-    rows, t = cpu_sample(cfg, X, budget_s=max(5.0, 150.0 / max(1, args.steps)))
-    Xs = X[:rows]
+    from paper_1502_04265_b200 import workloads as W
+    cfg = W.CONFIGS[args.config]
+    n_total = args.rows or cfg.n
+    rows, t, Xs = cpu_sample(cfg, n_total, budget_s=max(5.0, 150.0 / max(1, args.steps)))
     for _ in range(min(args.warmup, 1)):
         cpu_run(cfg, Xs)
     times = [cpu_run(cfg, Xs) for _ in range(args.steps)]
@@ -163,9 +164,9 @@ def run_reference(args, rank):
         "impl": "reference", "metric": METRIC, "value": val, "unit": "points/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": min(args.warmup, 1), "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": config_json(cfg, X, 1),
+        "data": "synthetic", "config": config_json(cfg, n_total, 1),
         "cpu_baseline": {"value": val, "unit": "points/s", "cores": cores, "kind": "port",
-                         "sample": f"first {rows} of {X.shape[0]} rows of {cfg.name}; BICO engine in C "
+                         "sample": f"first {rows} of {n_total} rows of {cfg.name}; BICO engine in C "
                                    f"(1 thread), clustering numpy/OpenBLAS ({cores} threads)"},
         "e2e": {"value": val, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -173,6 +174,101 @@ def run_reference(args, rank):
 
 
 # --------------------------------------------------------------------- ours
+class PiecyWork:
+    """cfg1-3: run_piecy on one engine; replicas across ranks (weak scaling)."""
+
+    scaling = "weak"
+
+    def __init__(self, cfg, args, dev):
+        import torch
+        from paper_1502_04265_b200 import workloads as W
+        from paper_1502_04265_b200.pipeline import PiecyConfig
+        self.cfg = cfg
+        self.X = W.generate(cfg.name, args.rows)
+        self.X_host_sample = self.X
+        self.Xd = torch.from_numpy(self.X).to(dev)
+        self.pcfg = PiecyConfig(k=cfg.k, piece_size=cfg.piece_size, svd_dim=cfg.svd_dim, coreset_size=cfg.m,
+                                seed=cfg.seed)
+        self.units = int(os.environ.get("WORLD_SIZE", "1"))
+        self.h2d_bytes = self.X.nbytes
+
+    def coreset_device(self):
+        from paper_1502_04265_b200.pipeline import run_piecy_device
+        eng = run_piecy_device(self.Xd, self.cfg.d, self.pcfg)
+        P, w = eng.extract_device()
+        return P, w, eng
+
+    def coreset_public(self):
+        from paper_1502_04265_b200.pipeline import run_piecy
+        return run_piecy(self.X, self.cfg.d, self.pcfg)
+
+    def cpu_rows(self):
+        return self.X
+
+
+class MrWork:
+    """cfg4-5: piecy-mr, level-0 groups sharded over the ranks (strong scaling);
+    each rank generates and uploads only its own groups' rows."""
+
+    scaling = "strong"
+
+    def __init__(self, cfg, args, dev, n_total, rank, world):
+        import torch
+        from paper_1502_04265_b200 import workloads as W
+        from paper_1502_04265_b200.distributed import level0_groups, owner
+        from paper_1502_04265_b200.mergereduce import MrConfig
+        self.cfg, self.dev, self.n, self.rank, self.world = cfg, dev, n_total, rank, world
+        self.mcfg = MrConfig(k=cfg.k, piece_size=cfg.piece_size, num_pieces=cfg.num_pieces, svd_dim=cfg.svd_dim,
+                             coreset_size=cfg.m, seed=cfg.seed)
+        self.groups = level0_groups(n_total, cfg.piece_size, cfg.num_pieces)
+        self.host = {}
+        self.dev_rows = {}
+        for g in self.groups:
+            if owner(g.index, world) == rank:
+                self.host[g.index] = W.generate_rows(cfg.name, g.row_start, g.row_end, n=n_total)
+                self.dev_rows[g.index] = torch.from_numpy(self.host[g.index]).to(dev)
+        self.X_host_sample = next(iter(self.host.values())) if self.host else np.zeros((0, cfg.d), np.float32)
+        self.units = 1
+        self.h2d_bytes = sum(a.nbytes for a in self.host.values())
+
+    def _src(self, table):
+        gs = self.groups
+
+        def source(a, b):
+            for g in gs:
+                if g.row_start <= a < g.row_end:
+                    return table[g.index][a - g.row_start:b - g.row_start]
+            raise IndexError(a)
+        return source
+
+    def _run(self, table):
+        from paper_1502_04265_b200.distributed import DeviceOps, run_piecy_mr_sharded
+        ops = DeviceOps(self.mcfg, self.dev)
+        dev = self.dev
+        import torch
+        src = self._src(table)
+
+        def source(a, b):
+            blk = src(a, b)
+            return blk if isinstance(blk, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(blk)).to(dev)
+        return run_piecy_mr_sharded(source, self.n, self.cfg.d, self.mcfg, rank=self.rank, world=self.world, ops=ops)
+
+    def coreset_device(self):
+        import torch
+        cs = self._run(self.dev_rows)
+        if cs is None:
+            return None, None, None
+        P = torch.from_numpy(cs.points).to(self.dev)
+        w = torch.from_numpy(cs.weights).to(self.dev)
+        return P, w, None
+
+    def coreset_public(self):
+        return self._run(self.host)
+
+    def cpu_rows(self):
+        return self.X_host_sample
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -190,31 +286,37 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     from paper_1502_04265_b200 import _native as nat
+    from paper_1502_04265_b200 import workloads as W
     from paper_1502_04265_b200.evaluation import kmeans_repetitions, kmeans_repetitions_device
-    from paper_1502_04265_b200.pipeline import PiecyConfig, run_piecy, run_piecy_device
 
-    cfg, X = workload(args)
-    n, d = X.shape
-    pcfg = PiecyConfig(k=cfg.k, piece_size=cfg.piece_size, svd_dim=cfg.svd_dim, coreset_size=cfg.m, seed=cfg.seed)
-    Xd = torch.from_numpy(X).to(dev)
+    cfg = W.CONFIGS[args.config]
+    n_total = args.rows or cfg.n
+    d = cfg.d
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-
-    phase_ms = {"coreset": 0.0, "kmeans": 0.0}
+    if cfg.entry == "piecy":
+        work = PiecyWork(cfg, args, dev)
+    else:
+        work = MrWork(cfg, args, dev, n_total, rank, world)
+    X = work.X_host_sample
+    n = n_total
 
     def step_device():
         st0 = torch.cuda.current_stream()
         a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         a.record(st0)
-        eng = run_piecy_device(Xd, d, pcfg)
-        P, w = eng.extract_device()
+        P, w, eng = work.coreset_device()
         b.record(st0)
-        C, costs = kmeans_repetitions_device(P, w, cfg.k, cfg.reps, cfg.seed, cfg.max_iters, 1e-4)
+        F, costs = 0, None
+        if P is not None:
+            F = int(P.shape[0])
+            C, costs = kmeans_repetitions_device(P, w, cfg.k, cfg.reps, cfg.seed, cfg.max_iters, 1e-4)
         c.record(st0)
         c.synchronize()
         step_device.phases.append((a.elapsed_time(b), b.elapsed_time(c)))
         step_device.engine = eng
-        return P.shape[0], costs
+        return F, costs
     step_device.phases = []
+    step_device.engine = None
 
     if args.ncu:
         step_device()
@@ -260,14 +362,17 @@ def main():
     for it in range(max(1, min(args.steps, 3))):
         flush.fill_(1.0)
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
-        cs = run_piecy(X, d, pcfg)
-        runs = kmeans_repetitions(cs.points, cs.weights.astype(np.float64), cfg.k, reps=cfg.reps, seed=cfg.seed,
-                                  max_iters=cfg.max_iters, tol=1e-4)
+        cs = work.coreset_public()
+        if cs is not None:
+            runs = kmeans_repetitions(cs.points, cs.weights.astype(np.float64), cfg.k, reps=cfg.reps,
+                                      seed=cfg.seed, max_iters=cfg.max_iters, tol=1e-4)
         torch.cuda.synchronize()
         e2e_times.append(time.perf_counter() - t0)
-        h2d = X.nbytes + cs.points.nbytes + cs.weights.size * 8 + cfg.reps * cfg.k * 8
-        d2h = cs.points.nbytes + cs.weights.nbytes + sum(c.nbytes + 8 for c, _ in runs)
+        h2d = work.h2d_bytes + (cs.points.nbytes + cs.weights.size * 8 + cfg.reps * cfg.k * 8 if cs is not None else 0)
+        d2h = (cs.points.nbytes + cs.weights.nbytes + sum(c.nbytes + 8 for c, _ in runs)) if cs is not None else 0
 
     t_local = torch.tensor([ms / args.steps, float(np.mean(e2e_times))], dtype=torch.float64, device=dev)
     if world > 1:
@@ -300,16 +405,16 @@ def main():
                      for k, v in prof.items()}
         cpu = None
         if not args.no_cpu_baseline:
-            rows, t = cpu_sample(cfg, X)
+            rows, t, _ = cpu_sample(cfg, n)
             cpu = {"value": rows / t, "unit": "points/s", "cores": os.cpu_count() or 1, "kind": "port",
                    "sample": f"first {rows} of {n} rows of {cfg.name}, one pass; BICO in C (1 thread), "
-                             f"clustering numpy/OpenBLAS"}
+                             f"projection + clustering numpy/OpenBLAS"}
         line = {
-            "metric": METRIC, "value": n * world / (ms_step / 1e3), "unit": "points/s", "n_gpus": world,
+            "metric": METRIC, "value": work.units * n / (ms_step / 1e3), "unit": "points/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_json(cfg, X, world),
-            "e2e": {"value": n * world / e2e_s, "unit": "points/s", "h2d_bytes_per_step": int(h2d),
+            "scaling": work.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_json(cfg, n, world),
+            "e2e": {"value": work.units * n / e2e_s, "unit": "points/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(launches),
             "roofline": roof,
@@ -318,7 +423,7 @@ def main():
             "kernel_ms_per_step": kernel_ms,
             "dominant_kernel": dom,
             "coreset_size": int(F),
-            "engine_counters": step_device.engine.counters(),
+            "engine_counters": step_device.engine.counters() if step_device.engine is not None else None,
             "step_ms": ms_steps,
             "phase_ms": [{"coreset": round(p[0], 2), "kmeans": round(p[1], 2)} for p in step_device.phases[-args.steps:]],
         }

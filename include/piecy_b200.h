@@ -71,6 +71,8 @@ int pcy_engine_extract(void* engine, double* points, long long* weights, long lo
 /* Instrumentation of the in-order resolve: out6 (host) = [levels walked,
  * direct scans, demand row loads, full capacity evaluations, items, max depth]. */
 int pcy_engine_counters(void* engine, long long* out6);
+/* The same counters summed over every engine destroyed so far in the process. */
+int pcy_engine_counters_total(long long* out6);
 
 /* --------------------------------------------------- clustering on coreset */
 

@@ -29,6 +29,7 @@ _SIGS = {
     "pcy_engine_features": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, P_i64, c_vp]),
     "pcy_engine_extract": (c_i32, [c_vp, c_vp, c_vp, c_i64, P_i64, c_vp]),
     "pcy_engine_counters": (c_i32, [c_vp, c_vp]),
+    "pcy_engine_counters_total": (c_i32, [c_vp]),
     # instrumentation
     "pcy_launch_count": (c_i64, []),
     "pcy_prof_enable": (c_i32, [c_i32]),
@@ -37,6 +38,14 @@ _SIGS = {
 }
 
 PROF_SLOTS = {"resolve": 0, "chain": 1, "reattach": 2, "seed": 3, "lloyd": 4, "gemm": 5}
+
+
+def engine_counters_total() -> dict:
+    import numpy as np
+    out = np.zeros(6, dtype=np.int64)
+    lib().pcy_engine_counters_total(out.ctypes.data)
+    keys = ("levels", "direct_scans", "demand_loads", "slow_capacity", "items", "max_depth")
+    return {k: int(v) for k, v in zip(keys, out)}
 
 
 def launch_count() -> int:

@@ -20,6 +20,14 @@ cudaError_t pcy_spin_sync(cudaStream_t st);
 // Device -> host copy of a small result through a thread-local pinned
 // staging buffer, completed with pcy_spin_sync.
 cudaError_t pcy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t st);
+// DMMA distance contraction (distance.cu)
+int pcy_launch_gram(const double* A, const int* aidx, long long lda, int M, const double* B, const int* bidx,
+                    long long ldb, int N, int K, double* C, long long ldc, cudaStream_t st);
+int pcy_launch_parts(const double* A, const int* aidx, long long lda, int M, const double* B, long long ldb,
+                     const double* rn, int N, int K, double* C, long long ldc, cudaStream_t st);
+int pcy_launch_nearest(const double* A, const int* aidx, long long lda, int M, const double* B, const int* bidx,
+                       long long ldb, const double* rn, int N, int K, double* ppart, int* ppos, int* out_pos,
+                       double* out_part, cudaStream_t st);
 
 // Per-kernel event timing (enabled by pcy_prof_enable).
 enum { PCY_PROF_RESOLVE = 0, PCY_PROF_CHAIN = 1, PCY_PROF_REATTACH = 2, PCY_PROF_SEED = 3,

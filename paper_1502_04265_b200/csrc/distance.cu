@@ -1,0 +1,223 @@
+// Distance contraction on the fp64 tensor pipe (sm_100a DMMA).
+//
+// The BICO decisions compare parts |r|^2 - 2 r.x in fp64 (coreset.py:172-176),
+// so the contraction runs on DMMA (mma.sync m8n8k4 f64, exact fp64 products
+// and sums) -- tcgen05 has no fp64 kind.  Two forms:
+//   k_dist_tile<0>  C[m][n] = A[ia(m)] . B[ib(n)]          (block Gram for K3)
+//   k_dist_tile<1>  per-(row, 64-column tile) argmin of rn[ib(n)] - 2 A.B,
+//                   first column on ties; k_argmin_reduce folds the tiles.
+// Rows of A and B may be gathered through index arrays (tree nodes live at
+// arbitrary slots), so no operand is ever copied into a packed buffer.
+#include "common.cuh"
+
+namespace {
+
+constexpr int DBM = 64, DBN = 64, DBK = 16;
+
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(128) k_dist_tile(int M, int N, int K,
+                                                  const double* __restrict__ A, const int* __restrict__ aidx, long long lda,
+                                                  const double* __restrict__ B, const int* __restrict__ bidx, long long ldb,
+                                                  const double* __restrict__ rn,
+                                                  double* __restrict__ C, long long ldc,
+                                                  double* __restrict__ ppart, int* __restrict__ ppos, int ntiles) {
+  __shared__ double As[2][DBM][DBK + 4];
+  __shared__ double Bs[2][DBK][DBN + 4];
+  __shared__ long long arow[DBM], brow[DBN];
+  __shared__ double s_rn[DBN];
+  __shared__ double red_p[DBM][2];
+  __shared__ int red_c[DBM][2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int m0 = blockIdx.y * DBM, n0 = blockIdx.x * DBN;
+  if (tid < DBM) {
+    const int m = m0 + tid;
+    arow[tid] = m < M ? (long long)(aidx ? aidx[m] : m) * lda : -1;
+  } else {
+    const int nn = tid - DBM, n = n0 + nn;
+    brow[nn] = n < N ? (long long)(bidx ? bidx[n] : n) * ldb : -1;
+    if (MODE != 0) s_rn[nn] = n < N ? rn[bidx ? bidx[n] : n] : INFINITY;
+  }
+  __syncthreads();
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) { acc[i][j][0] = 0.0; acc[i][j][1] = 0.0; }
+
+  // register-staged double buffering of the 64x16 operand tiles
+  double ra[8], rb[8];
+  auto fetch = [&](int k0) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int e = tid + r * 128;
+      const int mm = e >> 4, kk = e & 15;
+      const long long ar = arow[mm], br = brow[mm];
+      ra[r] = (ar >= 0 && k0 + kk < K) ? A[ar + k0 + kk] : 0.0;
+      rb[r] = (br >= 0 && k0 + kk < K) ? B[br + k0 + kk] : 0.0;
+    }
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int e = tid + r * 128;
+      const int mm = e >> 4, kk = e & 15;
+      As[buf][mm][kk] = ra[r];
+      Bs[buf][kk][mm] = rb[r];
+    }
+  };
+  int buf = 0;
+  fetch(0);
+  stash(0);
+  __syncthreads();
+  for (int k0 = 0; k0 < K; k0 += DBK) {
+    const bool more = k0 + DBK < K;
+    if (more) fetch(k0 + DBK);
+#pragma unroll
+    for (int ks = 0; ks < DBK; ks += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = As[buf][wm + i * 8 + g][ks + t4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = Bs[buf][ks + t4][wn + j * 8 + g];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    if (more) {
+      stash(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+
+  if (MODE == 0 || MODE == 2) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int m = m0 + wm + i * 8 + g, cl = wn + j * 8 + 2 * t4 + h, n = n0 + cl;
+          if (m < M && n < N)
+            C[(long long)m * ldc + n] = MODE == 0 ? acc[i][j][h] : radd(s_rn[cl], rmul(acc[i][j][h], -2.0));
+        }
+    return;
+  }
+  // MODE 1: argmin over this tile's 64 columns per row, lowest column on ties
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    double bp = INFINITY; int bc = 0x7fffffff;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int cl = wn + j * 8 + 2 * t4 + h;
+        if (n0 + cl < N) {
+          const double p = radd(s_rn[cl], rmul(acc[i][j][h], -2.0));
+          if (p < bp || (p == bp && cl < bc)) { bp = p; bc = cl; }
+        }
+      }
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+      const double op = __shfl_xor_sync(PCY_FULL, bp, o);
+      const int oc = __shfl_xor_sync(PCY_FULL, bc, o);
+      if (op < bp || (op == bp && oc < bc)) { bp = op; bc = oc; }
+    }
+    if (t4 == 0) { red_p[wm + i * 8 + g][warp & 1] = bp; red_c[wm + i * 8 + g][warp & 1] = bc; }
+  }
+  __syncthreads();
+  if (tid < DBM) {
+    const int m = m0 + tid;
+    double p0 = red_p[tid][0], p1 = red_p[tid][1];
+    int c0 = red_c[tid][0], c1 = red_c[tid][1];
+    if (p1 < p0 || (p1 == p0 && c1 < c0)) { p0 = p1; c0 = c1; }
+    if (m < M) {
+      ppart[(long long)m * ntiles + blockIdx.x] = p0;
+      ppos[(long long)m * ntiles + blockIdx.x] = c0 == 0x7fffffff ? 0x7fffffff : n0 + c0;
+    }
+  }
+}
+
+// per row: argmin over tiles (positions increase with the tile index)
+__global__ void k_argmin_reduce(int M, int ntiles, const double* __restrict__ ppart, const int* __restrict__ ppos,
+                                int* __restrict__ out_pos, double* __restrict__ out_part) {
+  const int lane = threadIdx.x & 31;
+  const int m = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (m >= M) return;
+  double bp = INFINITY; int bc = 0x7fffffff;
+  for (int t = lane; t < ntiles; t += 32) {
+    const double p = ppart[(long long)m * ntiles + t];
+    const int c = ppos[(long long)m * ntiles + t];
+    if (p < bp || (p == bp && c < bc)) { bp = p; bc = c; }
+  }
+  warp_argmin(bp, bc);
+  if (lane == 0) { out_pos[m] = bc; out_part[m] = bp; }
+}
+
+}  // namespace
+
+int pcy_launch_gram(const double* A, const int* aidx, long long lda, int M, const double* B, const int* bidx,
+                    long long ldb, int N, int K, double* C, long long ldc, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return PCY_OK;
+  dim3 grid((unsigned)((N + DBN - 1) / DBN), (unsigned)((M + DBM - 1) / DBM));
+  k_dist_tile<0><<<grid, 128, 0, st>>>(M, N, K, A, aidx, lda, B, bidx, ldb, nullptr, C, ldc, nullptr, nullptr, 0);
+  pcy_count_launch();
+  PCY_LAUNCH_CHECK();
+  return PCY_OK;
+}
+
+// Parts matrix: C[m][n] = rn[n] - 2 A[ia(m)].B[n] (the full-set form of K1:
+// every block row against every allocated reference slot).
+int pcy_launch_parts(const double* A, const int* aidx, long long lda, int M, const double* B, long long ldb,
+                     const double* rn, int N, int K, double* C, long long ldc, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return PCY_OK;
+  dim3 grid((unsigned)((N + DBN - 1) / DBN), (unsigned)((M + DBM - 1) / DBM));
+  k_dist_tile<2><<<grid, 128, 0, st>>>(M, N, K, A, aidx, lda, B, nullptr, ldb, rn, C, ldc, nullptr, nullptr, 0);
+  pcy_count_launch();
+  PCY_LAUNCH_CHECK();
+  return PCY_OK;
+}
+
+// Nearest reference per row: out_pos[m] = column (position) of the minimum
+// part rn[ib(n)] - 2 A[ia(m)].B[ib(n)], lowest position on ties.  Scratch:
+// ppart / ppos of M x ceil(N/64).
+int pcy_launch_nearest(const double* A, const int* aidx, long long lda, int M, const double* B, const int* bidx,
+                       long long ldb, const double* rn, int N, int K, double* ppart, int* ppos, int* out_pos,
+                       double* out_part, cudaStream_t st) {
+  if (M <= 0) return PCY_OK;
+  const int ntiles = (N + DBN - 1) / DBN;
+  dim3 grid((unsigned)ntiles, (unsigned)((M + DBM - 1) / DBM));
+  k_dist_tile<1><<<grid, 128, 0, st>>>(M, N, K, A, aidx, lda, B, bidx, ldb, rn, nullptr, 0, ppart, ppos, ntiles);
+  pcy_count_launch();
+  k_argmin_reduce<<<(unsigned)((M + 7) / 8), 256, 0, st>>>(M, ntiles, ppart, ppos, out_pos, out_part);
+  pcy_count_launch();
+  PCY_LAUNCH_CHECK();
+  return PCY_OK;
+}
+
+extern "C" int pcy_nearest_refs(const double* X, long long ldx, int M, const double* R, const int* ridx,
+                                long long ldr, const double* rn, int N, int K, int* out_pos, double* out_part,
+                                void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int ntiles = (N + DBN - 1) / DBN;
+  double* pp = nullptr; int* pc = nullptr;
+  PCY_CUDA(cudaMallocAsync(&pp, sizeof(double) * (size_t)M * (ntiles > 0 ? ntiles : 1), st));
+  PCY_CUDA(cudaMallocAsync(&pc, sizeof(int) * (size_t)M * (ntiles > 0 ? ntiles : 1), st));
+  int rc = pcy_launch_nearest(X, nullptr, ldx, M, R, ridx, ldr, rn, N, K, pp, pc, out_pos, out_part, st);
+  cudaFreeAsync(pp, st);
+  cudaFreeAsync(pc, st);
+  return rc;
+}
+
+extern "C" int pcy_gram(const double* A, long long lda, int M, const double* B, long long ldb, int N, int K,
+                        double* C, long long ldc, void* stream) {
+  return pcy_launch_gram(A, nullptr, lda, M, B, nullptr, ldb, N, K, C, ldc, (cudaStream_t)stream);
+}

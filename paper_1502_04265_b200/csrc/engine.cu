@@ -31,6 +31,7 @@ extern "C" const char* pcy_last_error(void) { return g_err; }
 // Launch counter (bench.py's gpu_launches) and optional per-kernel event
 // timing of the engine's sequential kernels (bench.py's roofline).
 static std::atomic<long long> g_launches{0};
+static std::atomic<long long> g_counters[6];   // summed over destroyed engines
 void pcy_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 static std::atomic<int> g_prof_on{0};
 static std::mutex g_prof_mu;
@@ -140,6 +141,19 @@ __device__ __forceinline__ void scan_members(const EngDev& E, const int* __restr
     if (lane < nm) { part = radd(E.rn[myid], rmul(dt, -2.0)); pos = c0 + lane; }
     warp_argmin(part, pos);
     if (part < bp) { bp = part; bpos = pos; }
+  }
+}
+
+// Nearest among members [0, cnt) using a precomputed parts row (full-set K1).
+__device__ __forceinline__ void scan_parts(const double* __restrict__ prow, const int* __restrict__ mem, int cnt,
+                                           int lane, double& bp, int& bpos) {
+  bp = INFINITY; bpos = 0x7fffffff;
+  for (int c0 = 0; c0 < cnt; c0 += 32) {
+    const int p = c0 + lane;
+    double v = INFINITY; int ps = 0x7fffffff;
+    if (p < cnt) { v = prow[mem[p]]; ps = p; }
+    warp_argmin(v, ps);
+    if (v < bp) { bp = v; bpos = ps; }
   }
 }
 
@@ -301,8 +315,11 @@ __global__ void k_mp_finish(EngDev E, long long ns) {
 }
 
 // ------------------------------------------------------- host publication
-__global__ void k_publish(const EngCtl* __restrict__ src, EngCtl* dst, long long seq) {
+__global__ void k_publish(EngCtl* __restrict__ src, EngCtl* dst, long long seq, const int* g_count,
+                          const int* g_base) {
   const int lane = threadIdx.x;
+  if (lane == 0) { src->root_count = g_count[0]; src->root_base = g_base[0]; }
+  __syncwarp();
   const int words = (int)(offsetof(EngCtl, seq) / sizeof(long long));
   const long long* s = reinterpret_cast<const long long*>(src);
   volatile long long* t = reinterpret_cast<volatile long long*>(dst);
@@ -736,6 +753,8 @@ struct Engine {
   cudaEvent_t ev[6] = {};
   ChainHdr* chh = nullptr;
   ChainLvl* chr = nullptr;
+  double* parts = nullptr;                             // full-set parts matrix (1024 x NC)
+  double* gram = nullptr;                              // block Gram (K3 with rows in HBM)
   int nper = 0;          // resolve kernel: 1..8 register rows, 100/101 shared-memory rows, 0 generic
   int nnew_cap = 0;
   size_t res_smem = 0, rea_smem = 0;
@@ -753,6 +772,12 @@ struct Engine {
     for (auto& a : allocs) if (a == p) { cudaFree(a); a = nullptr; }
   }
   ~Engine() {
+    if (ctl_h) {
+      g_counters[0] += ctl_h->cnt_levels; g_counters[1] += ctl_h->cnt_direct; g_counters[2] += ctl_h->cnt_demand;
+      g_counters[3] += ctl_h->cnt_slow; g_counters[4] += ctl_h->cnt_items;
+      long long md = g_counters[5].load();
+      while (ctl_h->max_depth > md && !g_counters[5].compare_exchange_weak(md, ctl_h->max_depth)) {}
+    }
     for (auto& e : ev) if (e) cudaEventDestroy(e);
     for (void* a : allocs) if (a) cudaFree(a);
     if (ctl_h) cudaFreeHost(ctl_h);
@@ -762,7 +787,7 @@ struct Engine {
   // sequence number: no stream synchronisation, no wake-up latency.
   int sync_ctl(cudaStream_t st) {
     const long long want = ++seq;
-    k_publish<<<1, 32, 0, st>>>(E.ctl, ctl_map_d, want); pcy_count_launch();
+    k_publish<<<1, 32, 0, st>>>(E.ctl, ctl_map_d, want, E.g_count, E.g_base); pcy_count_launch();
     PCY_LAUNCH_CHECK();
     volatile long long* sp = &ctl_h->seq;
     for (long long spins = 0; *sp != want; ++spins) {
@@ -800,6 +825,7 @@ struct Engine {
     A_(E.xb, Bmax * ld); A_(E.xsq, Bmax); A_(E.wb, Bmax); A_(E.hsh, Bmax); A_(E.bad, Bmax);
     A_(E.ch_node, Bmax * PCY_MAXL); A_(E.ch_part, Bmax * PCY_MAXL); A_(E.ch_len, Bmax);
     A_(chh, Bmax); A_(chr, Bmax * PCY_FMAXL);
+    A_(gram, (long long)1024 * 1024);
     E.pend_cap = m + 2;
     A_(E.pend_x, E.pend_cap * ld); A_(E.pend_w, E.pend_cap); A_(E.pend_xsq, E.pend_cap);
     A_(E.dist_x, (m + 2) * ld);
@@ -844,12 +870,12 @@ struct Engine {
         rea_smem = resolve3_smem_bytes<2048>(ld, nnew_cap, true, NC, GC, 2);
         PCY_CUDA(cudaFuncSetAttribute(k_resolve3<true, 2048>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
         PCY_CUDA(cudaFuncSetAttribute(k_reattach3<true, 2048>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem));
-      } else if (resolve3_smem_bytes<1024>(ld, 0, false, NC, GC, 2) <= maxsm) {
+      } else if (resolve3_smem_bytes<512>(ld, 0, false, NC, GC, 2) <= maxsm) {
         nper = 101; nnew_cap = PCY_NNEW_MAX;
-        res_smem = resolve3_smem_bytes<1024>(ld, 0, false, NC, GC, 0);
-        rea_smem = resolve3_smem_bytes<1024>(ld, 0, false, NC, GC, 2);
-        PCY_CUDA(cudaFuncSetAttribute(k_resolve3<false, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
-        PCY_CUDA(cudaFuncSetAttribute(k_reattach3<false, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem));
+        res_smem = resolve3_smem_bytes<512>(ld, 0, false, NC, GC, 0);
+        rea_smem = resolve3_smem_bytes<512>(ld, 0, false, NC, GC, 2);
+        PCY_CUDA(cudaFuncSetAttribute(k_resolve3<false, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
+        PCY_CUDA(cudaFuncSetAttribute(k_reattach3<false, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem));
       }
     }
     if (getenv("PCY_GENERIC_RESOLVE")) nper = 0;
@@ -859,9 +885,23 @@ struct Engine {
     PCY_CUDA(cudaMemcpy(E.ctl, ctl_h, sizeof(EngCtl), cudaMemcpyHostToDevice));
     PCY_CUDA(cudaMemset(E.htab, 0xff, sizeof(int) * E.hcap));
     PCY_CUDA(cudaMemset(E.alive, 0, sizeof(int) * NC));
+    PCY_CUDA(cudaMemset(E.g_count, 0, sizeof(int) * GC));
+    PCY_CUDA(cudaMemset(E.g_base, 0, sizeof(int) * GC));
     PCY_CUDA(cudaMemset(E.s, 0, sizeof(double) * NC * ld));
     PCY_CUDA(cudaMemset(E.r, 0, sizeof(double) * NC * ld));
     return PCY_OK;
+  }
+
+  // Full-set K1: one DMMA contraction of the block against every allocated
+  // reference slot gives the parts matrix; the chain walk then only gathers
+  // parts of the visited groups' members.  Used once the tree is large.
+  bool full_set(const double* A, const int* aidx, long long M, cudaStream_t st, int* rc) {
+    *rc = PCY_OK;
+    const long long N = ctl_h->F_alloc;
+    if (!nper || N < 256 || getenv("PCY_NO_FULLSET")) return false;
+    if (!parts) { if ((*rc = alloc(parts, (long long)1024 * NC))) return false; }
+    *rc = pcy_launch_parts(A, aidx, ld, (int)M, E.r, ld, E.rn, (int)N, d, parts, N, st);
+    return true;
   }
 
   int grow_pending(cudaStream_t st) {
@@ -885,6 +925,7 @@ struct Engine {
       const long long nodes = ctl_h->F;
       k_rb_rank<<<(unsigned)((nslots + 255) / 256), 256, 0, st>>>(E, nslots); pcy_count_launch();
       k_rb_reset<<<(unsigned)((nslots + 255) / 256), 256, 0, st>>>(E, nslots); pcy_count_launch();
+      ctl_h->root_count = 0;   // fresh roots; the mirror refreshes at the next publication
       const bool prof = pcy_prof_enabled();
       if (prof) PCY_CUDA(cudaEventRecord(ev[3], st));
       int rc;
@@ -893,14 +934,22 @@ struct Engine {
         const int wpc = ld <= 512 ? 8 : (ld <= 2048 ? 4 : 2);
         while (off < nodes) {
           const long long nb = nodes - off < 1024 ? nodes - off : 1024;
-          k_rchain<<<(unsigned)((nb + wpc - 1) / wpc), wpc * 32, sizeof(double) * wpc * ld, st>>>(E, E.order + off, nb, chh, chr); pcy_count_launch();
+          int grc;
+          const bool use_p = full_set(E.r, E.order + off, nb, st, &grc);
+          if (grc) return grc;
+          k_rchain<<<(unsigned)((nb + wpc - 1) / wpc), wpc * 32, sizeof(double) * wpc * ld, st>>>(
+              E, E.order + off, nb, chh, chr, use_p ? parts : nullptr, ctl_h->F_alloc); pcy_count_launch();
+          if (nper == 101) {
+            grc = pcy_launch_gram(E.r, E.order + off, ld, (int)nb, E.r, E.order + off, ld, (int)nb, d, gram, nb, st);
+            if (grc) return grc;
+          }
           switch (nper) {
             case 1: k_reattach2<1><<<1, 32, res_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr); pcy_count_launch(); break;
             case 2: k_reattach2<2><<<1, 32, res_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr); pcy_count_launch(); break;
             case 4: k_reattach2<4><<<1, 32, res_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr); pcy_count_launch(); break;
             case 8: k_reattach2<8><<<1, 32, res_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr); pcy_count_launch(); break;
-            case 100: k_reattach3<true, 2048><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr); pcy_count_launch(); break;
-            default: k_reattach3<false, 1024><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr); pcy_count_launch(); break;
+            case 100: k_reattach3<true, 2048><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr, nullptr, 0, 0); pcy_count_launch(); break;
+            default: k_reattach3<false, 512><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr, gram, nb, 0); pcy_count_launch(); break;
           }
           PCY_LAUNCH_CHECK();
           rc = sync_ctl(st); if (rc) return rc;
@@ -942,6 +991,7 @@ struct Engine {
         const double* Xs = X + (off + start) * ld;
         const double* XSs = XS + off + start;
         const bool prof = pcy_prof_enabled();
+        int rc0 = PCY_OK;
         const long long* Ws = W ? W + off + start : nullptr;
         const int* Bs = BAD ? BAD + off + start : nullptr;
         const int wpc = ld <= 512 ? 8 : (ld <= 2048 ? 4 : 2);
@@ -949,7 +999,17 @@ struct Engine {
         if (!nper) { k_snapshot<<<64, 256, 0, st>>>(E); pcy_count_launch(); }
         if (prof) PCY_CUDA(cudaEventRecord(ev[0], st));
         if (nper) {
-          k_chain2<<<nblk, wpc * 32, sizeof(double) * wpc * ld, st>>>(E, Xs, XSs, Ws, nb - start, chh, chr); pcy_count_launch();
+          int grc;
+          const bool use_p = full_set(Xs, nullptr, nb - start, st, &grc);
+          if (grc) return grc;
+          k_chain2<<<nblk, wpc * 32, sizeof(double) * wpc * ld, st>>>(E, Xs, XSs, Ws, nb - start, chh, chr,
+                                                                       use_p ? parts : nullptr,
+                                                                       ctl_h->F_alloc); pcy_count_launch();
+          if (nper == 101) {
+            rc0 = pcy_launch_gram(Xs, nullptr, ld, (int)(nb - start), Xs, nullptr, ld, (int)(nb - start), d, gram,
+                                  nb - start, st);
+            if (rc0) return rc0;
+          }
         } else {
           k_chain<<<nblk, wpc * 32, sizeof(double) * wpc * ld, st>>>(E, Xs, XSs, nb - start); pcy_count_launch();
         }
@@ -959,8 +1019,8 @@ struct Engine {
           case 2: k_resolve2<2><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
           case 4: k_resolve2<4><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
           case 8: k_resolve2<8><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
-          case 100: k_resolve3<true, 2048><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
-          case 101: k_resolve3<false, 1024><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
+          case 100: k_resolve3<true, 2048><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr, nullptr, 0, 0); pcy_count_launch(); break;
+          case 101: k_resolve3<false, 512><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr, gram, nb - start, 0); pcy_count_launch(); break;
           default:
             k_resolve<<<1, 32, sizeof(double) * ld, st>>>(E, Xs, XSs, Ws, Bs, nb - start, 0, first_rem, countw); pcy_count_launch();
         }
@@ -1133,6 +1193,12 @@ int pcy_engine_counters(void* h, long long* out6) {
   Engine* e = (Engine*)h;
   out6[0] = e->ctl_h->cnt_levels; out6[1] = e->ctl_h->cnt_direct; out6[2] = e->ctl_h->cnt_demand;
   out6[3] = e->ctl_h->cnt_slow; out6[4] = e->ctl_h->cnt_items; out6[5] = e->ctl_h->max_depth;
+  return PCY_OK;
+}
+
+// Same counters summed over every engine destroyed so far in this process.
+int pcy_engine_counters_total(long long* out6) {
+  for (int k = 0; k < 6; ++k) out6[k] = g_counters[k].load();
   return PCY_OK;
 }
 

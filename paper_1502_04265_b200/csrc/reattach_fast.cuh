@@ -10,7 +10,7 @@
 // merge test for hosts touched in the launch.
 
 __global__ void k_rchain(EngDev E, const int* __restrict__ order, long long n, ChainHdr* __restrict__ H,
-                         ChainLvl* __restrict__ R) {
+                         ChainLvl* __restrict__ R, const double* __restrict__ P, long long ldp) {
   extern __shared__ double sm_x[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const long long i = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
@@ -31,7 +31,8 @@ __global__ void k_rchain(EngDev E, const int* __restrict__ order, long long n, C
   for (;;) {
     const int cnt = E.g_count[g], base = E.g_base[g];
     double bp; int bpos;
-    scan_members(E, E.arena + base, 0, cnt, xv, lane, bp, bpos);
+    if (P) scan_parts(P + i * ldp, E.arena + base, cnt, lane, bp, bpos);
+    else scan_members(E, E.arena + base, 0, cnt, xv, lane, bp, bpos);
     const int j = bpos < cnt ? E.arena[base + bpos] : -1;
     ChainLvl c = empty_level();
     c.part = bp; c.j = j; c.g = g;

@@ -58,7 +58,7 @@ __device__ __forceinline__ long long capacity(long long nn, double qv, double sn
 // ------------------------------------------------------------------- K1
 __global__ void k_chain2(EngDev E, const double* __restrict__ X, const double* __restrict__ XS,
                          const long long* __restrict__ W, long long n, ChainHdr* __restrict__ H,
-                         ChainLvl* __restrict__ R) {
+                         ChainLvl* __restrict__ R, const double* __restrict__ P, long long ldp) {
   extern __shared__ double sm_x[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const long long i = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
@@ -77,7 +77,8 @@ __global__ void k_chain2(EngDev E, const double* __restrict__ X, const double* _
   for (;;) {
     const int cnt = E.g_count[g], base = E.g_base[g];
     double bp; int bpos;
-    scan_members(E, E.arena + base, 0, cnt, xv, lane, bp, bpos);
+    if (P) scan_parts(P + i * ldp, E.arena + base, cnt, lane, bp, bpos);   // parts from the DMMA contraction
+    else scan_members(E, E.arena + base, 0, cnt, xv, lane, bp, bpos);
     const int j = bpos < cnt ? E.arena[base + bpos] : -1;
     ChainLvl c = empty_level();
     c.part = bp; c.j = j; c.g = g;

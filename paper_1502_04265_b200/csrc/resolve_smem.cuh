@@ -36,6 +36,7 @@ struct ResolveSmemT {
   int gkey[PCY_GMAP_SLOTS], ghead[PCY_GMAP_SLOTS], gtail[PCY_GMAP_SLOTS];
   int tid[PCY_NNEW_MAX], tgrp[PCY_NNEW_MAX], tchild[PCY_NNEW_MAX], tnext[PCY_NNEW_MAX];
   int tk[PCY_NNEW_MAX], tfirst[PCY_NNEW_MAX], tcnt[PCY_NNEW_MAX], tbase[PCY_NNEW_MAX], tcap[PCY_NNEW_MAX];
+  int titem[PCY_NNEW_MAX];   // Gram row of the item that placed the entry
   long long tw[PCY_NNEW_MAX];
   double trn[PCY_NNEW_MAX], tq[PCY_NNEW_MAX], tsn[PCY_NNEW_MAX];
   int modcount;
@@ -110,9 +111,25 @@ __device__ __forceinline__ void gchain_append(ResolveSmemT<MS>& S, unsigned* gbi
 template <bool TROWS, int MS>
 __device__ __forceinline__ void scan_new(const EngDev& E, const ResolveSmemT<MS>& S, const unsigned* gbits,
                                          const double* tref, int lds, const double* xsm, int g, int nnew,
-                                         int lane, double& bp, int& bj, int& bt) {
+                                         int lane, double& bp, int& bj, int& bt,
+                                         const double* gram, long long gld, long long gq) {
   if (!((gbits[g >> 5] >> (g & 31)) & 1u)) return;
   const int d = E.d, ld = E.ld;
+  if (!TROWS && gram) {
+    // same-launch members are rows of this block: their dots come from the
+    // block Gram computed on the tensor pipe before the launch
+    double np_ = INFINITY; int nt = 0x7fffffff;
+    for (int c0 = 0; c0 < nnew; c0 += 32) {
+      const int t = c0 + lane;
+      if (t < nnew && S.tgrp[t] == g) {
+        const double part = radd(S.trn[t], rmul(gram[(long long)S.titem[t] * gld + gq], -2.0));
+        if (part < np_) { np_ = part; nt = t; }
+      }
+    }
+    warp_argmin(np_, nt);
+    if (nt != 0x7fffffff && (np_ < bp || bj < 0)) { bp = np_; bt = nt; bj = S.tid[nt]; }
+    return;
+  }
   if (TROWS) {
     double np_ = INFINITY; int nt = 0x7fffffff;
     for (int c0 = 0; c0 < nnew; c0 += 32) {
@@ -183,7 +200,8 @@ __global__ void __launch_bounds__(32, 1) k_resolve3(EngDev E, const double* __re
                                                     const double* __restrict__ XS, const long long* __restrict__ W,
                                                     const int* __restrict__ BAD, long long n, long long first_rem,
                                                     int countw, int nnew_cap, const ChainHdr* __restrict__ H,
-                                                    const ChainLvl* __restrict__ R) {
+                                                    const ChainLvl* __restrict__ R, const double* __restrict__ gram,
+                                                    long long gld, long long goff) {
   extern __shared__ __align__(16) unsigned char smraw[];
   ResolveSmemT<MS>& S = *reinterpret_cast<ResolveSmemT<MS>*>(smraw);
   const int lane = threadIdx.x;
@@ -286,6 +304,7 @@ __global__ void __launch_bounds__(32, 1) k_resolve3(EngDev E, const double* __re
       for (int e = lane; e < ld; e += 32) { rr[e] = xsm[e]; sr[e] = rmul(fw, xsm[e]); }
       gchain_append<MS>(S, gbits, gg, t, lane);
       if (lane == 0) {
+        S.titem[t] = (int)(goff + i);
         S.tid[t] = (int)slot; S.tgrp[t] = gg; S.tchild[t] = -1; S.tw[t] = wopen;
         S.tq[t] = rmul(fw, xs); S.tsn[t] = rmul((double)(wopen * wopen), xs); S.trn[t] = xs;
         E.idx[slot] = nidx; E.alive[slot] = 1; E.child[slot] = -1;
@@ -365,7 +384,7 @@ __global__ void __launch_bounds__(32, 1) k_resolve3(EngDev E, const double* __re
         }
       }
       int bt = -1;
-      scan_new<TROWS, MS>(E, S, gbits, tref, lds, xsm, g, nnew, lane, bp, bj, bt);
+      scan_new<TROWS, MS>(E, S, gbits, tref, lds, xsm, g, nnew, lane, bp, bj, bt, gram, gld, goff + i);
       if (bj < 0 || radd(bp, xs) > radius) {
         if (do_open(g, L)) { status = ST_REBUILD; stop = i; remaining = rem; }
         break;
@@ -501,7 +520,8 @@ __global__ void __launch_bounds__(32, 1) k_resolve3(EngDev E, const double* __re
 template <bool TROWS, int MS>
 __global__ void __launch_bounds__(32, 1) k_reattach3(EngDev E, const int* __restrict__ order, long long n,
                                                      int nnew_cap, const ChainHdr* __restrict__ H,
-                                                     const ChainLvl* __restrict__ R) {
+                                                     const ChainLvl* __restrict__ R, const double* __restrict__ gram,
+                                                     long long gld, long long goff) {
   extern __shared__ __align__(16) unsigned char smraw[];
   ResolveSmemT<MS>& S = *reinterpret_cast<ResolveSmemT<MS>*>(smraw);
   const int lane = threadIdx.x;
@@ -591,7 +611,7 @@ __global__ void __launch_bounds__(32, 1) k_reattach3(EngDev E, const int* __rest
         }
       }
       int bt = -1;
-      scan_new<TROWS, MS>(E, S, gbits, tref, lds, xsm, g, nnew, lane, bp, bj, bt);
+      scan_new<TROWS, MS>(E, S, gbits, tref, lds, xsm, g, nnew, lane, bp, bj, bt, gram, gld, goff + i);
       if (bj < 0 || radd(bp, rsq_c) > radius) {
         // group.add(node): u keeps its statistics (coreset.py:403-406)
         const int t = nnew++;
@@ -601,6 +621,7 @@ __global__ void __launch_bounds__(32, 1) k_reattach3(EngDev E, const int* __rest
         }
         gchain_append<MS>(S, gbits, g, t, lane);
         if (lane == 0) {
+          S.titem[t] = (int)(goff + i);
           S.tid[t] = u; S.tgrp[t] = g; S.tchild[t] = -1;
           S.tw[t] = wu_c; S.tq[t] = qu_c; S.tsn[t] = snu_c; S.trn[t] = rsq_c;
         }

@@ -99,36 +99,51 @@ def gen_cfg3(seed: int = 2, n: int = 200_000, d: int = 1_024, clusters: int = 10
     return X
 
 
-def gen_cfg4(seed: int = 3, n: int = 11_620_300, d: int = 57) -> np.ndarray:
-    """BigCross-shaped: 500 components, centers U[0,100]^57, sigma U[0.5,5]
-    per component, 1% uniform outliers in [0,100]^57 (fp32)."""
+_CH4 = 262_144
+_CH5 = 8_192
+
+
+def _cfg4_params(seed: int, d: int):
     rng = np.random.default_rng(seed)
-    centers = rng.uniform(0.0, 100.0, size=(500, d))
-    sig = rng.uniform(0.5, 5.0, size=500)
-    X = np.empty((n, d), dtype=np.float32)
-    for a in range(0, n, 262_144):
-        b = min(n, a + 262_144)
-        m = b - a
+    return rng.uniform(0.0, 100.0, size=(500, d)), rng.uniform(0.5, 5.0, size=500)
+
+
+def gen_cfg4(seed: int = 3, n: int = 11_620_300, d: int = 57, rows: tuple | None = None) -> np.ndarray:
+    """BigCross-shaped: 500 components, centers U[0,100]^57, sigma U[0.5,5]
+    per component, 1% uniform outliers in [0,100]^57 (fp32).  Chunk c of
+    262,144 rows draws from PCG64([seed, c]), so any row range can be made
+    on its own (``rows=(a, b)``) -- each rank generates only its groups."""
+    centers, sig = _cfg4_params(seed, d)
+    a0, b0 = rows if rows is not None else (0, n)
+    X = np.empty((b0 - a0, d), dtype=np.float32)
+    for c in range(a0 // _CH4, (b0 + _CH4 - 1) // _CH4):
+        ca, cb = c * _CH4, min(n, (c + 1) * _CH4)
+        rng = np.random.default_rng([seed, c])
+        m = cb - ca
         lab = rng.integers(0, 500, size=m)
         blk = centers[lab] + rng.standard_normal((m, d)) * sig[lab, None]
         out = rng.random(m) < 0.01
         blk[out] = rng.uniform(0.0, 100.0, size=(int(out.sum()), d))
-        X[a:b] = blk
+        lo, hi = max(ca, a0), min(cb, b0)
+        X[lo - a0:hi - a0] = blk[lo - ca:hi - ca]
     return X
 
 
 def gen_cfg5(seed: int = 4, n: int = 1_000_000, d: int = 4_096, topics: int = 250,
-             active: int = 400, nnz: int = 205) -> np.ndarray:
+             active: int = 400, nnz: int = 205, rows: tuple | None = None) -> np.ndarray:
     """Sparse-valued dense rows: topic t (uniform of 250) active on 400 dims;
     ~5% of coordinates (205) nonzero at random positions among them with
-    values lognormal(0,1) times the topic profile; rows L2-normalised (fp32)."""
-    rng = np.random.default_rng(seed)
-    dims = np.stack([rng.choice(d, size=active, replace=False) for _ in range(topics)])
-    prof = rng.uniform(0.5, 1.5, size=(topics, active))
-    X = np.zeros((n, d), dtype=np.float32)
-    for a in range(0, n, 8_192):
-        b = min(n, a + 8_192)
-        m = b - a
+    values lognormal(0,1) times the topic profile; rows L2-normalised (fp32).
+    Chunk c of 8,192 rows draws from PCG64([seed, c]) (row ranges as cfg4)."""
+    rng0 = np.random.default_rng(seed)
+    dims = np.stack([rng0.choice(d, size=active, replace=False) for _ in range(topics)])
+    prof = rng0.uniform(0.5, 1.5, size=(topics, active))
+    a0, b0 = rows if rows is not None else (0, n)
+    X = np.zeros((b0 - a0, d), dtype=np.float32)
+    for c in range(a0 // _CH5, (b0 + _CH5 - 1) // _CH5):
+        ca, cb = c * _CH5, min(n, (c + 1) * _CH5)
+        rng = np.random.default_rng([seed, c])
+        m = cb - ca
         t = rng.integers(0, topics, size=m)
         pick = np.argsort(rng.random((m, active)), axis=1)[:, :nnz]
         cols = dims[t[:, None], pick]
@@ -136,11 +151,23 @@ def gen_cfg5(seed: int = 4, n: int = 1_000_000, d: int = 4_096, topics: int = 25
         vals /= np.sqrt((vals * vals).sum(axis=1, keepdims=True))
         blk = np.zeros((m, d), dtype=np.float32)
         np.put_along_axis(blk, cols, vals.astype(np.float32), axis=1)
-        X[a:b] = blk
+        lo, hi = max(ca, a0), min(cb, b0)
+        X[lo - a0:hi - a0] = blk[lo - ca:hi - ca]
     return X
 
 
 GENERATORS = {"cfg1": gen_cfg1, "cfg2": gen_cfg2, "cfg3": gen_cfg3, "cfg4": gen_cfg4, "cfg5": gen_cfg5}
+
+
+def generate_rows(name: str, a: int, b: int, n: int | None = None) -> np.ndarray:
+    """Rows [a, b) of a config's stream (cfg4/cfg5 without generating the rest)."""
+    cfg = CONFIGS[name]
+    total = cfg.n if n is None else n
+    if name == "cfg4":
+        return gen_cfg4(cfg.seed, n=total, rows=(a, b))
+    if name == "cfg5":
+        return gen_cfg5(cfg.seed, n=total, rows=(a, b))
+    return generate(name, n)[a:b]
 
 
 def generate(name: str, n: int | None = None) -> np.ndarray:
