@@ -756,7 +756,7 @@ struct Engine {
   double* parts = nullptr;                             // full-set parts matrix (1024 x NC)
   double* gram = nullptr;                              // block Gram (K3 with rows in HBM)
   int nper = 0;          // resolve kernel: 1..8 register rows, 100/101 shared-memory rows, 0 generic
-  int nnew_cap = 0;
+  int nnew_cap = 0, crows = 0;
   size_t res_smem = 0, rea_smem = 0;
   std::vector<void*> allocs;
 
@@ -841,21 +841,24 @@ struct Engine {
     PCY_CUDA(cudaFuncSetAttribute(k_rchain, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
     if (ld <= 256 && !getenv("PCY_SMEM_RESOLVE")) {
       nper = ld <= 32 ? 1 : ld <= 64 ? 2 : ld <= 128 ? 4 : 8;
-      const size_t base = resolve_smem_bytes(ld, 0, NC, GC);
+      crows = 0;   // touched-row cache: measured neutral on cfg2/cfg4 (demand loads are not the bound)
+      if (const char* cr = getenv("PCY_CROWS")) crows = atoi(cr);
+      const size_t base = resolve_smem_bytes(ld, 0, NC, GC, crows);
       long long cap = maxsm > base ? (long long)((maxsm - base) / (sizeof(double) * (2 * ld + 1))) : 0;
       if (cap > PCY_NNEW_MAX) cap = PCY_NNEW_MAX;
       nnew_cap = (int)cap;
-      res_smem = rea_smem = resolve_smem_bytes(ld, nnew_cap, NC, GC);
+      res_smem = resolve_smem_bytes(ld, nnew_cap, NC, GC, crows);
+      rea_smem = resolve_smem_bytes(ld, nnew_cap, NC, GC, 0);
       if (nnew_cap < 8) nper = 0;
       switch (nper) {
         case 1: PCY_CUDA(cudaFuncSetAttribute(k_resolve2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
-                PCY_CUDA(cudaFuncSetAttribute(k_reattach2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem)); break;
+                PCY_CUDA(cudaFuncSetAttribute(k_reattach2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem)); break;
         case 2: PCY_CUDA(cudaFuncSetAttribute(k_resolve2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
-                PCY_CUDA(cudaFuncSetAttribute(k_reattach2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem)); break;
+                PCY_CUDA(cudaFuncSetAttribute(k_reattach2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem)); break;
         case 4: PCY_CUDA(cudaFuncSetAttribute(k_resolve2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
-                PCY_CUDA(cudaFuncSetAttribute(k_reattach2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem)); break;
+                PCY_CUDA(cudaFuncSetAttribute(k_reattach2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem)); break;
         case 8: PCY_CUDA(cudaFuncSetAttribute(k_resolve2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
-                PCY_CUDA(cudaFuncSetAttribute(k_reattach2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem)); break;
+                PCY_CUDA(cudaFuncSetAttribute(k_reattach2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem)); break;
         default: break;
       }
     }
@@ -944,10 +947,10 @@ struct Engine {
             if (grc) return grc;
           }
           switch (nper) {
-            case 1: k_reattach2<1><<<1, 32, res_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr); pcy_count_launch(); break;
-            case 2: k_reattach2<2><<<1, 32, res_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr); pcy_count_launch(); break;
-            case 4: k_reattach2<4><<<1, 32, res_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr); pcy_count_launch(); break;
-            case 8: k_reattach2<8><<<1, 32, res_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr); pcy_count_launch(); break;
+            case 1: k_reattach2<1><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr); pcy_count_launch(); break;
+            case 2: k_reattach2<2><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr); pcy_count_launch(); break;
+            case 4: k_reattach2<4><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr); pcy_count_launch(); break;
+            case 8: k_reattach2<8><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr); pcy_count_launch(); break;
             case 100: k_reattach3<true, 2048><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr, nullptr, 0, 0); pcy_count_launch(); break;
             default: k_reattach3<false, 512><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr, gram, nb, 0); pcy_count_launch(); break;
           }
@@ -1015,10 +1018,10 @@ struct Engine {
         }
         if (prof) PCY_CUDA(cudaEventRecord(ev[1], st));
         switch (nper) {
-          case 1: k_resolve2<1><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
-          case 2: k_resolve2<2><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
-          case 4: k_resolve2<4><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
-          case 8: k_resolve2<8><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
+          case 1: k_resolve2<1><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr, crows); pcy_count_launch(); break;
+          case 2: k_resolve2<2><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr, crows); pcy_count_launch(); break;
+          case 4: k_resolve2<4><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr, crows); pcy_count_launch(); break;
+          case 8: k_resolve2<8><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr, crows); pcy_count_launch(); break;
           case 100: k_resolve3<true, 2048><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr, nullptr, 0, 0); pcy_count_launch(); break;
           case 101: k_resolve3<false, 512><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr, gram, nb - start, 0); pcy_count_launch(); break;
           default:
@@ -1034,6 +1037,12 @@ struct Engine {
           const long long done = ctl_h->status == ST_DONE ? nb - start : ctl_h->stop + (ctl_h->status == ST_FULL ? 0 : 1);
           pcy_prof_add(PCY_PROF_CHAIN, t1, nb - start);
           pcy_prof_add(PCY_PROF_RESOLVE, t2, done);
+          static FILE* trace = getenv("PCY_TRACE_K3") ? fopen(getenv("PCY_TRACE_K3"), "a") : nullptr;
+          if (trace) {
+            fprintf(trace, "%lld %.4f %.4f %d %lld %lld %lld %lld\n", done, t1, t2, ctl_h->status, ctl_h->F,
+                    ctl_h->cnt_slow, ctl_h->cnt_levels, ctl_h->root_count);
+            fflush(trace);
+          }
         }
         const int status = ctl_h->status;
         if (status == ST_DONE) break;
@@ -1193,6 +1202,9 @@ int pcy_engine_counters(void* h, long long* out6) {
   Engine* e = (Engine*)h;
   out6[0] = e->ctl_h->cnt_levels; out6[1] = e->ctl_h->cnt_direct; out6[2] = e->ctl_h->cnt_demand;
   out6[3] = e->ctl_h->cnt_slow; out6[4] = e->ctl_h->cnt_items; out6[5] = e->ctl_h->max_depth;
+  if (getenv("PCY_DEBUG_COUNTERS"))
+    fprintf(stderr, "[pcy] demand loads on the fast path %lld, nodes touched only by a new child %lld\n",
+            e->ctl_h->cnt_dem_fast, e->ctl_h->cnt_touch_child);
   return PCY_OK;
 }
 

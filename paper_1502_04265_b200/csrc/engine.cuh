@@ -33,7 +33,7 @@ struct EngCtl {
   long long max_depth;
   // instrumentation (k_resolve2): levels walked, direct scans, demand row
   // loads, full capacity evaluations, items resolved
-  long long cnt_levels, cnt_direct, cnt_demand, cnt_slow, cnt_items;
+  long long cnt_levels, cnt_direct, cnt_demand, cnt_slow, cnt_items, cnt_dem_fast, cnt_touch_child;
   long long root_count, root_base;   // group 0 (copied by k_publish for the host)
   long long seq;          // publication sequence number (mapped host mirror)
 };

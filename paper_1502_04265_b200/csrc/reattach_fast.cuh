@@ -170,8 +170,14 @@ __global__ void __launch_bounds__(32, 1) k_reattach2(EngDev E, const int* __rest
           const int t = c0 + lane;
           if (t < nnew && S.tgrp[t] == g) {
             const double* rr = tref + (long long)t * lds;
-            double acc = 0.0;
-            for (int e = 0; e < d; ++e) acc = fma(rr[e], xsm[e], acc);
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;   // 4 chains: ILP over d
+            int e = 0;
+            for (; e + 3 < d; e += 4) {
+              a0 = fma(rr[e], xsm[e], a0); a1 = fma(rr[e + 1], xsm[e + 1], a1);
+              a2 = fma(rr[e + 2], xsm[e + 2], a2); a3 = fma(rr[e + 3], xsm[e + 3], a3);
+            }
+            for (; e < d; ++e) a0 = fma(rr[e], xsm[e], a0);
+            const double acc = (a0 + a1) + (a2 + a3);
             const double part = radd(S.trn[t], rmul(acc, -2.0));
             if (part < np_) { np_ = part; nt = t; }
           }

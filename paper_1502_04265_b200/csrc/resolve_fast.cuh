@@ -126,14 +126,16 @@ struct ResolveSmem {
   int tk[PCY_NNEW_MAX], tfirst[PCY_NNEW_MAX], tcnt[PCY_NNEW_MAX], tbase[PCY_NNEW_MAX], tcap[PCY_NNEW_MAX];
   long long tw[PCY_NNEW_MAX];
   double trn[PCY_NNEW_MAX], tq[PCY_NNEW_MAX], tsn[PCY_NNEW_MAX];
-  int modcount;
+  short mrow[PCY_MOD_SLOTS];   // row-cache slot of a touched node (-1: none)
+  int modcount, ncache;
 };
 // dynamic tail: double xsm[ld]; double tref[nnew][ld|1]; double ts[nnew][ld];
-//               unsigned mbits[NC/32+1]; unsigned gbits[GC/32+1]
+//               unsigned mbits[NC/32+1]; unsigned gbits[GC/32+1]; double cpool[crows][ld]
 
-__host__ __device__ inline size_t resolve_smem_bytes(int ld, int nnew, long long NC, long long GC) {
+__host__ __device__ inline size_t resolve_smem_bytes(int ld, int nnew, long long NC, long long GC, int crows = 0) {
   return ((sizeof(ResolveSmem) + 15) & ~size_t(15)) + sizeof(double) * ((size_t)ld + (size_t)nnew * ((size_t)(ld | 1) + ld)) +
-         sizeof(unsigned) * (size_t)(NC / 32 + 1 + GC / 32 + 1);
+         ((sizeof(unsigned) * (size_t)(NC / 32 + 1 + GC / 32 + 1) + 15) & ~size_t(15)) +
+         sizeof(double) * (size_t)crows * ld;
 }
 
 __device__ __forceinline__ int map_slot(int id) { return (int)(((unsigned)id * 2654435761u) >> 21) & (PCY_MOD_SLOTS - 1); }
@@ -154,7 +156,7 @@ __device__ __forceinline__ int map_put(ResolveSmem& S, unsigned* mbits, int id, 
   int s = map_slot(id);
   while (S.mkey[s] >= 0 && S.mkey[s] != id) s = (s + 1) & (PCY_MOD_SLOTS - 1);
   if (lane == 0) {
-    if (S.mkey[s] < 0) { S.modcount++; mbits[id >> 5] |= 1u << (id & 31); }
+    if (S.mkey[s] < 0) { S.modcount++; mbits[id >> 5] |= 1u << (id & 31); S.mrow[s] = -1; }
     S.mkey[s] = id; S.mw[s] = w; S.mq[s] = q; S.msn[s] = sn; S.mchild[s] = child;
   }
   __syncwarp();
@@ -206,7 +208,7 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
                                                     const double* __restrict__ XS, const long long* __restrict__ W,
                                                     const int* __restrict__ BAD, long long n, long long first_rem,
                                                     int countw, int nnew_cap, const ChainHdr* __restrict__ H,
-                                                    const ChainLvl* __restrict__ R) {
+                                                    const ChainLvl* __restrict__ R, int crows) {
   extern __shared__ __align__(16) unsigned char smraw[];
   ResolveSmem& S = *reinterpret_cast<ResolveSmem*>(smraw);
   const int lane = threadIdx.x;
@@ -219,12 +221,14 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
   const int mwords = (int)(E.NC / 32 + 1);
   unsigned* gbits = mbits + mwords;
   const int gwords = (int)(E.GC / 32 + 1);
+  double* cpool = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(mbits) +
+                                            ((sizeof(unsigned) * (size_t)(mwords + gwords) + 15) & ~size_t(15)));
   EngCtl* C = E.ctl;
   const long long m = E.m;
   const double T = C->T;
   long long F = C->F, Falloc = C->F_alloc, freen = C->free_n, Galloc = C->G_alloc;
   long long Aalloc = C->A_alloc, nidx = C->next_index, totw = C->total_w, maxdepth = C->max_depth;
-  long long c_lv = 0, c_dir = 0, c_dem = 0, c_slow = 0, c_it = 0;
+  long long c_lv = 0, c_dir = 0, c_dem = 0, c_slow = 0, c_it = 0, c_demf = 0, c_tch = 0;
   const long long G0 = Galloc;
   int status = ST_DONE, err = 0; long long stop = n, remaining = 0;
 
@@ -232,7 +236,7 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
   for (int s2 = lane; s2 < PCY_GMAP_SLOTS; s2 += 32) S.gkey[s2] = -1;
   for (int s2 = lane; s2 < mwords; s2 += 32) mbits[s2] = 0u;
   for (int s2 = lane; s2 < gwords; s2 += 32) gbits[s2] = 0u;
-  if (lane == 0) S.modcount = 0;
+  if (lane == 0) { S.modcount = 0; S.ncache = 0; }
   int nnew = 0;
   int free_top = freen > 0 ? E.free_ids[freen - 1] : -1;
 
@@ -289,6 +293,33 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
     __syncwarp();
     int lastmod = -1, nmod = 0;
     int modl[4] = {-1, -1, -1, -1};   // snapshot nodes rewritten by this item
+    // current row of snapshot node bj into pr: row cache (touched nodes) or HBM
+    auto fetch_row = [&](int bj, int ms_) {
+      if (bj == prnode) return;
+      const int slot = ms_ >= 0 ? (int)S.mrow[ms_] : -1;
+      if (slot >= 0) {
+#pragma unroll
+        for (int k = 0; k < NPER; ++k) { const int e = lane + 32 * k; pr[k] = e < d ? cpool[(long long)slot * ld + e] : 0.0; }
+      } else {
+        load_row<NPER>(pr, E.s + (long long)bj * ld, d, lane);
+        ++c_dem;
+      }
+      prnode = bj;
+    };
+    // keep the just-updated row (pr) of map entry ms_ in the row cache
+    auto cache_row = [&](int ms_) {
+      int slot = S.mrow[ms_];
+      if (slot < 0 && S.ncache < crows) {
+        slot = S.ncache;
+        __syncwarp();
+        if (lane == 0) { S.mrow[ms_] = (short)slot; S.ncache = slot + 1; }
+      }
+      if (slot >= 0) {
+#pragma unroll
+        for (int k = 0; k < NPER; ++k) { const int e = lane + 32 * k; if (e < d) cpool[(long long)slot * ld + e] = pr[k]; }
+      }
+      __syncwarp();
+    };
     // _open (coreset.py:329-335, :374-377) into group g at level L; returns true when full (rebuild)
     auto do_open = [&](int g, int L) -> bool {
         const bool full = F >= m;
@@ -342,12 +373,13 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
           const int bj = rp.j;
           const long long take = rp.take;
           const double ft = (double)take;
-          if (bj != prnode) { load_row<NPER>(pr, E.s + (long long)bj * ld, d, lane); prnode = bj; ++c_dem; }
+          if (bj != prnode) ++c_demf;
+          fetch_row(bj, -1);
 #pragma unroll
           for (int k = 0; k < NPER; ++k) pr[k] = take == 1 ? radd(pr[k], xr[k]) : radd(pr[k], rmul(ft, xr[k]));
           store_row<NPER>(E.s + (long long)bj * ld, pr, d, lane);
           const long long nw2 = rp.w + take;
-          map_put(S, mbits, bj, nw2, rp.nq, rp.nsn, rp.child, lane);
+          cache_row(map_put(S, mbits, bj, nw2, rp.nq, rp.nsn, rp.child, lane));
           if (lane == 0) { E.w[bj] = nw2; E.q[bj] = rp.nq; E.sn[bj] = rp.nsn; }
           modl[0] = bj; nmod = 1; lastmod = bj;
           rem = 0;
@@ -397,8 +429,14 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
           const int t = c0 + lane;
           if (t < nnew && S.tgrp[t] == g) {
             const double* rr = tref + (long long)t * lds;
-            double acc = 0.0;
-            for (int e = 0; e < d; ++e) acc = fma(rr[e], xsm[e], acc);
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;   // 4 chains: ILP over d
+            int e = 0;
+            for (; e + 3 < d; e += 4) {
+              a0 = fma(rr[e], xsm[e], a0); a1 = fma(rr[e + 1], xsm[e + 1], a1);
+              a2 = fma(rr[e + 2], xsm[e + 2], a2); a3 = fma(rr[e + 3], xsm[e + 3], a3);
+            }
+            for (; e < d; ++e) a0 = fma(rr[e], xsm[e], a0);
+            const double acc = (a0 + a1) + (a2 + a3);
             const double part = radd(S.trn[t], rmul(acc, -2.0));
             if (part < np_) { np_ = part; nt = t; }
           }
@@ -433,7 +471,7 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
           else { nn = E.w[bj]; qv = E.q[bj]; snv = E.sn[bj]; }
           if (!touched && li >= 0) dt = S.rb[cur][li].dot;
           else {
-            if (bj != prnode) { load_row<NPER>(pr, E.s + (long long)bj * ld, d, lane); prnode = bj; ++c_dem; }
+            fetch_row(bj, ms);
             dt = reg_dot<NPER>(pr, xr);
           }
         }
@@ -457,14 +495,16 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
           if (lane == 0) { S.tw[bt] = nw2; S.tq[bt] = nq; S.tsn[bt] = nsn; }
           __syncwarp();
         } else {
-          if (bj != prnode) { load_row<NPER>(pr, E.s + (long long)bj * ld, d, lane); prnode = bj; ++c_dem; }
+          if (touched && ms < 0) ms = map_find(S, bj);
+          fetch_row(bj, touched ? ms : -1);
 #pragma unroll
           for (int k = 0; k < NPER; ++k) pr[k] = take == 1 ? radd(pr[k], xr[k]) : radd(pr[k], rmul(ft, xr[k]));
           store_row<NPER>(E.s + (long long)bj * ld, pr, d, lane);
           int child_now;
-          if (touched) { if (ms < 0) ms = map_find(S, bj); child_now = S.mchild[ms]; }
+          if (touched) child_now = S.mchild[ms];
           else child_now = li >= 0 ? S.rb[cur][li].child : E.child[bj];
           ms = map_put(S, mbits, bj, nw2, nq, nsn, child_now, lane);
+          cache_row(ms);
           if (lane == 0) { E.w[bj] = nw2; E.q[bj] = nq; E.sn[bj] = nsn; }
           if (nmod < 4) modl[nmod] = bj;
           ++nmod;
@@ -491,7 +531,7 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
           c = (int)Galloc++;
           if (lane == 0) { E.g_count[c] = 0; E.g_cap[c] = 0; E.g_base[c] = 0; E.child[bj] = c; }
           if (tnow) { if (lane == 0) S.mchild[ms] = c; __syncwarp(); }
-          else ms = map_put(S, mbits, bj, nn, qv, snv, c, lane);   // untouched: current stats
+          else { ms = map_put(S, mbits, bj, nn, qv, snv, c, lane); ++c_tch; }   // untouched: current stats
         }
       }
       g = c;
@@ -586,6 +626,6 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
     C->A_alloc = Aalloc; C->next_index = nidx; C->total_w = totw; C->max_depth = maxdepth;
     C->status = status; C->err = err; C->stop = stop; C->remaining = remaining;
     C->cnt_levels += c_lv; C->cnt_direct += c_dir; C->cnt_demand += c_dem; C->cnt_slow += c_slow;
-    C->cnt_items += c_it;
+    C->cnt_items += c_it; C->cnt_dem_fast += c_demf; C->cnt_touch_child += c_tch;
   }
 }
