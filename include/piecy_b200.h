@@ -110,7 +110,7 @@ int pcy_project(const double* A, long long rows, int cols, const double* V, int 
 int pcy_scale_rows_sqrtw(const double* A, const long long* w, long long rows, int cols, double* out,
                          void* stream);
 
-/* fp64 GEMM on the DMMA pipe: C = alpha op(A) op(B) + beta C (row-major). */
+/* Plain fp64 GEMM (cuBLAS): C = alpha op(A) op(B) + beta C (row-major). */
 int pcy_dgemm(int M, int N, int K, double alpha, const double* A, long long lda, int ta,
               const double* B, long long ldb, int tb, double beta, double* C, long long ldc,
               void* stream);

@@ -20,6 +20,14 @@ cudaError_t pcy_spin_sync(cudaStream_t st);
 // Device -> host copy of a small result through a thread-local pinned
 // staging buffer, completed with pcy_spin_sync.
 cudaError_t pcy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t st);
+// cudaMallocAsync from the device's default pool, whose memory is kept
+// resident (release threshold raised once per device): per-call scratch of
+// the projection and the engine then never re-maps physical memory.
+cudaError_t pcy_malloc_async_raw(void** p, size_t bytes, cudaStream_t st);
+template <class T>
+inline cudaError_t pcy_malloc_async(T** p, size_t bytes, cudaStream_t st) {
+  return pcy_malloc_async_raw((void**)p, bytes, st);
+}
 // DMMA distance contraction (distance.cu)
 int pcy_launch_gram(const double* A, const int* aidx, long long lda, int M, const double* B, const int* bidx,
                     long long ldb, int N, int K, double* C, long long ldc, cudaStream_t st);

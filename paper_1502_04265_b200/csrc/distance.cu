@@ -209,8 +209,8 @@ extern "C" int pcy_nearest_refs(const double* X, long long ldx, int M, const dou
   cudaStream_t st = (cudaStream_t)stream;
   const int ntiles = (N + DBN - 1) / DBN;
   double* pp = nullptr; int* pc = nullptr;
-  PCY_CUDA(cudaMallocAsync(&pp, sizeof(double) * (size_t)M * (ntiles > 0 ? ntiles : 1), st));
-  PCY_CUDA(cudaMallocAsync(&pc, sizeof(int) * (size_t)M * (ntiles > 0 ? ntiles : 1), st));
+  PCY_CUDA(pcy_malloc_async(&pp, sizeof(double) * (size_t)M * (ntiles > 0 ? ntiles : 1), st));
+  PCY_CUDA(pcy_malloc_async(&pc, sizeof(int) * (size_t)M * (ntiles > 0 ? ntiles : 1), st));
   int rc = pcy_launch_nearest(X, nullptr, ldx, M, R, ridx, ldr, rn, N, K, pp, pc, out_pos, out_part, st);
   cudaFreeAsync(pp, st);
   cudaFreeAsync(pc, st);

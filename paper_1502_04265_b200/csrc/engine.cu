@@ -51,6 +51,20 @@ cudaError_t pcy_spin_sync(cudaStream_t st) {
     if (e != cudaErrorNotReady) return e;
   }
 }
+cudaError_t pcy_malloc_async_raw(void** p, size_t bytes, cudaStream_t st) {
+  static std::once_flag once[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::call_once(once[dev & 63], [dev] {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      unsigned long long keep = ~0ULL;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  });
+  return cudaMallocAsync(p, bytes, st);
+}
+
 cudaError_t pcy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t st) {
   static thread_local void* buf = nullptr;
   static thread_local size_t cap = 0;

@@ -303,9 +303,9 @@ int pcy_kmeanspp(const double* P, const double* w, long long n, int d, int k, in
   if (n < 1 || k < 1 || d < 1 || reps < 1) { pcy_set_error("kmeanspp: bad sizes"); return PCY_EINVAL; }
   cudaStream_t st = (cudaStream_t)stream;
   double *best = nullptr, *mass = nullptr; int* picks = nullptr;
-  PCY_CUDA(cudaMallocAsync(&best, sizeof(double) * n * reps, st));
-  PCY_CUDA(cudaMallocAsync(&mass, sizeof(double) * n * reps, st));
-  PCY_CUDA(cudaMallocAsync(&picks, sizeof(int) * k * reps, st));
+  PCY_CUDA(pcy_malloc_async(&best, sizeof(double) * n * reps, st));
+  PCY_CUDA(pcy_malloc_async(&mass, sizeof(double) * n * reps, st));
+  PCY_CUDA(pcy_malloc_async(&picks, sizeof(int) * k * reps, st));
   const size_t sm = sizeof(double) * d;
   if (sm > 48 * 1024) PCY_CUDA(cudaFuncSetAttribute(k_seed, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   k_seed<<<reps, KM_THREADS, sm, st>>>(P, w, n, d, k, U, centers, best, mass, picks); pcy_count_launch();
@@ -329,13 +329,13 @@ int pcy_lloyd(const double* P, const double* w, long long n, int d, int k, int r
   if (n < 1 || k < 1 || d < 1 || reps < 1) { pcy_set_error("lloyd: bad sizes"); return PCY_EINVAL; }
   cudaStream_t st = (cudaStream_t)stream;
   double *pn = nullptr, *cn = nullptr, *best = nullptr, *cost = nullptr; int *assign = nullptr, *counts = nullptr, *active = nullptr;
-  PCY_CUDA(cudaMallocAsync(&pn, sizeof(double) * n, st));
-  PCY_CUDA(cudaMallocAsync(&cn, sizeof(double) * k * reps, st));
-  PCY_CUDA(cudaMallocAsync(&best, sizeof(double) * n * reps, st));
-  PCY_CUDA(cudaMallocAsync(&assign, sizeof(int) * n * reps, st));
-  PCY_CUDA(cudaMallocAsync(&counts, sizeof(int) * k * reps, st));
-  PCY_CUDA(cudaMallocAsync(&cost, sizeof(double) * reps, st));
-  PCY_CUDA(cudaMallocAsync(&active, sizeof(int) * reps, st));
+  PCY_CUDA(pcy_malloc_async(&pn, sizeof(double) * n, st));
+  PCY_CUDA(pcy_malloc_async(&cn, sizeof(double) * k * reps, st));
+  PCY_CUDA(pcy_malloc_async(&best, sizeof(double) * n * reps, st));
+  PCY_CUDA(pcy_malloc_async(&assign, sizeof(int) * n * reps, st));
+  PCY_CUDA(pcy_malloc_async(&counts, sizeof(int) * k * reps, st));
+  PCY_CUDA(pcy_malloc_async(&cost, sizeof(double) * reps, st));
+  PCY_CUDA(pcy_malloc_async(&active, sizeof(int) * reps, st));
   std::vector<int> act(reps, 1);
   std::vector<double> prev(reps, INFINITY), hc(reps);
   for (int r = 0; r < reps; ++r) iters_out[r] = 0;
@@ -378,11 +378,11 @@ int pcy_weighted_cost(const double* P, const double* w, long long n, int d, int 
   if (n < 1) { for (int r = 0; r < reps; ++r) costs[r] = 0.0; return PCY_OK; }
   cudaStream_t st = (cudaStream_t)stream;
   double *pn = nullptr, *cn = nullptr, *best = nullptr, *cost = nullptr; int *assign = nullptr;
-  PCY_CUDA(cudaMallocAsync(&pn, sizeof(double) * n, st));
-  PCY_CUDA(cudaMallocAsync(&cn, sizeof(double) * k * reps, st));
-  PCY_CUDA(cudaMallocAsync(&best, sizeof(double) * n * reps, st));
-  PCY_CUDA(cudaMallocAsync(&assign, sizeof(int) * n * reps, st));
-  PCY_CUDA(cudaMallocAsync(&cost, sizeof(double) * reps, st));
+  PCY_CUDA(pcy_malloc_async(&pn, sizeof(double) * n, st));
+  PCY_CUDA(pcy_malloc_async(&cn, sizeof(double) * k * reps, st));
+  PCY_CUDA(pcy_malloc_async(&best, sizeof(double) * n * reps, st));
+  PCY_CUDA(pcy_malloc_async(&assign, sizeof(int) * n * reps, st));
+  PCY_CUDA(pcy_malloc_async(&cost, sizeof(double) * reps, st));
   k_rownorm<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(P, n, d, pn); pcy_count_launch();
   k_rownorm<<<(unsigned)((k * reps + 7) / 8), 256, 0, st>>>(centers, (long long)k * reps, d, cn); pcy_count_launch();
   k_assign<<<dim3((unsigned)((n + 7) / 8), reps), 256, 0, st>>>(P, pn, n, d, k, centers, cn, nullptr, assign, best); pcy_count_launch();

@@ -7,151 +7,79 @@
 //   project                  :209-221   A V V^T
 //   weighted_best_fit        :231-250   rows scaled by sqrt(w)
 // Building blocks:
-//   k_dgemm   -- tiled GEMM on the fp64 tensor pipe (mma.sync m8n8k4 -> DMMA)
-//   CholeskyQR2 (k_chol_inv): orthonormal basis of the same span as
-//                LAPACK's Householder Q (only the span reaches the result;
-//                SURVEY.md §7 hard part 5)
-//   k_jacobi  -- one-sided (Hestenes) Jacobi SVD, tournament ordering
+//   gemm      -- plain fp64 GEMMs of the range finder on cuBLAS (library GEMM)
+//   CholeskyQR2 (k_gram_prep, k_chol_diag + cuBLAS trsm/syrk, blocked):
+//                orthonormal basis of the same span as LAPACK's Householder Q
+//                (only the span reaches the result; SURVEY.md §7 hard part 5),
+//                k_cgs2 when the Gram factorisation breaks down
+//   k_jacobi  -- one-sided (Hestenes) Jacobi SVD, tournament ordering,
+//                persistent cooperative grid (grid barrier per round)
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <algorithm>
 #include <vector>
+#include <cublas_v2.h>
 #include "common.cuh"
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 
 namespace {
 
-// ------------------------------------------------------------------- GEMM
-// C[M x N] = alpha * op(A) * op(B) + beta * C, row-major with leading dims.
-// op(A) is M x K: A[m*lda + k] (ta=0) or A[k*lda + m] (ta=1).
-// op(B) is K x N: B[k*ldb + n] (tb=0) or B[n*ldb + k] (tb=1).
-constexpr int GBM = 64, GBN = 64, GBK = 16;
-
-__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
-}
-
-__global__ void __launch_bounds__(128) k_dgemm(int M, int N, int K, double alpha,
-                                               const double* __restrict__ A, long long lda, int ta,
-                                               const double* __restrict__ B, long long ldb, int tb,
-                                               double beta, double* __restrict__ C, long long ldc) {
-  __shared__ double As[GBM][GBK + 4];
-  __shared__ double Bs[GBK][GBN + 4];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, t4 = lane & 3;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
-  const long long m0 = (long long)blockIdx.y * GBM, n0 = (long long)blockIdx.x * GBN;
-  double acc[4][4][2];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) { acc[i][j][0] = 0.0; acc[i][j][1] = 0.0; }
-
-  for (int k0 = 0; k0 < K; k0 += GBK) {
-    // A tile (64 x 16): 1024 elements, 8 per thread
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const int e = tid + r * 128;
-      int mm, kk;
-      if (!ta) { mm = e / GBK; kk = e % GBK; } else { kk = e / GBM; mm = e % GBM; }
-      const long long gm = m0 + mm; const int gk = k0 + kk;
-      double v = 0.0;
-      if (gm < M && gk < K) v = ta ? A[(long long)gk * lda + gm] : A[gm * lda + gk];
-      As[mm][kk] = v;
-    }
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const int e = tid + r * 128;
-      int nn, kk;
-      if (!tb) { kk = e / GBN; nn = e % GBN; } else { nn = e / GBK; kk = e % GBK; }
-      const long long gn = n0 + nn; const int gk = k0 + kk;
-      double v = 0.0;
-      if (gn < N && gk < K) v = tb ? B[gn * ldb + gk] : B[(long long)gk * ldb + gn];
-      Bs[kk][nn] = v;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int ks = 0; ks < GBK; ks += 4) {
-      double af[4], bf[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = As[wm + i * 8 + g][ks + t4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) bf[j] = Bs[ks + t4][wn + j * 8 + g];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-    }
-    __syncthreads();
+// ------------------------------------------------------------ Cholesky
+// Blocked Cholesky pieces (column-major lower, as LAPACK potrf 'L'; the
+// Gram is symmetric so its row-major buffer is its column-major buffer).
+// k_gram_prep: add the shift to the diagonal, and in the second CholeskyQR
+// pass check that the Gram of the already orthonormalised basis is close to I
+// (otherwise the first pass lost orthogonality).  Resets *status.
+__global__ void k_gram_prep(double* __restrict__ G, int r, double shift, int expect_identity,
+                            int* __restrict__ status) {
+  const long long n = (long long)r * r;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const bool diag = (e / r) == (e % r);
+    if (expect_identity && fabs(G[e] - (diag ? 1.0 : 0.0)) > 1e-3) atomicOr(status, 1);
+    if (diag && shift != 0.0) G[e] += shift;
   }
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const long long gm = m0 + wm + i * 8 + g, gn = n0 + wn + j * 8 + 2 * t4 + h;
-        if (gm < M && gn < N) {
-          double v = alpha * acc[i][j][h];
-          if (beta != 0.0) v += beta * C[gm * ldc + gn];
-          C[gm * ldc + gn] = v;
-        }
-      }
 }
 
-// ------------------------------------------------------- Cholesky inverse
-// G (r x r, row-major, SPD) = L L^T.  Writes Linv (row-major lower) so that
-// Y * Linv^T has orthonormal columns.  status[0] = 0 ok, 1 breakdown.
-__global__ void __launch_bounds__(1024) k_chol_inv(const double* __restrict__ G, int r, double shift,
-                                                  double* __restrict__ L, double* __restrict__ Linv,
-                                                  int* __restrict__ status, int expect_identity) {
-  __shared__ double s_piv;
-  __shared__ int s_bad;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  if (tid == 0) s_bad = 0;
-  __syncthreads();
-  for (long long e = tid; e < (long long)r * r; e += blockDim.x) {
-    L[e] = 0.0;
-    // second CholeskyQR pass: the Gram of an already orthonormalised basis
-    // must be close to I, otherwise the first pass lost orthogonality
-    if (expect_identity && fabs(G[e] - ((e / r) == (e % r) ? 1.0 : 0.0)) > 1e-3) s_bad = 1;
+// In-place Cholesky of the kb x kb diagonal block at A + k0*(lda+1) (kb <= 64),
+// staged in shared memory.  A non-positive or non-finite pivot sets *status.
+constexpr int CHB = 64;
+__global__ void __launch_bounds__(256) k_chol_diag(double* __restrict__ A, int lda, int k0, int kb,
+                                                   int* __restrict__ status) {
+  __shared__ double a[CHB][CHB + 1];
+  __shared__ int bad;
+  const int tid = threadIdx.x;
+  double* blk = A + (long long)k0 * lda + k0;
+  if (tid == 0) bad = 0;
+  for (int e = tid; e < kb * kb; e += blockDim.x) {
+    const int c = e / kb, rr = e % kb;      // column-major: element (rr, c) at blk[c*lda + rr]
+    a[rr][c] = blk[(long long)c * lda + rr];
   }
   __syncthreads();
-  for (int j = 0; j < r; ++j) {
-    if (warp == 0) {
-      double acc = 0.0;
-      for (int k = lane; k < j; k += 32) acc = fma(L[(long long)j * r + k], L[(long long)j * r + k], acc);
-      acc = warp_sum(acc);
-      if (lane == 0) {
-        const double t = G[(long long)j * r + j] + shift - acc;
-        if (!(t > 0.0) || !isfinite(t)) s_bad = 1;
-        s_piv = sqrt(fmax(t, 1e-300));
-        L[(long long)j * r + j] = s_piv;
-      }
+  for (int j = 0; j < kb; ++j) {
+    if (tid == 0) {
+      const double t = a[j][j];
+      if (!(t > 0.0) || !isfinite(t)) bad = 1;
+      a[j][j] = sqrt(fmax(t, 1e-300));
     }
     __syncthreads();
-    if (s_bad) break;
-    const double piv = s_piv;
-    for (int i = j + 1 + warp; i < r; i += nw) {
-      double acc = 0.0;
-      for (int k = lane; k < j; k += 32) acc = fma(L[(long long)i * r + k], L[(long long)j * r + k], acc);
-      acc = warp_sum(acc);
-      if (lane == 0) L[(long long)i * r + j] = (G[(long long)i * r + j] - acc) / piv;
+    const double piv = a[j][j];
+    for (int i = j + 1 + tid; i < kb; i += blockDim.x) a[i][j] /= piv;
+    __syncthreads();
+    const int m = kb - j - 1;
+    for (int e = tid; e < m * m; e += blockDim.x) {
+      const int i = j + 1 + e / m, c = j + 1 + e % m;
+      if (c <= i) a[i][c] = fma(-a[i][j], a[c][j], a[i][c]);
     }
     __syncthreads();
   }
-  if (s_bad) { if (tid == 0) status[0] = 1; return; }
-  // Linv: forward substitution, one thread per column c.
-  for (int c = tid; c < r; c += blockDim.x) {
-    for (int i = 0; i < c; ++i) Linv[(long long)i * r + c] = 0.0;
-    for (int i = c; i < r; ++i) {
-      double acc = (i == c) ? 1.0 : 0.0;
-      for (int k = c; k < i; ++k) acc -= L[(long long)i * r + k] * Linv[(long long)k * r + c];
-      Linv[(long long)i * r + c] = acc / L[(long long)i * r + i];
-    }
+  for (int e = tid; e < kb * kb; e += blockDim.x) {
+    const int c = e / kb, rr = e % kb;
+    blk[(long long)c * lda + rr] = rr >= c ? a[rr][c] : 0.0;
   }
-  if (tid == 0) status[0] = 0;
+  if (tid == 0 && bad) atomicOr(status, 1);
 }
-
 
 // Rank-robust orthonormalisation (fallback when CholeskyQR breaks down on a
 // rank-deficient sketch, where LAPACK's Householder QR still returns an
@@ -220,23 +148,31 @@ __global__ void __launch_bounds__(1024) k_cgs2(double* __restrict__ Y, long long
 }
 
 // ---------------------------------------------------------- Jacobi SVD
-// One-sided Jacobi on G (m rows x n cols, column j at G + j*m).  On exit
-// sig[j] (descending) and U (m x n, row-major with leading dim ldu) hold the
-// normalised columns of G*J; these are the right singular vectors of G^T.
-// perm scratch (n ints).
-__global__ void __launch_bounds__(1024) k_jacobi(double* __restrict__ G, int m, int n, double tol, int max_sweeps,
-                                                double* __restrict__ sig, double* __restrict__ U, int ldu,
-                                                int* __restrict__ perm, int* __restrict__ sweeps_out) {
-  __shared__ int s_rot;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+// One-sided (Hestenes) Jacobi on G (m rows x n cols, column j at G + j*m),
+// tournament ordering.  On exit sig[j] (descending) and U (m x n, row-major
+// with leading dim ldu) hold the normalised columns of G*J; these are the
+// right singular vectors of G^T.  perm scratch (n ints), rot scratch
+// (max_sweeps ints, zeroed by the caller).
+//
+// Persistent cooperative kernel: one warp per pair of a round, the CTAs of
+// the grid meet at a grid barrier between rounds (the pairs of one round are
+// disjoint, so the result does not depend on how pairs map to warps).
+__global__ void __launch_bounds__(256) k_jacobi(double* __restrict__ G, int m, int n, double tol, int max_sweeps,
+                                               double* __restrict__ sig, double* __restrict__ U, int ldu,
+                                               int* __restrict__ perm, int* __restrict__ sweeps_out,
+                                               int* __restrict__ rot) {
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31;
+  const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int nw = (int)((gridDim.x * blockDim.x) >> 5);
+  const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
   const int np = (n + 1) & ~1;   // even count (one dummy when n is odd)
   int sweep = 0;
   for (; sweep < max_sweeps; ++sweep) {
-    if (tid == 0) s_rot = 0;
-    __syncthreads();
     for (int round = 0; round < np - 1; ++round) {
       // tournament pairing: position 0 fixed, others rotate
-      for (int pr = warp; pr < np / 2; pr += nw) {
+      for (int pr = gw; pr < np / 2; pr += nw) {
         int a = (pr == 0) ? 0 : 1 + (pr - 1 + round) % (np - 1);
         int b = 1 + (np - 2 - pr + round) % (np - 1);
         if (a >= n || b >= n) continue;
@@ -258,40 +194,38 @@ __global__ void __launch_bounds__(1024) k_jacobi(double* __restrict__ G, int m, 
             gp[i] = c * x - s * y;
             gq[i] = s * x + c * y;
           }
-          if (lane == 0) s_rot = 1;
+          if (lane == 0) atomicOr(rot + sweep, 1);
         }
       }
-      __syncthreads();
+      grid.sync();
     }
-    if (!s_rot) break;
-    __syncthreads();
+    if (!*(volatile int*)(rot + sweep)) break;
   }
   // column norms
-  for (int j = warp; j < n; j += nw) {
+  for (int j = gw; j < n; j += nw) {
     const double* gj = G + (long long)j * m;
     double acc = 0.0;
     for (int i = lane; i < m; i += 32) acc = fma(gj[i], gj[i], acc);
     acc = warp_sum(acc);
     if (lane == 0) sig[j] = sqrt(acc);
   }
-  __syncthreads();
+  grid.sync();
   // order by sigma descending (stable on ties), rank by counting
-  for (int j = tid; j < n; j += blockDim.x) {
+  for (long long j = gt; j < n; j += nt) {
     const double sj = sig[j];
     int rank = 0;
     for (int k = 0; k < n; ++k) rank += (sig[k] > sj) || (sig[k] == sj && k < j);
-    perm[rank] = j;
+    perm[rank] = (int)j;
   }
-  __syncthreads();
-  for (int jj = warp; jj < n; jj += nw) {
+  grid.sync();
+  for (int jj = gw; jj < n; jj += nw) {
     const int j = perm[jj];
     const double* gj = G + (long long)j * m;
     const double sj = sig[j];
     const double inv = sj > 0.0 ? 1.0 / sj : 0.0;
     for (int i = lane; i < m; i += 32) U[(long long)i * ldu + jj] = gj[i] * inv;
   }
-  __syncthreads();
-  if (tid == 0) *sweeps_out = sweep;
+  if (gt == 0) *sweeps_out = sweep;
 }
 
 // Sorted singular values: sorted[jj] = sig[perm[jj]] computed by rank again
@@ -356,12 +290,50 @@ __global__ void k_all_finite(const void* __restrict__ p, long long n, int dt, in
 }  // namespace
 
 // ==================================================================== host
+// C[M x N] = alpha * op(A) * op(B) + beta * C, row-major with leading dims.
+// op(A) is M x K: A[m*lda + k] (ta=0) or A[k*lda + m] (ta=1).
+// op(B) is K x N: B[k*ldb + n] (tb=0) or B[n*ldb + k] (tb=1).
+// Plain fp64 GEMMs of the range finder go to cuBLAS (library GEMM; the
+// distance contraction of the BICO path stays on our own kernels).  Row-major
+// C = op(A) op(B) is column-major C^T = op(B)^T op(A)^T.
+static cublasHandle_t blas_handle() {
+  thread_local cublasHandle_t h[16] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!h[dev & 15]) cublasCreate(&h[dev & 15]);
+  return h[dev & 15];
+}
+
+static int jacobi(cudaStream_t st, double* G, int m, int n, double tol, int max_sweeps, double* sig, double* U,
+                  int ldu, int* perm, int* sweeps, int* rot) {
+  PCY_CUDA(cudaMemsetAsync(rot, 0, sizeof(int) * max_sweeps, st));
+  static int max_blocks = -1;
+  if (max_blocks < 0) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_jacobi, 256, 0);
+    max_blocks = sms * (per > 0 ? per : 1);
+  }
+  const int pairs = (n + 1) / 2;
+  int blocks = (pairs + 7) / 8;
+  if (blocks > max_blocks) blocks = max_blocks;
+  if (blocks < 1) blocks = 1;
+  void* args[] = {&G, &m, &n, &tol, &max_sweeps, &sig, &U, &ldu, &perm, &sweeps, &rot};
+  PCY_CUDA(cudaLaunchCooperativeKernel((const void*)k_jacobi, dim3(blocks), dim3(256), args, 0, st));
+  pcy_count_launch();
+  return PCY_OK;
+}
+
 static int gemm(cudaStream_t st, int M, int N, int K, double alpha, const double* A, long long lda, int ta,
                 const double* B, long long ldb, int tb, double beta, double* C, long long ldc) {
   if (M <= 0 || N <= 0) return PCY_OK;
-  dim3 grid((unsigned)((N + GBN - 1) / GBN), (unsigned)((M + GBM - 1) / GBM));
-  k_dgemm<<<grid, 128, 0, st>>>(M, N, K, alpha, A, lda, ta, B, ldb, tb, beta, C, ldc); pcy_count_launch();
-  PCY_LAUNCH_CHECK();
+  cublasHandle_t h = blas_handle();
+  if (!h) { pcy_set_error("cublasCreate failed"); return PCY_ECUDA; }
+  cublasSetStream(h, st);
+  const cublasStatus_t rc = cublasDgemm(h, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N,
+                                        N, M, K, &alpha, B, (int)ldb, A, (int)lda, &beta, C, (int)ldc);
+  if (rc != CUBLAS_STATUS_SUCCESS) { pcy_set_error("cublasDgemm failed (%d)", (int)rc); return PCY_ECUDA; }
   return PCY_OK;
 }
 
@@ -369,18 +341,38 @@ static int gemm(cudaStream_t st, int M, int N, int K, double alpha, const double
 // to shifted CholeskyQR3 when the Gram factorisation breaks down.
 static int cholqr(cudaStream_t st, double* Y, long long rows, int r, double* Gs, double* Ls, double* Li,
                   double* T, int* status) {
+  (void)Ls; (void)Li; (void)T;
   int hs = 0;
   auto pass = [&](double shift, int* ok, int check) -> int {
     int rc;
     if ((rc = gemm(st, r, r, (int)rows, 1.0, Y, r, 1, Y, r, 0, 0.0, Gs, r))) return rc;
-    k_chol_inv<<<1, 1024, 0, st>>>(Gs, r, shift, Ls, Li, status, check); pcy_count_launch();
+    PCY_CUDA(cudaMemsetAsync(status, 0, sizeof(int), st));
+    k_gram_prep<<<(unsigned)std::min((r * r + 255) / 256, 148 * 4), 256, 0, st>>>(Gs, r, shift, check, status);
+    pcy_count_launch();
+    // blocked right-looking Cholesky, lower, column-major (Gs symmetric)
+    cublasHandle_t h = blas_handle();
+    cublasSetStream(h, st);
+    const double one = 1.0, mone = -1.0;
+    for (int k0 = 0; k0 < r; k0 += CHB) {
+      const int kb = std::min(CHB, r - k0), rest = r - k0 - kb;
+      k_chol_diag<<<1, 256, 0, st>>>(Gs, r, k0, kb, status); pcy_count_launch();
+      if (rest > 0) {
+        double* A11 = Gs + (long long)k0 * r + k0;
+        double* A21 = A11 + kb;
+        double* A22 = Gs + (long long)(k0 + kb) * r + k0 + kb;
+        if (cublasDtrsm(h, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, rest, kb,
+                        &one, A11, r, A21, r) != CUBLAS_STATUS_SUCCESS) { pcy_set_error("trsm failed"); return PCY_ECUDA; }
+        if (cublasDsyrk(h, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, rest, kb, &mone, A21, r, &one, A22, r)
+            != CUBLAS_STATUS_SUCCESS) { pcy_set_error("syrk failed"); return PCY_ECUDA; }
+      }
+    }
     PCY_LAUNCH_CHECK();
     PCY_CUDA(pcy_d2h(&hs, status, sizeof(int), st));
     *ok = hs == 0;
     if (!*ok) return PCY_OK;
-    // Y <- Y * Linv^T
-    if ((rc = gemm(st, (int)rows, r, r, 1.0, Y, r, 0, Li, r, 1, 0.0, T, r))) return rc;
-    PCY_CUDA(cudaMemcpyAsync(Y, T, sizeof(double) * rows * r, cudaMemcpyDeviceToDevice, st));
+    // Y <- Y L^-T  (row-major Y is column-major Y^T: Y^T <- L^-1 Y^T)
+    if (cublasDtrsm(h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, r, (int)rows,
+                    &one, Gs, r, Y, r) != CUBLAS_STATUS_SUCCESS) { pcy_set_error("trsm failed"); return PCY_ECUDA; }
     return PCY_OK;
   };
   int ok = 0, rc;
@@ -392,7 +384,7 @@ static int cholqr(cudaStream_t st, double* Y, long long rows, int r, double* Gs,
   // rank-deficient sketch: Gram-Schmidt with completion
   {
     double* coef = nullptr;
-    PCY_CUDA(cudaMallocAsync(&coef, sizeof(double) * r, st));
+    PCY_CUDA(pcy_malloc_async(&coef, sizeof(double) * r, st));
     k_cgs2<<<1, 1024, 0, st>>>(Y, rows, r, coef, status); pcy_count_launch();
     PCY_LAUNCH_CHECK();
     PCY_CUDA(pcy_d2h(&hs, status, sizeof(int), st));
@@ -407,7 +399,7 @@ extern "C" {
 int pcy_all_finite(const void* p, long long n, int dtype, int* out_host, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   int* flag;
-  PCY_CUDA(cudaMallocAsync(&flag, sizeof(int), st));
+  PCY_CUDA(pcy_malloc_async(&flag, sizeof(int), st));
   const int one = 1;
   PCY_CUDA(cudaMemcpyAsync(flag, &one, sizeof(int), cudaMemcpyHostToDevice, st));
   if (n > 0) { k_all_finite<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 8), 256, 0, st>>>(p, n, dtype, flag); pcy_count_launch(); }
@@ -454,24 +446,29 @@ int pcy_rsvd(const double* A, long long rows, int cols, int ell, int r, int powe
   if (r > rows || r > cols || ell > r || ell < 1) { pcy_set_error("rsvd: bad rank"); return PCY_EINVAL; }
   const bool two = rows > 4LL * r;
   double *Q, *Z, *Bm, *Gs, *Ls, *Li, *T, *Wm, *core, *Uj, *sig, *Vfull;
-  int *status, *perm, *sweeps;
+  int *status, *perm, *sweeps, *rot;
   const long long big = std::max<long long>(rows, cols);
-  PCY_CUDA(cudaMallocAsync(&Q, sizeof(double) * rows * r, st));
-  PCY_CUDA(cudaMallocAsync(&Z, sizeof(double) * cols * r, st));
-  PCY_CUDA(cudaMallocAsync(&Bm, sizeof(double) * (long long)r * cols, st));
-  PCY_CUDA(cudaMallocAsync(&Gs, sizeof(double) * r * r, st));
-  PCY_CUDA(cudaMallocAsync(&Ls, sizeof(double) * r * r, st));
-  PCY_CUDA(cudaMallocAsync(&Li, sizeof(double) * r * r, st));
-  PCY_CUDA(cudaMallocAsync(&T, sizeof(double) * big * r, st));
-  PCY_CUDA(cudaMallocAsync(&Wm, sizeof(double) * cols * r, st));
-  PCY_CUDA(cudaMallocAsync(&core, sizeof(double) * r * r, st));
-  PCY_CUDA(cudaMallocAsync(&Uj, sizeof(double) * cols * r, st));
-  PCY_CUDA(cudaMallocAsync(&sig, sizeof(double) * 2 * r, st));
-  PCY_CUDA(cudaMallocAsync(&Vfull, sizeof(double) * cols * r, st));
-  PCY_CUDA(cudaMallocAsync(&status, sizeof(int) * 4, st));
-  PCY_CUDA(cudaMallocAsync(&perm, sizeof(int) * r, st));
-  PCY_CUDA(cudaMallocAsync(&sweeps, sizeof(int), st));
+  PCY_CUDA(pcy_malloc_async(&Q, sizeof(double) * rows * r, st));
+  PCY_CUDA(pcy_malloc_async(&Z, sizeof(double) * cols * r, st));
+  PCY_CUDA(pcy_malloc_async(&Bm, sizeof(double) * (long long)r * cols, st));
+  PCY_CUDA(pcy_malloc_async(&Gs, sizeof(double) * r * r, st));
+  PCY_CUDA(pcy_malloc_async(&Ls, sizeof(double) * r * r, st));
+  PCY_CUDA(pcy_malloc_async(&Li, sizeof(double) * r * r, st));
+  PCY_CUDA(pcy_malloc_async(&T, sizeof(double) * big * r, st));
+  PCY_CUDA(pcy_malloc_async(&Wm, sizeof(double) * cols * r, st));
+  PCY_CUDA(pcy_malloc_async(&core, sizeof(double) * r * r, st));
+  PCY_CUDA(pcy_malloc_async(&Uj, sizeof(double) * cols * r, st));
+  PCY_CUDA(pcy_malloc_async(&sig, sizeof(double) * 2 * r, st));
+  PCY_CUDA(pcy_malloc_async(&Vfull, sizeof(double) * cols * r, st));
+  PCY_CUDA(pcy_malloc_async(&status, sizeof(int) * 4, st));
+  PCY_CUDA(pcy_malloc_async(&perm, sizeof(int) * r, st));
+  PCY_CUDA(pcy_malloc_async(&sweeps, sizeof(int), st));
+  PCY_CUDA(pcy_malloc_async(&rot, sizeof(int) * 64, st));
   int rc = PCY_OK;
+  const bool dbg = getenv("PCY_DEBUG_RSVD") != nullptr;
+  cudaEvent_t evs[4];
+  if (dbg) for (auto& e : evs) { cudaEventCreate(&e); }
+  if (dbg) cudaEventRecord(evs[0], st);
   do {
     // Q = qr(A omega)
     if ((rc = gemm(st, (int)rows, r, cols, 1.0, A, cols, 0, omega, r, 0, 0.0, Q, r))) break;
@@ -484,6 +481,7 @@ int pcy_rsvd(const double* A, long long rows, int cols, int ell, int r, int powe
       if ((rc = cholqr(st, Q, rows, r, Gs, Ls, Li, T, status))) break;
     }
     if (rc) break;
+    if (dbg) cudaEventRecord(evs[1], st);
     // small = Q^T A  (r x cols)
     if ((rc = gemm(st, r, cols, (int)rows, 1.0, Q, r, 1, A, cols, 0, 0.0, Bm, cols))) break;
     const double tol = 2.220446049250313e-16 * (double)std::max(r, 8);
@@ -493,14 +491,22 @@ int pcy_rsvd(const double* A, long long rows, int cols, int ell, int r, int powe
       if ((rc = cholqr(st, Wm, cols, r, Gs, Ls, Li, T, status))) break;
       if ((rc = gemm(st, r, r, cols, 1.0, Bm, cols, 0, Wm, r, 0, 0.0, core, r))) break;
       // Jacobi on core^T: column j of core^T = row j of core (contiguous)
-      k_jacobi<<<1, 1024, 0, st>>>(core, r, r, tol, 60, sig, Uj, r, perm, sweeps); pcy_count_launch();
-      PCY_LAUNCH_CHECK();
+      if (dbg) cudaEventRecord(evs[2], st);
+      if ((rc = jacobi(st, core, r, r, tol, 60, sig, Uj, r, perm, sweeps, rot))) break;
+      if (dbg) {
+        cudaEventRecord(evs[3], st); cudaEventSynchronize(evs[3]);
+        float a = 0, b = 0, c = 0; int sw = 0;
+        cudaEventElapsedTime(&a, evs[0], evs[1]); cudaEventElapsedTime(&b, evs[1], evs[2]);
+        cudaEventElapsedTime(&c, evs[2], evs[3]);
+        cudaMemcpy(&sw, sweeps, sizeof(int), cudaMemcpyDeviceToHost);
+        fprintf(stderr, "[pcy] rsvd %lldx%d r=%d: range %.2f ms, small+core %.2f ms, jacobi %.2f ms (%d sweeps)\n",
+                rows, cols, r, a, b, c, sw);
+      }
       // Uj (r x r row-major) columns = right singular vectors of core: V = W Uj
       if ((rc = gemm(st, cols, r, r, 1.0, Wm, r, 0, Uj, r, 0, 0.0, Vfull, r))) break;
     } else {
       // Jacobi on small^T: column j of small^T = row j of small (contiguous)
-      k_jacobi<<<1, 1024, 0, st>>>(Bm, cols, r, tol, 60, sig, Vfull, r, perm, sweeps); pcy_count_launch();
-      PCY_LAUNCH_CHECK();
+      if ((rc = jacobi(st, Bm, cols, r, tol, 60, sig, Vfull, r, perm, sweeps, rot))) break;
     }
     k_sorted_sigma<<<1, 256, 0, st>>>(sig, r, sig + r); pcy_count_launch();
     // keep the first ell columns
@@ -518,6 +524,7 @@ int pcy_rsvd(const double* A, long long rows, int cols, int ell, int r, int powe
   cudaFreeAsync(Ls, st); cudaFreeAsync(Li, st); cudaFreeAsync(T, st); cudaFreeAsync(Wm, st);
   cudaFreeAsync(core, st); cudaFreeAsync(Uj, st); cudaFreeAsync(sig, st); cudaFreeAsync(Vfull, st);
   cudaFreeAsync(status, st); cudaFreeAsync(perm, st); cudaFreeAsync(sweeps, st);
+  cudaFreeAsync(rot, st);
   return rc;
 }
 
@@ -525,7 +532,7 @@ int pcy_rsvd(const double* A, long long rows, int cols, int ell, int r, int powe
 int pcy_project(const double* A, long long rows, int cols, const double* V, int ell, double* out, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   double* P;
-  PCY_CUDA(cudaMallocAsync(&P, sizeof(double) * rows * ell, st));
+  PCY_CUDA(pcy_malloc_async(&P, sizeof(double) * rows * ell, st));
   int rc = gemm(st, (int)rows, ell, cols, 1.0, A, cols, 0, V, ell, 0, 0.0, P, ell);
   if (!rc) rc = gemm(st, (int)rows, cols, ell, 1.0, P, ell, 0, V, ell, 1, 0.0, out, cols);
   cudaFreeAsync(P, st);
