@@ -69,7 +69,8 @@ int pcy_engine_extract(void* engine, double* points, long long* weights, long lo
                        long long* count, void* stream);
 
 /* Instrumentation of the in-order resolve: out6 (host) = [levels walked,
- * direct scans, demand row loads, full capacity evaluations, items, max depth]. */
+ * tensor-core near-tie rechecks, demand row loads, full capacity evaluations,
+ * items, max depth]. */
 int pcy_engine_counters(void* engine, long long* out6);
 /* The same counters summed over every engine destroyed so far in the process. */
 int pcy_engine_counters_total(long long* out6);
@@ -119,6 +120,16 @@ int pcy_dgemm(int M, int N, int K, double alpha, const double* A, long long lda,
 int pcy_cast_f32_f64(const float* src, long long n, double* dst, void* stream);
 int pcy_cast_i64_f64(const long long* src, long long n, double* dst, void* stream);
 int pcy_all_finite(const void* p, long long n, int dtype, int* out_host, void* stream);
+
+/* --------------------------------------------- distance contraction (test) */
+
+/* Split-TF32 (3xTF32) dots on tcgen05: out (device, M x N fp32) ~= (A_m - c).(B_n - c)
+ * with c = A_0, A/B (device) fp64 rows of dimension d.  *tau_out (host) = the
+ * rigorous relative error factor: |out - exact| <= tau |A_m - c| |B_n - c|.
+ * This is the contraction of the full-set nearest-reference search
+ * (coreset.py:318-330) that the engine runs for d >= 256. */
+int pcy_tc_dots_f64(const double* A, long long lda, int M, const double* B, long long ldb, int N, int d,
+                    float* out, double* tau_out, void* stream);
 
 /* -------------------------------------------------------- instrumentation */
 long long pcy_launch_count(void);

@@ -35,6 +35,8 @@ _SIGS = {
     "pcy_prof_enable": (c_i32, [c_i32]),
     "pcy_prof_reset": (c_i32, []),
     "pcy_prof_read": (c_i32, [c_i32, P_f64, P_i64, P_i64]),
+    # tensor-core distance contraction (test entry)
+    "pcy_tc_dots_f64": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_i64, c_i32, c_i32, c_vp, P_f64, c_vp]),
 }
 
 PROF_SLOTS = {"resolve": 0, "chain": 1, "reattach": 2, "seed": 3, "lloyd": 4, "gemm": 5}
@@ -44,7 +46,7 @@ def engine_counters_total() -> dict:
     import numpy as np
     out = np.zeros(6, dtype=np.int64)
     lib().pcy_engine_counters_total(out.ctypes.data)
-    keys = ("levels", "direct_scans", "demand_loads", "slow_capacity", "items", "max_depth")
+    keys = ("levels", "tc_rechecks", "demand_loads", "slow_capacity", "items", "max_depth")
     return {k: int(v) for k, v in zip(keys, out)}
 
 

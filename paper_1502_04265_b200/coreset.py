@@ -276,7 +276,7 @@ class BicoEngine:
         self._flush()
         out = np.zeros(6, dtype=np.int64)
         nat.check(nat.lib().pcy_engine_counters(self._h, out.ctypes.data), "pcy_engine_counters")
-        keys = ("levels", "direct_scans", "demand_loads", "slow_capacity", "items", "max_depth")
+        keys = ("levels", "tc_rechecks", "demand_loads", "slow_capacity", "items", "max_depth")
         return {k: int(v) for k, v in zip(keys, out)}
 
     # -- extraction ---------------------------------------------------------

@@ -20,6 +20,15 @@ cudaError_t pcy_spin_sync(cudaStream_t st);
 // Device -> host copy of a small result through a thread-local pinned
 // staging buffer, completed with pcy_spin_sync.
 cudaError_t pcy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t st);
+// split-TF32 distance contraction on tcgen05 (tc_dots.cu)
+double pcy_tc_error_tau(int Kp);
+int pcy_tc_pad(int d);
+int pcy_tc_center(const double* src, const int* idx, long long ld, int d, double* center, cudaStream_t st);
+// rows_dev (nullable): device row count capping `rows` / `N`
+int pcy_tc_split(const double* src, const int* idx, long long ld, int d, long long rows, const int* rows_dev,
+                 const double* center, float* hi, float* lo, double* nrm2, cudaStream_t st);
+int pcy_tc_dots(const float* Ahi, const float* Alo, long long a_cap, int M, const float* Bhi, const float* Blo,
+                long long b_cap, int N, const int* n_dev, int Kp, float* out, long long ldo, cudaStream_t st);
 // cudaMallocAsync from the device's default pool, whose memory is kept
 // resident (release threshold raised once per device): per-call scratch of
 // the projection and the engine then never re-maps physical memory.
@@ -31,8 +40,9 @@ inline cudaError_t pcy_malloc_async(T** p, size_t bytes, cudaStream_t st) {
 // DMMA distance contraction (distance.cu)
 int pcy_launch_gram(const double* A, const int* aidx, long long lda, int M, const double* B, const int* bidx,
                     long long ldb, int N, int K, double* C, long long ldc, cudaStream_t st);
-int pcy_launch_parts(const double* A, const int* aidx, long long lda, int M, const double* B, long long ldb,
-                     const double* rn, int N, int K, double* C, long long ldc, cudaStream_t st);
+int pcy_launch_parts(const double* A, const int* aidx, long long lda, int M, const double* B, const int* bidx,
+                     long long ldb, const double* rn, int N, const int* n_dev, int K, double* C, long long ldc,
+                     cudaStream_t st);
 int pcy_launch_nearest(const double* A, const int* aidx, long long lda, int M, const double* B, const int* bidx,
                        long long ldb, const double* rn, int N, int K, double* ppart, int* ppos, int* out_pos,
                        double* out_part, cudaStream_t st);
@@ -94,11 +104,50 @@ __device__ __forceinline__ void warp_argmin(double& v, int& pos) {
 }
 
 // Lane-strided fp64 dot of two length-d vectors, all lanes get the total.
+// Lane-strided fp64 dot: lane l sums a[e] b[e] for e = l, l+32, ... in that
+// order, then the warp tree.  Loads are issued 16 rows ahead (the FMA order
+// is unchanged, so every caller sees bit-identical values at any d).
 __device__ __forceinline__ double warp_dot(const double* __restrict__ a,
                                            const double* __restrict__ b, int d, int lane) {
   double acc = 0.0;
-  for (int e = lane; e < d; e += 32) acc = fma(a[e], b[e], acc);
+  int e = lane;
+  for (; e + 15 * 32 < d; e += 16 * 32) {
+    double av[16], bv[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) { av[q] = a[e + 32 * q]; bv[q] = b[e + 32 * q]; }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) acc = fma(av[q], bv[q], acc);
+  }
+  for (; e < d; e += 32) acc = fma(a[e], b[e], acc);
   return warp_sum(acc);
+}
+
+// CTA-cooperative fp64 dot for one item per CTA (WPI warps): warp w sums the
+// lane-strided elements e = 32 w + l + 32 WPI k in order, then the warp tree,
+// then red[0] + red[1] + ... in warp order.  Deterministic; every warp of the
+// CTA must call it (two __syncthreads).
+template <int WPI>
+__device__ __forceinline__ double cta_dot(const double* __restrict__ a, const double* __restrict__ b, int d,
+                                          int lane, int warp, double* red) {
+  double acc = 0.0;
+  int e = warp * 32 + lane;
+  constexpr int S = 32 * WPI;
+  for (; e + 7 * S < d; e += 8 * S) {
+    double av[8], bv[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) { av[q] = a[e + S * q]; bv[q] = b[e + S * q]; }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc = fma(av[q], bv[q], acc);
+  }
+  for (; e < d; e += S) acc = fma(a[e], b[e], acc);
+  acc = warp_sum(acc);
+  __syncthreads();
+  if (lane == 0) red[warp] = acc;
+  __syncthreads();
+  double t = red[0];
+#pragma unroll
+  for (int w = 1; w < WPI; ++w) t += red[w];
+  return t;
 }
 
 // Transpose-reduce: lane l holds 32 partial sums acc[0..31] (one per member);

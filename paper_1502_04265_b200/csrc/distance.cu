@@ -25,7 +25,8 @@ __global__ void __launch_bounds__(128) k_dist_tile(int M, int N, int K,
                                                   const double* __restrict__ B, const int* __restrict__ bidx, long long ldb,
                                                   const double* __restrict__ rn,
                                                   double* __restrict__ C, long long ldc,
-                                                  double* __restrict__ ppart, int* __restrict__ ppos, int ntiles) {
+                                                  double* __restrict__ ppart, int* __restrict__ ppos, int ntiles,
+                                                  const int* __restrict__ n_dev = nullptr) {
   __shared__ double As[2][DBM][DBK + 4];
   __shared__ double Bs[2][DBK][DBN + 4];
   __shared__ long long arow[DBM], brow[DBN];
@@ -36,6 +37,7 @@ __global__ void __launch_bounds__(128) k_dist_tile(int M, int N, int K,
   const int g = lane >> 2, t4 = lane & 3;
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
   const int m0 = blockIdx.y * DBM, n0 = blockIdx.x * DBN;
+  if (n_dev) { N = min(N, *n_dev); if (n0 >= N) return; }
   if (tid < DBM) {
     const int m = m0 + tid;
     arow[tid] = m < M ? (long long)(aidx ? aidx[m] : m) * lda : -1;
@@ -174,13 +176,15 @@ int pcy_launch_gram(const double* A, const int* aidx, long long lda, int M, cons
   return PCY_OK;
 }
 
-// Parts matrix: C[m][n] = rn[n] - 2 A[ia(m)].B[n] (the full-set form of K1:
-// every block row against every allocated reference slot).
-int pcy_launch_parts(const double* A, const int* aidx, long long lda, int M, const double* B, long long ldb,
-                     const double* rn, int N, int K, double* C, long long ldc, cudaStream_t st) {
+// Parts matrix: C[m][n] = rn[ib(n)] - 2 A[ia(m)].B[ib(n)] (the full-set form
+// of K1: every block row against every live reference slot; n_dev, when set,
+// caps N with a device-side count).
+int pcy_launch_parts(const double* A, const int* aidx, long long lda, int M, const double* B, const int* bidx,
+                     long long ldb, const double* rn, int N, const int* n_dev, int K, double* C, long long ldc,
+                     cudaStream_t st) {
   if (M <= 0 || N <= 0) return PCY_OK;
   dim3 grid((unsigned)((N + DBN - 1) / DBN), (unsigned)((M + DBM - 1) / DBM));
-  k_dist_tile<2><<<grid, 128, 0, st>>>(M, N, K, A, aidx, lda, B, nullptr, ldb, rn, C, ldc, nullptr, nullptr, 0);
+  k_dist_tile<2><<<grid, 128, 0, st>>>(M, N, K, A, aidx, lda, B, bidx, ldb, rn, C, ldc, nullptr, nullptr, 0, n_dev);
   pcy_count_launch();
   PCY_LAUNCH_CHECK();
   return PCY_OK;

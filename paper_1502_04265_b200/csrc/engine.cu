@@ -159,21 +159,106 @@ __device__ __forceinline__ void scan_members(const EngDev& E, const int* __restr
 }
 
 // Nearest among members [0, cnt) using a precomputed parts row (full-set K1).
-__device__ __forceinline__ void scan_parts(const double* __restrict__ prow, const int* __restrict__ mem, int cnt,
-                                           int lane, double& bp, int& bpos) {
+__device__ __forceinline__ void scan_parts(const double* __restrict__ prow, int cnt, int lane, double& bp,
+                                           int& bpos) {
   bp = INFINITY; bpos = 0x7fffffff;
   for (int c0 = 0; c0 < cnt; c0 += 32) {
     const int p = c0 + lane;
     double v = INFINITY; int ps = 0x7fffffff;
-    if (p < cnt) { v = prow[mem[p]]; ps = p; }
+    if (p < cnt) { v = prow[p]; ps = p; }
     warp_argmin(v, ps);
     if (v < bp) { bp = v; bpos = ps; }
   }
 }
 
+// Nearest among members [0, cnt) from the tensor-core dots row of item i:
+// approximate centred parts a_j = |r_j-c|^2 - 2 dot_j carry the rigorous
+// error e_j = 2 tau |r_j-c| |x-c|; every member with a_j - e_j <= min(a + e)
+// is re-decided with its exact fp64 part (first position on ties), so the
+// result is the fp64 argmin.  *nre counts the exact re-decisions.
+template <class RDot>
+__device__ __forceinline__ void scan_parts_tc(const EngDev& E, long long i, int g, const int* __restrict__ mem,
+                                              int cnt, RDot rdot, int lane, double& bp, int& bpos, int& nre) {
+  const long long col = E.fs_gofs[g];
+  const float* __restrict__ dots = E.tc_dots + i * E.tc_ldo + col;
+  const double* __restrict__ rnc = E.tc_rnc + col;
+  const double xn = sqrt(E.tc_xn2[i]);
+  const double tau2 = 2.0 * E.tc_tau * (1.0 + 1e-9);
+  double U = INFINITY;
+  for (int p = lane; p < cnt; p += 32) {
+    const double rc = rnc[p];
+    U = fmin(U, rc - 2.0 * (double)dots[p] + tau2 * sqrt(rc) * xn + 1e-300);
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) U = fmin(U, __shfl_xor_sync(PCY_FULL, U, o));
+  bp = INFINITY; bpos = 0x7fffffff;
+  int ncand = 0;
+  for (int c0 = 0; c0 < cnt; c0 += 32) {
+    const int p = c0 + lane;
+    bool cand = false;
+    if (p < cnt) {
+      const double rc = rnc[p];
+      cand = rc - 2.0 * (double)dots[p] - tau2 * sqrt(rc) * xn <= U;
+    }
+    unsigned m = __ballot_sync(PCY_FULL, cand);
+    while (m) {
+      const int b = __ffs(m) - 1;
+      m &= m - 1;
+      const int jj = mem[c0 + b];
+      const double part = radd(E.rn[jj], rmul(rdot(jj), -2.0));
+      if (part < bp) { bp = part; bpos = c0 + b; }
+      ++ncand;
+    }
+  }
+  if (ncand > 1) nre += ncand - 1;   // members re-decided beyond the winner
+}
+
 #include "resolve_fast.cuh"
 #include "reattach_fast.cuh"
 #include "resolve_smem.cuh"
+
+// Column order of the full-set contraction (one CTA): gofs[g] = exclusive
+// prefix sum of the group member counts, *cnt = total.  Group g's members
+// then occupy columns [gofs[g], gofs[g] + g_count[g]), so the chain walk reads
+// its parts / dots row contiguously, with no slot indirection.
+__global__ void __launch_bounds__(1024) k_group_offsets(const int* __restrict__ gcount, long long ng,
+                                                        int* __restrict__ gofs, int* __restrict__ cnt) {
+  __shared__ int wsum[32];
+  __shared__ int carry;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) carry = 0;
+  __syncthreads();
+  for (long long base = 0; base < ng; base += 1024) {
+    const long long g = base + tid;
+    const int c = g < ng ? gcount[g] : 0;
+    int v = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) { const int t = __shfl_up_sync(PCY_FULL, v, o); if (lane >= o) v += t; }
+    if (lane == 31) wsum[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+      int u = wsum[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) { const int t = __shfl_up_sync(PCY_FULL, u, o); if (lane >= o) u += t; }
+      wsum[lane] = u;   // inclusive over warps
+    }
+    __syncthreads();
+    if (g < ng) gofs[g] = carry + (warp ? wsum[warp - 1] : 0) + v - c;
+    __syncthreads();
+    if (tid == 0) carry += wsum[31];
+    __syncthreads();
+  }
+  if (tid == 0) *cnt = carry;
+}
+
+// list[gofs[g] + p] = member p of group g (one warp per group)
+__global__ void k_group_scatter(EngDev E, long long ng, int* __restrict__ list) {
+  const int lane = threadIdx.x & 31;
+  const long long g = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (g >= ng) return;
+  const int c = E.g_count[g], b = E.g_base[g], o = E.fs_gofs[g];
+  for (int p = lane; p < c; p += 32) list[o + p] = E.arena[b + p];
+}
 
 // ------------------------------------------------------------------ stage
 // One warp per row: fp32/fp64 -> fp64 padded row, x_sq, validation, hash.
@@ -769,6 +854,11 @@ struct Engine {
   ChainLvl* chr = nullptr;
   double* parts = nullptr;                             // full-set parts matrix (1024 x NC)
   double* gram = nullptr;                              // block Gram (K3 with rows in HBM)
+  bool use_tc = false;                                 // full-set K1 on tcgen05 (split TF32 + recheck)
+  int Kp = 0;
+  double tc_tau = 0.0;
+  float *tc_ahi = nullptr, *tc_alo = nullptr, *tc_bhi = nullptr, *tc_blo = nullptr, *tc_dots = nullptr;
+  double *tc_rnc = nullptr, *tc_xn2 = nullptr, *tc_c = nullptr;
   int nper = 0;          // resolve kernel: 1..8 register rows, 100/101 shared-memory rows, 0 generic
   int nnew_cap = 0, crows = 0;
   size_t res_smem = 0, rea_smem = 0;
@@ -832,6 +922,7 @@ struct Engine {
 #define A_(p, n) if ((rc = alloc(p, n))) return rc
     A_(E.w, NC); A_(E.q, NC); A_(E.sn, NC); A_(E.rn, NC); A_(E.idx, NC);
     A_(E.child, NC); A_(E.alive, NC); A_(E.free_ids, NC);
+    A_(E.fs_list, NC); A_(E.fs_gofs, GC); A_(E.fs_cnt, 1);
     A_(E.s, NC * ld); A_(E.r, NC * ld);
     A_(E.g_base, GC); A_(E.g_count, GC); A_(E.g_cap, GC); A_(E.g_bs, GC); A_(E.g_bsbase, GC);
     A_(E.arena, AC);
@@ -850,8 +941,15 @@ struct Engine {
     A_(aggw, m + 2); A_(mp_nrm, sample_cap + 1);
 #undef A_
     for (auto& e : ev) PCY_CUDA(cudaEventCreate(&e));
+    {
+      const char* tcenv = getenv("PCY_TC_PARTS");
+      use_tc = tcenv ? atoi(tcenv) != 0 : d >= 256;
+      Kp = pcy_tc_pad(d);
+      tc_tau = pcy_tc_error_tau(Kp);
+    }
     const size_t maxsm = 227 * 1024;
-    PCY_CUDA(cudaFuncSetAttribute(k_chain2, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    PCY_CUDA(cudaFuncSetAttribute(k_chain2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    PCY_CUDA(cudaFuncSetAttribute(k_chain2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
     PCY_CUDA(cudaFuncSetAttribute(k_rchain, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
     if (ld <= 256 && !getenv("PCY_SMEM_RESOLVE")) {
       nper = ld <= 32 ? 1 : ld <= 64 ? 2 : ld <= 128 ? 4 : 8;
@@ -863,7 +961,7 @@ struct Engine {
       nnew_cap = (int)cap;
       res_smem = resolve_smem_bytes(ld, nnew_cap, NC, GC, crows);
       rea_smem = resolve_smem_bytes(ld, nnew_cap, NC, GC, 0);
-      if (nnew_cap < 8) nper = 0;
+      if (nnew_cap < 8) { nper = 0; use_tc = false; }
       switch (nper) {
         case 1: PCY_CUDA(cudaFuncSetAttribute(k_resolve2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
                 PCY_CUDA(cudaFuncSetAttribute(k_reattach2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem)); break;
@@ -914,10 +1012,32 @@ struct Engine {
   // parts of the visited groups' members.  Used once the tree is large.
   bool full_set(const double* A, const int* aidx, long long M, cudaStream_t st, int* rc) {
     *rc = PCY_OK;
-    const long long N = ctl_h->F_alloc;
+    E.tc_dots = nullptr;
+    const long long N = ctl_h->F_alloc;   // upper bound on the live columns (device count in fs_cnt)
     if (!nper || N < 256 || getenv("PCY_NO_FULLSET")) return false;
+    const long long ng = ctl_h->G_alloc;
+    k_group_offsets<<<1, 1024, 0, st>>>(E.g_count, ng, E.fs_gofs, E.fs_cnt); pcy_count_launch();
+    k_group_scatter<<<(unsigned)((ng + 7) / 8), 256, 0, st>>>(E, ng, E.fs_list); pcy_count_launch();
+    if (use_tc) {
+      // tensor cores: split-TF32 dots around the block's first row
+      if (!tc_dots) {
+        const long long acap = 1024, bcap = (NC + 127) / 128 * 128;
+        if ((*rc = alloc(tc_ahi, acap * Kp)) || (*rc = alloc(tc_alo, acap * Kp)) || (*rc = alloc(tc_bhi, bcap * Kp)) ||
+            (*rc = alloc(tc_blo, bcap * Kp)) || (*rc = alloc(tc_dots, acap * NC)) || (*rc = alloc(tc_rnc, NC)) ||
+            (*rc = alloc(tc_xn2, acap)) || (*rc = alloc(tc_c, (long long)Kp)))
+          return false;
+      }
+      if ((*rc = pcy_tc_center(A, aidx, ld, d, tc_c, st))) return false;
+      if ((*rc = pcy_tc_split(A, aidx, ld, d, M, nullptr, tc_c, tc_ahi, tc_alo, tc_xn2, st))) return false;
+      if ((*rc = pcy_tc_split(E.r, E.fs_list, ld, d, N, E.fs_cnt, tc_c, tc_bhi, tc_blo, tc_rnc, st))) return false;
+      if ((*rc = pcy_tc_dots(tc_ahi, tc_alo, 1024, (int)M, tc_bhi, tc_blo, (NC + 127) / 128 * 128, (int)N, E.fs_cnt,
+                             Kp, tc_dots, N, st)))
+        return false;
+      E.tc_dots = tc_dots; E.tc_ldo = N; E.tc_rnc = tc_rnc; E.tc_xn2 = tc_xn2; E.tc_tau = tc_tau;
+      return false;   // no fp64 parts matrix: K1 reads E.tc_dots
+    }
     if (!parts) { if ((*rc = alloc(parts, (long long)1024 * NC))) return false; }
-    *rc = pcy_launch_parts(A, aidx, ld, (int)M, E.r, ld, E.rn, (int)N, d, parts, N, st);
+    *rc = pcy_launch_parts(A, aidx, ld, (int)M, E.r, E.fs_list, ld, E.rn, (int)N, E.fs_cnt, d, parts, N, st);
     return true;
   }
 
@@ -1019,9 +1139,13 @@ struct Engine {
           int grc;
           const bool use_p = full_set(Xs, nullptr, nb - start, st, &grc);
           if (grc) return grc;
-          k_chain2<<<nblk, wpc * 32, sizeof(double) * wpc * ld, st>>>(E, Xs, XSs, Ws, nb - start, chh, chr,
-                                                                       use_p ? parts : nullptr,
-                                                                       ctl_h->F_alloc); pcy_count_launch();
+          if (ld > 512)   // one item per CTA, dots split over 4 warps
+            k_chain2<4><<<(unsigned)(nb - start), 128, sizeof(double) * (ld + 8), st>>>(
+                E, Xs, XSs, Ws, nb - start, chh, chr, use_p ? parts : nullptr, ctl_h->F_alloc);
+          else
+            k_chain2<1><<<nblk, wpc * 32, sizeof(double) * wpc * ld, st>>>(E, Xs, XSs, Ws, nb - start, chh, chr,
+                                                                          use_p ? parts : nullptr, ctl_h->F_alloc);
+          pcy_count_launch();
           if (nper == 101) {
             rc0 = pcy_launch_gram(Xs, nullptr, ld, (int)(nb - start), Xs, nullptr, ld, (int)(nb - start), d, gram,
                                   nb - start, st);

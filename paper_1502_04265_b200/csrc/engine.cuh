@@ -55,6 +55,12 @@ struct EngDev {
   // bootstrap
   double* pend_x; long long* pend_w; double* pend_xsq; long long pend_cap;
   double* dist_x; int* htab; long long hcap;
+  // full-set K1 on the tensor cores (tc_dots.cu): 3xTF32 dots of the block
+  // against every slot, centred norms and the error factor; null when unused
+  const float* tc_dots; long long tc_ldo; const double* tc_rnc; const double* tc_xn2; double tc_tau;
+  // column order of the full-set contraction: group g's members occupy the
+  // contiguous columns [fs_gofs[g], fs_gofs[g] + g_count[g]) (fs_list = slots)
+  int* fs_list; int* fs_gofs; int* fs_cnt;
   // rebuild / extraction scratch
   int* order; int* lvl; int* stk_g; int* stk_p;
   unsigned long long* minbits;

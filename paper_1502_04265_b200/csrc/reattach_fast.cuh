@@ -27,11 +27,14 @@ __global__ void k_rchain(EngDev E, const int* __restrict__ order, long long n, C
   const double T = E.ctl->T;
   ChainLvl* rec = R + i * PCY_FMAXL;
   double radius = T;
-  int g = 0, L = 0, pred = -1, predj = -1, trunc = 0;
+  int g = 0, L = 0, pred = -1, predj = -1, trunc = 0, nre = 0;
   for (;;) {
     const int cnt = E.g_count[g], base = E.g_base[g];
     double bp; int bpos;
-    if (P) scan_parts(P + i * ldp, E.arena + base, cnt, lane, bp, bpos);
+    if (E.tc_dots)   // tensor-core dots + near-tie recheck
+      scan_parts_tc(E, i, g, E.arena + base, cnt, [&](int jj) { return warp_dot(E.r + (long long)jj * ld, xv, d, lane); },
+                    lane, bp, bpos, nre);
+    else if (P) scan_parts(P + i * ldp + E.fs_gofs[g], cnt, lane, bp, bpos);   // parts from the DMMA contraction
     else scan_members(E, E.arena + base, 0, cnt, xv, lane, bp, bpos);
     const int j = bpos < cnt ? E.arena[base + bpos] : -1;
     ChainLvl c = empty_level();
@@ -66,6 +69,7 @@ __global__ void k_rchain(EngDev E, const int* __restrict__ order, long long n, C
   }
   if (pred < 0) pred = L - 1;
   if (lane == 0) H[i] = ChainHdr{L, pred, predj, trunc};
+  if (lane == 0 && nre > 0) atomicAdd((unsigned long long*)&E.ctl->cnt_direct, (unsigned long long)nre);
 }
 
 template <int NPER>

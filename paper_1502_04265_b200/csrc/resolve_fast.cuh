@@ -56,34 +56,52 @@ __device__ __forceinline__ long long capacity(long long nn, double qv, double sn
 }
 
 // ------------------------------------------------------------------- K1
+template <int WPI>
 __global__ void k_chain2(EngDev E, const double* __restrict__ X, const double* __restrict__ XS,
                          const long long* __restrict__ W, long long n, ChainHdr* __restrict__ H,
                          ChainLvl* __restrict__ R, const double* __restrict__ P, long long ldp) {
+  // WPI == 1: one warp per item, several items per CTA.  WPI > 1: one item per
+  // CTA; every warp walks the same chain (identical decisions) and the fp64
+  // dots are split over the warps (cta_dot), for large d.
   extern __shared__ double sm_x[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const long long i = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
+  const long long i = WPI == 1 ? (long long)blockIdx.x * (blockDim.x >> 5) + wib : (long long)blockIdx.x;
   if (i >= n) return;
   const int d = E.d, ld = E.ld;
-  double* xv = sm_x + (long long)wib * ld;
+  double* xv = WPI == 1 ? sm_x + (long long)wib * ld : sm_x;
+  double* red = sm_x + ld;
+  const bool writer = lane == 0 && (WPI == 1 || wib == 0);
+  auto xdot = [&](const double* row) -> double {
+    if constexpr (WPI == 1) return warp_dot(row, xv, d, lane);
+    else return cta_dot<WPI>(row, xv, d, lane, wib, red);
+  };
   const double xs = XS[i];
   ChainLvl* rec = R + i * PCY_FMAXL;
-  if (!isfinite(xs)) { if (lane == 0) H[i] = ChainHdr{0, 0, -1, 0}; return; }
-  for (int e = lane; e < d; e += 32) xv[e] = X[i * ld + e];
-  __syncwarp();
+  if (!isfinite(xs)) { if (writer) H[i] = ChainHdr{0, 0, -1, 0}; return; }
+  if constexpr (WPI == 1) {
+    for (int e = lane; e < d; e += 32) xv[e] = X[i * ld + e];
+    __syncwarp();
+  } else {
+    for (int e = threadIdx.x; e < d; e += blockDim.x) xv[e] = X[i * ld + e];
+    __syncthreads();
+  }
   const double T = E.ctl->T;
   const long long rem = W ? W[i] : 1LL;
   double radius = T;
-  int g = 0, L = 0, pred = -1, predj = -1, trunc = 0;
+  int g = 0, L = 0, pred = -1, predj = -1, trunc = 0, nre = 0;
   for (;;) {
     const int cnt = E.g_count[g], base = E.g_base[g];
     double bp; int bpos;
-    if (P) scan_parts(P + i * ldp, E.arena + base, cnt, lane, bp, bpos);   // parts from the DMMA contraction
+    if (E.tc_dots)   // tensor-core dots + near-tie recheck
+      scan_parts_tc(E, i, g, E.arena + base, cnt, [&](int jj) { return xdot(E.r + (long long)jj * ld); }, lane, bp,
+                    bpos, nre);
+    else if (P) scan_parts(P + i * ldp + E.fs_gofs[g], cnt, lane, bp, bpos);   // DMMA parts
     else scan_members(E, E.arena + base, 0, cnt, xv, lane, bp, bpos);
     const int j = bpos < cnt ? E.arena[base + bpos] : -1;
     ChainLvl c = empty_level();
     c.part = bp; c.j = j; c.g = g;
     if (j >= 0) {
-      c.dot = warp_dot(E.s + (long long)j * ld, xv, d, lane);
+      c.dot = xdot(E.s + (long long)j * ld);
       c.w = E.w[j]; c.q = E.q[j]; c.sn = E.sn[j]; c.child = E.child[j];
     }
     ++L;
@@ -97,11 +115,11 @@ __global__ void k_chain2(EngDev E, const double* __restrict__ X, const double* _
         if (pred < 0) { pred = L - 1; predj = j; }
       }
     }
-    if (lane == 0) rec[L - 1] = c;
+    if (writer) rec[L - 1] = c;
     if (outside) { if (pred < 0) pred = L - 1; break; }
     if (c.child < 0) {
       if (L < PCY_FMAXL) {
-        if (lane == 0) rec[L] = empty_level();
+        if (writer) rec[L] = empty_level();
         ++L;
         if (pred < 0) pred = L - 1;
       } else trunc = 1;
@@ -112,7 +130,8 @@ __global__ void k_chain2(EngDev E, const double* __restrict__ X, const double* _
     radius = rmul(radius, 0.25);
   }
   if (pred < 0) pred = L - 1;
-  if (lane == 0) H[i] = ChainHdr{L, pred, predj, trunc};
+  if (writer) H[i] = ChainHdr{L, pred, predj, trunc};
+  if (writer && nre > 0) atomicAdd((unsigned long long*)&E.ctl->cnt_direct, (unsigned long long)nre);
 }
 
 // ------------------------------------------------------------------- K3

@@ -22,9 +22,7 @@ __device__ __forceinline__ void row_fetch(double* dst, const double* src, int ld
 }
 // lane-strided fp64 dot in warp_dot order (shared with K1's snapshot dots)
 __device__ __forceinline__ double row_dot(const double* a, const double* b, int d, int lane) {
-  double acc = 0.0;
-  for (int e = lane; e < d; e += 32) acc = fma(a[e], b[e], acc);
-  return warp_sum(acc);
+  return warp_dot(a, b, d, lane);   // same lane-strided order, loads issued ahead
 }
 
 template <int MS>
