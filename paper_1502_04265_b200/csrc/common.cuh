@@ -20,6 +20,9 @@ cudaError_t pcy_spin_sync(cudaStream_t st);
 // Device -> host copy of a small result through a thread-local pinned
 // staging buffer, completed with pcy_spin_sync.
 cudaError_t pcy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t st);
+int pcy_launch_assign_d2(const double* P, long long ldp, int n, const double* pn, const double* C, long long ldc,
+                         const double* cn, int k, int d, double* ppart, int* ppos, int* assign, double* best,
+                         cudaStream_t st);
 // split-TF32 distance contraction on tcgen05 (tc_dots.cu)
 double pcy_tc_error_tau(int Kp);
 int pcy_tc_pad(int d);

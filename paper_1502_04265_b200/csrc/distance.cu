@@ -26,7 +26,8 @@ __global__ void __launch_bounds__(128) k_dist_tile(int M, int N, int K,
                                                   const double* __restrict__ rn,
                                                   double* __restrict__ C, long long ldc,
                                                   double* __restrict__ ppart, int* __restrict__ ppos, int ntiles,
-                                                  const int* __restrict__ n_dev = nullptr) {
+                                                  const int* __restrict__ n_dev = nullptr,
+                                                  const double* __restrict__ rv = nullptr) {
   __shared__ double As[2][DBM][DBK + 4];
   __shared__ double Bs[2][DBK][DBN + 4];
   __shared__ long long arow[DBM], brow[DBN];
@@ -113,17 +114,23 @@ __global__ void __launch_bounds__(128) k_dist_tile(int M, int N, int K,
         }
     return;
   }
-  // MODE 1: argmin over this tile's 64 columns per row, lowest column on ties
+  // MODE 1: argmin of rn[n] - 2 g over this tile's 64 columns per row;
+  // MODE 3: argmin of max(((-2 g) + rv[m]) + rn[n], 0) (evaluation.py:41-46);
+  // lowest column on ties
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     double bp = INFINITY; int bc = 0x7fffffff;
+    double rvm = 0.0;
+    if (MODE == 3) { const int mm = m0 + wm + i * 8 + g; rvm = mm < M ? rv[mm] : 0.0; }
 #pragma unroll
     for (int j = 0; j < 4; ++j)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int cl = wn + j * 8 + 2 * t4 + h;
         if (n0 + cl < N) {
-          const double p = radd(s_rn[cl], rmul(acc[i][j][h], -2.0));
+          double p;
+          if (MODE == 3) { p = radd(radd(rmul(-2.0, acc[i][j][h]), rvm), s_rn[cl]); if (p < 0.0) p = 0.0; }
+          else p = radd(s_rn[cl], rmul(acc[i][j][h], -2.0));
           if (p < bp || (p == bp && cl < bc)) { bp = p; bc = cl; }
         }
       }
@@ -202,6 +209,24 @@ int pcy_launch_nearest(const double* A, const int* aidx, long long lda, int M, c
   k_dist_tile<1><<<grid, 128, 0, st>>>(M, N, K, A, aidx, lda, B, bidx, ldb, rn, nullptr, 0, ppart, ppos, ntiles);
   pcy_count_launch();
   k_argmin_reduce<<<(unsigned)((M + 7) / 8), 256, 0, st>>>(M, ntiles, ppart, ppos, out_pos, out_part);
+  pcy_count_launch();
+  PCY_LAUNCH_CHECK();
+  return PCY_OK;
+}
+
+// Lloyd assignment (evaluation.py:104-107): assign[m] = first argmin over
+// centres of max(((-2 P C^T) + pn) + cn, 0), best[m] = that value.  Scratch
+// ppart / ppos of n x ceil(k/64).
+int pcy_launch_assign_d2(const double* P, long long ldp, int n, const double* pn, const double* C, long long ldc,
+                         const double* cn, int k, int d, double* ppart, int* ppos, int* assign, double* best,
+                         cudaStream_t st) {
+  if (n <= 0 || k <= 0) return PCY_OK;
+  const int ntiles = (k + DBN - 1) / DBN;
+  dim3 grid((unsigned)ntiles, (unsigned)((n + DBM - 1) / DBM));
+  k_dist_tile<3><<<grid, 128, 0, st>>>(n, k, d, P, nullptr, ldp, C, nullptr, ldc, cn, nullptr, 0, ppart, ppos, ntiles,
+                                      nullptr, pn);
+  pcy_count_launch();
+  k_argmin_reduce<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(n, ntiles, ppart, ppos, assign, best);
   pcy_count_launch();
   PCY_LAUNCH_CHECK();
   return PCY_OK;

@@ -9,8 +9,11 @@
 // All sums are fixed-order (no float atomics) so repeated runs are bitwise
 // deterministic, like the reference.
 #include <cmath>
+#include <algorithm>
 #include <vector>
 #include "common.cuh"
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -55,29 +58,50 @@ __device__ __forceinline__ double block_exscan(double v, double* red, double* to
   return red[32 + wid] + (inc - v);
 }
 
-// _draw: first index i with cumsum(mass)[i] > u * cumsum[-1], clamped to n-1.
-// Each thread owns a contiguous chunk; the running sum inside a chunk is
-// sequential, chunk offsets come from the block scan.
-__device__ int block_draw(const double* __restrict__ mass, long long n, double u, double* red, int* ired) {
-  const long long per = (n + blockDim.x - 1) / blockDim.x;
-  const long long a = (long long)threadIdx.x * per, b = min(n, a + per);
+// Cooperative k-means++ (all repetitions in one persistent launch).  Points
+// are split into chunks of KS_CHUNK in index order; the cumulative mass of
+// point i is  sum(chunk totals before its chunk) + sum(masses in its chunk up
+// to i), every sum in a fixed order, so the draw is deterministic.
+//   phase A (all CTAs, one chunk per CTA iteration, warp per point): the
+//     diff-form distance of each point to every repetition's newest centre
+//     (:74-75, :80-81), best = min(best, dist), mass = w * best, chunk totals;
+//     each point row is read once for all repetitions (the HBM-bound pass)
+//   phase B (CTA r < reps): _draw (:49-53) of repetition r from the chunk
+//     totals, falling back to the weights when the mass is all zero (:77-78),
+//     and the pick copied into the centre list.
+constexpr int KS_THREADS = 512, KS_CHUNK = 64, KS_RMAX = 8;
+
+__device__ int chunk_draw(const double* __restrict__ part, long long nch, const double* __restrict__ vals,
+                          long long n, double u, double* red, int* ired, double* s_tot) {
+  // prefix over chunk totals: thread t owns a contiguous run of chunks
+  const long long per = (nch + blockDim.x - 1) / blockDim.x;
+  const long long a = (long long)threadIdx.x * per, b = min(nch, a + per);
   double loc = 0.0;
-  for (long long i = a; i < b; ++i) loc += mass[i];
+  for (long long c = a; c < b; ++c) loc += part[c];
   double total;
   const double pre = block_exscan(loc, red, &total);
+  if (threadIdx.x == 0) *s_tot = total;
   const double target = rmul(u, total);
-  int cand = 0x7fffffff;
-  double c = pre;
-  for (long long i = a; i < b; ++i) {
-    c += mass[i];
-    if (c > target) { cand = (int)i; break; }
+  long long cand = 0x7fffffffffffLL;
+  double cum = pre;
+  for (long long c = a; c < b; ++c) {
+    if (cum + part[c] > target) {
+      // inside chunk c: sequential over its points
+      const long long p0 = c * KS_CHUNK, p1 = min(n, p0 + KS_CHUNK);
+      double cc = cum;
+      for (long long i = p0; i < p1; ++i) {
+        cc += vals[i];
+        if (cc > target) { cand = i; break; }
+      }
+      if (cand != 0x7fffffffffffLL) break;
+    }
+    cum += part[c];
   }
-  // min over threads
-  int v = cand;
+  long long v = cand;
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) v = min(v, __shfl_xor_sync(PCY_FULL, v, o));
   __syncthreads();
-  if ((threadIdx.x & 31) == 0) ired[threadIdx.x >> 5] = v;
+  if ((threadIdx.x & 31) == 0) ired[threadIdx.x >> 5] = (int)min(v, (long long)0x7fffffff);
   __syncthreads();
   int r = 0x7fffffff;
   for (int k = 0; k < (int)(blockDim.x >> 5); ++k) r = min(r, ired[k]);
@@ -85,52 +109,111 @@ __device__ int block_draw(const double* __restrict__ mass, long long n, double u
   return r == 0x7fffffff ? (int)(n - 1) : r;
 }
 
-// One CTA per repetition.  best[] and mass[] are per-rep scratch (n each).
-__global__ void __launch_bounds__(KM_THREADS) k_seed(const double* __restrict__ P, const double* __restrict__ w,
-                                                    long long n, int d, int k, const double* __restrict__ U,
-                                                    double* __restrict__ centers, double* __restrict__ best_all,
-                                                    double* __restrict__ mass_all, int* __restrict__ picks) {
-  extern __shared__ double cv[];
+__global__ void __launch_bounds__(KS_THREADS) k_seed_coop(const double* __restrict__ P, const double* __restrict__ w,
+                                                         long long n, int d, int k, int reps,
+                                                         const double* __restrict__ U, double* __restrict__ centers,
+                                                         double* __restrict__ best_all, double* __restrict__ mass_all,
+                                                         double* __restrict__ part_all, double* __restrict__ wpart,
+                                                         int* __restrict__ picks, int rg) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double ks_smem[];
+  double* cs = ks_smem;                          // rg x d newest centres
+  double* ms = ks_smem + (long long)rg * d;      // rg x KS_CHUNK chunk masses
   __shared__ double red[72];
   __shared__ int ired[32];
-  __shared__ int s_pos;
-  const int rep = blockIdx.x;
-  const double* u = U + (long long)rep * k;
-  double* best = best_all + (long long)rep * n;
-  double* mass = mass_all + (long long)rep * n;
-  double* C = centers + (long long)rep * k * d;
+  __shared__ double s_tot;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = KS_THREADS / 32;
+  const long long nch = (n + KS_CHUNK - 1) / KS_CHUNK;
+  // weight chunk totals (the fallback / first draw), fixed order
+  for (long long c = blockIdx.x; c < nch; c += gridDim.x) {
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (long long i = c * KS_CHUNK; i < min(n, (c + 1) * KS_CHUNK); ++i) t += w[i];
+      wpart[c] = t;
+    }
+  }
+  grid.sync();
   for (int j = 0; j < k; ++j) {
-    int idx;
-    if (j == 0) {
-      idx = block_draw(w, n, u[0], red, ired);
-    } else {
-      // mass = w * best; draw from it unless it sums to zero (:77-78).  The
-      // sum of nonnegative terms is positive iff some term is positive.
-      if (threadIdx.x == 0) s_pos = 0;
-      __syncthreads();
-      for (long long i = threadIdx.x; i < n; i += blockDim.x) {
-        const double mv = rmul(w[i], best[i]);
-        mass[i] = mv;
-        if (mv > 0.0) s_pos = 1;
+    // phase B: draw centre j of every repetition
+    for (int r = blockIdx.x; r < reps; r += gridDim.x) {
+      int idx;
+      if (j == 0) {
+        idx = chunk_draw(wpart, nch, w, n, U[(long long)r * k], red, ired, &s_tot);
+      } else {
+        const double* part = part_all + (long long)r * nch;
+        idx = chunk_draw(part, nch, mass_all + (long long)r * n, n, U[(long long)r * k + j], red, ired, &s_tot);
+        __syncthreads();
+        if (!(s_tot > 0.0)) idx = chunk_draw(wpart, nch, w, n, U[(long long)r * k + j], red, ired, &s_tot);
       }
+      if (threadIdx.x == 0) picks[r * k + j] = idx;
+      double* C = centers + ((long long)r * k + j) * d;
+      for (int e = threadIdx.x; e < d; e += blockDim.x) C[e] = P[(long long)idx * d + e];
       __syncthreads();
-      idx = block_draw(s_pos ? mass : w, n, u[j], red, ired);
     }
-    if (threadIdx.x == 0) picks[rep * k + j] = idx;
-    for (int e = threadIdx.x; e < d; e += blockDim.x) {
-      const double v = P[(long long)idx * d + e];
-      cv[e] = v;
-      C[(long long)j * d + e] = v;
+    if (j == k - 1) break;
+    grid.sync();
+    // phase A: distances to the new centres, mass, chunk totals.  The newest
+    // centres of a group of rg repetitions are staged in shared memory; each
+    // point row is streamed from HBM once per group.
+    for (int r0 = 0; r0 < reps; r0 += rg) {
+      const int rn = min(rg, reps - r0);
+      __syncthreads();
+      for (int q = 0; q < rn; ++q)
+        for (int e = threadIdx.x; e < d; e += blockDim.x) cs[(long long)q * d + e] = centers[((long long)(r0 + q) * k + j) * d + e];
+      __syncthreads();
+      for (long long c = blockIdx.x; c < nch; c += gridDim.x) {
+        const long long p0 = c * KS_CHUNK, p1 = min(n, p0 + KS_CHUNK);
+        for (long long i = p0 + warp; i < p1; i += nwarp) {
+          const double* p = P + i * d;
+          double acc[KS_RMAX];
+#pragma unroll
+          for (int q = 0; q < KS_RMAX; ++q) acc[q] = 0.0;
+          // 8 row elements in flight per lane; each repetition still sums its
+          // elements in increasing e order
+          int e = lane;
+          for (; e + 7 * 32 < d; e += 8 * 32) {
+            double pv[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) pv[t] = p[e + 32 * t];
+#pragma unroll
+            for (int q = 0; q < KS_RMAX; ++q)
+              if (q < rn) {
+                const double* cq = cs + (long long)q * d + e;
+#pragma unroll
+                for (int t = 0; t < 8; ++t) { const double df = rsub(pv[t], cq[32 * t]); acc[q] = fma(df, df, acc[q]); }
+              }
+          }
+          for (; e < d; e += 32) {
+            const double pe = p[e];
+#pragma unroll
+            for (int q = 0; q < KS_RMAX; ++q)
+              if (q < rn) { const double df = rsub(pe, cs[(long long)q * d + e]); acc[q] = fma(df, df, acc[q]); }
+          }
+#pragma unroll
+          for (int q = 0; q < KS_RMAX; ++q) {
+            if (q >= rn) break;
+            const double a = warp_sum(acc[q]);
+            if (lane == 0) {
+              const int r = r0 + q;
+              double* best = best_all + (long long)r * n;
+              const double b = j == 0 ? a : fmin(best[i], a);
+              best[i] = b;
+              const double mv = rmul(w[i], b);
+              mass_all[(long long)r * n + i] = mv;
+              ms[q * KS_CHUNK + (int)(i - p0)] = mv;
+            }
+          }
+        }
+        __syncthreads();
+        for (int q = threadIdx.x; q < rn; q += blockDim.x) {
+          double t = 0.0;
+          for (long long i = p0; i < p1; ++i) t += ms[q * KS_CHUNK + (int)(i - p0)];
+          part_all[(long long)(r0 + q) * nch + c] = t;
+        }
+        __syncthreads();
+      }
     }
-    __syncthreads();
-    // best = min(best, |p - c|^2), diff form (:74-75, :80-81)
-    for (long long i = threadIdx.x; i < n; i += blockDim.x) {
-      const double* p = P + i * d;
-      double acc = 0.0;
-      for (int e = 0; e < d; ++e) { const double df = rsub(p[e], cv[e]); acc = fma(df, df, acc); }
-      best[i] = j == 0 ? acc : fmin(best[i], acc);
-    }
-    __syncthreads();
+    grid.sync();
   }
 }
 
@@ -143,98 +226,93 @@ __global__ void k_rownorm(const double* __restrict__ X, long long n, int d, doub
   if (lane == 0) out[i] = v;
 }
 
-// Assignment: warp per (point, rep).  d2 = max(((-2 g) + pn) + cn, 0),
-// first minimum wins (:41-46, :105-107).
-__global__ void k_assign(const double* __restrict__ P, const double* __restrict__ pn, long long n, int d, int k,
-                         const double* __restrict__ centers, const double* __restrict__ cn,
-                         const int* __restrict__ active, int* __restrict__ assign, double* __restrict__ bestd) {
+// Empty-cluster repair (:109-124), one round for every repetition that needs
+// it.  k_counts_empty (CTA per rep): occupancy counts; the first empty centre
+// `emp`; far = first argmax of w * best; when that gain is positive the centre
+// becomes P[far] and rep_state = {emp, far}, otherwise (or with no empty
+// centre) the repetition's repair is over (emp = -1).
+__global__ void __launch_bounds__(KM_THREADS) k_counts_empty(const double* __restrict__ P,
+                                                            const double* __restrict__ w, long long n, int d, int k,
+                                                            double* __restrict__ centers, const int* __restrict__ active,
+                                                            const int* __restrict__ assign_all,
+                                                            const double* __restrict__ best_all,
+                                                            int* __restrict__ counts_all, int* __restrict__ rep_state) {
+  __shared__ int s_empty, s_far;
+  __shared__ double s_gmax;
+  __shared__ double wg[32];
+  __shared__ long long wi[32];
+  const int rep = blockIdx.x;
+  if (active && !active[rep]) { if (threadIdx.x == 0) rep_state[2 * rep] = -1; return; }
+  const int* assign = assign_all + (long long)rep * n;
+  const double* best = best_all + (long long)rep * n;
+  int* counts = counts_all + (long long)rep * k;
+  double* C = centers + (long long)rep * k * d;
+  for (int j = threadIdx.x; j < k; j += blockDim.x) counts[j] = 0;
+  __syncthreads();
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&counts[assign[i]], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s_empty = -1;
+    for (int j = 0; j < k; ++j) if (counts[j] == 0) { s_empty = j; break; }
+  }
+  __syncthreads();
+  if (s_empty < 0) { if (threadIdx.x == 0) rep_state[2 * rep] = -1; return; }
+  double gv = -INFINITY; long long gi = 0x7fffffffffffLL;
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+    const double g = rmul(w[i], best[i]);
+    if (g > gv) { gv = g; gi = i; }
+  }
+  for (int o = 16; o >= 1; o >>= 1) {
+    const double og = __shfl_xor_sync(PCY_FULL, gv, o);
+    const long long oi = __shfl_xor_sync(PCY_FULL, gi, o);
+    if (og > gv || (og == gv && oi < gi)) { gv = og; gi = oi; }
+  }
+  if ((threadIdx.x & 31) == 0) { wg[threadIdx.x >> 5] = gv; wi[threadIdx.x >> 5] = gi; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double bg = -INFINITY; long long bi = 0x7fffffffffffLL;
+    for (int t = 0; t < (int)(blockDim.x >> 5); ++t)
+      if (wg[t] > bg || (wg[t] == bg && wi[t] < bi)) { bg = wg[t]; bi = wi[t]; }
+    s_gmax = bg; s_far = (int)bi;
+  }
+  __syncthreads();
+  if (!(s_gmax > 0.0)) { if (threadIdx.x == 0) rep_state[2 * rep] = -1; return; }   // every point on a centre
+  const int emp = s_empty, far = s_far;
+  for (int e = threadIdx.x; e < d; e += blockDim.x) C[(long long)emp * d + e] = P[(long long)far * d + e];
+  if (threadIdx.x == 0) { rep_state[2 * rep] = emp; rep_state[2 * rep + 1] = far; }
+}
+
+// Points closer to the re-seeded centre move to it (diff form); the far point
+// itself sits on it.  Grid over points x repetitions, warp per point.
+__global__ void k_repair_dist(const double* __restrict__ P, long long n, int d, int k,
+                              const double* __restrict__ centers, const int* __restrict__ rep_state,
+                              int* __restrict__ assign_all, double* __restrict__ best_all) {
   const int lane = threadIdx.x & 31;
   const long long i = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int rep = blockIdx.y;
-  if (i >= n || (active && !active[rep])) return;
+  const int emp = rep_state[2 * rep], far = rep_state[2 * rep + 1];
+  if (i >= n || emp < 0) return;
   const double* p = P + i * d;
-  const double* C = centers + (long long)rep * k * d;
-  const double* cnr = cn + (long long)rep * k;
-  double bv = INFINITY; int bj = 0;
-  for (int j = 0; j < k; ++j) {
-    const double g = warp_dot(p, C + (long long)j * d, d, lane);
-    double v = radd(radd(rmul(-2.0, g), pn[i]), cnr[j]);
-    if (v < 0.0) v = 0.0;
-    if (v < bv) { bv = v; bj = j; }
-  }
+  const double* c = centers + ((long long)rep * k + emp) * d;
+  double acc = 0.0;
+  for (int e = lane; e < d; e += 32) { const double df = rsub(p[e], c[e]); acc = fma(df, df, acc); }
+  acc = warp_sum(acc);
   if (lane == 0) {
-    assign[(long long)rep * n + i] = bj;
-    bestd[(long long)rep * n + i] = bv;
+    int* assign = assign_all + (long long)rep * n;
+    double* best = best_all + (long long)rep * n;
+    if (i == far) { assign[i] = emp; best[i] = 0.0; }
+    else if (acc < best[i]) { assign[i] = emp; best[i] = acc; }
   }
 }
 
-// Per rep: occupancy, empty-cluster repair (:109-124), cost = w . best (:126).
-// One CTA per rep.  repair=0 computes only the cost (weighted_cost).
-__global__ void __launch_bounds__(KM_THREADS) k_finish(const double* __restrict__ P, const double* __restrict__ w,
-                                                      long long n, int d, int k, double* __restrict__ centers,
-                                                      const int* __restrict__ active, int* __restrict__ assign_all,
-                                                      double* __restrict__ best_all, int* __restrict__ counts_all,
-                                                      double* __restrict__ cost_out, int repair) {
+// cost = w . best per repetition (:126), fixed order (chunked then tree).
+__global__ void __launch_bounds__(KM_THREADS) k_cost(const double* __restrict__ w, long long n,
+                                                    const int* __restrict__ active,
+                                                    const double* __restrict__ best_all, double* __restrict__ cost_out) {
   __shared__ double red[72];
-  __shared__ int s_empty, s_far;
-  __shared__ double s_gmax;
   const int rep = blockIdx.x;
   if (active && !active[rep]) return;
-  int* assign = assign_all + (long long)rep * n;
-  double* best = best_all + (long long)rep * n;
-  int* counts = counts_all + (long long)rep * k;
-  double* C = centers + (long long)rep * k * d;
-  if (repair) {
-    for (;;) {
-      for (int j = threadIdx.x; j < k; j += blockDim.x) counts[j] = 0;
-      __syncthreads();
-      for (long long i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&counts[assign[i]], 1);
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        s_empty = -1;
-        for (int j = 0; j < k; ++j) if (counts[j] == 0) { s_empty = j; break; }
-      }
-      __syncthreads();
-      if (s_empty < 0) break;
-      // far = first argmax of w * best
-      double gv = -INFINITY; long long gi = 0x7fffffffffffLL;
-      for (long long i = threadIdx.x; i < n; i += blockDim.x) {
-        const double g = rmul(w[i], best[i]);
-        if (g > gv) { gv = g; gi = i; }
-      }
-      // block argmax with lowest index on ties
-      for (int o = 16; o >= 1; o >>= 1) {
-        const double og = __shfl_xor_sync(PCY_FULL, gv, o);
-        const long long oi = __shfl_xor_sync(PCY_FULL, gi, o);
-        if (og > gv || (og == gv && oi < gi)) { gv = og; gi = oi; }
-      }
-      __shared__ double wg[32]; __shared__ long long wi[32];
-      if ((threadIdx.x & 31) == 0) { wg[threadIdx.x >> 5] = gv; wi[threadIdx.x >> 5] = gi; }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        double bg = -INFINITY; long long bi = 0x7fffffffffffLL;
-        for (int t = 0; t < (int)(blockDim.x >> 5); ++t)
-          if (wg[t] > bg || (wg[t] == bg && wi[t] < bi)) { bg = wg[t]; bi = wi[t]; }
-        s_gmax = bg; s_far = (int)bi;
-      }
-      __syncthreads();
-      if (!(s_gmax > 0.0)) break;   // every point sits on a center
-      const int emp = s_empty, far = s_far;
-      for (int e = threadIdx.x; e < d; e += blockDim.x) C[(long long)emp * d + e] = P[(long long)far * d + e];
-      __syncthreads();
-      for (long long i = threadIdx.x; i < n; i += blockDim.x) {
-        const double* p = P + i * d;
-        const double* c = C + (long long)emp * d;
-        double acc = 0.0;
-        for (int e = 0; e < d; ++e) { const double df = rsub(p[e], c[e]); acc = fma(df, df, acc); }
-        if (acc < best[i]) { assign[i] = emp; best[i] = acc; }
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) { assign[far] = emp; best[far] = 0.0; }
-      __syncthreads();
-    }
-  }
-  // cost = w . best in fixed order (chunked then tree)
+  const double* best = best_all + (long long)rep * n;
   const long long per = (n + blockDim.x - 1) / blockDim.x;
   const long long a = (long long)threadIdx.x * per, b = min(n, a + per);
   double loc = 0.0;
@@ -302,13 +380,30 @@ int pcy_kmeanspp(const double* P, const double* w, long long n, int d, int k, in
                  double* centers, long long* picks_out, void* stream) {
   if (n < 1 || k < 1 || d < 1 || reps < 1) { pcy_set_error("kmeanspp: bad sizes"); return PCY_EINVAL; }
   cudaStream_t st = (cudaStream_t)stream;
-  double *best = nullptr, *mass = nullptr; int* picks = nullptr;
+  double *best = nullptr, *mass = nullptr, *part = nullptr, *wpart = nullptr; int* picks = nullptr;
+  const long long nch = (n + KS_CHUNK - 1) / KS_CHUNK;
   PCY_CUDA(pcy_malloc_async(&best, sizeof(double) * n * reps, st));
   PCY_CUDA(pcy_malloc_async(&mass, sizeof(double) * n * reps, st));
+  PCY_CUDA(pcy_malloc_async(&part, sizeof(double) * nch * reps, st));
+  PCY_CUDA(pcy_malloc_async(&wpart, sizeof(double) * nch, st));
   PCY_CUDA(pcy_malloc_async(&picks, sizeof(int) * k * reps, st));
-  const size_t sm = sizeof(double) * d;
-  if (sm > 48 * 1024) PCY_CUDA(cudaFuncSetAttribute(k_seed, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  k_seed<<<reps, KM_THREADS, sm, st>>>(P, w, n, d, k, U, centers, best, mass, picks); pcy_count_launch();
+  // centres of rg repetitions per shared-memory pass (<= 200 KB with the chunk masses)
+  const size_t budget = 200 * 1024;
+  int rg = (int)std::min<long long>(std::min(reps, KS_RMAX), (long long)(budget / (sizeof(double) * (d + KS_CHUNK))));
+  if (rg < 1) { pcy_set_error("kmeanspp: dimension too large for the seeding kernel"); return PCY_EINVAL; }
+  const size_t sm = sizeof(double) * ((size_t)rg * d + (size_t)rg * KS_CHUNK);
+  PCY_CUDA(cudaFuncSetAttribute(k_seed_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  int dev = 0, sms = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_seed_coop, KS_THREADS, sm);
+  const long long max_blocks = (long long)sms * (per > 0 ? per : 1);
+  long long blocks = std::max<long long>(std::min<long long>(nch, max_blocks), std::min<long long>(reps, max_blocks));
+  int nb = (int)blocks;
+  long long n_ = n; int d_ = d, k_ = k, reps_ = reps;
+  void* args[] = {(void*)&P, (void*)&w, &n_, &d_, &k_, &reps_, (void*)&U, &centers, &best, &mass, &part, &wpart, &picks, &rg};
+  PCY_CUDA(cudaLaunchCooperativeKernel((const void*)k_seed_coop, dim3(nb), dim3(KS_THREADS), args, sm, st));
+  pcy_count_launch();
   PCY_LAUNCH_CHECK();
   if (picks_out) {
     std::vector<int> h((size_t)k * reps);
@@ -317,6 +412,8 @@ int pcy_kmeanspp(const double* P, const double* w, long long n, int d, int k, in
   }
   PCY_CUDA(cudaFreeAsync(best, st));
   PCY_CUDA(cudaFreeAsync(mass, st));
+  PCY_CUDA(cudaFreeAsync(part, st));
+  PCY_CUDA(cudaFreeAsync(wpart, st));
   PCY_CUDA(cudaFreeAsync(picks, st));
   return PCY_OK;
 }
@@ -336,6 +433,12 @@ int pcy_lloyd(const double* P, const double* w, long long n, int d, int k, int r
   PCY_CUDA(pcy_malloc_async(&counts, sizeof(int) * k * reps, st));
   PCY_CUDA(pcy_malloc_async(&cost, sizeof(double) * reps, st));
   PCY_CUDA(pcy_malloc_async(&active, sizeof(int) * reps, st));
+  const int ntiles = (k + 63) / 64;
+  double* ppart = nullptr; int* ppos = nullptr; int* rstate = nullptr;
+  PCY_CUDA(pcy_malloc_async(&ppart, sizeof(double) * n * ntiles, st));
+  PCY_CUDA(pcy_malloc_async(&ppos, sizeof(int) * n * ntiles, st));
+  PCY_CUDA(pcy_malloc_async(&rstate, sizeof(int) * 2 * reps, st));
+  std::vector<int> hstate(2 * reps);
   std::vector<int> act(reps, 1);
   std::vector<double> prev(reps, INFINITY), hc(reps);
   for (int r = 0; r < reps; ++r) iters_out[r] = 0;
@@ -348,8 +451,24 @@ int pcy_lloyd(const double* P, const double* w, long long n, int d, int k, int r
     if (!nact) break;
     PCY_CUDA(cudaMemcpyAsync(active, act.data(), sizeof(int) * reps, cudaMemcpyHostToDevice, st));
     k_rownorm<<<(unsigned)((k * reps + 7) / 8), 256, 0, st>>>(centers, (long long)k * reps, d, cn); pcy_count_launch();
-    k_assign<<<dim3((unsigned)((n + 7) / 8), reps), 256, 0, st>>>(P, pn, n, d, k, centers, cn, active, assign, best); pcy_count_launch();
-    k_finish<<<reps, KM_THREADS, 0, st>>>(P, w, n, d, k, centers, active, assign, best, counts, cost, 1); pcy_count_launch();
+    for (int r = 0; r < reps; ++r) {
+      if (!act[r]) continue;
+      int rc = pcy_launch_assign_d2(P, d, (int)n, pn, centers + (long long)r * k * d, d, cn + (long long)r * k, k, d,
+                                    ppart, ppos, assign + (long long)r * n, best + (long long)r * n, st);
+      if (rc) return rc;
+    }
+    // empty-cluster repair rounds until no repetition has an empty centre
+    for (;;) {
+      k_counts_empty<<<reps, KM_THREADS, 0, st>>>(P, w, n, d, k, centers, active, assign, best, counts, rstate);
+      pcy_count_launch();
+      PCY_CUDA(pcy_d2h(hstate.data(), rstate, sizeof(int) * 2 * reps, st));
+      bool any = false;
+      for (int r = 0; r < reps; ++r) any |= hstate[2 * r] >= 0;
+      if (!any) break;
+      k_repair_dist<<<dim3((unsigned)((n + 7) / 8), reps), 256, 0, st>>>(P, n, d, k, centers, rstate, assign, best);
+      pcy_count_launch();
+    }
+    k_cost<<<reps, KM_THREADS, 0, st>>>(w, n, active, best, cost); pcy_count_launch();
     PCY_LAUNCH_CHECK();
     PCY_CUDA(pcy_d2h(hc.data(), cost, sizeof(double) * reps, st));
     bool any_update = false;
@@ -369,6 +488,7 @@ int pcy_lloyd(const double* P, const double* w, long long n, int d, int k, int r
   PCY_CUDA(pcy_spin_sync(st));
   cudaFreeAsync(pn, st); cudaFreeAsync(cn, st); cudaFreeAsync(best, st); cudaFreeAsync(assign, st);
   cudaFreeAsync(counts, st); cudaFreeAsync(cost, st); cudaFreeAsync(active, st);
+  cudaFreeAsync(ppart, st); cudaFreeAsync(ppos, st); cudaFreeAsync(rstate, st);
   return PCY_OK;
 }
 
@@ -385,12 +505,20 @@ int pcy_weighted_cost(const double* P, const double* w, long long n, int d, int 
   PCY_CUDA(pcy_malloc_async(&cost, sizeof(double) * reps, st));
   k_rownorm<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(P, n, d, pn); pcy_count_launch();
   k_rownorm<<<(unsigned)((k * reps + 7) / 8), 256, 0, st>>>(centers, (long long)k * reps, d, cn); pcy_count_launch();
-  k_assign<<<dim3((unsigned)((n + 7) / 8), reps), 256, 0, st>>>(P, pn, n, d, k, centers, cn, nullptr, assign, best); pcy_count_launch();
-  k_finish<<<reps, KM_THREADS, 0, st>>>(P, w, n, d, k, (double*)centers, nullptr, assign, best, nullptr, cost, 0); pcy_count_launch();
+  const int ntiles = (k + 63) / 64;
+  double* ppart = nullptr; int* ppos = nullptr;
+  PCY_CUDA(pcy_malloc_async(&ppart, sizeof(double) * n * ntiles, st));
+  PCY_CUDA(pcy_malloc_async(&ppos, sizeof(int) * n * ntiles, st));
+  for (int r = 0; r < reps; ++r) {
+    int rc = pcy_launch_assign_d2(P, d, (int)n, pn, centers + (long long)r * k * d, d, cn + (long long)r * k, k, d,
+                                  ppart, ppos, assign + (long long)r * n, best + (long long)r * n, st);
+    if (rc) return rc;
+  }
+  k_cost<<<reps, KM_THREADS, 0, st>>>(w, n, nullptr, best, cost); pcy_count_launch();
   PCY_LAUNCH_CHECK();
   PCY_CUDA(pcy_d2h(costs, cost, sizeof(double) * reps, st));
   cudaFreeAsync(pn, st); cudaFreeAsync(cn, st); cudaFreeAsync(best, st); cudaFreeAsync(assign, st);
-  cudaFreeAsync(cost, st);
+  cudaFreeAsync(cost, st); cudaFreeAsync(ppart, st); cudaFreeAsync(ppos, st);
   return PCY_OK;
 }
 
