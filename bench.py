@@ -269,6 +269,34 @@ class MrWork:
         return self.X_host_sample
 
 
+def measure_gemm_peaks(dev):
+    """cuBLAS TF32 and FP64 GEMM throughput on this GPU (best of a few 8192^3 /
+    4096^3 runs): the denominators of the tensor-core and DMMA distance kernels,
+    which MEASURED_PEAKS.json does not carry (it has bf16 and HBM only)."""
+    import torch
+    out = {}
+    prev = torch.backends.cuda.matmul.allow_tf32
+    try:
+        for name, dt, nn, reps in (("tf32_tflops", torch.float32, 8192, 5), ("fp64_tflops", torch.float64, 4096, 3)):
+            torch.backends.cuda.matmul.allow_tf32 = name == "tf32_tflops"
+            a = torch.randn(nn, nn, dtype=dt, device=dev)
+            b = torch.randn(nn, nn, dtype=dt, device=dev)
+            torch.matmul(a, b)
+            best = 1e30
+            for _ in range(reps):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                torch.matmul(a, b)
+                e1.record()
+                e1.synchronize()
+                best = min(best, e0.elapsed_time(e1))
+            out[name] = 2.0 * nn ** 3 / (best / 1e3) / 1e12
+            del a, b
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    return out
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -299,6 +327,7 @@ def main():
         work = MrWork(cfg, args, dev, n_total, rank, world)
     X = work.X_host_sample
     n = n_total
+    gemm_peaks = measure_gemm_peaks(dev) if rank == 0 and not args.ncu else {}
 
     def step_device():
         st0 = torch.cuda.current_stream()
@@ -354,6 +383,7 @@ def main():
     ms_steps = [a.elapsed_time(b) for a, b in evs]
     ms = float(np.sum(ms_steps))
     prof = {k: nat.prof_read(k) for k in ("resolve", "chain", "reattach")}
+    prof_x = {k: nat.prof_read(k) for k in ("gemm", "seed", "lloyd")}
     clk = clocks.stop()
 
     # e2e: public API with host buffers (H2D of the stream, D2H of coreset + centers + costs)
@@ -403,6 +433,40 @@ def main():
                 "share_of_step": r_ms / ms if ms > 0 else None}
         kernel_ms = {k: {"ms": v[0] / args.steps, "launches": v[1] / args.steps, "units": v[2] / args.steps}
                      for k, v in prof.items()}
+        # north-star kernels: distance contraction (tensor), seeding (HBM), Lloyd assignment (tensor)
+        rooflines = []
+        tc = d >= 256
+        g_ms, g_cnt, g_flops = prof_x["gemm"]
+        if g_ms > 0:
+            ach = g_flops / (g_ms / 1e3) / 1e12
+            if tc:
+                pk = gemm_peaks.get("tf32_tflops", 1100.0) / 3.0
+                rooflines.append({"kernel": "k_tc_dots (K1 full-set distance contraction, split-TF32 on tcgen05)",
+                                  "bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s", "frac": ach / pk,
+                                  "launches_per_step": g_cnt / args.steps, "traffic": None,
+                                  "peak_source": "measured cuBLAS TF32 GEMM / 3 (three TF32 products per "
+                                                 "fp32-faithful product); achieved = 2*M*F*d per launch"})
+            else:
+                pk = gemm_peaks.get("fp64_tflops", 40.0)
+                rooflines.append({"kernel": "k_dist_tile<2> (K1 full-set distance contraction, fp64 DMMA)",
+                                  "bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s", "frac": ach / pk,
+                                  "launches_per_step": g_cnt / args.steps, "traffic": None,
+                                  "peak_source": "measured cuBLAS FP64 GEMM; achieved = 2*M*F*d per launch"})
+        s_ms, s_cnt, s_bytes = prof_x["seed"]
+        if s_ms > 0:
+            ach = s_bytes / (s_ms / 1e3) / 1e9
+            rooflines.append({"kernel": "k_seed_coop (weighted k-means++, all repetitions)", "bound": "hbm",
+                              "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                              "launches_per_step": s_cnt / args.steps, "traffic": None,
+                              "peak_source": peak_src + " HBM; algorithmic bytes = (k-1)(8nd + 24n*reps + 8n)"})
+        l_ms, l_cnt, l_flops = prof_x["lloyd"]
+        if l_ms > 0:
+            ach = l_flops / (l_ms / 1e3) / 1e12
+            pk = gemm_peaks.get("fp64_tflops", 40.0)
+            rooflines.append({"kernel": "k_dist_tile<3> (Lloyd assignment, fp64 DMMA + argmin)", "bound": "tensor",
+                              "achieved": ach, "peak": pk, "unit": "TFLOP/s", "frac": ach / pk,
+                              "launches_per_step": l_cnt / args.steps, "traffic": None,
+                              "peak_source": "measured cuBLAS FP64 GEMM; achieved = 2*n*k*d per repetition"})
         cpu = None
         if not args.no_cpu_baseline:
             rows, t, _ = cpu_sample(cfg, n)
@@ -418,6 +482,8 @@ def main():
                     "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(launches),
             "roofline": roof,
+            "rooflines": rooflines,
+            "gemm_peaks": gemm_peaks,
             "cpu_baseline": cpu,
             "clocks": clk,
             "kernel_ms_per_step": kernel_ms,

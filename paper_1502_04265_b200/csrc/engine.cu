@@ -849,7 +849,9 @@ struct Engine {
   long long seq = 0;
   long long* aggw = nullptr;
   double* mp_nrm = nullptr;
-  cudaEvent_t ev[6] = {};
+  cudaEvent_t ev[8] = {};
+  bool gemm_timed = false;           // ev[6..7] bracket the last full-set contraction
+  double gemm_flops = 0.0;
   ChainHdr* chh = nullptr;
   ChainLvl* chr = nullptr;
   double* parts = nullptr;                             // full-set parts matrix (1024 x NC)
@@ -1030,14 +1032,20 @@ struct Engine {
       if ((*rc = pcy_tc_center(A, aidx, ld, d, tc_c, st))) return false;
       if ((*rc = pcy_tc_split(A, aidx, ld, d, M, nullptr, tc_c, tc_ahi, tc_alo, tc_xn2, st))) return false;
       if ((*rc = pcy_tc_split(E.r, E.fs_list, ld, d, N, E.fs_cnt, tc_c, tc_bhi, tc_blo, tc_rnc, st))) return false;
+      const bool prof = pcy_prof_enabled();
+      if (prof) PCY_CUDA(cudaEventRecord(ev[6], st));
       if ((*rc = pcy_tc_dots(tc_ahi, tc_alo, 1024, (int)M, tc_bhi, tc_blo, (NC + 127) / 128 * 128, (int)N, E.fs_cnt,
                              Kp, tc_dots, N, st)))
         return false;
+      if (prof) { PCY_CUDA(cudaEventRecord(ev[7], st)); gemm_timed = true; gemm_flops = 2.0 * (double)M * (double)ctl_h->F * d; }
       E.tc_dots = tc_dots; E.tc_ldo = N; E.tc_rnc = tc_rnc; E.tc_xn2 = tc_xn2; E.tc_tau = tc_tau;
       return false;   // no fp64 parts matrix: K1 reads E.tc_dots
     }
     if (!parts) { if ((*rc = alloc(parts, (long long)1024 * NC))) return false; }
+    const bool prof = pcy_prof_enabled();
+    if (prof) { cudaEventRecord(ev[6], st); }
     *rc = pcy_launch_parts(A, aidx, ld, (int)M, E.r, E.fs_list, ld, E.rn, (int)N, E.fs_cnt, d, parts, N, st);
+    if (prof) { cudaEventRecord(ev[7], st); gemm_timed = true; gemm_flops = 2.0 * (double)M * (double)ctl_h->F * d; }
     return true;
   }
 
@@ -1175,6 +1183,12 @@ struct Engine {
           const long long done = ctl_h->status == ST_DONE ? nb - start : ctl_h->stop + (ctl_h->status == ST_FULL ? 0 : 1);
           pcy_prof_add(PCY_PROF_CHAIN, t1, nb - start);
           pcy_prof_add(PCY_PROF_RESOLVE, t2, done);
+          if (gemm_timed) {
+            float tg = 0.f;
+            PCY_CUDA(cudaEventElapsedTime(&tg, ev[6], ev[7]));
+            pcy_prof_add(PCY_PROF_GEMM, tg, (long long)gemm_flops);
+            gemm_timed = false;
+          }
           static FILE* trace = getenv("PCY_TRACE_K3") ? fopen(getenv("PCY_TRACE_K3"), "a") : nullptr;
           if (trace) {
             fprintf(trace, "%lld %.4f %.4f %d %lld %lld %lld %lld\n", done, t1, t2, ctl_h->status, ctl_h->F,

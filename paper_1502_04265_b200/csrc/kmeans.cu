@@ -402,9 +402,23 @@ int pcy_kmeanspp(const double* P, const double* w, long long n, int d, int k, in
   int nb = (int)blocks;
   long long n_ = n; int d_ = d, k_ = k, reps_ = reps;
   void* args[] = {(void*)&P, (void*)&w, &n_, &d_, &k_, &reps_, (void*)&U, &centers, &best, &mass, &part, &wpart, &picks, &rg};
+  const bool prof = pcy_prof_enabled();
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (prof) { cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventRecord(e0, st); }
   PCY_CUDA(cudaLaunchCooperativeKernel((const void*)k_seed_coop, dim3(nb), dim3(KS_THREADS), args, sm, st));
   pcy_count_launch();
   PCY_LAUNCH_CHECK();
+  if (prof) {
+    // algorithmic bytes: per distance pass the point rows once (n d 8) and, per
+    // repetition, best read + write and mass write (24 n); weights n 8
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, e0, e1);
+    const double bytes = (double)(k - 1) * ((double)n * d * 8.0 + (double)n * reps * 24.0 + (double)n * 8.0);
+    pcy_prof_add(PCY_PROF_SEED, t, (long long)bytes);
+    cudaEventDestroy(e0); cudaEventDestroy(e1);
+  }
   if (picks_out) {
     std::vector<int> h((size_t)k * reps);
     PCY_CUDA(pcy_d2h(h.data(), picks, sizeof(int) * k * reps, st));
@@ -439,6 +453,9 @@ int pcy_lloyd(const double* P, const double* w, long long n, int d, int k, int r
   PCY_CUDA(pcy_malloc_async(&ppos, sizeof(int) * n * ntiles, st));
   PCY_CUDA(pcy_malloc_async(&rstate, sizeof(int) * 2 * reps, st));
   std::vector<int> hstate(2 * reps);
+  cudaEvent_t pe0 = nullptr, pe1 = nullptr;
+  PCY_CUDA(cudaEventCreate(&pe0));
+  PCY_CUDA(cudaEventCreate(&pe1));
   std::vector<int> act(reps, 1);
   std::vector<double> prev(reps, INFINITY), hc(reps);
   for (int r = 0; r < reps; ++r) iters_out[r] = 0;
@@ -451,12 +468,17 @@ int pcy_lloyd(const double* P, const double* w, long long n, int d, int k, int r
     if (!nact) break;
     PCY_CUDA(cudaMemcpyAsync(active, act.data(), sizeof(int) * reps, cudaMemcpyHostToDevice, st));
     k_rownorm<<<(unsigned)((k * reps + 7) / 8), 256, 0, st>>>(centers, (long long)k * reps, d, cn); pcy_count_launch();
+    const bool prof = pcy_prof_enabled();
+    if (prof) cudaEventRecord(pe0, st);
+    int nassign = 0;
     for (int r = 0; r < reps; ++r) {
       if (!act[r]) continue;
       int rc = pcy_launch_assign_d2(P, d, (int)n, pn, centers + (long long)r * k * d, d, cn + (long long)r * k, k, d,
                                     ppart, ppos, assign + (long long)r * n, best + (long long)r * n, st);
       if (rc) return rc;
+      ++nassign;
     }
+    if (prof) cudaEventRecord(pe1, st);
     // empty-cluster repair rounds until no repetition has an empty centre
     for (;;) {
       k_counts_empty<<<reps, KM_THREADS, 0, st>>>(P, w, n, d, k, centers, active, assign, best, counts, rstate);
@@ -471,6 +493,11 @@ int pcy_lloyd(const double* P, const double* w, long long n, int d, int k, int r
     k_cost<<<reps, KM_THREADS, 0, st>>>(w, n, active, best, cost); pcy_count_launch();
     PCY_LAUNCH_CHECK();
     PCY_CUDA(pcy_d2h(hc.data(), cost, sizeof(double) * reps, st));
+    if (prof) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, pe0, pe1);
+      pcy_prof_add(PCY_PROF_LLOYD, t, (long long)(2.0 * (double)n * k * d * nassign));
+    }
     bool any_update = false;
     for (int r = 0; r < reps; ++r) {
       if (!act[r]) continue;
@@ -489,6 +516,7 @@ int pcy_lloyd(const double* P, const double* w, long long n, int d, int k, int r
   cudaFreeAsync(pn, st); cudaFreeAsync(cn, st); cudaFreeAsync(best, st); cudaFreeAsync(assign, st);
   cudaFreeAsync(counts, st); cudaFreeAsync(cost, st); cudaFreeAsync(active, st);
   cudaFreeAsync(ppart, st); cudaFreeAsync(ppos, st); cudaFreeAsync(rstate, st);
+  cudaEventDestroy(pe0); cudaEventDestroy(pe1);
   return PCY_OK;
 }
 
