@@ -169,11 +169,14 @@ __device__ __forceinline__ int map_find(const ResolveSmem& S, int id) {
   }
 }
 
-// insert-or-update; lane 0 writes; caller syncs
+// insert-or-update; lane 0 writes; caller syncs.  *fresh (nullable, every
+// lane) is incremented when the key was not present.
 __device__ __forceinline__ int map_put(ResolveSmem& S, unsigned* mbits, int id, long long w, double q, double sn,
-                                       int child, int lane) {
+                                       int child, int lane, int* fresh = nullptr) {
   int s = map_slot(id);
   while (S.mkey[s] >= 0 && S.mkey[s] != id) s = (s + 1) & (PCY_MOD_SLOTS - 1);
+  if (fresh && S.mkey[s] < 0) ++*fresh;
+  __syncwarp();
   if (lane == 0) {
     if (S.mkey[s] < 0) { S.modcount++; mbits[id >> 5] |= 1u << (id & 31); S.mrow[s] = -1; }
     S.mkey[s] = id; S.mw[s] = w; S.mq[s] = q; S.msn[s] = sn; S.mchild[s] = child;
@@ -256,7 +259,7 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
   for (int s2 = lane; s2 < mwords; s2 += 32) mbits[s2] = 0u;
   for (int s2 = lane; s2 < gwords; s2 += 32) gbits[s2] = 0u;
   if (lane == 0) { S.modcount = 0; S.ncache = 0; }
-  int nnew = 0;
+  int nnew = 0, mcount = 0;   // mcount: touched-node map entries (register copy, every lane)
   int free_top = freen > 0 ? E.free_ids[freen - 1] : -1;
 
   // ---- prologue: item 0
@@ -279,7 +282,7 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
 
   for (long long i = 0; i < n; ++i) {
     if (bad_c) { status = ST_INVALID; err = bad_c; stop = i; break; }
-    if (nnew >= nnew_cap || S.modcount >= PCY_MOD_SLOTS / 2) { status = ST_FULL; stop = i; break; }
+    if (nnew >= nnew_cap || mcount >= PCY_MOD_SLOTS / 2) { status = ST_FULL; stop = i; break; }
     // ---- prefetch item i+1 (scalars, x row, chain record, predicted row) and header of i+2
     double xn[NPER], pn[NPER];
     uint4 rpf[(REC_CHUNKS + 31) / 32];
@@ -292,8 +295,9 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
       xs_n = XS[i + 1];
       load_row<NPER>(xn, X + (i + 1) * ld, d, lane);
       const uint4* src = reinterpret_cast<const uint4*>(R + (i + 1) * PCY_FMAXL);
+      const int nch = hn.len * (int)(sizeof(ChainLvl) / 16);   // only the levels of the chain
 #pragma unroll
-      for (int q = 0; q < (REC_CHUNKS + 31) / 32; ++q) { const int c = lane + 32 * q; if (c < REC_CHUNKS) rpf[q] = src[c]; }
+      for (int q = 0; q < (REC_CHUNKS + 31) / 32; ++q) { const int c = lane + 32 * q; if (c < nch) rpf[q] = src[c]; }
       if (hn.predj >= 0) load_row<NPER>(pn, E.s + (long long)hn.predj * ld, d, lane);
       if (i + 2 < n) h2 = H[i + 2];
     }
@@ -381,10 +385,14 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
     if (!resume && len > 0 && !hc.trunc) {
       const int pl = hc.pred;
       bool ok = pl >= 0 && pl < len;
-      for (int L2 = 0; ok && L2 <= pl; ++L2) {
-        const int g2 = S.rb[cur][L2].g, j2 = S.rb[cur][L2].j;
-        if (g2 >= 0 && ((gbits[g2 >> 5] >> (g2 & 31)) & 1u)) ok = false;
-        if (j2 >= 0 && ((mbits[j2 >> 5] >> (j2 & 31)) & 1u)) ok = false;
+      if (ok) {
+        // one level per lane: a group that gained a member or a touched node fails
+        bool bad = false;
+        if (lane <= pl) {
+          const int g2 = S.rb[cur][lane].g, j2 = S.rb[cur][lane].j;
+          bad = (g2 >= 0 && ((gbits[g2 >> 5] >> (g2 & 31)) & 1u)) || (j2 >= 0 && ((mbits[j2 >> 5] >> (j2 & 31)) & 1u));
+        }
+        ok = !__any_sync(PCY_FULL, bad);
       }
       if (ok) {
         const ChainLvl& rp = S.rb[cur][pl];
@@ -398,7 +406,7 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
           for (int k = 0; k < NPER; ++k) pr[k] = take == 1 ? radd(pr[k], xr[k]) : radd(pr[k], rmul(ft, xr[k]));
           store_row<NPER>(E.s + (long long)bj * ld, pr, d, lane);
           const long long nw2 = rp.w + take;
-          cache_row(map_put(S, mbits, bj, nw2, rp.nq, rp.nsn, rp.child, lane));
+          cache_row(map_put(S, mbits, bj, nw2, rp.nq, rp.nsn, rp.child, lane, &mcount));
           if (lane == 0) { E.w[bj] = nw2; E.q[bj] = rp.nq; E.sn[bj] = rp.nsn; }
           modl[0] = bj; nmod = 1; lastmod = bj;
           rem = 0;
@@ -412,7 +420,7 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
             const ChainLvl& pp = S.rb[cur][pl - 1];
             g = (int)Galloc++;
             if (lane == 0) { E.g_count[g] = 0; E.g_cap[g] = 0; E.g_base[g] = 0; E.child[pp.j] = g; }
-            map_put(S, mbits, pp.j, pp.w, pp.q, pp.sn, g, lane);
+            map_put(S, mbits, pp.j, pp.w, pp.q, pp.sn, g, lane, &mcount);
           }
           if (do_open(g, pl)) { status = ST_REBUILD; stop = i; remaining = rem; }
           c_lv += pl + 1;
@@ -522,7 +530,7 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
           int child_now;
           if (touched) child_now = S.mchild[ms];
           else child_now = li >= 0 ? S.rb[cur][li].child : E.child[bj];
-          ms = map_put(S, mbits, bj, nw2, nq, nsn, child_now, lane);
+          ms = map_put(S, mbits, bj, nw2, nq, nsn, child_now, lane, &mcount);
           cache_row(ms);
           if (lane == 0) { E.w[bj] = nw2; E.q[bj] = nq; E.sn[bj] = nsn; }
           if (nmod < 4) modl[nmod] = bj;
@@ -550,7 +558,7 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
           c = (int)Galloc++;
           if (lane == 0) { E.g_count[c] = 0; E.g_cap[c] = 0; E.g_base[c] = 0; E.child[bj] = c; }
           if (tnow) { if (lane == 0) S.mchild[ms] = c; __syncwarp(); }
-          else { ms = map_put(S, mbits, bj, nn, qv, snv, c, lane); ++c_tch; }   // untouched: current stats
+          else { ms = map_put(S, mbits, bj, nn, qv, snv, c, lane, &mcount); ++c_tch; }   // untouched: current stats
         }
       }
       g = c;
@@ -563,8 +571,9 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
     // ---- rotate prefetched data into place
     if (has_next) {
       uint4* dst = reinterpret_cast<uint4*>(&S.rb[cur ^ 1][0]);
+      const int nch = hn.len * (int)(sizeof(ChainLvl) / 16);
 #pragma unroll
-      for (int q = 0; q < (REC_CHUNKS + 31) / 32; ++q) { const int c = lane + 32 * q; if (c < REC_CHUNKS) dst[c] = rpf[q]; }
+      for (int q = 0; q < (REC_CHUNKS + 31) / 32; ++q) { const int c = lane + 32 * q; if (c < nch) dst[c] = rpf[q]; }
 #pragma unroll
       for (int k = 0; k < NPER; ++k) xr[k] = xn[k];
       int nextnode = hn.predj;
