@@ -862,7 +862,7 @@ struct Engine {
   float *tc_ahi = nullptr, *tc_alo = nullptr, *tc_bhi = nullptr, *tc_blo = nullptr, *tc_dots = nullptr;
   double *tc_rnc = nullptr, *tc_xn2 = nullptr, *tc_c = nullptr;
   int nper = 0;          // resolve kernel: 1..8 register rows, 100/101 shared-memory rows, 0 generic
-  int nnew_cap = 0, crows = 0;
+  int nnew_cap = 0;
   size_t res_smem = 0, rea_smem = 0;
   std::vector<void*> allocs;
 
@@ -955,14 +955,12 @@ struct Engine {
     PCY_CUDA(cudaFuncSetAttribute(k_rchain, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
     if (ld <= 256 && !getenv("PCY_SMEM_RESOLVE")) {
       nper = ld <= 32 ? 1 : ld <= 64 ? 2 : ld <= 128 ? 4 : 8;
-      crows = 0;   // touched-row cache: measured neutral on cfg2/cfg4 (demand loads are not the bound)
-      if (const char* cr = getenv("PCY_CROWS")) crows = atoi(cr);
-      const size_t base = resolve_smem_bytes(ld, 0, NC, GC, crows);
+      const size_t base = resolve_smem_bytes(ld, 0, NC, GC);
       long long cap = maxsm > base ? (long long)((maxsm - base) / (sizeof(double) * (2 * ld + 1))) : 0;
       if (cap > PCY_NNEW_MAX) cap = PCY_NNEW_MAX;
       nnew_cap = (int)cap;
-      res_smem = resolve_smem_bytes(ld, nnew_cap, NC, GC, crows);
-      rea_smem = resolve_smem_bytes(ld, nnew_cap, NC, GC, 0);
+      res_smem = resolve_smem_bytes(ld, nnew_cap, NC, GC);
+      rea_smem = res_smem;
       if (nnew_cap < 8) { nper = 0; use_tc = false; }
       switch (nper) {
         case 1: PCY_CUDA(cudaFuncSetAttribute(k_resolve2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
@@ -1164,10 +1162,10 @@ struct Engine {
         }
         if (prof) PCY_CUDA(cudaEventRecord(ev[1], st));
         switch (nper) {
-          case 1: k_resolve2<1><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr, crows); pcy_count_launch(); break;
-          case 2: k_resolve2<2><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr, crows); pcy_count_launch(); break;
-          case 4: k_resolve2<4><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr, crows); pcy_count_launch(); break;
-          case 8: k_resolve2<8><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr, crows); pcy_count_launch(); break;
+          case 1: k_resolve2<1><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
+          case 2: k_resolve2<2><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
+          case 4: k_resolve2<4><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
+          case 8: k_resolve2<8><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
           case 100: k_resolve3<true, 2048><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr, nullptr, 0, 0); pcy_count_launch(); break;
           case 101: k_resolve3<false, 512><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr, gram, nb - start, 0); pcy_count_launch(); break;
           default:

@@ -145,16 +145,14 @@ struct ResolveSmem {
   int tk[PCY_NNEW_MAX], tfirst[PCY_NNEW_MAX], tcnt[PCY_NNEW_MAX], tbase[PCY_NNEW_MAX], tcap[PCY_NNEW_MAX];
   long long tw[PCY_NNEW_MAX];
   double trn[PCY_NNEW_MAX], tq[PCY_NNEW_MAX], tsn[PCY_NNEW_MAX];
-  short mrow[PCY_MOD_SLOTS];   // row-cache slot of a touched node (-1: none)
-  int modcount, ncache;
+  int modcount;
 };
 // dynamic tail: double xsm[ld]; double tref[nnew][ld|1]; double ts[nnew][ld];
-//               unsigned mbits[NC/32+1]; unsigned gbits[GC/32+1]; double cpool[crows][ld]
+//               unsigned mbits[NC/32+1]; unsigned gbits[GC/32+1]
 
-__host__ __device__ inline size_t resolve_smem_bytes(int ld, int nnew, long long NC, long long GC, int crows = 0) {
+__host__ __device__ inline size_t resolve_smem_bytes(int ld, int nnew, long long NC, long long GC) {
   return ((sizeof(ResolveSmem) + 15) & ~size_t(15)) + sizeof(double) * ((size_t)ld + (size_t)nnew * ((size_t)(ld | 1) + ld)) +
-         ((sizeof(unsigned) * (size_t)(NC / 32 + 1 + GC / 32 + 1) + 15) & ~size_t(15)) +
-         sizeof(double) * (size_t)crows * ld;
+         ((sizeof(unsigned) * (size_t)(NC / 32 + 1 + GC / 32 + 1) + 15) & ~size_t(15));
 }
 
 __device__ __forceinline__ int map_slot(int id) { return (int)(((unsigned)id * 2654435761u) >> 21) & (PCY_MOD_SLOTS - 1); }
@@ -178,7 +176,7 @@ __device__ __forceinline__ int map_put(ResolveSmem& S, unsigned* mbits, int id, 
   if (fresh && S.mkey[s] < 0) ++*fresh;
   __syncwarp();
   if (lane == 0) {
-    if (S.mkey[s] < 0) { S.modcount++; mbits[id >> 5] |= 1u << (id & 31); S.mrow[s] = -1; }
+    if (S.mkey[s] < 0) { S.modcount++; mbits[id >> 5] |= 1u << (id & 31); }
     S.mkey[s] = id; S.mw[s] = w; S.mq[s] = q; S.msn[s] = sn; S.mchild[s] = child;
   }
   __syncwarp();
@@ -230,7 +228,7 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
                                                     const double* __restrict__ XS, const long long* __restrict__ W,
                                                     const int* __restrict__ BAD, long long n, long long first_rem,
                                                     int countw, int nnew_cap, const ChainHdr* __restrict__ H,
-                                                    const ChainLvl* __restrict__ R, int crows) {
+                                                    const ChainLvl* __restrict__ R) {
   extern __shared__ __align__(16) unsigned char smraw[];
   ResolveSmem& S = *reinterpret_cast<ResolveSmem*>(smraw);
   const int lane = threadIdx.x;
@@ -243,8 +241,6 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
   const int mwords = (int)(E.NC / 32 + 1);
   unsigned* gbits = mbits + mwords;
   const int gwords = (int)(E.GC / 32 + 1);
-  double* cpool = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(mbits) +
-                                            ((sizeof(unsigned) * (size_t)(mwords + gwords) + 15) & ~size_t(15)));
   EngCtl* C = E.ctl;
   const long long m = E.m;
   const double T = C->T;
@@ -258,7 +254,7 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
   for (int s2 = lane; s2 < PCY_GMAP_SLOTS; s2 += 32) S.gkey[s2] = -1;
   for (int s2 = lane; s2 < mwords; s2 += 32) mbits[s2] = 0u;
   for (int s2 = lane; s2 < gwords; s2 += 32) gbits[s2] = 0u;
-  if (lane == 0) { S.modcount = 0; S.ncache = 0; }
+  if (lane == 0) S.modcount = 0;
   int nnew = 0, mcount = 0;   // mcount: touched-node map entries (register copy, every lane)
   int free_top = freen > 0 ? E.free_ids[freen - 1] : -1;
 
@@ -314,34 +310,14 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
 #pragma unroll
     for (int k = 0; k < NPER; ++k) { const int e = lane + 32 * k; if (e < ld) xsm[e] = xr[k]; }
     __syncwarp();
-    int lastmod = -1, nmod = 0;
-    int modl[4] = {-1, -1, -1, -1};   // snapshot nodes rewritten by this item
-    // current row of snapshot node bj into pr: row cache (touched nodes) or HBM
-    auto fetch_row = [&](int bj, int ms_) {
+    int lastmod = -1;      // last snapshot node this item rewrote (its row is in pr)
+    bool multi = false;    // the item rewrote more than one snapshot node
+    // current row of snapshot node bj into pr (HBM unless it is the held row)
+    auto fetch_row = [&](int bj) {
       if (bj == prnode) return;
-      const int slot = ms_ >= 0 ? (int)S.mrow[ms_] : -1;
-      if (slot >= 0) {
-#pragma unroll
-        for (int k = 0; k < NPER; ++k) { const int e = lane + 32 * k; pr[k] = e < d ? cpool[(long long)slot * ld + e] : 0.0; }
-      } else {
-        load_row<NPER>(pr, E.s + (long long)bj * ld, d, lane);
-        ++c_dem;
-      }
+      load_row<NPER>(pr, E.s + (long long)bj * ld, d, lane);
+      ++c_dem;
       prnode = bj;
-    };
-    // keep the just-updated row (pr) of map entry ms_ in the row cache
-    auto cache_row = [&](int ms_) {
-      int slot = S.mrow[ms_];
-      if (slot < 0 && S.ncache < crows) {
-        slot = S.ncache;
-        __syncwarp();
-        if (lane == 0) { S.mrow[ms_] = (short)slot; S.ncache = slot + 1; }
-      }
-      if (slot >= 0) {
-#pragma unroll
-        for (int k = 0; k < NPER; ++k) { const int e = lane + 32 * k; if (e < d) cpool[(long long)slot * ld + e] = pr[k]; }
-      }
-      __syncwarp();
     };
     // _open (coreset.py:329-335, :374-377) into group g at level L; returns true when full (rebuild)
     auto do_open = [&](int g, int L) -> bool {
@@ -401,14 +377,14 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
           const long long take = rp.take;
           const double ft = (double)take;
           if (bj != prnode) ++c_demf;
-          fetch_row(bj, -1);
+          fetch_row(bj);
 #pragma unroll
           for (int k = 0; k < NPER; ++k) pr[k] = take == 1 ? radd(pr[k], xr[k]) : radd(pr[k], rmul(ft, xr[k]));
           store_row<NPER>(E.s + (long long)bj * ld, pr, d, lane);
           const long long nw2 = rp.w + take;
-          cache_row(map_put(S, mbits, bj, nw2, rp.nq, rp.nsn, rp.child, lane, &mcount));
+          map_put(S, mbits, bj, nw2, rp.nq, rp.nsn, rp.child, lane, &mcount);
           if (lane == 0) { E.w[bj] = nw2; E.q[bj] = rp.nq; E.sn[bj] = rp.nsn; }
-          modl[0] = bj; nmod = 1; lastmod = bj;
+          lastmod = bj;
           rem = 0;
           if (pl + 1 > maxdepth) maxdepth = pl + 1;
           c_lv += pl + 1;
@@ -498,7 +474,7 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
           else { nn = E.w[bj]; qv = E.q[bj]; snv = E.sn[bj]; }
           if (!touched && li >= 0) dt = S.rb[cur][li].dot;
           else {
-            fetch_row(bj, ms);
+            fetch_row(bj);
             dt = reg_dot<NPER>(pr, xr);
           }
         }
@@ -523,7 +499,7 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
           __syncwarp();
         } else {
           if (touched && ms < 0) ms = map_find(S, bj);
-          fetch_row(bj, touched ? ms : -1);
+          fetch_row(bj);
 #pragma unroll
           for (int k = 0; k < NPER; ++k) pr[k] = take == 1 ? radd(pr[k], xr[k]) : radd(pr[k], rmul(ft, xr[k]));
           store_row<NPER>(E.s + (long long)bj * ld, pr, d, lane);
@@ -531,10 +507,8 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
           if (touched) child_now = S.mchild[ms];
           else child_now = li >= 0 ? S.rb[cur][li].child : E.child[bj];
           ms = map_put(S, mbits, bj, nw2, nq, nsn, child_now, lane, &mcount);
-          cache_row(ms);
           if (lane == 0) { E.w[bj] = nw2; E.q[bj] = nq; E.sn[bj] = nsn; }
-          if (nmod < 4) modl[nmod] = bj;
-          ++nmod;
+          if (lastmod >= 0 && lastmod != bj) multi = true;
           lastmod = bj;
         }
         rem -= take;
@@ -577,17 +551,14 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
 #pragma unroll
       for (int k = 0; k < NPER; ++k) xr[k] = xn[k];
       int nextnode = hn.predj;
-      bool hit = nmod > 4 || nextnode == lastmod;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) hit |= (modl[q] >= 0 && modl[q] == nextnode);
-      if (nextnode >= 0 && hit) {
+      if (nextnode >= 0 && (multi || nextnode == lastmod)) {
         // a node sits in one group, so an item rewrites it at most once: pr is
         // its current row exactly when it was the item's last rewrite
         if (nextnode == lastmod && prnode == lastmod) {
 #pragma unroll
           for (int k = 0; k < NPER; ++k) pn[k] = pr[k];   // the row this item just rewrote
         } else {
-          nextnode = -1;                                   // stale prefetch: demand-load later
+          nextnode = -1;                                   // possibly stale prefetch: demand-load later
         }
       }
 #pragma unroll
