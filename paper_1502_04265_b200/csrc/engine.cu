@@ -850,6 +850,11 @@ struct Engine {
   long long* aggw = nullptr;
   double* mp_nrm = nullptr;
   cudaEvent_t ev[8] = {};
+  // K3 (the critical path of an engine) runs on a highest-priority stream so
+  // that, with several engines on one GPU, it is scheduled ahead of the other
+  // engines' contraction CTAs; events order it after K1 and before the next block.
+  cudaStream_t hi = nullptr;
+  cudaEvent_t evk1 = nullptr, evk3 = nullptr;
   bool gemm_timed = false;           // ev[6..7] bracket the last full-set contraction
   double gemm_flops = 0.0;
   ChainHdr* chh = nullptr;
@@ -862,7 +867,7 @@ struct Engine {
   float *tc_ahi = nullptr, *tc_alo = nullptr, *tc_bhi = nullptr, *tc_blo = nullptr, *tc_dots = nullptr;
   double *tc_rnc = nullptr, *tc_xn2 = nullptr, *tc_c = nullptr;
   int nper = 0;          // resolve kernel: 1..8 register rows, 100/101 shared-memory rows, 0 generic
-  int nnew_cap = 0;
+  int nnew_cap = 0, rea_cap = 0;   // new-node table sizes of K3 and of the reattach
   size_t res_smem = 0, rea_smem = 0;
   std::vector<void*> allocs;
 
@@ -878,6 +883,9 @@ struct Engine {
     for (auto& a : allocs) if (a == p) { cudaFree(a); a = nullptr; }
   }
   ~Engine() {
+    if (hi) { cudaStreamSynchronize(hi); cudaStreamDestroy(hi); }
+    if (evk1) cudaEventDestroy(evk1);
+    if (evk3) cudaEventDestroy(evk3);
     if (ctl_h) {
       g_counters[0] += ctl_h->cnt_levels; g_counters[1] += ctl_h->cnt_direct; g_counters[2] += ctl_h->cnt_demand;
       g_counters[3] += ctl_h->cnt_slow; g_counters[4] += ctl_h->cnt_items;
@@ -944,6 +952,16 @@ struct Engine {
 #undef A_
     for (auto& e : ev) PCY_CUDA(cudaEventCreate(&e));
     {
+      const char* pe = getenv("PCY_K3_PRIORITY");
+      if (!pe || atoi(pe) != 0) {
+        int least = 0, greatest = 0;
+        PCY_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        PCY_CUDA(cudaStreamCreateWithPriority(&hi, cudaStreamNonBlocking, greatest));
+        PCY_CUDA(cudaEventCreateWithFlags(&evk1, cudaEventDisableTiming));
+        PCY_CUDA(cudaEventCreateWithFlags(&evk3, cudaEventDisableTiming));
+      }
+    }
+    {
       const char* tcenv = getenv("PCY_TC_PARTS");
       use_tc = tcenv ? atoi(tcenv) != 0 : d >= 256;
       Kp = pcy_tc_pad(d);
@@ -957,10 +975,13 @@ struct Engine {
       nper = ld <= 32 ? 1 : ld <= 64 ? 2 : ld <= 128 ? 4 : 8;
       const size_t base = resolve_smem_bytes(ld, 0, NC, GC);
       long long cap = maxsm > base ? (long long)((maxsm - base) / (sizeof(double) * (2 * ld + 1))) : 0;
-      if (cap > PCY_NNEW_MAX) cap = PCY_NNEW_MAX;
+      if (cap > PCY_NNEW_FAST) cap = PCY_NNEW_FAST;
       nnew_cap = (int)cap;
       res_smem = resolve_smem_bytes(ld, nnew_cap, NC, GC);
-      rea_smem = res_smem;
+      long long rcap = maxsm > base ? (long long)((maxsm - base) / (sizeof(double) * (ld | 1))) : 0;
+      if (rcap > PCY_NNEW_FAST) rcap = PCY_NNEW_FAST;
+      rea_cap = (int)rcap;
+      rea_smem = reattach_smem_bytes(ld, rea_cap, NC, GC);
       if (nnew_cap < 8) { nper = 0; use_tc = false; }
       switch (nper) {
         case 1: PCY_CUDA(cudaFuncSetAttribute(k_resolve2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
@@ -1073,10 +1094,10 @@ struct Engine {
       if (prof) PCY_CUDA(cudaEventRecord(ev[3], st));
       int rc;
       if (nper) {
-        long long off = 0;
+        long long off = 0, batch = 1024;   // K1 rows per reattach launch, adapted to where launches stop
         const int wpc = ld <= 512 ? 8 : (ld <= 2048 ? 4 : 2);
         while (off < nodes) {
-          const long long nb = nodes - off < 1024 ? nodes - off : 1024;
+          const long long nb = nodes - off < batch ? nodes - off : batch;
           int grc;
           const bool use_p = full_set(E.r, E.order + off, nb, st, &grc);
           if (grc) return grc;
@@ -1087,20 +1108,27 @@ struct Engine {
             if (grc) return grc;
           }
           switch (nper) {
-            case 1: k_reattach2<1><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr); pcy_count_launch(); break;
-            case 2: k_reattach2<2><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr); pcy_count_launch(); break;
-            case 4: k_reattach2<4><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr); pcy_count_launch(); break;
-            case 8: k_reattach2<8><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr); pcy_count_launch(); break;
+            case 1: k_reattach2<1><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr); pcy_count_launch(); break;
+            case 2: k_reattach2<2><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr); pcy_count_launch(); break;
+            case 4: k_reattach2<4><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr); pcy_count_launch(); break;
+            case 8: k_reattach2<8><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr); pcy_count_launch(); break;
             case 100: k_reattach3<true, 2048><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr, nullptr, 0, 0); pcy_count_launch(); break;
             default: k_reattach3<false, 512><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr, gram, nb, 0); pcy_count_launch(); break;
           }
           PCY_LAUNCH_CHECK();
           rc = sync_ctl(st); if (rc) return rc;
           if (ctl_h->status == ST_ARENA) { pcy_set_error("member arena exhausted in rebuild"); return PCY_ESTATE; }
+          if (getenv("PCY_DEBUG_REBUILD"))
+            fprintf(stderr, "[pcy] reattach launch: off %lld nb %lld status %d stop %lld F %lld nnew_cap %d\n", off, nb,
+                    ctl_h->status, ctl_h->stop, ctl_h->F, nnew_cap);
           if (ctl_h->status == ST_FULL) {
             if (ctl_h->stop == 0) { pcy_set_error("reattach made no progress"); return PCY_ESTATE; }
             off += ctl_h->stop;
-          } else off += nb;
+            batch = std::min<long long>(1024, std::max<long long>(128, 2 * ctl_h->stop));
+          } else {
+            off += nb;
+            batch = 1024;
+          }
         }
       } else {
         k_rb_reattach<<<1, 512, sizeof(double) * ld, st>>>(E, nodes); pcy_count_launch();
@@ -1160,20 +1188,24 @@ struct Engine {
         } else {
           k_chain<<<nblk, wpc * 32, sizeof(double) * wpc * ld, st>>>(E, Xs, XSs, nb - start); pcy_count_launch();
         }
-        if (prof) PCY_CUDA(cudaEventRecord(ev[1], st));
+        cudaStream_t rs = st;
+        if (hi) { PCY_CUDA(cudaEventRecord(evk1, st)); PCY_CUDA(cudaStreamWaitEvent(hi, evk1, 0)); rs = hi; }
+        if (prof) PCY_CUDA(cudaEventRecord(ev[1], rs));
         switch (nper) {
-          case 1: k_resolve2<1><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
-          case 2: k_resolve2<2><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
-          case 4: k_resolve2<4><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
-          case 8: k_resolve2<8><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
-          case 100: k_resolve3<true, 2048><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr, nullptr, 0, 0); pcy_count_launch(); break;
-          case 101: k_resolve3<false, 512><<<1, 32, res_smem, st>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr, gram, nb - start, 0); pcy_count_launch(); break;
+          case 1: k_resolve2<1><<<1, 32, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
+          case 2: k_resolve2<2><<<1, 32, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
+          case 4: k_resolve2<4><<<1, 32, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
+          case 8: k_resolve2<8><<<1, 32, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
+          case 100: k_resolve3<true, 2048><<<1, 32, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr, nullptr, 0, 0); pcy_count_launch(); break;
+          case 101: k_resolve3<false, 512><<<1, 32, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr, gram, nb - start, 0); pcy_count_launch(); break;
           default:
-            k_resolve<<<1, 32, sizeof(double) * ld, st>>>(E, Xs, XSs, Ws, Bs, nb - start, 0, first_rem, countw); pcy_count_launch();
+            k_resolve<<<1, 32, sizeof(double) * ld, rs>>>(E, Xs, XSs, Ws, Bs, nb - start, 0, first_rem, countw); pcy_count_launch();
         }
-        if (prof) PCY_CUDA(cudaEventRecord(ev[2], st));
+        if (prof) PCY_CUDA(cudaEventRecord(ev[2], rs));
         PCY_LAUNCH_CHECK();
-        int rc = sync_ctl(st); if (rc) return rc;
+        int rc = sync_ctl(rs);
+        if (hi) { PCY_CUDA(cudaEventRecord(evk3, hi)); PCY_CUDA(cudaStreamWaitEvent(st, evk3, 0)); }
+        if (rc) return rc;
         if (prof) {
           float t1 = 0.f, t2 = 0.f;
           PCY_CUDA(cudaEventElapsedTime(&t1, ev[0], ev[1]));

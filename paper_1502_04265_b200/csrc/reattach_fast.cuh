@@ -83,8 +83,7 @@ __global__ void __launch_bounds__(32, 1) k_reattach2(EngDev E, const int* __rest
   double* xsm = reinterpret_cast<double*>(smraw + ((sizeof(ResolveSmem) + 15) & ~size_t(15)));
   const int lds = ld | 1;   // odd stride: conflict-free lane-per-row reads
   double* tref = xsm + ld;
-  double* ts_unused = tref + (long long)nnew_cap * lds;
-  unsigned* mbits = reinterpret_cast<unsigned*>(ts_unused + (long long)nnew_cap * ld);
+  unsigned* mbits = reinterpret_cast<unsigned*>(tref + (long long)nnew_cap * lds);   // layout: reattach_smem_bytes
   const int mwords = (int)(E.NC / 32 + 1);
   unsigned* gbits = mbits + mwords;
   const int gwords = (int)(E.GC / 32 + 1);

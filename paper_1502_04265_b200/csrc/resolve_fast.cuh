@@ -20,7 +20,8 @@
 
 #define PCY_FMAXL 16
 #define PCY_MOD_SLOTS 2048
-#define PCY_NNEW_MAX 96
+#define PCY_NNEW_MAX 96    // new-node table of the large-d kernels (resolve_smem.cuh)
+#define PCY_NNEW_FAST 96   // new-node table of k_resolve2 / k_reattach2 (d <= 256); larger is slower (O(table) scans)
 #define PCY_GMAP_SLOTS 256
 
 struct __align__(16) ChainLvl {
@@ -141,10 +142,10 @@ struct ResolveSmem {
   long long mw[PCY_MOD_SLOTS];
   double mq[PCY_MOD_SLOTS], msn[PCY_MOD_SLOTS];
   int gkey[PCY_GMAP_SLOTS], ghead[PCY_GMAP_SLOTS], gtail[PCY_GMAP_SLOTS];  // groups with new members
-  int tid[PCY_NNEW_MAX], tgrp[PCY_NNEW_MAX], tchild[PCY_NNEW_MAX], tnext[PCY_NNEW_MAX];
-  int tk[PCY_NNEW_MAX], tfirst[PCY_NNEW_MAX], tcnt[PCY_NNEW_MAX], tbase[PCY_NNEW_MAX], tcap[PCY_NNEW_MAX];
-  long long tw[PCY_NNEW_MAX];
-  double trn[PCY_NNEW_MAX], tq[PCY_NNEW_MAX], tsn[PCY_NNEW_MAX];
+  int tid[PCY_NNEW_FAST], tgrp[PCY_NNEW_FAST], tchild[PCY_NNEW_FAST], tnext[PCY_NNEW_FAST];
+  int tk[PCY_NNEW_FAST], tfirst[PCY_NNEW_FAST], tcnt[PCY_NNEW_FAST], tbase[PCY_NNEW_FAST], tcap[PCY_NNEW_FAST];
+  long long tw[PCY_NNEW_FAST];
+  double trn[PCY_NNEW_FAST], tq[PCY_NNEW_FAST], tsn[PCY_NNEW_FAST];
   int modcount;
 };
 // dynamic tail: double xsm[ld]; double tref[nnew][ld|1]; double ts[nnew][ld];
@@ -152,6 +153,11 @@ struct ResolveSmem {
 
 __host__ __device__ inline size_t resolve_smem_bytes(int ld, int nnew, long long NC, long long GC) {
   return ((sizeof(ResolveSmem) + 15) & ~size_t(15)) + sizeof(double) * ((size_t)ld + (size_t)nnew * ((size_t)(ld | 1) + ld)) +
+         ((sizeof(unsigned) * (size_t)(NC / 32 + 1 + GC / 32 + 1) + 15) & ~size_t(15));
+}
+// k_reattach2 keeps only the reference rows of its new entries (no s rows)
+__host__ __device__ inline size_t reattach_smem_bytes(int ld, int nnew, long long NC, long long GC) {
+  return ((sizeof(ResolveSmem) + 15) & ~size_t(15)) + sizeof(double) * ((size_t)ld + (size_t)nnew * (size_t)(ld | 1)) +
          ((sizeof(unsigned) * (size_t)(NC / 32 + 1 + GC / 32 + 1) + 15) & ~size_t(15));
 }
 

@@ -22,7 +22,9 @@ with the CUDA engine (DeviceOps, NCCL) or, in the CPU tests, with the oracle
 from __future__ import annotations
 
 import math
+import os
 import threading
+import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -92,6 +94,8 @@ def run_piecy_mr_sharded(source, n_rows: int, dim: int, cfg, *, rank: int = 0, w
         with ops.stream_scope():
             results[grp.index] = group_summary(ops, source, grp, dim, cfg, len(groups))
 
+    _dbg = os.environ.get("PCY_DEBUG_MR")
+    _t0 = time.perf_counter()
     if concurrent and len(mine) > 1:
         errs = []
 
@@ -111,6 +115,9 @@ def run_piecy_mr_sharded(source, n_rows: int, dim: int, cfg, *, rank: int = 0, w
         for g in mine:
             work(g)
     ops.sync()
+    if _dbg:
+        print(f"[mr] rank {rank}: {len(mine)} level-0 groups in {time.perf_counter() - _t0:.3f} s", flush=True)
+        _t0 = time.perf_counter()
 
     # gather to rank 0 in group order (the exchange step)
     if world > 1:
@@ -138,7 +145,15 @@ def run_piecy_mr_sharded(source, n_rows: int, dim: int, cfg, *, rank: int = 0, w
         tree.insert_reduced(1, pts, wts)
     tree.stats.pieces = sum(g.pieces for g in groups)
     tree.stats.points_read = n_rows
-    return ops.finish(tree, None)
+    if _dbg:
+        ops.sync()
+        print(f"[mr] rank {rank}: merge of {len(groups)} summaries in {time.perf_counter() - _t0:.3f} s", flush=True)
+        _t0 = time.perf_counter()
+    out = ops.finish(tree, None)
+    if _dbg:
+        ops.sync()
+        print(f"[mr] rank {rank}: finalize in {time.perf_counter() - _t0:.3f} s", flush=True)
+    return out
 
 
 class DeviceOps:
