@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--rows", type=int, default=None, help="override stream length (smaller same-family stream)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-full-eval", action="store_true", help="skip the full-data evaluation pass (SURVEY 8f row 1)")
     ap.add_argument("--ncu", action="store_true", help="one short step for profiler capture, no JSON")
     return ap.parse_args()
 
@@ -339,6 +340,7 @@ def main():
         if P is not None:
             F = int(P.shape[0])
             C, costs = kmeans_repetitions_device(P, w, cfg.k, cfg.reps, cfg.seed, cfg.max_iters, 1e-4)
+            step_device.C = C
         c.record(st0)
         c.synchronize()
         step_device.phases.append((a.elapsed_time(b), b.elapsed_time(c)))
@@ -346,6 +348,7 @@ def main():
         return F, costs
     step_device.phases = []
     step_device.engine = None
+    step_device.C = None
 
     if args.ncu:
         step_device()
@@ -403,6 +406,30 @@ def main():
         e2e_times.append(time.perf_counter() - t0)
         h2d = work.h2d_bytes + (cs.points.nbytes + cs.weights.size * 8 + cfg.reps * cfg.k * 8 if cs is not None else 0)
         d2h = (cs.points.nbytes + cs.weights.nbytes + sum(c.nbytes + 8 for c, _ in runs)) if cs is not None else 0
+
+    # full-data second pass, unweighted SSE of the whole
+    # stream against every repetition's centres (evaluate_cost_multi), stream
+    # resident in HBM; one GPU (it is a separate pass, not part of the step)
+    full_eval = None
+    if world == 1 and step_device.C is not None and not args.no_full_eval:
+        from paper_1502_04265_b200.evaluation import evaluate_cost_multi
+        Cs = [step_device.C[r].cpu().numpy() for r in range(step_device.C.shape[0])]
+        stream = work.Xd if hasattr(work, "Xd") else torch.cat([work.dev_rows[g] for g in sorted(work.dev_rows)])
+        evaluate_cost_multi(Cs, stream[: min(int(stream.shape[0]), 65536)])   # warm-up
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        fcost = evaluate_cost_multi(Cs, stream)
+        torch.cuda.synchronize()
+        tf = time.perf_counter() - t0
+        flops = 2.0 * int(stream.shape[0]) * sum(c.shape[0] for c in Cs) * d
+        full_eval = {"value": int(stream.shape[0]) / tf, "unit": "points/s", "center_sets": len(Cs), "k": cfg.k,
+                     "seconds": tf, "achieved_tflops": flops / tf / 1e12,
+                     "frac_of_fp64_peak": (flops / tf / 1e12) / max(gemm_peaks.get("fp64_tflops", 40.0), 1e-9)
+                     if rank == 0 else None,
+                     "costs": fcost, "chunk": 8192,
+                     "note": "evaluate_cost_multi over the resident stream (chunks of 8192 rows, fp64 DMMA "
+                             "distance + first-min per set, chunk costs summed in order)"}
 
     t_local = torch.tensor([ms / args.steps, float(np.mean(e2e_times))], dtype=torch.float64, device=dev)
     if world > 1:
@@ -483,6 +510,7 @@ def main():
             "gpu_launches": int(launches),
             "roofline": roof,
             "rooflines": rooflines,
+            "full_data_eval": full_eval,
             "gemm_peaks": gemm_peaks,
             "cpu_baseline": cpu,
             "clocks": clk,

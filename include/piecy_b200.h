@@ -94,6 +94,19 @@ int pcy_lloyd(const double* P, const double* w, long long n, int d, int k, int r
 int pcy_weighted_cost(const double* P, const double* w, long long n, int d, int k, int reps,
                       const double* centers, double* costs, void* stream);
 
+/* The same into device memory without a host sync: costs_dev (device, reps);
+ * w (device, nullable = unit weights).  The streaming evaluation
+ * (evaluate_cost_multi, evaluation.py:157-180) costs each chunk with it. */
+int pcy_weighted_cost_dev(const double* P, const double* w, long long n, int d, int k, int reps,
+                          const double* centers, double* costs_dev, void* stream);
+
+/* evaluate_cost_multi block (evaluation.py:157-180): rows P (device, n x d) against
+ * one centre set C (device, k x d); out (device) receives the unweighted sum of the
+ * first-minimum GEMM-form distances of every `chunk` consecutive rows at
+ * out[c * out_stride]. */
+int pcy_cost_chunks(const double* P, long long n, int d, const double* C, int k, long long chunk,
+                    double* out, long long out_stride, void* stream);
+
 /* ------------------------------------------------------------- projection */
 
 /* randomized_truncated_svd -- linalg.py:167-206, with _fix_signs/_clip_small :77-94.

@@ -418,3 +418,19 @@ def piecy_mr(X, k, piece_size, num_pieces, svd_dim=None, coreset_size=None,
     for piece in _pieces(X, piece_size):
         t.push_piece(piece)
     return t.finalize()
+
+
+def evaluate_cost_multi(center_sets, X: np.ndarray, chunk: int = 8192) -> list:
+    """Streaming unweighted SSE against several center sets (evaluation.py:157-180):
+    chunks of ``chunk`` rows, GEMM-form distances to the stacked centers, per-set
+    minimum, chunk sums accumulated in chunk order."""
+    sets = [np.asarray(c, dtype=np.float64) for c in center_sets]
+    stacked = np.vstack(sets)
+    bounds = np.cumsum([0] + [c.shape[0] for c in sets])
+    totals = np.zeros(len(sets))
+    X = np.asarray(X, dtype=np.float64)
+    for a in range(0, X.shape[0], chunk):
+        d2 = pairwise_sq(X[a:a + chunk], stacked)
+        for i in range(len(sets)):
+            totals[i] += d2[:, bounds[i]:bounds[i + 1]].min(axis=1).sum()
+    return [float(t) for t in totals]

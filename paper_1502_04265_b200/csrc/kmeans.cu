@@ -217,6 +217,25 @@ __global__ void __launch_bounds__(KS_THREADS) k_seed_coop(const double* __restri
   }
 }
 
+__global__ void k_fill(double* __restrict__ p, long long n, double v) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) p[i] = v;
+}
+
+// Per-chunk sums of best (rows [c*chunk, (c+1)*chunk)), one CTA per chunk,
+// fixed order (thread-chunked then tree) -- the reference's chunked running
+// totals of evaluate_cost_multi (evaluation.py:172-179) group the same rows.
+__global__ void __launch_bounds__(256) k_chunk_sums(const double* __restrict__ best, long long n, long long chunk,
+                                                   double* __restrict__ out, long long out_stride) {
+  __shared__ double red[72];
+  const long long a0 = (long long)blockIdx.x * chunk, a1 = min(n, a0 + chunk);
+  const long long per = (a1 - a0 + blockDim.x - 1) / blockDim.x;
+  const long long a = a0 + (long long)threadIdx.x * per, b = min(a1, a + per);
+  double loc = 0.0;
+  for (long long i = a; i < b; ++i) loc += best[i];
+  const double tot = block_sum(loc, red);
+  if (threadIdx.x == 0) out[(long long)blockIdx.x * out_stride] = tot;
+}
+
 // Row squared norms (einsum 'ij,ij->i').
 __global__ void k_rownorm(const double* __restrict__ X, long long n, int d, double* __restrict__ out) {
   const int lane = threadIdx.x & 31;
@@ -520,34 +539,84 @@ int pcy_lloyd(const double* P, const double* w, long long n, int d, int k, int r
   return PCY_OK;
 }
 
-// weighted_cost for `reps` center sets: costs (host, reps).
-int pcy_weighted_cost(const double* P, const double* w, long long n, int d, int k, int reps,
-                      const double* centers, double* costs, void* stream) {
-  if (n < 1) { for (int r = 0; r < reps; ++r) costs[r] = 0.0; return PCY_OK; }
+// weighted_cost for `reps` center sets into device memory: costs_dev (device,
+// reps) -- no host synchronisation (the streaming evaluation accumulates
+// chunk costs on the device).  w (device, fp64) may be null for unit weights.
+int pcy_weighted_cost_dev(const double* P, const double* w, long long n, int d, int k, int reps,
+                          const double* centers, double* costs_dev, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  double *pn = nullptr, *cn = nullptr, *best = nullptr, *cost = nullptr; int *assign = nullptr;
+  if (n < 1) { PCY_CUDA(cudaMemsetAsync(costs_dev, 0, sizeof(double) * reps, st)); return PCY_OK; }
+  double *pn = nullptr, *cn = nullptr, *best = nullptr, *ones = nullptr; int *assign = nullptr;
   PCY_CUDA(pcy_malloc_async(&pn, sizeof(double) * n, st));
   PCY_CUDA(pcy_malloc_async(&cn, sizeof(double) * k * reps, st));
   PCY_CUDA(pcy_malloc_async(&best, sizeof(double) * n * reps, st));
   PCY_CUDA(pcy_malloc_async(&assign, sizeof(int) * n * reps, st));
-  PCY_CUDA(pcy_malloc_async(&cost, sizeof(double) * reps, st));
+  if (!w) {
+    PCY_CUDA(pcy_malloc_async(&ones, sizeof(double) * n, st));
+    k_fill<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 8), 256, 0, st>>>(ones, n, 1.0); pcy_count_launch();
+    w = ones;
+  }
   k_rownorm<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(P, n, d, pn); pcy_count_launch();
   k_rownorm<<<(unsigned)((k * reps + 7) / 8), 256, 0, st>>>(centers, (long long)k * reps, d, cn); pcy_count_launch();
   const int ntiles = (k + 63) / 64;
   double* ppart = nullptr; int* ppos = nullptr;
   PCY_CUDA(pcy_malloc_async(&ppart, sizeof(double) * n * ntiles, st));
   PCY_CUDA(pcy_malloc_async(&ppos, sizeof(int) * n * ntiles, st));
-  for (int r = 0; r < reps; ++r) {
-    int rc = pcy_launch_assign_d2(P, d, (int)n, pn, centers + (long long)r * k * d, d, cn + (long long)r * k, k, d,
-                                  ppart, ppos, assign + (long long)r * n, best + (long long)r * n, st);
-    if (rc) return rc;
-  }
-  k_cost<<<reps, KM_THREADS, 0, st>>>(w, n, nullptr, best, cost); pcy_count_launch();
+  int rc = PCY_OK;
+  for (int r = 0; r < reps && rc == PCY_OK; ++r)
+    rc = pcy_launch_assign_d2(P, d, (int)n, pn, centers + (long long)r * k * d, d, cn + (long long)r * k, k, d,
+                              ppart, ppos, assign + (long long)r * n, best + (long long)r * n, st);
+  if (rc == PCY_OK) { k_cost<<<reps, KM_THREADS, 0, st>>>(w, n, nullptr, best, costs_dev); pcy_count_launch(); }
   PCY_LAUNCH_CHECK();
-  PCY_CUDA(pcy_d2h(costs, cost, sizeof(double) * reps, st));
   cudaFreeAsync(pn, st); cudaFreeAsync(cn, st); cudaFreeAsync(best, st); cudaFreeAsync(assign, st);
-  cudaFreeAsync(cost, st); cudaFreeAsync(ppart, st); cudaFreeAsync(ppos, st);
-  return PCY_OK;
+  cudaFreeAsync(ppart, st); cudaFreeAsync(ppos, st);
+  if (ones) cudaFreeAsync(ones, st);
+  return rc;
+}
+
+// Streaming evaluation block (evaluate_cost_multi, evaluation.py:157-180):
+// rows P (device, n x d fp64, n a multiple of `chunk` except at the stream
+// end) against one centre set C (device, k x d): out (device) receives the
+// unweighted chunk sums of the first-min GEMM-form distances at
+// out[c * out_stride], c = 0 .. ceil(n/chunk)-1.  Scratch is allocated once
+// per call; 5 launches per call whatever n is.
+int pcy_cost_chunks(const double* P, long long n, int d, const double* C, int k, long long chunk, double* out,
+                    long long out_stride, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n < 1) return PCY_OK;
+  if (chunk < 1 || k < 1) { pcy_set_error("cost_chunks: bad sizes"); return PCY_EINVAL; }
+  const int ntiles = (k + 63) / 64;
+  double *pn = nullptr, *cn = nullptr, *best = nullptr, *ppart = nullptr; int *assign = nullptr, *ppos = nullptr;
+  PCY_CUDA(pcy_malloc_async(&pn, sizeof(double) * n, st));
+  PCY_CUDA(pcy_malloc_async(&cn, sizeof(double) * k, st));
+  PCY_CUDA(pcy_malloc_async(&best, sizeof(double) * n, st));
+  PCY_CUDA(pcy_malloc_async(&assign, sizeof(int) * n, st));
+  PCY_CUDA(pcy_malloc_async(&ppart, sizeof(double) * n * ntiles, st));
+  PCY_CUDA(pcy_malloc_async(&ppos, sizeof(int) * n * ntiles, st));
+  k_rownorm<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(P, n, d, pn); pcy_count_launch();
+  k_rownorm<<<(unsigned)((k + 7) / 8), 256, 0, st>>>(C, k, d, cn); pcy_count_launch();
+  int rc = pcy_launch_assign_d2(P, d, (int)n, pn, C, d, cn, k, d, ppart, ppos, assign, best, st);
+  if (rc == PCY_OK) {
+    k_chunk_sums<<<(unsigned)((n + chunk - 1) / chunk), 256, 0, st>>>(best, n, chunk, out, out_stride);
+    pcy_count_launch();
+  }
+  PCY_LAUNCH_CHECK();
+  cudaFreeAsync(pn, st); cudaFreeAsync(cn, st); cudaFreeAsync(best, st); cudaFreeAsync(assign, st);
+  cudaFreeAsync(ppart, st); cudaFreeAsync(ppos, st);
+  return rc;
+}
+
+// weighted_cost for `reps` center sets: costs (host, reps).
+int pcy_weighted_cost(const double* P, const double* w, long long n, int d, int k, int reps,
+                      const double* centers, double* costs, void* stream) {
+  if (n < 1) { for (int r = 0; r < reps; ++r) costs[r] = 0.0; return PCY_OK; }
+  cudaStream_t st = (cudaStream_t)stream;
+  double* cost = nullptr;
+  PCY_CUDA(pcy_malloc_async(&cost, sizeof(double) * reps, st));
+  int rc = pcy_weighted_cost_dev(P, w, n, d, k, reps, centers, cost, stream);
+  if (rc == PCY_OK) PCY_CUDA(pcy_d2h(costs, cost, sizeof(double) * reps, st));
+  cudaFreeAsync(cost, st);
+  return rc;
 }
 
 }  // extern "C"

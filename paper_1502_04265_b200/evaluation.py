@@ -27,6 +27,8 @@ nat.register("pcy_kmeanspp", c_i32, [c_vp, c_vp, c_i64, c_i32, c_i32, c_i32, c_v
 nat.register("pcy_lloyd", c_i32, [c_vp, c_vp, c_i64, c_i32, c_i32, c_i32, c_vp, c_i32, c_f64, c_vp, c_vp, c_vp])
 nat.register("pcy_cast_i64_f64", c_i32, [c_vp, c_i64, c_vp, c_vp])
 nat.register("pcy_weighted_cost", c_i32, [c_vp, c_vp, c_i64, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp])
+nat.register("pcy_weighted_cost_dev", c_i32, [c_vp, c_vp, c_i64, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp])
+nat.register("pcy_cost_chunks", c_i32, [c_vp, c_i64, c_i32, c_vp, c_i32, c_i64, c_vp, c_i64, c_vp])
 
 
 def _as_points(points) -> np.ndarray:
@@ -208,29 +210,64 @@ class CostSummary:
         return cls(float(arr.min()), float(arr.max()), float(arr.mean()), float(np.median(arr)))
 
 
-def evaluate_cost_multi(center_sets, point_stream, chunk: int = 8192) -> list:
-    """One streaming pass; unweighted SSE of the stream against each center
-    set (evaluation.py:157-180).  Chunks are costed on the device."""
-    import torch
-    sets = [np.asarray(c, dtype=np.float64) for c in center_sets]
-    totals = [0.0] * len(sets)
+def _stream_blocks(point_stream, chunk: int):
+    """The reference's chunk framing (evaluation.py:172-179): consecutive blocks
+    of ``chunk`` rows, the last one partial.  Arrays and tensors are sliced;
+    a ``streams.PointSource`` is read block-wise; other iterables are gathered
+    row by row."""
+    if _is_tensor(point_stream) or isinstance(point_stream, np.ndarray):
+        n = int(point_stream.shape[0])
+        for a in range(0, n, chunk):
+            yield point_stream[a:a + chunk]
+        return
+    blocks = getattr(point_stream, "blocks", None)
+    if callable(blocks):
+        for blk in blocks(chunk):
+            yield blk[0] if isinstance(blk, tuple) else blk
+        return
     buf = []
-    dev = torch.device("cuda", torch.cuda.current_device())
-    Cs = [torch.from_numpy(np.ascontiguousarray(c)).to(dev)[None].contiguous() for c in sets]
-
-    def _flush(rows):
-        P = torch.from_numpy(np.ascontiguousarray(np.stack(rows))).to(dev)
-        w = torch.ones(P.shape[0], dtype=torch.float64, device=dev)
-        for i, C in enumerate(Cs):
-            totals[i] += float(cost_device(P, w, C)[0])
-
     for x in point_stream:
         buf.append(np.asarray(x, dtype=np.float64))
         if len(buf) == chunk:
-            _flush(buf)
+            yield np.stack(buf)
             buf = []
     if buf:
-        _flush(buf)
+        yield np.stack(buf)
+
+
+def evaluate_cost_multi(center_sets, point_stream, chunk: int = 8192) -> list:
+    """One streaming pass; unweighted SSE of the stream against each center
+    set (evaluation.py:157-180).  The stream is taken in super-blocks of 64
+    chunks; per block and set one device call computes the GEMM-form distances
+    (fp64 tensor pipe), the first minimum and the per-chunk sums.  The chunk
+    sums stay on the device until the end and are then added in chunk order,
+    like the reference's running totals."""
+    import torch
+    from .linalg import to_f64_device
+    if chunk < 1:
+        raise ValueError("chunk must be >= 1")
+    sets = [np.asarray(c, dtype=np.float64) for c in center_sets]
+    if not sets:
+        return []
+    dev = torch.device("cuda", torch.cuda.current_device())
+    Cs = [torch.from_numpy(np.ascontiguousarray(c)).to(dev) for c in sets]
+    parts = []
+    for blk in _stream_blocks(point_stream, chunk * 64):
+        P = to_f64_device(blk)
+        if P.dim() != 2 or any(P.shape[1] != c.shape[1] for c in sets):
+            raise ValueError("points and centers must have the same dimension")
+        nb = int(P.shape[0])
+        out = torch.empty(((nb + chunk - 1) // chunk, len(sets)), dtype=torch.float64, device=dev)
+        for i, C in enumerate(Cs):
+            nat.check(nat.lib().pcy_cost_chunks(nat.ptr(P), nb, int(P.shape[1]), nat.ptr(C), int(C.shape[0]),
+                                                chunk, nat.ptr(out[:, i:]), len(sets), nat.stream_ptr()),
+                      "pcy_cost_chunks")
+        parts.append(out)
+    totals = [0.0] * len(sets)
+    if parts:
+        for row in torch.cat(parts).cpu().numpy():
+            for i in range(len(sets)):
+                totals[i] += float(row[i])
     return [float(t) for t in totals]
 
 
