@@ -839,12 +839,36 @@ __global__ void k_boot_gather(EngDev E, long long cnt, const long long* __restri
 // ====================================================================== host
 namespace {
 
+// Mapped pinned control mirrors are recycled across engines: cudaFreeHost
+// would synchronise the device whenever an engine is destroyed.
+static std::mutex g_ctl_mu;
+static std::vector<EngCtl*> g_ctl_pool;
+static EngCtl* ctl_pool_get() {
+  {
+    std::lock_guard<std::mutex> lk(g_ctl_mu);
+    if (!g_ctl_pool.empty()) { EngCtl* c = g_ctl_pool.back(); g_ctl_pool.pop_back(); return c; }
+  }
+  EngCtl* c = nullptr;
+  if (cudaHostAlloc(&c, sizeof(EngCtl), cudaHostAllocMapped) != cudaSuccess) return nullptr;
+  return c;
+}
+static void ctl_pool_put(EngCtl* c) {
+  std::lock_guard<std::mutex> lk(g_ctl_mu);
+  g_ctl_pool.push_back(c);
+}
+
 struct Engine {
   int dev = 0, d = 0, ld = 0;
   long long m = 0, sample_cap = 0, NC = 0, GC = 0, AC = 0, Bmax = 0;
   bool built = false;
   EngDev E{};
   EngCtl* ctl_h = nullptr;   // mapped pinned mirror (host view)
+  // Engine buffers come from the stream-ordered pool on `own`; destruction
+  // waits (on the device) for the last public call's stream through `done_ev`
+  // and frees asynchronously -- no device-wide synchronisation.
+  cudaStream_t own = nullptr;
+  cudaEvent_t done_ev = nullptr;
+  bool done_rec = false;
   EngCtl* ctl_map_d = nullptr;   // device view of the mirror
   long long seq = 0;
   long long* aggw = nullptr;
@@ -873,28 +897,32 @@ struct Engine {
 
   template <class T> int alloc(T*& p, long long count) {
     void* q = nullptr;
-    cudaError_t e = cudaMalloc(&q, sizeof(T) * (size_t)(count > 0 ? count : 1));
-    if (e != cudaSuccess) { pcy_set_error("cudaMalloc(%lld x %zu): %s", count, sizeof(T), cudaGetErrorString(e)); return PCY_ENOMEM; }
+    cudaError_t e = pcy_malloc_async_raw(&q, sizeof(T) * (size_t)(count > 0 ? count : 1), own);
+    if (e != cudaSuccess) { pcy_set_error("cudaMallocAsync(%lld x %zu): %s", count, sizeof(T), cudaGetErrorString(e)); return PCY_ENOMEM; }
     allocs.push_back(q);
     p = (T*)q;
     return PCY_OK;
   }
-  void release(void* p) {
-    for (auto& a : allocs) if (a == p) { cudaFree(a); a = nullptr; }
+  void release(void* p) {   // caller guarantees no pending use (it synchronised)
+    for (auto& a : allocs) if (a == p) { cudaFreeAsync(a, own); a = nullptr; }
   }
+  void touch(cudaStream_t st) { if (cudaEventRecord(done_ev, st) == cudaSuccess) done_rec = true; }
   ~Engine() {
-    if (hi) { cudaStreamSynchronize(hi); cudaStreamDestroy(hi); }
-    if (evk1) cudaEventDestroy(evk1);
-    if (evk3) cudaEventDestroy(evk3);
     if (ctl_h) {
       g_counters[0] += ctl_h->cnt_levels; g_counters[1] += ctl_h->cnt_direct; g_counters[2] += ctl_h->cnt_demand;
       g_counters[3] += ctl_h->cnt_slow; g_counters[4] += ctl_h->cnt_items;
       long long md = g_counters[5].load();
       while (ctl_h->max_depth > md && !g_counters[5].compare_exchange_weak(md, ctl_h->max_depth)) {}
     }
+    if (own && done_rec) cudaStreamWaitEvent(own, done_ev, 0);
+    for (void* a : allocs) if (a) cudaFreeAsync(a, own);
+    if (hi) cudaStreamDestroy(hi);
+    if (evk1) cudaEventDestroy(evk1);
+    if (evk3) cudaEventDestroy(evk3);
     for (auto& e : ev) if (e) cudaEventDestroy(e);
-    for (void* a : allocs) if (a) cudaFree(a);
-    if (ctl_h) cudaFreeHost(ctl_h);
+    if (done_ev) cudaEventDestroy(done_ev);
+    if (own) cudaStreamDestroy(own);
+    if (ctl_h) ctl_pool_put(ctl_h);
   }
 
   // Publish the device counters into the mapped host mirror and spin on its
@@ -924,6 +952,8 @@ struct Engine {
     NC = m + 2; GC = NC + 2; AC = 24 * NC + 4096;
     Bmax = block_rows > 0 ? block_rows : 4096;
     PCY_CUDA(cudaSetDevice(dev));
+    PCY_CUDA(cudaStreamCreateWithFlags(&own, cudaStreamNonBlocking));
+    PCY_CUDA(cudaEventCreateWithFlags(&done_ev, cudaEventDisableTiming));
     PCY_CUDA(cudaFuncSetAttribute(k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
     PCY_CUDA(cudaFuncSetAttribute(k_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
     PCY_CUDA(cudaFuncSetAttribute(k_rb_reattach, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
@@ -1015,16 +1045,17 @@ struct Engine {
       }
     }
     if (getenv("PCY_GENERIC_RESOLVE")) nper = 0;
-    PCY_CUDA(cudaHostAlloc(&ctl_h, sizeof(EngCtl), cudaHostAllocMapped));
+    if (!(ctl_h = ctl_pool_get())) { pcy_set_error("cudaHostAlloc of the control mirror failed"); return PCY_ENOMEM; }
     memset(ctl_h, 0, sizeof(EngCtl));
     PCY_CUDA(cudaHostGetDevicePointer((void**)&ctl_map_d, ctl_h, 0));
-    PCY_CUDA(cudaMemcpy(E.ctl, ctl_h, sizeof(EngCtl), cudaMemcpyHostToDevice));
-    PCY_CUDA(cudaMemset(E.htab, 0xff, sizeof(int) * E.hcap));
-    PCY_CUDA(cudaMemset(E.alive, 0, sizeof(int) * NC));
-    PCY_CUDA(cudaMemset(E.g_count, 0, sizeof(int) * GC));
-    PCY_CUDA(cudaMemset(E.g_base, 0, sizeof(int) * GC));
-    PCY_CUDA(cudaMemset(E.s, 0, sizeof(double) * NC * ld));
-    PCY_CUDA(cudaMemset(E.r, 0, sizeof(double) * NC * ld));
+    PCY_CUDA(cudaMemcpyAsync(E.ctl, ctl_h, sizeof(EngCtl), cudaMemcpyHostToDevice, own));
+    PCY_CUDA(cudaMemsetAsync(E.htab, 0xff, sizeof(int) * E.hcap, own));
+    PCY_CUDA(cudaMemsetAsync(E.alive, 0, sizeof(int) * NC, own));
+    PCY_CUDA(cudaMemsetAsync(E.g_count, 0, sizeof(int) * GC, own));
+    PCY_CUDA(cudaMemsetAsync(E.g_base, 0, sizeof(int) * GC, own));
+    PCY_CUDA(cudaMemsetAsync(E.s, 0, sizeof(double) * NC * ld, own));
+    PCY_CUDA(cudaMemsetAsync(E.r, 0, sizeof(double) * NC * ld, own));
+    PCY_CUDA(cudaStreamSynchronize(own));   // buffers ready for any stream
     return PCY_OK;
   }
 
@@ -1364,13 +1395,17 @@ int pcy_engine_insert(void* h, const void* x, int dtype, long long stride, const
   Engine* e = (Engine*)h;
   if (!e) { pcy_set_error("null engine"); return PCY_EINVAL; }
   if (n <= 0) { *consumed = 0; *bad_code = 0; return PCY_OK; }
-  return e->insert(x, dtype, stride, w, n, (cudaStream_t)stream, consumed, bad_code);
+  const int rc = e->insert(x, dtype, stride, w, n, (cudaStream_t)stream, consumed, bad_code);
+  e->touch((cudaStream_t)stream);
+  return rc;
 }
 
 int pcy_engine_stats(void* h, long long* num_features, double* threshold, long long* total_weight,
                      int* built, void* stream) {
   Engine* e = (Engine*)h;
-  int rc = e->sync_ctl((cudaStream_t)stream); if (rc) return rc;
+  int rc = e->sync_ctl((cudaStream_t)stream);
+  e->touch((cudaStream_t)stream);
+  if (rc) return rc;
   *num_features = e->built ? e->ctl_h->F : e->ctl_h->ndist;
   *threshold = e->ctl_h->T;
   *total_weight = e->ctl_h->total_w;
@@ -1398,13 +1433,18 @@ int pcy_engine_counters_total(long long* out6) {
 
 int pcy_engine_features(void* h, int* level, long long* weight, double* lsum, double* sqsum,
                         double* ref, long long cap, long long* count, void* stream) {
-  return ((Engine*)h)->features(level, weight, lsum, sqsum, ref, nullptr, cap, count, (cudaStream_t)stream);
+  Engine* e = (Engine*)h;
+  const int rc = e->features(level, weight, lsum, sqsum, ref, nullptr, cap, count, (cudaStream_t)stream);
+  e->touch((cudaStream_t)stream);
+  return rc;
 }
 
 int pcy_engine_extract(void* h, double* points, long long* weights, long long cap, long long* count,
                        void* stream) {
-  return ((Engine*)h)->features(nullptr, weights, nullptr, nullptr, nullptr, points, cap, count,
-                                (cudaStream_t)stream);
+  Engine* e = (Engine*)h;
+  const int rc = e->features(nullptr, weights, nullptr, nullptr, nullptr, points, cap, count, (cudaStream_t)stream);
+  e->touch((cudaStream_t)stream);
+  return rc;
 }
 
 }  // extern "C"
