@@ -1223,10 +1223,10 @@ struct Engine {
         if (hi) { PCY_CUDA(cudaEventRecord(evk1, st)); PCY_CUDA(cudaStreamWaitEvent(hi, evk1, 0)); rs = hi; }
         if (prof) PCY_CUDA(cudaEventRecord(ev[1], rs));
         switch (nper) {
-          case 1: k_resolve2<1><<<1, 32, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
-          case 2: k_resolve2<2><<<1, 32, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
-          case 4: k_resolve2<4><<<1, 32, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
-          case 8: k_resolve2<8><<<1, 32, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
+          case 1: k_resolve2<1><<<1, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
+          case 2: k_resolve2<2><<<1, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
+          case 4: k_resolve2<4><<<1, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
+          case 8: k_resolve2<8><<<1, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
           case 100: k_resolve3<true, 2048><<<1, 32, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr, nullptr, 0, 0); pcy_count_launch(); break;
           case 101: k_resolve3<false, 512><<<1, 32, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr, gram, nb - start, 0); pcy_count_launch(); break;
           default:

@@ -137,7 +137,7 @@ __global__ void k_chain2(EngDev E, const double* __restrict__ X, const double* _
 
 // ------------------------------------------------------------------- K3
 struct ResolveSmem {
-  ChainLvl rb[2][PCY_FMAXL];                 // chain records, double buffered
+  ChainLvl rb[4][PCY_FMAXL];                 // chain records: staging ring (k_resolve2) / double buffer
   int mkey[PCY_MOD_SLOTS], mchild[PCY_MOD_SLOTS];   // touched snapshot nodes
   long long mw[PCY_MOD_SLOTS];
   double mq[PCY_MOD_SLOTS], msn[PCY_MOD_SLOTS];
@@ -146,13 +146,20 @@ struct ResolveSmem {
   int tk[PCY_NNEW_FAST], tfirst[PCY_NNEW_FAST], tcnt[PCY_NNEW_FAST], tbase[PCY_NNEW_FAST], tcap[PCY_NNEW_FAST];
   long long tw[PCY_NNEW_FAST];
   double trn[PCY_NNEW_FAST], tq[PCY_NNEW_FAST], tsn[PCY_NNEW_FAST];
+  // item staging ring of k_resolve2 (producer warp -> decision warp), K3_SLOTS slots
+  ChainHdr shdr[4];
+  long long sw[4];
+  double sxs[4];
+  int sbad[4];
+  int stop_flag;
   int modcount;
 };
-// dynamic tail: double xsm[ld]; double tref[nnew][ld|1]; double ts[nnew][ld];
+// dynamic tail: double slotx[4][ld], slotp[4][ld]; double tref[nnew][ld|1]; double ts[nnew][ld];
+// (k_reattach2 keeps a single xsm[ld] and no ts, see reattach_smem_bytes)
 //               unsigned mbits[NC/32+1]; unsigned gbits[GC/32+1]
 
 __host__ __device__ inline size_t resolve_smem_bytes(int ld, int nnew, long long NC, long long GC) {
-  return ((sizeof(ResolveSmem) + 15) & ~size_t(15)) + sizeof(double) * ((size_t)ld + (size_t)nnew * ((size_t)(ld | 1) + ld)) +
+  return ((sizeof(ResolveSmem) + 15) & ~size_t(15)) + sizeof(double) * ((size_t)8 * ld + (size_t)nnew * ((size_t)(ld | 1) + ld)) +
          ((sizeof(unsigned) * (size_t)(NC / 32 + 1 + GC / 32 + 1) + 15) & ~size_t(15));
 }
 // k_reattach2 keeps only the reference rows of its new entries (no s rows)
@@ -229,24 +236,82 @@ __device__ __forceinline__ void store_row(double* __restrict__ dst, const double
 
 constexpr int REC_CHUNKS = PCY_FMAXL * (int)sizeof(ChainLvl) / 16;   // uint4 per record
 
+// named barriers between the decision warp and the staging warp of k_resolve2
+__device__ __forceinline__ void nbar_sync(int id, int cnt) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(cnt) : "memory"); }
+__device__ __forceinline__ void nbar_arrive(int id, int cnt) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(cnt) : "memory"); }
+constexpr int K3_SLOTS = 4, K3_BAR_FULL = 1, K3_BAR_EMPTY = 1 + K3_SLOTS;   // + slot
+
 template <int NPER>
-__global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __restrict__ X,
+__global__ void __launch_bounds__(64, 1) k_resolve2(EngDev E, const double* __restrict__ X,
                                                     const double* __restrict__ XS, const long long* __restrict__ W,
                                                     const int* __restrict__ BAD, long long n, long long first_rem,
                                                     int countw, int nnew_cap, const ChainHdr* __restrict__ H,
                                                     const ChainLvl* __restrict__ R) {
   extern __shared__ __align__(16) unsigned char smraw[];
   ResolveSmem& S = *reinterpret_cast<ResolveSmem*>(smraw);
-  const int lane = threadIdx.x;
+  const int lane = threadIdx.x & 31;
   const int d = E.d, ld = E.ld;
-  double* xsm = reinterpret_cast<double*>(smraw + ((sizeof(ResolveSmem) + 15) & ~size_t(15)));
+  double* slotx = reinterpret_cast<double*>(smraw + ((sizeof(ResolveSmem) + 15) & ~size_t(15)));   // [K3_SLOTS][ld]
+  double* slotp = slotx + K3_SLOTS * ld;                                                             // [K3_SLOTS][ld]
   const int lds = ld | 1;   // odd stride: conflict-free lane-per-row reads
-  double* tref = xsm + ld;
+  double* tref = slotp + K3_SLOTS * ld;
   double* ts = tref + (long long)nnew_cap * lds;
   unsigned* mbits = reinterpret_cast<unsigned*>(ts + (long long)nnew_cap * ld);
   const int mwords = (int)(E.NC / 32 + 1);
   unsigned* gbits = mbits + mwords;
   const int gwords = (int)(E.GC / 32 + 1);
+
+  if (threadIdx.x >= 32) {
+    // ---- staging warp: item j's header, scalars, x row, chain levels and
+    // predicted s row into slot j&1, once the decision warp has finished item
+    // j-2 (the slot's previous user).  Rows of nodes the decision warp rewrites
+    // meanwhile may be read stale or torn here; the decision warp never uses a
+    // predicted row of a node that the previous item rewrote.
+    // software pipeline: item j+1's rows are in registers while item j is
+    // stored; headers run two items ahead (a record's length and predicted
+    // node are needed to issue its loads)
+    constexpr int RQ = (REC_CHUNKS + 31) / 32;
+    struct Stage { double x[NPER], p[NPER]; uint4 r[RQ]; ChainHdr h; int bad; long long w; double xs; };
+    auto fetch = [&](Stage& t, long long j, const ChainHdr& h) {
+      t.h = h;
+      t.bad = BAD ? BAD[j] : 0; t.w = W ? W[j] : 1LL; t.xs = XS[j];
+      load_row<NPER>(t.x, X + j * ld, d, lane);
+      if (h.predj >= 0) load_row<NPER>(t.p, E.s + (long long)h.predj * ld, d, lane);
+      const uint4* src = reinterpret_cast<const uint4*>(R + j * PCY_FMAXL);
+      const int nch = h.len * (int)(sizeof(ChainLvl) / 16);
+#pragma unroll
+      for (int q = 0; q < RQ; ++q) { const int c = lane + 32 * q; if (c < nch) t.r[q] = src[c]; }
+    };
+    Stage cur_st, nxt_st;
+    ChainHdr h_ahead = n > 1 ? H[1] : ChainHdr{0, 0, -1, 0};
+    if (n > 0) fetch(cur_st, 0, H[0]);
+    for (long long j = 0; j < n; ++j) {
+      const int sl = (int)(j & (K3_SLOTS - 1));
+      if (j >= K3_SLOTS) {
+        nbar_sync(K3_BAR_EMPTY + sl, 64);
+        if (*(volatile int*)&S.stop_flag) break;
+      }
+      if (j + 1 < n) {
+        const ChainHdr h1 = h_ahead;
+        if (j + 2 < n) h_ahead = H[j + 2];
+        fetch(nxt_st, j + 1, h1);
+      }
+      // store item j into its slot
+      if (lane == 0) { S.shdr[sl] = cur_st.h; S.sbad[sl] = cur_st.bad; S.sw[sl] = cur_st.w; S.sxs[sl] = cur_st.xs; }
+      store_row<NPER>(slotx + sl * ld, cur_st.x, ld, lane);
+      if (cur_st.h.predj >= 0) store_row<NPER>(slotp + sl * ld, cur_st.p, ld, lane);
+      uint4* dst = reinterpret_cast<uint4*>(&S.rb[sl][0]);
+      const int nch = cur_st.h.len * (int)(sizeof(ChainLvl) / 16);
+#pragma unroll
+      for (int q = 0; q < RQ; ++q) { const int c = lane + 32 * q; if (c < nch) dst[c] = cur_st.r[q]; }
+      __threadfence_block();
+      __syncwarp();
+      nbar_arrive(K3_BAR_FULL + sl, 64);
+      cur_st = nxt_st;
+    }
+    return;
+  }
+
   EngCtl* C = E.ctl;
   const long long m = E.m;
   const double T = C->T;
@@ -260,49 +325,54 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
   for (int s2 = lane; s2 < PCY_GMAP_SLOTS; s2 += 32) S.gkey[s2] = -1;
   for (int s2 = lane; s2 < mwords; s2 += 32) mbits[s2] = 0u;
   for (int s2 = lane; s2 < gwords; s2 += 32) gbits[s2] = 0u;
-  if (lane == 0) S.modcount = 0;
+  if (lane == 0) { S.modcount = 0; S.stop_flag = 0; }
   int nnew = 0, mcount = 0;   // mcount: touched-node map entries (register copy, every lane)
   int free_top = freen > 0 ? E.free_ids[freen - 1] : -1;
 
-  // ---- prologue: item 0
-  double xr[NPER], pr[NPER];
-  int bad_c = (n > 0 && BAD) ? BAD[0] : 0;
-  long long w_c = (n > 0 && W) ? W[0] : 1LL;
-  double xs_c = n > 0 ? XS[0] : 0.0;
-  ChainHdr hc = n > 0 ? H[0] : ChainHdr{0, 0, -1, 0};
-  ChainHdr hn = n > 1 ? H[1] : ChainHdr{0, 0, -1, 0};
-  if (n > 0) {
-    load_row<NPER>(xr, X, d, lane);
-    if (hc.predj >= 0) load_row<NPER>(pr, E.s + (long long)hc.predj * ld, d, lane);
-    const uint4* src = reinterpret_cast<const uint4*>(R);
-    uint4* dst = reinterpret_cast<uint4*>(&S.rb[0][0]);
-    for (int c = lane; c < REC_CHUNKS; c += 32) dst[c] = src[c];
-  }
-  __syncwarp();
-  int cur = 0;
-  int prnode = hc.predj;   // node whose current s row is held in pr[]
+  double pr[NPER];
+  int prnode = -1;               // node whose current s row is held in pr[]
+  // rewrites of the last K3_SLOTS items: the staging warp reads item i's
+  // predicted row once item i-K3_SLOTS-1 is done (one item ahead of its slot
+  // store), so any of items i-K3_SLOTS .. i-1 may have rewritten it since
+  int rec_mod[K3_SLOTS];
+#pragma unroll
+  for (int q = 0; q < K3_SLOTS; ++q) rec_mod[q] = -1;
+  int multi_left = 0;            // items left in the window since one rewrote several nodes
+  // a stop (FULL / REBUILD / INVALID) releases the staging warp
+  auto signal_stop = [&](int sl) {
+    if (lane == 0) S.stop_flag = 1;
+    __threadfence_block();
+    __syncwarp();
+    nbar_arrive(K3_BAR_EMPTY + sl, 64);
+  };
 
   for (long long i = 0; i < n; ++i) {
-    if (bad_c) { status = ST_INVALID; err = bad_c; stop = i; break; }
-    if (nnew >= nnew_cap || mcount >= PCY_MOD_SLOTS / 2) { status = ST_FULL; stop = i; break; }
-    // ---- prefetch item i+1 (scalars, x row, chain record, predicted row) and header of i+2
-    double xn[NPER], pn[NPER];
-    uint4 rpf[(REC_CHUNKS + 31) / 32];
-    const bool has_next = i + 1 < n;
-    ChainHdr h2 = ChainHdr{0, 0, -1, 0};
-    int bad_n = 0; long long w_n = 1; double xs_n = 0.0;
-    if (has_next) {
-      bad_n = BAD ? BAD[i + 1] : 0;
-      w_n = W ? W[i + 1] : 1LL;
-      xs_n = XS[i + 1];
-      load_row<NPER>(xn, X + (i + 1) * ld, d, lane);
-      const uint4* src = reinterpret_cast<const uint4*>(R + (i + 1) * PCY_FMAXL);
-      const int nch = hn.len * (int)(sizeof(ChainLvl) / 16);   // only the levels of the chain
+    const int sl = (int)(i & (K3_SLOTS - 1));
+    const int cur = sl;
+    nbar_sync(K3_BAR_FULL + sl, 64);
+    const ChainHdr hc = S.shdr[sl];
+    const int bad_c = S.sbad[sl];
+    const long long w_c = S.sw[sl];
+    const double xs_c = S.sxs[sl];
+    double* xsm = slotx + sl * ld;
+    double xr[NPER];
 #pragma unroll
-      for (int q = 0; q < (REC_CHUNKS + 31) / 32; ++q) { const int c = lane + 32 * q; if (c < nch) rpf[q] = src[c]; }
-      if (hn.predj >= 0) load_row<NPER>(pn, E.s + (long long)hn.predj * ld, d, lane);
-      if (i + 2 < n) h2 = H[i + 2];
+    for (int k = 0; k < NPER; ++k) { const int e = lane + 32 * k; xr[k] = e < d ? xsm[e] : 0.0; }
+    {
+      // staged predicted row: usable unless the previous item rewrote that node
+      const int np_ = hc.predj;
+      bool recent = multi_left > 0;
+#pragma unroll
+      for (int q = 0; q < K3_SLOTS; ++q) recent |= rec_mod[q] == np_;
+      if (np_ >= 0 && np_ != prnode && !recent) {
+        const double* pd = slotp + sl * ld;
+#pragma unroll
+        for (int k = 0; k < NPER; ++k) { const int e = lane + 32 * k; pr[k] = e < d ? pd[e] : 0.0; }
+        prnode = np_;
+      }
     }
+    if (bad_c) { status = ST_INVALID; err = bad_c; stop = i; signal_stop(sl); break; }
+    if (nnew >= nnew_cap || mcount >= PCY_MOD_SLOTS / 2) { status = ST_FULL; stop = i; signal_stop(sl); break; }
     // ---- item i
     const bool resume = (i == 0 && first_rem >= 0);
     const long long wi = w_c;
@@ -313,9 +383,6 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
     int g = 0, L = 0;
     double radius = T;
     bool direct = false;
-#pragma unroll
-    for (int k = 0; k < NPER; ++k) { const int e = lane + 32 * k; if (e < ld) xsm[e] = xr[k]; }
-    __syncwarp();
     int lastmod = -1;      // last snapshot node this item rewrote (its row is in pr)
     bool multi = false;    // the item rewrote more than one snapshot node
     // current row of snapshot node bj into pr (HBM unless it is the held row)
@@ -547,34 +614,13 @@ __global__ void __launch_bounds__(32, 1) k_resolve2(EngDev E, const double* __re
     }
     __syncwarp();
     ++c_it;
-    if (status != ST_DONE) break;
-    // ---- rotate prefetched data into place
-    if (has_next) {
-      uint4* dst = reinterpret_cast<uint4*>(&S.rb[cur ^ 1][0]);
-      const int nch = hn.len * (int)(sizeof(ChainLvl) / 16);
 #pragma unroll
-      for (int q = 0; q < (REC_CHUNKS + 31) / 32; ++q) { const int c = lane + 32 * q; if (c < nch) dst[c] = rpf[q]; }
-#pragma unroll
-      for (int k = 0; k < NPER; ++k) xr[k] = xn[k];
-      int nextnode = hn.predj;
-      if (nextnode >= 0 && (multi || nextnode == lastmod)) {
-        // a node sits in one group, so an item rewrites it at most once: pr is
-        // its current row exactly when it was the item's last rewrite
-        if (nextnode == lastmod && prnode == lastmod) {
-#pragma unroll
-          for (int k = 0; k < NPER; ++k) pn[k] = pr[k];   // the row this item just rewrote
-        } else {
-          nextnode = -1;                                   // possibly stale prefetch: demand-load later
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < NPER; ++k) pr[k] = pn[k];
-      prnode = nextnode;
-      hc = hn; hn = h2;
-      bad_c = bad_n; w_c = w_n; xs_c = xs_n;
-      cur ^= 1;
-    }
-    __syncwarp();
+    for (int q = K3_SLOTS - 1; q > 0; --q) rec_mod[q] = rec_mod[q - 1];
+    rec_mod[0] = lastmod;
+    multi_left = multi ? K3_SLOTS : (multi_left > 0 ? multi_left - 1 : 0);
+    if (status != ST_DONE) { signal_stop(sl); break; }
+    __threadfence_block();
+    nbar_arrive(K3_BAR_EMPTY + sl, 64);
   }
 
   // ---- cleanup: new nodes and their memberships to HBM (position order per group)
