@@ -25,6 +25,34 @@ __device__ __forceinline__ double row_dot(const double* a, const double* b, int 
   return warp_dot(a, b, d, lane);   // same lane-strided order, loads issued ahead
 }
 
+// s += take * x over one row (lane-strided), written to the smem copy and to
+// HBM: 8 elements in flight per lane; the same rounded operations as
+// element-at-a-time (radd / rmul per element), so the values are identical.
+__device__ __forceinline__ void row_absorb(double* __restrict__ prow, const double* __restrict__ x,
+                                           double* __restrict__ dst, int d, int lane, long long take) {
+  const double ft = (double)take;
+  int e = lane;
+  if (take == 1) {
+    for (; e + 7 * 32 < d; e += 8 * 32) {
+      double v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = radd(prow[e + 32 * q], x[e + 32 * q]);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) { prow[e + 32 * q] = v[q]; if (dst) dst[e + 32 * q] = v[q]; }
+    }
+    for (; e < d; e += 32) { const double v = radd(prow[e], x[e]); prow[e] = v; if (dst) dst[e] = v; }
+  } else {
+    for (; e + 7 * 32 < d; e += 8 * 32) {
+      double v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = radd(prow[e + 32 * q], rmul(ft, x[e + 32 * q]));
+#pragma unroll
+      for (int q = 0; q < 8; ++q) { prow[e + 32 * q] = v[q]; if (dst) dst[e + 32 * q] = v[q]; }
+    }
+    for (; e < d; e += 32) { const double v = radd(prow[e], rmul(ft, x[e])); prow[e] = v; if (dst) dst[e] = v; }
+  }
+}
+
 template <int MS>
 struct ResolveSmemT {
   ChainLvl rb[2][PCY_FMAXL];
@@ -322,12 +350,8 @@ __global__ void __launch_bounds__(32, 1) k_resolve3(EngDev E, const double* __re
     auto absorb_snapshot = [&](int bj, long long take, long long nw2, double nq, double nsn, int child_now) {
       const double ft = (double)take;
       if (bj != prnode) load_prow(bj);
-      double* dst = E.s + (long long)bj * ld;
-      for (int e = lane; e < d; e += 32) {
-        const double v = take == 1 ? radd(prow[e], xsm[e]) : radd(prow[e], rmul(ft, xsm[e]));
-        prow[e] = v;
-        dst[e] = v;
-      }
+      (void)ft;
+      row_absorb(prow, xsm, E.s + (long long)bj * ld, d, lane, take);
       __syncwarp();
       const int ms = map3_put<MS>(S, mbits, bj, nw2, nq, nsn, child_now, lane);
       if (lane == 0) { E.w[bj] = nw2; E.q[bj] = nq; E.sn[bj] = nsn; }
@@ -430,8 +454,7 @@ __global__ void __launch_bounds__(32, 1) k_resolve3(EngDev E, const double* __re
       if (take > 0) {
         const double ft = (double)take;
         if (bt >= 0) {
-          for (int e = lane; e < d; e += 32)
-            trow[e] = take == 1 ? radd(trow[e], xsm[e]) : radd(trow[e], rmul(ft, xsm[e]));
+          row_absorb(trow, xsm, nullptr, d, lane, take);
           if (lane == 0) { S.tw[bt] = nw2; S.tq[bt] = nq; S.tsn[bt] = nsn; }
           __syncwarp();
         } else {
@@ -665,7 +688,7 @@ __global__ void __launch_bounds__(32, 1) k_reattach3(EngDev E, const int* __rest
           prnode = bj;
         }
         double* dst = E.s + (long long)bj * ld;
-        for (int e = lane; e < d; e += 32) { const double v = radd(prow[e], su[e]); prow[e] = v; dst[e] = v; }
+        row_absorb(prow, su, dst, d, lane, 1);
         __syncwarp();
         if (bt >= 0) {
           if (lane == 0) { S.tw[bt] = mw; S.tq[bt] = mq; S.tsn[bt] = mnorm; }
