@@ -20,6 +20,67 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 __device__ __forceinline__ void row_fetch(double* dst, const double* src, int ld, int lane) {
   for (int c = lane; c < ld / 2; c += 32) cp_async16(dst + 2 * c, src + 2 * c);
 }
+
+// Whole rows global -> shared with one bulk (TMA) copy each, completed on an
+// mbarrier (expect_tx = all bytes of the batch).  All lanes first fence the
+// generic proxy against the async proxy (earlier plain stores to the source
+// rows in HBM and to the destination buffers in shared memory), then lane 0
+// issues.  rows_wait spins on the barrier's current phase.
+__device__ __forceinline__ void rows_issue(unsigned long long* bar, int lane, unsigned bytes, double* d0,
+                                           const double* s0, double* d1, const double* s1, double* d2,
+                                           const double* s2) {
+  asm volatile("fence.proxy.async;" ::: "memory");
+  __syncwarp();
+  if (lane == 0) {
+    const unsigned total = bytes * (unsigned)(1 + (s1 != nullptr) + (s2 != nullptr));
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(total) : "memory");
+    double* ds[3] = {d0, d1, d2};
+    const double* ss[3] = {s0, s1, s2};
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+      if (ss[q])
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         (unsigned)__cvta_generic_to_shared(ds[q])),
+                     "l"(ss[q]), "r"(bytes), "r"(b)
+                     : "memory");
+  }
+}
+__device__ __forceinline__ void rows_wait(unsigned long long* bar, unsigned& phase) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "RW_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra RW_DONE;\n\t"
+      "bra RW_WAIT;\n"
+      "RW_DONE:\n\t}" ::"r"(b),
+      "r"(phase)
+      : "memory");
+  phase ^= 1u;
+}
+// Row prefetch: bulk copies for long rows (>= 16 KB, where one TMA copy per
+// row beats 512+ cp.async per lane and the proxy fence), cp.async otherwise.
+__device__ __forceinline__ void rows_fetch(bool bulk, unsigned long long* bar, int lane, int ld, double* d0,
+                                           const double* s0, double* d1, const double* s1, double* d2,
+                                           const double* s2) {
+  if (bulk) {
+    rows_issue(bar, lane, (unsigned)(sizeof(double) * ld), d0, s0, d1, s1, d2, s2);
+  } else {
+    row_fetch(d0, s0, ld, lane);
+    if (s1) row_fetch(d1, s1, ld, lane);
+    if (s2) row_fetch(d2, s2, ld, lane);
+  }
+}
+
+__device__ __forceinline__ void rows_bar_init(unsigned long long* bar, int n, int lane) {
+  if (lane == 0) {
+    for (int q = 0; q < n; ++q)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(bar + q)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+}
 // lane-strided fp64 dot in warp_dot order (shared with K1's snapshot dots)
 __device__ __forceinline__ double row_dot(const double* a, const double* b, int d, int lane) {
   return warp_dot(a, b, d, lane);   // same lane-strided order, loads issued ahead
@@ -65,6 +126,7 @@ struct ResolveSmemT {
   int titem[PCY_NNEW_MAX];   // Gram row of the item that placed the entry
   long long tw[PCY_NNEW_MAX];
   double trn[PCY_NNEW_MAX], tq[PCY_NNEW_MAX], tsn[PCY_NNEW_MAX];
+  unsigned long long rbar[2];   // bulk row copies into buffer 0 / 1
   int modcount;
 };
 
@@ -269,14 +331,18 @@ __global__ void __launch_bounds__(32, 1) k_resolve3(EngDev E, const double* __re
   double xs_c = n > 0 ? XS[0] : 0.0;
   ChainHdr hc = n > 0 ? H[0] : ChainHdr{0, 0, -1, 0};
   ChainHdr hn = n > 1 ? H[1] : ChainHdr{0, 0, -1, 0};
+  rows_bar_init(S.rbar, 2, lane);
+  unsigned rph[2] = {0u, 0u};
+  const bool bulk = ld >= 2048;
   if (n > 0) {
-    row_fetch(xb, X, ld, lane);
-    if (hc.predj >= 0) row_fetch(pb, E.s + (long long)hc.predj * ld, ld, lane);
+    rows_fetch(bulk, &S.rbar[0], lane, ld, xb, X, pb, hc.predj >= 0 ? E.s + (long long)hc.predj * ld : nullptr,
+               nullptr, nullptr);
     const uint4* src = reinterpret_cast<const uint4*>(R);
     uint4* dst = reinterpret_cast<uint4*>(&S.rb[0][0]);
     for (int c = lane; c < REC3_CHUNKS; c += 32) cp_async16(dst + c, src + c);
     cp_async_commit();
     cp_async_wait_all();
+    if (bulk) rows_wait(&S.rbar[0], rph[0]);
   }
   __syncwarp();
   int cur = 0;
@@ -295,8 +361,9 @@ __global__ void __launch_bounds__(32, 1) k_resolve3(EngDev E, const double* __re
       bad_n = BAD ? BAD[i + 1] : 0;
       w_n = W ? W[i + 1] : 1LL;
       xs_n = XS[i + 1];
-      row_fetch(xb + (long long)(cur ^ 1) * ld, X + (i + 1) * ld, ld, lane);
-      if (hn.predj >= 0) row_fetch(pb + (long long)(cur ^ 1) * ld, E.s + (long long)hn.predj * ld, ld, lane);
+      rows_fetch(bulk, &S.rbar[cur ^ 1], lane, ld, xb + (long long)(cur ^ 1) * ld, X + (i + 1) * ld,
+                 pb + (long long)(cur ^ 1) * ld, hn.predj >= 0 ? E.s + (long long)hn.predj * ld : nullptr,
+                 nullptr, nullptr);
       const uint4* src = reinterpret_cast<const uint4*>(R + (i + 1) * PCY_FMAXL);
       uint4* dst = reinterpret_cast<uint4*>(&S.rb[cur ^ 1][0]);
       for (int c = lane; c < REC3_CHUNKS; c += 32) cp_async16(dst + c, src + c);
@@ -492,9 +559,10 @@ __global__ void __launch_bounds__(32, 1) k_resolve3(EngDev E, const double* __re
     }
     __syncwarp();
     ++c_it;
-    if (status != ST_DONE) break;
+    if (status != ST_DONE) { if (has_next && bulk) rows_wait(&S.rbar[cur ^ 1], rph[cur ^ 1]); break; }
     if (has_next) {
       cp_async_wait_all();
+      if (bulk) rows_wait(&S.rbar[cur ^ 1], rph[cur ^ 1]);
       __syncwarp();
       int nextnode = hn.predj;
       bool hit = nmod > 4 || nextnode == lastmod;
@@ -580,16 +648,19 @@ __global__ void __launch_bounds__(32, 1) k_reattach3(EngDev E, const int* __rest
   ChainHdr hc = n > 0 ? H[0] : ChainHdr{0, 0, -1, 0};
   ChainHdr hn = n > 1 ? H[1] : ChainHdr{0, 0, -1, 0};
   long long wu_c = 0; double qu_c = 0.0, snu_c = 0.0, rsq_c = 0.0;
+  rows_bar_init(S.rbar, 2, lane);
+  unsigned rph[2] = {0u, 0u};
+  const bool bulk = ld >= 2048;
   if (n > 0) {
-    row_fetch(xb, E.r + (long long)u_c * ld, ld, lane);
-    row_fetch(sb, E.s + (long long)u_c * ld, ld, lane);
-    if (hc.predj >= 0) row_fetch(pb, E.s + (long long)hc.predj * ld, ld, lane);
+    rows_fetch(bulk, &S.rbar[0], lane, ld, xb, E.r + (long long)u_c * ld, sb, E.s + (long long)u_c * ld, pb,
+               hc.predj >= 0 ? E.s + (long long)hc.predj * ld : nullptr);
     wu_c = E.w[u_c]; qu_c = E.q[u_c]; snu_c = E.sn[u_c]; rsq_c = E.rn[u_c];
     const uint4* src = reinterpret_cast<const uint4*>(R);
     uint4* dst = reinterpret_cast<uint4*>(&S.rb[0][0]);
     for (int c = lane; c < REC3_CHUNKS; c += 32) cp_async16(dst + c, src + c);
     cp_async_commit();
     cp_async_wait_all();
+    if (bulk) rows_wait(&S.rbar[0], rph[0]);
   }
   __syncwarp();
   int cur = 0;
@@ -605,9 +676,9 @@ __global__ void __launch_bounds__(32, 1) k_reattach3(EngDev E, const int* __rest
     int u2 = 0;
     long long wu_n = 0; double qu_n = 0.0, snu_n = 0.0, rsq_n = 0.0;
     if (has_next) {
-      row_fetch(xb + (long long)(cur ^ 1) * ld, E.r + (long long)u_n * ld, ld, lane);
-      row_fetch(sb + (long long)(cur ^ 1) * ld, E.s + (long long)u_n * ld, ld, lane);
-      if (hn.predj >= 0) row_fetch(pb + (long long)(cur ^ 1) * ld, E.s + (long long)hn.predj * ld, ld, lane);
+      rows_fetch(bulk, &S.rbar[cur ^ 1], lane, ld, xb + (long long)(cur ^ 1) * ld, E.r + (long long)u_n * ld,
+                 sb + (long long)(cur ^ 1) * ld, E.s + (long long)u_n * ld, pb + (long long)(cur ^ 1) * ld,
+                 hn.predj >= 0 ? E.s + (long long)hn.predj * ld : nullptr);
       const uint4* src = reinterpret_cast<const uint4*>(R + (i + 1) * PCY_FMAXL);
       uint4* dst = reinterpret_cast<uint4*>(&S.rb[cur ^ 1][0]);
       for (int c = lane; c < REC3_CHUNKS; c += 32) cp_async16(dst + c, src + c);
@@ -733,6 +804,7 @@ __global__ void __launch_bounds__(32, 1) k_reattach3(EngDev E, const int* __rest
     __syncwarp();
     if (has_next) {
       cp_async_wait_all();
+      if (bulk) rows_wait(&S.rbar[cur ^ 1], rph[cur ^ 1]);
       __syncwarp();
       int nextnode = hn.predj;
       if (nextnode >= 0 && nextnode == lastmod) {
