@@ -25,6 +25,12 @@ constexpr int TBM = 128, TBN = 128, TBK = 32, TSTAGES = 3;
 constexpr int TILE_BYTES = TBM * TBK * 4;            // 16 KB: one operand tile (hi or lo)
 constexpr int STAGE_BYTES = 4 * TILE_BYTES;          // Ahi, Alo, Bhi, Blo
 constexpr int TC_SMEM = TSTAGES * STAGE_BYTES + 1024 + 256;
+// K is split into up to TC_NACC consecutive chunks, each accumulated in its own
+// 128-column TMEM accumulator (4 x 128 = all 512 columns); the epilogue adds
+// the chunk sums in fp64.  Fewer fp32 accumulation steps per sum tighten the
+// rigorous error bound (pcy_tc_error_tau) and so the near-tie window.
+constexpr int TC_NACC = 4;
+__host__ __device__ inline int tc_nacc(int nk) { return nk < TC_NACC ? nk : TC_NACC; }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -104,7 +110,7 @@ __global__ void __launch_bounds__(128, 1) k_tc_dots(const __grid_constant__ CUte
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(TBN));
+                 "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -129,19 +135,23 @@ __global__ void __launch_bounds__(128, 1) k_tc_dots(const __grid_constant__ CUte
     // MMA issuer: M=128, N=128, K=8 per instruction, fp32 accumulate
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TBN >> 3) << 17) |
                            ((uint32_t)(TBM >> 4) << 24);
+    const int nacc = tc_nacc(nk);
     for (int kb = 0; kb < nk; ++kb) {
       const int s = kb % TSTAGES;
       mbar_wait(full + s, (kb / TSTAGES) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t a_hi = smem_u32(smem + s * STAGE_BYTES);
       const uint32_t a_lo = a_hi + TILE_BYTES, b_hi = a_hi + 2 * TILE_BYTES, b_lo = a_hi + 3 * TILE_BYTES;
+      const int ac = (kb * nacc) / nk;                                  // this stage's K chunk
+      const bool first = kb == 0 || ((kb - 1) * nacc) / nk != ac;      // first stage of the chunk
+      const uint32_t dcol = tmem + (uint32_t)(ac * TBN);
 #pragma unroll
       for (int ks = 0; ks < TBK / 8; ++ks) {
         const uint32_t off = ks * 32;   // 8 tf32 = 32 B along K inside the swizzle atom
-        const uint32_t acc0 = (kb | ks) != 0;
-        mma_tf32(tmem, sw128_desc(a_hi + off), sw128_desc(b_hi + off), idesc, acc0);
-        mma_tf32(tmem, sw128_desc(a_hi + off), sw128_desc(b_lo + off), idesc, 1u);
-        mma_tf32(tmem, sw128_desc(a_lo + off), sw128_desc(b_hi + off), idesc, 1u);
+        const uint32_t acc0 = (first && ks == 0) ? 0u : 1u;
+        mma_tf32(dcol, sw128_desc(a_hi + off), sw128_desc(b_hi + off), idesc, acc0);
+        mma_tf32(dcol, sw128_desc(a_hi + off), sw128_desc(b_lo + off), idesc, 1u);
+        mma_tf32(dcol, sw128_desc(a_lo + off), sw128_desc(b_hi + off), idesc, 1u);
       }
       mma_commit(empty + s);   // frees the stage when these MMAs complete
     }
@@ -154,35 +164,43 @@ __global__ void __launch_bounds__(128, 1) k_tc_dots(const __grid_constant__ CUte
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const int row = warp * 32 + lane;
   const long long gm = m0 + row;
+  const int nacc = tc_nacc(nk);
   for (int c0 = 0; c0 < TBN; c0 += 32) {
-    uint32_t v[32];
-    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    double acc[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) acc[q] = 0.0;
+    for (int ac = 0; ac < nacc; ++ac) {
+      uint32_t v[32];
+      const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(ac * TBN + c0);
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+            "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+            "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int q = 0; q < 32; ++q) acc[q] += (double)__uint_as_float(v[q]);   // chunk order, fp64
+    }
     if (gm < M) {
       float* o = out + gm * ldo + n0 + c0;
       if (n0 + c0 + 32 <= N && ((ldo & 3) == 0)) {
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-          reinterpret_cast<float4*>(o)[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
-                                                        __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+          reinterpret_cast<float4*>(o)[q] = make_float4((float)acc[4 * q], (float)acc[4 * q + 1], (float)acc[4 * q + 2],
+                                                        (float)acc[4 * q + 3]);
       } else {
 #pragma unroll
         for (int q = 0; q < 32; ++q)
-          if (n0 + c0 + q < N) o[q] = __uint_as_float(v[q]);
+          if (n0 + c0 + q < N) o[q] = (float)acc[q];
       }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TBN));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
 // One warp per row: hi/lo TF32 split of (row - c), zero padded to Kp, and the
@@ -248,13 +266,18 @@ int make_map(CUtensorMap* map, const float* base, long long rows, int Kp) {
 }  // namespace
 
 // Rigorous bound on |approx - exact| of a 3xTF32 dot over Kp (padded) terms,
-// relative to |a - c| |b - c|: split residues (<= 3 * 2^-22 per term) plus one
-// fp32 rounding (<= 2^-23 of the running magnitude, which never exceeds the
-// sum of |terms| <= |a-c||b-c| (1 + 2^-10)) per accumulation step: 3 products
-// x Kp/8 MMAs into the accumulator and <= 4 steps inside each 8-term MMA.
+// relative to |a - c| |b - c|: split residues (<= 3 * 2^-22 per term); per K
+// chunk one fp32 rounding (<= 2^-23 of the chunk's running magnitude, at most
+// the chunk's sum of |terms|) per accumulation step: 3 products x Kc/8 MMAs
+// and <= 4 steps inside each 8-term MMA.  The chunk sums are added in fp64 and
+// their |terms| sums add up to <= |a-c||b-c| (1 + 2^-10) by Cauchy-Schwarz;
+// the fp32 output adds 2^-24 of |dot| <= |a-c||b-c|.
 double pcy_tc_error_tau(int Kp) {
-  const double steps = 3.0 * (Kp / 8.0) * 5.0 + 8.0;
-  return (steps * 0x1p-23 + 3.0 * 0x1p-22) * (1.0 + 0x1p-9);
+  const int nk = Kp / TBK;
+  const int nacc = tc_nacc(nk > 0 ? nk : 1);
+  const int kc = ((nk + nacc - 1) / nacc) * TBK;   // longest chunk
+  const double steps = 3.0 * (kc / 8.0) * 5.0 + 8.0;
+  return (steps * 0x1p-23 + 3.0 * 0x1p-22 + 0x1p-24 + 8.0 * 0x1p-53) * (1.0 + 0x1p-9);
 }
 
 int pcy_tc_pad(int d) { return (d + TBK - 1) / TBK * TBK; }
