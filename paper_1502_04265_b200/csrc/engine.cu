@@ -890,6 +890,10 @@ struct Engine {
   double tc_tau = 0.0;
   float *tc_ahi = nullptr, *tc_alo = nullptr, *tc_bhi = nullptr, *tc_blo = nullptr, *tc_dots = nullptr;
   double *tc_rnc = nullptr, *tc_xn2 = nullptr, *tc_c = nullptr;
+  unsigned* parbits = nullptr;   // k_plan scratch: nodes some window item acts on
+  ParCtl* parctl = nullptr;   // k_plan output (subtree-parallel resolve)
+  long long kbatch = 1024;     // K1 rows per launch when k3par
+  bool k3par = false;         // subtree-parallel resolve enabled (nper 1..8)
   int nper = 0;          // resolve kernel: 1..8 register rows, 100/101 shared-memory rows, 0 generic
   int nnew_cap = 0, rea_cap = 0;   // new-node table sizes of K3 and of the reattach
   size_t res_smem = 0, rea_smem = 0;
@@ -979,6 +983,7 @@ struct Engine {
     A_(E.order, NC); A_(E.lvl, NC); A_(E.stk_g, NC + 1); A_(E.stk_p, NC + 1);
     A_(E.minbits, 2);
     A_(aggw, m + 2); A_(mp_nrm, sample_cap + 1);
+    A_(parctl, 1); A_(parbits, NC / 32 + 2);
 #undef A_
     for (auto& e : ev) PCY_CUDA(cudaEventCreate(&e));
     {
@@ -1015,12 +1020,16 @@ struct Engine {
       if (nnew_cap < 8) { nper = 0; use_tc = false; }
       switch (nper) {
         case 1: PCY_CUDA(cudaFuncSetAttribute(k_resolve2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
+                PCY_CUDA(cudaFuncSetAttribute(k_resolve2<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
                 PCY_CUDA(cudaFuncSetAttribute(k_reattach2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem)); break;
         case 2: PCY_CUDA(cudaFuncSetAttribute(k_resolve2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
+                PCY_CUDA(cudaFuncSetAttribute(k_resolve2<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
                 PCY_CUDA(cudaFuncSetAttribute(k_reattach2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem)); break;
         case 4: PCY_CUDA(cudaFuncSetAttribute(k_resolve2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
+                PCY_CUDA(cudaFuncSetAttribute(k_resolve2<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
                 PCY_CUDA(cudaFuncSetAttribute(k_reattach2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem)); break;
         case 8: PCY_CUDA(cudaFuncSetAttribute(k_resolve2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
+                PCY_CUDA(cudaFuncSetAttribute(k_resolve2<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
                 PCY_CUDA(cudaFuncSetAttribute(k_reattach2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem)); break;
         default: break;
       }
@@ -1045,6 +1054,10 @@ struct Engine {
       }
     }
     if (getenv("PCY_GENERIC_RESOLVE")) nper = 0;
+    {
+      const char* pe = getenv("PCY_K3PAR");
+      k3par = nper >= 1 && nper <= 8 && (!pe || atoi(pe) != 0);
+    }
     if (!(ctl_h = ctl_pool_get())) { pcy_set_error("cudaHostAlloc of the control mirror failed"); return PCY_ENOMEM; }
     memset(ctl_h, 0, sizeof(EngCtl));
     PCY_CUDA(cudaHostGetDevicePointer((void**)&ctl_map_d, ctl_h, 0));
@@ -1190,6 +1203,9 @@ struct Engine {
       const long long nb = n - off < sub ? n - off : sub;
       long long start = 0, first_rem = -1;
       while (start < nb) {
+        // K1 chains kn rows; with the subtree-parallel resolve the batch follows
+        // where the windows stop, so rows are not re-chained many times
+        const long long kn = k3par && nb - start > kbatch ? kbatch : nb - start;
         const double* Xs = X + (off + start) * ld;
         const double* XSs = XS + off + start;
         const bool prof = pcy_prof_enabled();
@@ -1197,40 +1213,56 @@ struct Engine {
         const long long* Ws = W ? W + off + start : nullptr;
         const int* Bs = BAD ? BAD + off + start : nullptr;
         const int wpc = ld <= 512 ? 8 : (ld <= 2048 ? 4 : 2);
-        const unsigned nblk = (unsigned)((nb - start + wpc - 1) / wpc);
+        const unsigned nblk = (unsigned)((kn + wpc - 1) / wpc);
         if (!nper) { k_snapshot<<<64, 256, 0, st>>>(E); pcy_count_launch(); }
         if (prof) PCY_CUDA(cudaEventRecord(ev[0], st));
         if (nper) {
           int grc;
-          const bool use_p = full_set(Xs, nullptr, nb - start, st, &grc);
+          const bool use_p = full_set(Xs, nullptr, kn, st, &grc);
           if (grc) return grc;
           if (ld > 512)   // one item per CTA, dots split over 4 warps
-            k_chain2<4><<<(unsigned)(nb - start), 128, sizeof(double) * (ld + 8), st>>>(
-                E, Xs, XSs, Ws, nb - start, chh, chr, use_p ? parts : nullptr, ctl_h->F_alloc);
+            k_chain2<4><<<(unsigned)(kn), 128, sizeof(double) * (ld + 8), st>>>(
+                E, Xs, XSs, Ws, kn, chh, chr, use_p ? parts : nullptr, ctl_h->F_alloc);
           else
-            k_chain2<1><<<nblk, wpc * 32, sizeof(double) * wpc * ld, st>>>(E, Xs, XSs, Ws, nb - start, chh, chr,
+            k_chain2<1><<<nblk, wpc * 32, sizeof(double) * wpc * ld, st>>>(E, Xs, XSs, Ws, kn, chh, chr,
                                                                           use_p ? parts : nullptr, ctl_h->F_alloc);
           pcy_count_launch();
           if (nper == 101) {
-            rc0 = pcy_launch_gram(Xs, nullptr, ld, (int)(nb - start), Xs, nullptr, ld, (int)(nb - start), d, gram,
-                                  nb - start, st);
+            rc0 = pcy_launch_gram(Xs, nullptr, ld, (int)(kn), Xs, nullptr, ld, (int)(kn), d, gram,
+                                  kn, st);
             if (rc0) return rc0;
           }
         } else {
-          k_chain<<<nblk, wpc * 32, sizeof(double) * wpc * ld, st>>>(E, Xs, XSs, nb - start); pcy_count_launch();
+          k_chain<<<nblk, wpc * 32, sizeof(double) * wpc * ld, st>>>(E, Xs, XSs, kn); pcy_count_launch();
         }
         cudaStream_t rs = st;
         if (hi) { PCY_CUDA(cudaEventRecord(evk1, st)); PCY_CUDA(cudaStreamWaitEvent(hi, evk1, 0)); rs = hi; }
         if (prof) PCY_CUDA(cudaEventRecord(ev[1], rs));
+        ParCtl* pp = nullptr;
+        if (k3par) {
+          // k_plan picks a subtree-parallel window or a sequential stretch; the
+          // launch that was not chosen returns at once
+          k_plan<<<1, PCY_PAR_MAXITEMS, 0, rs>>>(E, XSs, Ws, Bs, kn, first_rem, nnew_cap, 16, chh, chr, parctl,
+                                                 parbits, (int)(NC / 32 + 1));
+          pcy_count_launch();
+          pp = parctl;
+          switch (nper) {
+            case 1: k_resolve2<1, true><<<PCY_PAR_MAXCTA, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, pp); break;
+            case 2: k_resolve2<2, true><<<PCY_PAR_MAXCTA, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, pp); break;
+            case 4: k_resolve2<4, true><<<PCY_PAR_MAXCTA, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, pp); break;
+            case 8: k_resolve2<8, true><<<PCY_PAR_MAXCTA, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, pp); break;
+          }
+          pcy_count_launch();
+        }
         switch (nper) {
-          case 1: k_resolve2<1><<<1, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
-          case 2: k_resolve2<2><<<1, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
-          case 4: k_resolve2<4><<<1, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
-          case 8: k_resolve2<8><<<1, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr); pcy_count_launch(); break;
-          case 100: k_resolve3<true, 2048><<<1, 32, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr, nullptr, 0, 0); pcy_count_launch(); break;
-          case 101: k_resolve3<false, 512><<<1, 32, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, nb - start, first_rem, countw, nnew_cap, chh, chr, gram, nb - start, 0); pcy_count_launch(); break;
+          case 1: k_resolve2<1><<<1, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, pp); pcy_count_launch(); break;
+          case 2: k_resolve2<2><<<1, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, pp); pcy_count_launch(); break;
+          case 4: k_resolve2<4><<<1, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, pp); pcy_count_launch(); break;
+          case 8: k_resolve2<8><<<1, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, pp); pcy_count_launch(); break;
+          case 100: k_resolve3<true, 2048><<<1, 32, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, nullptr, 0, 0); pcy_count_launch(); break;
+          case 101: k_resolve3<false, 512><<<1, 32, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, gram, kn, 0); pcy_count_launch(); break;
           default:
-            k_resolve<<<1, 32, sizeof(double) * ld, rs>>>(E, Xs, XSs, Ws, Bs, nb - start, 0, first_rem, countw); pcy_count_launch();
+            k_resolve<<<1, 32, sizeof(double) * ld, rs>>>(E, Xs, XSs, Ws, Bs, kn, 0, first_rem, countw); pcy_count_launch();
         }
         if (prof) PCY_CUDA(cudaEventRecord(ev[2], rs));
         PCY_LAUNCH_CHECK();
@@ -1241,8 +1273,8 @@ struct Engine {
           float t1 = 0.f, t2 = 0.f;
           PCY_CUDA(cudaEventElapsedTime(&t1, ev[0], ev[1]));
           PCY_CUDA(cudaEventElapsedTime(&t2, ev[1], ev[2]));
-          const long long done = ctl_h->status == ST_DONE ? nb - start : ctl_h->stop + (ctl_h->status == ST_FULL ? 0 : 1);
-          pcy_prof_add(PCY_PROF_CHAIN, t1, nb - start);
+          const long long done = ctl_h->status == ST_DONE ? kn : ctl_h->stop + (ctl_h->status == ST_FULL ? 0 : 1);
+          pcy_prof_add(PCY_PROF_CHAIN, t1, kn);
           pcy_prof_add(PCY_PROF_RESOLVE, t2, done);
           if (gemm_timed) {
             float tg = 0.f;
@@ -1252,18 +1284,26 @@ struct Engine {
           }
           static FILE* trace = getenv("PCY_TRACE_K3") ? fopen(getenv("PCY_TRACE_K3"), "a") : nullptr;
           if (trace) {
-            fprintf(trace, "%lld %.4f %.4f %d %lld %lld %lld %lld\n", done, t1, t2, ctl_h->status, ctl_h->F,
-                    ctl_h->cnt_slow, ctl_h->cnt_levels, ctl_h->root_count);
+            int pm[2] = {-1, 0};
+            if (k3par) cudaMemcpy(pm, parctl, sizeof(pm), cudaMemcpyDeviceToHost);
+            fprintf(trace, "%lld %.4f %.4f %d %lld %lld %lld %lld %d %d\n", done, t1, t2, ctl_h->status, ctl_h->F,
+                    ctl_h->cnt_slow, ctl_h->cnt_levels, ctl_h->root_count, pm[0], pm[1]);
             fflush(trace);
           }
         }
         const int status = ctl_h->status;
-        if (status == ST_DONE) break;
+        if (status == ST_DONE) {
+          if (k3par) kbatch = kbatch * 2 > 1024 ? 1024 : kbatch * 2;
+          if (kn < nb - start) { start += kn; first_rem = -1; continue; }
+          break;
+        }
         if (status == ST_INVALID) { *bad_at = off + start + ctl_h->stop; *bad_code = ctl_h->err; return PCY_OK; }
         if (status == ST_ARENA) { pcy_set_error("member arena exhausted"); return PCY_ESTATE; }
+        if (status == ST_PAR_BROKEN) { pcy_set_error("subtree-parallel resolve met an excluded stop"); return PCY_ESTATE; }
         if (status == ST_FULL) {
           if (ctl_h->stop == 0) { pcy_set_error("resolve made no progress"); return PCY_ESTATE; }
           start += ctl_h->stop; first_rem = -1;
+          if (k3par) { const long long b2 = 2 * ctl_h->stop; kbatch = b2 < 128 ? 128 : b2 > 1024 ? 1024 : b2; }
           continue;
         }
         if (status == ST_REBUILD) {

@@ -15,6 +15,7 @@ enum {
   ST_GROW = 4,      // bootstrap pending buffer full before item `stop`
   ST_ARENA = 5,     // member arena exhausted (internal error)
   ST_FULL = 6,      // resolve tables full before item `stop`: relaunch from there
+  ST_PAR_BROKEN = 7,  // a subtree-parallel resolve CTA met a stop k_plan excludes (internal error)
 };
 
 struct EngCtl {
@@ -36,6 +37,28 @@ struct EngCtl {
   long long cnt_levels, cnt_direct, cnt_demand, cnt_slow, cnt_items, cnt_dem_fast, cnt_touch_child;
   long long root_count, root_base;   // group 0 (copied by k_publish for the host)
   long long seq;          // publication sequence number (mapped host mirror)
+};
+
+// Subtree-parallel resolve (k_plan + k_resolve2<NPER, true>, resolve_fast.cuh).
+// Between two changes of the root group, an item's decisions read and write
+// only the subtree of its root winner (coreset.py:318-372 descend from
+// group.nodes[j] into its children), so the items of a window with no root
+// open, no rebuild (F0 + window <= budget) and no invalid row are resolved by
+// one CTA per root subtree, each in stream order.  k_plan writes the window
+// and the per-CTA item lists; the resolve CTAs allocate slots, groups and
+// arena extents through the tickets and the last CTA publishes the counters.
+#define PCY_PAR_MAXCTA 148
+#define PCY_PAR_MAXITEMS 1024
+struct ParCtl {
+  int mode;            // 0: parallel window, 1: sequential kernel
+  int P;               // resolve CTAs with items
+  long long n_win;     // items in the window (parallel) / for the sequential kernel
+  long long n_total;   // items chained by K1 (the block)
+  long long F0, Falloc0, freen0, Galloc0, Aalloc0, nidx0;   // control snapshot
+  unsigned long long open_ticket, g_ticket, a_ticket, done, opens;
+  int arena_fail, pad;
+  int off[PCY_PAR_MAXCTA + 1];
+  int list[PCY_PAR_MAXITEMS];
 };
 
 struct EngDev {

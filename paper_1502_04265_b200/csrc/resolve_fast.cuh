@@ -241,15 +241,37 @@ __device__ __forceinline__ void nbar_sync(int id, int cnt) { asm volatile("bar.s
 __device__ __forceinline__ void nbar_arrive(int id, int cnt) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(cnt) : "memory"); }
 constexpr int K3_SLOTS = 4, K3_BAR_FULL = 1, K3_BAR_EMPTY = 1 + K3_SLOTS;   // + slot
 
-template <int NPER>
+// PAR = false: one CTA resolves items 0..n-1 in stream order (with `par`
+// non-null it runs only when k_plan chose the sequential mode, for
+// par->n_win items).  PAR = true: CTA b resolves the items of root subtree
+// list b of k_plan's window (see ParCtl), allocating through the tickets.
+template <int NPER, bool PAR = false>
 __global__ void __launch_bounds__(64, 1) k_resolve2(EngDev E, const double* __restrict__ X,
                                                     const double* __restrict__ XS, const long long* __restrict__ W,
                                                     const int* __restrict__ BAD, long long n, long long first_rem,
                                                     int countw, int nnew_cap, const ChainHdr* __restrict__ H,
-                                                    const ChainLvl* __restrict__ R) {
+                                                    const ChainLvl* __restrict__ R, ParCtl* __restrict__ par = nullptr) {
   extern __shared__ __align__(16) unsigned char smraw[];
   ResolveSmem& S = *reinterpret_cast<ResolveSmem*>(smraw);
   const int lane = threadIdx.x & 31;
+  const int* ilist = nullptr;
+  if constexpr (PAR) {
+    if (par->mode != 0 || (int)blockIdx.x >= par->P) return;
+    const int o0 = par->off[blockIdx.x];
+    ilist = par->list + o0;
+    n = par->off[blockIdx.x + 1] - o0;
+    first_rem = -1;
+  } else {
+    if (par) {
+      if (par->mode != 1) return;
+      n = par->n_win;
+    }
+  }
+  // window position of local item j (the block row K1 chained)
+  auto gix = [&](long long j) -> long long {
+    if constexpr (PAR) return (long long)ilist[j];
+    else return j;
+  };
   const int d = E.d, ld = E.ld;
   double* slotx = reinterpret_cast<double*>(smraw + ((sizeof(ResolveSmem) + 15) & ~size_t(15)));   // [K3_SLOTS][ld]
   double* slotp = slotx + K3_SLOTS * ld;                                                             // [K3_SLOTS][ld]
@@ -272,7 +294,8 @@ __global__ void __launch_bounds__(64, 1) k_resolve2(EngDev E, const double* __re
     // node are needed to issue its loads)
     constexpr int RQ = (REC_CHUNKS + 31) / 32;
     struct Stage { double x[NPER], p[NPER]; uint4 r[RQ]; ChainHdr h; int bad; long long w; double xs; };
-    auto fetch = [&](Stage& t, long long j, const ChainHdr& h) {
+    auto fetch = [&](Stage& t, long long jl, const ChainHdr& h) {
+      const long long j = gix(jl);
       t.h = h;
       t.bad = BAD ? BAD[j] : 0; t.w = W ? W[j] : 1LL; t.xs = XS[j];
       load_row<NPER>(t.x, X + j * ld, d, lane);
@@ -283,8 +306,8 @@ __global__ void __launch_bounds__(64, 1) k_resolve2(EngDev E, const double* __re
       for (int q = 0; q < RQ; ++q) { const int c = lane + 32 * q; if (c < nch) t.r[q] = src[c]; }
     };
     Stage cur_st, nxt_st;
-    ChainHdr h_ahead = n > 1 ? H[1] : ChainHdr{0, 0, -1, 0};
-    if (n > 0) fetch(cur_st, 0, H[0]);
+    ChainHdr h_ahead = n > 1 ? H[gix(1)] : ChainHdr{0, 0, -1, 0};
+    if (n > 0) fetch(cur_st, 0, H[gix(0)]);
     for (long long j = 0; j < n; ++j) {
       const int sl = (int)(j & (K3_SLOTS - 1));
       if (j >= K3_SLOTS) {
@@ -293,7 +316,7 @@ __global__ void __launch_bounds__(64, 1) k_resolve2(EngDev E, const double* __re
       }
       if (j + 1 < n) {
         const ChainHdr h1 = h_ahead;
-        if (j + 2 < n) h_ahead = H[j + 2];
+        if (j + 2 < n) h_ahead = H[gix(j + 2)];
         fetch(nxt_st, j + 1, h1);
       }
       // store item j into its slot
@@ -318,7 +341,18 @@ __global__ void __launch_bounds__(64, 1) k_resolve2(EngDev E, const double* __re
   long long F = C->F, Falloc = C->F_alloc, freen = C->free_n, Galloc = C->G_alloc;
   long long Aalloc = C->A_alloc, nidx = C->next_index, totw = C->total_w, maxdepth = C->max_depth;
   long long c_lv = 0, c_dir = 0, c_dem = 0, c_slow = 0, c_it = 0, c_demf = 0, c_tch = 0;
-  const long long G0 = Galloc;
+  long long G0 = Galloc, opened = 0;
+  if constexpr (PAR) { G0 = par->Galloc0; totw = 0; maxdepth = 0; freen = 0; }
+  // a fresh child group (coreset.py:369-371); lane-uniform
+  auto new_group = [&]() -> int {
+    if constexpr (PAR) {
+      unsigned long long t = 0;
+      if (lane == 0) t = atomicAdd(&par->g_ticket, 1ULL);
+      return (int)(par->Galloc0 + (long long)__shfl_sync(PCY_FULL, t, 0));
+    } else {
+      return (int)Galloc++;
+    }
+  };
   int status = ST_DONE, err = 0; long long stop = n, remaining = 0;
 
   for (int s2 = lane; s2 < PCY_MOD_SLOTS; s2 += 32) S.mkey[s2] = -1;
@@ -394,11 +428,22 @@ __global__ void __launch_bounds__(64, 1) k_resolve2(EngDev E, const double* __re
     };
     // _open (coreset.py:329-335, :374-377) into group g at level L; returns true when full (rebuild)
     auto do_open = [&](int g, int L) -> bool {
-        const bool full = F >= m;
+        const bool full = !PAR && F >= m;   // k_plan: F0 + window <= m
         const long long wopen = full ? 1LL : rem;
-        long long slot;
-        if (freen > 0) { slot = free_top; --freen; free_top = freen > 0 ? E.free_ids[freen - 1] : -1; }
-        else slot = Falloc++;
+        long long slot, nid = nidx;
+        if constexpr (PAR) {
+          // the t-th open of the window pops the free stack, then bumps F_alloc;
+          // creation index = window position (same order as one-at-a-time)
+          unsigned long long t = 0;
+          if (lane == 0) t = atomicAdd(&par->open_ticket, 1ULL);
+          const long long tt = (long long)__shfl_sync(PCY_FULL, t, 0);
+          slot = tt < par->freen0 ? (long long)E.free_ids[par->freen0 - 1 - tt] : par->Falloc0 + (tt - par->freen0);
+          nid = par->nidx0 + gix(i);
+          ++opened;
+        } else {
+          if (freen > 0) { slot = free_top; --freen; free_top = freen > 0 ? E.free_ids[freen - 1] : -1; }
+          else slot = Falloc++;
+        }
         const int t = nnew++;
         const double fw = (double)wopen;
         double* rr = tref + (long long)t * lds;
@@ -420,7 +465,7 @@ __global__ void __launch_bounds__(64, 1) k_resolve2(EngDev E, const double* __re
           S.tq[t] = rmul(fw, xs); S.tsn[t] = rmul((double)(wopen * wopen), xs); S.trn[t] = xs;
           if (had) { S.tnext[S.gtail[gs]] = t; S.gtail[gs] = t; }
           else { S.gkey[gs] = g; S.ghead[gs] = t; S.gtail[gs] = t; gbits[g >> 5] |= 1u << (g & 31); }
-          E.idx[slot] = nidx; E.alive[slot] = 1; E.child[slot] = -1;
+          E.idx[slot] = nid; E.alive[slot] = 1; E.child[slot] = -1;
         }
         ++nidx; ++F;
         if (L + 1 > maxdepth) maxdepth = L + 1;
@@ -467,7 +512,7 @@ __global__ void __launch_bounds__(64, 1) k_resolve2(EngDev E, const double* __re
           if (g < 0) {
             // the snapshot parent had no child group: create it (coreset.py:369-371)
             const ChainLvl& pp = S.rb[cur][pl - 1];
-            g = (int)Galloc++;
+            g = new_group();
             if (lane == 0) { E.g_count[g] = 0; E.g_cap[g] = 0; E.g_base[g] = 0; E.child[pp.j] = g; }
             map_put(S, mbits, pp.j, pp.w, pp.q, pp.sn, g, lane, &mcount);
           }
@@ -592,7 +637,7 @@ __global__ void __launch_bounds__(64, 1) k_resolve2(EngDev E, const double* __re
       if (bt >= 0) {
         c = S.tchild[bt];
         if (c < 0) {
-          c = (int)Galloc++;
+          c = new_group();
           if (lane == 0) { S.tchild[bt] = c; E.g_count[c] = 0; E.g_cap[c] = 0; E.g_base[c] = 0; }
           __syncwarp();
         }
@@ -602,7 +647,7 @@ __global__ void __launch_bounds__(64, 1) k_resolve2(EngDev E, const double* __re
         if (tnow && ms < 0) ms = map_find(S, bj);
         c = tnow ? S.mchild[ms] : (li >= 0 ? S.rb[cur][li].child : E.child[bj]);
         if (c < 0) {
-          c = (int)Galloc++;
+          c = new_group();
           if (lane == 0) { E.g_count[c] = 0; E.g_cap[c] = 0; E.g_base[c] = 0; E.child[bj] = c; }
           if (tnow) { if (lane == 0) S.mchild[ms] = c; __syncwarp(); }
           else { ms = map_put(S, mbits, bj, nn, qv, snv, c, lane, &mcount); ++c_tch; }   // untouched: current stats
@@ -653,8 +698,16 @@ __global__ void __launch_bounds__(64, 1) k_resolve2(EngDev E, const double* __re
     if (cnt + total > cap) {
       ncap = cap ? 2 * cap : PCY_GROUP_MIN_CAP;
       while (ncap < cnt + total) ncap *= 2;
-      if (Aalloc + ncap > E.AC) { arena_ok = false; break; }
-      nb = (int)Aalloc; Aalloc += ncap;
+      if constexpr (PAR) {
+        unsigned long long at = 0;
+        if (lane == 0) at = atomicAdd(&par->a_ticket, (unsigned long long)ncap);
+        const long long a0 = par->Aalloc0 + (long long)__shfl_sync(PCY_FULL, at, 0);
+        if (a0 + ncap > E.AC) { arena_ok = false; break; }
+        nb = (int)a0;
+      } else {
+        if (Aalloc + ncap > E.AC) { arena_ok = false; break; }
+        nb = (int)Aalloc; Aalloc += ncap;
+      }
       for (int p = lane; p < cnt; p += 32) E.arena[nb + p] = E.arena[base + p];
     }
     if (lane == 0) {
@@ -672,6 +725,38 @@ __global__ void __launch_bounds__(64, 1) k_resolve2(EngDev E, const double* __re
     status = ST_ARENA;
   }
   __syncwarp();
+  if constexpr (PAR) {
+    // deltas of this subtree, then the last CTA publishes the window
+    if (lane == 0) {
+      using ull = unsigned long long;
+      if (status != ST_DONE) atomicExch(&par->arena_fail, status == ST_ARENA ? ST_ARENA : ST_PAR_BROKEN);
+      atomicAdd((ull*)&C->F, (ull)opened);
+      atomicAdd((ull*)&C->total_w, (ull)totw);
+      atomicMax(&C->max_depth, maxdepth);
+      atomicAdd((ull*)&C->cnt_levels, (ull)c_lv); atomicAdd((ull*)&C->cnt_direct, (ull)c_dir);
+      atomicAdd((ull*)&C->cnt_demand, (ull)c_dem); atomicAdd((ull*)&C->cnt_slow, (ull)c_slow);
+      atomicAdd((ull*)&C->cnt_items, (ull)c_it); atomicAdd((ull*)&C->cnt_dem_fast, (ull)c_demf);
+      atomicAdd((ull*)&C->cnt_touch_child, (ull)c_tch);
+      __threadfence();
+      const ull ticket = atomicAdd(&par->done, 1ULL);
+      if (ticket == (ull)par->P - 1) {
+        __threadfence();
+        const long long opens = (long long)*(volatile ull*)&par->open_ticket;
+        const long long fr = par->freen0;
+        C->free_n = opens < fr ? fr - opens : 0;
+        C->F_alloc = par->Falloc0 + (opens > fr ? opens - fr : 0);
+        C->G_alloc = par->Galloc0 + (long long)*(volatile ull*)&par->g_ticket;
+        C->A_alloc = par->Aalloc0 + (long long)*(volatile ull*)&par->a_ticket;
+        C->next_index = par->nidx0 + par->n_win;
+        const int fail = *(volatile int*)&par->arena_fail;
+        C->status = fail ? fail : (par->n_win < par->n_total ? ST_FULL : ST_DONE);
+        C->err = 0; C->stop = par->n_win; C->remaining = 0;
+        __threadfence();
+      }
+    }
+    return;
+  }
+  if (par && status == ST_DONE && n < par->n_total) { status = ST_FULL; stop = n; }   // k_plan's sequential stretch
   if (lane == 0) {
     C->F = F; C->F_alloc = Falloc; C->free_n = freen; C->G_alloc = Galloc;
     C->A_alloc = Aalloc; C->next_index = nidx; C->total_w = totw; C->max_depth = maxdepth;
@@ -679,4 +764,166 @@ __global__ void __launch_bounds__(64, 1) k_resolve2(EngDev E, const double* __re
     C->cnt_levels += c_lv; C->cnt_direct += c_dir; C->cnt_demand += c_dem; C->cnt_slow += c_slow;
     C->cnt_items += c_it; C->cnt_dem_fast += c_demf; C->cnt_touch_child += c_tch;
   }
+}
+
+// ------------------------------------------------------------- K3 planner
+// k_plan (one CTA, thread per item of the K1 block) chooses how the block's
+// next stretch is resolved and writes the ParCtl the two resolve launches read.
+//   window c = the longest prefix with no root open (K1's level-0 decision is
+//     exact until the root group changes: coreset.py:325-335 at group =
+//     self._roots), no invalid row, at most m - F0 items (every item opens at
+//     most one feature without a rebuild, so F < m before each of them,
+//     coreset.py:330-332) and at most cap items per resolve CTA (its
+//     new-node table and touched-node map cannot fill);
+//   roots get CTAs in order of first appearance (mod PCY_PAR_MAXCTA) and each
+//     CTA's list keeps stream order.
+// A window shorter than theta (roots being opened, budget nearly spent, a
+// resumed weighted item) goes to the sequential kernel instead: through the
+// last root open / invalid row among the next 64 items, or the whole block
+// when the budget is close (the rebuild happens there).
+constexpr int PLAN_HASH = 2048;
+__global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const double* __restrict__ XS,
+                                                           const long long* __restrict__ W,
+                                                           const int* __restrict__ BAD, long long n,
+                                                           long long first_rem, int cap_items, int theta,
+                                                           const ChainHdr* __restrict__ H,
+                                                           const ChainLvl* __restrict__ R, ParCtl* __restrict__ par,
+                                                           unsigned* __restrict__ act_bits, int nwords) {
+  __shared__ int hkey[PLAN_HASH], hfirst[PLAN_HASH], hticket[PLAN_HASH];
+  __shared__ int ccnt[PCY_PAR_MAXITEMS / 32][PCY_PAR_MAXCTA];
+  __shared__ int ctot[PCY_PAR_MAXCTA];
+  __shared__ int wsum[32];
+  __shared__ int s_c, s_last, s_heavy, s_cut, s_P;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const EngCtl* C = E.ctl;
+  const long long F0 = C->F;
+  const double T = C->T;
+  const int nn = (int)(n < PCY_PAR_MAXITEMS ? n : PCY_PAR_MAXITEMS);
+  long long room = E.m - F0;
+  if (room < 0) room = 0;
+  for (int h = tid; h < PLAN_HASH; h += blockDim.x) { hkey[h] = -1; hfirst[h] = 0x7fffffff; }
+  for (int q = tid; q < (PCY_PAR_MAXITEMS / 32) * PCY_PAR_MAXCTA; q += blockDim.x) (&ccnt[0][0])[q] = 0;
+  if (tid == 0) {
+    s_c = (int)(room < nn ? room : nn);
+    if (first_rem >= 0) s_c = 0;
+    s_last = -1; s_heavy = 0; s_cut = 0x7fffffff;
+  }
+  __syncthreads();
+  // pass 1: stoppers (root open / invalid) and heavy items
+  int root = -1;
+  if (tid < nn) {
+    const ChainHdr h = H[tid];
+    bool stopper = (BAD && BAD[tid]) || h.len == 0;
+    if (!stopper) {
+      const ChainLvl& r0 = R[(long long)tid * PCY_FMAXL];
+      stopper = r0.j < 0 || radd(r0.part, XS[tid]) > T;
+      root = r0.j;
+    }
+    if (stopper) {
+      atomicMin(&s_c, tid);
+      if (tid < 64) atomicMax(&s_last, tid);
+    }
+    if (W && W[tid] > 1) s_heavy = 1;
+  }
+  __syncthreads();
+  const int c0 = s_c;
+  if (c0 < theta) {
+    if (tid == 0) {
+      par->mode = 1; par->P = 0; par->n_total = n;
+      long long ns = s_last >= 0 ? s_last + 1 : n;
+      if (first_rem >= 0 || room < theta) ns = n;   // resume / rebuild ahead: sequential block
+      if (ns > n) ns = n;
+      par->n_win = ns;
+    }
+    return;
+  }
+  // pass 2: partition keys.  An item's key is the first node on its K1 path at
+  // which some item of the window is predicted to act (absorb there, or open
+  // in its child group).  Nodes above the key see no absorbs and their child
+  // groups no opens, so by induction over stream order every item follows K1
+  // down to its key, and items with different keys touch disjoint subtrees.
+  // With a weighted item in the window the keys stay at the roots (K1 does
+  // not follow partial takes).
+  const bool act = tid < c0;
+  if (!s_heavy) {
+    for (int q = tid; q < nwords; q += blockDim.x) act_bits[q] = 0u;
+    __syncthreads();
+    if (act) {
+      const ChainHdr h = H[tid];
+      const ChainLvl* rec = R + (long long)tid * PCY_FMAXL;
+      const int pl = h.pred < h.len ? h.pred : h.len - 1;
+      int an = -1;
+      if (h.trunc) an = rec[h.len - 1].j;
+      else if (rec[pl].take > 0) an = rec[pl].j;
+      else if (pl >= 1) an = rec[pl - 1].j;
+      if (an >= 0) atomicOr(&act_bits[an >> 5], 1u << (an & 31));
+    }
+    __syncthreads();
+    if (act) {
+      const ChainHdr h = H[tid];
+      const ChainLvl* rec = R + (long long)tid * PCY_FMAXL;
+      for (int l = 0; l < h.len; ++l) {
+        const int j = rec[l].j;
+        if (j < 0) break;
+        root = j;
+        if ((act_bits[j >> 5] >> (j & 31)) & 1u) break;
+      }
+    }
+  }
+  int hs = -1;
+  if (act) {
+    hs = (int)(((unsigned)root * 2654435761u) >> 21) & (PLAN_HASH - 1);
+    for (;;) {
+      const int prev = atomicCAS(&hkey[hs], -1, root);
+      if (prev == -1 || prev == root) break;
+      hs = (hs + 1) & (PLAN_HASH - 1);
+    }
+    atomicMin(&hfirst[hs], tid);
+  }
+  __syncthreads();
+  const int isfirst = act && hfirst[hs] == tid;
+  // exclusive scan of isfirst in item order
+  const unsigned bal = __ballot_sync(PCY_FULL, isfirst);
+  if (lane == 0) wsum[wid] = __popc(bal);
+  __syncthreads();
+  if (tid == 0) {
+    int t = 0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) { const int v = wsum[q]; wsum[q] = t; t += v; }
+  }
+  __syncthreads();
+  if (isfirst) hticket[hs] = wsum[wid] + __popc(bal & ((1u << lane) - 1u));
+  __syncthreads();
+  const int cta = act ? hticket[hs] % PCY_PAR_MAXCTA : -1 - lane;
+  // rank of each item within its CTA (stream order): per-warp chunk counts
+  const unsigned grp = __match_any_sync(PCY_FULL, cta);
+  const int rin = __popc(grp & ((1u << lane) - 1u));
+  if (act && rin == 0) ccnt[wid][cta] = __popc(grp);
+  __syncthreads();
+  for (int q = tid; q < PCY_PAR_MAXCTA; q += blockDim.x) {
+    int run = 0;
+    for (int w2 = 0; w2 < PCY_PAR_MAXITEMS / 32; ++w2) { const int v = ccnt[w2][q]; ccnt[w2][q] = run; run += v; }
+    ctot[q] = 0;
+  }
+  __syncthreads();
+  const int cap = s_heavy ? (PCY_MOD_SLOTS / 2) / (PCY_FMAXL + 2) : cap_items;
+  const int rank = act ? ccnt[wid][cta] + rin : 0;
+  if (act && rank >= cap) atomicMin(&s_cut, tid);
+  __syncthreads();
+  const int c = c0 < s_cut ? c0 : s_cut;
+  if (tid < c) atomicMax(&ctot[cta], rank + 1);
+  __syncthreads();
+  if (tid == 0) {
+    int P = 0, run = 0;
+    for (int q = 0; q < PCY_PAR_MAXCTA; ++q) if (ctot[q] > 0) P = q + 1;
+    for (int q = 0; q < P; ++q) { par->off[q] = run; const int v = ctot[q]; ctot[q] = run; run += v; }
+    par->off[P] = run;
+    s_P = P;
+    par->mode = 0; par->P = P; par->n_win = c; par->n_total = n;
+    par->F0 = F0; par->Falloc0 = C->F_alloc; par->freen0 = C->free_n; par->Galloc0 = C->G_alloc;
+    par->Aalloc0 = C->A_alloc; par->nidx0 = C->next_index;
+    par->open_ticket = 0; par->g_ticket = 0; par->a_ticket = 0; par->done = 0; par->opens = 0;
+    par->arena_fail = 0;
+  }
+  __syncthreads();
+  if (tid < c) par->list[ctot[cta] + rank] = tid;
 }

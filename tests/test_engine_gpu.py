@@ -114,3 +114,15 @@ def test_fp32_input_upcast():
     X = (rng.normal(size=(3000, 54)) * np.geomspace(1, 3000, 54)).astype(np.float32)
     g, o = run_pair(X, None, 54, 500)
     assert_same(g, o)
+
+
+@pytest.mark.parametrize("name,rows,m", [("cfg2", 120_000, 10_000), ("cfg4", 150_000, 20_000), ("cfg2", 60_000, 1_000),
+                                         ("cfg1", 20_000, 1_000)])
+def test_workload_streams(name, rows, m):
+    """Long streams of the bench families: these run mostly through the
+    subtree-parallel resolve (k_plan windows), with rebuilds in between."""
+    from paper_1502_04265_b200 import workloads
+    X = workloads.generate_rows(name, 0, rows)
+    d = X.shape[1]
+    g, o = run_pair(X, None, d, m, block=40_000)
+    assert_same(g, o)
