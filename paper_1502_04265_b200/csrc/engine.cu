@@ -1021,16 +1021,20 @@ struct Engine {
       switch (nper) {
         case 1: PCY_CUDA(cudaFuncSetAttribute(k_resolve2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
                 PCY_CUDA(cudaFuncSetAttribute(k_resolve2<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
-                PCY_CUDA(cudaFuncSetAttribute(k_reattach2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem)); break;
+                PCY_CUDA(cudaFuncSetAttribute(k_reattach2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem));
+                PCY_CUDA(cudaFuncSetAttribute(k_reattach2<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem)); break;
         case 2: PCY_CUDA(cudaFuncSetAttribute(k_resolve2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
                 PCY_CUDA(cudaFuncSetAttribute(k_resolve2<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
-                PCY_CUDA(cudaFuncSetAttribute(k_reattach2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem)); break;
+                PCY_CUDA(cudaFuncSetAttribute(k_reattach2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem));
+                PCY_CUDA(cudaFuncSetAttribute(k_reattach2<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem)); break;
         case 4: PCY_CUDA(cudaFuncSetAttribute(k_resolve2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
                 PCY_CUDA(cudaFuncSetAttribute(k_resolve2<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
-                PCY_CUDA(cudaFuncSetAttribute(k_reattach2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem)); break;
+                PCY_CUDA(cudaFuncSetAttribute(k_reattach2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem));
+                PCY_CUDA(cudaFuncSetAttribute(k_reattach2<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem)); break;
         case 8: PCY_CUDA(cudaFuncSetAttribute(k_resolve2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
                 PCY_CUDA(cudaFuncSetAttribute(k_resolve2<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
-                PCY_CUDA(cudaFuncSetAttribute(k_reattach2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem)); break;
+                PCY_CUDA(cudaFuncSetAttribute(k_reattach2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem));
+                PCY_CUDA(cudaFuncSetAttribute(k_reattach2<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem)); break;
         default: break;
       }
     }
@@ -1151,11 +1155,25 @@ struct Engine {
             grc = pcy_launch_gram(E.r, E.order + off, ld, (int)nb, E.r, E.order + off, ld, (int)nb, d, gram, nb, st);
             if (grc) return grc;
           }
+          ParCtl* pp = nullptr;
+          if (k3par) {
+            k_plan<<<1, PCY_PAR_MAXITEMS, 0, st>>>(E, nullptr, nullptr, nullptr, nb, -1, rea_cap, 16, chh, chr, parctl,
+                                                   parbits, (int)(NC / 32 + 1), E.order + off);
+            pcy_count_launch();
+            pp = parctl;
+            switch (nper) {
+              case 1: k_reattach2<1, true><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp); break;
+              case 2: k_reattach2<2, true><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp); break;
+              case 4: k_reattach2<4, true><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp); break;
+              case 8: k_reattach2<8, true><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp); break;
+            }
+            pcy_count_launch();
+          }
           switch (nper) {
-            case 1: k_reattach2<1><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr); pcy_count_launch(); break;
-            case 2: k_reattach2<2><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr); pcy_count_launch(); break;
-            case 4: k_reattach2<4><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr); pcy_count_launch(); break;
-            case 8: k_reattach2<8><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr); pcy_count_launch(); break;
+            case 1: k_reattach2<1><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp); pcy_count_launch(); break;
+            case 2: k_reattach2<2><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp); pcy_count_launch(); break;
+            case 4: k_reattach2<4><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp); pcy_count_launch(); break;
+            case 8: k_reattach2<8><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp); pcy_count_launch(); break;
             case 100: k_reattach3<true, 2048><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr, nullptr, 0, 0); pcy_count_launch(); break;
             default: k_reattach3<false, 512><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr, gram, nb, 0); pcy_count_launch(); break;
           }
@@ -1165,6 +1183,7 @@ struct Engine {
           if (getenv("PCY_DEBUG_REBUILD"))
             fprintf(stderr, "[pcy] reattach launch: off %lld nb %lld status %d stop %lld F %lld nnew_cap %d\n", off, nb,
                     ctl_h->status, ctl_h->stop, ctl_h->F, nnew_cap);
+          if (ctl_h->status == ST_PAR_BROKEN) { pcy_set_error("subtree-parallel reattach met an excluded stop"); return PCY_ESTATE; }
           if (ctl_h->status == ST_FULL) {
             if (ctl_h->stop == 0) { pcy_set_error("reattach made no progress"); return PCY_ESTATE; }
             off += ctl_h->stop;

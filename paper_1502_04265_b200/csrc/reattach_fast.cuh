@@ -72,13 +72,32 @@ __global__ void k_rchain(EngDev E, const int* __restrict__ order, long long n, C
   if (lane == 0 && nre > 0) atomicAdd((unsigned long long*)&E.ctl->cnt_direct, (unsigned long long)nre);
 }
 
-template <int NPER>
+// PAR = true: CTA b reattaches the nodes of k_plan's subtree list b (the same
+// partition argument as the resolve: merges change only the host, adds only
+// the group of the parent); PAR = false with `par`: k_plan's sequential stretch.
+template <int NPER, bool PAR = false>
 __global__ void __launch_bounds__(32, 1) k_reattach2(EngDev E, const int* __restrict__ order, long long n,
                                                      int nnew_cap, const ChainHdr* __restrict__ H,
-                                                     const ChainLvl* __restrict__ R) {
+                                                     const ChainLvl* __restrict__ R, ParCtl* __restrict__ par = nullptr) {
   extern __shared__ __align__(16) unsigned char smraw[];
   ResolveSmem& S = *reinterpret_cast<ResolveSmem*>(smraw);
   const int lane = threadIdx.x;
+  const int* ilist = nullptr;
+  if constexpr (PAR) {
+    if (par->mode != 0 || (int)blockIdx.x >= par->P) return;
+    const int o0 = par->off[blockIdx.x];
+    ilist = par->list + o0;
+    n = par->off[blockIdx.x + 1] - o0;
+  } else {
+    if (par) {
+      if (par->mode != 1) return;
+      n = par->n_win;
+    }
+  }
+  auto gix = [&](long long j) -> long long {
+    if constexpr (PAR) return (long long)ilist[j];
+    else return j;
+  };
   const int d = E.d, ld = E.ld;
   double* xsm = reinterpret_cast<double*>(smraw + ((sizeof(ResolveSmem) + 15) & ~size_t(15)));
   const int lds = ld | 1;   // odd stride: conflict-free lane-per-row reads
@@ -90,7 +109,17 @@ __global__ void __launch_bounds__(32, 1) k_reattach2(EngDev E, const int* __rest
   EngCtl* C = E.ctl;
   const double T = C->T;
   long long F = C->F, freen = C->free_n, Galloc = C->G_alloc, Aalloc = C->A_alloc;
-  const long long G0 = Galloc;
+  long long G0 = Galloc;
+  if constexpr (PAR) { G0 = par->Galloc0; F = 0; freen = 0; }
+  auto new_group = [&]() -> int {
+    if constexpr (PAR) {
+      unsigned long long t = 0;
+      if (lane == 0) t = atomicAdd(&par->g_ticket, 1ULL);
+      return (int)(par->Galloc0 + (long long)__shfl_sync(PCY_FULL, t, 0));
+    } else {
+      return (int)Galloc++;
+    }
+  };
   int status = ST_DONE; long long stop = n;
 
   for (int s2 = lane; s2 < PCY_MOD_SLOTS; s2 += 32) S.mkey[s2] = -1;
@@ -102,17 +131,17 @@ __global__ void __launch_bounds__(32, 1) k_reattach2(EngDev E, const int* __rest
 
   // ---- prologue: item 0
   double xr[NPER], su[NPER], pr[NPER];
-  int u_c = n > 0 ? order[0] : 0;
-  int u_n = n > 1 ? order[1] : 0;
-  ChainHdr hc = n > 0 ? H[0] : ChainHdr{0, 0, -1, 0};
-  ChainHdr hn = n > 1 ? H[1] : ChainHdr{0, 0, -1, 0};
+  int u_c = n > 0 ? order[gix(0)] : 0;
+  int u_n = n > 1 ? order[gix(1)] : 0;
+  ChainHdr hc = n > 0 ? H[gix(0)] : ChainHdr{0, 0, -1, 0};
+  ChainHdr hn = n > 1 ? H[gix(1)] : ChainHdr{0, 0, -1, 0};
   long long wu_c = 0; double qu_c = 0.0, snu_c = 0.0, rsq_c = 0.0;
   if (n > 0) {
     load_row<NPER>(xr, E.r + (long long)u_c * ld, d, lane);
     load_row<NPER>(su, E.s + (long long)u_c * ld, d, lane);
     if (hc.predj >= 0) load_row<NPER>(pr, E.s + (long long)hc.predj * ld, d, lane);
     wu_c = E.w[u_c]; qu_c = E.q[u_c]; snu_c = E.sn[u_c]; rsq_c = E.rn[u_c];
-    const uint4* src = reinterpret_cast<const uint4*>(R);
+    const uint4* src = reinterpret_cast<const uint4*>(R + gix(0) * PCY_FMAXL);
     uint4* dst = reinterpret_cast<uint4*>(&S.rb[0][0]);
     for (int c = lane; c < REC_CHUNKS; c += 32) dst[c] = src[c];
   }
@@ -133,11 +162,11 @@ __global__ void __launch_bounds__(32, 1) k_reattach2(EngDev E, const int* __rest
       load_row<NPER>(xn, E.r + (long long)u_n * ld, d, lane);
       load_row<NPER>(sun, E.s + (long long)u_n * ld, d, lane);
       wu_n = E.w[u_n]; qu_n = E.q[u_n]; snu_n = E.sn[u_n]; rsq_n = E.rn[u_n];
-      const uint4* src = reinterpret_cast<const uint4*>(R + (i + 1) * PCY_FMAXL);
+      const uint4* src = reinterpret_cast<const uint4*>(R + gix(i + 1) * PCY_FMAXL);
 #pragma unroll
       for (int q = 0; q < (REC_CHUNKS + 31) / 32; ++q) { const int c = lane + 32 * q; if (c < REC_CHUNKS) rpf[q] = src[c]; }
       if (hn.predj >= 0) load_row<NPER>(pn, E.s + (long long)hn.predj * ld, d, lane);
-      if (i + 2 < n) { h2 = H[i + 2]; u2 = order[i + 2]; }
+      if (i + 2 < n) { h2 = H[gix(i + 2)]; u2 = order[gix(i + 2)]; }
     }
     // ---- item i: node u
     const int u = u_c;
@@ -248,8 +277,16 @@ __global__ void __launch_bounds__(32, 1) k_reattach2(EngDev E, const int* __rest
           ms = map_put(S, mbits, bj, mw, mq, mnorm, child_now, lane);
           if (lane == 0) { E.w[bj] = mw; E.q[bj] = mq; E.sn[bj] = mnorm; }
         }
-        if (lane == 0) { E.alive[u] = 0; E.free_ids[freen] = u; }
-        ++freen;
+        if constexpr (PAR) {
+          if (lane == 0) {
+            E.alive[u] = 0;
+            const unsigned long long t = atomicAdd(&par->open_ticket, 1ULL);   // free-stack pushes
+            E.free_ids[par->freen0 + (long long)t] = u;
+          }
+        } else {
+          if (lane == 0) { E.alive[u] = 0; E.free_ids[freen] = u; }
+          ++freen;
+        }
         lastmod = bj;
         __syncwarp();
         break;
@@ -258,7 +295,7 @@ __global__ void __launch_bounds__(32, 1) k_reattach2(EngDev E, const int* __rest
       if (bt >= 0) {
         c = S.tchild[bt];
         if (c < 0) {
-          c = (int)Galloc++;
+          c = new_group();
           if (lane == 0) { S.tchild[bt] = c; E.g_count[c] = 0; E.g_cap[c] = 0; E.g_base[c] = 0; }
           __syncwarp();
         }
@@ -268,7 +305,7 @@ __global__ void __launch_bounds__(32, 1) k_reattach2(EngDev E, const int* __rest
         if (tnow && ms < 0) ms = map_find(S, bj);
         c = tnow ? S.mchild[ms] : (li >= 0 ? S.rb[cur][li].child : E.child[bj]);
         if (c < 0) {
-          c = (int)Galloc++;
+          c = new_group();
           if (lane == 0) { E.g_count[c] = 0; E.g_cap[c] = 0; E.g_base[c] = 0; E.child[bj] = c; }
           if (tnow) { if (lane == 0) S.mchild[ms] = c; __syncwarp(); }
           else ms = map_put(S, mbits, bj, hw, hq, hsn, c, lane);
@@ -327,8 +364,16 @@ __global__ void __launch_bounds__(32, 1) k_reattach2(EngDev E, const int* __rest
     if (cnt + total > cap) {
       ncap = cap ? 2 * cap : PCY_GROUP_MIN_CAP;
       while (ncap < cnt + total) ncap *= 2;
-      if (Aalloc + ncap > E.AC) { arena_ok = false; break; }
-      nb = (int)Aalloc; Aalloc += ncap;
+      if constexpr (PAR) {
+        unsigned long long at = 0;
+        if (lane == 0) at = atomicAdd(&par->a_ticket, (unsigned long long)ncap);
+        const long long a0 = par->Aalloc0 + (long long)__shfl_sync(PCY_FULL, at, 0);
+        if (a0 + ncap > E.AC) { arena_ok = false; break; }
+        nb = (int)a0;
+      } else {
+        if (Aalloc + ncap > E.AC) { arena_ok = false; break; }
+        nb = (int)Aalloc; Aalloc += ncap;
+      }
       for (int p = lane; p < cnt; p += 32) E.arena[nb + p] = E.arena[base + p];
     }
     if (lane == 0) {
@@ -344,6 +389,27 @@ __global__ void __launch_bounds__(32, 1) k_reattach2(EngDev E, const int* __rest
     }
   } else status = ST_ARENA;
   __syncwarp();
+  if constexpr (PAR) {
+    if (lane == 0) {
+      using ull = unsigned long long;
+      if (status != ST_DONE) atomicExch(&par->arena_fail, status == ST_ARENA ? ST_ARENA : ST_PAR_BROKEN);
+      atomicAdd((ull*)&C->F, (ull)F);
+      __threadfence();
+      const ull ticket = atomicAdd(&par->done, 1ULL);
+      if (ticket == (ull)par->P - 1) {
+        __threadfence();
+        C->free_n = par->freen0 + (long long)*(volatile ull*)&par->open_ticket;
+        C->G_alloc = par->Galloc0 + (long long)*(volatile ull*)&par->g_ticket;
+        C->A_alloc = par->Aalloc0 + (long long)*(volatile ull*)&par->a_ticket;
+        const int fail = *(volatile int*)&par->arena_fail;
+        C->status = fail ? fail : (par->n_win < par->n_total ? ST_FULL : ST_DONE);
+        C->stop = par->n_win;
+        __threadfence();
+      }
+    }
+    return;
+  }
+  if (par && status == ST_DONE && n < par->n_total) { status = ST_FULL; stop = n; }   // k_plan's sequential stretch
   if (lane == 0) {
     C->F = F; C->free_n = freen; C->G_alloc = Galloc; C->A_alloc = Aalloc;
     C->status = status; C->stop = stop;

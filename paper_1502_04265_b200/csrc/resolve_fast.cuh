@@ -777,6 +777,8 @@ __global__ void __launch_bounds__(64, 1) k_resolve2(EngDev E, const double* __re
 //     new-node table and touched-node map cannot fill);
 //   roots get CTAs in order of first appearance (mod PCY_PAR_MAXCTA) and each
 //     CTA's list keeps stream order.
+// With `order` (rebuild reattach, coreset.py:395-421) the items are the
+// collected nodes in rebuild order: a merge is the absorb, a group add the open.
 // A window shorter than theta (roots being opened, budget nearly spent, a
 // resumed weighted item) goes to the sequential kernel instead: through the
 // last root open / invalid row among the next 64 items, or the whole block
@@ -788,7 +790,8 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
                                                            long long first_rem, int cap_items, int theta,
                                                            const ChainHdr* __restrict__ H,
                                                            const ChainLvl* __restrict__ R, ParCtl* __restrict__ par,
-                                                           unsigned* __restrict__ act_bits, int nwords) {
+                                                           unsigned* __restrict__ act_bits, int nwords,
+                                                           const int* __restrict__ order = nullptr) {
   __shared__ int hkey[PLAN_HASH], hfirst[PLAN_HASH], hticket[PLAN_HASH];
   __shared__ int ccnt[PCY_PAR_MAXITEMS / 32][PCY_PAR_MAXCTA];
   __shared__ int ctot[PCY_PAR_MAXCTA];
@@ -801,6 +804,7 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
   const int nn = (int)(n < PCY_PAR_MAXITEMS ? n : PCY_PAR_MAXITEMS);
   long long room = E.m - F0;
   if (room < 0) room = 0;
+  if (order) room = n;   // rebuild reattach: merges and adds never exceed the budget
   for (int h = tid; h < PLAN_HASH; h += blockDim.x) { hkey[h] = -1; hfirst[h] = 0x7fffffff; }
   for (int q = tid; q < (PCY_PAR_MAXITEMS / 32) * PCY_PAR_MAXCTA; q += blockDim.x) (&ccnt[0][0])[q] = 0;
   if (tid == 0) {
@@ -816,7 +820,8 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
     bool stopper = (BAD && BAD[tid]) || h.len == 0;
     if (!stopper) {
       const ChainLvl& r0 = R[(long long)tid * PCY_FMAXL];
-      stopper = r0.j < 0 || radd(r0.part, XS[tid]) > T;
+      const double xs = order ? E.rn[order[tid]] : XS[tid];
+      stopper = r0.j < 0 || radd(r0.part, xs) > T;
       root = r0.j;
     }
     if (stopper) {
