@@ -891,7 +891,8 @@ struct Engine {
   float *tc_ahi = nullptr, *tc_alo = nullptr, *tc_bhi = nullptr, *tc_blo = nullptr, *tc_dots = nullptr;
   double *tc_rnc = nullptr, *tc_xn2 = nullptr, *tc_c = nullptr;
   unsigned* parbits = nullptr;   // k_plan scratch: nodes some window item acts on
-  ParCtl* parctl = nullptr;   // k_plan output (subtree-parallel resolve)
+  ParCtl* parctl = nullptr;
+  int* planbuf = nullptr;       // k_plan scratch: window openers   // k_plan output (subtree-parallel resolve)
   long long kbatch = 1024;     // K1 rows per launch when k3par
   bool k3par = false;         // subtree-parallel resolve enabled (nper 1..8)
   int nper = 0;          // resolve kernel: 1..8 register rows, 100/101 shared-memory rows, 0 generic
@@ -983,7 +984,7 @@ struct Engine {
     A_(E.order, NC); A_(E.lvl, NC); A_(E.stk_g, NC + 1); A_(E.stk_p, NC + 1);
     A_(E.minbits, 2);
     A_(aggw, m + 2); A_(mp_nrm, sample_cap + 1);
-    A_(parctl, 1); A_(parbits, NC / 32 + 2);
+    A_(parctl, 1); A_(parbits, NC / 32 + 2); A_(planbuf, 2 * PCY_PAR_MAXITEMS);
 #undef A_
     for (auto& e : ev) PCY_CUDA(cudaEventCreate(&e));
     {
@@ -1049,18 +1050,23 @@ struct Engine {
         rea_smem = resolve3_smem_bytes<2048>(ld, nnew_cap, true, NC, GC, 2);
         PCY_CUDA(cudaFuncSetAttribute(k_resolve3<true, 2048>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
         PCY_CUDA(cudaFuncSetAttribute(k_reattach3<true, 2048>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem));
+        PCY_CUDA(cudaFuncSetAttribute(k_resolve3<true, 2048, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
+        PCY_CUDA(cudaFuncSetAttribute(k_reattach3<true, 2048, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem));
       } else if (resolve3_smem_bytes<512>(ld, 0, false, NC, GC, 2) <= maxsm) {
         nper = 101; nnew_cap = PCY_NNEW_MAX;
         res_smem = resolve3_smem_bytes<512>(ld, 0, false, NC, GC, 0);
         rea_smem = resolve3_smem_bytes<512>(ld, 0, false, NC, GC, 2);
         PCY_CUDA(cudaFuncSetAttribute(k_resolve3<false, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
         PCY_CUDA(cudaFuncSetAttribute(k_reattach3<false, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem));
+        PCY_CUDA(cudaFuncSetAttribute(k_resolve3<false, 512, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
+        PCY_CUDA(cudaFuncSetAttribute(k_reattach3<false, 512, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem));
       }
     }
     if (getenv("PCY_GENERIC_RESOLVE")) nper = 0;
+    PCY_CUDA(cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLAN_SMEM));
     {
       const char* pe = getenv("PCY_K3PAR");
-      k3par = nper >= 1 && nper <= 8 && (!pe || atoi(pe) != 0);
+      k3par = nper >= 1 && (!pe || atoi(pe) != 0);
     }
     if (!(ctl_h = ctl_pool_get())) { pcy_set_error("cudaHostAlloc of the control mirror failed"); return PCY_ENOMEM; }
     memset(ctl_h, 0, sizeof(EngCtl));
@@ -1157,8 +1163,13 @@ struct Engine {
           }
           ParCtl* pp = nullptr;
           if (k3par) {
-            k_plan<<<1, PCY_PAR_MAXITEMS, 0, st>>>(E, nullptr, nullptr, nullptr, nb, -1, rea_cap, 16, chh, chr, parctl,
-                                                   parbits, (int)(NC / 32 + 1), E.order + off);
+            if (nper != 101) {   // opener rows against the batch (k_plan's conflict test)
+              grc = pcy_launch_gram(E.r, E.order + off, ld, (int)nb, E.r, E.order + off, ld, (int)nb, d, gram, nb, st);
+              if (grc) return grc;
+            }
+            k_plan<<<1, PCY_PAR_MAXITEMS, PLAN_SMEM, st>>>(E, nullptr, nullptr, nullptr, nb, -1, nper <= 8 ? rea_cap : nnew_cap,
+                                                   16, chh, chr, parctl, parbits, (int)(NC / 32 + 1), E.order + off,
+                                                   gram, nb, planbuf);
             pcy_count_launch();
             pp = parctl;
             switch (nper) {
@@ -1166,6 +1177,8 @@ struct Engine {
               case 2: k_reattach2<2, true><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp); break;
               case 4: k_reattach2<4, true><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp); break;
               case 8: k_reattach2<8, true><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp); break;
+              case 100: k_reattach3<true, 2048, true><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr, nullptr, 0, 0, pp); break;
+              default: k_reattach3<false, 512, true><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr, gram, nb, 0, pp); break;
             }
             pcy_count_launch();
           }
@@ -1174,8 +1187,8 @@ struct Engine {
             case 2: k_reattach2<2><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp); pcy_count_launch(); break;
             case 4: k_reattach2<4><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp); pcy_count_launch(); break;
             case 8: k_reattach2<8><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp); pcy_count_launch(); break;
-            case 100: k_reattach3<true, 2048><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr, nullptr, 0, 0); pcy_count_launch(); break;
-            default: k_reattach3<false, 512><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr, gram, nb, 0); pcy_count_launch(); break;
+            case 100: k_reattach3<true, 2048><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr, nullptr, 0, 0, pp); pcy_count_launch(); break;
+            default: k_reattach3<false, 512><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr, gram, nb, 0, pp); pcy_count_launch(); break;
           }
           PCY_LAUNCH_CHECK();
           rc = sync_ctl(st); if (rc) return rc;
@@ -1261,8 +1274,12 @@ struct Engine {
         if (k3par) {
           // k_plan picks a subtree-parallel window or a sequential stretch; the
           // launch that was not chosen returns at once
-          k_plan<<<1, PCY_PAR_MAXITEMS, 0, rs>>>(E, XSs, Ws, Bs, kn, first_rem, nnew_cap, 16, chh, chr, parctl,
-                                                 parbits, (int)(NC / 32 + 1));
+          if (nper != 101) {   // opener rows against the batch (k_plan's conflict test)
+            const int grc = pcy_launch_gram(Xs, nullptr, ld, (int)kn, Xs, nullptr, ld, (int)kn, d, gram, kn, rs);
+            if (grc) return grc;
+          }
+          k_plan<<<1, PCY_PAR_MAXITEMS, PLAN_SMEM, rs>>>(E, XSs, Ws, Bs, kn, first_rem, nnew_cap, 16, chh, chr, parctl,
+                                                 parbits, (int)(NC / 32 + 1), nullptr, gram, kn, planbuf);
           pcy_count_launch();
           pp = parctl;
           switch (nper) {
@@ -1270,6 +1287,8 @@ struct Engine {
             case 2: k_resolve2<2, true><<<PCY_PAR_MAXCTA, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, pp); break;
             case 4: k_resolve2<4, true><<<PCY_PAR_MAXCTA, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, pp); break;
             case 8: k_resolve2<8, true><<<PCY_PAR_MAXCTA, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, pp); break;
+            case 100: k_resolve3<true, 2048, true><<<PCY_PAR_MAXCTA, 32, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, nullptr, 0, 0, pp); break;
+            case 101: k_resolve3<false, 512, true><<<PCY_PAR_MAXCTA, 32, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, gram, kn, 0, pp); break;
           }
           pcy_count_launch();
         }
@@ -1278,8 +1297,8 @@ struct Engine {
           case 2: k_resolve2<2><<<1, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, pp); pcy_count_launch(); break;
           case 4: k_resolve2<4><<<1, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, pp); pcy_count_launch(); break;
           case 8: k_resolve2<8><<<1, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, pp); pcy_count_launch(); break;
-          case 100: k_resolve3<true, 2048><<<1, 32, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, nullptr, 0, 0); pcy_count_launch(); break;
-          case 101: k_resolve3<false, 512><<<1, 32, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, gram, kn, 0); pcy_count_launch(); break;
+          case 100: k_resolve3<true, 2048><<<1, 32, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, nullptr, 0, 0, pp); pcy_count_launch(); break;
+          case 101: k_resolve3<false, 512><<<1, 32, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, gram, kn, 0, pp); pcy_count_launch(); break;
           default:
             k_resolve<<<1, 32, sizeof(double) * ld, rs>>>(E, Xs, XSs, Ws, Bs, kn, 0, first_rem, countw); pcy_count_launch();
         }

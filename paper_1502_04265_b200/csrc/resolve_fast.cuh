@@ -767,23 +767,75 @@ __global__ void __launch_bounds__(64, 1) k_resolve2(EngDev E, const double* __re
 }
 
 // ------------------------------------------------------------- K3 planner
-// k_plan (one CTA, thread per item of the K1 block) chooses how the block's
+// k_plan (one CTA, thread per item of the K1 batch) chooses how the batch's
 // next stretch is resolved and writes the ParCtl the two resolve launches read.
-//   window c = the longest prefix with no root open (K1's level-0 decision is
-//     exact until the root group changes: coreset.py:325-335 at group =
-//     self._roots), no invalid row, at most m - F0 items (every item opens at
-//     most one feature without a rebuild, so F < m before each of them,
-//     coreset.py:330-332) and at most cap items per resolve CTA (its
-//     new-node table and touched-node map cannot fill);
-//   roots get CTAs in order of first appearance (mod PCY_PAR_MAXCTA) and each
-//     CTA's list keeps stream order.
+//
+// Window: the longest prefix with no invalid row, at most m - F0 items (every
+// item opens at most one feature without a rebuild, so F < m before each of
+// them, coreset.py:330-332) and no conflicting root open (below).
+//
+// Domains.  From K1's record every item has a predicted action: absorb at node
+// a (coreset.py:336-368, take > 0) or open into the child group of a parent P
+// (coreset.py:329-335; P = ROOT for group 0).  Items are grouped into domains
+// that own disjoint state:
+//   SUB(v)  node v, its statistics and everything below it;
+//   OPEN(P) the membership of P's child group (its opens, in stream order).
+// v is a domain root when some window item absorbs at v, or when an earlier
+// window open into the group containing v would be preferred by an item whose
+// K1 winner there is v (the opener's row against the item, from the batch
+// Gram, below the recorded part plus a rounding margin): then the opener and
+// that item may interact, and OPEN(P) is united with SUB(v).  An item joins
+// the first domain on its path (an opener that meets none joins OPEN(P)), and
+// every further domain below it on its path, or its open group, is united
+// with that one (nested state).  Above its domain an item sees no absorbs and
+// no preferred new members, so by induction over stream order it follows K1
+// there; the united domains partition the window's writes, so one CTA per
+// domain set resolves the window exactly.  A conflicting root open ends the
+// window.  With a weighted item in the window the domains stay at the roots
+// and every root open ends the window (K1 does not follow partial takes).
+//
+// Domain sets get CTAs in order of first appearance (mod PCY_PAR_MAXCTA); each
+// CTA list keeps stream order and holds at most cap items (its tables cannot
+// fill).  A window shorter than theta goes to the sequential kernel.
 // With `order` (rebuild reattach, coreset.py:395-421) the items are the
 // collected nodes in rebuild order: a merge is the absorb, a group add the open.
-// A window shorter than theta (roots being opened, budget nearly spent, a
-// resumed weighted item) goes to the sequential kernel instead: through the
-// last root open / invalid row among the next 64 items, or the whole block
-// when the budget is close (the rebuild happens there).
-constexpr int PLAN_HASH = 2048;
+constexpr int PLAN_HASH = 4096;
+constexpr int PLAN_ROOT = -2;
+constexpr size_t PLAN_SMEM = sizeof(int) * 4 * PLAN_HASH;
+__device__ __forceinline__ int ph_slot(int key) { return (int)(((unsigned)key * 2654435761u) >> 20) & (PLAN_HASH - 1); }
+__device__ __forceinline__ int ph_insert(int* hkey, int key) {
+  int s = ph_slot(key);
+  for (;;) {
+    const int prev = atomicCAS(&hkey[s], -1, key);
+    if (prev == -1 || prev == key) return s;
+    s = (s + 1) & (PLAN_HASH - 1);
+  }
+}
+__device__ __forceinline__ int ph_find(const int* hkey, int key) {
+  int s = ph_slot(key);
+  for (;;) {
+    const int k = *(volatile const int*)&hkey[s];
+    if (k == key) return s;
+    if (k == -1) return -1;
+    s = (s + 1) & (PLAN_HASH - 1);
+  }
+}
+__device__ __forceinline__ int uf_find(int* uf, int a) {
+  for (;;) {
+    const int p = *(volatile int*)&uf[a];
+    if (p == a) return a;
+    a = p;
+  }
+}
+__device__ __forceinline__ void uf_union(int* uf, int a, int b) {
+  for (;;) {
+    a = uf_find(uf, a); b = uf_find(uf, b);
+    if (a == b) return;
+    if (a > b) { const int t = a; a = b; b = t; }
+    if (atomicCAS(&uf[b], b, a) == b) return;   // link the larger root under the smaller
+  }
+}
+
 __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const double* __restrict__ XS,
                                                            const long long* __restrict__ W,
                                                            const int* __restrict__ BAD, long long n,
@@ -791,103 +843,141 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
                                                            const ChainHdr* __restrict__ H,
                                                            const ChainLvl* __restrict__ R, ParCtl* __restrict__ par,
                                                            unsigned* __restrict__ act_bits, int nwords,
-                                                           const int* __restrict__ order = nullptr) {
-  __shared__ int hkey[PLAN_HASH], hfirst[PLAN_HASH], hticket[PLAN_HASH];
+                                                           const int* __restrict__ order, const double* __restrict__ gram,
+                                                           long long gld, int* __restrict__ scratch) {
+  extern __shared__ int plan_sm[];
+  int* hkey = plan_sm;                    // domain keys: SUB(v) = v, OPEN(P) = NC + P, OPEN(ROOT) = 2 NC
+  int* uf = plan_sm + PLAN_HASH;          // union-find over hash slots
+  int* ohead = plan_sm + 2 * PLAN_HASH;   // OPEN(P): list of its openers; later: set tickets
+  int* hfirst = plan_sm + 3 * PLAN_HASH;  // first item of each domain set
   __shared__ int ccnt[PCY_PAR_MAXITEMS / 32][PCY_PAR_MAXCTA];
   __shared__ int ctot[PCY_PAR_MAXCTA];
   __shared__ int wsum[32];
-  __shared__ int s_c, s_last, s_heavy, s_cut, s_P;
+  __shared__ int s_c, s_last, s_heavy, s_cut;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const EngCtl* C = E.ctl;
   const long long F0 = C->F;
-  const double T = C->T;
+  const int NC = (int)E.NC;
   const int nn = (int)(n < PCY_PAR_MAXITEMS ? n : PCY_PAR_MAXITEMS);
+  int* onext = scratch;   // opener list links, by item
   long long room = E.m - F0;
   if (room < 0) room = 0;
   if (order) room = n;   // rebuild reattach: merges and adds never exceed the budget
-  for (int h = tid; h < PLAN_HASH; h += blockDim.x) { hkey[h] = -1; hfirst[h] = 0x7fffffff; }
+  for (int h = tid; h < PLAN_HASH; h += blockDim.x) { hkey[h] = -1; uf[h] = h; ohead[h] = -1; hfirst[h] = 0x7fffffff; }
   for (int q = tid; q < (PCY_PAR_MAXITEMS / 32) * PCY_PAR_MAXCTA; q += blockDim.x) (&ccnt[0][0])[q] = 0;
+  for (int q = tid; q < nwords; q += blockDim.x) act_bits[q] = 0u;
   if (tid == 0) {
     s_c = (int)(room < nn ? room : nn);
     if (first_rem >= 0) s_c = 0;
     s_last = -1; s_heavy = 0; s_cut = 0x7fffffff;
   }
   __syncthreads();
-  // pass 1: stoppers (root open / invalid) and heavy items
-  int root = -1;
+  // pass 1: invalid rows, weighted items, predicted actions
+  ChainHdr h = ChainHdr{0, 0, -1, 0};
+  const ChainLvl* rec = R + (long long)tid * PCY_FMAXL;
+  double xs = 0.0;
+  int pl = -1, alev = -1, absorb = -1, target = -1;   // absorb at `absorb` (level alev), or open under `target`
+  bool opener = false;
   if (tid < nn) {
-    const ChainHdr h = H[tid];
-    bool stopper = (BAD && BAD[tid]) || h.len == 0;
-    if (!stopper) {
-      const ChainLvl& r0 = R[(long long)tid * PCY_FMAXL];
-      const double xs = order ? E.rn[order[tid]] : XS[tid];
-      stopper = r0.j < 0 || radd(r0.part, xs) > T;
-      root = r0.j;
-    }
-    if (stopper) {
+    h = H[tid];
+    const bool invalid = (BAD && BAD[tid]) || h.len == 0;
+    if (!invalid) {
+      xs = order ? E.rn[order[tid]] : XS[tid];
+      pl = h.pred < h.len ? h.pred : h.len - 1;
+      if (h.trunc) { alev = h.len - 1; absorb = rec[alev].j; }   // acts somewhere below the record
+      else if (rec[pl].take > 0) { alev = pl; absorb = rec[pl].j; }
+      else { opener = true; target = pl >= 1 ? rec[pl - 1].j : PLAN_ROOT; }
+    } else {
       atomicMin(&s_c, tid);
       if (tid < 64) atomicMax(&s_last, tid);
     }
     if (W && W[tid] > 1) s_heavy = 1;
   }
   __syncthreads();
+  const bool heavy = s_heavy != 0;
+  auto open_key = [&](int P) { return NC + (P == PLAN_ROOT ? NC : P); };
+  if (heavy) {
+    if (tid < nn && opener && target == PLAN_ROOT) {   // root opens end the window
+      atomicMin(&s_c, tid);
+      if (tid < 64) atomicMax(&s_last, tid);
+    }
+  } else {
+    // opener lists per open group
+    if (tid < s_c && opener) {
+      const int so = ph_insert(hkey, open_key(target));
+      onext[tid] = atomicExch(&ohead[so], tid);
+    }
+    __syncthreads();
+    // conflicts: an earlier opener y of a group x visits (at a level <= its
+    // action) whose row x would prefer to its K1 winner there
+    if (tid < s_c) {
+      const int lmax = opener ? pl : alev;
+      for (int l = 0; l <= lmax; ++l) {
+        const int P = l == 0 ? PLAN_ROOT : rec[l - 1].j;
+        if (opener && P == target) break;   // x opens there itself: same domain
+        const int so = ph_find(hkey, open_key(P));
+        if (so < 0) continue;
+        const double prec = rec[l].part;
+        for (int y = ohead[so]; y >= 0; y = onext[y]) {
+          if (y >= tid) continue;
+          const double xsy = order ? E.rn[order[y]] : XS[y];
+          const double pnew = radd(xsy, rmul(gram[(long long)tid * gld + y], -2.0));
+          if (pnew < prec + 1e-10 * (xs + xsy) + 1e-300) {
+            if (P == PLAN_ROOT) {   // the window ends before this root open
+              atomicMin(&s_c, y);
+              if (y < 64) atomicMax(&s_last, y);
+            } else {
+              const int v = rec[l].j;
+              atomicOr(&act_bits[v >> 5], 1u << (v & 31));
+              uf_union(uf, so, ph_insert(hkey, v));
+            }
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
   const int c0 = s_c;
   if (c0 < theta) {
     if (tid == 0) {
       par->mode = 1; par->P = 0; par->n_total = n;
-      long long ns = s_last >= 0 ? s_last + 1 : n;
-      if (first_rem >= 0 || room < theta) ns = n;   // resume / rebuild ahead: sequential block
+      long long ns = n;
+      // through the stoppers among the next 64 items (invalid rows, root opens)
+      if (first_rem < 0 && room >= theta && c0 < nn) ns = (s_last > c0 ? s_last : c0) + 1;
       if (ns > n) ns = n;
       par->n_win = ns;
     }
     return;
   }
-  // pass 2: partition keys.  An item's key is the first node on its K1 path at
-  // which some item of the window is predicted to act (absorb there, or open
-  // in its child group).  Nodes above the key see no absorbs and their child
-  // groups no opens, so by induction over stream order every item follows K1
-  // down to its key, and items with different keys touch disjoint subtrees.
-  // With a weighted item in the window the keys stay at the roots (K1 does
-  // not follow partial takes).
   const bool act = tid < c0;
-  if (!s_heavy) {
-    for (int q = tid; q < nwords; q += blockDim.x) act_bits[q] = 0u;
-    __syncthreads();
-    if (act) {
-      const ChainHdr h = H[tid];
-      const ChainLvl* rec = R + (long long)tid * PCY_FMAXL;
-      const int pl = h.pred < h.len ? h.pred : h.len - 1;
-      int an = -1;
-      if (h.trunc) an = rec[h.len - 1].j;
-      else if (rec[pl].take > 0) an = rec[pl].j;
-      else if (pl >= 1) an = rec[pl - 1].j;
-      if (an >= 0) atomicOr(&act_bits[an >> 5], 1u << (an & 31));
-    }
-    __syncthreads();
-    if (act) {
-      const ChainHdr h = H[tid];
-      const ChainLvl* rec = R + (long long)tid * PCY_FMAXL;
-      for (int l = 0; l < h.len; ++l) {
-        const int j = rec[l].j;
-        if (j < 0) break;
-        root = j;
-        if ((act_bits[j >> 5] >> (j & 31)) & 1u) break;
+  if (act && absorb >= 0) atomicOr(&act_bits[absorb >> 5], 1u << (absorb & 31));
+  __syncthreads();
+  // the item's first domain, united with every further domain on its path
+  int k1 = -1;
+  if (act) {
+    if (heavy) k1 = ph_insert(hkey, rec[0].j >= 0 ? rec[0].j : 2 * NC + 1);
+    else {
+      const int lmax = opener ? pl : alev;
+      for (int l = 0; l <= lmax; ++l) {
+        int ks = -1;
+        if (opener && l == pl) ks = ph_insert(hkey, open_key(target));
+        else {
+          const int j = rec[l].j;
+          if (j >= 0 && ((act_bits[j >> 5] >> (j & 31)) & 1u)) ks = ph_insert(hkey, j);
+        }
+        if (ks >= 0) {
+          if (k1 < 0) k1 = ks;
+          else uf_union(uf, k1, ks);
+        }
       }
     }
   }
-  int hs = -1;
-  if (act) {
-    hs = (int)(((unsigned)root * 2654435761u) >> 21) & (PLAN_HASH - 1);
-    for (;;) {
-      const int prev = atomicCAS(&hkey[hs], -1, root);
-      if (prev == -1 || prev == root) break;
-      hs = (hs + 1) & (PLAN_HASH - 1);
-    }
-    atomicMin(&hfirst[hs], tid);
-  }
   __syncthreads();
-  const int isfirst = act && hfirst[hs] == tid;
-  // exclusive scan of isfirst in item order
+  const int root = act ? uf_find(uf, k1) : -1;
+  if (act) atomicMin(&hfirst[root], tid);
+  __syncthreads();
+  const int isfirst = act && hfirst[root] == tid;
+  // exclusive scan of isfirst in item order: set tickets
   const unsigned bal = __ballot_sync(PCY_FULL, isfirst);
   if (lane == 0) wsum[wid] = __popc(bal);
   __syncthreads();
@@ -896,9 +986,9 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
     for (int q = 0; q < (int)(blockDim.x >> 5); ++q) { const int v = wsum[q]; wsum[q] = t; t += v; }
   }
   __syncthreads();
-  if (isfirst) hticket[hs] = wsum[wid] + __popc(bal & ((1u << lane) - 1u));
+  if (isfirst) ohead[root] = wsum[wid] + __popc(bal & ((1u << lane) - 1u));
   __syncthreads();
-  const int cta = act ? hticket[hs] % PCY_PAR_MAXCTA : -1 - lane;
+  const int cta = act ? ohead[root] % PCY_PAR_MAXCTA : -1 - lane;
   // rank of each item within its CTA (stream order): per-warp chunk counts
   const unsigned grp = __match_any_sync(PCY_FULL, cta);
   const int rin = __popc(grp & ((1u << lane) - 1u));
@@ -910,7 +1000,7 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
     ctot[q] = 0;
   }
   __syncthreads();
-  const int cap = s_heavy ? (PCY_MOD_SLOTS / 2) / (PCY_FMAXL + 2) : cap_items;
+  const int cap = heavy ? (PCY_MOD_SLOTS / 2) / (PCY_FMAXL + 2) : cap_items;
   const int rank = act ? ccnt[wid][cta] + rin : 0;
   if (act && rank >= cap) atomicMin(&s_cut, tid);
   __syncthreads();
@@ -922,7 +1012,6 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
     for (int q = 0; q < PCY_PAR_MAXCTA; ++q) if (ctot[q] > 0) P = q + 1;
     for (int q = 0; q < P; ++q) { par->off[q] = run; const int v = ctot[q]; ctot[q] = run; run += v; }
     par->off[P] = run;
-    s_P = P;
     par->mode = 0; par->P = P; par->n_win = c; par->n_total = n;
     par->F0 = F0; par->Falloc0 = C->F_alloc; par->freen0 = C->free_n; par->Galloc0 = C->G_alloc;
     par->Aalloc0 = C->A_alloc; par->nidx0 = C->next_index;

@@ -248,7 +248,8 @@ __device__ __forceinline__ void scan_new(const EngDev& E, const ResolveSmemT<MS>
 
 // memberships of the launch's table entries -> arena, position order (both kernels)
 template <int MS>
-__device__ bool table_cleanup(const EngDev& E, ResolveSmemT<MS>& S, int nnew, long long& Aalloc, int lane) {
+__device__ bool table_cleanup(const EngDev& E, ResolveSmemT<MS>& S, int nnew, long long& Aalloc, int lane,
+                              ParCtl* par = nullptr) {
   for (int t = lane; t < nnew; t += 32) {
     const int g = S.tgrp[t];
     int k = 0, f = t;
@@ -268,8 +269,16 @@ __device__ bool table_cleanup(const EngDev& E, ResolveSmemT<MS>& S, int nnew, lo
     if (cnt + total > cap) {
       ncap = cap ? 2 * cap : PCY_GROUP_MIN_CAP;
       while (ncap < cnt + total) ncap *= 2;
-      if (Aalloc + ncap > E.AC) { ok = false; break; }
-      nb = (int)Aalloc; Aalloc += ncap;
+      if (par) {   // subtree-parallel launch: arena extents by ticket
+        unsigned long long at = 0;
+        if (lane == 0) at = atomicAdd(&par->a_ticket, (unsigned long long)ncap);
+        const long long a0 = par->Aalloc0 + (long long)__shfl_sync(PCY_FULL, at, 0);
+        if (a0 + ncap > E.AC) { ok = false; break; }
+        nb = (int)a0;
+      } else {
+        if (Aalloc + ncap > E.AC) { ok = false; break; }
+        nb = (int)Aalloc; Aalloc += ncap;
+      }
       for (int p = lane; p < cnt; p += 32) E.arena[nb + p] = E.arena[base + p];
     }
     if (lane == 0) {
@@ -289,16 +298,34 @@ __device__ bool table_cleanup(const EngDev& E, ResolveSmemT<MS>& S, int nnew, lo
 
 constexpr int REC3_CHUNKS = PCY_FMAXL * (int)sizeof(ChainLvl) / 16;
 
-template <bool TROWS, int MS>
+// PAR / par: as k_resolve2 (k_plan windows, one CTA per subtree list).
+template <bool TROWS, int MS, bool PAR = false>
 __global__ void __launch_bounds__(32, 1) k_resolve3(EngDev E, const double* __restrict__ X,
                                                     const double* __restrict__ XS, const long long* __restrict__ W,
                                                     const int* __restrict__ BAD, long long n, long long first_rem,
                                                     int countw, int nnew_cap, const ChainHdr* __restrict__ H,
                                                     const ChainLvl* __restrict__ R, const double* __restrict__ gram,
-                                                    long long gld, long long goff) {
+                                                    long long gld, long long goff, ParCtl* __restrict__ par = nullptr) {
   extern __shared__ __align__(16) unsigned char smraw[];
   ResolveSmemT<MS>& S = *reinterpret_cast<ResolveSmemT<MS>*>(smraw);
   const int lane = threadIdx.x;
+  const int* ilist = nullptr;
+  if constexpr (PAR) {
+    if (par->mode != 0 || (int)blockIdx.x >= par->P) return;
+    const int o0 = par->off[blockIdx.x];
+    ilist = par->list + o0;
+    n = par->off[blockIdx.x + 1] - o0;
+    first_rem = -1;
+  } else {
+    if (par) {
+      if (par->mode != 1) return;
+      n = par->n_win;
+    }
+  }
+  auto gix = [&](long long j) -> long long {
+    if constexpr (PAR) return (long long)ilist[j];
+    else return j;
+  };
   const int d = E.d, ld = E.ld;
   double* xb = reinterpret_cast<double*>(smraw + ((sizeof(ResolveSmemT<MS>) + 15) & ~size_t(15)));
   double* pb = xb + 2 * (long long)ld;
@@ -315,7 +342,17 @@ __global__ void __launch_bounds__(32, 1) k_resolve3(EngDev E, const double* __re
   long long F = C->F, Falloc = C->F_alloc, freen = C->free_n, Galloc = C->G_alloc;
   long long Aalloc = C->A_alloc, nidx = C->next_index, totw = C->total_w, maxdepth = C->max_depth;
   long long c_lv = 0, c_dir = 0, c_dem = 0, c_slow = 0, c_it = 0;
-  const long long G0 = Galloc;
+  long long G0 = Galloc, opened = 0;
+  if constexpr (PAR) { G0 = par->Galloc0; totw = 0; maxdepth = 0; freen = 0; }
+  auto new_group = [&]() -> int {
+    if constexpr (PAR) {
+      unsigned long long t = 0;
+      if (lane == 0) t = atomicAdd(&par->g_ticket, 1ULL);
+      return (int)(par->Galloc0 + (long long)__shfl_sync(PCY_FULL, t, 0));
+    } else {
+      return (int)Galloc++;
+    }
+  };
   int status = ST_DONE, err = 0; long long stop = n, remaining = 0;
 
   for (int s2 = lane; s2 < MS; s2 += 32) S.mkey[s2] = -1;
@@ -326,18 +363,18 @@ __global__ void __launch_bounds__(32, 1) k_resolve3(EngDev E, const double* __re
   int nnew = 0;
   int free_top = freen > 0 ? E.free_ids[freen - 1] : -1;
 
-  int bad_c = (n > 0 && BAD) ? BAD[0] : 0;
-  long long w_c = (n > 0 && W) ? W[0] : 1LL;
-  double xs_c = n > 0 ? XS[0] : 0.0;
-  ChainHdr hc = n > 0 ? H[0] : ChainHdr{0, 0, -1, 0};
-  ChainHdr hn = n > 1 ? H[1] : ChainHdr{0, 0, -1, 0};
+  int bad_c = (n > 0 && BAD) ? BAD[gix(0)] : 0;
+  long long w_c = (n > 0 && W) ? W[gix(0)] : 1LL;
+  double xs_c = n > 0 ? XS[gix(0)] : 0.0;
+  ChainHdr hc = n > 0 ? H[gix(0)] : ChainHdr{0, 0, -1, 0};
+  ChainHdr hn = n > 1 ? H[gix(1)] : ChainHdr{0, 0, -1, 0};
   rows_bar_init(S.rbar, 2, lane);
   unsigned rph[2] = {0u, 0u};
   const bool bulk = ld >= 2048;
   if (n > 0) {
-    rows_fetch(bulk, &S.rbar[0], lane, ld, xb, X, pb, hc.predj >= 0 ? E.s + (long long)hc.predj * ld : nullptr,
-               nullptr, nullptr);
-    const uint4* src = reinterpret_cast<const uint4*>(R);
+    rows_fetch(bulk, &S.rbar[0], lane, ld, xb, X + gix(0) * ld, pb,
+               hc.predj >= 0 ? E.s + (long long)hc.predj * ld : nullptr, nullptr, nullptr);
+    const uint4* src = reinterpret_cast<const uint4*>(R + gix(0) * PCY_FMAXL);
     uint4* dst = reinterpret_cast<uint4*>(&S.rb[0][0]);
     for (int c = lane; c < REC3_CHUNKS; c += 32) cp_async16(dst + c, src + c);
     cp_async_commit();
@@ -358,17 +395,18 @@ __global__ void __launch_bounds__(32, 1) k_resolve3(EngDev E, const double* __re
     ChainHdr h2 = ChainHdr{0, 0, -1, 0};
     int bad_n = 0; long long w_n = 1; double xs_n = 0.0;
     if (has_next) {
-      bad_n = BAD ? BAD[i + 1] : 0;
-      w_n = W ? W[i + 1] : 1LL;
-      xs_n = XS[i + 1];
-      rows_fetch(bulk, &S.rbar[cur ^ 1], lane, ld, xb + (long long)(cur ^ 1) * ld, X + (i + 1) * ld,
+      const long long gn = gix(i + 1);
+      bad_n = BAD ? BAD[gn] : 0;
+      w_n = W ? W[gn] : 1LL;
+      xs_n = XS[gn];
+      rows_fetch(bulk, &S.rbar[cur ^ 1], lane, ld, xb + (long long)(cur ^ 1) * ld, X + gn * ld,
                  pb + (long long)(cur ^ 1) * ld, hn.predj >= 0 ? E.s + (long long)hn.predj * ld : nullptr,
                  nullptr, nullptr);
-      const uint4* src = reinterpret_cast<const uint4*>(R + (i + 1) * PCY_FMAXL);
+      const uint4* src = reinterpret_cast<const uint4*>(R + gn * PCY_FMAXL);
       uint4* dst = reinterpret_cast<uint4*>(&S.rb[cur ^ 1][0]);
       for (int c = lane; c < REC3_CHUNKS; c += 32) cp_async16(dst + c, src + c);
       cp_async_commit();
-      if (i + 2 < n) h2 = H[i + 2];
+      if (i + 2 < n) h2 = H[gix(i + 2)];
     }
     // ---- item i
     const bool resume = (i == 0 && first_rem >= 0);
@@ -391,11 +429,20 @@ __global__ void __launch_bounds__(32, 1) k_resolve3(EngDev E, const double* __re
       ++c_dem;
     };
     auto do_open = [&](int gg, int LL) -> bool {
-      const bool full = F >= m;
+      const bool full = !PAR && F >= m;   // k_plan: F0 + window <= m
       const long long wopen = full ? 1LL : rem;
-      long long slot;
-      if (freen > 0) { slot = free_top; --freen; free_top = freen > 0 ? E.free_ids[freen - 1] : -1; }
-      else slot = Falloc++;
+      long long slot, nid = nidx;
+      if constexpr (PAR) {
+        unsigned long long tk = 0;
+        if (lane == 0) tk = atomicAdd(&par->open_ticket, 1ULL);
+        const long long tt = (long long)__shfl_sync(PCY_FULL, tk, 0);
+        slot = tt < par->freen0 ? (long long)E.free_ids[par->freen0 - 1 - tt] : par->Falloc0 + (tt - par->freen0);
+        nid = par->nidx0 + gix(i);
+        ++opened;
+      } else {
+        if (freen > 0) { slot = free_top; --freen; free_top = freen > 0 ? E.free_ids[freen - 1] : -1; }
+        else slot = Falloc++;
+      }
       const int t = nnew++;
       const double fw = (double)wopen;
       double* rr = TROWS ? tref + (long long)t * lds : E.r + slot * ld;
@@ -403,10 +450,10 @@ __global__ void __launch_bounds__(32, 1) k_resolve3(EngDev E, const double* __re
       for (int e = lane; e < ld; e += 32) { rr[e] = xsm[e]; sr[e] = rmul(fw, xsm[e]); }
       gchain_append<MS>(S, gbits, gg, t, lane);
       if (lane == 0) {
-        S.titem[t] = (int)(goff + i);
+        S.titem[t] = (int)(goff + gix(i));
         S.tid[t] = (int)slot; S.tgrp[t] = gg; S.tchild[t] = -1; S.tw[t] = wopen;
         S.tq[t] = rmul(fw, xs); S.tsn[t] = rmul((double)(wopen * wopen), xs); S.trn[t] = xs;
-        E.idx[slot] = nidx; E.alive[slot] = 1; E.child[slot] = -1;
+        E.idx[slot] = nid; E.alive[slot] = 1; E.child[slot] = -1;
       }
       ++nidx; ++F;
       if (LL + 1 > maxdepth) maxdepth = LL + 1;
@@ -450,7 +497,7 @@ __global__ void __launch_bounds__(32, 1) k_resolve3(EngDev E, const double* __re
           int gg = rp.g;
           if (gg < 0) {
             const ChainLvl& pp = S.rb[cur][pl - 1];
-            gg = (int)Galloc++;
+            gg = new_group();
             if (lane == 0) { E.g_count[gg] = 0; E.g_cap[gg] = 0; E.g_base[gg] = 0; E.child[pp.j] = gg; }
             map3_put<MS>(S, mbits, pp.j, pp.w, pp.q, pp.sn, gg, lane);
           }
@@ -479,7 +526,7 @@ __global__ void __launch_bounds__(32, 1) k_resolve3(EngDev E, const double* __re
         }
       }
       int bt = -1;
-      scan_new<TROWS, MS>(E, S, gbits, tref, lds, xsm, g, nnew, lane, bp, bj, bt, gram, gld, goff + i);
+      scan_new<TROWS, MS>(E, S, gbits, tref, lds, xsm, g, nnew, lane, bp, bj, bt, gram, gld, goff + gix(i));
       if (bj < 0 || radd(bp, xs) > radius) {
         if (do_open(g, L)) { status = ST_REBUILD; stop = i; remaining = rem; }
         break;
@@ -537,7 +584,7 @@ __global__ void __launch_bounds__(32, 1) k_resolve3(EngDev E, const double* __re
       if (bt >= 0) {
         c = S.tchild[bt];
         if (c < 0) {
-          c = (int)Galloc++;
+          c = new_group();
           if (lane == 0) { S.tchild[bt] = c; E.g_count[c] = 0; E.g_cap[c] = 0; E.g_base[c] = 0; }
           __syncwarp();
         }
@@ -547,7 +594,7 @@ __global__ void __launch_bounds__(32, 1) k_resolve3(EngDev E, const double* __re
         if (tnow && ms < 0) ms = map3_find<MS>(S, bj);
         c = tnow ? S.mchild[ms] : (li >= 0 ? S.rb[cur][li].child : E.child[bj]);
         if (c < 0) {
-          c = (int)Galloc++;
+          c = new_group();
           if (lane == 0) { E.g_count[c] = 0; E.g_cap[c] = 0; E.g_base[c] = 0; E.child[bj] = c; }
           if (tnow) { if (lane == 0) S.mchild[ms] = c; __syncwarp(); }
           else ms = map3_put<MS>(S, mbits, bj, nn, qv, snv, c, lane);
@@ -601,7 +648,37 @@ __global__ void __launch_bounds__(32, 1) k_resolve3(EngDev E, const double* __re
     E.child[node] = S.tchild[t];
   }
   __syncwarp();
-  if (!table_cleanup<MS>(E, S, nnew, Aalloc, lane)) status = ST_ARENA;
+  if (!table_cleanup<MS>(E, S, nnew, Aalloc, lane, PAR ? par : nullptr)) status = ST_ARENA;
+  if constexpr (PAR) {
+    if (lane == 0) {
+      using ull = unsigned long long;
+      if (status != ST_DONE) atomicExch(&par->arena_fail, status == ST_ARENA ? ST_ARENA : ST_PAR_BROKEN);
+      atomicAdd((ull*)&C->F, (ull)opened);
+      atomicAdd((ull*)&C->total_w, (ull)totw);
+      atomicMax(&C->max_depth, maxdepth);
+      atomicAdd((ull*)&C->cnt_levels, (ull)c_lv); atomicAdd((ull*)&C->cnt_direct, (ull)c_dir);
+      atomicAdd((ull*)&C->cnt_demand, (ull)c_dem); atomicAdd((ull*)&C->cnt_slow, (ull)c_slow);
+      atomicAdd((ull*)&C->cnt_items, (ull)c_it);
+      __threadfence();
+      const ull ticket = atomicAdd(&par->done, 1ULL);
+      if (ticket == (ull)par->P - 1) {
+        __threadfence();
+        const long long opens = (long long)*(volatile ull*)&par->open_ticket;
+        const long long fr = par->freen0;
+        C->free_n = opens < fr ? fr - opens : 0;
+        C->F_alloc = par->Falloc0 + (opens > fr ? opens - fr : 0);
+        C->G_alloc = par->Galloc0 + (long long)*(volatile ull*)&par->g_ticket;
+        C->A_alloc = par->Aalloc0 + (long long)*(volatile ull*)&par->a_ticket;
+        C->next_index = par->nidx0 + par->n_win;
+        const int fail = *(volatile int*)&par->arena_fail;
+        C->status = fail ? fail : (par->n_win < par->n_total ? ST_FULL : ST_DONE);
+        C->err = 0; C->stop = par->n_win; C->remaining = 0;
+        __threadfence();
+      }
+    }
+    return;
+  }
+  if (par && status == ST_DONE && n < par->n_total) { status = ST_FULL; stop = n; }   // k_plan's sequential stretch
   if (lane == 0) {
     C->F = F; C->F_alloc = Falloc; C->free_n = freen; C->G_alloc = Galloc;
     C->A_alloc = Aalloc; C->next_index = nidx; C->total_w = totw; C->max_depth = maxdepth;
@@ -612,14 +689,30 @@ __global__ void __launch_bounds__(32, 1) k_resolve3(EngDev E, const double* __re
 }
 
 // ------------------------------------------------------------- reattach
-template <bool TROWS, int MS>
+template <bool TROWS, int MS, bool PAR = false>
 __global__ void __launch_bounds__(32, 1) k_reattach3(EngDev E, const int* __restrict__ order, long long n,
                                                      int nnew_cap, const ChainHdr* __restrict__ H,
                                                      const ChainLvl* __restrict__ R, const double* __restrict__ gram,
-                                                     long long gld, long long goff) {
+                                                     long long gld, long long goff, ParCtl* __restrict__ par = nullptr) {
   extern __shared__ __align__(16) unsigned char smraw[];
   ResolveSmemT<MS>& S = *reinterpret_cast<ResolveSmemT<MS>*>(smraw);
   const int lane = threadIdx.x;
+  const int* ilist = nullptr;
+  if constexpr (PAR) {
+    if (par->mode != 0 || (int)blockIdx.x >= par->P) return;
+    const int o0 = par->off[blockIdx.x];
+    ilist = par->list + o0;
+    n = par->off[blockIdx.x + 1] - o0;
+  } else {
+    if (par) {
+      if (par->mode != 1) return;
+      n = par->n_win;
+    }
+  }
+  auto gix = [&](long long j) -> long long {
+    if constexpr (PAR) return (long long)ilist[j];
+    else return j;
+  };
   const int d = E.d, ld = E.ld;
   double* xb = reinterpret_cast<double*>(smraw + ((sizeof(ResolveSmemT<MS>) + 15) & ~size_t(15)));
   double* pb = xb + 2 * (long long)ld;     // [2][ld]: predicted host rows
@@ -633,7 +726,17 @@ __global__ void __launch_bounds__(32, 1) k_reattach3(EngDev E, const int* __rest
   EngCtl* C = E.ctl;
   const double T = C->T;
   long long F = C->F, freen = C->free_n, Galloc = C->G_alloc, Aalloc = C->A_alloc;
-  const long long G0 = Galloc;
+  long long G0 = Galloc;
+  if constexpr (PAR) { G0 = par->Galloc0; F = 0; freen = 0; }
+  auto new_group = [&]() -> int {
+    if constexpr (PAR) {
+      unsigned long long t = 0;
+      if (lane == 0) t = atomicAdd(&par->g_ticket, 1ULL);
+      return (int)(par->Galloc0 + (long long)__shfl_sync(PCY_FULL, t, 0));
+    } else {
+      return (int)Galloc++;
+    }
+  };
   int status = ST_DONE; long long stop = n;
 
   for (int s2 = lane; s2 < MS; s2 += 32) S.mkey[s2] = -1;
@@ -643,10 +746,10 @@ __global__ void __launch_bounds__(32, 1) k_reattach3(EngDev E, const int* __rest
   if (lane == 0) S.modcount = 0;
   int nnew = 0;
 
-  int u_c = n > 0 ? order[0] : 0;
-  int u_n = n > 1 ? order[1] : 0;
-  ChainHdr hc = n > 0 ? H[0] : ChainHdr{0, 0, -1, 0};
-  ChainHdr hn = n > 1 ? H[1] : ChainHdr{0, 0, -1, 0};
+  int u_c = n > 0 ? order[gix(0)] : 0;
+  int u_n = n > 1 ? order[gix(1)] : 0;
+  ChainHdr hc = n > 0 ? H[gix(0)] : ChainHdr{0, 0, -1, 0};
+  ChainHdr hn = n > 1 ? H[gix(1)] : ChainHdr{0, 0, -1, 0};
   long long wu_c = 0; double qu_c = 0.0, snu_c = 0.0, rsq_c = 0.0;
   rows_bar_init(S.rbar, 2, lane);
   unsigned rph[2] = {0u, 0u};
@@ -655,7 +758,7 @@ __global__ void __launch_bounds__(32, 1) k_reattach3(EngDev E, const int* __rest
     rows_fetch(bulk, &S.rbar[0], lane, ld, xb, E.r + (long long)u_c * ld, sb, E.s + (long long)u_c * ld, pb,
                hc.predj >= 0 ? E.s + (long long)hc.predj * ld : nullptr);
     wu_c = E.w[u_c]; qu_c = E.q[u_c]; snu_c = E.sn[u_c]; rsq_c = E.rn[u_c];
-    const uint4* src = reinterpret_cast<const uint4*>(R);
+    const uint4* src = reinterpret_cast<const uint4*>(R + gix(0) * PCY_FMAXL);
     uint4* dst = reinterpret_cast<uint4*>(&S.rb[0][0]);
     for (int c = lane; c < REC3_CHUNKS; c += 32) cp_async16(dst + c, src + c);
     cp_async_commit();
@@ -679,12 +782,12 @@ __global__ void __launch_bounds__(32, 1) k_reattach3(EngDev E, const int* __rest
       rows_fetch(bulk, &S.rbar[cur ^ 1], lane, ld, xb + (long long)(cur ^ 1) * ld, E.r + (long long)u_n * ld,
                  sb + (long long)(cur ^ 1) * ld, E.s + (long long)u_n * ld, pb + (long long)(cur ^ 1) * ld,
                  hn.predj >= 0 ? E.s + (long long)hn.predj * ld : nullptr);
-      const uint4* src = reinterpret_cast<const uint4*>(R + (i + 1) * PCY_FMAXL);
+      const uint4* src = reinterpret_cast<const uint4*>(R + gix(i + 1) * PCY_FMAXL);
       uint4* dst = reinterpret_cast<uint4*>(&S.rb[cur ^ 1][0]);
       for (int c = lane; c < REC3_CHUNKS; c += 32) cp_async16(dst + c, src + c);
       cp_async_commit();
       wu_n = E.w[u_n]; qu_n = E.q[u_n]; snu_n = E.sn[u_n]; rsq_n = E.rn[u_n];
-      if (i + 2 < n) { h2 = H[i + 2]; u2 = order[i + 2]; }
+      if (i + 2 < n) { h2 = H[gix(i + 2)]; u2 = order[gix(i + 2)]; }
     }
     const int u = u_c;
     const int len = hc.len;
@@ -709,7 +812,7 @@ __global__ void __launch_bounds__(32, 1) k_reattach3(EngDev E, const int* __rest
         }
       }
       int bt = -1;
-      scan_new<TROWS, MS>(E, S, gbits, tref, lds, xsm, g, nnew, lane, bp, bj, bt, gram, gld, goff + i);
+      scan_new<TROWS, MS>(E, S, gbits, tref, lds, xsm, g, nnew, lane, bp, bj, bt, gram, gld, goff + gix(i));
       if (bj < 0 || radd(bp, rsq_c) > radius) {
         // group.add(node): u keeps its statistics (coreset.py:403-406)
         const int t = nnew++;
@@ -719,7 +822,7 @@ __global__ void __launch_bounds__(32, 1) k_reattach3(EngDev E, const int* __rest
         }
         gchain_append<MS>(S, gbits, g, t, lane);
         if (lane == 0) {
-          S.titem[t] = (int)(goff + i);
+          S.titem[t] = (int)(goff + gix(i));
           S.tid[t] = u; S.tgrp[t] = g; S.tchild[t] = -1;
           S.tw[t] = wu_c; S.tq[t] = qu_c; S.tsn[t] = snu_c; S.trn[t] = rsq_c;
         }
@@ -771,8 +874,16 @@ __global__ void __launch_bounds__(32, 1) k_reattach3(EngDev E, const int* __rest
           ms = map3_put<MS>(S, mbits, bj, mw, mq, mnorm, child_now, lane);
           if (lane == 0) { E.w[bj] = mw; E.q[bj] = mq; E.sn[bj] = mnorm; }
         }
-        if (lane == 0) { E.alive[u] = 0; E.free_ids[freen] = u; }
-        ++freen;
+        if constexpr (PAR) {
+          if (lane == 0) {
+            E.alive[u] = 0;
+            const unsigned long long tk = atomicAdd(&par->open_ticket, 1ULL);   // free-stack pushes
+            E.free_ids[par->freen0 + (long long)tk] = u;
+          }
+        } else {
+          if (lane == 0) { E.alive[u] = 0; E.free_ids[freen] = u; }
+          ++freen;
+        }
         lastmod = bj;
         __syncwarp();
         break;
@@ -781,7 +892,7 @@ __global__ void __launch_bounds__(32, 1) k_reattach3(EngDev E, const int* __rest
       if (bt >= 0) {
         c = S.tchild[bt];
         if (c < 0) {
-          c = (int)Galloc++;
+          c = new_group();
           if (lane == 0) { S.tchild[bt] = c; E.g_count[c] = 0; E.g_cap[c] = 0; E.g_base[c] = 0; }
           __syncwarp();
         }
@@ -791,7 +902,7 @@ __global__ void __launch_bounds__(32, 1) k_reattach3(EngDev E, const int* __rest
         if (tnow && ms < 0) ms = map3_find<MS>(S, bj);
         c = tnow ? S.mchild[ms] : (li >= 0 ? S.rb[cur][li].child : E.child[bj]);
         if (c < 0) {
-          c = (int)Galloc++;
+          c = new_group();
           if (lane == 0) { E.g_count[c] = 0; E.g_cap[c] = 0; E.g_base[c] = 0; E.child[bj] = c; }
           if (tnow) { if (lane == 0) S.mchild[ms] = c; __syncwarp(); }
           else ms = map3_put<MS>(S, mbits, bj, hw, hq, hsn, c, lane);
@@ -829,7 +940,28 @@ __global__ void __launch_bounds__(32, 1) k_reattach3(EngDev E, const int* __rest
     E.child[node] = S.tchild[t];
   }
   __syncwarp();
-  if (!table_cleanup<MS>(E, S, nnew, Aalloc, lane)) status = ST_ARENA;
+  if (!table_cleanup<MS>(E, S, nnew, Aalloc, lane, PAR ? par : nullptr)) status = ST_ARENA;
+  if constexpr (PAR) {
+    if (lane == 0) {
+      using ull = unsigned long long;
+      if (status != ST_DONE) atomicExch(&par->arena_fail, status == ST_ARENA ? ST_ARENA : ST_PAR_BROKEN);
+      atomicAdd((ull*)&C->F, (ull)F);
+      __threadfence();
+      const ull ticket = atomicAdd(&par->done, 1ULL);
+      if (ticket == (ull)par->P - 1) {
+        __threadfence();
+        C->free_n = par->freen0 + (long long)*(volatile ull*)&par->open_ticket;
+        C->G_alloc = par->Galloc0 + (long long)*(volatile ull*)&par->g_ticket;
+        C->A_alloc = par->Aalloc0 + (long long)*(volatile ull*)&par->a_ticket;
+        const int fail = *(volatile int*)&par->arena_fail;
+        C->status = fail ? fail : (par->n_win < par->n_total ? ST_FULL : ST_DONE);
+        C->stop = par->n_win;
+        __threadfence();
+      }
+    }
+    return;
+  }
+  if (par && status == ST_DONE && n < par->n_total) { status = ST_FULL; stop = n; }   // k_plan's sequential stretch
   if (lane == 0) {
     C->F = F; C->free_n = freen; C->G_alloc = Galloc; C->A_alloc = Aalloc;
     C->status = status; C->stop = stop;

@@ -50,3 +50,13 @@ def test_forced_smem_variant_small_dim(seed, n, d, m, weighted, monkeypatch):
     W = rng.integers(1, 9, size=n) if weighted else None
     g, o = _pair(X, W, d, m)
     assert_same(g, o)
+
+
+@pytest.mark.parametrize("name,rows,m", [("cfg3", 40_000, 3_000), ("cfg5", 6_000, 1_500)])
+def test_high_dim_workload_streams(name, rows, m):
+    """Bench-family streams at d = 1024 / 4096: long enough for the
+    subtree-parallel resolve and reattach windows (k_plan) between rebuilds."""
+    from paper_1502_04265_b200 import workloads
+    X = workloads.generate_rows(name, 0, rows)
+    g, o = _pair(X, None, X.shape[1], m)
+    assert_same(g, o)
