@@ -179,15 +179,16 @@ __device__ __forceinline__ void scan_parts(const double* __restrict__ prow, int 
 template <class RDot>
 __device__ __forceinline__ void scan_parts_tc(const EngDev& E, long long i, int g, const int* __restrict__ mem,
                                               int cnt, RDot rdot, int lane, double& bp, int& bpos, int& nre) {
-  const long long col = E.fs_gofs[g];
-  const float* __restrict__ dots = E.tc_dots + i * E.tc_ldo + col;
-  const double* __restrict__ rnc = E.tc_rnc + col;
+  // columns are reference slots (k_tc_split_slots): gathered per member
+  const float* __restrict__ dots = E.tc_dots + i * E.tc_ldo;
+  const double* __restrict__ rnc = E.tc_rnc;
   const double xn = sqrt(E.tc_xn2[i]);
   const double tau2 = 2.0 * E.tc_tau * (1.0 + 1e-9);
   double U = INFINITY;
   for (int p = lane; p < cnt; p += 32) {
-    const double rc = rnc[p];
-    U = fmin(U, rc - 2.0 * (double)dots[p] + tau2 * sqrt(rc) * xn + 1e-300);
+    const int jj = mem[p];
+    const double rc = rnc[jj];
+    U = fmin(U, rc - 2.0 * (double)dots[jj] + tau2 * sqrt(rc) * xn + 1e-300);
   }
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) U = fmin(U, __shfl_xor_sync(PCY_FULL, U, o));
@@ -197,8 +198,9 @@ __device__ __forceinline__ void scan_parts_tc(const EngDev& E, long long i, int 
     const int p = c0 + lane;
     bool cand = false;
     if (p < cnt) {
-      const double rc = rnc[p];
-      cand = rc - 2.0 * (double)dots[p] - tau2 * sqrt(rc) * xn <= U;
+      const int jj = mem[p];
+      const double rc = rnc[jj];
+      cand = rc - 2.0 * (double)dots[jj] - tau2 * sqrt(rc) * xn <= U;
     }
     unsigned m = __ballot_sync(PCY_FULL, cand);
     while (m) {
@@ -351,6 +353,194 @@ __global__ void k_boot(EngDev E, long long start, long long n) {
   if (lane == 0) {
     C->npend = npend; C->ndist = ndist; C->total_w = totw;
     C->status = status; C->err = err; C->stop = stop;
+  }
+}
+
+// Parallel bootstrap (same result as k_boot, coreset.py:283-295).  The last
+// pending entry always holds the previous row's key, so row i starts a new
+// pending entry iff it differs from row i-1 (from the last entry for the
+// first row); a row is a new distinct key iff it is not in the table and no
+// earlier row of the block has its bytes.  A prefix scan over the block then
+// places the stop (invalid row, pending buffer full, budget + 1 distinct) and
+// the pending / distinct positions.
+struct BootScratch {
+  int* flags;    // per row: bit0 starts a pending entry, bit1 new distinct key
+  int* spos;     // per row: scratch-table slot
+  int* ppos;     // per row: pending position (rows starting an entry)
+  int* dpos;     // per row: distinct position (new keys)
+  int* skey;     // scratch table: first claiming row (-1 empty)
+  int* sfirst;   // scratch table: lowest row with those bytes
+  long long scap;
+};
+
+__global__ void k_boot_scan_rows(EngDev E, BootScratch B, long long start, long long n) {
+  const int lane = threadIdx.x & 31;
+  const long long i = start + (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= n) return;
+  const int d = E.d, ld = E.ld;
+  const double* x = E.xb + i * ld;
+  const long long npend0 = E.ctl->npend;
+  bool newp;
+  if (i == start) newp = !(npend0 > 0 && rows_equal(E.pend_x + (npend0 - 1) * ld, x, d, lane));
+  else newp = !rows_equal(E.xb + (i - 1) * ld, x, d, lane);
+  // known key?
+  const unsigned long long mask = (unsigned long long)E.hcap - 1ULL;
+  unsigned long long slot = E.hsh[i] & mask;
+  bool found = false;
+  for (;;) {
+    const int k = E.htab[slot];
+    if (k < 0) break;
+    if (rows_equal(E.dist_x + (long long)k * ld, x, d, lane)) { found = true; break; }
+    slot = (slot + 1) & mask;
+  }
+  int sp = -1;
+  if (!found) {
+    // first row of the block with these bytes
+    const unsigned long long smask = (unsigned long long)B.scap - 1ULL;
+    unsigned long long ss = E.hsh[i] & smask;
+    for (;;) {
+      int k = 0;
+      if (lane == 0) k = atomicCAS(&B.skey[ss], -1, (int)(i - start));
+      k = __shfl_sync(PCY_FULL, k, 0);
+      if (k == -1 || rows_equal(E.xb + (start + k) * ld, x, d, lane)) break;
+      ss = (ss + 1) & smask;
+    }
+    sp = (int)ss;
+    if (lane == 0) atomicMin(&B.sfirst[ss], (int)(i - start));
+  }
+  if (lane == 0) { B.flags[i - start] = newp ? 1 : 0; B.spos[i - start] = sp; }
+}
+
+// One CTA: flags -> stop, positions, counters.
+__global__ void __launch_bounds__(1024) k_boot_plan(EngDev E, BootScratch B, long long start, long long n) {
+  __shared__ long long red[2][33];
+  __shared__ long long s_stop;
+  __shared__ int s_status;
+  __shared__ long long s_np, s_nd, s_w;
+  EngCtl* C = E.ctl;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const long long cnt = n - start;
+  if (tid == 0) { s_stop = cnt; s_status = ST_DONE; s_np = C->npend; s_nd = C->ndist; s_w = 0; C->err = 0; }
+  __syncthreads();
+  for (long long c0 = 0; c0 < cnt; c0 += blockDim.x) {
+    const long long r = c0 + tid;
+    const bool in = r < cnt && r < s_stop;
+    int fl = 0;
+    if (in) {
+      fl = B.flags[r];
+      if (B.spos[r] >= 0 && B.sfirst[B.spos[r]] == (int)r) fl |= 2;
+    }
+    const long long np_in = (fl & 1), nd_in = (fl >> 1) & 1;
+    // inclusive scans of (new pending, new distinct) in row order
+    long long a = np_in, b = nd_in;
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long ta = __shfl_up_sync(PCY_FULL, a, o), tb = __shfl_up_sync(PCY_FULL, b, o);
+      if (lane >= o) { a += ta; b += tb; }
+    }
+    if (lane == 31) { red[0][wid] = a; red[1][wid] = b; }
+    __syncthreads();
+    if (wid == 0) {
+      long long wa = lane < (int)(blockDim.x >> 5) ? red[0][lane] : 0, wb = lane < (int)(blockDim.x >> 5) ? red[1][lane] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long ta = __shfl_up_sync(PCY_FULL, wa, o), tb = __shfl_up_sync(PCY_FULL, wb, o);
+        if (lane >= o) { wa += ta; wb += tb; }
+      }
+      red[0][lane] = wa; red[1][lane] = wb;   // inclusive warp totals
+    }
+    __syncthreads();
+    const long long pa = (wid ? red[0][wid - 1] : 0) + a, pb = (wid ? red[1][wid - 1] : 0) + b;   // inclusive
+    const long long np0 = s_np, nd0 = s_nd;
+    // per-row events in k_boot's order: invalid (row not taken), pending full
+    // (row not taken), then the row is taken and may be the budget + 1-th key
+    long long ev = 0x7fffffffffffLL; int st = ST_DONE;
+    if (in) {
+      const int bad = E.bad[start + r];
+      if (bad) { ev = 2 * r; st = ST_INVALID; }
+      else if (np_in && np0 + pa - 1 >= E.pend_cap) { ev = 2 * r; st = ST_GROW; }
+      else if (nd_in && nd0 + pb > E.m) { ev = 2 * r + 1; st = ST_BUILD; }
+    }
+    // earliest event of the chunk
+    long long evm = ev;
+    for (int o = 16; o >= 1; o >>= 1) evm = min(evm, __shfl_xor_sync(PCY_FULL, evm, o));
+    __syncthreads();
+    if (lane == 0) red[0][wid] = evm;
+    __syncthreads();
+    if (tid == 0) {
+      long long e = 0x7fffffffffffLL;
+      for (int q = 0; q < (int)(blockDim.x >> 5); ++q) e = min(e, red[0][q]);
+      red[1][32] = e;
+    }
+    __syncthreads();
+    const long long eall = red[1][32];
+    if (in && eall != 0x7fffffffffffLL && ev == eall) {   // the event's (unique) row
+      s_status = st;
+      s_stop = r;
+      C->err = st == ST_INVALID ? E.bad[start + r] : 0;
+    }
+    __syncthreads();
+    const long long lim = eall == 0x7fffffffffffLL ? cnt : (eall >> 1) + (eall & 1);   // rows taken in this chunk range
+    const bool take = in && r < lim;
+    if (take) {
+      if (np_in) B.ppos[r] = (int)(np0 + pa - 1);
+      if (nd_in) B.dpos[r] = (int)(nd0 + pb - 1);
+    }
+    // counters over taken rows
+    long long wsum = take ? E.wb[start + r] : 0;
+    long long tnp = take ? np_in : 0, tnd = take ? nd_in : 0;
+    for (int o = 16; o >= 1; o >>= 1) {
+      wsum += __shfl_xor_sync(PCY_FULL, wsum, o);
+      tnp += __shfl_xor_sync(PCY_FULL, tnp, o);
+      tnd += __shfl_xor_sync(PCY_FULL, tnd, o);
+    }
+    __syncthreads();
+    if (lane == 0) { red[0][wid] = wsum; red[1][wid] = tnp * 65536LL + tnd; }
+    __syncthreads();
+    if (tid == 0) {
+      for (int q = 0; q < (int)(blockDim.x >> 5); ++q) { s_w += red[0][q]; s_np += red[1][q] >> 16; s_nd += red[1][q] & 65535; }
+    }
+    __syncthreads();
+    if (eall != 0x7fffffffffffLL) break;
+  }
+  if (tid == 0) {
+    C->npend = s_np; C->ndist = s_nd; C->total_w += s_w;
+    C->status = s_status; C->stop = start + (s_status == ST_DONE ? cnt : s_stop);
+    B.flags[cnt] = (int)(s_status == ST_DONE ? cnt : s_stop + (s_status == ST_BUILD ? 1 : 0));   // rows taken
+  }
+}
+
+// Rows taken: pending rows and weights (a run of equal rows sums into its
+// first), new keys into the distinct rows and the table.
+__global__ void k_boot_apply(EngDev E, BootScratch B, long long start, long long n, long long npend0) {
+  const int lane = threadIdx.x & 31;
+  const long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const long long taken = B.flags[n - start];
+  if (r >= taken) return;
+  const int d = E.d, ld = E.ld;
+  const double* x = E.xb + (start + r) * ld;
+  const int fl = B.flags[r];
+  if ((fl & 1) || r == 0) {
+    // weight of the run starting here (the leading run continues the last entry)
+    long long q = r;
+    long long wsum = E.wb[start + q];
+    for (++q; q < taken && !(B.flags[q] & 1); ++q) wsum += E.wb[start + q];
+    if (fl & 1) {
+      const long long p = B.ppos[r];
+      double* pr = E.pend_x + p * ld;
+      for (int e = lane; e < ld; e += 32) pr[e] = x[e];
+      if (lane == 0) { E.pend_w[p] = wsum; E.pend_xsq[p] = E.xsq[start + r]; }
+    } else if (lane == 0) {
+      E.pend_w[npend0 - 1] += wsum;   // leading run of the previous entry's key
+    }
+  }
+  if (B.spos[r] >= 0 && B.sfirst[B.spos[r]] == (int)r) {
+    const long long p = B.dpos[r];
+    double* dr = E.dist_x + p * ld;
+    for (int e = lane; e < ld; e += 32) dr[e] = x[e];
+    if (lane == 0) {
+      const unsigned long long mask = (unsigned long long)E.hcap - 1ULL;
+      unsigned long long slot = E.hsh[start + r] & mask;
+      while (atomicCAS(&E.htab[slot], -1, (int)p) != -1) slot = (slot + 1) & mask;
+    }
   }
 }
 
@@ -890,7 +1080,10 @@ struct Engine {
   double tc_tau = 0.0;
   float *tc_ahi = nullptr, *tc_alo = nullptr, *tc_bhi = nullptr, *tc_blo = nullptr, *tc_dots = nullptr;
   double *tc_rnc = nullptr, *tc_xn2 = nullptr, *tc_c = nullptr;
+  long long* tc_done = nullptr;   // creation index each slot's split was made for
   unsigned* parbits = nullptr;   // k_plan scratch: nodes some window item acts on
+  BootScratch bs{};            // parallel bootstrap scratch
+  bool seq_boot = false;       // PCY_SEQ_BOOT: the one-warp k_boot instead
   ParCtl* parctl = nullptr;
   int* planbuf = nullptr;       // k_plan scratch: window openers   // k_plan output (subtree-parallel resolve)
   long long kbatch = 1024;     // K1 rows per launch when k3par
@@ -984,6 +1177,9 @@ struct Engine {
     A_(E.order, NC); A_(E.lvl, NC); A_(E.stk_g, NC + 1); A_(E.stk_p, NC + 1);
     A_(E.minbits, 2);
     A_(aggw, m + 2); A_(mp_nrm, sample_cap + 1);
+    bs.scap = 1; while (bs.scap < 2 * Bmax) bs.scap <<= 1;
+    A_(bs.flags, Bmax + 1); A_(bs.spos, Bmax); A_(bs.ppos, Bmax); A_(bs.dpos, Bmax); A_(bs.skey, bs.scap); A_(bs.sfirst, bs.scap);
+    seq_boot = getenv("PCY_SEQ_BOOT") != nullptr;
     A_(parctl, 1); A_(parbits, NC / 32 + 2); A_(planbuf, 2 * PCY_PAR_MAXITEMS);
 #undef A_
     for (auto& e : ev) PCY_CUDA(cudaEventCreate(&e));
@@ -1090,30 +1286,38 @@ struct Engine {
     E.tc_dots = nullptr;
     const long long N = ctl_h->F_alloc;   // upper bound on the live columns (device count in fs_cnt)
     if (!nper || N < 256 || getenv("PCY_NO_FULLSET")) return false;
-    const long long ng = ctl_h->G_alloc;
-    k_group_offsets<<<1, 1024, 0, st>>>(E.g_count, ng, E.fs_gofs, E.fs_cnt); pcy_count_launch();
-    k_group_scatter<<<(unsigned)((ng + 7) / 8), 256, 0, st>>>(E, ng, E.fs_list); pcy_count_launch();
     if (use_tc) {
-      // tensor cores: split-TF32 dots around the block's first row
+      // tensor cores: split-TF32 dots against the reference slots.  The slots
+      // keep their split (fixed engine centre, re-split only when a slot gets a
+      // new reference), so a launch splits only the block rows.
       if (!tc_dots) {
         const long long acap = 1024, bcap = (NC + 127) / 128 * 128;
         if ((*rc = alloc(tc_ahi, acap * Kp)) || (*rc = alloc(tc_alo, acap * Kp)) || (*rc = alloc(tc_bhi, bcap * Kp)) ||
             (*rc = alloc(tc_blo, bcap * Kp)) || (*rc = alloc(tc_dots, acap * NC)) || (*rc = alloc(tc_rnc, NC)) ||
-            (*rc = alloc(tc_xn2, acap)) || (*rc = alloc(tc_c, (long long)Kp)))
+            (*rc = alloc(tc_xn2, acap)) || (*rc = alloc(tc_c, (long long)Kp)) || (*rc = alloc(tc_done, NC)))
           return false;
+        if (cudaMemsetAsync(tc_done, 0xff, sizeof(long long) * NC, st) != cudaSuccess ||
+            cudaMemsetAsync(tc_bhi, 0, sizeof(float) * bcap * Kp, st) != cudaSuccess ||
+            cudaMemsetAsync(tc_blo, 0, sizeof(float) * bcap * Kp, st) != cudaSuccess) {
+          pcy_set_error("tc buffer init failed"); *rc = PCY_ECUDA; return false;
+        }
+        if ((*rc = pcy_tc_center(A, aidx, ld, d, tc_c, st))) return false;   // the engine's centre
       }
-      if ((*rc = pcy_tc_center(A, aidx, ld, d, tc_c, st))) return false;
       if ((*rc = pcy_tc_split(A, aidx, ld, d, M, nullptr, tc_c, tc_ahi, tc_alo, tc_xn2, st))) return false;
-      if ((*rc = pcy_tc_split(E.r, E.fs_list, ld, d, N, E.fs_cnt, tc_c, tc_bhi, tc_blo, tc_rnc, st))) return false;
+      if ((*rc = pcy_tc_split_slots(E.r, ld, d, N, E.alive, E.idx, tc_done, tc_c, tc_bhi, tc_blo, tc_rnc, st)))
+        return false;
       const bool prof = pcy_prof_enabled();
       if (prof) PCY_CUDA(cudaEventRecord(ev[6], st));
-      if ((*rc = pcy_tc_dots(tc_ahi, tc_alo, 1024, (int)M, tc_bhi, tc_blo, (NC + 127) / 128 * 128, (int)N, E.fs_cnt,
+      if ((*rc = pcy_tc_dots(tc_ahi, tc_alo, 1024, (int)M, tc_bhi, tc_blo, (NC + 127) / 128 * 128, (int)N, nullptr,
                              Kp, tc_dots, N, st)))
         return false;
-      if (prof) { PCY_CUDA(cudaEventRecord(ev[7], st)); gemm_timed = true; gemm_flops = 2.0 * (double)M * (double)ctl_h->F * d; }
+      if (prof) { PCY_CUDA(cudaEventRecord(ev[7], st)); gemm_timed = true; gemm_flops = 2.0 * (double)M * (double)N * d; }
       E.tc_dots = tc_dots; E.tc_ldo = N; E.tc_rnc = tc_rnc; E.tc_xn2 = tc_xn2; E.tc_tau = tc_tau;
       return false;   // no fp64 parts matrix: K1 reads E.tc_dots
     }
+    const long long ng = ctl_h->G_alloc;
+    k_group_offsets<<<1, 1024, 0, st>>>(E.g_count, ng, E.fs_gofs, E.fs_cnt); pcy_count_launch();
+    k_group_scatter<<<(unsigned)((ng + 7) / 8), 256, 0, st>>>(E, ng, E.fs_list); pcy_count_launch();
     if (!parts) { if ((*rc = alloc(parts, (long long)1024 * NC))) return false; }
     const bool prof = pcy_prof_enabled();
     if (prof) { cudaEventRecord(ev[6], st); }
@@ -1392,7 +1596,16 @@ struct Engine {
       long long i = 0;
       while (i < nb) {
         if (!built) {
-          k_boot<<<1, 32, 0, st>>>(E, i, nb); pcy_count_launch();
+          if (seq_boot) {
+            k_boot<<<1, 32, 0, st>>>(E, i, nb); pcy_count_launch();
+          } else {
+            PCY_CUDA(cudaMemsetAsync(bs.skey, 0xff, sizeof(int) * bs.scap, st));
+            PCY_CUDA(cudaMemsetAsync(bs.sfirst, 0x7f, sizeof(int) * bs.scap, st));
+            const unsigned g8 = (unsigned)((nb - i + 7) / 8);
+            k_boot_scan_rows<<<g8, 256, 0, st>>>(E, bs, i, nb); pcy_count_launch();
+            k_boot_plan<<<1, 1024, 0, st>>>(E, bs, i, nb); pcy_count_launch();
+            k_boot_apply<<<g8, 256, 0, st>>>(E, bs, i, nb, ctl_h->npend); pcy_count_launch();
+          }
           PCY_LAUNCH_CHECK();
           int rc = sync_ctl(st); if (rc) return rc;
           const int status = ctl_h->status;

@@ -97,7 +97,8 @@ __global__ void __launch_bounds__(128, 1) k_tc_dots(const __grid_constant__ CUte
   uint64_t* accum_full = empty + TSTAGES;
   uint32_t* tmem_slot = (uint32_t*)(accum_full + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * TBM, n0 = blockIdx.x * TBN;
+  // row tiles fastest: the CTAs sharing a B panel run together (one HBM read of B)
+  const int m0 = blockIdx.x * TBM, n0 = blockIdx.y * TBN;
   const int nk = Kp / TBK;
   if (n_dev) { N = min(N, *n_dev); if (n0 >= N) return; }
 
@@ -227,6 +228,32 @@ __global__ void k_tc_split(const double* __restrict__ src, const int* __restrict
   if (lane == 0 && nrm2) nrm2[i] = acc;
 }
 
+// Reference slots, split in place (row = slot) once per reference: a slot is
+// re-split when it is alive and its creation index differs from the one it
+// was split for (references never change while a node lives, coreset.py:193).
+__global__ void k_tc_split_slots(const double* __restrict__ src, long long ld, int d, long long nslots,
+                                 const int* __restrict__ alive, const long long* __restrict__ cidx,
+                                 long long* __restrict__ done_idx, const double* __restrict__ center, int Kp,
+                                 float* __restrict__ hi, float* __restrict__ lo, double* __restrict__ nrm2) {
+  const int lane = threadIdx.x & 31;
+  const long long i = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= nslots || !alive[i] || done_idx[i] == cidx[i]) return;
+  const double* x = src + i * ld;
+  float* h = hi + i * Kp;
+  float* l = lo + i * Kp;
+  double acc = 0.0;
+  for (int k = lane; k < Kp; k += 32) {
+    const double v = k < d ? x[k] - center[k] : 0.0;
+    const float vh = to_tf32((float)v);
+    const float vl = to_tf32((float)(v - (double)vh));
+    h[k] = vh;
+    l[k] = vl;
+    acc = fma(v, v, acc);
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) { nrm2[i] = acc; done_idx[i] = cidx[i]; }
+}
+
 __global__ void k_copy_row(const double* __restrict__ src, const int* __restrict__ idx, long long ld, int d,
                            double* __restrict__ dst) {
   for (int k = threadIdx.x; k < d; k += blockDim.x) dst[k] = src[(long long)(idx ? idx[0] : 0) * ld + k];
@@ -295,6 +322,18 @@ int pcy_tc_split(const double* src, const int* idx, long long ld, int d, long lo
   return PCY_OK;
 }
 
+int pcy_tc_split_slots(const double* src, long long ld, int d, long long nslots, const int* alive,
+                       const long long* cidx, long long* done_idx, const double* center, float* hi, float* lo,
+                       double* nrm2, cudaStream_t st) {
+  if (nslots <= 0) return PCY_OK;
+  const int Kp = pcy_tc_pad(d);
+  k_tc_split_slots<<<(unsigned)((nslots + 7) / 8), 256, 0, st>>>(src, ld, d, nslots, alive, cidx, done_idx, center, Kp,
+                                                                 hi, lo, nrm2);
+  pcy_count_launch();
+  PCY_LAUNCH_CHECK();
+  return PCY_OK;
+}
+
 int pcy_tc_center(const double* src, const int* idx, long long ld, int d, double* center, cudaStream_t st) {
   k_copy_row<<<1, 256, 0, st>>>(src, idx, ld, d, center);
   pcy_count_launch();
@@ -314,7 +353,7 @@ int pcy_tc_dots(const float* Ahi, const float* Alo, long long a_cap, int M, cons
   if ((rc = make_map(&ma, Ahi, a_cap, Kp)) || (rc = make_map(&mal, Alo, a_cap, Kp)) ||
       (rc = make_map(&mb, Bhi, b_cap, Kp)) || (rc = make_map(&mbl, Blo, b_cap, Kp)))
     return rc;
-  dim3 grid((unsigned)((N + TBN - 1) / TBN), (unsigned)((M + TBM - 1) / TBM));
+  dim3 grid((unsigned)((M + TBM - 1) / TBM), (unsigned)((N + TBN - 1) / TBN));
   k_tc_dots<<<grid, 128, TC_SMEM, st>>>(ma, mal, mb, mbl, M, N, Kp, out, ldo, n_dev);
   pcy_count_launch();
   PCY_LAUNCH_CHECK();

@@ -126,3 +126,26 @@ def test_workload_streams(name, rows, m):
     d = X.shape[1]
     g, o = run_pair(X, None, d, m, block=40_000)
     assert_same(g, o)
+
+
+def test_bootstrap_runs_weights_and_invalid_row():
+    """Bootstrap block semantics (coreset.py:283-295) on the parallel scan:
+    runs of equal rows fold into one pending entry with summed weights,
+    non-consecutive repeats grow the pending buffer, and an invalid row inside
+    the bootstrap leaves exactly the earlier rows."""
+    rng = np.random.default_rng(21)
+    base = rng.normal(size=(90, 6))
+    idx = np.repeat(rng.integers(0, 90, size=700), rng.integers(1, 4, size=700))
+    X = base[idx]
+    W = rng.integers(1, 5, size=len(X))
+    for m in (50, 200):   # builds mid-block / stays in bootstrap
+        g, o = run_pair(X, W, 6, m, block=333)
+        assert_same(g, o)
+    Xb = X.copy()
+    Xb[400, 2] = np.inf
+    g = _engine(6, 200)
+    with pytest.raises(ValueError, match="non-finite"):
+        g.insert_block(Xb, W)
+    o = OracleEngine(6, 200)
+    o.insert_block(X[:400], W[:400])
+    assert_same(g, o)
