@@ -158,14 +158,15 @@ __device__ __forceinline__ void scan_members(const EngDev& E, const int* __restr
   }
 }
 
-// Nearest among members [0, cnt) using a precomputed parts row (full-set K1).
-__device__ __forceinline__ void scan_parts(const double* __restrict__ prow, int cnt, int lane, double& bp,
-                                           int& bpos) {
+// Nearest among members [0, cnt) using a precomputed parts row (full-set K1;
+// columns are reference slots, gathered per member).
+__device__ __forceinline__ void scan_parts(const double* __restrict__ prow, const int* __restrict__ mem, int cnt,
+                                           int lane, double& bp, int& bpos) {
   bp = INFINITY; bpos = 0x7fffffff;
   for (int c0 = 0; c0 < cnt; c0 += 32) {
     const int p = c0 + lane;
     double v = INFINITY; int ps = 0x7fffffff;
-    if (p < cnt) { v = prow[p]; ps = p; }
+    if (p < cnt) { v = prow[mem[p]]; ps = p; }
     warp_argmin(v, ps);
     if (v < bp) { bp = v; bpos = ps; }
   }
@@ -1081,13 +1082,12 @@ struct Engine {
   float *tc_ahi = nullptr, *tc_alo = nullptr, *tc_bhi = nullptr, *tc_blo = nullptr, *tc_dots = nullptr;
   double *tc_rnc = nullptr, *tc_xn2 = nullptr, *tc_c = nullptr;
   long long* tc_done = nullptr;   // creation index each slot's split was made for
-  unsigned* parbits = nullptr;   // k_plan scratch: nodes some window item acts on
   BootScratch bs{};            // parallel bootstrap scratch
   bool seq_boot = false;       // PCY_SEQ_BOOT: the one-warp k_boot instead
-  ParCtl* parctl = nullptr;
-  int* planbuf = nullptr;       // k_plan scratch: window openers   // k_plan output (subtree-parallel resolve)
+  size_t plan_smem = 0;        // k_plan dynamic shared memory
+  ParCtl* parctl = nullptr;    // k_plan output (subtree-parallel resolve)
   long long kbatch = 1024;     // K1 rows per launch when k3par
-  bool k3par = false;         // subtree-parallel resolve enabled (nper 1..8)
+  bool k3par = false;         // subtree-parallel resolve / reattach enabled
   int nper = 0;          // resolve kernel: 1..8 register rows, 100/101 shared-memory rows, 0 generic
   int nnew_cap = 0, rea_cap = 0;   // new-node table sizes of K3 and of the reattach
   size_t res_smem = 0, rea_smem = 0;
@@ -1161,6 +1161,7 @@ struct Engine {
     A_(E.w, NC); A_(E.q, NC); A_(E.sn, NC); A_(E.rn, NC); A_(E.idx, NC);
     A_(E.child, NC); A_(E.alive, NC); A_(E.free_ids, NC);
     A_(E.fs_list, NC); A_(E.fs_gofs, GC); A_(E.fs_cnt, 1);
+    A_(E.pathj, Bmax * 16);
     A_(E.s, NC * ld); A_(E.r, NC * ld);
     A_(E.g_base, GC); A_(E.g_count, GC); A_(E.g_cap, GC); A_(E.g_bs, GC); A_(E.g_bsbase, GC);
     A_(E.arena, AC);
@@ -1180,7 +1181,7 @@ struct Engine {
     bs.scap = 1; while (bs.scap < 2 * Bmax) bs.scap <<= 1;
     A_(bs.flags, Bmax + 1); A_(bs.spos, Bmax); A_(bs.ppos, Bmax); A_(bs.dpos, Bmax); A_(bs.skey, bs.scap); A_(bs.sfirst, bs.scap);
     seq_boot = getenv("PCY_SEQ_BOOT") != nullptr;
-    A_(parctl, 1); A_(parbits, NC / 32 + 2); A_(planbuf, 2 * PCY_PAR_MAXITEMS);
+    A_(parctl, 1);
 #undef A_
     for (auto& e : ev) PCY_CUDA(cudaEventCreate(&e));
     {
@@ -1259,10 +1260,11 @@ struct Engine {
       }
     }
     if (getenv("PCY_GENERIC_RESOLVE")) nper = 0;
-    PCY_CUDA(cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLAN_SMEM));
+    plan_smem = plan_smem_bytes((int)(NC / 32 + 1));
     {
       const char* pe = getenv("PCY_K3PAR");
-      k3par = nper >= 1 && (!pe || atoi(pe) != 0);
+      k3par = nper >= 1 && (!pe || atoi(pe) != 0) && plan_smem <= maxsm;
+      if (k3par) PCY_CUDA(cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan_smem));
     }
     if (!(ctl_h = ctl_pool_get())) { pcy_set_error("cudaHostAlloc of the control mirror failed"); return PCY_ENOMEM; }
     memset(ctl_h, 0, sizeof(EngCtl));
@@ -1315,14 +1317,12 @@ struct Engine {
       E.tc_dots = tc_dots; E.tc_ldo = N; E.tc_rnc = tc_rnc; E.tc_xn2 = tc_xn2; E.tc_tau = tc_tau;
       return false;   // no fp64 parts matrix: K1 reads E.tc_dots
     }
-    const long long ng = ctl_h->G_alloc;
-    k_group_offsets<<<1, 1024, 0, st>>>(E.g_count, ng, E.fs_gofs, E.fs_cnt); pcy_count_launch();
-    k_group_scatter<<<(unsigned)((ng + 7) / 8), 256, 0, st>>>(E, ng, E.fs_list); pcy_count_launch();
     if (!parts) { if ((*rc = alloc(parts, (long long)1024 * NC))) return false; }
     const bool prof = pcy_prof_enabled();
     if (prof) { cudaEventRecord(ev[6], st); }
-    *rc = pcy_launch_parts(A, aidx, ld, (int)M, E.r, E.fs_list, ld, E.rn, (int)N, E.fs_cnt, d, parts, N, st);
-    if (prof) { cudaEventRecord(ev[7], st); gemm_timed = true; gemm_flops = 2.0 * (double)M * (double)ctl_h->F * d; }
+    // columns = reference slots (dead slots give unused columns)
+    *rc = pcy_launch_parts(A, aidx, ld, (int)M, E.r, nullptr, ld, E.rn, (int)N, nullptr, d, parts, N, st);
+    if (prof) { cudaEventRecord(ev[7], st); gemm_timed = true; gemm_flops = 2.0 * (double)M * (double)N * d; }
     return true;
   }
 
@@ -1371,9 +1371,9 @@ struct Engine {
               grc = pcy_launch_gram(E.r, E.order + off, ld, (int)nb, E.r, E.order + off, ld, (int)nb, d, gram, nb, st);
               if (grc) return grc;
             }
-            k_plan<<<1, PCY_PAR_MAXITEMS, PLAN_SMEM, st>>>(E, nullptr, nullptr, nullptr, nb, -1, nper <= 8 ? rea_cap : nnew_cap,
-                                                   16, chh, chr, parctl, parbits, (int)(NC / 32 + 1), E.order + off,
-                                                   gram, nb, planbuf);
+            k_plan<<<1, PCY_PAR_MAXITEMS, plan_smem, st>>>(E, nullptr, nullptr, nullptr, nb, -1, nper <= 8 ? rea_cap : nnew_cap,
+                                                   16, chh, chr, parctl, (int)(NC / 32 + 1), E.order + off,
+                                                   gram, nb);
             pcy_count_launch();
             pp = parctl;
             switch (nper) {
@@ -1482,8 +1482,8 @@ struct Engine {
             const int grc = pcy_launch_gram(Xs, nullptr, ld, (int)kn, Xs, nullptr, ld, (int)kn, d, gram, kn, rs);
             if (grc) return grc;
           }
-          k_plan<<<1, PCY_PAR_MAXITEMS, PLAN_SMEM, rs>>>(E, XSs, Ws, Bs, kn, first_rem, nnew_cap, 16, chh, chr, parctl,
-                                                 parbits, (int)(NC / 32 + 1), nullptr, gram, kn, planbuf);
+          k_plan<<<1, PCY_PAR_MAXITEMS, plan_smem, rs>>>(E, XSs, Ws, Bs, kn, first_rem, nnew_cap, 16, chh, chr, parctl,
+                                                 (int)(NC / 32 + 1), nullptr, gram, kn);
           pcy_count_launch();
           pp = parctl;
           switch (nper) {

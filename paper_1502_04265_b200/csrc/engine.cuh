@@ -84,6 +84,8 @@ struct EngDev {
   // column order of the full-set contraction: group g's members occupy the
   // contiguous columns [fs_gofs[g], fs_gofs[g] + g_count[g]) (fs_list = slots)
   int* fs_list; int* fs_gofs; int* fs_cnt;
+  // K1 winners per level (Bmax x PCY_FMAXL ints, -1 past the record): k_plan's compact view of the chains
+  int* pathj;
   // rebuild / extraction scratch
   int* order; int* lvl; int* stk_g; int* stk_p;
   unsigned long long* minbits;

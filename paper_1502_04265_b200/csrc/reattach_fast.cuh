@@ -34,7 +34,7 @@ __global__ void k_rchain(EngDev E, const int* __restrict__ order, long long n, C
     if (E.tc_dots)   // tensor-core dots + near-tie recheck
       scan_parts_tc(E, i, g, E.arena + base, cnt, [&](int jj) { return warp_dot(E.r + (long long)jj * ld, xv, d, lane); },
                     lane, bp, bpos, nre);
-    else if (P) scan_parts(P + i * ldp + E.fs_gofs[g], cnt, lane, bp, bpos);   // parts from the DMMA contraction
+    else if (P) scan_parts(P + i * ldp, E.arena + base, cnt, lane, bp, bpos);   // parts from the DMMA contraction
     else scan_members(E, E.arena + base, 0, cnt, xv, lane, bp, bpos);
     const int j = bpos < cnt ? E.arena[base + bpos] : -1;
     ChainLvl c = empty_level();
@@ -53,11 +53,11 @@ __global__ void k_rchain(EngDev E, const int* __restrict__ order, long long n, C
       c.take = rsub(mq, rdiv(mnorm, (double)mw)) <= T ? 1 : 0;
       if (c.take && pred < 0) { pred = L - 1; predj = j; }
     }
-    if (lane == 0) rec[L - 1] = c;
+    if (lane == 0) { rec[L - 1] = c; E.pathj[i * PCY_FMAXL + L - 1] = c.j; }
     if (outside) { if (pred < 0) pred = L - 1; break; }
     if (c.child < 0) {
       if (L < PCY_FMAXL) {
-        if (lane == 0) rec[L] = empty_level();
+        if (lane == 0) { rec[L] = empty_level(); E.pathj[i * PCY_FMAXL + L] = -1; }
         ++L;
         if (pred < 0) pred = L - 1;
       } else trunc = 1;

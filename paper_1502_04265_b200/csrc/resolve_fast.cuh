@@ -96,7 +96,7 @@ __global__ void k_chain2(EngDev E, const double* __restrict__ X, const double* _
     if (E.tc_dots)   // tensor-core dots + near-tie recheck
       scan_parts_tc(E, i, g, E.arena + base, cnt, [&](int jj) { return xdot(E.r + (long long)jj * ld); }, lane, bp,
                     bpos, nre);
-    else if (P) scan_parts(P + i * ldp + E.fs_gofs[g], cnt, lane, bp, bpos);   // DMMA parts
+    else if (P) scan_parts(P + i * ldp, E.arena + base, cnt, lane, bp, bpos);   // DMMA parts
     else scan_members(E, E.arena + base, 0, cnt, xv, lane, bp, bpos);
     const int j = bpos < cnt ? E.arena[base + bpos] : -1;
     ChainLvl c = empty_level();
@@ -116,11 +116,11 @@ __global__ void k_chain2(EngDev E, const double* __restrict__ X, const double* _
         if (pred < 0) { pred = L - 1; predj = j; }
       }
     }
-    if (writer) rec[L - 1] = c;
+    if (writer) { rec[L - 1] = c; E.pathj[i * PCY_FMAXL + L - 1] = c.j; }
     if (outside) { if (pred < 0) pred = L - 1; break; }
     if (c.child < 0) {
       if (L < PCY_FMAXL) {
-        if (writer) rec[L] = empty_level();
+        if (writer) { rec[L] = empty_level(); E.pathj[i * PCY_FMAXL + L] = -1; }
         ++L;
         if (pred < 0) pred = L - 1;
       } else trunc = 1;
@@ -801,7 +801,12 @@ __global__ void __launch_bounds__(64, 1) k_resolve2(EngDev E, const double* __re
 // collected nodes in rebuild order: a merge is the absorb, a group add the open.
 constexpr int PLAN_HASH = 4096;
 constexpr int PLAN_ROOT = -2;
-constexpr size_t PLAN_SMEM = sizeof(int) * 4 * PLAN_HASH;
+// dynamic shared memory of k_plan: the hash / union-find tables, per-item xs
+// and opener links, and the active-node bitmap (nwords words)
+__host__ __device__ inline size_t plan_smem_bytes(int nwords) {
+  return sizeof(int) * 4 * PLAN_HASH + sizeof(double) * PCY_PAR_MAXITEMS + sizeof(int) * PCY_PAR_MAXITEMS +
+         sizeof(unsigned) * (size_t)nwords;
+}
 __device__ __forceinline__ int ph_slot(int key) { return (int)(((unsigned)key * 2654435761u) >> 20) & (PLAN_HASH - 1); }
 __device__ __forceinline__ int ph_insert(int* hkey, int key) {
   int s = ph_slot(key);
@@ -842,14 +847,17 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
                                                            long long first_rem, int cap_items, int theta,
                                                            const ChainHdr* __restrict__ H,
                                                            const ChainLvl* __restrict__ R, ParCtl* __restrict__ par,
-                                                           unsigned* __restrict__ act_bits, int nwords,
+                                                           int nwords,
                                                            const int* __restrict__ order, const double* __restrict__ gram,
-                                                           long long gld, int* __restrict__ scratch) {
+                                                           long long gld) {
   extern __shared__ int plan_sm[];
   int* hkey = plan_sm;                    // domain keys: SUB(v) = v, OPEN(P) = NC + P, OPEN(ROOT) = 2 NC
   int* uf = plan_sm + PLAN_HASH;          // union-find over hash slots
   int* ohead = plan_sm + 2 * PLAN_HASH;   // OPEN(P): list of its openers; later: set tickets
   int* hfirst = plan_sm + 3 * PLAN_HASH;  // first item of each domain set
+  double* xs_s = reinterpret_cast<double*>(plan_sm + 4 * PLAN_HASH);   // per item: |x|^2 (rn of the node)
+  int* onext = reinterpret_cast<int*>(xs_s + PCY_PAR_MAXITEMS);        // opener list links, by item
+  unsigned* act_bits = reinterpret_cast<unsigned*>(onext + PCY_PAR_MAXITEMS);   // active nodes
   __shared__ int ccnt[PCY_PAR_MAXITEMS / 32][PCY_PAR_MAXCTA];
   __shared__ int ctot[PCY_PAR_MAXCTA];
   __shared__ int wsum[32];
@@ -859,7 +867,6 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
   const long long F0 = C->F;
   const int NC = (int)E.NC;
   const int nn = (int)(n < PCY_PAR_MAXITEMS ? n : PCY_PAR_MAXITEMS);
-  int* onext = scratch;   // opener list links, by item
   long long room = E.m - F0;
   if (room < 0) room = 0;
   if (order) room = n;   // rebuild reattach: merges and adds never exceed the budget
@@ -878,15 +885,31 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
   double xs = 0.0;
   int pl = -1, alev = -1, absorb = -1, target = -1;   // absorb at `absorb` (level alev), or open under `target`
   bool opener = false;
+  int pj[PCY_FMAXL];   // K1 winner per level (E.pathj: 64 contiguous bytes per item)
+#pragma unroll
+  for (int l = 0; l < PCY_FMAXL; ++l) pj[l] = -1;
   if (tid < nn) {
     h = H[tid];
+    const int4* src = reinterpret_cast<const int4*>(E.pathj + (long long)tid * PCY_FMAXL);
+#pragma unroll
+    for (int q = 0; q < PCY_FMAXL / 4; ++q) {
+      const int4 v = src[q];
+      pj[4 * q] = v.x; pj[4 * q + 1] = v.y; pj[4 * q + 2] = v.z; pj[4 * q + 3] = v.w;
+    }
     const bool invalid = (BAD && BAD[tid]) || h.len == 0;
     if (!invalid) {
       xs = order ? E.rn[order[tid]] : XS[tid];
+      xs_s[tid] = xs;
       pl = h.pred < h.len ? h.pred : h.len - 1;
-      if (h.trunc) { alev = h.len - 1; absorb = rec[alev].j; }   // acts somewhere below the record
-      else if (rec[pl].take > 0) { alev = pl; absorb = rec[pl].j; }
-      else { opener = true; target = pl >= 1 ? rec[pl - 1].j : PLAN_ROOT; }
+      if (h.trunc) alev = h.len - 1;   // acts somewhere below the record
+      else if (rec[pl].take > 0) alev = pl;
+      else opener = true;
+#pragma unroll
+      for (int l = 0; l < PCY_FMAXL; ++l) {
+        if (l == alev) absorb = pj[l];
+        if (opener && l + 1 == pl) target = pj[l];
+      }
+      if (opener && pl == 0) target = PLAN_ROOT;
     } else {
       atomicMin(&s_c, tid);
       if (tid < 64) atomicMax(&s_last, tid);
@@ -912,22 +935,24 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
     // action) whose row x would prefer to its K1 winner there
     if (tid < s_c) {
       const int lmax = opener ? pl : alev;
-      for (int l = 0; l <= lmax; ++l) {
-        const int P = l == 0 ? PLAN_ROOT : rec[l - 1].j;
+#pragma unroll
+      for (int l = 0; l < PCY_FMAXL; ++l) {
+        if (l > lmax) break;
+        const int P = l == 0 ? PLAN_ROOT : pj[l - 1];
         if (opener && P == target) break;   // x opens there itself: same domain
         const int so = ph_find(hkey, open_key(P));
         if (so < 0) continue;
         const double prec = rec[l].part;
         for (int y = ohead[so]; y >= 0; y = onext[y]) {
           if (y >= tid) continue;
-          const double xsy = order ? E.rn[order[y]] : XS[y];
+          const double xsy = xs_s[y];
           const double pnew = radd(xsy, rmul(gram[(long long)tid * gld + y], -2.0));
           if (pnew < prec + 1e-10 * (xs + xsy) + 1e-300) {
             if (P == PLAN_ROOT) {   // the window ends before this root open
               atomicMin(&s_c, y);
               if (y < 64) atomicMax(&s_last, y);
             } else {
-              const int v = rec[l].j;
+              const int v = pj[l];
               atomicOr(&act_bits[v >> 5], 1u << (v & 31));
               uf_union(uf, so, ph_insert(hkey, v));
             }
@@ -955,14 +980,16 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
   // the item's first domain, united with every further domain on its path
   int k1 = -1;
   if (act) {
-    if (heavy) k1 = ph_insert(hkey, rec[0].j >= 0 ? rec[0].j : 2 * NC + 1);
+    if (heavy) k1 = ph_insert(hkey, pj[0] >= 0 ? pj[0] : 2 * NC + 1);
     else {
       const int lmax = opener ? pl : alev;
-      for (int l = 0; l <= lmax; ++l) {
+#pragma unroll
+      for (int l = 0; l < PCY_FMAXL; ++l) {
+        if (l > lmax) break;
         int ks = -1;
         if (opener && l == pl) ks = ph_insert(hkey, open_key(target));
         else {
-          const int j = rec[l].j;
+          const int j = pj[l];
           if (j >= 0 && ((act_bits[j >> 5] >> (j & 31)) & 1u)) ks = ph_insert(hkey, j);
         }
         if (ks >= 0) {
