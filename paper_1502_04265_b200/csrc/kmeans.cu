@@ -69,7 +69,7 @@ __device__ __forceinline__ double block_exscan(double v, double* red, double* to
 //   phase B (CTA r < reps): _draw (:49-53) of repetition r from the chunk
 //     totals, falling back to the weights when the mass is all zero (:77-78),
 //     and the pick copied into the centre list.
-constexpr int KS_THREADS = 512, KS_CHUNK = 64, KS_RMAX = 8;
+constexpr int KS_THREADS = 512, KS_CHUNK = 32, KS_RMAX = 8;
 
 __device__ int chunk_draw(const double* __restrict__ part, long long nch, const double* __restrict__ vals,
                           long long n, double u, double* red, int* ired, double* s_tot) {
@@ -168,9 +168,44 @@ __global__ void __launch_bounds__(KS_THREADS) k_seed_coop(const double* __restri
           double acc[KS_RMAX];
 #pragma unroll
           for (int q = 0; q < KS_RMAX; ++q) acc[q] = 0.0;
-          // 8 row elements in flight per lane; each repetition still sums its
-          // elements in increasing e order
           int e = lane;
+          if ((d & 1) == 0) {
+            // even d (16-byte rows): 16 row elements in flight per lane as
+            // 128-bit loads, element pairs (2l, 2l+1) + 64 t
+            const double2* p2 = reinterpret_cast<const double2*>(p);
+            const int d2 = d >> 1;
+            int e2 = lane;
+            for (; e2 + 7 * 32 < d2; e2 += 8 * 32) {
+              double2 pv[8];
+#pragma unroll
+              for (int t = 0; t < 8; ++t) pv[t] = p2[e2 + 32 * t];
+#pragma unroll
+              for (int q = 0; q < KS_RMAX; ++q)
+                if (q < rn) {
+                  const double2* cq = reinterpret_cast<const double2*>(cs + (long long)q * d) + e2;
+#pragma unroll
+                  for (int t = 0; t < 8; ++t) {
+                    const double2 cv = cq[32 * t];
+                    const double dx = rsub(pv[t].x, cv.x), dy = rsub(pv[t].y, cv.y);
+                    acc[q] = fma(dx, dx, acc[q]);
+                    acc[q] = fma(dy, dy, acc[q]);
+                  }
+                }
+            }
+            for (int t = e2; t < d2; t += 32) {
+              const double2 pv = p2[t];
+#pragma unroll
+              for (int q = 0; q < KS_RMAX; ++q)
+                if (q < rn) {
+                  const double2 cv = reinterpret_cast<const double2*>(cs + (long long)q * d)[t];
+                  const double dx = rsub(pv.x, cv.x), dy = rsub(pv.y, cv.y);
+                  acc[q] = fma(dx, dx, acc[q]);
+                  acc[q] = fma(dy, dy, acc[q]);
+                }
+            }
+            e = d;   // done
+          }
+          // odd d: 8 row elements in flight per lane, lane-strided
           for (; e + 7 * 32 < d; e += 8 * 32) {
             double pv[8];
 #pragma unroll
@@ -340,39 +375,56 @@ __global__ void __launch_bounds__(KM_THREADS) k_cost(const double* __restrict__ 
   if (threadIdx.x == 0) cost_out[rep] = tot;
 }
 
-// Centroid update (:133-138): one CTA per (center, rep); points of the center
-// summed in index order.  Empty centers keep their previous value.
-__global__ void k_update(const double* __restrict__ P, const double* __restrict__ w, long long n, int d, int k,
-                         const int* __restrict__ active, const int* __restrict__ assign_all,
-                         double* __restrict__ centers) {
+// Centroid update (:133-138): one CTA per (center, rep); the members of the
+// center are compacted in index order, 4096 assignments per window (16 per
+// thread, one block scan per window), and their weighted rows summed in index
+// order.  Empty centers keep their previous value.
+constexpr int KU_THREADS = 256, KU_PER = 16, KU_WIN = KU_THREADS * KU_PER;
+__global__ void __launch_bounds__(KU_THREADS) k_update(const double* __restrict__ P, const double* __restrict__ w,
+                                                       long long n, int d, int k, const int* __restrict__ active,
+                                                       const int* __restrict__ assign_all, double* __restrict__ centers) {
   extern __shared__ double acc_s[];
+  __shared__ int s_list[KU_WIN];
+  __shared__ int wtot[KU_THREADS / 32 + 1];
   __shared__ double s_mass;
-  __shared__ int s_list[256];
-  __shared__ int s_cnt;
   const int j = blockIdx.x, rep = blockIdx.y;
   if (active && !active[rep]) return;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int* assign = assign_all + (long long)rep * n;
   double* C = centers + (long long)rep * k * d;
   for (int e = threadIdx.x; e < d; e += blockDim.x) acc_s[e] = 0.0;
   if (threadIdx.x == 0) s_mass = 0.0;
   __syncthreads();
-  for (long long base = 0; base < n; base += blockDim.x) {
-    // compact this window's members (in index order) into s_list
-    const long long i = base + threadIdx.x;
-    const bool mine = i < n && assign[i] == j;
-    const unsigned bal = __ballot_sync(PCY_FULL, mine);
-    __shared__ int wcnt[32];
-    if ((threadIdx.x & 31) == 0) wcnt[threadIdx.x >> 5] = __popc(bal);
+  for (long long base = 0; base < n; base += KU_WIN) {
+    // my 16 consecutive assignments
+    const long long i0 = base + (long long)threadIdx.x * KU_PER;
+    unsigned mine = 0u;
+#pragma unroll
+    for (int t = 0; t < KU_PER; ++t) {
+      const long long i = i0 + t;
+      if (i < n && assign[i] == j) mine |= 1u << t;
+    }
+    const int c = __popc(mine);
+    // exclusive scan of the counts in thread order
+    int inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(PCY_FULL, inc, o);
+      if (lane >= o) inc += v;
+    }
+    if (lane == 31) wtot[wid] = inc;
     __syncthreads();
     if (threadIdx.x == 0) {
-      int t = 0;
-      for (int q = 0; q < (int)(blockDim.x >> 5); ++q) { const int c = wcnt[q]; wcnt[q] = t; t += c; }
-      s_cnt = t;
+      int run = 0;
+      for (int q = 0; q < KU_THREADS / 32; ++q) { const int v = wtot[q]; wtot[q] = run; run += v; }
+      wtot[KU_THREADS / 32] = run;
     }
     __syncthreads();
-    if (mine) s_list[wcnt[threadIdx.x >> 5] + __popc(bal & ((1u << (threadIdx.x & 31)) - 1u))] = (int)(i - base);
+    int pos = wtot[wid] + inc - c;
+    for (int t = 0; t < KU_PER; ++t)
+      if ((mine >> t) & 1u) s_list[pos++] = (int)(i0 + t - base);
     __syncthreads();
-    const int cnt = s_cnt;
+    const int cnt = wtot[KU_THREADS / 32];
     for (int e = threadIdx.x; e < d; e += blockDim.x) {
       double a = acc_s[e];
       for (int t = 0; t < cnt; ++t) {
@@ -480,7 +532,7 @@ int pcy_lloyd(const double* P, const double* w, long long n, int d, int k, int r
   for (int r = 0; r < reps; ++r) iters_out[r] = 0;
   k_rownorm<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(P, n, d, pn); pcy_count_launch();
   const size_t usm = sizeof(double) * d;
-  if (usm > 48 * 1024) PCY_CUDA(cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usm));
+  PCY_CUDA(cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usm));
   for (int it = 0; it < max_iters; ++it) {
     int nact = 0;
     for (int r = 0; r < reps; ++r) nact += act[r];
@@ -528,7 +580,7 @@ int pcy_lloyd(const double* P, const double* w, long long n, int d, int k, int r
     }
     if (!any_update) break;
     PCY_CUDA(cudaMemcpyAsync(active, act.data(), sizeof(int) * reps, cudaMemcpyHostToDevice, st));
-    k_update<<<dim3(k, reps), 256, usm, st>>>(P, w, n, d, k, active, assign, centers); pcy_count_launch();
+    k_update<<<dim3(k, reps), KU_THREADS, usm, st>>>(P, w, n, d, k, active, assign, centers); pcy_count_launch();
     PCY_LAUNCH_CHECK();
   }
   PCY_CUDA(pcy_spin_sync(st));
