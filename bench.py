@@ -452,12 +452,14 @@ def main():
         # node scalars (w, q, sn) read+write, chain entry (id + part)
         bytes_per_pt = 8 * d * 3 + 48 + 12
         achieved = (r_units * bytes_per_pt) / (r_ms / 1e3) / 1e9 if r_ms > 0 else 0.0
-        roof = {"kernel": "k_resolve (K3 in-order resolve + CF update)", "bound": "hbm",
-                "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": None, "peak_source": peak_src,
-                "note": "latency-bound sequential scan (one warp); algorithmic bytes = 24*d+60 per point",
-                "ns_per_point": (r_ms * 1e6 / r_units) if r_units else None,
-                "share_of_step": r_ms / ms if ms > 0 else None}
+        k3 = {"kernel": "k_resolve2/3 (K3 subtree-parallel resolve + CF update, incl. k_plan)", "bound": "hbm",
+              "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+              "traffic": None, "peak_source": peak_src,
+              "note": "latency-bound: one CTA per k_plan domain walks its items in stream order; "
+                      "algorithmic bytes = 24*d+60 per point",
+              "ns_per_point": (r_ms * 1e6 / r_units) if r_units else None,
+              "ms_per_step": r_ms / args.steps,
+              "share_of_step": r_ms / ms if ms > 0 else None}
         kernel_ms = {k: {"ms": v[0] / args.steps, "launches": v[1] / args.steps, "units": v[2] / args.steps}
                      for k, v in prof.items()}
         # north-star kernels: distance contraction (tensor), seeding (HBM), Lloyd assignment (tensor)
@@ -471,20 +473,25 @@ def main():
                 rooflines.append({"kernel": "k_tc_dots (K1 full-set distance contraction, split-TF32 on tcgen05)",
                                   "bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s", "frac": ach / pk,
                                   "launches_per_step": g_cnt / args.steps, "traffic": None,
+                                  "ms_per_step": g_ms / args.steps, "share_of_step": g_ms / ms if ms > 0 else None,
                                   "peak_source": "measured cuBLAS TF32 GEMM / 3 (three TF32 products per "
-                                                 "fp32-faithful product); achieved = 2*M*F*d per launch"})
+                                                 "fp32-faithful product); achieved = 2*M*N*d per launch "
+                                                 "(M block rows x N reference slots)"})
             else:
                 pk = gemm_peaks.get("fp64_tflops", 40.0)
                 rooflines.append({"kernel": "k_dist_tile<2> (K1 full-set distance contraction, fp64 DMMA)",
                                   "bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s", "frac": ach / pk,
                                   "launches_per_step": g_cnt / args.steps, "traffic": None,
-                                  "peak_source": "measured cuBLAS FP64 GEMM; achieved = 2*M*F*d per launch"})
+                                  "ms_per_step": g_ms / args.steps, "share_of_step": g_ms / ms if ms > 0 else None,
+                                  "peak_source": "measured cuBLAS FP64 GEMM; achieved = 2*M*N*d per launch "
+                                                 "(M block rows x N reference slots)"})
         s_ms, s_cnt, s_bytes = prof_x["seed"]
         if s_ms > 0:
             ach = s_bytes / (s_ms / 1e3) / 1e9
             rooflines.append({"kernel": "k_seed_coop (weighted k-means++, all repetitions)", "bound": "hbm",
                               "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
                               "launches_per_step": s_cnt / args.steps, "traffic": None,
+                              "ms_per_step": s_ms / args.steps, "share_of_step": s_ms / ms if ms > 0 else None,
                               "peak_source": peak_src + " HBM; algorithmic bytes = (k-1)(8nd + 24n*reps + 8n)"})
         l_ms, l_cnt, l_flops = prof_x["lloyd"]
         if l_ms > 0:
@@ -493,7 +500,14 @@ def main():
             rooflines.append({"kernel": "k_dist_tile<3> (Lloyd assignment, fp64 DMMA + argmin)", "bound": "tensor",
                               "achieved": ach, "peak": pk, "unit": "TFLOP/s", "frac": ach / pk,
                               "launches_per_step": l_cnt / args.steps, "traffic": None,
+                              "ms_per_step": l_ms / args.steps, "share_of_step": l_ms / ms if ms > 0 else None,
                               "peak_source": "measured cuBLAS FP64 GEMM; achieved = 2*n*k*d per repetition"})
+        # the headline roofline is the single kernel with the largest share of the
+        # step (the K1 contraction and the K3 launch set are the candidates; the
+        # ncu launch list under profiles/ gives the same ranking)
+        rooflines.append(k3)
+        roof = max(rooflines, key=lambda r: r.get("ms_per_step") or 0.0)
+        rooflines = [r for r in rooflines if r is not roof]
         cpu = None
         if not args.no_cpu_baseline:
             rows, t, _ = cpu_sample(cfg, n)
