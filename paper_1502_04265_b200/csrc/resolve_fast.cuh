@@ -21,7 +21,7 @@
 #define PCY_FMAXL 16
 #define PCY_MOD_SLOTS 2048
 #define PCY_NNEW_MAX 96    // new-node table of the large-d kernels (resolve_smem.cuh)
-#define PCY_NNEW_FAST 96   // new-node table of k_resolve2 / k_reattach2 (d <= 256); larger is slower (O(table) scans)
+#define PCY_NNEW_FAST 160  // new-node table of k_resolve2 / k_reattach2 (d <= 256), capped by shared memory
 #define PCY_GMAP_SLOTS 256
 
 struct __align__(16) ChainLvl {
@@ -861,7 +861,7 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
   __shared__ int ccnt[PCY_PAR_MAXITEMS / 32][PCY_PAR_MAXCTA];
   __shared__ int ctot[PCY_PAR_MAXCTA];
   __shared__ int wsum[32];
-  __shared__ int s_c, s_last, s_heavy, s_cut;
+  __shared__ int s_c, s_last, s_heavy, s_cut, s_P;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const EngCtl* C = E.ctl;
   const long long F0 = C->F;
@@ -876,7 +876,7 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
   if (tid == 0) {
     s_c = (int)(room < nn ? room : nn);
     if (first_rem >= 0) s_c = 0;
-    s_last = -1; s_heavy = 0; s_cut = 0x7fffffff;
+    s_last = -1; s_heavy = 0; s_cut = 0x7fffffff; s_P = 0;
   }
   __syncthreads();
   // pass 1: invalid rows, weighted items, predicted actions
@@ -1008,9 +1008,15 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
   const unsigned bal = __ballot_sync(PCY_FULL, isfirst);
   if (lane == 0) wsum[wid] = __popc(bal);
   __syncthreads();
-  if (tid == 0) {
-    int t = 0;
-    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) { const int v = wsum[q]; wsum[q] = t; t += v; }
+  if (wid == 0) {   // exclusive scan of the 32 warp counts
+    const int v = wsum[lane];
+    int inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(PCY_FULL, inc, o);
+      if (lane >= o) inc += t;
+    }
+    wsum[lane] = inc - v;
   }
   __syncthreads();
   if (isfirst) ohead[root] = wsum[wid] + __popc(bal & ((1u << lane) - 1u));
@@ -1034,11 +1040,31 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
   const int c = c0 < s_cut ? c0 : s_cut;
   if (tid < c) atomicMax(&ctot[cta], rank + 1);
   __syncthreads();
+  // list offsets: exclusive scan of the CTA counts (warps 0..4), P = last CTA with items + 1
+  constexpr int SCAN_T = (PCY_PAR_MAXCTA + 1 + 31) / 32 * 32;
+  int cv = 0, cinc = 0;
+  if (tid < SCAN_T) {
+    cv = tid < PCY_PAR_MAXCTA ? ctot[tid] : 0;
+    cinc = cv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(PCY_FULL, cinc, o);
+      if (lane >= o) cinc += t;
+    }
+    if (lane == 31) wsum[wid] = cinc;
+    if (cv > 0) atomicMax(&s_P, tid + 1);
+  }
+  __syncthreads();
+  if (tid < SCAN_T) {
+    int base = 0;
+    for (int q = 0; q < wid; ++q) base += wsum[q];
+    const int ex = base + cinc - cv;
+    if (tid < PCY_PAR_MAXCTA) ctot[tid] = ex;
+    if (tid <= PCY_PAR_MAXCTA) par->off[tid] = ex;   // off[P] = window size
+  }
+  __syncthreads();
   if (tid == 0) {
-    int P = 0, run = 0;
-    for (int q = 0; q < PCY_PAR_MAXCTA; ++q) if (ctot[q] > 0) P = q + 1;
-    for (int q = 0; q < P; ++q) { par->off[q] = run; const int v = ctot[q]; ctot[q] = run; run += v; }
-    par->off[P] = run;
+    const int P = s_P;
     par->mode = 0; par->P = P; par->n_win = c; par->n_total = n;
     par->F0 = F0; par->Falloc0 = C->F_alloc; par->freen0 = C->free_n; par->Galloc0 = C->G_alloc;
     par->Aalloc0 = C->A_alloc; par->nidx0 = C->next_index;
