@@ -180,40 +180,123 @@ __device__ __forceinline__ void scan_parts(const double* __restrict__ prow, cons
 template <class RDot>
 __device__ __forceinline__ void scan_parts_tc(const EngDev& E, long long i, int g, const int* __restrict__ mem,
                                               int cnt, RDot rdot, int lane, double& bp, int& bpos, int& nre) {
-  // columns are reference slots (k_tc_split_slots): gathered per member
+  // columns are reference slots (k_tc_split_slots): gathered per member, four
+  // chunks of 32 members in flight per pass
   const float* __restrict__ dots = E.tc_dots + i * E.tc_ldo;
   const double* __restrict__ rnc = E.tc_rnc;
   const double xn = sqrt(E.tc_xn2[i]);
   const double tau2 = 2.0 * E.tc_tau * (1.0 + 1e-9);
   double U = INFINITY;
-  for (int p = lane; p < cnt; p += 32) {
-    const int jj = mem[p];
-    const double rc = rnc[jj];
-    U = fmin(U, rc - 2.0 * (double)dots[jj] + tau2 * sqrt(rc) * xn + 1e-300);
+  for (int c0 = 0; c0 < cnt; c0 += 128) {
+    int jj[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) { const int p = c0 + 32 * q + lane; jj[q] = p < cnt ? mem[p] : -1; }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (jj[q] >= 0) {
+        const double rc = rnc[jj[q]];
+        U = fmin(U, rc - 2.0 * (double)dots[jj[q]] + tau2 * sqrt(rc) * xn + 1e-300);
+      }
   }
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) U = fmin(U, __shfl_xor_sync(PCY_FULL, U, o));
   bp = INFINITY; bpos = 0x7fffffff;
   int ncand = 0;
-  for (int c0 = 0; c0 < cnt; c0 += 32) {
-    const int p = c0 + lane;
-    bool cand = false;
-    if (p < cnt) {
-      const int jj = mem[p];
-      const double rc = rnc[jj];
-      cand = rc - 2.0 * (double)dots[jj] - tau2 * sqrt(rc) * xn <= U;
+  for (int c0 = 0; c0 < cnt; c0 += 128) {
+    int jj[4];
+    bool cand[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) { const int p = c0 + 32 * q + lane; jj[q] = p < cnt ? mem[p] : -1; }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      cand[q] = false;
+      if (jj[q] >= 0) {
+        const double rc = rnc[jj[q]];
+        cand[q] = rc - 2.0 * (double)dots[jj[q]] - tau2 * sqrt(rc) * xn <= U;
+      }
     }
-    unsigned m = __ballot_sync(PCY_FULL, cand);
-    while (m) {
-      const int b = __ffs(m) - 1;
-      m &= m - 1;
-      const int jj = mem[c0 + b];
-      const double part = radd(E.rn[jj], rmul(rdot(jj), -2.0));
-      if (part < bp) { bp = part; bpos = c0 + b; }
-      ++ncand;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      unsigned m = __ballot_sync(PCY_FULL, cand[q]);
+      while (m) {   // position order
+        const int b = __ffs(m) - 1;
+        m &= m - 1;
+        const int j = __shfl_sync(PCY_FULL, jj[q], b);
+        const double part = radd(E.rn[j], rmul(rdot(j), -2.0));
+        if (part < bp) { bp = part; bpos = c0 + 32 * q + b; }
+        ++ncand;
+      }
     }
   }
   if (ncand > 1) nre += ncand - 1;   // members re-decided beyond the winner
+}
+
+// CTA form (WPI warps walk one item together, k_chain2<WPI>): the members are
+// split over the CTA's threads for both passes; the candidates gather in a
+// shared list (clist[0] = count) and are re-decided together with the CTA
+// dot, the lowest position winning exact ties as in the warp form.
+constexpr int TC_CAND_MAX = 256;
+template <int WPI, class RDot>
+__device__ __forceinline__ void scan_parts_tc_cta(const EngDev& E, long long i, const int* __restrict__ mem, int cnt,
+                                                  RDot rdot, int lane, int wib, double* red, int* clist, double& bp,
+                                                  int& bpos, int& nre) {
+  const float* __restrict__ dots = E.tc_dots + i * E.tc_ldo;
+  const double* __restrict__ rnc = E.tc_rnc;
+  const double xn = sqrt(E.tc_xn2[i]);
+  const double tau2 = 2.0 * E.tc_tau * (1.0 + 1e-9);
+  constexpr int T = 32 * WPI;
+  const int t = wib * 32 + lane;
+  double U = INFINITY;
+  for (int p0 = t; p0 < cnt; p0 += 4 * T) {
+    int jj[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) { const int p = p0 + T * q; jj[q] = p < cnt ? mem[p] : -1; }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (jj[q] >= 0) {
+        const double rc = rnc[jj[q]];
+        U = fmin(U, rc - 2.0 * (double)dots[jj[q]] + tau2 * sqrt(rc) * xn + 1e-300);
+      }
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) U = fmin(U, __shfl_xor_sync(PCY_FULL, U, o));
+  __syncthreads();
+  if (lane == 0) red[wib] = U;
+  if (t == 0) clist[0] = 0;
+  __syncthreads();
+#pragma unroll
+  for (int w = 0; w < WPI; ++w) U = fmin(U, red[w]);
+  for (int p0 = t; p0 < cnt; p0 += 4 * T) {
+    int jj[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) { const int p = p0 + T * q; jj[q] = p < cnt ? mem[p] : -1; }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (jj[q] >= 0) {
+        const double rc = rnc[jj[q]];
+        if (rc - 2.0 * (double)dots[jj[q]] - tau2 * sqrt(rc) * xn <= U) {
+          const int k = atomicAdd(&clist[0], 1);
+          if (k < TC_CAND_MAX) clist[1 + k] = p0 + T * q;
+        }
+      }
+  }
+  __syncthreads();
+  const int nc = clist[0];
+  bp = INFINITY; bpos = 0x7fffffff;
+  if (nc <= TC_CAND_MAX) {
+    for (int c = 0; c < nc; ++c) {
+      const int p = clist[1 + c];
+      const double part = radd(E.rn[mem[p]], rmul(rdot(mem[p]), -2.0));
+      if (part < bp || (part == bp && p < bpos)) { bp = part; bpos = p; }
+    }
+  } else {   // very wide near-tie window: every member exactly, position order
+    for (int p = 0; p < cnt; ++p) {
+      const double part = radd(E.rn[mem[p]], rmul(rdot(mem[p]), -2.0));
+      if (part < bp) { bp = part; bpos = p; }
+    }
+  }
+  if (nc > 1) nre += nc - 1;
+  __syncthreads();   // clist / red reuse
 }
 
 #include "resolve_fast.cuh"
@@ -1457,7 +1540,7 @@ struct Engine {
           const bool use_p = full_set(Xs, nullptr, kn, st, &grc);
           if (grc) return grc;
           if (ld > 512)   // one item per CTA, dots split over 4 warps
-            k_chain2<4><<<(unsigned)(kn), 128, sizeof(double) * (ld + 8), st>>>(
+            k_chain2<4><<<(unsigned)(kn), 128, sizeof(double) * (ld + 8) + sizeof(int) * (TC_CAND_MAX + 4), st>>>(
                 E, Xs, XSs, Ws, kn, chh, chr, use_p ? parts : nullptr, ctl_h->F_alloc);
           else
             k_chain2<1><<<nblk, wpc * 32, sizeof(double) * wpc * ld, st>>>(E, Xs, XSs, Ws, kn, chh, chr,

@@ -93,9 +93,14 @@ __global__ void k_chain2(EngDev E, const double* __restrict__ X, const double* _
   for (;;) {
     const int cnt = E.g_count[g], base = E.g_base[g];
     double bp; int bpos;
-    if (E.tc_dots)   // tensor-core dots + near-tie recheck
-      scan_parts_tc(E, i, g, E.arena + base, cnt, [&](int jj) { return xdot(E.r + (long long)jj * ld); }, lane, bp,
-                    bpos, nre);
+    if (E.tc_dots) {   // tensor-core dots + near-tie recheck
+      if constexpr (WPI == 1)
+        scan_parts_tc(E, i, g, E.arena + base, cnt, [&](int jj) { return xdot(E.r + (long long)jj * ld); }, lane, bp,
+                      bpos, nre);
+      else
+        scan_parts_tc_cta<WPI>(E, i, E.arena + base, cnt, [&](int jj) { return xdot(E.r + (long long)jj * ld); },
+                               lane, wib, red, reinterpret_cast<int*>(red + 8), bp, bpos, nre);
+    }
     else if (P) scan_parts(P + i * ldp, E.arena + base, cnt, lane, bp, bpos);   // DMMA parts
     else scan_members(E, E.arena + base, 0, cnt, xv, lane, bp, bpos);
     const int j = bpos < cnt ? E.arena[base + bpos] : -1;
