@@ -149,3 +149,38 @@ def test_bootstrap_runs_weights_and_invalid_row():
     o = OracleEngine(6, 200)
     o.insert_block(X[:400], W[:400])
     assert_same(g, o)
+
+
+def test_parallel_resolve_deterministic_and_equal_to_sequential(monkeypatch):
+    """The subtree-parallel resolve allocates slots and groups through atomic
+    tickets; the features (order, levels, weights, sums) must not depend on
+    that, and must equal the one-CTA sequential resolve (PCY_K3PAR=0)."""
+    from paper_1502_04265_b200 import workloads
+    X = workloads.generate_rows("cfg2", 0, 60_000)
+    d = X.shape[1]
+
+    def feats():
+        g = _engine(d, 2_000)
+        g.insert_block(X)
+        f = g.features()
+        return ([L for L, _ in f], [cf.weight for _, cf in f],
+                np.stack([cf.linear_sum for _, cf in f]), np.stack([cf.reference for _, cf in f]))
+
+    a, b = feats(), feats()
+    monkeypatch.setenv("PCY_K3PAR", "0")
+    c = feats()
+    for u, v, w in zip(a, b, c):
+        assert np.array_equal(np.asarray(u), np.asarray(v))
+        assert np.array_equal(np.asarray(u), np.asarray(w))
+
+
+def test_weighted_long_stream():
+    """Weighted items keep k_plan's windows at root keys with root opens as
+    stoppers (K1 does not follow partial takes)."""
+    rng = np.random.default_rng(77)
+    centers = rng.uniform(-30, 30, size=(40, 12))
+    X = centers[rng.integers(0, 40, size=30_000)] + rng.normal(size=(30_000, 12))
+    W = rng.integers(1, 6, size=30_000)
+    W[rng.random(30_000) < 0.7] = 1
+    g, o = run_pair(X, W, 12, 800, block=7_000)
+    assert_same(g, o)
