@@ -27,11 +27,12 @@ int pcy_launch_assign_d2(const double* P, long long ldp, int n, const double* pn
 double pcy_tc_error_tau(int Kp);
 int pcy_tc_pad(int d);
 int pcy_tc_center(const double* src, const int* idx, long long ld, int d, double* center, cudaStream_t st);
-// reference slots split in place (row = slot), only those alive and not yet
-// split for their creation index (done_idx)
+// reference slots alive and not yet split for their creation index
+// (done_idx) get the next live column (ncol ticket, col_of / col_slot) and
+// their split in that row of hi / lo; nrm2 stays slot-indexed
 int pcy_tc_split_slots(const double* src, long long ld, int d, long long nslots, const int* alive,
                        const long long* cidx, long long* done_idx, const double* center, float* hi, float* lo,
-                       double* nrm2, cudaStream_t st);
+                       double* nrm2, int* col_of, int* col_slot, int* ncol, cudaStream_t st);
 // rows_dev (nullable): device row count capping `rows` / `N`
 int pcy_tc_split(const double* src, const int* idx, long long ld, int d, long long rows, const int* rows_dev,
                  const double* center, float* hi, float* lo, double* nrm2, cudaStream_t st);

@@ -159,14 +159,14 @@ __device__ __forceinline__ void scan_members(const EngDev& E, const int* __restr
 }
 
 // Nearest among members [0, cnt) using a precomputed parts row (full-set K1;
-// columns are reference slots, gathered per member).
-__device__ __forceinline__ void scan_parts(const double* __restrict__ prow, const int* __restrict__ mem, int cnt,
-                                           int lane, double& bp, int& bpos) {
+// columns are the live columns, gathered per member through col_of).
+__device__ __forceinline__ void scan_parts(const double* __restrict__ prow, const int* __restrict__ col_of,
+                                           const int* __restrict__ mem, int cnt, int lane, double& bp, int& bpos) {
   bp = INFINITY; bpos = 0x7fffffff;
   for (int c0 = 0; c0 < cnt; c0 += 32) {
     const int p = c0 + lane;
     double v = INFINITY; int ps = 0x7fffffff;
-    if (p < cnt) { v = prow[mem[p]]; ps = p; }
+    if (p < cnt) { v = prow[col_of[mem[p]]]; ps = p; }
     warp_argmin(v, ps);
     if (v < bp) { bp = v; bpos = ps; }
   }
@@ -180,10 +180,11 @@ __device__ __forceinline__ void scan_parts(const double* __restrict__ prow, cons
 template <class RDot>
 __device__ __forceinline__ void scan_parts_tc(const EngDev& E, long long i, int g, const int* __restrict__ mem,
                                               int cnt, RDot rdot, int lane, double& bp, int& bpos, int& nre) {
-  // columns are reference slots (k_tc_split_slots): gathered per member, four
-  // chunks of 32 members in flight per pass
+  // columns are live columns (k_tc_split_slots): gathered per member through
+  // col_of, four chunks of 32 members in flight per pass
   const float* __restrict__ dots = E.tc_dots + i * E.tc_ldo;
   const double* __restrict__ rnc = E.tc_rnc;
+  const int* __restrict__ col_of = E.col_of;
   const double xn = sqrt(E.tc_xn2[i]);
   const double tau2 = 2.0 * E.tc_tau * (1.0 + 1e-9);
   double U = INFINITY;
@@ -195,7 +196,7 @@ __device__ __forceinline__ void scan_parts_tc(const EngDev& E, long long i, int 
     for (int q = 0; q < 4; ++q)
       if (jj[q] >= 0) {
         const double rc = rnc[jj[q]];
-        U = fmin(U, rc - 2.0 * (double)dots[jj[q]] + tau2 * sqrt(rc) * xn + 1e-300);
+        U = fmin(U, rc - 2.0 * (double)dots[col_of[jj[q]]] + tau2 * sqrt(rc) * xn + 1e-300);
       }
   }
 #pragma unroll
@@ -212,7 +213,7 @@ __device__ __forceinline__ void scan_parts_tc(const EngDev& E, long long i, int 
       cand[q] = false;
       if (jj[q] >= 0) {
         const double rc = rnc[jj[q]];
-        cand[q] = rc - 2.0 * (double)dots[jj[q]] - tau2 * sqrt(rc) * xn <= U;
+        cand[q] = rc - 2.0 * (double)dots[col_of[jj[q]]] - tau2 * sqrt(rc) * xn <= U;
       }
     }
 #pragma unroll
@@ -242,6 +243,7 @@ __device__ __forceinline__ void scan_parts_tc_cta(const EngDev& E, long long i, 
                                                   int& bpos, int& nre) {
   const float* __restrict__ dots = E.tc_dots + i * E.tc_ldo;
   const double* __restrict__ rnc = E.tc_rnc;
+  const int* __restrict__ col_of = E.col_of;
   const double xn = sqrt(E.tc_xn2[i]);
   const double tau2 = 2.0 * E.tc_tau * (1.0 + 1e-9);
   constexpr int T = 32 * WPI;
@@ -255,7 +257,7 @@ __device__ __forceinline__ void scan_parts_tc_cta(const EngDev& E, long long i, 
     for (int q = 0; q < 4; ++q)
       if (jj[q] >= 0) {
         const double rc = rnc[jj[q]];
-        U = fmin(U, rc - 2.0 * (double)dots[jj[q]] + tau2 * sqrt(rc) * xn + 1e-300);
+        U = fmin(U, rc - 2.0 * (double)dots[col_of[jj[q]]] + tau2 * sqrt(rc) * xn + 1e-300);
       }
   }
 #pragma unroll
@@ -274,7 +276,7 @@ __device__ __forceinline__ void scan_parts_tc_cta(const EngDev& E, long long i, 
     for (int q = 0; q < 4; ++q)
       if (jj[q] >= 0) {
         const double rc = rnc[jj[q]];
-        if (rc - 2.0 * (double)dots[jj[q]] - tau2 * sqrt(rc) * xn <= U) {
+        if (rc - 2.0 * (double)dots[col_of[jj[q]]] - tau2 * sqrt(rc) * xn <= U) {
           const int k = atomicAdd(&clist[0], 1);
           if (k < TC_CAND_MAX) clist[1 + k] = p0 + T * q;
         }
@@ -688,6 +690,30 @@ __global__ void k_mp_finish(EngDev E, long long ns) {
 }
 
 // ------------------------------------------------------- host publication
+// Live columns of the full-set contraction (DMMA path; the tensor-core path
+// assigns them in k_tc_split_slots): every slot that holds a node without a
+// column for its creation index takes the next column.  Between rebuilds no
+// node dies, so the columns are exactly the live nodes; after a rebuild the
+// engine recompacts (done = -1, ncol = 0), and the contraction spans F
+// columns instead of every slot ever allocated.
+__global__ void k_assign_cols(const int* __restrict__ alive, const long long* __restrict__ cidx, long long n,
+                              long long* __restrict__ done, int* __restrict__ col_of, int* __restrict__ col_slot,
+                              int* __restrict__ ncol) {
+  const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const bool need = s < n && alive[s] && done[s] != cidx[s];
+  const unsigned msk = __ballot_sync(PCY_FULL, need);
+  if (!msk) return;
+  const int leader = __ffs(msk) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(ncol, __popc(msk));
+  base = __shfl_sync(PCY_FULL, base, leader);
+  if (need) {
+    const int c = base + __popc(msk & ((1u << lane) - 1u));
+    col_of[s] = c; col_slot[c] = (int)s; done[s] = cidx[s];
+  }
+}
+
 __global__ void k_publish(EngCtl* __restrict__ src, EngCtl* dst, long long seq, const int* g_count,
                           const int* g_base) {
   const int lane = threadIdx.x;
@@ -1164,7 +1190,10 @@ struct Engine {
   double tc_tau = 0.0;
   float *tc_ahi = nullptr, *tc_alo = nullptr, *tc_bhi = nullptr, *tc_blo = nullptr, *tc_dots = nullptr;
   double *tc_rnc = nullptr, *tc_xn2 = nullptr, *tc_c = nullptr;
-  long long* tc_done = nullptr;   // creation index each slot's split was made for
+  long long* tc_done = nullptr;   // creation index each slot's column (and split) was made for
+  int* col_slot = nullptr;        // live column -> slot
+  int* ncol = nullptr;            // device count of live columns
+  bool cols_reset = true;         // recompact the live columns at the next contraction
   BootScratch bs{};            // parallel bootstrap scratch
   bool seq_boot = false;       // PCY_SEQ_BOOT: the one-warp k_boot instead
   size_t plan_smem = 0;        // k_plan dynamic shared memory
@@ -1244,6 +1273,8 @@ struct Engine {
     A_(E.w, NC); A_(E.q, NC); A_(E.sn, NC); A_(E.rn, NC); A_(E.idx, NC);
     A_(E.child, NC); A_(E.alive, NC); A_(E.free_ids, NC);
     A_(E.fs_list, NC); A_(E.fs_gofs, GC); A_(E.fs_cnt, 1);
+    { int* co = nullptr; A_(co, NC); E.col_of = co; }
+    A_(col_slot, NC); A_(ncol, 1); A_(tc_done, NC);
     A_(E.pathj, Bmax * 16);
     A_(E.s, NC * ld); A_(E.r, NC * ld);
     A_(E.g_base, GC); A_(E.g_count, GC); A_(E.g_cap, GC); A_(E.g_bs, GC); A_(E.g_bsbase, GC);
@@ -1369,8 +1400,15 @@ struct Engine {
   bool full_set(const double* A, const int* aidx, long long M, cudaStream_t st, int* rc) {
     *rc = PCY_OK;
     E.tc_dots = nullptr;
-    const long long N = ctl_h->F_alloc;   // upper bound on the live columns (device count in fs_cnt)
+    const long long N = ctl_h->F_alloc;   // upper bound on the live columns (device count in ncol)
     if (!nper || N < 256 || getenv("PCY_NO_FULLSET")) return false;
+    if (cols_reset) {   // recompact: every live node takes a fresh column below
+      if (cudaMemsetAsync(tc_done, 0xff, sizeof(long long) * NC, st) != cudaSuccess ||
+          cudaMemsetAsync(ncol, 0, sizeof(int), st) != cudaSuccess) {
+        pcy_set_error("live-column reset failed"); *rc = PCY_ECUDA; return false;
+      }
+      cols_reset = false;
+    }
     if (use_tc) {
       // tensor cores: split-TF32 dots against the reference slots.  The slots
       // keep their split (fixed engine centre, re-split only when a slot gets a
@@ -1379,21 +1417,21 @@ struct Engine {
         const long long acap = 1024, bcap = (NC + 127) / 128 * 128;
         if ((*rc = alloc(tc_ahi, acap * Kp)) || (*rc = alloc(tc_alo, acap * Kp)) || (*rc = alloc(tc_bhi, bcap * Kp)) ||
             (*rc = alloc(tc_blo, bcap * Kp)) || (*rc = alloc(tc_dots, acap * NC)) || (*rc = alloc(tc_rnc, NC)) ||
-            (*rc = alloc(tc_xn2, acap)) || (*rc = alloc(tc_c, (long long)Kp)) || (*rc = alloc(tc_done, NC)))
+            (*rc = alloc(tc_xn2, acap)) || (*rc = alloc(tc_c, (long long)Kp)))
           return false;
-        if (cudaMemsetAsync(tc_done, 0xff, sizeof(long long) * NC, st) != cudaSuccess ||
-            cudaMemsetAsync(tc_bhi, 0, sizeof(float) * bcap * Kp, st) != cudaSuccess ||
+        if (cudaMemsetAsync(tc_bhi, 0, sizeof(float) * bcap * Kp, st) != cudaSuccess ||
             cudaMemsetAsync(tc_blo, 0, sizeof(float) * bcap * Kp, st) != cudaSuccess) {
           pcy_set_error("tc buffer init failed"); *rc = PCY_ECUDA; return false;
         }
         if ((*rc = pcy_tc_center(A, aidx, ld, d, tc_c, st))) return false;   // the engine's centre
       }
       if ((*rc = pcy_tc_split(A, aidx, ld, d, M, nullptr, tc_c, tc_ahi, tc_alo, tc_xn2, st))) return false;
-      if ((*rc = pcy_tc_split_slots(E.r, ld, d, N, E.alive, E.idx, tc_done, tc_c, tc_bhi, tc_blo, tc_rnc, st)))
+      if ((*rc = pcy_tc_split_slots(E.r, ld, d, N, E.alive, E.idx, tc_done, tc_c, tc_bhi, tc_blo, tc_rnc,
+                                    const_cast<int*>(E.col_of), col_slot, ncol, st)))
         return false;
       const bool prof = pcy_prof_enabled();
       if (prof) PCY_CUDA(cudaEventRecord(ev[6], st));
-      if ((*rc = pcy_tc_dots(tc_ahi, tc_alo, 1024, (int)M, tc_bhi, tc_blo, (NC + 127) / 128 * 128, (int)N, nullptr,
+      if ((*rc = pcy_tc_dots(tc_ahi, tc_alo, 1024, (int)M, tc_bhi, tc_blo, (NC + 127) / 128 * 128, (int)N, ncol,
                              Kp, tc_dots, N, st)))
         return false;
       if (prof) { PCY_CUDA(cudaEventRecord(ev[7], st)); gemm_timed = true; gemm_flops = 2.0 * (double)M * (double)N * d; }
@@ -1403,8 +1441,11 @@ struct Engine {
     if (!parts) { if ((*rc = alloc(parts, (long long)1024 * NC))) return false; }
     const bool prof = pcy_prof_enabled();
     if (prof) { cudaEventRecord(ev[6], st); }
-    // columns = reference slots (dead slots give unused columns)
-    *rc = pcy_launch_parts(A, aidx, ld, (int)M, E.r, nullptr, ld, E.rn, (int)N, nullptr, d, parts, N, st);
+    // columns = live columns (B rows gathered through col_slot; CTAs past ncol exit)
+    k_assign_cols<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(E.alive, E.idx, N, tc_done, const_cast<int*>(E.col_of),
+                                                               col_slot, ncol);
+    pcy_count_launch();
+    *rc = pcy_launch_parts(A, aidx, ld, (int)M, E.r, col_slot, ld, E.rn, (int)N, ncol, d, parts, N, st);
     if (prof) { cudaEventRecord(ev[7], st); gemm_timed = true; gemm_flops = 2.0 * (double)M * (double)N * d; }
     return true;
   }
@@ -1497,6 +1538,7 @@ struct Engine {
         k_rb_reattach<<<1, 512, sizeof(double) * ld, st>>>(E, nodes); pcy_count_launch();
       }
       if (prof) PCY_CUDA(cudaEventRecord(ev[4], st));
+      cols_reset = true;   // merged nodes left dead columns
       PCY_LAUNCH_CHECK();
       rc = sync_ctl(st); if (rc) return rc;
       if (ctl_h->status == ST_ARENA) { pcy_set_error("member arena exhausted in rebuild"); return PCY_ESTATE; }

@@ -81,6 +81,9 @@ struct EngDev {
   // full-set K1 on the tensor cores (tc_dots.cu): 3xTF32 dots of the block
   // against every slot, centred norms and the error factor; null when unused
   const float* tc_dots; long long tc_ldo; const double* tc_rnc; const double* tc_xn2; double tc_tau;
+  // live columns of the full-set contraction: slot -> column (assigned when a
+  // slot first holds a node, recompacted after every rebuild)
+  const int* col_of;
   // column order of the full-set contraction: group g's members occupy the
   // contiguous columns [fs_gofs[g], fs_gofs[g] + g_count[g]) (fs_list = slots)
   int* fs_list; int* fs_gofs; int* fs_cnt;

@@ -34,7 +34,7 @@ __global__ void k_rchain(EngDev E, const int* __restrict__ order, long long n, C
     if (E.tc_dots)   // tensor-core dots + near-tie recheck
       scan_parts_tc(E, i, g, E.arena + base, cnt, [&](int jj) { return warp_dot(E.r + (long long)jj * ld, xv, d, lane); },
                     lane, bp, bpos, nre);
-    else if (P) scan_parts(P + i * ldp, E.arena + base, cnt, lane, bp, bpos);   // parts from the DMMA contraction
+    else if (P) scan_parts(P + i * ldp, E.col_of, E.arena + base, cnt, lane, bp, bpos);   // parts from the DMMA contraction
     else scan_members(E, E.arena + base, 0, cnt, xv, lane, bp, bpos);
     const int j = bpos < cnt ? E.arena[base + bpos] : -1;
     ChainLvl c = empty_level();

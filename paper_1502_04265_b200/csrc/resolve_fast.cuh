@@ -101,7 +101,7 @@ __global__ void k_chain2(EngDev E, const double* __restrict__ X, const double* _
         scan_parts_tc_cta<WPI>(E, i, E.arena + base, cnt, [&](int jj) { return xdot(E.r + (long long)jj * ld); },
                                lane, wib, red, reinterpret_cast<int*>(red + 8), bp, bpos, nre);
     }
-    else if (P) scan_parts(P + i * ldp, E.arena + base, cnt, lane, bp, bpos);   // DMMA parts
+    else if (P) scan_parts(P + i * ldp, E.col_of, E.arena + base, cnt, lane, bp, bpos);   // DMMA parts
     else scan_members(E, E.arena + base, 0, cnt, xv, lane, bp, bpos);
     const int j = bpos < cnt ? E.arena[base + bpos] : -1;
     ChainLvl c = empty_level();

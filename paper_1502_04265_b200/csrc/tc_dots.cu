@@ -234,13 +234,17 @@ __global__ void k_tc_split(const double* __restrict__ src, const int* __restrict
 __global__ void k_tc_split_slots(const double* __restrict__ src, long long ld, int d, long long nslots,
                                  const int* __restrict__ alive, const long long* __restrict__ cidx,
                                  long long* __restrict__ done_idx, const double* __restrict__ center, int Kp,
-                                 float* __restrict__ hi, float* __restrict__ lo, double* __restrict__ nrm2) {
+                                 float* __restrict__ hi, float* __restrict__ lo, double* __restrict__ nrm2,
+                                 int* __restrict__ col_of, int* __restrict__ col_slot, int* __restrict__ ncol) {
   const int lane = threadIdx.x & 31;
   const long long i = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (i >= nslots || !alive[i] || done_idx[i] == cidx[i]) return;
+  int c = 0;
+  if (lane == 0) c = atomicAdd(ncol, 1);   // column order is free: a dot does not depend on its column
+  c = __shfl_sync(PCY_FULL, c, 0);
   const double* x = src + i * ld;
-  float* h = hi + i * Kp;
-  float* l = lo + i * Kp;
+  float* h = hi + (long long)c * Kp;
+  float* l = lo + (long long)c * Kp;
   double acc = 0.0;
   for (int k = lane; k < Kp; k += 32) {
     const double v = k < d ? x[k] - center[k] : 0.0;
@@ -251,7 +255,7 @@ __global__ void k_tc_split_slots(const double* __restrict__ src, long long ld, i
     acc = fma(v, v, acc);
   }
   acc = warp_sum(acc);
-  if (lane == 0) { nrm2[i] = acc; done_idx[i] = cidx[i]; }
+  if (lane == 0) { nrm2[i] = acc; done_idx[i] = cidx[i]; col_of[i] = c; col_slot[c] = (int)i; }
 }
 
 __global__ void k_copy_row(const double* __restrict__ src, const int* __restrict__ idx, long long ld, int d,
@@ -324,11 +328,11 @@ int pcy_tc_split(const double* src, const int* idx, long long ld, int d, long lo
 
 int pcy_tc_split_slots(const double* src, long long ld, int d, long long nslots, const int* alive,
                        const long long* cidx, long long* done_idx, const double* center, float* hi, float* lo,
-                       double* nrm2, cudaStream_t st) {
+                       double* nrm2, int* col_of, int* col_slot, int* ncol, cudaStream_t st) {
   if (nslots <= 0) return PCY_OK;
   const int Kp = pcy_tc_pad(d);
   k_tc_split_slots<<<(unsigned)((nslots + 7) / 8), 256, 0, st>>>(src, ld, d, nslots, alive, cidx, done_idx, center, Kp,
-                                                                 hi, lo, nrm2);
+                                                                 hi, lo, nrm2, col_of, col_slot, ncol);
   pcy_count_launch();
   PCY_LAUNCH_CHECK();
   return PCY_OK;
