@@ -46,7 +46,8 @@ template <class T>
 inline cudaError_t pcy_malloc_async(T** p, size_t bytes, cudaStream_t st) {
   return pcy_malloc_async_raw((void**)p, bytes, st);
 }
-// DMMA distance contraction (distance.cu)
+// DMMA distance contraction (distance.cu).  pcy_launch_gram of a block with
+// itself (A == B) computes only the lower triangle (column <= row).
 int pcy_launch_gram(const double* A, const int* aidx, long long lda, int M, const double* B, const int* bidx,
                     long long ldb, int N, int K, double* C, long long ldc, cudaStream_t st);
 int pcy_launch_parts(const double* A, const int* aidx, long long lda, int M, const double* B, const int* bidx,

@@ -27,7 +27,7 @@ __global__ void __launch_bounds__(128) k_dist_tile(int M, int N, int K,
                                                   double* __restrict__ C, long long ldc,
                                                   double* __restrict__ ppart, int* __restrict__ ppos, int ntiles,
                                                   const int* __restrict__ n_dev = nullptr,
-                                                  const double* __restrict__ rv = nullptr) {
+                                                  const double* __restrict__ rv = nullptr, int lower = 0) {
   __shared__ double As[2][DBM][DBK + 4];
   __shared__ double Bs[2][DBK][DBN + 4];
   __shared__ long long arow[DBM], brow[DBN];
@@ -38,6 +38,7 @@ __global__ void __launch_bounds__(128) k_dist_tile(int M, int N, int K,
   const int g = lane >> 2, t4 = lane & 3;
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
   const int m0 = blockIdx.y * DBM, n0 = blockIdx.x * DBN;
+  if (lower && n0 > m0) return;   // tile strictly above the diagonal (DBM == DBN)
   if (n_dev) { N = min(N, *n_dev); if (n0 >= N) return; }
   if (tid < DBM) {
     const int m = m0 + tid;
@@ -177,7 +178,10 @@ int pcy_launch_gram(const double* A, const int* aidx, long long lda, int M, cons
                     long long ldb, int N, int K, double* C, long long ldc, cudaStream_t st) {
   if (M <= 0 || N <= 0) return PCY_OK;
   dim3 grid((unsigned)((N + DBN - 1) / DBN), (unsigned)((M + DBM - 1) / DBM));
-  k_dist_tile<0><<<grid, 128, 0, st>>>(M, N, K, A, aidx, lda, B, bidx, ldb, nullptr, C, ldc, nullptr, nullptr, 0);
+  // only the tiles on or below the diagonal: the engine's batch Grams are
+  // symmetric and read at (later item, earlier item) only
+  k_dist_tile<0><<<grid, 128, 0, st>>>(M, N, K, A, aidx, lda, B, bidx, ldb, nullptr, C, ldc, nullptr, nullptr, 0,
+                                       nullptr, nullptr, A == B && aidx == bidx && M == N ? 1 : 0);
   pcy_count_launch();
   PCY_LAUNCH_CHECK();
   return PCY_OK;

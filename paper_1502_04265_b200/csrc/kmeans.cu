@@ -109,6 +109,86 @@ __device__ int chunk_draw(const double* __restrict__ part, long long nch, const 
   return r == 0x7fffffff ? (int)(n - 1) : r;
 }
 
+// Diff-form squared distances (evaluation.py:74-75, :80-81) of two point
+// rows pa, pb to the rn staged centres cs (rn x d), lane partial sums in
+// acc[row][centre].  Even d: 128-bit loads, 8 pairs in flight per row and
+// lane; odd d: 8 elements per row and lane.
+__device__ __forceinline__ void seed_rows2(const double* __restrict__ pa, const double* __restrict__ pb,
+                                           const double* cs, int d, int rn, int lane, double (&acc)[2][KS_RMAX]) {
+#pragma unroll
+  for (int q = 0; q < KS_RMAX; ++q) { acc[0][q] = 0.0; acc[1][q] = 0.0; }
+  if ((d & 1) == 0) {
+    const double2* a2 = reinterpret_cast<const double2*>(pa);
+    const double2* b2 = reinterpret_cast<const double2*>(pb);
+    const int d2 = d >> 1;
+    int e2 = lane;
+    for (; e2 + 7 * 32 < d2; e2 += 8 * 32) {
+      double2 av[8], bv[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) { av[t] = a2[e2 + 32 * t]; bv[t] = b2[e2 + 32 * t]; }
+#pragma unroll
+      for (int q = 0; q < KS_RMAX; ++q)
+        if (q < rn) {
+          const double2* cq = reinterpret_cast<const double2*>(cs + (long long)q * d) + e2;
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const double2 cv = cq[32 * t];
+            double dx = rsub(av[t].x, cv.x), dy = rsub(av[t].y, cv.y);
+            acc[0][q] = fma(dx, dx, acc[0][q]);
+            acc[0][q] = fma(dy, dy, acc[0][q]);
+            dx = rsub(bv[t].x, cv.x); dy = rsub(bv[t].y, cv.y);
+            acc[1][q] = fma(dx, dx, acc[1][q]);
+            acc[1][q] = fma(dy, dy, acc[1][q]);
+          }
+        }
+    }
+    for (int t = e2; t < d2; t += 32) {
+      const double2 av = a2[t], bv = b2[t];
+#pragma unroll
+      for (int q = 0; q < KS_RMAX; ++q)
+        if (q < rn) {
+          const double2 cv = reinterpret_cast<const double2*>(cs + (long long)q * d)[t];
+          double dx = rsub(av.x, cv.x), dy = rsub(av.y, cv.y);
+          acc[0][q] = fma(dx, dx, acc[0][q]);
+          acc[0][q] = fma(dy, dy, acc[0][q]);
+          dx = rsub(bv.x, cv.x); dy = rsub(bv.y, cv.y);
+          acc[1][q] = fma(dx, dx, acc[1][q]);
+          acc[1][q] = fma(dy, dy, acc[1][q]);
+        }
+    }
+    return;
+  }
+  int e = lane;
+  for (; e + 7 * 32 < d; e += 8 * 32) {
+    double av[8], bv[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) { av[t] = pa[e + 32 * t]; bv[t] = pb[e + 32 * t]; }
+#pragma unroll
+    for (int q = 0; q < KS_RMAX; ++q)
+      if (q < rn) {
+        const double* cq = cs + (long long)q * d + e;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const double c = cq[32 * t];
+          const double da = rsub(av[t], c), db = rsub(bv[t], c);
+          acc[0][q] = fma(da, da, acc[0][q]);
+          acc[1][q] = fma(db, db, acc[1][q]);
+        }
+      }
+  }
+  for (; e < d; e += 32) {
+    const double av = pa[e], bv = pb[e];
+#pragma unroll
+    for (int q = 0; q < KS_RMAX; ++q)
+      if (q < rn) {
+        const double c = cs[(long long)q * d + e];
+        const double da = rsub(av, c), db = rsub(bv, c);
+        acc[0][q] = fma(da, da, acc[0][q]);
+        acc[1][q] = fma(db, db, acc[1][q]);
+      }
+  }
+}
+
 __global__ void __launch_bounds__(KS_THREADS) k_seed_coop(const double* __restrict__ P, const double* __restrict__ w,
                                                          long long n, int d, int k, int reps,
                                                          const double* __restrict__ U, double* __restrict__ centers,
@@ -163,79 +243,29 @@ __global__ void __launch_bounds__(KS_THREADS) k_seed_coop(const double* __restri
       __syncthreads();
       for (long long c = blockIdx.x; c < nch; c += gridDim.x) {
         const long long p0 = c * KS_CHUNK, p1 = min(n, p0 + KS_CHUNK);
-        for (long long i = p0 + warp; i < p1; i += nwarp) {
-          const double* p = P + i * d;
-          double acc[KS_RMAX];
+        // two rows per warp: every centre element read from shared memory
+        // serves both rows, and twice the row bytes are in flight
+        for (long long i = p0 + warp; i < p1; i += 2 * nwarp) {
+          const long long ib = i + nwarp < p1 ? i + nwarp : -1;
+          double acc[2][KS_RMAX];
+          seed_rows2(P + i * d, P + (ib >= 0 ? ib : i) * d, cs, d, rn, lane, acc);
 #pragma unroll
-          for (int q = 0; q < KS_RMAX; ++q) acc[q] = 0.0;
-          int e = lane;
-          if ((d & 1) == 0) {
-            // even d (16-byte rows): 16 row elements in flight per lane as
-            // 128-bit loads, element pairs (2l, 2l+1) + 64 t
-            const double2* p2 = reinterpret_cast<const double2*>(p);
-            const int d2 = d >> 1;
-            int e2 = lane;
-            for (; e2 + 7 * 32 < d2; e2 += 8 * 32) {
-              double2 pv[8];
+          for (int h = 0; h < 2; ++h) {
+            const long long ii = h == 0 ? i : ib;
+            if (ii < 0) break;
 #pragma unroll
-              for (int t = 0; t < 8; ++t) pv[t] = p2[e2 + 32 * t];
-#pragma unroll
-              for (int q = 0; q < KS_RMAX; ++q)
-                if (q < rn) {
-                  const double2* cq = reinterpret_cast<const double2*>(cs + (long long)q * d) + e2;
-#pragma unroll
-                  for (int t = 0; t < 8; ++t) {
-                    const double2 cv = cq[32 * t];
-                    const double dx = rsub(pv[t].x, cv.x), dy = rsub(pv[t].y, cv.y);
-                    acc[q] = fma(dx, dx, acc[q]);
-                    acc[q] = fma(dy, dy, acc[q]);
-                  }
-                }
-            }
-            for (int t = e2; t < d2; t += 32) {
-              const double2 pv = p2[t];
-#pragma unroll
-              for (int q = 0; q < KS_RMAX; ++q)
-                if (q < rn) {
-                  const double2 cv = reinterpret_cast<const double2*>(cs + (long long)q * d)[t];
-                  const double dx = rsub(pv.x, cv.x), dy = rsub(pv.y, cv.y);
-                  acc[q] = fma(dx, dx, acc[q]);
-                  acc[q] = fma(dy, dy, acc[q]);
-                }
-            }
-            e = d;   // done
-          }
-          // odd d: 8 row elements in flight per lane, lane-strided
-          for (; e + 7 * 32 < d; e += 8 * 32) {
-            double pv[8];
-#pragma unroll
-            for (int t = 0; t < 8; ++t) pv[t] = p[e + 32 * t];
-#pragma unroll
-            for (int q = 0; q < KS_RMAX; ++q)
-              if (q < rn) {
-                const double* cq = cs + (long long)q * d + e;
-#pragma unroll
-                for (int t = 0; t < 8; ++t) { const double df = rsub(pv[t], cq[32 * t]); acc[q] = fma(df, df, acc[q]); }
+            for (int q = 0; q < KS_RMAX; ++q) {
+              if (q >= rn) break;
+              const double a = warp_sum(acc[h][q]);
+              if (lane == 0) {
+                const int r = r0 + q;
+                double* best = best_all + (long long)r * n;
+                const double b = j == 0 ? a : fmin(best[ii], a);
+                best[ii] = b;
+                const double mv = rmul(w[ii], b);
+                mass_all[(long long)r * n + ii] = mv;
+                ms[q * KS_CHUNK + (int)(ii - p0)] = mv;
               }
-          }
-          for (; e < d; e += 32) {
-            const double pe = p[e];
-#pragma unroll
-            for (int q = 0; q < KS_RMAX; ++q)
-              if (q < rn) { const double df = rsub(pe, cs[(long long)q * d + e]); acc[q] = fma(df, df, acc[q]); }
-          }
-#pragma unroll
-          for (int q = 0; q < KS_RMAX; ++q) {
-            if (q >= rn) break;
-            const double a = warp_sum(acc[q]);
-            if (lane == 0) {
-              const int r = r0 + q;
-              double* best = best_all + (long long)r * n;
-              const double b = j == 0 ? a : fmin(best[i], a);
-              best[i] = b;
-              const double mv = rmul(w[i], b);
-              mass_all[(long long)r * n + i] = mv;
-              ms[q * KS_CHUNK + (int)(i - p0)] = mv;
             }
           }
         }

@@ -210,7 +210,8 @@ __device__ __forceinline__ void scan_new(const EngDev& E, const ResolveSmemT<MS>
     for (int c0 = 0; c0 < nnew; c0 += 32) {
       const int t = c0 + lane;
       if (t < nnew && S.tgrp[t] == g) {
-        const double part = radd(S.trn[t], rmul(gram[(long long)S.titem[t] * gld + gq], -2.0));
+        // (current item, earlier item): the lower triangle pcy_launch_gram computes
+        const double part = radd(S.trn[t], rmul(gram[gq * gld + S.titem[t]], -2.0));
         if (part < np_) { np_ = part; nt = t; }
       }
     }

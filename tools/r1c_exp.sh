@@ -9,4 +9,5 @@ for c in "cfg2 581012" "cfg1 20000" "cfg3 200000" "cfg5 125000"; do
   PCY_DEBUG_REBUILD=1 PCY_TRACE_K3=gpurun_out/${tag}_trace_$1.txt timeout 600 python tools/probe_cfg.py $1 $2 > gpurun_out/${tag}_$1.log 2>&1; echo "$1 rc=$?"
   grep -v "reattach launch" gpurun_out/${tag}_$1.log | tail -3
 done
+timeout 300 python tools/probe_kmeans.py 25000 4096 250 5 20 > gpurun_out/${tag}_km.log 2>&1; echo "km rc=$?"; tail -4 gpurun_out/${tag}_km.log
 gzip -f gpurun_out/${tag}_trace_*.txt
