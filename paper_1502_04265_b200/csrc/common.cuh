@@ -50,6 +50,10 @@ inline cudaError_t pcy_malloc_async(T** p, size_t bytes, cudaStream_t st) {
 // itself (A == B) computes only the lower triangle (column <= row).
 int pcy_launch_gram(const double* A, const int* aidx, long long lda, int M, const double* B, const int* bidx,
                     long long ldb, int N, int K, double* C, long long ldc, cudaStream_t st);
+// the same self-Gram (lower triangle) with K split over S slices (scratch:
+// S x M x ldc doubles), partials summed in slice order
+int pcy_launch_gram_split(const double* A, const int* aidx, long long lda, int M, int K, double* C, long long ldc,
+                          double* scratch, int S, cudaStream_t st);
 int pcy_launch_parts(const double* A, const int* aidx, long long lda, int M, const double* B, const int* bidx,
                      long long ldb, const double* rn, int N, const int* n_dev, int K, double* C, long long ldc,
                      cudaStream_t st);

@@ -27,7 +27,8 @@ __global__ void __launch_bounds__(128) k_dist_tile(int M, int N, int K,
                                                   double* __restrict__ C, long long ldc,
                                                   double* __restrict__ ppart, int* __restrict__ ppos, int ntiles,
                                                   const int* __restrict__ n_dev = nullptr,
-                                                  const double* __restrict__ rv = nullptr, int lower = 0) {
+                                                  const double* __restrict__ rv = nullptr, int lower = 0,
+                                                  int kslice = 0, long long cstride = 0) {
   __shared__ double As[2][DBM][DBK + 4];
   __shared__ double Bs[2][DBK][DBN + 4];
   __shared__ long long arow[DBM], brow[DBN];
@@ -39,6 +40,10 @@ __global__ void __launch_bounds__(128) k_dist_tile(int M, int N, int K,
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
   const int m0 = blockIdx.y * DBM, n0 = blockIdx.x * DBN;
   if (lower && n0 > m0) return;   // tile strictly above the diagonal (DBM == DBN)
+  if (kslice > 0) {   // split K: slice blockIdx.z of the contraction into partial z of C
+    const int kb = blockIdx.z * kslice;
+    A += kb; B += kb; K = min(kslice, K - kb); C += blockIdx.z * cstride;
+  }
   if (n_dev) { N = min(N, *n_dev); if (n0 >= N) return; }
   if (tid < DBM) {
     const int m = m0 + tid;
@@ -157,6 +162,20 @@ __global__ void __launch_bounds__(128) k_dist_tile(int M, int N, int K,
 }
 
 // per row: argmin over tiles (positions increase with the tile index)
+// Sum of the split-K partials in slice order (fixed order: deterministic), on
+// and below the diagonal.
+__global__ void k_gram_sum(const double* __restrict__ part, int S, long long pstride, int M, double* __restrict__ C,
+                           long long ldc) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (long long)M * M) return;
+  const int m = (int)(e / M), n = (int)(e % M);
+  if (n > m) return;
+  const long long o = (long long)m * ldc + n;
+  double v = part[o];
+  for (int z = 1; z < S; ++z) v += part[z * pstride + o];
+  C[o] = v;
+}
+
 __global__ void k_argmin_reduce(int M, int ntiles, const double* __restrict__ ppart, const int* __restrict__ ppos,
                                 int* __restrict__ out_pos, double* __restrict__ out_part) {
   const int lane = threadIdx.x & 31;
@@ -182,6 +201,28 @@ int pcy_launch_gram(const double* A, const int* aidx, long long lda, int M, cons
   // symmetric and read at (later item, earlier item) only
   k_dist_tile<0><<<grid, 128, 0, st>>>(M, N, K, A, aidx, lda, B, bidx, ldb, nullptr, C, ldc, nullptr, nullptr, 0,
                                        nullptr, nullptr, A == B && aidx == bidx && M == N ? 1 : 0);
+  pcy_count_launch();
+  PCY_LAUNCH_CHECK();
+  return PCY_OK;
+}
+
+// Self-Gram of a block (lower triangle) with K split over S slices: a tile's
+// K loop is latency-bound at large d (one stage of loads ahead), so S slices
+// run S times more tiles at once; the partials (scratch, S x M x ldc) are
+// summed in slice order.
+int pcy_launch_gram_split(const double* A, const int* aidx, long long lda, int M, int K, double* C, long long ldc,
+                          double* scratch, int S, cudaStream_t st) {
+  if (M <= 0) return PCY_OK;
+  int kslice = (K + S - 1) / S;
+  kslice = (kslice + DBK - 1) / DBK * DBK;
+  S = (K + kslice - 1) / kslice;
+  if (S <= 1 || !scratch) return pcy_launch_gram(A, aidx, lda, M, A, aidx, lda, M, K, C, ldc, st);
+  const long long pstride = (long long)M * ldc;
+  dim3 grid((unsigned)((M + DBN - 1) / DBN), (unsigned)((M + DBM - 1) / DBM), (unsigned)S);
+  k_dist_tile<0><<<grid, 128, 0, st>>>(M, M, K, A, aidx, lda, A, aidx, lda, nullptr, scratch, ldc, nullptr, nullptr, 0,
+                                       nullptr, nullptr, 1, kslice, pstride);
+  pcy_count_launch();
+  k_gram_sum<<<(unsigned)(((long long)M * M + 255) / 256), 256, 0, st>>>(scratch, S, pstride, M, C, ldc);
   pcy_count_launch();
   PCY_LAUNCH_CHECK();
   return PCY_OK;

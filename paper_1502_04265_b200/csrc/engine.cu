@@ -1185,6 +1185,8 @@ struct Engine {
   ChainLvl* chr = nullptr;
   double* parts = nullptr;                             // full-set parts matrix (1024 x NC)
   double* gram = nullptr;                              // block Gram (K3 with rows in HBM)
+  double* gram_part = nullptr;                         // split-K partials of the block Gram (large d)
+  int gram_split = 1;
   bool use_tc = false;                                 // full-set K1 on tcgen05 (split TF32 + recheck)
   int Kp = 0;
   double tc_tau = 0.0;
@@ -1284,6 +1286,8 @@ struct Engine {
     A_(E.ch_node, Bmax * PCY_MAXL); A_(E.ch_part, Bmax * PCY_MAXL); A_(E.ch_len, Bmax);
     A_(chh, Bmax); A_(chr, Bmax * PCY_FMAXL);
     A_(gram, (long long)1024 * 1024);
+    gram_split = d >= 2048 ? 8 : d >= 512 ? 4 : 1;   // K slices of >= 128-512 elements
+    if (gram_split > 1) A_(gram_part, (long long)gram_split * 1024 * 1024);
     E.pend_cap = m + 2;
     A_(E.pend_x, E.pend_cap * ld); A_(E.pend_w, E.pend_cap); A_(E.pend_xsq, E.pend_cap);
     A_(E.dist_x, (m + 2) * ld);
@@ -1486,13 +1490,13 @@ struct Engine {
           k_rchain<<<(unsigned)((nb + wpc - 1) / wpc), wpc * 32, sizeof(double) * wpc * ld, st>>>(
               E, E.order + off, nb, chh, chr, use_p ? parts : nullptr, ctl_h->F_alloc); pcy_count_launch();
           if (nper == 101) {
-            grc = pcy_launch_gram(E.r, E.order + off, ld, (int)nb, E.r, E.order + off, ld, (int)nb, d, gram, nb, st);
+            grc = pcy_launch_gram_split(E.r, E.order + off, ld, (int)nb, d, gram, nb, gram_part, gram_split, st);
             if (grc) return grc;
           }
           ParCtl* pp = nullptr;
           if (k3par) {
             if (nper != 101) {   // opener rows against the batch (k_plan's conflict test)
-              grc = pcy_launch_gram(E.r, E.order + off, ld, (int)nb, E.r, E.order + off, ld, (int)nb, d, gram, nb, st);
+              grc = pcy_launch_gram_split(E.r, E.order + off, ld, (int)nb, d, gram, nb, gram_part, gram_split, st);
               if (grc) return grc;
             }
             k_plan<<<1, PCY_PAR_MAXITEMS, plan_smem, st>>>(E, nullptr, nullptr, nullptr, nb, -1, nper <= 8 ? rea_cap : nnew_cap,
@@ -1589,8 +1593,7 @@ struct Engine {
                                                                           use_p ? parts : nullptr, ctl_h->F_alloc);
           pcy_count_launch();
           if (nper == 101) {
-            rc0 = pcy_launch_gram(Xs, nullptr, ld, (int)(kn), Xs, nullptr, ld, (int)(kn), d, gram,
-                                  kn, st);
+            rc0 = pcy_launch_gram_split(Xs, nullptr, ld, (int)(kn), d, gram, kn, gram_part, gram_split, st);
             if (rc0) return rc0;
           }
         } else {
@@ -1604,7 +1607,7 @@ struct Engine {
           // k_plan picks a subtree-parallel window or a sequential stretch; the
           // launch that was not chosen returns at once
           if (nper != 101) {   // opener rows against the batch (k_plan's conflict test)
-            const int grc = pcy_launch_gram(Xs, nullptr, ld, (int)kn, Xs, nullptr, ld, (int)kn, d, gram, kn, rs);
+            const int grc = pcy_launch_gram_split(Xs, nullptr, ld, (int)kn, d, gram, kn, gram_part, gram_split, rs);
             if (grc) return grc;
           }
           k_plan<<<1, PCY_PAR_MAXITEMS, plan_smem, rs>>>(E, XSs, Ws, Bs, kn, first_rem, nnew_cap, 16, chh, chr, parctl,

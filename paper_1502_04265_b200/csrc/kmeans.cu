@@ -58,55 +58,84 @@ __device__ __forceinline__ double block_exscan(double v, double* red, double* to
   return red[32 + wid] + (inc - v);
 }
 
-// Cooperative k-means++ (all repetitions in one persistent launch).  Points
-// are split into chunks of KS_CHUNK in index order; the cumulative mass of
-// point i is  sum(chunk totals before its chunk) + sum(masses in its chunk up
-// to i), every sum in a fixed order, so the draw is deterministic.
-//   phase A (all CTAs, one chunk per CTA iteration, warp per point): the
-//     diff-form distance of each point to every repetition's newest centre
-//     (:74-75, :80-81), best = min(best, dist), mass = w * best, chunk totals;
-//     each point row is read once for all repetitions (the HBM-bound pass)
-//   phase B (CTA r < reps): _draw (:49-53) of repetition r from the chunk
-//     totals, falling back to the weights when the mass is all zero (:77-78),
-//     and the pick copied into the centre list.
-constexpr int KS_THREADS = 512, KS_CHUNK = 32, KS_RMAX = 8;
+// Cooperative k-means++ (all repetitions in one persistent launch).  CTA c
+// of the G CTAs owns the rows [c n / G, (c+1) n / G) (equal ranges: every SM
+// streams the same number of rows, no tail wave).  The cumulative mass of
+// point i is  sum(range totals before its range) + running sum within its
+// range up to i, every sum in a fixed order, so the draw is deterministic.
+// Per centre:
+//   draw (every CTA, one warp per repetition, identical results): _draw
+//     (:49-53) from the range totals, falling back to the weights when the
+//     mass is all zero (:77-78); CTA 0 records the picks and centre rows;
+//   distance pass (all CTAs, two rows per warp): the diff-form distance of
+//     each point to every repetition's newest centre (:74-75, :80-81), best =
+//     min(best, dist), mass = w * best, the range totals; each point row is
+//     read from HBM once for all repetitions (the HBM-bound pass);
+// and one grid barrier.
+constexpr int KS_THREADS = 512, KS_RMAX = 8;
 
-__device__ int chunk_draw(const double* __restrict__ part, long long nch, const double* __restrict__ vals,
-                          long long n, double u, double* red, int* ired, double* s_tot) {
-  // prefix over chunk totals: thread t owns a contiguous run of chunks
-  const long long per = (nch + blockDim.x - 1) / blockDim.x;
-  const long long a = (long long)threadIdx.x * per, b = min(nch, a + per);
-  double loc = 0.0;
-  for (long long c = a; c < b; ++c) loc += part[c];
-  double total;
-  const double pre = block_exscan(loc, red, &total);
-  if (threadIdx.x == 0) *s_tot = total;
-  const double target = rmul(u, total);
-  long long cand = 0x7fffffffffffLL;
-  double cum = pre;
-  for (long long c = a; c < b; ++c) {
-    if (cum + part[c] > target) {
-      // inside chunk c: sequential over its points
-      const long long p0 = c * KS_CHUNK, p1 = min(n, p0 + KS_CHUNK);
-      double cc = cum;
-      for (long long i = p0; i < p1; ++i) {
-        cc += vals[i];
-        if (cc > target) { cand = i; break; }
-      }
-      if (cand != 0x7fffffffffffLL) break;
-    }
-    cum += part[c];
-  }
-  long long v = cand;
+__device__ __forceinline__ long long ks_lo(long long n, int c, int G) { return n * c / G; }
+
+// Fixed-order total of vals[p0, p1): 32-element blocks, each an inclusive
+// warp scan, added in block order -- the association warp_draw's in-range
+// search uses, so the draw's running sum reaches exactly prefix + total at
+// the end of a range.
+__device__ __forceinline__ double warp_scan32(double v, int lane) {
 #pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) v = min(v, __shfl_xor_sync(PCY_FULL, v, o));
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) ired[threadIdx.x >> 5] = (int)min(v, (long long)0x7fffffff);
-  __syncthreads();
-  int r = 0x7fffffff;
-  for (int k = 0; k < (int)(blockDim.x >> 5); ++k) r = min(r, ired[k]);
-  __syncthreads();
-  return r == 0x7fffffff ? (int)(n - 1) : r;
+  for (int o = 1; o < 32; o <<= 1) {
+    const double t = __shfl_up_sync(PCY_FULL, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+__device__ double warp_range_total(const double* vals, long long p0, long long p1, int lane) {
+  double tb = 0.0;
+  for (long long b0 = p0; b0 < p1; b0 += 32) {
+    const long long i = b0 + lane;
+    const double v = warp_scan32(i < p1 ? __ldcg(vals + i) : 0.0, lane);
+    tb = tb + __shfl_sync(PCY_FULL, v, 31);
+  }
+  return tb;
+}
+
+// Warp form of _draw (evaluation.py:49-53) over the G range totals `part`
+// and the point values `vals`: the first i whose cumulative sum exceeds
+// u * total, clamped to n - 1.  *total_out receives the grand total (lane-
+// contiguous runs of range totals, then the warp scan).
+__device__ long long warp_draw(const double* part, int G, const double* __restrict__ vals, long long n, double u,
+                               int lane, double* total_out) {
+  const int per = (G + 31) / 32;
+  const int a = lane * per, b = min(G, a + per);
+  double loc = 0.0;
+  for (int c = a; c < b; ++c) loc += __ldcg(part + c);
+  const double inc = warp_scan32(loc, lane);
+  const double total = __shfl_sync(PCY_FULL, inc, 31);
+  *total_out = total;
+  const double target = rmul(u, total);
+  // the range holding the target: first c (lane order = range order)
+  int cfound = 0x7fffffff;
+  double cum = inc - loc, cstart = 0.0;
+  for (int c = a; c < b; ++c) {
+    const double pc = __ldcg(part + c);
+    if (cum + pc > target) { cfound = c; cstart = cum; break; }
+    cum += pc;
+  }
+  const unsigned hit = __ballot_sync(PCY_FULL, cfound != 0x7fffffff);
+  if (!hit) return n - 1;
+  const int src = __ffs(hit) - 1;
+  const int cs = __shfl_sync(PCY_FULL, cfound, src);
+  cum = __shfl_sync(PCY_FULL, cstart, src);
+  // in-range search, in the association of warp_range_total
+  const long long p0 = ks_lo(n, cs, G), p1 = ks_lo(n, cs + 1, G);
+  double tb = 0.0;
+  for (long long b0 = p0; b0 < p1; b0 += 32) {
+    const long long i = b0 + lane;
+    const double v = warp_scan32(i < p1 ? __ldcg(vals + i) : 0.0, lane);
+    const unsigned over = __ballot_sync(PCY_FULL, i < p1 && cum + (tb + v) > target);
+    if (over) return b0 + __ffs(over) - 1;
+    tb = tb + __shfl_sync(PCY_FULL, v, 31);
+  }
+  return p1 - 1 < n - 1 ? p1 - 1 : n - 1;   // rounding guard: the range end
 }
 
 // Diff-form squared distances (evaluation.py:74-75, :80-81) of two point
@@ -198,85 +227,84 @@ __global__ void __launch_bounds__(KS_THREADS) k_seed_coop(const double* __restri
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double ks_smem[];
   double* cs = ks_smem;                          // rg x d newest centres
-  double* ms = ks_smem + (long long)rg * d;      // rg x KS_CHUNK chunk masses
-  __shared__ double red[72];
-  __shared__ int ired[32];
-  __shared__ double s_tot;
+  __shared__ long long s_idx[64];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = KS_THREADS / 32;
-  const long long nch = (n + KS_CHUNK - 1) / KS_CHUNK;
-  // weight chunk totals (the fallback / first draw), fixed order
-  for (long long c = blockIdx.x; c < nch; c += gridDim.x) {
-    if (threadIdx.x == 0) {
-      double t = 0.0;
-      for (long long i = c * KS_CHUNK; i < min(n, (c + 1) * KS_CHUNK); ++i) t += w[i];
-      wpart[c] = t;
-    }
+  const int G = gridDim.x, c = blockIdx.x;
+  const long long p0 = ks_lo(n, c, G), p1 = ks_lo(n, c + 1, G);
+  // weight range totals (the first draw / fallback), fixed order
+  if (warp == 0) {
+    const double t = warp_range_total(w, p0, p1, lane);
+    if (lane == 0) wpart[c] = t;
   }
   grid.sync();
   for (int j = 0; j < k; ++j) {
-    // phase B: draw centre j of every repetition
-    for (int r = blockIdx.x; r < reps; r += gridDim.x) {
-      int idx;
+    // masses and range totals alternate between two buffers: centre j reads
+    // those of centre j - 1 while faster CTAs already write centre j's
+    const long long mstride = (long long)reps * n, pstride = (long long)reps * G;
+    const double* mass_r = mass_all + ((j - 1) & 1) * mstride;
+    const double* part_r = part_all + ((j - 1) & 1) * pstride;
+    double* mass_w = mass_all + (j & 1) * mstride;
+    double* part_w = part_all + (j & 1) * pstride;
+    // draw centre j of every repetition, redundantly in every CTA
+    for (int r = warp; r < reps; r += nwarp) {
+      const double u = U[(long long)r * k + j];
+      double tot = 0.0;
+      long long idx;
       if (j == 0) {
-        idx = chunk_draw(wpart, nch, w, n, U[(long long)r * k], red, ired, &s_tot);
+        idx = warp_draw(wpart, G, w, n, u, lane, &tot);
       } else {
-        const double* part = part_all + (long long)r * nch;
-        idx = chunk_draw(part, nch, mass_all + (long long)r * n, n, U[(long long)r * k + j], red, ired, &s_tot);
-        __syncthreads();
-        if (!(s_tot > 0.0)) idx = chunk_draw(wpart, nch, w, n, U[(long long)r * k + j], red, ired, &s_tot);
+        idx = warp_draw(part_r + (long long)r * G, G, mass_r + (long long)r * n, n, u, lane, &tot);
+        if (!(tot > 0.0)) idx = warp_draw(wpart, G, w, n, u, lane, &tot);
       }
-      if (threadIdx.x == 0) picks[r * k + j] = idx;
-      double* C = centers + ((long long)r * k + j) * d;
-      for (int e = threadIdx.x; e < d; e += blockDim.x) C[e] = P[(long long)idx * d + e];
-      __syncthreads();
+      if (lane == 0) {
+        s_idx[r] = idx;
+        if (c == 0) picks[r * k + j] = (int)idx;
+      }
     }
+    __syncthreads();
+    if (c == 0)
+      for (int r = 0; r < reps; ++r) {
+        double* C = centers + ((long long)r * k + j) * d;
+        for (int e = threadIdx.x; e < d; e += blockDim.x) C[e] = P[s_idx[r] * d + e];
+      }
     if (j == k - 1) break;
-    grid.sync();
-    // phase A: distances to the new centres, mass, chunk totals.  The newest
-    // centres of a group of rg repetitions are staged in shared memory; each
-    // point row is streamed from HBM once per group.
+    // distances to the new centres, mass, range totals
     for (int r0 = 0; r0 < reps; r0 += rg) {
       const int rn = min(rg, reps - r0);
-      __syncthreads();
       for (int q = 0; q < rn; ++q)
-        for (int e = threadIdx.x; e < d; e += blockDim.x) cs[(long long)q * d + e] = centers[((long long)(r0 + q) * k + j) * d + e];
+        for (int e = threadIdx.x; e < d; e += blockDim.x) cs[(long long)q * d + e] = P[s_idx[r0 + q] * d + e];
       __syncthreads();
-      for (long long c = blockIdx.x; c < nch; c += gridDim.x) {
-        const long long p0 = c * KS_CHUNK, p1 = min(n, p0 + KS_CHUNK);
-        // two rows per warp: every centre element read from shared memory
-        // serves both rows, and twice the row bytes are in flight
-        for (long long i = p0 + warp; i < p1; i += 2 * nwarp) {
-          const long long ib = i + nwarp < p1 ? i + nwarp : -1;
-          double acc[2][KS_RMAX];
-          seed_rows2(P + i * d, P + (ib >= 0 ? ib : i) * d, cs, d, rn, lane, acc);
+      // two rows per warp: every centre element read from shared memory
+      // serves both rows, and twice the row bytes are in flight
+      for (long long i = p0 + 2 * warp; i < p1; i += 2 * nwarp) {
+        const long long ib = i + 1 < p1 ? i + 1 : -1;
+        double acc[2][KS_RMAX];
+        seed_rows2(P + i * d, P + (ib >= 0 ? ib : i) * d, cs, d, rn, lane, acc);
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const long long ii = h == 0 ? i : ib;
-            if (ii < 0) break;
+        for (int h = 0; h < 2; ++h) {
+          const long long ii = h == 0 ? i : ib;
+          if (ii < 0) break;
 #pragma unroll
-            for (int q = 0; q < KS_RMAX; ++q) {
-              if (q >= rn) break;
-              const double a = warp_sum(acc[h][q]);
-              if (lane == 0) {
-                const int r = r0 + q;
-                double* best = best_all + (long long)r * n;
-                const double b = j == 0 ? a : fmin(best[ii], a);
-                best[ii] = b;
-                const double mv = rmul(w[ii], b);
-                mass_all[(long long)r * n + ii] = mv;
-                ms[q * KS_CHUNK + (int)(ii - p0)] = mv;
-              }
+          for (int q = 0; q < KS_RMAX; ++q) {
+            if (q >= rn) break;
+            const double a = warp_sum(acc[h][q]);
+            if (lane == 0) {
+              const int r = r0 + q;
+              double* best = best_all + (long long)r * n;
+              const double bb = j == 0 ? a : fmin(best[ii], a);
+              best[ii] = bb;
+              mass_w[(long long)r * n + ii] = rmul(w[ii], bb);
             }
           }
         }
-        __syncthreads();
-        for (int q = threadIdx.x; q < rn; q += blockDim.x) {
-          double t = 0.0;
-          for (long long i = p0; i < p1; ++i) t += ms[q * KS_CHUNK + (int)(i - p0)];
-          part_all[(long long)(r0 + q) * nch + c] = t;
-        }
-        __syncthreads();
       }
+      __syncthreads();
+      // range totals, one warp per repetition (the association of warp_draw)
+      for (int q = warp; q < rn; q += nwarp) {
+        const double t = warp_range_total(mass_w + (long long)(r0 + q) * n, p0, p1, lane);
+        if (lane == 0) part_w[(long long)(r0 + q) * G + c] = t;
+      }
+      __syncthreads();
     }
     grid.sync();
   }
@@ -482,25 +510,26 @@ int pcy_kmeanspp(const double* P, const double* w, long long n, int d, int k, in
   if (n < 1 || k < 1 || d < 1 || reps < 1) { pcy_set_error("kmeanspp: bad sizes"); return PCY_EINVAL; }
   cudaStream_t st = (cudaStream_t)stream;
   double *best = nullptr, *mass = nullptr, *part = nullptr, *wpart = nullptr; int* picks = nullptr;
-  const long long nch = (n + KS_CHUNK - 1) / KS_CHUNK;
-  PCY_CUDA(pcy_malloc_async(&best, sizeof(double) * n * reps, st));
-  PCY_CUDA(pcy_malloc_async(&mass, sizeof(double) * n * reps, st));
-  PCY_CUDA(pcy_malloc_async(&part, sizeof(double) * nch * reps, st));
-  PCY_CUDA(pcy_malloc_async(&wpart, sizeof(double) * nch, st));
-  PCY_CUDA(pcy_malloc_async(&picks, sizeof(int) * k * reps, st));
-  // centres of rg repetitions per shared-memory pass (<= 200 KB with the chunk masses)
+  // centres of rg repetitions per shared-memory pass (<= 200 KB)
   const size_t budget = 200 * 1024;
-  int rg = (int)std::min<long long>(std::min(reps, KS_RMAX), (long long)(budget / (sizeof(double) * (d + KS_CHUNK))));
+  int rg = (int)std::min<long long>(std::min(reps, KS_RMAX), (long long)(budget / (sizeof(double) * d)));
   if (rg < 1) { pcy_set_error("kmeanspp: dimension too large for the seeding kernel"); return PCY_EINVAL; }
-  const size_t sm = sizeof(double) * ((size_t)rg * d + (size_t)rg * KS_CHUNK);
+  if (reps > 64) { pcy_set_error("kmeanspp: at most 64 repetitions per call"); return PCY_EINVAL; }
+  const size_t sm = sizeof(double) * (size_t)rg * d;
   PCY_CUDA(cudaFuncSetAttribute(k_seed_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   int dev = 0, sms = 0, per = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_seed_coop, KS_THREADS, sm);
   const long long max_blocks = (long long)sms * (per > 0 ? per : 1);
-  long long blocks = std::max<long long>(std::min<long long>(nch, max_blocks), std::min<long long>(reps, max_blocks));
+  // one row range per CTA, at least 32 rows each
+  const long long blocks = std::max<long long>(1, std::min<long long>(max_blocks, (n + 31) / 32));
   int nb = (int)blocks;
+  PCY_CUDA(pcy_malloc_async(&best, sizeof(double) * n * reps, st));
+  PCY_CUDA(pcy_malloc_async(&mass, sizeof(double) * 2 * n * reps, st));
+  PCY_CUDA(pcy_malloc_async(&part, sizeof(double) * 2 * blocks * reps, st));
+  PCY_CUDA(pcy_malloc_async(&wpart, sizeof(double) * blocks, st));
+  PCY_CUDA(pcy_malloc_async(&picks, sizeof(int) * k * reps, st));
   long long n_ = n; int d_ = d, k_ = k, reps_ = reps;
   void* args[] = {(void*)&P, (void*)&w, &n_, &d_, &k_, &reps_, (void*)&U, &centers, &best, &mass, &part, &wpart, &picks, &rg};
   const bool prof = pcy_prof_enabled();

@@ -13,7 +13,7 @@
 //                (only the span reaches the result; SURVEY.md §7 hard part 5),
 //                k_cgs2 when the Gram factorisation breaks down
 //   k_jacobi  -- one-sided (Hestenes) Jacobi SVD, tournament ordering,
-//                one thread-block cluster (cluster barrier per round)
+//                persistent cooperative grid (grid barrier per round)
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -154,18 +154,14 @@ __global__ void __launch_bounds__(1024) k_cgs2(double* __restrict__ Y, long long
 // right singular vectors of G^T.  perm scratch (n ints), rot scratch
 // (max_sweeps ints, zeroed by the caller).
 //
-// One warp per pair of a round; the CTAs meet at a barrier between rounds
-// (the pairs of one round are disjoint, so the result does not depend on how
-// pairs map to warps).  The launch is one thread-block cluster (JAC_CLUSTER CTAs of JAC_THREADS):
-// the per-round barrier is the hardware cluster barrier (~0.2 us) instead of
-// a grid barrier, and the columns (<= a few MB) stay in L2, read with .cg
-// loads.  A round is then a few L2 round trips.
-constexpr int JAC_CLUSTER = 8, JAC_THREADS = 1024;
-__global__ void __launch_bounds__(JAC_THREADS) k_jacobi(double* __restrict__ G, int m, int n, double tol, int max_sweeps,
+// Persistent cooperative kernel: one warp per pair of a round, the CTAs of
+// the grid meet at a grid barrier between rounds (the pairs of one round are
+// disjoint, so the result does not depend on how pairs map to warps).
+__global__ void __launch_bounds__(256) k_jacobi(double* __restrict__ G, int m, int n, double tol, int max_sweeps,
                                                double* __restrict__ sig, double* __restrict__ U, int ldu,
                                                int* __restrict__ perm, int* __restrict__ sweeps_out,
                                                int* __restrict__ rot) {
-  cg::cluster_group grid = cg::this_cluster();   // the whole launch
+  cg::grid_group grid = cg::this_grid();
   const int lane = threadIdx.x & 31;
   const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int nw = (int)((gridDim.x * blockDim.x) >> 5);
@@ -185,7 +181,7 @@ __global__ void __launch_bounds__(JAC_THREADS) k_jacobi(double* __restrict__ G, 
         double* gq = G + (long long)b * m;
         double al = 0.0, be = 0.0, ga = 0.0;
         for (int i = lane; i < m; i += 32) {
-          const double x = __ldcg(gp + i), y = __ldcg(gq + i);
+          const double x = gp[i], y = gq[i];
           al = fma(x, x, al); be = fma(y, y, be); ga = fma(x, y, ga);
         }
         al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
@@ -194,7 +190,7 @@ __global__ void __launch_bounds__(JAC_THREADS) k_jacobi(double* __restrict__ G, 
           const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
           const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
           for (int i = lane; i < m; i += 32) {
-            const double x = __ldcg(gp + i), y = __ldcg(gq + i);
+            const double x = gp[i], y = gq[i];
             gp[i] = c * x - s * y;
             gq[i] = s * x + c * y;
           }
@@ -209,25 +205,25 @@ __global__ void __launch_bounds__(JAC_THREADS) k_jacobi(double* __restrict__ G, 
   for (int j = gw; j < n; j += nw) {
     const double* gj = G + (long long)j * m;
     double acc = 0.0;
-    for (int i = lane; i < m; i += 32) { const double v = __ldcg(gj + i); acc = fma(v, v, acc); }
+    for (int i = lane; i < m; i += 32) acc = fma(gj[i], gj[i], acc);
     acc = warp_sum(acc);
     if (lane == 0) sig[j] = sqrt(acc);
   }
   grid.sync();
   // order by sigma descending (stable on ties), rank by counting
   for (long long j = gt; j < n; j += nt) {
-    const double sj = __ldcg(sig + j);
+    const double sj = sig[j];
     int rank = 0;
-    for (int k = 0; k < n; ++k) { const double sk = __ldcg(sig + k); rank += (sk > sj) || (sk == sj && k < j); }
+    for (int k = 0; k < n; ++k) rank += (sig[k] > sj) || (sig[k] == sj && k < j);
     perm[rank] = (int)j;
   }
   grid.sync();
   for (int jj = gw; jj < n; jj += nw) {
-    const int j = __ldcg(perm + jj);
+    const int j = perm[jj];
     const double* gj = G + (long long)j * m;
-    const double sj = __ldcg(sig + j);
+    const double sj = sig[j];
     const double inv = sj > 0.0 ? 1.0 / sj : 0.0;
-    for (int i = lane; i < m; i += 32) U[(long long)i * ldu + jj] = __ldcg(gj + i) * inv;
+    for (int i = lane; i < m; i += 32) U[(long long)i * ldu + jj] = gj[i] * inv;
   }
   if (gt == 0) *sweeps_out = sweep;
 }
@@ -311,16 +307,20 @@ static cublasHandle_t blas_handle() {
 static int jacobi(cudaStream_t st, double* G, int m, int n, double tol, int max_sweeps, double* sig, double* U,
                   int ldu, int* perm, int* sweeps, int* rot) {
   PCY_CUDA(cudaMemsetAsync(rot, 0, sizeof(int) * max_sweeps, st));
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(JAC_CLUSTER);
-  cfg.blockDim = dim3(JAC_THREADS);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = JAC_CLUSTER; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr; cfg.numAttrs = 1;
-  PCY_CUDA(cudaLaunchKernelEx(&cfg, k_jacobi, G, m, n, tol, max_sweeps, sig, U, ldu, perm, sweeps, rot));
+  static int max_blocks = -1;
+  if (max_blocks < 0) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_jacobi, 256, 0);
+    max_blocks = sms * (per > 0 ? per : 1);
+  }
+  const int pairs = (n + 1) / 2;
+  int blocks = (pairs + 7) / 8;
+  if (blocks > max_blocks) blocks = max_blocks;
+  if (blocks < 1) blocks = 1;
+  void* args[] = {&G, &m, &n, &tol, &max_sweeps, &sig, &U, &ldu, &perm, &sweeps, &rot};
+  PCY_CUDA(cudaLaunchCooperativeKernel((const void*)k_jacobi, dim3(blocks), dim3(256), args, 0, st));
   pcy_count_launch();
   return PCY_OK;
 }
