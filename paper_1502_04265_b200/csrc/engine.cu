@@ -1581,6 +1581,15 @@ struct Engine {
         const unsigned nblk = (unsigned)((kn + wpc - 1) / wpc);
         if (!nper) { k_snapshot<<<64, 256, 0, st>>>(E); pcy_count_launch(); }
         if (prof) PCY_CUDA(cudaEventRecord(ev[0], st));
+        // the batch Gram for k_plan's open-conflict test depends only on the
+        // batch rows: on the K3 stream it runs beside the K1 contraction
+        static const bool gram_late = getenv("PCY_GRAM_LATE") != nullptr;
+        const bool gram_early = k3par && nper != 101 && hi && !gram_late;
+        if (gram_early) {
+          PCY_CUDA(cudaEventRecord(evk1, st)); PCY_CUDA(cudaStreamWaitEvent(hi, evk1, 0));
+          const int grc = pcy_launch_gram_split(Xs, nullptr, ld, (int)kn, d, gram, kn, gram_part, gram_split, hi);
+          if (grc) return grc;
+        }
         if (nper) {
           int grc;
           const bool use_p = full_set(Xs, nullptr, kn, st, &grc);
@@ -1606,7 +1615,7 @@ struct Engine {
         if (k3par) {
           // k_plan picks a subtree-parallel window or a sequential stretch; the
           // launch that was not chosen returns at once
-          if (nper != 101) {   // opener rows against the batch (k_plan's conflict test)
+          if (nper != 101 && !gram_early) {   // opener rows against the batch (k_plan's conflict test)
             const int grc = pcy_launch_gram_split(Xs, nullptr, ld, (int)kn, d, gram, kn, gram_part, gram_split, rs);
             if (grc) return grc;
           }
