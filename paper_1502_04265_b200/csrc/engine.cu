@@ -945,6 +945,41 @@ __global__ void k_rb_rank(EngDev E, long long nslots) {
   if (mine) E.order[rank] = (int)u;
 }
 
+// Sliced form of k_rb_rank: blockIdx.y counts over one slice of the
+// candidates and adds its count into rank[u] (zeroed before); the scatter
+// k_rb_scatter then places each alive node.  The (-weight, index) keys are
+// distinct among alive nodes, so the ranks are a permutation, as above.
+constexpr int RB_SLICES = 16;
+__global__ void __launch_bounds__(256) k_rb_rank_sliced(EngDev E, long long nslots, int* __restrict__ rank) {
+  __shared__ long long sw[256], si[256];
+  __shared__ int sa[256];
+  const long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool mine = u < nslots && E.alive[u];
+  const long long wu = mine ? E.w[u] : 0, iu = mine ? E.idx[u] : 0;
+  const long long per = ((nslots + RB_SLICES - 1) / RB_SLICES + 255) / 256 * 256;
+  const long long lo = (long long)blockIdx.y * per, hi = min(nslots, lo + per);
+  int cnt = 0;
+  for (long long t0 = lo; t0 < hi; t0 += 256) {
+    const long long v = t0 + threadIdx.x;
+    sa[threadIdx.x] = v < hi ? E.alive[v] : 0;
+    sw[threadIdx.x] = v < hi ? E.w[v] : 0;
+    si[threadIdx.x] = v < hi ? E.idx[v] : 0;
+    __syncthreads();
+    if (mine) {
+      const int nt = (int)min(256LL, hi - t0);
+      for (int k = 0; k < nt; ++k)
+        cnt += sa[k] && (sw[k] > wu || (sw[k] == wu && si[k] < iu));
+    }
+    __syncthreads();
+  }
+  if (mine && cnt) atomicAdd(&rank[u], cnt);
+}
+
+__global__ void k_rb_scatter(EngDev E, long long nslots, const int* __restrict__ rank) {
+  const long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (u < nslots && E.alive[u]) E.order[rank[u]] = (int)u;
+}
+
 // T *= 2; detach every subtree; fresh roots (coreset.py:386-391).
 __global__ void k_rb_reset(EngDev E, long long nslots) {
   const long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1194,6 +1229,7 @@ struct Engine {
   double *tc_rnc = nullptr, *tc_xn2 = nullptr, *tc_c = nullptr;
   long long* tc_done = nullptr;   // creation index each slot's column (and split) was made for
   int* col_slot = nullptr;        // live column -> slot
+  int* rb_rank = nullptr;         // rebuild order: rank of each slot (k_rb_rank_sliced)
   int* ncol = nullptr;            // device count of live columns
   bool cols_reset = true;         // recompact the live columns at the next contraction
   BootScratch bs{};            // parallel bootstrap scratch
@@ -1276,7 +1312,7 @@ struct Engine {
     A_(E.child, NC); A_(E.alive, NC); A_(E.free_ids, NC);
     A_(E.fs_list, NC); A_(E.fs_gofs, GC); A_(E.fs_cnt, 1);
     { int* co = nullptr; A_(co, NC); E.col_of = co; }
-    A_(col_slot, NC); A_(ncol, 1); A_(tc_done, NC);
+    A_(col_slot, NC); A_(ncol, 1); A_(tc_done, NC); A_(rb_rank, NC);
     A_(E.pathj, Bmax * 16);
     A_(E.s, NC * ld); A_(E.r, NC * ld);
     A_(E.g_base, GC); A_(E.g_count, GC); A_(E.g_cap, GC); A_(E.g_bs, GC); A_(E.g_bsbase, GC);
@@ -1473,7 +1509,14 @@ struct Engine {
     while (ctl_h->F > m) {
       const long long nslots = ctl_h->F_alloc;
       const long long nodes = ctl_h->F;
-      k_rb_rank<<<(unsigned)((nslots + 255) / 256), 256, 0, st>>>(E, nslots); pcy_count_launch();
+      if (nslots >= 4096) {   // one thread per node is too few CTAs: slice the candidates
+        PCY_CUDA(cudaMemsetAsync(rb_rank, 0, sizeof(int) * nslots, st));
+        k_rb_rank_sliced<<<dim3((unsigned)((nslots + 255) / 256), RB_SLICES), 256, 0, st>>>(E, nslots, rb_rank);
+        pcy_count_launch();
+        k_rb_scatter<<<(unsigned)((nslots + 255) / 256), 256, 0, st>>>(E, nslots, rb_rank); pcy_count_launch();
+      } else {
+        k_rb_rank<<<(unsigned)((nslots + 255) / 256), 256, 0, st>>>(E, nslots); pcy_count_launch();
+      }
       k_rb_reset<<<(unsigned)((nslots + 255) / 256), 256, 0, st>>>(E, nslots); pcy_count_launch();
       ctl_h->root_count = 0;   // fresh roots; the mirror refreshes at the next publication
       const bool prof = pcy_prof_enabled();
@@ -1485,17 +1528,28 @@ struct Engine {
         while (off < nodes) {
           const long long nb = nodes - off < batch ? nodes - off : batch;
           int grc;
+          // the batch Gram depends only on the batch's references: a side
+          // stream computes it beside the contraction and the chain walk
+          static const bool gram_late = getenv("PCY_GRAM_LATE") != nullptr;
+          const bool gram_early = k3par && nper <= 8 && hi && !gram_late;   // small d only: at large d the Gram competes with the K1 contraction
+          if (gram_early) {
+            PCY_CUDA(cudaEventRecord(evk1, st)); PCY_CUDA(cudaStreamWaitEvent(hi, evk1, 0));
+            grc = pcy_launch_gram_split(E.r, E.order + off, ld, (int)nb, d, gram, nb, gram_part, gram_split, hi);
+            if (grc) return grc;
+            PCY_CUDA(cudaEventRecord(evk3, hi));
+          }
           const bool use_p = full_set(E.r, E.order + off, nb, st, &grc);
           if (grc) return grc;
           k_rchain<<<(unsigned)((nb + wpc - 1) / wpc), wpc * 32, sizeof(double) * wpc * ld, st>>>(
               E, E.order + off, nb, chh, chr, use_p ? parts : nullptr, ctl_h->F_alloc); pcy_count_launch();
-          if (nper == 101) {
+          if (nper == 101 && !gram_early) {
             grc = pcy_launch_gram_split(E.r, E.order + off, ld, (int)nb, d, gram, nb, gram_part, gram_split, st);
             if (grc) return grc;
           }
+          if (gram_early) PCY_CUDA(cudaStreamWaitEvent(st, evk3, 0));
           ParCtl* pp = nullptr;
           if (k3par) {
-            if (nper != 101) {   // opener rows against the batch (k_plan's conflict test)
+            if (nper != 101 && !gram_early) {   // opener rows against the batch (k_plan's conflict test)
               grc = pcy_launch_gram_split(E.r, E.order + off, ld, (int)nb, d, gram, nb, gram_part, gram_split, st);
               if (grc) return grc;
             }
@@ -1584,7 +1638,7 @@ struct Engine {
         // the batch Gram for k_plan's open-conflict test depends only on the
         // batch rows: on the K3 stream it runs beside the K1 contraction
         static const bool gram_late = getenv("PCY_GRAM_LATE") != nullptr;
-        const bool gram_early = k3par && nper != 101 && hi && !gram_late;
+        const bool gram_early = k3par && nper <= 8 && hi && !gram_late;   // small d only: at large d the Gram competes with the K1 contraction
         if (gram_early) {
           PCY_CUDA(cudaEventRecord(evk1, st)); PCY_CUDA(cudaStreamWaitEvent(hi, evk1, 0));
           const int grc = pcy_launch_gram_split(Xs, nullptr, ld, (int)kn, d, gram, kn, gram_part, gram_split, hi);
@@ -1601,7 +1655,7 @@ struct Engine {
             k_chain2<1><<<nblk, wpc * 32, sizeof(double) * wpc * ld, st>>>(E, Xs, XSs, Ws, kn, chh, chr,
                                                                           use_p ? parts : nullptr, ctl_h->F_alloc);
           pcy_count_launch();
-          if (nper == 101) {
+          if (nper == 101 && !gram_early) {
             rc0 = pcy_launch_gram_split(Xs, nullptr, ld, (int)(kn), d, gram, kn, gram_part, gram_split, st);
             if (rc0) return rc0;
           }
