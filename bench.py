@@ -363,8 +363,6 @@ def main():
 
     clocks = ClockSampler(local)
     clocks.start()
-    nat.prof_reset()
-    nat.prof_enable(True)
     l0 = nat.launch_count()
     st = torch.cuda.current_stream()
     evs = []
@@ -382,12 +380,29 @@ def main():
     if world > 1:
         dist.barrier()
     launches = nat.launch_count() - l0
-    nat.prof_enable(False)
+    clk = clocks.stop()
     ms_steps = [a.elapsed_time(b) for a, b in evs]
-    ms = float(np.sum(ms_steps))
+    ms_timed = float(np.sum(ms_steps))
+
+    # per-kernel breakdown: a second pass of the same steps with the engine's
+    # per-launch event timing on (its host-side event reads sit between
+    # launches, so it is kept out of the timed steps above)
+    nat.prof_reset()
+    nat.prof_enable(True)
+    torch.cuda.synchronize()
+    evp = []
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        step_device()
+        e1.record(st)
+        evp.append((e0, e1))
+    torch.cuda.synchronize()
+    nat.prof_enable(False)
+    ms = float(np.sum([a.elapsed_time(b) for a, b in evp]))   # profiled pass: denominators of the shares
     prof = {k: nat.prof_read(k) for k in ("resolve", "chain", "reattach")}
     prof_x = {k: nat.prof_read(k) for k in ("gemm", "seed", "lloyd")}
-    clk = clocks.stop()
 
     # e2e: public API with host buffers (H2D of the stream, D2H of coreset + centers + costs)
     e2e_times = []
@@ -431,7 +446,7 @@ def main():
                      "note": "evaluate_cost_multi over the resident stream (chunks of 8192 rows, fp64 DMMA "
                              "distance + first-min per set, chunk costs summed in order)"}
 
-    t_local = torch.tensor([ms / args.steps, float(np.mean(e2e_times))], dtype=torch.float64, device=dev)
+    t_local = torch.tensor([ms_timed / args.steps, float(np.mean(e2e_times))], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
     ms_step, e2e_s = float(t_local[0]), float(t_local[1])
@@ -445,6 +460,20 @@ def main():
             pass
         hbm = float(peaks.get("hbm_gbs", 6650.0))
         peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+        # per-launch DRAM traffic from the committed ncu --set full captures
+        # (profiles/ncu_traffic.json, tools/ncu_traffic.py); None when the
+        # config has no capture
+        ncu_tr = {}
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+                ncu_tr = json.load(f).get(cfg.name, {})
+        except Exception:
+            pass
+
+        def traffic(pred):
+            ks = [v["bytes_per_launch"] for k, v in ncu_tr.get("kernels", {}).items() if pred(k)]
+            return max(ks) if ks else None
+
         # dominant kernel by device time share
         dom = max(prof, key=lambda k: prof[k][0])
         r_ms, r_cnt, r_units = prof["resolve"]
@@ -454,7 +483,10 @@ def main():
         achieved = (r_units * bytes_per_pt) / (r_ms / 1e3) / 1e9 if r_ms > 0 else 0.0
         k3 = {"kernel": "k_resolve2/3 (K3 subtree-parallel resolve + CF update, incl. k_plan)", "bound": "hbm",
               "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-              "traffic": None, "peak_source": peak_src,
+              "traffic": traffic(lambda k: k.startswith("k_resolve") and k.endswith("1>")),
+              "traffic_unit": "bytes per launch (ncu dram read+write, subtree-parallel launch)",
+              "bytes_per_launch": (r_units * bytes_per_pt / r_cnt) if r_cnt else None,
+              "peak_source": peak_src,
               "note": "latency-bound: one CTA per k_plan domain walks its items in stream order; "
                       "algorithmic bytes = 24*d+60 per point",
               "ns_per_point": (r_ms * 1e6 / r_units) if r_units else None,
@@ -472,7 +504,8 @@ def main():
                 pk = gemm_peaks.get("tf32_tflops", 1100.0) / 3.0
                 rooflines.append({"kernel": "k_tc_dots (K1 full-set distance contraction, split-TF32 on tcgen05)",
                                   "bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s", "frac": ach / pk,
-                                  "launches_per_step": g_cnt / args.steps, "traffic": None,
+                                  "launches_per_step": g_cnt / args.steps,
+                                  "traffic": traffic(lambda k: k.startswith("k_tc_dots")),
                                   "ms_per_step": g_ms / args.steps, "share_of_step": g_ms / ms if ms > 0 else None,
                                   "peak_source": "measured cuBLAS TF32 GEMM / 3 (three TF32 products per "
                                                  "fp32-faithful product); achieved = 2*M*N*d per launch "
@@ -481,7 +514,8 @@ def main():
                 pk = gemm_peaks.get("fp64_tflops", 40.0)
                 rooflines.append({"kernel": "k_dist_tile<2> (K1 full-set distance contraction, fp64 DMMA)",
                                   "bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s", "frac": ach / pk,
-                                  "launches_per_step": g_cnt / args.steps, "traffic": None,
+                                  "launches_per_step": g_cnt / args.steps,
+                                  "traffic": traffic(lambda k: k == "k_dist_tile<2>"),
                                   "ms_per_step": g_ms / args.steps, "share_of_step": g_ms / ms if ms > 0 else None,
                                   "peak_source": "measured cuBLAS FP64 GEMM; achieved = 2*M*N*d per launch "
                                                  "(M block rows x N reference slots)"})
@@ -533,7 +567,8 @@ def main():
             "coreset_size": int(F),
             "engine_counters": step_device.engine.counters() if step_device.engine is not None else None,
             "step_ms": ms_steps,
-            "phase_ms": [{"coreset": round(p[0], 2), "kmeans": round(p[1], 2)} for p in step_device.phases[-args.steps:]],
+            "phase_ms": [{"coreset": round(p[0], 2), "kmeans": round(p[1], 2)} for p in step_device.phases[-2 * args.steps:-args.steps]],
+            "profiled_ms_per_step": ms / args.steps,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
