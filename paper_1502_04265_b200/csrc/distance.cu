@@ -8,6 +8,7 @@
 //                   first column on ties; k_argmin_reduce folds the tiles.
 // Rows of A and B may be gathered through index arrays (tree nodes live at
 // arbitrary slots), so no operand is ever copied into a packed buffer.
+#include <cstdlib>
 #include "common.cuh"
 
 namespace {
@@ -19,8 +20,17 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
                : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(128) k_dist_tile(int M, int N, int K,
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool ok) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" :: "r"(sa), "l"(src), "r"(ok ? 8 : 0));
+}
+
+// CPA: operand tiles go global -> shared with cp.async (no register staging:
+// fewer registers, five CTAs per SM instead of four), double-buffered as in
+// the register-staged form; the k4 steps and the epilogue are unchanged, so
+// the results are bitwise the same.
+template <int MODE, bool CPA = false>
+__global__ void __launch_bounds__(128, CPA ? 5 : 1) k_dist_tile(int M, int N, int K,
                                                   const double* __restrict__ A, const int* __restrict__ aidx, long long lda,
                                                   const double* __restrict__ B, const int* __restrict__ bidx, long long ldb,
                                                   const double* __restrict__ rn,
@@ -81,13 +91,31 @@ __global__ void __launch_bounds__(128) k_dist_tile(int M, int N, int K,
       Bs[buf][kk][mm] = rb[r];
     }
   };
+  auto issue = [&](int k0, int b) {   // CPA: the tile k0 straight into buffer b
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int e = tid + r * 128;
+      const int mm = e >> 4, kk = e & 15;
+      const long long ar = arow[mm], br = brow[mm];
+      const bool ka = k0 + kk < K;
+      cp_async8(&As[b][mm][kk], ar >= 0 && ka ? A + ar + k0 + kk : A, ar >= 0 && ka);
+      cp_async8(&Bs[b][kk][mm], br >= 0 && ka ? B + br + k0 + kk : B, br >= 0 && ka);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
   int buf = 0;
-  fetch(0);
-  stash(0);
+  if constexpr (CPA) {
+    issue(0, 0);
+    asm volatile("cp.async.wait_group 0;\n" ::);
+  } else {
+    fetch(0);
+    stash(0);
+  }
   __syncthreads();
   for (int k0 = 0; k0 < K; k0 += DBK) {
     const bool more = k0 + DBK < K;
-    if (more) fetch(k0 + DBK);
+    if constexpr (CPA) { if (more) issue(k0 + DBK, buf ^ 1); }
+    else if (more) fetch(k0 + DBK);
 #pragma unroll
     for (int ks = 0; ks < DBK; ks += 4) {
       double af[4], bf[4];
@@ -101,7 +129,8 @@ __global__ void __launch_bounds__(128) k_dist_tile(int M, int N, int K,
         for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
     if (more) {
-      stash(buf ^ 1);
+      if constexpr (CPA) asm volatile("cp.async.wait_group 0;\n" ::);
+      else stash(buf ^ 1);
       __syncthreads();
       buf ^= 1;
     }
@@ -199,7 +228,7 @@ int pcy_launch_gram(const double* A, const int* aidx, long long lda, int M, cons
   dim3 grid((unsigned)((N + DBN - 1) / DBN), (unsigned)((M + DBM - 1) / DBM));
   // only the tiles on or below the diagonal: the engine's batch Grams are
   // symmetric and read at (later item, earlier item) only
-  k_dist_tile<0><<<grid, 128, 0, st>>>(M, N, K, A, aidx, lda, B, bidx, ldb, nullptr, C, ldc, nullptr, nullptr, 0,
+  k_dist_tile<0, true><<<grid, 128, 0, st>>>(M, N, K, A, aidx, lda, B, bidx, ldb, nullptr, C, ldc, nullptr, nullptr, 0,
                                        nullptr, nullptr, A == B && aidx == bidx && M == N ? 1 : 0);
   pcy_count_launch();
   PCY_LAUNCH_CHECK();
@@ -219,7 +248,7 @@ int pcy_launch_gram_split(const double* A, const int* aidx, long long lda, int M
   if (S <= 1 || !scratch) return pcy_launch_gram(A, aidx, lda, M, A, aidx, lda, M, K, C, ldc, st);
   const long long pstride = (long long)M * ldc;
   dim3 grid((unsigned)((M + DBN - 1) / DBN), (unsigned)((M + DBM - 1) / DBM), (unsigned)S);
-  k_dist_tile<0><<<grid, 128, 0, st>>>(M, M, K, A, aidx, lda, A, aidx, lda, nullptr, scratch, ldc, nullptr, nullptr, 0,
+  k_dist_tile<0, true><<<grid, 128, 0, st>>>(M, M, K, A, aidx, lda, A, aidx, lda, nullptr, scratch, ldc, nullptr, nullptr, 0,
                                        nullptr, nullptr, 1, kslice, pstride);
   pcy_count_launch();
   k_gram_sum<<<(unsigned)(((long long)M * M + 255) / 256), 256, 0, st>>>(scratch, S, pstride, M, C, ldc);
@@ -236,7 +265,11 @@ int pcy_launch_parts(const double* A, const int* aidx, long long lda, int M, con
                      cudaStream_t st) {
   if (M <= 0 || N <= 0) return PCY_OK;
   dim3 grid((unsigned)((N + DBN - 1) / DBN), (unsigned)((M + DBM - 1) / DBM));
-  k_dist_tile<2><<<grid, 128, 0, st>>>(M, N, K, A, aidx, lda, B, bidx, ldb, rn, C, ldc, nullptr, nullptr, 0, n_dev);
+  static const bool old_parts = getenv("PCY_OLD_PARTS") != nullptr;
+  if (old_parts)
+    k_dist_tile<2><<<grid, 128, 0, st>>>(M, N, K, A, aidx, lda, B, bidx, ldb, rn, C, ldc, nullptr, nullptr, 0, n_dev);
+  else
+    k_dist_tile<2, true><<<grid, 128, 0, st>>>(M, N, K, A, aidx, lda, B, bidx, ldb, rn, C, ldc, nullptr, nullptr, 0, n_dev);
   pcy_count_launch();
   PCY_LAUNCH_CHECK();
   return PCY_OK;
@@ -251,7 +284,7 @@ int pcy_launch_nearest(const double* A, const int* aidx, long long lda, int M, c
   if (M <= 0) return PCY_OK;
   const int ntiles = (N + DBN - 1) / DBN;
   dim3 grid((unsigned)ntiles, (unsigned)((M + DBM - 1) / DBM));
-  k_dist_tile<1><<<grid, 128, 0, st>>>(M, N, K, A, aidx, lda, B, bidx, ldb, rn, nullptr, 0, ppart, ppos, ntiles);
+  k_dist_tile<1, true><<<grid, 128, 0, st>>>(M, N, K, A, aidx, lda, B, bidx, ldb, rn, nullptr, 0, ppart, ppos, ntiles);
   pcy_count_launch();
   k_argmin_reduce<<<(unsigned)((M + 7) / 8), 256, 0, st>>>(M, ntiles, ppart, ppos, out_pos, out_part);
   pcy_count_launch();
@@ -268,7 +301,7 @@ int pcy_launch_assign_d2(const double* P, long long ldp, int n, const double* pn
   if (n <= 0 || k <= 0) return PCY_OK;
   const int ntiles = (k + DBN - 1) / DBN;
   dim3 grid((unsigned)ntiles, (unsigned)((n + DBM - 1) / DBM));
-  k_dist_tile<3><<<grid, 128, 0, st>>>(n, k, d, P, nullptr, ldp, C, nullptr, ldc, cn, nullptr, 0, ppart, ppos, ntiles,
+  k_dist_tile<3, true><<<grid, 128, 0, st>>>(n, k, d, P, nullptr, ldp, C, nullptr, ldc, cn, nullptr, 0, ppart, ppos, ntiles,
                                       nullptr, pn);
   pcy_count_launch();
   k_argmin_reduce<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(n, ntiles, ppart, ppos, assign, best);
