@@ -1240,6 +1240,9 @@ struct Engine {
   bool k3par = false;         // subtree-parallel resolve / reattach enabled
   int nper = 0;          // resolve kernel: 1..8 register rows, 100/101 shared-memory rows, 0 generic
   int nnew_cap = 0, rea_cap = 0;   // new-node table sizes of K3 and of the reattach
+  int rea_cap_t = 0;               // reattach table with reference rows (no batch Gram)
+  bool rea_gram = false;           // k_reattach2 takes new-entry dots from the batch Gram
+  size_t rea_smem_t = 0, rea_smem_g = 0;
   size_t res_smem = 0, rea_smem = 0;
   std::vector<void*> allocs;
 
@@ -1365,10 +1368,16 @@ struct Engine {
       if (cap > PCY_NNEW_FAST) cap = PCY_NNEW_FAST;
       nnew_cap = (int)cap;
       res_smem = resolve_smem_bytes(ld, nnew_cap, NC, GC);
-      long long rcap = maxsm > base ? (long long)((maxsm - base) / (sizeof(double) * (ld | 1))) : 0;
-      if (rcap > PCY_NNEW_FAST) rcap = PCY_NNEW_FAST;
-      rea_cap = (int)rcap;
-      rea_smem = reattach_smem_bytes(ld, rea_cap, NC, GC);
+      // reattach table: with the batch Gram (subtree-parallel mode) the new
+      // entries need no reference rows in shared memory; without it they do
+      const size_t rbase = reattach_smem_bytes(ld, 0, NC, GC);
+      long long rcap = maxsm > rbase ? (long long)((maxsm - rbase) / (sizeof(double) * (ld | 1))) : 0;
+      if (rcap > PCY_NNEW_REA) rcap = PCY_NNEW_REA;
+      rea_cap_t = (int)rcap;
+      rea_smem_t = reattach_smem_bytes(ld, rea_cap_t, NC, GC);
+      rea_smem_g = reattach_smem_bytes(ld, PCY_NNEW_REA, NC, GC, false);
+      rea_cap = rea_cap_t;
+      rea_smem = rea_smem_t > rea_smem_g ? rea_smem_t : rea_smem_g;   // attribute: either variant fits
       if (nnew_cap < 8) { nper = 0; use_tc = false; }
       switch (nper) {
         case 1: PCY_CUDA(cudaFuncSetAttribute(k_resolve2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
@@ -1419,6 +1428,13 @@ struct Engine {
       const char* pe = getenv("PCY_K3PAR");
       k3par = nper >= 1 && (!pe || atoi(pe) != 0) && plan_smem <= maxsm;
       if (k3par) PCY_CUDA(cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan_smem));
+      static const bool rea_trows = getenv("PCY_REA_TROWS") != nullptr;   // A/B: reference rows, no Gram dots
+      if (nper >= 1 && nper <= 8) {
+        const bool g = k3par && !rea_trows;
+        rea_cap = g ? PCY_NNEW_REA : rea_cap_t;
+        rea_smem = g ? rea_smem_g : rea_smem_t;
+        rea_gram = g;
+      }
     }
     if (!(ctl_h = ctl_pool_get())) { pcy_set_error("cudaHostAlloc of the control mirror failed"); return PCY_ENOMEM; }
     memset(ctl_h, 0, sizeof(EngCtl));
@@ -1548,6 +1564,7 @@ struct Engine {
           }
           if (gram_early) PCY_CUDA(cudaStreamWaitEvent(st, evk3, 0));
           ParCtl* pp = nullptr;
+          const double* rg = rea_gram ? gram : nullptr;   // the batch Gram exists exactly when k3par
           if (k3par) {
             if (nper != 101 && !gram_early) {   // opener rows against the batch (k_plan's conflict test)
               grc = pcy_launch_gram_split(E.r, E.order + off, ld, (int)nb, d, gram, nb, gram_part, gram_split, st);
@@ -1559,20 +1576,20 @@ struct Engine {
             pcy_count_launch();
             pp = parctl;
             switch (nper) {
-              case 1: k_reattach2<1, true><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp); break;
-              case 2: k_reattach2<2, true><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp); break;
-              case 4: k_reattach2<4, true><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp); break;
-              case 8: k_reattach2<8, true><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp); break;
+              case 1: k_reattach2<1, true><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp, rg, nb); break;
+              case 2: k_reattach2<2, true><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp, rg, nb); break;
+              case 4: k_reattach2<4, true><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp, rg, nb); break;
+              case 8: k_reattach2<8, true><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp, rg, nb); break;
               case 100: k_reattach3<true, 2048, true><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr, nullptr, 0, 0, pp); break;
               default: k_reattach3<false, 512, true><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr, gram, nb, 0, pp); break;
             }
             pcy_count_launch();
           }
           switch (nper) {
-            case 1: k_reattach2<1><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp); pcy_count_launch(); break;
-            case 2: k_reattach2<2><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp); pcy_count_launch(); break;
-            case 4: k_reattach2<4><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp); pcy_count_launch(); break;
-            case 8: k_reattach2<8><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp); pcy_count_launch(); break;
+            case 1: k_reattach2<1><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp, rg, nb); pcy_count_launch(); break;
+            case 2: k_reattach2<2><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp, rg, nb); pcy_count_launch(); break;
+            case 4: k_reattach2<4><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp, rg, nb); pcy_count_launch(); break;
+            case 8: k_reattach2<8><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp, rg, nb); pcy_count_launch(); break;
             case 100: k_reattach3<true, 2048><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr, nullptr, 0, 0, pp); pcy_count_launch(); break;
             default: k_reattach3<false, 512><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr, gram, nb, 0, pp); pcy_count_launch(); break;
           }

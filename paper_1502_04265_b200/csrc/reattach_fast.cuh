@@ -78,9 +78,10 @@ __global__ void k_rchain(EngDev E, const int* __restrict__ order, long long n, C
 template <int NPER, bool PAR = false>
 __global__ void __launch_bounds__(32, 1) k_reattach2(EngDev E, const int* __restrict__ order, long long n,
                                                      int nnew_cap, const ChainHdr* __restrict__ H,
-                                                     const ChainLvl* __restrict__ R, ParCtl* __restrict__ par = nullptr) {
+                                                     const ChainLvl* __restrict__ R, ParCtl* __restrict__ par = nullptr,
+                                                     const double* __restrict__ gram = nullptr, long long gld = 0) {
   extern __shared__ __align__(16) unsigned char smraw[];
-  ResolveSmem& S = *reinterpret_cast<ResolveSmem*>(smraw);
+  ReattachSmem& S = *reinterpret_cast<ReattachSmem*>(smraw);
   const int lane = threadIdx.x;
   const int* ilist = nullptr;
   if constexpr (PAR) {
@@ -99,10 +100,10 @@ __global__ void __launch_bounds__(32, 1) k_reattach2(EngDev E, const int* __rest
     else return j;
   };
   const int d = E.d, ld = E.ld;
-  double* xsm = reinterpret_cast<double*>(smraw + ((sizeof(ResolveSmem) + 15) & ~size_t(15)));
+  double* xsm = reinterpret_cast<double*>(smraw + ((sizeof(ReattachSmem) + 15) & ~size_t(15)));
   const int lds = ld | 1;   // odd stride: conflict-free lane-per-row reads
   double* tref = xsm + ld;
-  unsigned* mbits = reinterpret_cast<unsigned*>(tref + (long long)nnew_cap * lds);   // layout: reattach_smem_bytes
+  unsigned* mbits = reinterpret_cast<unsigned*>(tref + (gram ? 0LL : (long long)nnew_cap * lds));   // layout: reattach_smem_bytes
   const int mwords = (int)(E.NC / 32 + 1);
   unsigned* gbits = mbits + mwords;
   const int gwords = (int)(E.GC / 32 + 1);
@@ -198,6 +199,17 @@ __global__ void __launch_bounds__(32, 1) k_reattach2(EngDev E, const int* __rest
       if ((gbits[g >> 5] >> (g & 31)) & 1u) {
         // one new member per lane: sequential dot over the padded smem row
         double np_ = INFINITY; int nt = 0x7fffffff;
+        if (gram) {
+          // same-launch nodes are rows of this batch: (current, earlier) entry of the batch Gram
+          const double* grow = gram + gix(i) * gld;
+          for (int c0 = 0; c0 < nnew; c0 += 32) {
+            const int t = c0 + lane;
+            if (t < nnew && S.tgrp[t] == g) {
+              const double part = radd(S.trn[t], rmul(grow[S.titem[t]], -2.0));
+              if (part < np_) { np_ = part; nt = t; }
+            }
+          }
+        } else
         for (int c0 = 0; c0 < nnew; c0 += 32) {
           const int t = c0 + lane;
           if (t < nnew && S.tgrp[t] == g) {
@@ -220,9 +232,11 @@ __global__ void __launch_bounds__(32, 1) k_reattach2(EngDev E, const int* __rest
       if (bj < 0 || radd(bp, rsq_c) > radius) {
         // group.add(node): u keeps its statistics (coreset.py:403-406)
         const int t = nnew++;
-        double* rr = tref + (long long)t * lds;
+        if (!gram) {
+          double* rr = tref + (long long)t * lds;
 #pragma unroll
-        for (int k = 0; k < NPER; ++k) { const int e = lane + 32 * k; if (e < ld) rr[e] = xr[k]; }
+          for (int k = 0; k < NPER; ++k) { const int e = lane + 32 * k; if (e < ld) rr[e] = xr[k]; }
+        }
         const bool had = ((gbits[g >> 5] >> (g & 31)) & 1u) != 0;
         int gs;
         if (had) gs = gmap_find(S, g);
@@ -231,7 +245,7 @@ __global__ void __launch_bounds__(32, 1) k_reattach2(EngDev E, const int* __rest
           while (S.gkey[gs] >= 0) gs = (gs + 1) & (PCY_GMAP_SLOTS - 1);
         }
         if (lane == 0) {
-          S.tid[t] = u; S.tgrp[t] = g; S.tchild[t] = -1; S.tnext[t] = -1;
+          S.tid[t] = u; S.tgrp[t] = g; S.tchild[t] = -1; S.tnext[t] = -1; S.titem[t] = (int)gix(i);
           S.tw[t] = wu_c; S.tq[t] = qu_c; S.tsn[t] = snu_c; S.trn[t] = rsq_c;
           if (had) { S.tnext[S.gtail[gs]] = t; S.gtail[gs] = t; }
           else { S.gkey[gs] = g; S.ghead[gs] = t; S.gtail[gs] = t; gbits[g >> 5] |= 1u << (g & 31); }
@@ -347,18 +361,23 @@ __global__ void __launch_bounds__(32, 1) k_reattach2(EngDev E, const int* __rest
     E.w[node] = S.tw[t]; E.q[node] = S.tq[t]; E.sn[node] = S.tsn[t];
     E.child[node] = S.tchild[t];
     const int g = S.tgrp[t];
-    int k = 0, f = t;
-    for (int v = t - 1; v >= 0; --v) if (S.tgrp[v] == g) { ++k; f = v; }
-    S.tk[t] = k; S.tfirst[t] = f;
     S.tcnt[t] = E.g_count[g]; S.tcap[t] = E.g_cap[g]; S.tbase[t] = E.g_base[g];
+  }
+  // rank within the group and the group's first entry: walk each group's
+  // list of new entries (linked in placement order through tnext)
+  for (int gs = lane; gs < PCY_GMAP_SLOTS; gs += 32) {
+    if (S.gkey[gs] < 0) continue;
+    const int f = S.ghead[gs];
+    int k = 0;
+    for (int t = f; t >= 0; t = S.tnext[t]) { S.tk[t] = k++; S.tfirst[t] = f; }
+    S.tgn[f] = k;
   }
   __syncwarp();
   bool arena_ok = true;
   for (int t = 0; t < nnew; ++t) {
     if (S.tfirst[t] != t) continue;
     const int g = S.tgrp[t];
-    int total = 0;
-    for (int v = t; v < nnew; ++v) total += (S.tgrp[v] == g);
+    const int total = S.tgn[t];
     const int cnt = S.tcnt[t], cap = S.tcap[t], base = S.tbase[t];
     int nb = base, ncap = cap;
     if (cnt + total > cap) {

@@ -21,7 +21,8 @@
 #define PCY_FMAXL 16
 #define PCY_MOD_SLOTS 2048
 #define PCY_NNEW_MAX 96    // new-node table of the large-d kernels (resolve_smem.cuh)
-#define PCY_NNEW_FAST 160  // new-node table of k_resolve2 / k_reattach2 (d <= 256), capped by shared memory
+#define PCY_NNEW_FAST 160  // new-node table of k_resolve2 (d <= 256), capped by shared memory
+#define PCY_NNEW_REA 320   // new-node table of k_reattach2 (Gram dots: no reference rows in shared memory)
 #define PCY_GMAP_SLOTS 256
 
 struct __align__(16) ChainLvl {
@@ -141,16 +142,19 @@ __global__ void k_chain2(EngDev E, const double* __restrict__ X, const double* _
 }
 
 // ------------------------------------------------------------------- K3
-struct ResolveSmem {
+template <int NT>
+struct ResolveSmemN {
   ChainLvl rb[4][PCY_FMAXL];                 // chain records: staging ring (k_resolve2) / double buffer
   int mkey[PCY_MOD_SLOTS], mchild[PCY_MOD_SLOTS];   // touched snapshot nodes
   long long mw[PCY_MOD_SLOTS];
   double mq[PCY_MOD_SLOTS], msn[PCY_MOD_SLOTS];
   int gkey[PCY_GMAP_SLOTS], ghead[PCY_GMAP_SLOTS], gtail[PCY_GMAP_SLOTS];  // groups with new members
-  int tid[PCY_NNEW_FAST], tgrp[PCY_NNEW_FAST], tchild[PCY_NNEW_FAST], tnext[PCY_NNEW_FAST];
-  int tk[PCY_NNEW_FAST], tfirst[PCY_NNEW_FAST], tcnt[PCY_NNEW_FAST], tbase[PCY_NNEW_FAST], tcap[PCY_NNEW_FAST];
-  long long tw[PCY_NNEW_FAST];
-  double trn[PCY_NNEW_FAST], tq[PCY_NNEW_FAST], tsn[PCY_NNEW_FAST];
+  int tid[NT], tgrp[NT], tchild[NT], tnext[NT];
+  int tk[NT], tfirst[NT], tcnt[NT], tbase[NT], tcap[NT];
+  int titem[NT];   // k_reattach2: batch row of the node that placed the entry (its Gram row)
+  int tgn[NT];     // k_reattach2: new entries of the group, at the group's first entry
+  long long tw[NT];
+  double trn[NT], tq[NT], tsn[NT];
   // item staging ring of k_resolve2 (producer warp -> decision warp), K3_SLOTS slots
   ChainHdr shdr[4];
   long long sw[4];
@@ -159,6 +163,8 @@ struct ResolveSmem {
   int stop_flag;
   int modcount;
 };
+using ResolveSmem = ResolveSmemN<PCY_NNEW_FAST>;
+using ReattachSmem = ResolveSmemN<PCY_NNEW_REA>;
 // dynamic tail: double slotx[4][ld], slotp[4][ld]; double tref[nnew][ld|1]; double ts[nnew][ld];
 // (k_reattach2 keeps a single xsm[ld] and no ts, see reattach_smem_bytes)
 //               unsigned mbits[NC/32+1]; unsigned gbits[GC/32+1]
@@ -167,15 +173,17 @@ __host__ __device__ inline size_t resolve_smem_bytes(int ld, int nnew, long long
   return ((sizeof(ResolveSmem) + 15) & ~size_t(15)) + sizeof(double) * ((size_t)8 * ld + (size_t)nnew * ((size_t)(ld | 1) + ld)) +
          ((sizeof(unsigned) * (size_t)(NC / 32 + 1 + GC / 32 + 1) + 15) & ~size_t(15));
 }
-// k_reattach2 keeps only the reference rows of its new entries (no s rows)
-__host__ __device__ inline size_t reattach_smem_bytes(int ld, int nnew, long long NC, long long GC) {
-  return ((sizeof(ResolveSmem) + 15) & ~size_t(15)) + sizeof(double) * ((size_t)ld + (size_t)nnew * (size_t)(ld | 1)) +
+// k_reattach2 keeps only the reference rows of its new entries (no s rows),
+// and none when the batch Gram gives their dots (trows = false)
+__host__ __device__ inline size_t reattach_smem_bytes(int ld, int nnew, long long NC, long long GC, bool trows = true) {
+  return ((sizeof(ReattachSmem) + 15) & ~size_t(15)) + sizeof(double) * ((size_t)ld + (trows ? (size_t)nnew * (size_t)(ld | 1) : 0)) +
          ((sizeof(unsigned) * (size_t)(NC / 32 + 1 + GC / 32 + 1) + 15) & ~size_t(15));
 }
 
 __device__ __forceinline__ int map_slot(int id) { return (int)(((unsigned)id * 2654435761u) >> 21) & (PCY_MOD_SLOTS - 1); }
 
-__device__ __forceinline__ int map_find(const ResolveSmem& S, int id) {
+template <class SM>
+__device__ __forceinline__ int map_find(const SM& S, int id) {
   int s = map_slot(id);
   for (;;) {
     const int k = S.mkey[s];
@@ -187,7 +195,8 @@ __device__ __forceinline__ int map_find(const ResolveSmem& S, int id) {
 
 // insert-or-update; lane 0 writes; caller syncs.  *fresh (nullable, every
 // lane) is incremented when the key was not present.
-__device__ __forceinline__ int map_put(ResolveSmem& S, unsigned* mbits, int id, long long w, double q, double sn,
+template <class SM>
+__device__ __forceinline__ int map_put(SM& S, unsigned* mbits, int id, long long w, double q, double sn,
                                        int child, int lane, int* fresh = nullptr) {
   int s = map_slot(id);
   while (S.mkey[s] >= 0 && S.mkey[s] != id) s = (s + 1) & (PCY_MOD_SLOTS - 1);
@@ -201,7 +210,8 @@ __device__ __forceinline__ int map_put(ResolveSmem& S, unsigned* mbits, int id, 
   return s;
 }
 
-__device__ __forceinline__ int gmap_find(const ResolveSmem& S, int g) {
+template <class SM>
+__device__ __forceinline__ int gmap_find(const SM& S, int g) {
   int s = (int)(((unsigned)g * 2654435761u) >> 24) & (PCY_GMAP_SLOTS - 1);
   for (;;) {
     const int k = S.gkey[s];
