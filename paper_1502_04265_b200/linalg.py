@@ -188,7 +188,8 @@ def project(a, projector: Projector) -> np.ndarray:
     if mat.shape[1] != v.shape[0]:
         raise ValueError(f"matrix has {mat.shape[1]} columns but the projector expects {v.shape[0]}")
     A = to_f64_device(mat)
-    Vd = torch.from_numpy(np.ascontiguousarray(v)).to(A.device)
+    # Projector freezes its vectors; hand torch a writable f64 copy
+    Vd = torch.as_tensor(np.array(v, dtype=np.float64, order="C", copy=True), device=A.device)
     return project_device(A, Vd).cpu().numpy()
 
 
