@@ -12,6 +12,7 @@ conventions of the QR do not matter (SURVEY.md §7 hard part 5).
 from __future__ import annotations
 
 import ctypes
+import warnings
 from dataclasses import dataclass
 
 import numpy as np
@@ -96,7 +97,13 @@ def to_f64_device(a, device=None):
         arr = np.asarray(a)
         if arr.dtype not in (np.float32, np.float64):
             arr = arr.astype(np.float64)
-        t = torch.from_numpy(np.ascontiguousarray(arr)).to(device or torch.device("cuda", torch.cuda.current_device()))
+        arr = np.ascontiguousarray(arr)
+        with warnings.catch_warnings():
+            # read-only inputs (memory-mapped stream files): the host view is
+            # only read by the H2D copy below, so no host copy is made
+            warnings.filterwarnings("ignore", message="The given NumPy array is not writable")
+            host = torch.from_numpy(arr)
+        t = host.to(device or torch.device("cuda", torch.cuda.current_device()))
     t = t.contiguous()
     if t.dtype == torch.float64:
         return t
