@@ -422,6 +422,29 @@ def main():
         h2d = work.h2d_bytes + (cs.points.nbytes + cs.weights.size * 8 + cfg.reps * cfg.k * 8 if cs is not None else 0)
         d2h = (cs.points.nbytes + cs.weights.nbytes + sum(c.nbytes + 8 for c, _ in runs)) if cs is not None else 0
 
+    # parity of this run's public-API result against the unmodified reference's
+    # output on the same bytes (tests/golden/full_<cfg>.npz, written by
+    # tests/golden/make_fullsize.py); full-size streams only
+    parity = None
+    if rank == 0 and cs is not None and args.rows in (None, cfg.n):
+        sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+        try:
+            import fullsize as FS
+            fx = FS.load(cfg.name)
+            if fx is None:
+                parity = {"checked": False, "why": f"no fixture tests/golden/full_{cfg.name}.npz"}
+            else:
+                Cr = np.stack([c for c, _ in runs])
+                cr = np.array([v for _, v in runs])
+                parity = FS.compare(fx, cs.points, cs.weights, Cr, cr, exact_points=cfg.svd_dim >= cfg.d)
+                parity.update({"checked": True, "against": f"tests/golden/full_{cfg.name}.npz (unmodified reference "
+                                                          f"run_{'piecy' if cfg.entry == 'piecy' else 'piecy_mr'} + "
+                                                          "kmeans_repetitions on the same stream bytes)",
+                               "tolerance": "weights/order exact; points bit-exact without projection, else 1e-9 "
+                                            "of row scale; costs and centres 1e-9 relative"})
+        except Exception as exc:   # a checker failure must not hide the measurement
+            parity = {"checked": False, "why": f"checker error: {exc!r}"}
+
     # full-data second pass, unweighted SSE of the whole
     # stream against every repetition's centres (evaluate_cost_multi), stream
     # resident in HBM; one GPU (it is a separate pass, not part of the step)
@@ -559,6 +582,7 @@ def main():
             "roofline": roof,
             "rooflines": rooflines,
             "full_data_eval": full_eval,
+            "parity": parity,
             "gemm_peaks": gemm_peaks,
             "cpu_baseline": cpu,
             "clocks": clk,

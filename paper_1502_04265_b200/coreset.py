@@ -219,7 +219,7 @@ class BicoEngine:
         x = torch.from_numpy(self._hb[:n]).to(self._dev, non_blocking=False)
         w = None if self._hunit else torch.from_numpy(self._hw[:n]).to(self._dev)
         self._hunit = True
-        self.insert_device(x, w)
+        self._insert_dev(x, w)
 
     def insert_block(self, points, weights=None) -> None:
         """Insert the rows of ``points`` in order (host array or CUDA tensor,
@@ -243,11 +243,26 @@ class BicoEngine:
             w = weights if isinstance(weights, torch.Tensor) else torch.from_numpy(
                 np.ascontiguousarray(np.asarray(weights, dtype=np.int64)))
             w = w.to(self._dev, dtype=torch.int64)
-        self.insert_device(x, w)
+        self._insert_dev(x, w)
 
     def insert_device(self, x, w=None, stream=None) -> int:
         """Insert rows of CUDA tensor ``x`` (n x dim, f32/f64, row stride may
-        exceed dim) with optional int64 weights ``w``.  Returns rows consumed."""
+        exceed dim) with optional int64 weights ``w``.  Returns rows consumed.
+        Rows buffered by ``insert`` go first, so the stream order holds."""
+        import torch
+        if not isinstance(x, torch.Tensor) or x.dim() != 2 or x.shape[1] != self._dim:
+            raise ValueError(f"expected a point of dimension {self._dim}")
+        if x.device != self._dev:
+            raise ValueError(f"points must be on the engine's device {self._dev}")
+        if w is not None:
+            if not isinstance(w, torch.Tensor) or w.shape != (x.shape[0],) or w.device != self._dev:
+                raise ValueError("weights must be one per point, on the engine's device")
+            if w.dtype != torch.int64:
+                w = w.to(torch.int64)
+        self._flush()
+        return self._insert_dev(x, w, stream)
+
+    def _insert_dev(self, x, w=None, stream=None) -> int:
         import torch
         n = int(x.shape[0])
         if n == 0:

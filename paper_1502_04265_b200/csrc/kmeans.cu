@@ -584,6 +584,8 @@ int pcy_lloyd(const double* P, const double* w, long long n, int d, int k, int r
   PCY_CUDA(pcy_malloc_async(&rstate, sizeof(int) * 2 * reps, st));
   std::vector<int> hstate(2 * reps);
   cudaEvent_t pe0 = nullptr, pe1 = nullptr;
+  // every exit below goes through the frees after the body
+  auto body = [&]() -> int {
   PCY_CUDA(cudaEventCreate(&pe0));
   PCY_CUDA(cudaEventCreate(&pe1));
   std::vector<int> act(reps, 1);
@@ -643,11 +645,15 @@ int pcy_lloyd(const double* P, const double* w, long long n, int d, int k, int r
     PCY_LAUNCH_CHECK();
   }
   PCY_CUDA(pcy_spin_sync(st));
+  return PCY_OK;
+  };
+  const int rc = body();
   cudaFreeAsync(pn, st); cudaFreeAsync(cn, st); cudaFreeAsync(best, st); cudaFreeAsync(assign, st);
   cudaFreeAsync(counts, st); cudaFreeAsync(cost, st); cudaFreeAsync(active, st);
   cudaFreeAsync(ppart, st); cudaFreeAsync(ppos, st); cudaFreeAsync(rstate, st);
-  cudaEventDestroy(pe0); cudaEventDestroy(pe1);
-  return PCY_OK;
+  if (pe0) cudaEventDestroy(pe0);
+  if (pe1) cudaEventDestroy(pe1);
+  return rc;
 }
 
 // weighted_cost for `reps` center sets into device memory: costs_dev (device,

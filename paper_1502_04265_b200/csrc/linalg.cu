@@ -307,10 +307,14 @@ static cublasHandle_t blas_handle() {
 static int jacobi(cudaStream_t st, double* G, int m, int n, double tol, int max_sweeps, double* sig, double* U,
                   int ldu, int* perm, int* sweeps, int* rot) {
   PCY_CUDA(cudaMemsetAsync(rot, 0, sizeof(int) * max_sweeps, st));
-  static int max_blocks = -1;
-  if (max_blocks < 0) {
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
+  // co-resident CTA limit of the cooperative launch, per device (threads of
+  // distributed.py may drive different GPUs)
+  thread_local int max_blocks_dev[16] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& max_blocks = max_blocks_dev[dev & 15];
+  if (max_blocks <= 0) {
+    int sms = 0, per = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_jacobi, 256, 0);
     max_blocks = sms * (per > 0 ? per : 1);

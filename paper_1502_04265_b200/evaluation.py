@@ -77,8 +77,11 @@ def _dev_points(points, weights, device=None):
             torch.from_numpy(np.ascontiguousarray(wts)).to(dev))
 
 
-def _uniforms(seed: int, reps: int, k: int) -> np.ndarray:
-    return np.stack([np.random.default_rng(mix_seed(seed, r)).random(k) for r in range(reps)])
+REPS_PER_LAUNCH = 64   # csrc/kmeans.cu: repetitions per seeding / Lloyd launch
+
+
+def _uniforms(seed: int, reps: int, k: int, start: int = 0) -> np.ndarray:
+    return np.stack([np.random.default_rng(mix_seed(seed, r)).random(k) for r in range(start, reps)])
 
 
 def seed_device(P, w, k: int, U: np.ndarray):
@@ -93,8 +96,16 @@ def seed_device(P, w, k: int, U: np.ndarray):
     return C
 
 
+def _check_centers(P, C) -> None:
+    """Centres (reps, k, d) must share the points' row length: the kernels take
+    d from the centres (the reference fails in sq_distances, evaluation.py:41)."""
+    if C.dim() != 3 or C.shape[2] != P.shape[1] or C.shape[1] < 1:
+        raise ValueError("centers must match the point dimension")
+
+
 def lloyd_device(P, w, C, max_iters: int, tol: float):
     """Lloyd in place on C (reps, k, d); returns per-rep cost logs."""
+    _check_centers(P, C)
     reps, k, d = C.shape
     n = P.shape[0]
     logs = np.zeros((reps, max(1, max_iters)))
@@ -107,6 +118,7 @@ def lloyd_device(P, w, C, max_iters: int, tol: float):
 
 
 def cost_device(P, w, C) -> np.ndarray:
+    _check_centers(P, C)
     reps, k, d = C.shape
     out = np.zeros(reps)
     nat.check(nat.lib().pcy_weighted_cost(nat.ptr(P), nat.ptr(w), P.shape[0], d, k, reps, nat.ptr(C),
@@ -154,6 +166,8 @@ def weighted_cost(points, weights, centers) -> float:
             return 0.0
     P, w = _dev_points(points, weights)
     ctr = np.asarray(centers, dtype=np.float64)
+    if ctr.ndim != 2 or ctr.shape[1] != P.shape[1] or ctr.shape[0] < 1:
+        raise ValueError("centers must match the point dimension")
     C = torch.from_numpy(np.ascontiguousarray(ctr)).to(P.device)[None].contiguous()
     return float(cost_device(P, w, C)[0])
 
@@ -164,8 +178,9 @@ def kmeans_repetitions(points, weights, k: int, reps: int = DEFAULT_REPETITIONS,
     """Seeding + Lloyd ``reps`` times, repetition rng = PCG64(mix_seed(seed, rep))
     (evaluation.py:199-210).  All repetitions run concurrently on the device.
     Returns [(centers, cost), ...]."""
-    runs = kmeans_repetitions_device(points, weights, k, reps, seed, max_iters, tol)
-    C, costs = runs
+    if reps <= 0:
+        return []
+    C, costs = kmeans_repetitions_device(points, weights, k, reps, seed, max_iters, tol)
     Ch = C.cpu().numpy()
     return [(Ch[r], float(costs[r])) for r in range(reps)]
 
@@ -179,12 +194,23 @@ def kmeans_repetitions_device(points, weights, k: int, reps: int = DEFAULT_REPET
         raise ValueError("cannot seed centers from an empty point set")
     if k < 1:
         raise ValueError("k must be >= 1")
-    U = _uniforms(seed, reps, k)
-    C = seed_device(P, w, k, U)
-    logs = lloyd_device(P, w, C, int(max_iters), float(tol))
-    if cost_logs is not None:
-        cost_logs.extend(logs)
-    return C, cost_device(P, w, C)
+    import torch
+    if reps <= 0:
+        return torch.empty((0, k, int(P.shape[1])), dtype=torch.float64, device=P.device), np.zeros(0)
+    # every repetition owns its PCG64(mix_seed(seed, rep)) stream, so running
+    # them in chunks of REPS_PER_LAUNCH gives the same results as one launch
+    Cs, costs = [], []
+    for r0 in range(0, reps, REPS_PER_LAUNCH):
+        U = _uniforms(seed, min(reps, r0 + REPS_PER_LAUNCH), k, start=r0)
+        C = seed_device(P, w, k, U)
+        logs = lloyd_device(P, w, C, int(max_iters), float(tol))
+        if cost_logs is not None:
+            cost_logs.extend(logs)
+        Cs.append(C)
+        costs.append(cost_device(P, w, C))
+    if len(Cs) == 1:
+        return Cs[0], costs[0]
+    return torch.cat(Cs), np.concatenate(costs)
 
 
 def _is_tensor(x) -> bool:

@@ -115,7 +115,12 @@ def to_f64_device(a, device=None):
 
 
 def check_finite_device(t) -> None:
+    """Raise ValueError if a CUDA tensor holds a non-finite entry.  The kernel
+    scans numel() contiguous f32/f64 elements, so anything else (another dtype,
+    a strided or sliced view) is first made a contiguous float64 copy."""
     import torch
+    if t.dtype not in (torch.float32, torch.float64) or not t.is_contiguous():
+        t = t.to(torch.float64).contiguous()
     flag = np.zeros(1, dtype=np.int32)
     dt = 0 if t.dtype == torch.float64 else 1
     nat.check(nat.lib().pcy_all_finite(nat.ptr(t), t.numel(), dt, flag.ctypes.data, nat.stream_ptr()),
