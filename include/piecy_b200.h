@@ -75,6 +75,14 @@ int pcy_engine_counters(void* engine, long long* out6);
 /* The same counters summed over every engine destroyed so far in the process. */
 int pcy_engine_counters_total(long long* out6);
 
+/* K1 work of the engine's chain walks (insertion and rebuild reattach), for
+ * the useful-work fraction of SURVEY.md §8d: out4 (host) = [member visits --
+ * the reference's own nearest-reference work, one d-length dot per member of
+ * every visited group (coreset.py:158-180, :324-329) --, visits served by
+ * direct fp64 scans, tensor-pipe flops of the panel contractions (3 TF32
+ * products over padded 128x128 tiles), panel launches]. */
+int pcy_engine_work(void* engine, double* out4);
+
 /* --------------------------------------------------- clustering on coreset */
 
 /* kmeanspp_seed for `reps` repetitions -- evaluation.py:56-82 with _draw :49-53.

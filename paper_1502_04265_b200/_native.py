@@ -30,6 +30,7 @@ _SIGS = {
     "pcy_engine_extract": (c_i32, [c_vp, c_vp, c_vp, c_i64, P_i64, c_vp]),
     "pcy_engine_counters": (c_i32, [c_vp, c_vp]),
     "pcy_engine_counters_total": (c_i32, [c_vp]),
+    "pcy_engine_work": (c_i32, [c_vp, c_vp]),
     # instrumentation
     "pcy_launch_count": (c_i64, []),
     "pcy_prof_enable": (c_i32, [c_i32]),

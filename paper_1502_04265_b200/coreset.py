@@ -294,6 +294,21 @@ class BicoEngine:
         keys = ("levels", "tc_rechecks", "demand_loads", "slow_capacity", "items", "max_depth")
         return {k: int(v) for k, v in zip(keys, out)}
 
+    def work(self) -> dict:
+        """K1 work counters (pcy_engine_work): member visits of the chain walks
+        (the reference's own dgemv work), those served by direct fp64 scans,
+        tensor-pipe flops of the big-group panel and its launches.  The
+        useful fraction of SURVEY.md §8d is 2*d*visits / executed flops."""
+        self._flush()
+        out = np.zeros(4, dtype=np.float64)
+        nat.check(nat.lib().pcy_engine_work(self._h, out.ctypes.data), "pcy_engine_work")
+        d = float(self._dim)
+        useful = 2.0 * d * out[0]
+        executed = 2.0 * d * out[1] + out[2]
+        return {"member_visits": int(out[0]), "direct_visits": int(out[1]), "tensor_flops": float(out[2]),
+                "panel_launches": int(out[3]), "useful_flops": useful, "executed_flops": executed,
+                "useful_fraction": useful / executed if executed > 0 else None}
+
     # -- extraction ---------------------------------------------------------
     def features_device(self):
         """(levels, weights, linear sums, square sums, references) as CUDA tensors, DFS order."""

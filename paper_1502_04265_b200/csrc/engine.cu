@@ -158,6 +158,43 @@ __device__ __forceinline__ void scan_members(const EngDev& E, const int* __restr
   }
 }
 
+// Nearest among members [0, cnt) of a small group, d <= 256 (visited-groups
+// K1): lane-per-member fp64 dots.  Each lane issues its member's whole
+// reference row (16-byte loads, up to 64 elements per pass) before the FMAs,
+// so a chunk of 32 members costs one L2 round trip instead of 32 dependent
+// warp reductions.  Part |r|^2 - 2 r.x as in coreset.py:173-176, lowest
+// position on ties.  xv: the point in shared memory (entries < d are read).
+__device__ __forceinline__ void scan_members_lane(const EngDev& E, const int* __restrict__ mem, int cnt,
+                                                  const double* __restrict__ xv, int lane, double& bp, int& bpos) {
+  const int d = E.d, ld = E.ld;
+  bp = INFINITY; bpos = 0x7fffffff;
+  for (int c0 = 0; c0 < cnt; c0 += 32) {
+    const int p = c0 + lane;
+    double part = INFINITY;
+    int pos = 0x7fffffff;
+    if (p < cnt) {
+      const int id = mem[p];
+      const double2* __restrict__ rr = reinterpret_cast<const double2*>(E.r + (long long)id * ld);
+      const double rn = E.rn[id];
+      double acc = 0.0;
+      for (int e0 = 0; e0 < d; e0 += 64) {
+        double2 v[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q) v[q] = (e0 + 2 * q < ld) ? __ldg(rr + (e0 >> 1) + q) : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          if (e0 + 2 * q < d) acc = fma(v[q].x, xv[e0 + 2 * q], acc);
+          if (e0 + 2 * q + 1 < d) acc = fma(v[q].y, xv[e0 + 2 * q + 1], acc);
+        }
+      }
+      part = radd(rn, rmul(acc, -2.0));
+      pos = p;
+    }
+    warp_argmin(part, pos);
+    if (part < bp) { bp = part; bpos = pos; }
+  }
+}
+
 // Nearest among members [0, cnt) using a precomputed parts row (full-set K1;
 // columns are the live columns, gathered per member through col_of).
 __device__ __forceinline__ void scan_parts(const double* __restrict__ prow, const int* __restrict__ col_of,
@@ -179,9 +216,12 @@ __device__ __forceinline__ void scan_parts(const double* __restrict__ prow, cons
 // result is the fp64 argmin.  *nre counts the exact re-decisions.
 template <class RDot>
 __device__ __forceinline__ void scan_parts_tc(const EngDev& E, long long i, int g, const int* __restrict__ mem,
-                                              int cnt, RDot rdot, int lane, double& bp, int& bpos, int& nre) {
-  // columns are live columns (k_tc_split_slots): gathered per member through
-  // col_of, four chunks of 32 members in flight per pass
+                                              int cnt, RDot rdot, int lane, double& bp, int& bpos, int& nre,
+                                              int pbase = -1) {
+  // pbase < 0: columns are live columns (k_tc_split_slots), gathered per
+  // member through col_of, norms slot-indexed.  pbase >= 0: the group's members
+  // are the panel columns pbase + position (k_publish_panel), norms by column.
+  // Four chunks of 32 members in flight per pass.
   const float* __restrict__ dots = E.tc_dots + i * E.tc_ldo;
   const double* __restrict__ rnc = E.tc_rnc;
   const int* __restrict__ col_of = E.col_of;
@@ -195,8 +235,9 @@ __device__ __forceinline__ void scan_parts_tc(const EngDev& E, long long i, int 
 #pragma unroll
     for (int q = 0; q < 4; ++q)
       if (jj[q] >= 0) {
-        const double rc = rnc[jj[q]];
-        U = fmin(U, rc - 2.0 * (double)dots[col_of[jj[q]]] + tau2 * sqrt(rc) * xn + 1e-300);
+        const int col = pbase >= 0 ? pbase + c0 + 32 * q + lane : col_of[jj[q]];
+        const double rc = rnc[pbase >= 0 ? col : jj[q]];
+        U = fmin(U, rc - 2.0 * (double)dots[col] + tau2 * sqrt(rc) * xn + 1e-300);
       }
   }
 #pragma unroll
@@ -212,8 +253,9 @@ __device__ __forceinline__ void scan_parts_tc(const EngDev& E, long long i, int 
     for (int q = 0; q < 4; ++q) {
       cand[q] = false;
       if (jj[q] >= 0) {
-        const double rc = rnc[jj[q]];
-        cand[q] = rc - 2.0 * (double)dots[col_of[jj[q]]] - tau2 * sqrt(rc) * xn <= U;
+        const int col = pbase >= 0 ? pbase + c0 + 32 * q + lane : col_of[jj[q]];
+        const double rc = rnc[pbase >= 0 ? col : jj[q]];
+        cand[q] = rc - 2.0 * (double)dots[col] - tau2 * sqrt(rc) * xn <= U;
       }
     }
 #pragma unroll
@@ -728,6 +770,86 @@ __global__ void k_publish(EngCtl* __restrict__ src, EngCtl* dst, long long seq, 
   if (lane == 0) t[words] = seq;
 }
 
+// Publication with the visited-groups panel (d <= 256, one CTA of 1024
+// threads): groups of at least PCY_PANEL_MIN members -- visited by many items
+// of the next K1 batch -- get consecutive panel columns in group-index order
+// (fs_gofs[g], -1 for the groups the chain walk scans directly), their member
+// slots go to fs_list in position order, and panel_n is published with the
+// counters.  The tree does not change between this publication and the next
+// K1 launch, so the panel is that launch's snapshot.
+constexpr int PCY_PANEL_MIN = 128;
+constexpr int PCY_PANEL_MAXG = 2048;   // listed big groups (later ones are scanned directly)
+__global__ void __launch_bounds__(1024) k_publish_panel(EngDev E, EngCtl* dst, long long seq) {
+  __shared__ int wsc[32], wsb[32];
+  __shared__ int big[PCY_PANEL_MAXG];
+  __shared__ int carry_c, carry_b;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  EngCtl* src = E.ctl;
+  const long long G = src->G_alloc;
+  if (tid == 0) { carry_c = 0; carry_b = 0; }
+  __syncthreads();
+  for (long long base = 0; base < G; base += 1024) {
+    const long long g = base + tid;
+    const int c = g < G ? E.g_count[g] : 0;
+    const int isb = c >= PCY_PANEL_MIN ? 1 : 0;
+    int vc = isb ? c : 0, vb = isb;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int tc = __shfl_up_sync(PCY_FULL, vc, o), tb = __shfl_up_sync(PCY_FULL, vb, o);
+      if (lane >= o) { vc += tc; vb += tb; }
+    }
+    if (lane == 31) { wsc[warp] = vc; wsb[warp] = vb; }
+    __syncthreads();
+    if (warp == 0) {
+      int uc = wsc[lane], ub = wsb[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int tc = __shfl_up_sync(PCY_FULL, uc, o), tb = __shfl_up_sync(PCY_FULL, ub, o);
+        if (lane >= o) { uc += tc; ub += tb; }
+      }
+      wsc[lane] = uc; wsb[lane] = ub;   // inclusive over warps
+    }
+    __syncthreads();
+    const int rank = carry_b + (warp ? wsb[warp - 1] : 0) + vb - isb;   // big groups before g
+    const int ofs = carry_c + (warp ? wsc[warp - 1] : 0) + vc - (isb ? c : 0);
+    if (g < G) {
+      const bool listed = isb && rank < PCY_PANEL_MAXG;
+      E.fs_gofs[g] = listed ? ofs : -1;
+      if (listed) big[rank] = (int)g;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      // columns stop at the last listed group: later big groups are scanned directly
+      const int tb = wsb[31], tcnt = wsc[31];
+      if (carry_b + tb <= PCY_PANEL_MAXG) carry_c += tcnt;
+      else if (carry_b < PCY_PANEL_MAXG) {
+        int acc = 0;   // columns of the listed groups of this tile
+        for (int k = carry_b; k < PCY_PANEL_MAXG; ++k) acc += E.g_count[big[k]];
+        carry_c += acc;
+      }
+      carry_b += tb;
+    }
+    __syncthreads();
+  }
+  const int nbig = carry_b < PCY_PANEL_MAXG ? carry_b : PCY_PANEL_MAXG;
+  for (int b = warp; b < nbig; b += 32) {
+    const int g = big[b];
+    const int c = E.g_count[g], bs = E.g_base[g], o = E.fs_gofs[g];
+    for (int p = lane; p < c; p += 32) E.fs_list[o + p] = E.arena[bs + p];
+  }
+  if (tid == 0) { src->panel_n = carry_c; src->root_count = E.g_count[0]; src->root_base = E.g_base[0]; }
+  __syncthreads();
+  if (warp == 0) {
+    const int words = (int)(offsetof(EngCtl, seq) / sizeof(long long));
+    const long long* s = reinterpret_cast<const long long*>(src);
+    volatile long long* t = reinterpret_cast<volatile long long*>(dst);
+    for (int k = lane; k < words; k += 32) t[k] = s[k];
+    __threadfence_system();
+    __syncwarp();
+    if (lane == 0) t[words] = seq;
+  }
+}
+
 // ------------------------------------------------------------- tree reset
 __global__ void k_tree_reset(EngDev E) {
   if (threadIdx.x || blockIdx.x) return;
@@ -1223,6 +1345,9 @@ struct Engine {
   double* gram_part = nullptr;                         // split-K partials of the block Gram (large d)
   int gram_split = 1;
   bool use_tc = false;                                 // full-set K1 on tcgen05 (split TF32 + recheck)
+  bool panel = false;                                  // visited-groups K1 (d <= 256): big-group panel + direct scans
+  double exec_tensor_flops = 0.0;                      // tensor-pipe flops of the panel contractions (3 TF32 products)
+  long long panel_launches = 0;
   int Kp = 0;
   double tc_tau = 0.0;
   float *tc_ahi = nullptr, *tc_alo = nullptr, *tc_bhi = nullptr, *tc_blo = nullptr, *tc_dots = nullptr;
@@ -1280,7 +1405,9 @@ struct Engine {
   // sequence number: no stream synchronisation, no wake-up latency.
   int sync_ctl(cudaStream_t st) {
     const long long want = ++seq;
-    k_publish<<<1, 32, 0, st>>>(E.ctl, ctl_map_d, want, E.g_count, E.g_base); pcy_count_launch();
+    if (panel) k_publish_panel<<<1, 1024, 0, st>>>(E, ctl_map_d, want);
+    else k_publish<<<1, 32, 0, st>>>(E.ctl, ctl_map_d, want, E.g_count, E.g_base);
+    pcy_count_launch();
     PCY_LAUNCH_CHECK();
     volatile long long* sp = &ctl_h->seq;
     for (long long spins = 0; *sp != want; ++spins) {
@@ -1436,6 +1563,10 @@ struct Engine {
         rea_gram = g;
       }
     }
+    // visited-groups K1 for d <= 256: small groups by direct fp64 scans, groups
+    // of >= PCY_PANEL_MIN members by a tcgen05 split-TF32 panel contraction
+    panel = nper >= 1 && nper <= 8 && !use_tc;
+    E.panel_gofs = panel ? E.fs_gofs : nullptr;
     if (!(ctl_h = ctl_pool_get())) { pcy_set_error("cudaHostAlloc of the control mirror failed"); return PCY_ENOMEM; }
     memset(ctl_h, 0, sizeof(EngCtl));
     PCY_CUDA(cudaHostGetDevicePointer((void**)&ctl_map_d, ctl_h, 0));
@@ -1444,6 +1575,7 @@ struct Engine {
     PCY_CUDA(cudaMemsetAsync(E.alive, 0, sizeof(int) * NC, own));
     PCY_CUDA(cudaMemsetAsync(E.g_count, 0, sizeof(int) * GC, own));
     PCY_CUDA(cudaMemsetAsync(E.g_base, 0, sizeof(int) * GC, own));
+    PCY_CUDA(cudaMemsetAsync(E.fs_gofs, 0xff, sizeof(int) * GC, own));
     PCY_CUDA(cudaMemsetAsync(E.s, 0, sizeof(double) * NC * ld, own));
     PCY_CUDA(cudaMemsetAsync(E.r, 0, sizeof(double) * NC * ld, own));
     PCY_CUDA(cudaStreamSynchronize(own));   // buffers ready for any stream
@@ -1456,6 +1588,35 @@ struct Engine {
   bool full_set(const double* A, const int* aidx, long long M, cudaStream_t st, int* rc) {
     *rc = PCY_OK;
     E.tc_dots = nullptr;
+    if (panel) {   // visited-groups K1: only the big groups' members are contracted
+      const long long NP = ctl_h->panel_n;   // published with the tree this launch walks
+      if (NP <= 0) return false;
+      const long long acap = 1024, bcap = (NC + 127) / 128 * 128;
+      if (!tc_dots) {
+        if ((*rc = alloc(tc_ahi, acap * Kp)) || (*rc = alloc(tc_alo, acap * Kp)) || (*rc = alloc(tc_bhi, bcap * Kp)) ||
+            (*rc = alloc(tc_blo, bcap * Kp)) || (*rc = alloc(tc_dots, acap * NC)) || (*rc = alloc(tc_rnc, NC)) ||
+            (*rc = alloc(tc_xn2, acap)) || (*rc = alloc(tc_c, (long long)Kp)))
+          return false;
+        if (cudaMemsetAsync(tc_bhi, 0, sizeof(float) * bcap * Kp, st) != cudaSuccess ||
+            cudaMemsetAsync(tc_blo, 0, sizeof(float) * bcap * Kp, st) != cudaSuccess ||
+            cudaMemsetAsync(tc_ahi, 0, sizeof(float) * acap * Kp, st) != cudaSuccess ||
+            cudaMemsetAsync(tc_alo, 0, sizeof(float) * acap * Kp, st) != cudaSuccess) {
+          pcy_set_error("tc buffer init failed"); *rc = PCY_ECUDA; return false;
+        }
+        if ((*rc = pcy_tc_center(A, aidx, ld, d, tc_c, st))) return false;   // the engine's centre
+      }
+      if ((*rc = pcy_tc_split(A, aidx, ld, d, M, nullptr, tc_c, tc_ahi, tc_alo, tc_xn2, st))) return false;
+      if ((*rc = pcy_tc_split(E.r, E.fs_list, ld, d, NP, nullptr, tc_c, tc_bhi, tc_blo, tc_rnc, st))) return false;
+      const bool prof = pcy_prof_enabled();
+      if (prof) PCY_CUDA(cudaEventRecord(ev[6], st));
+      if ((*rc = pcy_tc_dots(tc_ahi, tc_alo, acap, (int)M, tc_bhi, tc_blo, bcap, (int)NP, nullptr, Kp, tc_dots, NP, st)))
+        return false;
+      if (prof) { PCY_CUDA(cudaEventRecord(ev[7], st)); gemm_timed = true; gemm_flops = 2.0 * (double)M * (double)NP * d; }
+      exec_tensor_flops += 3.0 * 2.0 * (double)((M + 127) / 128 * 128) * (double)((NP + 127) / 128 * 128) * Kp;
+      ++panel_launches;
+      E.tc_dots = tc_dots; E.tc_ldo = NP; E.tc_rnc = tc_rnc; E.tc_xn2 = tc_xn2; E.tc_tau = tc_tau;
+      return false;
+    }
     const long long N = ctl_h->F_alloc;   // upper bound on the live columns (device count in ncol)
     if (!nper || N < 256 || getenv("PCY_NO_FULLSET")) return false;
     if (cols_reset) {   // recompact: every live node takes a fresh column below
@@ -1491,6 +1652,8 @@ struct Engine {
                              Kp, tc_dots, N, st)))
         return false;
       if (prof) { PCY_CUDA(cudaEventRecord(ev[7], st)); gemm_timed = true; gemm_flops = 2.0 * (double)M * (double)N * d; }
+      exec_tensor_flops += 3.0 * 2.0 * (double)((M + 127) / 128 * 128) * (double)((N + 127) / 128 * 128) * Kp;
+      ++panel_launches;
       E.tc_dots = tc_dots; E.tc_ldo = N; E.tc_rnc = tc_rnc; E.tc_xn2 = tc_xn2; E.tc_tau = tc_tau;
       return false;   // no fp64 parts matrix: K1 reads E.tc_dots
     }
@@ -1535,6 +1698,10 @@ struct Engine {
       }
       k_rb_reset<<<(unsigned)((nslots + 255) / 256), 256, 0, st>>>(E, nslots); pcy_count_launch();
       ctl_h->root_count = 0;   // fresh roots; the mirror refreshes at the next publication
+      if (panel) {   // the reattach K1 needs the panel of the emptied tree
+        const int prc = sync_ctl(st);
+        if (prc) return prc;
+      }
       const bool prof = pcy_prof_enabled();
       if (prof) PCY_CUDA(cudaEventRecord(ev[3], st));
       int rc;
@@ -1921,6 +2088,18 @@ int pcy_engine_counters(void* h, long long* out6) {
   if (getenv("PCY_DEBUG_COUNTERS"))
     fprintf(stderr, "[pcy] demand loads on the fast path %lld, nodes touched only by a new child %lld\n",
             e->ctl_h->cnt_dem_fast, e->ctl_h->cnt_touch_child);
+  return PCY_OK;
+}
+
+// K1 work of this engine's chain walks (insertion and rebuild reattach):
+// out[0] member visits (the reference's own nearest-reference work,
+// coreset.py:172: one d-length dot per visited member), out[1] the visits
+// served by direct fp64 scans, out[2] tensor-pipe flops executed by the
+// panel contractions (3 TF32 products, padded tiles), out[3] panel launches.
+int pcy_engine_work(void* h, double* out4) {
+  Engine* e = (Engine*)h;
+  out4[0] = (double)e->ctl_h->cnt_vis; out4[1] = (double)e->ctl_h->cnt_vis_direct;
+  out4[2] = e->exec_tensor_flops; out4[3] = (double)e->panel_launches;
   return PCY_OK;
 }
 

@@ -36,6 +36,11 @@ struct EngCtl {
   // loads, full capacity evaluations, items resolved
   long long cnt_levels, cnt_direct, cnt_demand, cnt_slow, cnt_items, cnt_dem_fast, cnt_touch_child;
   long long root_count, root_base;   // group 0 (copied by k_publish for the host)
+  // visited-groups K1 (d <= 256): members in the tensor-core panel (groups of
+  // >= PCY_PANEL_MIN members, k_publish_panel) and the work counters --
+  // member visits of the chain walks (the reference's own dgemv work,
+  // coreset.py:172) and the visits served by direct fp64 scans
+  long long panel_n, cnt_vis, cnt_vis_direct;
   long long seq;          // publication sequence number (mapped host mirror)
 };
 
@@ -87,6 +92,9 @@ struct EngDev {
   // column order of the full-set contraction: group g's members occupy the
   // contiguous columns [fs_gofs[g], fs_gofs[g] + g_count[g]) (fs_list = slots)
   int* fs_list; int* fs_gofs; int* fs_cnt;
+  // visited-groups K1: panel column of group g's first member, -1 when the
+  // group is scanned directly (null outside panel mode; = fs_gofs)
+  const int* panel_gofs;
   // K1 winners per level (Bmax x PCY_FMAXL ints, -1 past the record): k_plan's compact view of the chains
   int* pathj;
   // rebuild / extraction scratch

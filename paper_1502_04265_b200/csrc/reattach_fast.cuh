@@ -28,14 +28,22 @@ __global__ void k_rchain(EngDev E, const int* __restrict__ order, long long n, C
   ChainLvl* rec = R + i * PCY_FMAXL;
   double radius = T;
   int g = 0, L = 0, pred = -1, predj = -1, trunc = 0, nre = 0;
+  long long vis = 0, vdir = 0;
   for (;;) {
     const int cnt = E.g_count[g], base = E.g_base[g];
     double bp; int bpos;
-    if (E.tc_dots)   // tensor-core dots + near-tie recheck
+    const int pb = E.panel_gofs ? E.panel_gofs[g] : -1;
+    vis += cnt;
+    if (E.panel_gofs) {   // visited-groups K1: panel for big groups, direct fp64 scans otherwise
+      if (E.tc_dots && pb >= 0)
+        scan_parts_tc(E, i, g, E.arena + base, cnt,
+                      [&](int jj) { return warp_dot(E.r + (long long)jj * ld, xv, d, lane); }, lane, bp, bpos, nre, pb);
+      else { scan_members_lane(E, E.arena + base, cnt, xv, lane, bp, bpos); vdir += cnt; }
+    } else if (E.tc_dots)   // tensor-core dots + near-tie recheck
       scan_parts_tc(E, i, g, E.arena + base, cnt, [&](int jj) { return warp_dot(E.r + (long long)jj * ld, xv, d, lane); },
                     lane, bp, bpos, nre);
     else if (P) scan_parts(P + i * ldp, E.col_of, E.arena + base, cnt, lane, bp, bpos);   // parts from the DMMA contraction
-    else scan_members(E, E.arena + base, 0, cnt, xv, lane, bp, bpos);
+    else { scan_members(E, E.arena + base, 0, cnt, xv, lane, bp, bpos); vdir += cnt; }
     const int j = bpos < cnt ? E.arena[base + bpos] : -1;
     ChainLvl c = empty_level();
     c.part = bp; c.j = j; c.g = g;
@@ -70,6 +78,10 @@ __global__ void k_rchain(EngDev E, const int* __restrict__ order, long long n, C
   if (pred < 0) pred = L - 1;
   if (lane == 0) H[i] = ChainHdr{L, pred, predj, trunc};
   if (lane == 0 && nre > 0) atomicAdd((unsigned long long*)&E.ctl->cnt_direct, (unsigned long long)nre);
+  if (lane == 0) {
+    atomicAdd((unsigned long long*)&E.ctl->cnt_vis, (unsigned long long)vis);
+    if (vdir) atomicAdd((unsigned long long*)&E.ctl->cnt_vis_direct, (unsigned long long)vdir);
+  }
 }
 
 // PAR = true: CTA b reattaches the nodes of k_plan's subtree list b (the same

@@ -91,10 +91,22 @@ __global__ void k_chain2(EngDev E, const double* __restrict__ X, const double* _
   const long long rem = W ? W[i] : 1LL;
   double radius = T;
   int g = 0, L = 0, pred = -1, predj = -1, trunc = 0, nre = 0;
+  long long vis = 0, vdir = 0;   // member visits (all / direct scans)
   for (;;) {
     const int cnt = E.g_count[g], base = E.g_base[g];
     double bp; int bpos;
-    if (E.tc_dots) {   // tensor-core dots + near-tie recheck
+    // visited-groups K1 (panel mode, d <= 256): big groups from the tensor-core
+    // panel, the others by direct fp64 scans; otherwise the full-set contraction
+    const int pb = E.panel_gofs ? E.panel_gofs[g] : -1;
+    vis += cnt;
+    if (E.panel_gofs) {
+      if constexpr (WPI == 1) {
+        if (E.tc_dots && pb >= 0)
+          scan_parts_tc(E, i, g, E.arena + base, cnt, [&](int jj) { return xdot(E.r + (long long)jj * ld); }, lane,
+                        bp, bpos, nre, pb);
+        else { scan_members_lane(E, E.arena + base, cnt, xv, lane, bp, bpos); vdir += cnt; }
+      }
+    } else if (E.tc_dots) {   // tensor-core dots + near-tie recheck
       if constexpr (WPI == 1)
         scan_parts_tc(E, i, g, E.arena + base, cnt, [&](int jj) { return xdot(E.r + (long long)jj * ld); }, lane, bp,
                       bpos, nre);
@@ -103,7 +115,7 @@ __global__ void k_chain2(EngDev E, const double* __restrict__ X, const double* _
                                lane, wib, red, reinterpret_cast<int*>(red + 8), bp, bpos, nre);
     }
     else if (P) scan_parts(P + i * ldp, E.col_of, E.arena + base, cnt, lane, bp, bpos);   // DMMA parts
-    else scan_members(E, E.arena + base, 0, cnt, xv, lane, bp, bpos);
+    else { scan_members(E, E.arena + base, 0, cnt, xv, lane, bp, bpos); vdir += cnt; }
     const int j = bpos < cnt ? E.arena[base + bpos] : -1;
     ChainLvl c = empty_level();
     c.part = bp; c.j = j; c.g = g;
@@ -139,6 +151,10 @@ __global__ void k_chain2(EngDev E, const double* __restrict__ X, const double* _
   if (pred < 0) pred = L - 1;
   if (writer) H[i] = ChainHdr{L, pred, predj, trunc};
   if (writer && nre > 0) atomicAdd((unsigned long long*)&E.ctl->cnt_direct, (unsigned long long)nre);
+  if (writer) {
+    atomicAdd((unsigned long long*)&E.ctl->cnt_vis, (unsigned long long)vis);
+    if (vdir) atomicAdd((unsigned long long*)&E.ctl->cnt_vis_direct, (unsigned long long)vdir);
+  }
 }
 
 // ------------------------------------------------------------------- K3
