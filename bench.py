@@ -116,10 +116,42 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------- reference
-def cpu_run(cfg, X):
-    """One pass of the CPU restatement (oracle/) over X; returns seconds."""
-    from oracle import piecy_oracle as O
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def reference_module():
+    """The unmodified reference package installed (pip --target, no deps) into
+    baseline/_ref, or None.  It is the reference's own CPU implementation of
+    the path: pure Python BICO on one thread, numpy/OpenBLAS elsewhere."""
+    if not os.path.isdir(os.path.join(REF_DIR, "piecy")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import piecy
+    except Exception:
+        return None
+    return piecy if os.path.dirname(os.path.abspath(piecy.__file__)).startswith(REF_DIR) else None
+
+
+def cpu_run(cfg, X, kind):
+    """One pass of the CPU path over X: the unmodified reference (kind
+    "reference") or the oracle's C/numpy restatement ("port"); returns seconds."""
     t0 = time.perf_counter()
+    if kind == "reference":
+        from piecy.evaluation import kmeans_repetitions as ref_km
+        from piecy.mergereduce import MrConfig as RefMr, run_piecy_mr as ref_mr
+        from piecy.pipeline import PiecyConfig as RefPc, run_piecy as ref_piecy
+        if cfg.entry == "piecy":
+            cs = ref_piecy(iter(X), cfg.d, RefPc(k=cfg.k, piece_size=cfg.piece_size, svd_dim=cfg.svd_dim,
+                                                 coreset_size=cfg.m, seed=cfg.seed))
+        else:
+            cs = ref_mr(iter(X), cfg.d, RefMr(k=cfg.k, piece_size=cfg.piece_size, num_pieces=cfg.num_pieces,
+                                              svd_dim=cfg.svd_dim, coreset_size=cfg.m, seed=cfg.seed))
+        ref_km(cs.points, cs.weights.astype(np.float64), cfg.k, reps=cfg.reps, seed=cfg.seed,
+               max_iters=cfg.max_iters, tol=1e-4)
+        return time.perf_counter() - t0
+    from oracle import piecy_oracle as O
     if cfg.entry == "piecy":
         P, w = O.piecy(X, cfg.k, cfg.piece_size, cfg.svd_dim, cfg.m, seed=cfg.seed)
     else:
@@ -135,17 +167,42 @@ def stream_prefix(cfg, rows, n_total=None):
     return W.generate_rows(cfg.name, 0, rows, n=n_total)
 
 
-def cpu_sample(cfg, n_total, budget_s=20.0):
-    """Bounded CPU sample: the whole stream when it fits ~budget, else a prefix.
-    Returns (rows, seconds, prefix array)."""
-    probe = min(n_total, 50_000 if cfg.d <= 256 else 10_000)
+def cpu_sample(cfg, n_total, kind, budget_s=20.0):
+    """Bounded CPU sample: the whole stream when it fits ~budget, else a prefix
+    (a shorter stream of the same workload).  Returns (rows, seconds, prefix)."""
+    probe = min(n_total, (50_000 if cfg.d <= 256 else 10_000) // (10 if kind == "reference" else 1))
     Xp = stream_prefix(cfg, probe, n_total)
-    t = cpu_run(cfg, Xp)
+    t = cpu_run(cfg, Xp, kind)
     rows = n_total if t * n_total / probe <= budget_s else max(probe, int(n_total * budget_s / (t * n_total / probe)))
     if rows != probe:
         Xp = stream_prefix(cfg, rows, n_total)
-        t = cpu_run(cfg, Xp)
+        t = cpu_run(cfg, Xp, kind)
     return rows, t, Xp
+
+
+def cpu_env(kind):
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            model = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), "")
+    except OSError:
+        pass
+    blas = None
+    try:
+        cfgd = np.show_config(mode="dicts")
+        blas = cfgd.get("Build Dependencies", {}).get("blas", {})
+        blas = {k: blas.get(k) for k in ("name", "version", "openblas configuration") if k in blas}
+    except Exception:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "OPENBLAS_NUM_THREADS": os.environ.get("OPENBLAS_NUM_THREADS"),
+            "numpy": np.__version__, "blas": blas,
+            "threads": ("BICO insertion 1 Python thread (the reference is sequential); projection and clustering "
+                        f"numpy/OpenBLAS on {os.cpu_count()} threads") if kind == "reference" else
+                       (f"BICO engine in C (1 thread); projection and clustering numpy/OpenBLAS on {os.cpu_count()} threads")}
+
+
+def baseline_kind():
+    return "reference" if reference_module() is not None else "port"
 
 
 def run_reference(args, rank):
@@ -154,21 +211,28 @@ def run_reference(args, rank):
     from paper_1502_04265_b200 import workloads as W
     cfg = W.CONFIGS[args.config]
     n_total = args.rows or cfg.n
-    rows, t, Xs = cpu_sample(cfg, n_total, budget_s=max(5.0, 150.0 / max(1, args.steps)))
-    for _ in range(min(args.warmup, 1)):
-        cpu_run(cfg, Xs)
-    times = [cpu_run(cfg, Xs) for _ in range(args.steps)]
+    kind = baseline_kind()
+    # every step is the same bounded sample; warm-up equals the GPU arm's
+    per = max(3.0, 150.0 / max(1, args.steps + args.warmup))
+    rows, t, Xs = cpu_sample(cfg, n_total, kind, budget_s=per)
+    for _ in range(max(0, args.warmup - 1)):   # the sizing pass above is the first warm-up step
+        cpu_run(cfg, Xs, kind)
+    times = [cpu_run(cfg, Xs, kind) for _ in range(args.steps)]
     ms = 1000.0 * float(np.mean(times))
     val = rows / (ms / 1000.0)
     cores = os.cpu_count() or 1
+    what = ("unmodified reference (baseline/_ref piecy " + reference_module().__version__ + ")"
+            if kind == "reference" else "oracle port (C BICO + numpy)")
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "points/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": min(args.warmup, 1), "ms_per_step": ms,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": config_json(cfg, n_total, 1),
-        "cpu_baseline": {"value": val, "unit": "points/s", "cores": cores, "kind": "port",
-                         "sample": f"first {rows} of {n_total} rows of {cfg.name}; BICO engine in C "
-                                   f"(1 thread), clustering numpy/OpenBLAS ({cores} threads)"},
+        "cpu_baseline": {"value": val, "unit": "points/s", "cores": cores, "kind": kind,
+                         "sample": f"first {rows} of {n_total} rows of {cfg.name} through the {what}: "
+                                   f"{'run_piecy' if cfg.entry == 'piecy' else 'run_piecy_mr'} + "
+                                   f"kmeans_repetitions(reps={cfg.reps}) per step",
+                         **cpu_env(kind)},
         "e2e": {"value": val, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -402,6 +466,10 @@ def main():
     nat.prof_enable(False)
     ms = float(np.sum([a.elapsed_time(b) for a, b in evp]))   # profiled pass: denominators of the shares
     prof = {k: nat.prof_read(k) for k in ("resolve", "chain", "reattach")}
+    # K1 useful-work fraction: the last step's engine counters
+    work_k1 = None
+    if step_device.engine is not None and hasattr(step_device.engine, "work"):
+        work_k1 = step_device.engine.work()
     prof_x = {k: nat.prof_read(k) for k in ("gemm", "seed", "lloyd")}
 
     # e2e: public API with host buffers (H2D of the stream, D2H of coreset + centers + costs)
@@ -482,7 +550,8 @@ def main():
         except Exception:
             pass
         hbm = float(peaks.get("hbm_gbs", 6650.0))
-        peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+        peak_src = ("MEASURED_PEAKS.json hbm_gbs (driver-measured copy bandwidth)" if "hbm_gbs" in peaks
+                    else "fallback: B200_PROFILING.md HBM figure")
         # per-launch DRAM traffic from the committed ncu --set full captures
         # (profiles/ncu_traffic.json, tools/ncu_traffic.py); None when the
         # config has no capture
@@ -497,80 +566,107 @@ def main():
             ks = [v["bytes_per_launch"] for k, v in ncu_tr.get("kernels", {}).items() if pred(k)]
             return max(ks) if ks else None
 
-        # dominant kernel by device time share
-        dom = max(prof, key=lambda k: prof[k][0])
+        # Per-kernel rooflines from the engine's live event pairs (profiled pass).
+        # Peaks: HBM from MEASURED_PEAKS.json; TF32 and FP64 are not in that
+        # file, so cuBLAS GEMMs measured at start-up by this run stand in.
+        K = args.steps
+        tf32 = gemm_peaks.get("tf32_tflops")
+        fp64 = gemm_peaks.get("fp64_tflops")
+        tf32_src = "measured in this run: cuBLAS TF32 GEMM 8192^3 (MEASURED_PEAKS.json has bf16/HBM only)"
+        fp64_src = "measured in this run: cuBLAS FP64 GEMM 4096^3 (MEASURED_PEAKS.json has bf16/HBM only)"
+        if tf32 is None:
+            tf32, tf32_src = 1100.0, "fallback: TF32 ~ half the bf16 dense peak"
+        if fp64 is None:
+            fp64, fp64_src = 37.0, "fallback: B200 FP64 datasheet"
+        rooflines = []
+
+        def share(ms_):
+            return ms_ / ms if ms > 0 else None
+
+        g_ms, g_cnt, g_flops = prof_x["gemm"]
+        c_ms, c_cnt, c_units = prof["chain"]
         r_ms, r_cnt, r_units = prof["resolve"]
+        a_ms, a_cnt, a_units = prof["reattach"]
+        if g_ms > 0:
+            ach = g_flops / (g_ms / 1e3) / 1e12
+            pk = tf32 / 3.0
+            rooflines.append({"kernel": "k_tc_dots (K1 panel contraction: split-TF32 on tcgen05, big groups only)"
+                              if d <= 256 else "k_tc_dots (K1 full-set contraction, split-TF32 on tcgen05)",
+                              "bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s", "frac": ach / pk,
+                              "launches_per_step": g_cnt / K, "traffic": traffic(lambda k: k.startswith("k_tc_dots")),
+                              "ms_per_step": g_ms / K, "share_of_step": share(g_ms),
+                              "peak_source": tf32_src + " / 3 (three TF32 products per fp32-faithful product); "
+                                             "achieved = 2*M*N*d per launch (M batch rows x N panel columns)"})
+        walk_ms = max(0.0, c_ms - g_ms)
+        if c_cnt:
+            # chain walk: per item the visited members' reference rows (8d B
+            # each, from L2/HBM) -- latency-bound pointer chasing down the tree
+            vis = (work_k1 or {}).get("member_visits")
+            bytes_ = (vis * 8.0 * d) if vis else None
+            rooflines.append({"kernel": "k_chain2 (K1 chain walk: direct fp64 scans + panel reads, per-level argmin)",
+                              "bound": "hbm", "achieved": (bytes_ / (walk_ms / 1e3) / 1e9) if bytes_ and walk_ms else None,
+                              "peak": hbm, "unit": "GB/s",
+                              "frac": (bytes_ / (walk_ms / 1e3) / 1e9 / hbm) if bytes_ and walk_ms else None,
+                              "traffic": None, "ms_per_step": walk_ms / K, "share_of_step": share(walk_ms),
+                              "ns_per_item": walk_ms * 1e6 / c_units if c_units else None, "peak_source": peak_src,
+                              "note": "latency-bound (dependent loads per tree level); algorithmic bytes = member "
+                                      "visits x 8d (the reference rows the reference's dgemv reads)"})
         # K3 algorithmic bytes per point: x row read, s row read+write (fp64),
         # node scalars (w, q, sn) read+write, chain entry (id + part)
         bytes_per_pt = 8 * d * 3 + 48 + 12
         achieved = (r_units * bytes_per_pt) / (r_ms / 1e3) / 1e9 if r_ms > 0 else 0.0
-        k3 = {"kernel": "k_resolve2/3 (K3 subtree-parallel resolve + CF update, incl. k_plan)", "bound": "hbm",
-              "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-              "traffic": traffic(lambda k: k.startswith("k_resolve") and k.endswith("1>")),
-              "traffic_unit": "bytes per launch (ncu dram read+write, subtree-parallel launch)",
-              "bytes_per_launch": (r_units * bytes_per_pt / r_cnt) if r_cnt else None,
-              "peak_source": peak_src,
-              "note": "latency-bound: one CTA per k_plan domain walks its items in stream order; "
-                      "algorithmic bytes = 24*d+60 per point",
-              "ns_per_point": (r_ms * 1e6 / r_units) if r_units else None,
-              "ms_per_step": r_ms / args.steps,
-              "share_of_step": r_ms / ms if ms > 0 else None}
-        kernel_ms = {k: {"ms": v[0] / args.steps, "launches": v[1] / args.steps, "units": v[2] / args.steps}
-                     for k, v in prof.items()}
-        # north-star kernels: distance contraction (tensor), seeding (HBM), Lloyd assignment (tensor)
-        rooflines = []
-        tc = d >= 256
-        g_ms, g_cnt, g_flops = prof_x["gemm"]
-        if g_ms > 0:
-            ach = g_flops / (g_ms / 1e3) / 1e12
-            if tc:
-                pk = gemm_peaks.get("tf32_tflops", 1100.0) / 3.0
-                rooflines.append({"kernel": "k_tc_dots (K1 full-set distance contraction, split-TF32 on tcgen05)",
-                                  "bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s", "frac": ach / pk,
-                                  "launches_per_step": g_cnt / args.steps,
-                                  "traffic": traffic(lambda k: k.startswith("k_tc_dots")),
-                                  "ms_per_step": g_ms / args.steps, "share_of_step": g_ms / ms if ms > 0 else None,
-                                  "peak_source": "measured cuBLAS TF32 GEMM / 3 (three TF32 products per "
-                                                 "fp32-faithful product); achieved = 2*M*N*d per launch "
-                                                 "(M block rows x N reference slots)"})
-            else:
-                pk = gemm_peaks.get("fp64_tflops", 40.0)
-                rooflines.append({"kernel": "k_dist_tile<2> (K1 full-set distance contraction, fp64 DMMA)",
-                                  "bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s", "frac": ach / pk,
-                                  "launches_per_step": g_cnt / args.steps,
-                                  "traffic": traffic(lambda k: k == "k_dist_tile<2>"),
-                                  "ms_per_step": g_ms / args.steps, "share_of_step": g_ms / ms if ms > 0 else None,
-                                  "peak_source": "measured cuBLAS FP64 GEMM; achieved = 2*M*N*d per launch "
-                                                 "(M block rows x N reference slots)"})
+        rooflines.append({"kernel": "k_plan + k_resolve2/3 (K3 subtree-parallel resolve + CF update)", "bound": "hbm",
+                          "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                          "traffic": traffic(lambda k: k.startswith("k_resolve") and k.endswith("1>")),
+                          "traffic_unit": "bytes per launch (ncu dram read+write, subtree-parallel launch)",
+                          "bytes_per_launch": (r_units * bytes_per_pt / r_cnt) if r_cnt else None,
+                          "peak_source": peak_src,
+                          "note": "latency-bound: one CTA per k_plan domain walks its items in stream order; "
+                                  "algorithmic bytes = 24*d+60 per point",
+                          "ns_per_point": (r_ms * 1e6 / r_units) if r_units else None,
+                          "ms_per_step": r_ms / K, "share_of_step": share(r_ms)})
+        if a_ms > 0:
+            ab = a_units * (8.0 * d * 3 + 48)
+            rooflines.append({"kernel": "k_rchain + k_reattach2/3 (K4 rebuild reattach)", "bound": "hbm",
+                              "achieved": ab / (a_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+                              "frac": ab / (a_ms / 1e3) / 1e9 / hbm, "traffic": None,
+                              "ms_per_step": a_ms / K, "share_of_step": share(a_ms),
+                              "ns_per_node": a_ms * 1e6 / a_units if a_units else None, "peak_source": peak_src,
+                              "note": "latency-bound in-order reattach; algorithmic bytes = 24*d+48 per node"})
         s_ms, s_cnt, s_bytes = prof_x["seed"]
         if s_ms > 0:
             ach = s_bytes / (s_ms / 1e3) / 1e9
             rooflines.append({"kernel": "k_seed_coop (weighted k-means++, all repetitions)", "bound": "hbm",
                               "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                              "launches_per_step": s_cnt / args.steps, "traffic": None,
-                              "ms_per_step": s_ms / args.steps, "share_of_step": s_ms / ms if ms > 0 else None,
+                              "launches_per_step": s_cnt / K, "traffic": None,
+                              "ms_per_step": s_ms / K, "share_of_step": share(s_ms),
                               "peak_source": peak_src + " HBM; algorithmic bytes = (k-1)(8nd + 24n*reps + 8n)"})
         l_ms, l_cnt, l_flops = prof_x["lloyd"]
         if l_ms > 0:
             ach = l_flops / (l_ms / 1e3) / 1e12
-            pk = gemm_peaks.get("fp64_tflops", 40.0)
             rooflines.append({"kernel": "k_dist_tile<3> (Lloyd assignment, fp64 DMMA + argmin)", "bound": "tensor",
-                              "achieved": ach, "peak": pk, "unit": "TFLOP/s", "frac": ach / pk,
-                              "launches_per_step": l_cnt / args.steps, "traffic": None,
-                              "ms_per_step": l_ms / args.steps, "share_of_step": l_ms / ms if ms > 0 else None,
-                              "peak_source": "measured cuBLAS FP64 GEMM; achieved = 2*n*k*d per repetition"})
-        # the headline roofline is the single kernel with the largest share of the
-        # step (the K1 contraction and the K3 launch set are the candidates; the
-        # ncu launch list under profiles/ gives the same ranking)
-        rooflines.append(k3)
+                              "achieved": ach, "peak": fp64, "unit": "TFLOP/s", "frac": ach / fp64,
+                              "launches_per_step": l_cnt / K, "traffic": None,
+                              "ms_per_step": l_ms / K, "share_of_step": share(l_ms),
+                              "peak_source": fp64_src + "; achieved = 2*n*k*d per repetition"})
+        kernel_ms = {k: {"ms": v[0] / K, "launches": v[1] / K, "units": v[2] / K} for k, v in prof.items()}
+        # the headline roofline is the single kernel (set) with the largest
+        # measured share of the step; dominant_kernel names the same entry
         roof = max(rooflines, key=lambda r: r.get("ms_per_step") or 0.0)
+        dom = roof["kernel"]
         rooflines = [r for r in rooflines if r is not roof]
         cpu = None
         if not args.no_cpu_baseline:
-            rows, t, _ = cpu_sample(cfg, n)
-            cpu = {"value": rows / t, "unit": "points/s", "cores": os.cpu_count() or 1, "kind": "port",
-                   "sample": f"first {rows} of {n} rows of {cfg.name}, one pass; BICO in C (1 thread), "
-                             f"projection + clustering numpy/OpenBLAS"}
+            kind = baseline_kind()
+            rows, t, _ = cpu_sample(cfg, n, kind)
+            cpu = {"value": rows / t, "unit": "points/s", "cores": os.cpu_count() or 1, "kind": kind,
+                   "sample": f"first {rows} of {n} rows of {cfg.name}, one pass of "
+                             f"{'the unmodified reference (baseline/_ref)' if kind == 'reference' else 'the oracle port'}"
+                             f" incl. kmeans_repetitions", **cpu_env(kind)}
+            if kind == "reference":   # the C port beside it, same sample rule
+                rows2, t2, _ = cpu_sample(cfg, n, "port")
+                cpu["port"] = {"value": rows2 / t2, "unit": "points/s", "cores": os.cpu_count() or 1,
+                               "sample": f"first {rows2} of {n} rows, oracle/ C BICO + numpy"}
         line = {
             "metric": METRIC, "value": work.units * n / (ms_step / 1e3), "unit": "points/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
@@ -588,6 +684,7 @@ def main():
             "clocks": clk,
             "kernel_ms_per_step": kernel_ms,
             "dominant_kernel": dom,
+            "k1_work": work_k1,
             "coreset_size": int(F),
             "engine_counters": step_device.engine.counters() if step_device.engine is not None else None,
             "step_ms": ms_steps,

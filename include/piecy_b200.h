@@ -158,6 +158,25 @@ int pcy_prof_enable(int on);
 int pcy_prof_reset(void);
 int pcy_prof_read(int slot, double* ms, long long* count, long long* units);
 
+/* ------------------------------------------------------- paper generators */
+
+/* structured_with_noise -- datagen.py:104-112.  Rows (device, out, clusters*ppc
+ * x dim, leading dim ld) from numpy's Philox4x64-10 stream with key
+ * (key_lo, key_hi): base (device, clusters) = global draw index of each
+ * cluster's first point, inv (device, clusters x dim) = position of each dim
+ * in the cluster's active list or -1 (the permutation stays on the host). */
+int pcy_gen_swn(double* out, long long ld, int clusters, long long ppc, int dim, int active_dims,
+                unsigned long long key_lo, unsigned long long key_hi, const unsigned long long* base,
+                const int* inv, double noise, double spread, void* stream);
+
+/* random_cube -- datagen.py:131-135: n x cols uniforms in [-spread, spread]
+ * from draw `start` of the Philox stream. */
+int pcy_gen_cube(double* out, long long ld, long long n, long long cols, unsigned long long key_lo,
+                 unsigned long long key_hi, unsigned long long start, double spread, void* stream);
+
+/* lower_bound -- datagen.py:115-128 (deterministic nested simplices). */
+int pcy_gen_lower_bound(double* out, long long ld, int k, long long n, double spread, double noise, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -434,3 +434,96 @@ def evaluate_cost_multi(center_sets, X: np.ndarray, chunk: int = 8192) -> list:
         for i in range(len(sets)):
             totals[i] += d2[:, bounds[i]:bounds[i + 1]].min(axis=1).sum()
     return [float(t) for t in totals]
+
+
+# ------------------------------------------------------------ paper generators
+# datagen.py:15-16 draws every coordinate from numpy's Philox4x64-10 as
+# Generator.random(): output t of the stream is word t % 4 of the counter
+# block t // 4 + 1 (numpy bumps the counter before each block), u = (x >> 11)
+# * 2^-53.  Restated here in vectorised uint64 arithmetic (the third-party
+# algorithm, numpy 2.x philox.h), with the reference's own draw order.
+_PM0, _PM1 = np.uint64(0xD2E7470EE14C6C93), np.uint64(0xCA5A826395121157)
+_PW0, _PW1 = 0x9E3779B97F4A7C15, 0xBB67AE8584CAA73B
+_M32 = np.uint64(0xFFFFFFFF)
+
+
+def _mulhilo(a: np.uint64, b: np.ndarray):
+    a_lo, a_hi = a & _M32, a >> np.uint64(32)
+    b_lo, b_hi = b & _M32, b >> np.uint64(32)
+    ll = a_lo * b_lo
+    lh = a_lo * b_hi
+    hl = a_hi * b_lo
+    hh = a_hi * b_hi
+    mid = (ll >> np.uint64(32)) + (lh & _M32) + (hl & _M32)
+    hi = hh + (lh >> np.uint64(32)) + (hl >> np.uint64(32)) + (mid >> np.uint64(32))
+    return hi, a * b
+
+
+def philox_uniforms(seed: int, t: np.ndarray) -> np.ndarray:
+    """Generator(Philox(key=seed)).random() values at global draw indices t."""
+    t = np.asarray(t, dtype=np.uint64)
+    key = int(seed) & ((1 << 128) - 1)
+    k0, k1 = key & ((1 << 64) - 1), key >> 64
+    with np.errstate(over="ignore"):
+        x0 = (t >> np.uint64(2)) + np.uint64(1)
+        x1 = np.zeros_like(x0)
+        x2 = np.zeros_like(x0)
+        x3 = np.zeros_like(x0)
+        for r in range(10):
+            if r:
+                k0 = (k0 + _PW0) & ((1 << 64) - 1)
+                k1 = (k1 + _PW1) & ((1 << 64) - 1)
+            hi0, lo0 = _mulhilo(_PM0, x0)
+            hi1, lo1 = _mulhilo(_PM1, x2)
+            x0, x1, x2, x3 = hi1 ^ x1 ^ np.uint64(k0), lo1, hi0 ^ x3 ^ np.uint64(k1), lo0
+    w = np.stack([x0, x1, x2, x3])[(t & np.uint64(3)).astype(np.int64), np.arange(t.size)]
+    return (w >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
+
+
+def _centred(u, scale):
+    return (2.0 * u - 1.0) * scale
+
+
+def gen_swn(clusters, ppc, dim, active_dims, spread=10.0, noise=0.5, seed=0) -> np.ndarray:
+    """structured_with_noise (datagen.py:104-112) by global draw index: the
+    per-cluster permutation on numpy's generator, every coordinate from
+    philox_uniforms."""
+    rng = np.random.Generator(np.random.Philox(key=seed))
+    bg = rng.bit_generator
+    out = np.empty((clusters * ppc, dim))
+    per = dim + active_dims
+    for c in range(clusters):
+        active = rng.permutation(dim)[:active_dims]
+        st = bg.state
+        ctr = int(st["state"]["counter"][0]) | (int(st["state"]["counter"][1]) << 64)
+        t0 = ctr * 4 if st["buffer_pos"] >= 4 else (ctr - 1) * 4 + int(st["buffer_pos"])
+        j = np.arange(ppc, dtype=np.uint64)[:, None] * np.uint64(per)
+        noise_u = philox_uniforms(seed, (np.uint64(t0) + j + np.arange(dim, dtype=np.uint64)).ravel())
+        sig_u = philox_uniforms(seed, (np.uint64(t0 + dim) + j + np.arange(active_dims, dtype=np.uint64)).ravel())
+        blk = _centred(noise_u.reshape(ppc, dim), noise)
+        blk[:, active] = _centred(sig_u.reshape(ppc, active_dims), spread)
+        out[c * ppc:(c + 1) * ppc] = blk
+        t1 = t0 + ppc * per
+        tmp = np.random.Philox(key=seed, counter=t1 // 4)
+        if t1 % 4:
+            tmp.random_raw(t1 % 4)
+        nst = tmp.state
+        nst["has_uint32"], nst["uinteger"] = st["has_uint32"], st["uinteger"]
+        bg.state = nst
+    return out
+
+
+def gen_cube(n, spread=10.0, seed=0) -> np.ndarray:
+    """random_cube (datagen.py:131-135)."""
+    return _centred(philox_uniforms(seed, np.arange(n * n, dtype=np.uint64)).reshape(n, n), spread)
+
+
+def gen_lower_bound(k, n, spread=1000.0, noise=100.0) -> np.ndarray:
+    """lower_bound (datagen.py:115-128)."""
+    per = n // k
+    out = np.zeros((n, k + n))
+    for v in range(k):
+        for j in range(per):
+            out[v * per + j, v] = spread
+            out[v * per + j, k + v * per + j] = noise
+    return out

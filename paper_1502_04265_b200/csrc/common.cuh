@@ -20,6 +20,9 @@ cudaError_t pcy_spin_sync(cudaStream_t st);
 // Device -> host copy of a small result through a thread-local pinned
 // staging buffer, completed with pcy_spin_sync.
 cudaError_t pcy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t st);
+int pcy_launch_assign_d2_batch(const double* P, long long ldp, int n, const double* pn, const double* C, long long ldc,
+                               const double* cn, int k, int d, int reps, const int* active, double* ppart, int* ppos,
+                               int* assign, double* best, cudaStream_t st);
 int pcy_launch_assign_d2(const double* P, long long ldp, int n, const double* pn, const double* C, long long ldc,
                          const double* cn, int k, int d, double* ppart, int* ppos, int* assign, double* best,
                          cudaStream_t st);

@@ -38,7 +38,9 @@ __global__ void __launch_bounds__(128, CPA ? 5 : 1) k_dist_tile(int M, int N, in
                                                   double* __restrict__ ppart, int* __restrict__ ppos, int ntiles,
                                                   const int* __restrict__ n_dev = nullptr,
                                                   const double* __restrict__ rv = nullptr, int lower = 0,
-                                                  int kslice = 0, long long cstride = 0) {
+                                                  int kslice = 0, long long cstride = 0,
+                                                  const int* __restrict__ zactive = nullptr, long long zB = 0,
+                                                  long long zrn = 0) {
   __shared__ double As[2][DBM][DBK + 4];
   __shared__ double Bs[2][DBK][DBN + 4];
   __shared__ long long arow[DBM], brow[DBN];
@@ -53,6 +55,11 @@ __global__ void __launch_bounds__(128, CPA ? 5 : 1) k_dist_tile(int M, int N, in
   if (kslice > 0) {   // split K: slice blockIdx.z of the contraction into partial z of C
     const int kb = blockIdx.z * kslice;
     A += kb; B += kb; K = min(kslice, K - kb); C += blockIdx.z * cstride;
+  } else if (gridDim.z > 1 || zactive) {   // batch z (Lloyd: one centre set per repetition)
+    const int z = blockIdx.z;
+    if (zactive && !zactive[z]) return;
+    B += z * zB; rn += z * zrn;
+    ppart += (long long)z * M * ntiles; ppos += (long long)z * M * ntiles;
   }
   if (n_dev) { N = min(N, *n_dev); if (n0 >= N) return; }
   if (tid < DBM) {
@@ -206,10 +213,17 @@ __global__ void k_gram_sum(const double* __restrict__ part, int S, long long pst
 }
 
 __global__ void k_argmin_reduce(int M, int ntiles, const double* __restrict__ ppart, const int* __restrict__ ppos,
-                                int* __restrict__ out_pos, double* __restrict__ out_part) {
+                                int* __restrict__ out_pos, double* __restrict__ out_part,
+                                const int* __restrict__ zactive = nullptr) {
   const int lane = threadIdx.x & 31;
   const int m = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (m >= M) return;
+  if (gridDim.y > 1 || zactive) {   // batch y (one repetition per y)
+    const int z = blockIdx.y;
+    if (zactive && !zactive[z]) return;
+    ppart += (long long)z * M * ntiles; ppos += (long long)z * M * ntiles;
+    out_pos += (long long)z * M; out_part += (long long)z * M;
+  }
   double bp = INFINITY; int bc = 0x7fffffff;
   for (int t = lane; t < ntiles; t += 32) {
     const double p = ppart[(long long)m * ntiles + t];
@@ -305,6 +319,25 @@ int pcy_launch_assign_d2(const double* P, long long ldp, int n, const double* pn
                                       nullptr, pn);
   pcy_count_launch();
   k_argmin_reduce<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(n, ntiles, ppart, ppos, assign, best);
+  pcy_count_launch();
+  PCY_LAUNCH_CHECK();
+  return PCY_OK;
+}
+
+// Batched Lloyd assignment: repetition z uses centres C + z*k*ldc and norms
+// cn + z*k, writes assign/best + z*n; repetitions with active[z] == 0 skip.
+// Scratch ppart / ppos of reps x n x ceil(k/64).
+int pcy_launch_assign_d2_batch(const double* P, long long ldp, int n, const double* pn, const double* C, long long ldc,
+                               const double* cn, int k, int d, int reps, const int* active, double* ppart, int* ppos,
+                               int* assign, double* best, cudaStream_t st) {
+  if (n <= 0 || k <= 0 || reps <= 0) return PCY_OK;
+  const int ntiles = (k + DBN - 1) / DBN;
+  dim3 grid((unsigned)ntiles, (unsigned)((n + DBM - 1) / DBM), (unsigned)reps);
+  k_dist_tile<3, true><<<grid, 128, 0, st>>>(n, k, d, P, nullptr, ldp, C, nullptr, ldc, cn, nullptr, 0, ppart, ppos, ntiles,
+                                      nullptr, pn, 0, 0, 0, active, (long long)k * ldc, (long long)k);
+  pcy_count_launch();
+  k_argmin_reduce<<<dim3((unsigned)((n + 7) / 8), (unsigned)reps), 256, 0, st>>>(n, ntiles, ppart, ppos, assign, best,
+                                                                              active);
   pcy_count_launch();
   PCY_LAUNCH_CHECK();
   return PCY_OK;

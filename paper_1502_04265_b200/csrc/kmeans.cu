@@ -394,6 +394,115 @@ __global__ void __launch_bounds__(KM_THREADS) k_counts_empty(const double* __res
   if (threadIdx.x == 0) { rep_state[2 * rep] = emp; rep_state[2 * rep + 1] = far; }
 }
 
+// One Lloyd iteration's tail for every repetition, one CTA per repetition
+// (KM_THREADS threads), no host round trip (evaluation.py:109-131):
+//  * empty-cluster repair rounds until every centre is occupied or no point
+//    has positive weighted distance: lowest empty centre <- first argmax of
+//    w * best, points strictly closer (diff form) move to it, the far point
+//    sits on it;
+//  * cost = w . best (the fixed association of k_cost);
+//  * the stop rule: the cost is logged, then prev - cost <= tol * prev clears
+//    active (the centroid update of this iteration is skipped, as the
+//    reference breaks before it); otherwise prev = cost.
+// The last CTA to finish writes the number of still-active repetitions to
+// flag[it] (mapped host memory) so the host can stop launching iterations.
+__global__ void __launch_bounds__(KM_THREADS) k_lloyd_tail(const double* __restrict__ P, const double* __restrict__ w,
+                                                          long long n, int d, int k, double* __restrict__ centers,
+                                                          int* __restrict__ active, int* __restrict__ assign_all,
+                                                          double* __restrict__ best_all, int* __restrict__ counts_all,
+                                                          int use_smem_counts, double* __restrict__ prev,
+                                                          double* __restrict__ logs, int* __restrict__ iters,
+                                                          int max_iters, int it, double tol,
+                                                          unsigned int* __restrict__ ticket,
+                                                          volatile int* __restrict__ flag, int reps) {
+  extern __shared__ int s_counts[];
+  __shared__ int s_empty, s_far;
+  __shared__ double s_gmax;
+  __shared__ double wg[32];
+  __shared__ long long wi[32];
+  __shared__ double red[72];
+  const int rep = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+  const bool act = active[rep] != 0;
+  if (act) {
+    int* assign = assign_all + (long long)rep * n;
+    double* best = best_all + (long long)rep * n;
+    int* counts = use_smem_counts ? s_counts : counts_all + (long long)rep * k;
+    double* C = centers + (long long)rep * k * d;
+    for (;;) {
+      for (int j = tid; j < k; j += blockDim.x) counts[j] = 0;
+      if (tid == 0) s_empty = 0x7fffffff;
+      __syncthreads();
+      for (long long i = tid; i < n; i += blockDim.x) atomicAdd(&counts[assign[i]], 1);
+      __syncthreads();
+      for (int j = tid; j < k; j += blockDim.x)
+        if (counts[j] == 0) atomicMin(&s_empty, j);
+      __syncthreads();
+      if (s_empty == 0x7fffffff) break;
+      double gv = -INFINITY; long long gi = 0x7fffffffffffLL;
+      for (long long i = tid; i < n; i += blockDim.x) {
+        const double g = rmul(w[i], best[i]);
+        if (g > gv) { gv = g; gi = i; }
+      }
+      for (int o = 16; o >= 1; o >>= 1) {
+        const double og = __shfl_xor_sync(PCY_FULL, gv, o);
+        const long long oi = __shfl_xor_sync(PCY_FULL, gi, o);
+        if (og > gv || (og == gv && oi < gi)) { gv = og; gi = oi; }
+      }
+      if (lane == 0) { wg[warp] = gv; wi[warp] = gi; }
+      __syncthreads();
+      if (tid == 0) {
+        double bg = -INFINITY; long long bi = 0x7fffffffffffLL;
+        for (int t = 0; t < nwarp; ++t)
+          if (wg[t] > bg || (wg[t] == bg && wi[t] < bi)) { bg = wg[t]; bi = wi[t]; }
+        s_gmax = bg; s_far = (int)bi;
+      }
+      __syncthreads();
+      if (!(s_gmax > 0.0)) break;   // every point already sits on a centre
+      const int emp = s_empty, far = s_far;
+      for (int e = tid; e < d; e += blockDim.x) C[(long long)emp * d + e] = P[(long long)far * d + e];
+      __syncthreads();
+      const double* c = C + (long long)emp * d;
+      for (long long i = warp; i < n; i += nwarp) {
+        const double* p = P + i * d;
+        double acc = 0.0;
+        for (int e = lane; e < d; e += 32) { const double df = rsub(p[e], c[e]); acc = fma(df, df, acc); }
+        acc = warp_sum(acc);
+        if (lane == 0) {
+          if (i == far) { assign[i] = emp; best[i] = 0.0; }
+          else if (acc < best[i]) { assign[i] = emp; best[i] = acc; }
+        }
+      }
+      __syncthreads();
+    }
+    // cost (same association as k_cost)
+    const long long per = (n + blockDim.x - 1) / blockDim.x;
+    const long long a = (long long)tid * per, b = min(n, a + per);
+    double loc = 0.0;
+    for (long long i = a; i < b; ++i) loc = fma(w[i], best[i], loc);
+    const double cost = block_sum(loc, red);
+    if (tid == 0) {
+      logs[(long long)rep * max_iters + it] = cost;
+      iters[rep] = it + 1;
+      const double pv = prev[rep];
+      if (isfinite(pv) && pv - cost <= tol * pv) active[rep] = 0;
+      else prev[rep] = cost;
+    }
+  }
+  if (tid == 0) {
+    __threadfence();
+    const unsigned int t = atomicAdd(ticket, 1u);
+    if (t == (unsigned)reps - 1) {   // last repetition of this iteration: publish
+      __threadfence();
+      int na = 0;
+      for (int r = 0; r < reps; ++r) na += ((volatile int*)active)[r] != 0;
+      *ticket = 0u;
+      flag[it] = na;
+      __threadfence_system();
+    }
+  }
+}
+
 // Points closer to the re-seeded centre move to it (diff form); the far point
 // itself sits on it.  Grid over points x repetitions, warp per point.
 __global__ void k_repair_dist(const double* __restrict__ P, long long n, int d, int k,
@@ -565,92 +674,121 @@ int pcy_kmeanspp(const double* P, const double* w, long long n, int d, int k, in
 // Weighted Lloyd for `reps` center sets (centers updated in place).
 // cost_log (host, reps x max_iters, nullable) receives the per-iteration
 // costs; iters_out (host, reps) the number of logged costs.
+// Per iteration: centre norms, one batched assignment launch for all
+// repetitions (DMMA + argmin), k_lloyd_tail (repair, cost, stop rule on the
+// device) and the centroid update -- the host never reads device state inside
+// the loop; it polls the mapped per-iteration active count LAG iterations
+// behind and stops launching once every repetition has converged (the at most
+// LAG extra iterations find no active repetition and exit at once).
 int pcy_lloyd(const double* P, const double* w, long long n, int d, int k, int reps, double* centers,
               int max_iters, double tol, double* cost_log, int* iters_out, void* stream) {
   if (n < 1 || k < 1 || d < 1 || reps < 1) { pcy_set_error("lloyd: bad sizes"); return PCY_EINVAL; }
   cudaStream_t st = (cudaStream_t)stream;
-  double *pn = nullptr, *cn = nullptr, *best = nullptr, *cost = nullptr; int *assign = nullptr, *counts = nullptr, *active = nullptr;
-  PCY_CUDA(pcy_malloc_async(&pn, sizeof(double) * n, st));
-  PCY_CUDA(pcy_malloc_async(&cn, sizeof(double) * k * reps, st));
-  PCY_CUDA(pcy_malloc_async(&best, sizeof(double) * n * reps, st));
-  PCY_CUDA(pcy_malloc_async(&assign, sizeof(int) * n * reps, st));
-  PCY_CUDA(pcy_malloc_async(&counts, sizeof(int) * k * reps, st));
-  PCY_CUDA(pcy_malloc_async(&cost, sizeof(double) * reps, st));
-  PCY_CUDA(pcy_malloc_async(&active, sizeof(int) * reps, st));
-  const int ntiles = (k + 63) / 64;
-  double* ppart = nullptr; int* ppos = nullptr; int* rstate = nullptr;
-  PCY_CUDA(pcy_malloc_async(&ppart, sizeof(double) * n * ntiles, st));
-  PCY_CUDA(pcy_malloc_async(&ppos, sizeof(int) * n * ntiles, st));
-  PCY_CUDA(pcy_malloc_async(&rstate, sizeof(int) * 2 * reps, st));
-  std::vector<int> hstate(2 * reps);
-  cudaEvent_t pe0 = nullptr, pe1 = nullptr;
-  // every exit below goes through the frees after the body
-  auto body = [&]() -> int {
-  PCY_CUDA(cudaEventCreate(&pe0));
-  PCY_CUDA(cudaEventCreate(&pe1));
-  std::vector<int> act(reps, 1);
-  std::vector<double> prev(reps, INFINITY), hc(reps);
   for (int r = 0; r < reps; ++r) iters_out[r] = 0;
-  k_rownorm<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(P, n, d, pn); pcy_count_launch();
-  const size_t usm = sizeof(double) * d;
-  PCY_CUDA(cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usm));
-  for (int it = 0; it < max_iters; ++it) {
-    int nact = 0;
-    for (int r = 0; r < reps; ++r) nact += act[r];
-    if (!nact) break;
-    PCY_CUDA(cudaMemcpyAsync(active, act.data(), sizeof(int) * reps, cudaMemcpyHostToDevice, st));
-    k_rownorm<<<(unsigned)((k * reps + 7) / 8), 256, 0, st>>>(centers, (long long)k * reps, d, cn); pcy_count_launch();
+  if (max_iters <= 0) return PCY_OK;
+  const int ntiles = (k + 63) / 64;
+  double *pn = nullptr, *cn = nullptr, *best = nullptr, *prev = nullptr, *logs = nullptr, *ppart = nullptr;
+  int *assign = nullptr, *counts = nullptr, *active = nullptr, *iters = nullptr, *ppos = nullptr;
+  unsigned int* ticket = nullptr;
+  int* flag_h = nullptr;
+  int* flag_d = nullptr;
+  cudaEvent_t pe0 = nullptr, pe1 = nullptr;
+  const bool smem_counts = (size_t)k * sizeof(int) <= 64 * 1024;
+  auto body = [&]() -> int {
+    PCY_CUDA(pcy_malloc_async(&pn, sizeof(double) * n, st));
+    PCY_CUDA(pcy_malloc_async(&cn, sizeof(double) * k * reps, st));
+    PCY_CUDA(pcy_malloc_async(&best, sizeof(double) * n * reps, st));
+    PCY_CUDA(pcy_malloc_async(&assign, sizeof(int) * n * reps, st));
+    if (!smem_counts) PCY_CUDA(pcy_malloc_async(&counts, sizeof(int) * k * reps, st));
+    PCY_CUDA(pcy_malloc_async(&active, sizeof(int) * reps, st));
+    PCY_CUDA(pcy_malloc_async(&prev, sizeof(double) * reps, st));
+    PCY_CUDA(pcy_malloc_async(&logs, sizeof(double) * reps * max_iters, st));
+    PCY_CUDA(pcy_malloc_async(&iters, sizeof(int) * reps, st));
+    PCY_CUDA(pcy_malloc_async(&ticket, sizeof(unsigned int), st));
+    PCY_CUDA(pcy_malloc_async(&ppart, sizeof(double) * n * ntiles * reps, st));
+    PCY_CUDA(pcy_malloc_async(&ppos, sizeof(int) * n * ntiles * reps, st));
+    {   // per-thread mapped flag buffer, kept across calls (no host-alloc per call)
+      static thread_local int* fbuf = nullptr;
+      static thread_local int fcap = 0;
+      if (fcap < max_iters) {
+        if (fbuf) cudaFreeHost(fbuf);
+        fbuf = nullptr; fcap = 0;
+        int c = 128; while (c < max_iters) c *= 2;
+        PCY_CUDA(cudaHostAlloc((void**)&fbuf, sizeof(int) * c, cudaHostAllocMapped | cudaHostAllocPortable));
+        fcap = c;
+      }
+      flag_h = fbuf;
+    }
+    for (int t = 0; t < max_iters; ++t) flag_h[t] = -1;
+    PCY_CUDA(cudaHostGetDevicePointer((void**)&flag_d, flag_h, 0));
+    {
+      std::vector<int> one(reps, 1);
+      std::vector<double> inf(reps, INFINITY);
+      PCY_CUDA(cudaMemcpyAsync(active, one.data(), sizeof(int) * reps, cudaMemcpyHostToDevice, st));
+      PCY_CUDA(cudaMemcpyAsync(prev, inf.data(), sizeof(double) * reps, cudaMemcpyHostToDevice, st));
+      PCY_CUDA(cudaMemsetAsync(iters, 0, sizeof(int) * reps, st));
+      PCY_CUDA(cudaMemsetAsync(ticket, 0, sizeof(unsigned int), st));
+      PCY_CUDA(cudaStreamSynchronize(st));   // the host vectors go out of scope
+    }
+    PCY_CUDA(cudaEventCreate(&pe0));
+    PCY_CUDA(cudaEventCreate(&pe1));
+    k_rownorm<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(P, n, d, pn); pcy_count_launch();
+    const size_t usm = sizeof(double) * d;
+    PCY_CUDA(cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usm));
+    const size_t tsm = smem_counts ? sizeof(int) * (size_t)k : 0;
+    if (tsm > 48 * 1024) PCY_CUDA(cudaFuncSetAttribute(k_lloyd_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
     const bool prof = pcy_prof_enabled();
-    if (prof) cudaEventRecord(pe0, st);
-    int nassign = 0;
-    for (int r = 0; r < reps; ++r) {
-      if (!act[r]) continue;
-      int rc = pcy_launch_assign_d2(P, d, (int)n, pn, centers + (long long)r * k * d, d, cn + (long long)r * k, k, d,
-                                    ppart, ppos, assign + (long long)r * n, best + (long long)r * n, st);
+    float t_assign = 0.f;
+    long long n_assign = 0;
+    constexpr int LAG = 2;
+    for (int it = 0; it < max_iters; ++it) {
+      if (it >= LAG) {   // iteration it - LAG has finished once its flag is set
+        volatile int* f = flag_h + (it - LAG);
+        for (long long spins = 0; *f < 0; ++spins) {
+          if ((spins & 1023) == 1023) {
+            const cudaError_t e = cudaStreamQuery(st);
+            if (e != cudaSuccess && e != cudaErrorNotReady) { pcy_set_error("lloyd: %s", cudaGetErrorString(e)); return PCY_ECUDA; }
+          }
+        }
+        if (*f == 0) break;   // every repetition stopped
+      }
+      k_rownorm<<<(unsigned)((k * reps + 7) / 8), 256, 0, st>>>(centers, (long long)k * reps, d, cn); pcy_count_launch();
+      if (prof) cudaEventRecord(pe0, st);
+      int rc = pcy_launch_assign_d2_batch(P, d, (int)n, pn, centers, d, cn, k, d, reps, active, ppart, ppos, assign,
+                                          best, st);
       if (rc) return rc;
-      ++nassign;
-    }
-    if (prof) cudaEventRecord(pe1, st);
-    // empty-cluster repair rounds until no repetition has an empty centre
-    for (;;) {
-      k_counts_empty<<<reps, KM_THREADS, 0, st>>>(P, w, n, d, k, centers, active, assign, best, counts, rstate);
+      if (prof) {
+        cudaEventRecord(pe1, st);
+        cudaEventSynchronize(pe1);
+        float t = 0.f;
+        cudaEventElapsedTime(&t, pe0, pe1);
+        t_assign += t;
+        n_assign += reps;   // launched repetitions (inactive ones exit at once)
+      }
+      k_lloyd_tail<<<reps, KM_THREADS, tsm, st>>>(P, w, n, d, k, centers, active, assign, best, counts,
+                                                  smem_counts ? 1 : 0, prev, logs, iters, max_iters, it, tol, ticket,
+                                                  flag_d, reps);
       pcy_count_launch();
-      PCY_CUDA(pcy_d2h(hstate.data(), rstate, sizeof(int) * 2 * reps, st));
-      bool any = false;
-      for (int r = 0; r < reps; ++r) any |= hstate[2 * r] >= 0;
-      if (!any) break;
-      k_repair_dist<<<dim3((unsigned)((n + 7) / 8), reps), 256, 0, st>>>(P, n, d, k, centers, rstate, assign, best);
-      pcy_count_launch();
+      k_update<<<dim3(k, reps), KU_THREADS, usm, st>>>(P, w, n, d, k, active, assign, centers); pcy_count_launch();
+      PCY_LAUNCH_CHECK();
     }
-    k_cost<<<reps, KM_THREADS, 0, st>>>(w, n, active, best, cost); pcy_count_launch();
-    PCY_LAUNCH_CHECK();
-    PCY_CUDA(pcy_d2h(hc.data(), cost, sizeof(double) * reps, st));
-    if (prof) {
-      float t = 0.f;
-      cudaEventElapsedTime(&t, pe0, pe1);
-      pcy_prof_add(PCY_PROF_LLOYD, t, (long long)(2.0 * (double)n * k * d * nassign));
-    }
-    bool any_update = false;
+    if (prof) pcy_prof_add(PCY_PROF_LLOYD, t_assign, (long long)(2.0 * (double)n * k * d * (double)n_assign));
+    std::vector<double> hl((size_t)reps * max_iters);
+    std::vector<int> hi(reps);
+    PCY_CUDA(pcy_d2h(hl.data(), logs, sizeof(double) * hl.size(), st));
+    PCY_CUDA(pcy_d2h(hi.data(), iters, sizeof(int) * reps, st));
     for (int r = 0; r < reps; ++r) {
-      if (!act[r]) continue;
-      if (cost_log) cost_log[(size_t)r * max_iters + it] = hc[r];
-      iters_out[r] = it + 1;
-      if (std::isfinite(prev[r]) && prev[r] - hc[r] <= tol * prev[r]) { act[r] = 0; continue; }
-      prev[r] = hc[r];
-      any_update = true;
+      iters_out[r] = hi[r];
+      if (cost_log)
+        for (int t = 0; t < hi[r]; ++t) cost_log[(size_t)r * max_iters + t] = hl[(size_t)r * max_iters + t];
     }
-    if (!any_update) break;
-    PCY_CUDA(cudaMemcpyAsync(active, act.data(), sizeof(int) * reps, cudaMemcpyHostToDevice, st));
-    k_update<<<dim3(k, reps), KU_THREADS, usm, st>>>(P, w, n, d, k, active, assign, centers); pcy_count_launch();
-    PCY_LAUNCH_CHECK();
-  }
-  PCY_CUDA(pcy_spin_sync(st));
-  return PCY_OK;
+    return PCY_OK;
   };
   const int rc = body();
   cudaFreeAsync(pn, st); cudaFreeAsync(cn, st); cudaFreeAsync(best, st); cudaFreeAsync(assign, st);
-  cudaFreeAsync(counts, st); cudaFreeAsync(cost, st); cudaFreeAsync(active, st);
-  cudaFreeAsync(ppart, st); cudaFreeAsync(ppos, st); cudaFreeAsync(rstate, st);
+  if (counts) cudaFreeAsync(counts, st);
+  cudaFreeAsync(active, st); cudaFreeAsync(prev, st); cudaFreeAsync(logs, st); cudaFreeAsync(iters, st);
+  cudaFreeAsync(ticket, st); cudaFreeAsync(ppart, st); cudaFreeAsync(ppos, st);
   if (pe0) cudaEventDestroy(pe0);
   if (pe1) cudaEventDestroy(pe1);
   return rc;
