@@ -1,0 +1,11 @@
+"""piecy.coreset -> paper_1502_04265_b200.coreset (drop-in under test)."""
+import sys
+
+from paper_1502_04265_b200 import coreset as _m
+from paper_1502_04265_b200.coreset import *  # noqa: F401,F403
+
+# the module's public names, underscored helpers included, as the reference's tests see them
+_self = sys.modules[__name__]
+for _k, _v in vars(_m).items():
+    if not _k.startswith("__") and not hasattr(_self, _k):
+        setattr(_self, _k, _v)
