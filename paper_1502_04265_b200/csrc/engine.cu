@@ -1766,7 +1766,11 @@ struct Engine {
           if (getenv("PCY_DEBUG_REBUILD"))
             fprintf(stderr, "[pcy] reattach launch: off %lld nb %lld status %d stop %lld F %lld nnew_cap %d\n", off, nb,
                     ctl_h->status, ctl_h->stop, ctl_h->F, nnew_cap);
-          if (ctl_h->status == ST_PAR_BROKEN) { pcy_set_error("subtree-parallel reattach met an excluded stop"); return PCY_ESTATE; }
+          if (ctl_h->status == ST_PAR_BROKEN) {
+            pcy_set_error("subtree-parallel reattach met an excluded stop (inner status %d, window %lld, F %lld, m %lld)",
+                          ctl_h->err, ctl_h->stop, ctl_h->F, m);
+            return PCY_ESTATE;
+          }
           if (ctl_h->status == ST_FULL) {
             if (ctl_h->stop == 0) { pcy_set_error("reattach made no progress"); return PCY_ESTATE; }
             off += ctl_h->stop;
@@ -1916,7 +1920,11 @@ struct Engine {
         }
         if (status == ST_INVALID) { *bad_at = off + start + ctl_h->stop; *bad_code = ctl_h->err; return PCY_OK; }
         if (status == ST_ARENA) { pcy_set_error("member arena exhausted"); return PCY_ESTATE; }
-        if (status == ST_PAR_BROKEN) { pcy_set_error("subtree-parallel resolve met an excluded stop"); return PCY_ESTATE; }
+        if (status == ST_PAR_BROKEN) {
+          pcy_set_error("subtree-parallel resolve met an excluded stop (inner status %d, window %lld of %lld, F %lld, m %lld, weighted %d)",
+                        ctl_h->err, ctl_h->stop, kn, ctl_h->F, m, W ? 1 : 0);
+          return PCY_ESTATE;
+        }
         if (status == ST_FULL) {
           if (ctl_h->stop == 0) { pcy_set_error("resolve made no progress"); return PCY_ESTATE; }
           start += ctl_h->stop; first_rem = -1;

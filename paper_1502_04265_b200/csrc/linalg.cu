@@ -39,6 +39,8 @@ __global__ void k_gram_prep(double* __restrict__ G, int r, double shift, int exp
     const bool diag = (e / r) == (e % r);
     if (expect_identity && fabs(G[e] - (diag ? 1.0 : 0.0)) > 1e-3) atomicOr(status, 1);
     if (diag && shift != 0.0) G[e] += shift;
+    if (diag)   // nonnegative doubles order like their bit patterns
+      atomicMax(reinterpret_cast<unsigned long long*>(status + 2), (unsigned long long)__double_as_longlong(fabs(G[e])));
   }
 }
 
@@ -49,9 +51,14 @@ __global__ void __launch_bounds__(256) k_chol_diag(double* __restrict__ A, int l
                                                    int* __restrict__ status) {
   __shared__ double a[CHB][CHB + 1];
   __shared__ int bad;
+  __shared__ double gmax;
   const int tid = threadIdx.x;
   double* blk = A + (long long)k0 * lda + k0;
-  if (tid == 0) bad = 0;
+  if (tid == 0) {
+    bad = 0;
+    // largest diagonal of the original Gram (k_gram_prep): the scale of a rounding-level pivot
+    gmax = __longlong_as_double(*reinterpret_cast<const long long*>(status + 2));
+  }
   for (int e = tid; e < kb * kb; e += blockDim.x) {
     const int c = e / kb, rr = e % kb;      // column-major: element (rr, c) at blk[c*lda + rr]
     a[rr][c] = blk[(long long)c * lda + rr];
@@ -60,7 +67,9 @@ __global__ void __launch_bounds__(256) k_chol_diag(double* __restrict__ A, int l
   for (int j = 0; j < kb; ++j) {
     if (tid == 0) {
       const double t = a[j][j];
-      if (!(t > 0.0) || !isfinite(t)) bad = 1;
+      // a pivot at rounding level of the Gram's scale: the sketch is rank
+      // deficient and CholeskyQR would amplify noise -- use the CGS2 path
+      if (!(t > 0.0) || !isfinite(t) || t <= 16.0 * 2.220446049250313e-16 * gmax) bad = 1;
       a[j][j] = sqrt(fmax(t, 1e-300));
     }
     __syncthreads();
@@ -140,8 +149,10 @@ __global__ void __launch_bounds__(1024) k_cgs2(double* __restrict__ Y, long long
         if (nrm > 0.5) break;
       }
     }
-    const double inv = 1.0 / nrm;
-    for (long long i = tid; i < rows; i += blockDim.x) Y[i * r + j] *= inv;
+    // true division (not a reciprocal multiply): a column c * e normalises to
+    // exactly +-e / |e| whatever c is, so degenerate (duplicated-row) sketches
+    // give the same basis for every seed, as LAPACK's Householder QR does
+    for (long long i = tid; i < rows; i += blockDim.x) Y[i * r + j] /= nrm;
     __syncthreads();
   }
   if (tid == 0) status[0] = 0;
@@ -222,8 +233,7 @@ __global__ void __launch_bounds__(256) k_jacobi(double* __restrict__ G, int m, i
     const int j = perm[jj];
     const double* gj = G + (long long)j * m;
     const double sj = sig[j];
-    const double inv = sj > 0.0 ? 1.0 / sj : 0.0;
-    for (int i = lane; i < m; i += 32) U[(long long)i * ldu + jj] = gj[i] * inv;
+    for (int i = lane; i < m; i += 32) U[(long long)i * ldu + jj] = sj > 0.0 ? gj[i] / sj : 0.0;
   }
   if (gt == 0) *sweeps_out = sweep;
 }
@@ -350,7 +360,7 @@ static int cholqr(cudaStream_t st, double* Y, long long rows, int r, double* Gs,
   auto pass = [&](double shift, int* ok, int check) -> int {
     int rc;
     if ((rc = gemm(st, r, r, (int)rows, 1.0, Y, r, 1, Y, r, 0, 0.0, Gs, r))) return rc;
-    PCY_CUDA(cudaMemsetAsync(status, 0, sizeof(int), st));
+    PCY_CUDA(cudaMemsetAsync(status, 0, sizeof(int) * 4, st));   // flag + the Gram's diagonal max (status + 2)
     k_gram_prep<<<(unsigned)std::min((r * r + 255) / 256, 148 * 4), 256, 0, st>>>(Gs, r, shift, check, status);
     pcy_count_launch();
     // blocked right-looking Cholesky, lower, column-major (Gs symmetric)

@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(32, 1) k_reattach2(EngDev E, const int* __rest
   if constexpr (PAR) {
     if (lane == 0) {
       using ull = unsigned long long;
-      if (status != ST_DONE) atomicExch(&par->arena_fail, status == ST_ARENA ? ST_ARENA : ST_PAR_BROKEN);
+      if (status != ST_DONE) { atomicExch(&par->arena_fail, status == ST_ARENA ? ST_ARENA : ST_PAR_BROKEN); par->pad = status; }
       atomicAdd((ull*)&C->F, (ull)F);
       __threadfence();
       const ull ticket = atomicAdd(&par->done, 1ULL);

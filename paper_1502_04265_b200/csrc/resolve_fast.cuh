@@ -760,7 +760,7 @@ __global__ void __launch_bounds__(64, 1) k_resolve2(EngDev E, const double* __re
     // deltas of this subtree, then the last CTA publishes the window
     if (lane == 0) {
       using ull = unsigned long long;
-      if (status != ST_DONE) atomicExch(&par->arena_fail, status == ST_ARENA ? ST_ARENA : ST_PAR_BROKEN);
+      if (status != ST_DONE) { atomicExch(&par->arena_fail, status == ST_ARENA ? ST_ARENA : ST_PAR_BROKEN); par->pad = status; }
       atomicAdd((ull*)&C->F, (ull)opened);
       atomicAdd((ull*)&C->total_w, (ull)totw);
       atomicMax(&C->max_depth, maxdepth);
@@ -781,7 +781,7 @@ __global__ void __launch_bounds__(64, 1) k_resolve2(EngDev E, const double* __re
         C->next_index = par->nidx0 + par->n_win;
         const int fail = *(volatile int*)&par->arena_fail;
         C->status = fail ? fail : (par->n_win < par->n_total ? ST_FULL : ST_DONE);
-        C->err = 0; C->stop = par->n_win; C->remaining = 0;
+        C->err = fail ? par->pad : 0; C->stop = par->n_win; C->remaining = 0;
         __threadfence();
       }
     }
@@ -1064,7 +1064,9 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
     ctot[q] = 0;
   }
   __syncthreads();
-  const int cap = heavy ? (PCY_MOD_SLOTS / 2) / (PCY_FMAXL + 2) : cap_items;
+  // items per CTA: the new-node table (one open per item) and, for weighted
+  // items (partial takes at up to PCY_FMAXL levels), the touched-node map
+  const int cap = heavy ? min((PCY_MOD_SLOTS / 2) / (PCY_FMAXL + 2), cap_items) : cap_items;
   const int rank = act ? ccnt[wid][cta] + rin : 0;
   if (act && rank >= cap) atomicMin(&s_cut, tid);
   __syncthreads();

@@ -653,7 +653,7 @@ __global__ void __launch_bounds__(32, 1) k_resolve3(EngDev E, const double* __re
   if constexpr (PAR) {
     if (lane == 0) {
       using ull = unsigned long long;
-      if (status != ST_DONE) atomicExch(&par->arena_fail, status == ST_ARENA ? ST_ARENA : ST_PAR_BROKEN);
+      if (status != ST_DONE) { atomicExch(&par->arena_fail, status == ST_ARENA ? ST_ARENA : ST_PAR_BROKEN); par->pad = status; }
       atomicAdd((ull*)&C->F, (ull)opened);
       atomicAdd((ull*)&C->total_w, (ull)totw);
       atomicMax(&C->max_depth, maxdepth);
@@ -673,7 +673,7 @@ __global__ void __launch_bounds__(32, 1) k_resolve3(EngDev E, const double* __re
         C->next_index = par->nidx0 + par->n_win;
         const int fail = *(volatile int*)&par->arena_fail;
         C->status = fail ? fail : (par->n_win < par->n_total ? ST_FULL : ST_DONE);
-        C->err = 0; C->stop = par->n_win; C->remaining = 0;
+        C->err = fail ? par->pad : 0; C->stop = par->n_win; C->remaining = 0;
         __threadfence();
       }
     }
@@ -945,7 +945,7 @@ __global__ void __launch_bounds__(32, 1) k_reattach3(EngDev E, const int* __rest
   if constexpr (PAR) {
     if (lane == 0) {
       using ull = unsigned long long;
-      if (status != ST_DONE) atomicExch(&par->arena_fail, status == ST_ARENA ? ST_ARENA : ST_PAR_BROKEN);
+      if (status != ST_DONE) { atomicExch(&par->arena_fail, status == ST_ARENA ? ST_ARENA : ST_PAR_BROKEN); par->pad = status; }
       atomicAdd((ull*)&C->F, (ull)F);
       __threadfence();
       const ull ticket = atomicAdd(&par->done, 1ULL);

@@ -215,13 +215,25 @@ def weighted_best_fit(points, weights, trunc: SvdTruncation, *, exact: bool = Fa
         raise ValueError("weights must be one per row")
     if not np.all(w >= 1):
         raise ValueError("weights must be positive integers (>= 1)")
-    if exact:
-        raise NotImplementedError("exact backend is a reference test oracle (out of scope)")
+    rows, cols = mat.shape
+    if exact:   # exact_truncated_svd's contract (linalg.py:120-164): rank range, entry limit
+        if trunc.rank < 1 or trunc.rank > min(rows, cols):
+            raise ValueError(f"rank {trunc.rank} out of range for a {rows}x{cols} matrix")
+        if rows * cols > max_entries:
+            raise ValueError(f"matrix with {rows * cols} entries exceeds the exact-backend "
+                             f"limit of {max_entries}")
     A = to_f64_device(mat)
     wd = torch.from_numpy(np.ascontiguousarray(w.astype(np.int64))).to(A.device)
     S = torch.empty_like(A)
     nat.check(nat.lib().pcy_scale_rows_sqrtw(nat.ptr(A), nat.ptr(wd), mat.shape[0], mat.shape[1], nat.ptr(S),
                                              nat.stream_ptr()), "scale_rows")
+    if exact:
+        # the exact backend: a sketch as wide as min(rows, cols) spans the whole
+        # row space, so the device range finder + Jacobi core SVD return the
+        # exact decomposition (to rounding; no squared condition number)
+        full = min(rows, cols)
+        V, sig = rsvd_device(S, trunc.rank, full - trunc.rank, 2, 0)
+        return Projector(V.cpu().numpy(), sig)
     r = trunc.rank + trunc.oversample
     if r > min(mat.shape):
         raise ValueError(f"rank + oversample = {r} exceeds min(rows, cols) = {min(mat.shape)}")
