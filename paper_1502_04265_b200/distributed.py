@@ -78,10 +78,19 @@ def group_summary(ops, source, grp: Group, dim: int, cfg, n_groups: int):
 
 
 def run_piecy_mr_sharded(source, n_rows: int, dim: int, cfg, *, rank: int = 0, world: int = 1,
-                         ops=None, concurrent: bool = True, tree_out: list | None = None):
+                         ops=None, concurrent: bool = True, tree_out: list | None = None,
+                         phases: dict | None = None):
     """Sharded run_piecy_mr.  ``source(a, b)`` returns rows [a, b) of the stream
     (any rank may read any range; each reads only its own groups).  Returns the
-    Coreset on rank 0 and None elsewhere."""
+    Coreset on rank 0 and None elsewhere.
+
+    Rank 0 merges in group order *as the summaries become available*: its own
+    groups run on worker threads (one CUDA stream each) and group g is
+    replayed into level 1 as soon as it -- and every group before it -- is
+    done, local or received, so the merge overlaps the remaining shard work.
+    The other ranks post their summaries with non-blocking sends.  ``phases``
+    (optional dict) receives the per-phase wall times of this rank: shard
+    compute, gather wait (rank 0: time blocked on remote summaries), merge."""
     if ops is None:
         ops = DeviceOps(cfg)
     if cfg.svd_dim > dim:
@@ -89,75 +98,138 @@ def run_piecy_mr_sharded(source, n_rows: int, dim: int, cfg, *, rank: int = 0, w
     groups = level0_groups(n_rows, cfg.piece_size, cfg.num_pieces)
     mine = [g for g in groups if owner(g.index, world) == rank]
     results = {}
+    done = {g.index: threading.Event() for g in mine}
+    errs = []
+    ph = {"shard_s": 0.0, "gather_wait_s": 0.0, "merge_s": 0.0, "groups_local": len(mine),
+          "groups_total": len(groups), "world": world}
+    t_start = time.perf_counter()
 
     def work(grp):
-        with ops.stream_scope():
-            results[grp.index] = group_summary(ops, source, grp, dim, cfg, len(groups))
+        try:
+            with ops.stream_scope():
+                results[grp.index] = group_summary(ops, source, grp, dim, cfg, len(groups))
+        except BaseException as exc:   # surface worker failures on the caller
+            errs.append(exc)
+        finally:
+            done[grp.index].set()
 
-    _dbg = os.environ.get("PCY_DEBUG_MR")
-    _t0 = time.perf_counter()
+    threads = []
     if concurrent and len(mine) > 1:
-        errs = []
-
-        def guard(fn, g):
-            try:
-                fn(g)
-            except BaseException as exc:   # surface worker failures on the caller
-                errs.append(exc)
-        threads = [threading.Thread(target=guard, args=(work, g)) for g in mine]
+        threads = [threading.Thread(target=work, args=(g,), daemon=True) for g in mine]
         for t in threads:
             t.start()
+    else:
+        for g in mine:
+            work(g)
+
+    def finish_local():
         for t in threads:
             t.join()
         if errs:
             raise errs[0]
-    else:
-        for g in mine:
-            work(g)
-    ops.sync()
-    if _dbg:
-        print(f"[mr] rank {rank}: {len(mine)} level-0 groups in {time.perf_counter() - _t0:.3f} s", flush=True)
-        _t0 = time.perf_counter()
+        ops.sync()
+        ph["shard_s"] = time.perf_counter() - t_start
 
-    # gather to rank 0 in group order (the exchange step)
-    if world > 1:
-        if rank == 0:
-            for g in groups:
-                if owner(g.index, world) != 0:
-                    results[g.index] = ops.recv(owner(g.index, world), dim)
-        else:
-            for g in mine:
-                ops.send(results[g.index], 0)
-            return None
+    if rank != 0:   # post every summary to rank 0 as it completes, in group order
+        pending = []
+        for g in mine:
+            done[g.index].wait()
+            if errs:
+                break
+            pending.append(ops.send(results[g.index], 0))
+        finish_local()
+        for h in pending:
+            if h is not None:
+                h.wait()
+        if phases is not None:
+            phases.update(ph)
+        return None
 
     tree = ops.tree(dim, cfg)
     if tree_out is not None:
         tree_out.append(tree)
     if not groups:
+        finish_local()
         return ops.finish(tree, None)
     if len(groups) == 1 and not groups[0].full:
+        finish_local()
         pts, wts, _ = results[0]
         tree.stats.pieces = groups[0].pieces
         return ops.coreset(pts, wts)
     for g in groups:
-        pts, wts, flushed = results[g.index]
+        if owner(g.index, world) == 0:
+            done[g.index].wait()
+            if errs:
+                finish_local()
+            item = results[g.index]
+            ops.ready(item)
+        else:
+            t0 = time.perf_counter()
+            item = ops.recv(owner(g.index, world), dim)
+            ph["gather_wait_s"] += time.perf_counter() - t0
+        t0 = time.perf_counter()
+        pts, wts, flushed = item
         tree.stats.flush_sources.append(0)
         tree.insert_reduced(1, pts, wts)
+        ph["merge_s"] += time.perf_counter() - t0
+    finish_local()
     tree.stats.pieces = sum(g.pieces for g in groups)
     tree.stats.points_read = n_rows
-    if _dbg:
-        ops.sync()
-        print(f"[mr] rank {rank}: merge of {len(groups)} summaries in {time.perf_counter() - _t0:.3f} s", flush=True)
-        _t0 = time.perf_counter()
+    t0 = time.perf_counter()
     out = ops.finish(tree, None)
-    if _dbg:
-        ops.sync()
-        print(f"[mr] rank {rank}: finalize in {time.perf_counter() - _t0:.3f} s", flush=True)
+    ops.sync()
+    ph["merge_s"] += time.perf_counter() - t0
+    ph["total_s"] = time.perf_counter() - t_start
+    if os.environ.get("PCY_DEBUG_MR"):
+        print(f"[mr] rank {rank}: {ph}", flush=True)
+    if phases is not None:
+        phases.update(ph)
     return out
 
 
+class Exchange:
+    """Point-to-point transport of the reduced summaries over the default
+    process group: NCCL sends device tensors directly (NVLink); gloo stages
+    them through host memory.  send() is non-blocking and returns a handle."""
+
+    def __init__(self, device):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist, self.device = torch, dist, device
+        self.host = dist.is_initialized() and dist.get_backend() == "gloo"
+
+    def _out(self, t):
+        return t.cpu() if self.host else t
+
+    def send(self, tensors, dst):
+        dist = self.dist
+        works = []
+        keep = []
+        for t in tensors:
+            t = self._out(t.contiguous())
+            keep.append(t)
+            works.append(dist.isend(t, dst))
+        return _Handles(works, keep)
+
+    def recv(self, shape, dtype, src):
+        torch = self.torch
+        t = torch.empty(shape, dtype=dtype, device="cpu" if self.host else self.device)
+        self.dist.recv(t, src)
+        return t.to(self.device) if self.host else t
+
+
+class _Handles:
+    def __init__(self, works, keep):
+        self.works, self.keep = works, keep
+
+    def wait(self):
+        for w in self.works:
+            w.wait()
+
+
 class DeviceOps:
-    """Group work on the CUDA engine; exchange over torch.distributed (NCCL)."""
+    """Group work on the CUDA engine; exchange over the default process group
+    (NCCL device-to-device, or gloo through host memory: ``Exchange``)."""
 
     def __init__(self, cfg, device=None):
         import torch
@@ -198,28 +270,34 @@ class DeviceOps:
     def finish(self, tree, _):
         return tree.finalize()
 
+    def ready(self, item):
+        """A locally produced summary is about to be merged: nothing to wait
+        for -- the worker synchronised its stream before signalling."""
+
+    def _xchg(self):
+        if not hasattr(self, "_ex"):
+            self._ex = Exchange(self.device)
+        return self._ex
+
     def send(self, item, dst):
-        import torch.distributed as dist
         pts, wts, flushed = item
         torch = self.torch
         pts = pts.to(torch.float64).contiguous()
         hdr = torch.tensor([pts.shape[0], 1 if flushed else 0], dtype=torch.int64, device=self.device)
-        dist.send(hdr, dst)
-        if pts.shape[0]:
-            dist.send(pts, dst)
-            dist.send(wts.contiguous(), dst)
+        torch.cuda.current_stream(self.device).synchronize()
+        return self._xchg().send([hdr, pts, wts.contiguous()] if pts.shape[0] else [hdr], dst)
 
     def recv(self, src, dim):
-        import torch.distributed as dist
         torch = self.torch
-        hdr = torch.zeros(2, dtype=torch.int64, device=self.device)
-        dist.recv(hdr, src)
+        ex = self._xchg()
+        hdr = ex.recv((2,), torch.int64, src)
         n = int(hdr[0])
-        pts = torch.empty((n, dim), dtype=torch.float64, device=self.device)
-        wts = torch.empty(n, dtype=torch.int64, device=self.device)
         if n:
-            dist.recv(pts, src)
-            dist.recv(wts, src)
+            pts = ex.recv((n, dim), torch.float64, src)
+            wts = ex.recv((n,), torch.int64, src)
+        else:
+            pts = torch.empty((0, dim), dtype=torch.float64, device=self.device)
+            wts = torch.empty(0, dtype=torch.int64, device=self.device)
         return pts, wts, bool(hdr[1])
 
 

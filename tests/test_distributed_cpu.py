@@ -73,6 +73,9 @@ class OracleOps:
     def finish(self, tree, _):
         return tree.t.finalize()
 
+    def ready(self, item):
+        pass
+
     def send(self, item, dst):
         pts, wts, flushed = item
         dist.send(torch.tensor([pts.shape[0], int(flushed)], dtype=torch.int64), dst)
