@@ -65,7 +65,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError(f"nvcc failed:\n{msg}")
     tmp = LIB + ".tmp"
     cmd = [_nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp, *objs,
-           "-lcudart", "-lcublas",
+           "-lcudart",
            "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
     subprocess.run(cmd, check=True)
     os.replace(tmp, LIB)

@@ -40,6 +40,8 @@ _SIGS = {
     "pcy_tc_dots_f64": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_i64, c_i32, c_i32, c_vp, P_f64, c_vp]),
 }
 
+PCY_ENONFINITE = -2   # include/piecy_b200.h error codes
+
 PROF_SLOTS = {"resolve": 0, "chain": 1, "reattach": 2, "seed": 3, "lloyd": 4, "gemm": 5}
 
 

@@ -144,8 +144,11 @@ def rsvd_device(A, rank: int, oversample: int, power: int, seed: int):
     om2d = torch.from_numpy(om2).to(dev) if om2 is not None else None
     V = torch.empty((cols, rank), dtype=torch.float64, device=dev)
     sig = np.zeros(rank)
-    nat.check(nat.lib().pcy_rsvd(nat.ptr(A), rows, cols, rank, r, power, nat.ptr(omd), nat.ptr(om2d),
-                                 nat.ptr(V), sig.ctypes.data, nat.stream_ptr()), "pcy_rsvd")
+    rc = nat.lib().pcy_rsvd(nat.ptr(A), rows, cols, rank, r, power, nat.ptr(omd), nat.ptr(om2d),
+                            nat.ptr(V), sig.ctypes.data, nat.stream_ptr())
+    if rc == nat.PCY_ENONFINITE:   # checked on the device, read back with sigma
+        raise ValueError("matrix contains non-finite entries")
+    nat.check(rc, "pcy_rsvd")
     return V, sig
 
 
@@ -160,8 +163,9 @@ def project_device(A, V):
 
 
 def project_piece_device(piece, trunc: SvdTruncation):
-    """Piece projection of run_piecy (pipeline.py:120-126) on the device."""
-    check_finite_device(piece)
+    """Piece projection of run_piecy (pipeline.py:120-126) on the device
+    (a non-finite entry raises ValueError from rsvd_device before anything is
+    inserted, as the reference's as_matrix check does)."""
     A = to_f64_device(piece)
     V, _ = rsvd_device(A, trunc.rank, trunc.oversample, trunc.power_iterations, trunc.seed)
     return project_device(A, V)
