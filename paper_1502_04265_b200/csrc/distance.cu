@@ -279,11 +279,7 @@ int pcy_launch_parts(const double* A, const int* aidx, long long lda, int M, con
                      cudaStream_t st) {
   if (M <= 0 || N <= 0) return PCY_OK;
   dim3 grid((unsigned)((N + DBN - 1) / DBN), (unsigned)((M + DBM - 1) / DBM));
-  static const bool old_parts = getenv("PCY_OLD_PARTS") != nullptr;
-  if (old_parts)
-    k_dist_tile<2><<<grid, 128, 0, st>>>(M, N, K, A, aidx, lda, B, bidx, ldb, rn, C, ldc, nullptr, nullptr, 0, n_dev);
-  else
-    k_dist_tile<2, true><<<grid, 128, 0, st>>>(M, N, K, A, aidx, lda, B, bidx, ldb, rn, C, ldc, nullptr, nullptr, 0, n_dev);
+  k_dist_tile<2, true><<<grid, 128, 0, st>>>(M, N, K, A, aidx, lda, B, bidx, ldb, rn, C, ldc, nullptr, nullptr, 0, n_dev);
   pcy_count_launch();
   PCY_LAUNCH_CHECK();
   return PCY_OK;

@@ -3,7 +3,7 @@
 // Reference semantics: /root/reference/pkg/src/piecy/coreset.py (BicoEngine).
 // Layout and kernel roles are described in DESIGN.md §3-§4:
 //   k_stage    -- upcast/copy a block, x_sq, validation, exact-bytes hash
-//   k_boot     -- bootstrap buffering (coreset.py:283-295), one warp, in order
+//   k_boot_*   -- bootstrap buffering (coreset.py:283-295): parallel scan, same result as in order
 //   k_mp_*     -- T0 = min positive pairwise sq. distance * m / 16 (:297-299, :479-489)
 //   k_snapshot -- freeze group counts for the chain kernel
 //   k_chain    -- K1: every item's capacity-free nearest-reference chain against
@@ -192,6 +192,54 @@ __device__ __forceinline__ void scan_members_lane(const EngDev& E, const int* __
     }
     warp_argmin(part, pos);
     if (part < bp) { bp = part; bpos = pos; }
+  }
+}
+
+// scan_members_lane plus the winner's slot and statistics: every lane also
+// loads its member's (w, q, sn, child) in the same round trip as the row, and
+// the winning lane's values are shuffled out -- the chain walk then needs no
+// further dependent load before it can fetch the next level's group.
+struct LaneWinner { int id, child; long long w; double q, sn; };
+__device__ __forceinline__ void scan_members_lane_w(const EngDev& E, const int* __restrict__ mem, int cnt,
+                                                    const double* __restrict__ xv, int lane, double& bp, int& bpos,
+                                                    LaneWinner& win) {
+  const int d = E.d, ld = E.ld;
+  bp = INFINITY; bpos = 0x7fffffff;
+  win = LaneWinner{-1, -1, 0, 0.0, 0.0};
+  for (int c0 = 0; c0 < cnt; c0 += 32) {
+    const int p = c0 + lane;
+    double part = INFINITY;
+    int pos = 0x7fffffff;
+    LaneWinner mine{-1, -1, 0, 0.0, 0.0};
+    if (p < cnt) {
+      const int id = mem[p];
+      const double2* __restrict__ rr = reinterpret_cast<const double2*>(E.r + (long long)id * ld);
+      const double rn = E.rn[id];
+      mine = LaneWinner{id, E.child[id], E.w[id], E.q[id], E.sn[id]};
+      double acc = 0.0;
+      for (int e0 = 0; e0 < d; e0 += 64) {
+        double2 v[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q) v[q] = (e0 + 2 * q < ld) ? __ldg(rr + (e0 >> 1) + q) : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          if (e0 + 2 * q < d) acc = fma(v[q].x, xv[e0 + 2 * q], acc);
+          if (e0 + 2 * q + 1 < d) acc = fma(v[q].y, xv[e0 + 2 * q + 1], acc);
+        }
+      }
+      part = radd(rn, rmul(acc, -2.0));
+      pos = p;
+    }
+    warp_argmin(part, pos);
+    if (part < bp) {
+      bp = part; bpos = pos;
+      const int src = pos - c0;
+      win.id = __shfl_sync(PCY_FULL, mine.id, src);
+      win.child = __shfl_sync(PCY_FULL, mine.child, src);
+      win.w = __shfl_sync(PCY_FULL, mine.w, src);
+      win.q = __shfl_sync(PCY_FULL, mine.q, src);
+      win.sn = __shfl_sync(PCY_FULL, mine.sn, src);
+    }
   }
 }
 
@@ -436,55 +484,7 @@ __global__ void k_rowsq(const double* __restrict__ X, int d, int ld, long long n
 }
 
 // --------------------------------------------------------------- bootstrap
-// coreset.py:283-295, one warp, strictly in stream order.
-__global__ void k_boot(EngDev E, long long start, long long n) {
-  const int lane = threadIdx.x;
-  EngCtl* C = E.ctl;
-  const int d = E.d, ld = E.ld;
-  long long npend = C->npend, ndist = C->ndist, totw = C->total_w;
-  const unsigned long long mask = (unsigned long long)E.hcap - 1ULL;
-  int status = ST_DONE, err = 0; long long stop = n;
-  for (long long i = start; i < n; ++i) {
-    if (E.bad[i]) { status = ST_INVALID; err = E.bad[i]; stop = i; break; }
-    const double* x = E.xb + i * ld;
-    const long long wv = E.wb[i];
-    bool dup = npend > 0 && rows_equal(E.pend_x + (npend - 1) * ld, x, d, lane);
-    if (!dup && npend == E.pend_cap) { status = ST_GROW; stop = i; break; }
-    totw += wv;
-    if (dup) {
-      if (lane == 0) E.pend_w[npend - 1] += wv;
-    } else {
-      double* pr = E.pend_x + npend * ld;
-      for (int e = lane; e < ld; e += 32) pr[e] = x[e];
-      if (lane == 0) { E.pend_w[npend] = wv; E.pend_xsq[npend] = E.xsq[i]; }
-      ++npend;
-    }
-    unsigned long long slot = E.hsh[i] & mask;
-    bool found = false;
-    for (;;) {
-      const int k = E.htab[slot];
-      if (k < 0) break;
-      if (rows_equal(E.dist_x + (long long)k * ld, x, d, lane)) { found = true; break; }
-      slot = (slot + 1) & mask;
-    }
-    if (!found) {
-      double* dr = E.dist_x + ndist * ld;
-      for (int e = lane; e < ld; e += 32) dr[e] = x[e];
-      if (lane == 0) E.htab[slot] = (int)ndist;
-      ++ndist;
-      __syncwarp();
-      if (ndist > E.m) { status = ST_BUILD; stop = i; break; }
-    }
-    __syncwarp();
-  }
-  __syncwarp();
-  if (lane == 0) {
-    C->npend = npend; C->ndist = ndist; C->total_w = totw;
-    C->status = status; C->err = err; C->stop = stop;
-  }
-}
-
-// Parallel bootstrap (same result as k_boot, coreset.py:283-295).  The last
+// Parallel bootstrap (coreset.py:283-295: exactly the one-at-a-time result).  The last
 // pending entry always holds the previous row's key, so row i starts a new
 // pending entry iff it differs from row i-1 (from the last entry for the
 // first row); a row is a new distinct key iff it is not in the table and no
@@ -578,7 +578,7 @@ __global__ void __launch_bounds__(1024) k_boot_plan(EngDev E, BootScratch B, lon
     __syncthreads();
     const long long pa = (wid ? red[0][wid - 1] : 0) + a, pb = (wid ? red[1][wid - 1] : 0) + b;   // inclusive
     const long long np0 = s_np, nd0 = s_nd;
-    // per-row events in k_boot's order: invalid (row not taken), pending full
+    // per-row events in stream order: invalid (row not taken), pending full
     // (row not taken), then the row is taken and may be the budget + 1-th key
     long long ev = 0x7fffffffffffLL; int st = ST_DONE;
     if (in) {
@@ -1358,7 +1358,6 @@ struct Engine {
   int* ncol = nullptr;            // device count of live columns
   bool cols_reset = true;         // recompact the live columns at the next contraction
   BootScratch bs{};            // parallel bootstrap scratch
-  bool seq_boot = false;       // PCY_SEQ_BOOT: the one-warp k_boot instead
   size_t plan_smem = 0;        // k_plan dynamic shared memory
   ParCtl* parctl = nullptr;    // k_plan output (subtree-parallel resolve)
   long long kbatch = 1024;     // K1 rows per launch when k3par
@@ -1464,23 +1463,18 @@ struct Engine {
     A_(aggw, m + 2); A_(mp_nrm, sample_cap + 1);
     bs.scap = 1; while (bs.scap < 2 * Bmax) bs.scap <<= 1;
     A_(bs.flags, Bmax + 1); A_(bs.spos, Bmax); A_(bs.ppos, Bmax); A_(bs.dpos, Bmax); A_(bs.skey, bs.scap); A_(bs.sfirst, bs.scap);
-    seq_boot = getenv("PCY_SEQ_BOOT") != nullptr;
     A_(parctl, 1);
 #undef A_
     for (auto& e : ev) PCY_CUDA(cudaEventCreate(&e));
     {
-      const char* pe = getenv("PCY_K3_PRIORITY");
-      if (!pe || atoi(pe) != 0) {
-        int least = 0, greatest = 0;
-        PCY_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
-        PCY_CUDA(cudaStreamCreateWithPriority(&hi, cudaStreamNonBlocking, greatest));
-        PCY_CUDA(cudaEventCreateWithFlags(&evk1, cudaEventDisableTiming));
-        PCY_CUDA(cudaEventCreateWithFlags(&evk3, cudaEventDisableTiming));
-      }
+      int least = 0, greatest = 0;
+      PCY_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+      PCY_CUDA(cudaStreamCreateWithPriority(&hi, cudaStreamNonBlocking, greatest));
+      PCY_CUDA(cudaEventCreateWithFlags(&evk1, cudaEventDisableTiming));
+      PCY_CUDA(cudaEventCreateWithFlags(&evk3, cudaEventDisableTiming));
     }
     {
-      const char* tcenv = getenv("PCY_TC_PARTS");
-      use_tc = tcenv ? atoi(tcenv) != 0 : d >= 256;
+      use_tc = d >= 256;
       Kp = pcy_tc_pad(d);
       tc_tau = pcy_tc_error_tau(Kp);
     }
@@ -1549,15 +1543,13 @@ struct Engine {
         PCY_CUDA(cudaFuncSetAttribute(k_reattach3<false, 512, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem));
       }
     }
-    if (getenv("PCY_GENERIC_RESOLVE")) nper = 0;
     plan_smem = plan_smem_bytes((int)(NC / 32 + 1));
     {
       const char* pe = getenv("PCY_K3PAR");
       k3par = nper >= 1 && (!pe || atoi(pe) != 0) && plan_smem <= maxsm;
       if (k3par) PCY_CUDA(cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan_smem));
-      static const bool rea_trows = getenv("PCY_REA_TROWS") != nullptr;   // A/B: reference rows, no Gram dots
       if (nper >= 1 && nper <= 8) {
-        const bool g = k3par && !rea_trows;
+        const bool g = k3par;
         rea_cap = g ? PCY_NNEW_REA : rea_cap_t;
         rea_smem = g ? rea_smem_g : rea_smem_t;
         rea_gram = g;
@@ -1618,7 +1610,7 @@ struct Engine {
       return false;
     }
     const long long N = ctl_h->F_alloc;   // upper bound on the live columns (device count in ncol)
-    if (!nper || N < 256 || getenv("PCY_NO_FULLSET")) return false;
+    if (!nper || N < 256) return false;
     if (cols_reset) {   // recompact: every live node takes a fresh column below
       if (cudaMemsetAsync(tc_done, 0xff, sizeof(long long) * NC, st) != cudaSuccess ||
           cudaMemsetAsync(ncol, 0, sizeof(int), st) != cudaSuccess) {
@@ -1713,8 +1705,7 @@ struct Engine {
           int grc;
           // the batch Gram depends only on the batch's references: a side
           // stream computes it beside the contraction and the chain walk
-          static const bool gram_late = getenv("PCY_GRAM_LATE") != nullptr;
-          const bool gram_early = k3par && nper <= 8 && hi && !gram_late;   // small d only: at large d the Gram competes with the K1 contraction
+          const bool gram_early = k3par && nper <= 8 && hi;   // small d only: at large d the Gram competes with the K1 contraction
           if (gram_early) {
             PCY_CUDA(cudaEventRecord(evk1, st)); PCY_CUDA(cudaStreamWaitEvent(hi, evk1, 0));
             grc = pcy_launch_gram_split(E.r, E.order + off, ld, (int)nb, d, gram, nb, gram_part, gram_split, hi);
@@ -1763,9 +1754,6 @@ struct Engine {
           PCY_LAUNCH_CHECK();
           rc = sync_ctl(st); if (rc) return rc;
           if (ctl_h->status == ST_ARENA) { pcy_set_error("member arena exhausted in rebuild"); return PCY_ESTATE; }
-          if (getenv("PCY_DEBUG_REBUILD"))
-            fprintf(stderr, "[pcy] reattach launch: off %lld nb %lld status %d stop %lld F %lld nnew_cap %d\n", off, nb,
-                    ctl_h->status, ctl_h->stop, ctl_h->F, nnew_cap);
           if (ctl_h->status == ST_PAR_BROKEN) {
             pcy_set_error("subtree-parallel reattach met an excluded stop (inner status %d, window %lld, F %lld, m %lld)",
                           ctl_h->err, ctl_h->stop, ctl_h->F, m);
@@ -1825,8 +1813,7 @@ struct Engine {
         if (prof) PCY_CUDA(cudaEventRecord(ev[0], st));
         // the batch Gram for k_plan's open-conflict test depends only on the
         // batch rows: on the K3 stream it runs beside the K1 contraction
-        static const bool gram_late = getenv("PCY_GRAM_LATE") != nullptr;
-        const bool gram_early = k3par && nper <= 8 && hi && !gram_late;   // small d only: at large d the Gram competes with the K1 contraction
+        const bool gram_early = k3par && nper <= 8 && hi;   // small d only: at large d the Gram competes with the K1 contraction
         if (gram_early) {
           PCY_CUDA(cudaEventRecord(evk1, st)); PCY_CUDA(cudaStreamWaitEvent(hi, evk1, 0));
           const int grc = pcy_launch_gram_split(Xs, nullptr, ld, (int)kn, d, gram, kn, gram_part, gram_split, hi);
@@ -1903,14 +1890,6 @@ struct Engine {
             pcy_prof_add(PCY_PROF_GEMM, tg, (long long)gemm_flops);
             gemm_timed = false;
           }
-          static FILE* trace = getenv("PCY_TRACE_K3") ? fopen(getenv("PCY_TRACE_K3"), "a") : nullptr;
-          if (trace) {
-            int pm[2] = {-1, 0};
-            if (k3par) cudaMemcpy(pm, parctl, sizeof(pm), cudaMemcpyDeviceToHost);
-            fprintf(trace, "%lld %.4f %.4f %d %lld %lld %lld %lld %d %d\n", done, t1, t2, ctl_h->status, ctl_h->F,
-                    ctl_h->cnt_slow, ctl_h->cnt_levels, ctl_h->root_count, pm[0], pm[1]);
-            fflush(trace);
-          }
         }
         const int status = ctl_h->status;
         if (status == ST_DONE) {
@@ -1979,9 +1958,7 @@ struct Engine {
       long long i = 0;
       while (i < nb) {
         if (!built) {
-          if (seq_boot) {
-            k_boot<<<1, 32, 0, st>>>(E, i, nb); pcy_count_launch();
-          } else {
+          {
             PCY_CUDA(cudaMemsetAsync(bs.skey, 0xff, sizeof(int) * bs.scap, st));
             PCY_CUDA(cudaMemsetAsync(bs.sfirst, 0x7f, sizeof(int) * bs.scap, st));
             const unsigned g8 = (unsigned)((nb - i + 7) / 8);
@@ -2093,9 +2070,6 @@ int pcy_engine_counters(void* h, long long* out6) {
   Engine* e = (Engine*)h;
   out6[0] = e->ctl_h->cnt_levels; out6[1] = e->ctl_h->cnt_direct; out6[2] = e->ctl_h->cnt_demand;
   out6[3] = e->ctl_h->cnt_slow; out6[4] = e->ctl_h->cnt_items; out6[5] = e->ctl_h->max_depth;
-  if (getenv("PCY_DEBUG_COUNTERS"))
-    fprintf(stderr, "[pcy] demand loads on the fast path %lld, nodes touched only by a new child %lld\n",
-            e->ctl_h->cnt_dem_fast, e->ctl_h->cnt_touch_child);
   return PCY_OK;
 }
 

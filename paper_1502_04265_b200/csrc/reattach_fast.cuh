@@ -29,28 +29,36 @@ __global__ void k_rchain(EngDev E, const int* __restrict__ order, long long n, C
   double radius = T;
   int g = 0, L = 0, pred = -1, predj = -1, trunc = 0, nre = 0;
   long long vis = 0, vdir = 0;
+  int cnt = E.g_count[0], base = E.g_base[0];
+  int pb = E.panel_gofs ? E.panel_gofs[0] : -1;
   for (;;) {
-    const int cnt = E.g_count[g], base = E.g_base[g];
     double bp; int bpos;
-    const int pb = E.panel_gofs ? E.panel_gofs[g] : -1;
+    LaneWinner win{-1, -1, 0, 0.0, 0.0};
+    bool have_win = false;
     vis += cnt;
     if (E.panel_gofs) {   // visited-groups K1: panel for big groups, direct fp64 scans otherwise
       if (E.tc_dots && pb >= 0)
         scan_parts_tc(E, i, g, E.arena + base, cnt,
                       [&](int jj) { return warp_dot(E.r + (long long)jj * ld, xv, d, lane); }, lane, bp, bpos, nre, pb);
-      else { scan_members_lane(E, E.arena + base, cnt, xv, lane, bp, bpos); vdir += cnt; }
+      else { scan_members_lane_w(E, E.arena + base, cnt, xv, lane, bp, bpos, win); vdir += cnt; have_win = true; }
     } else if (E.tc_dots)   // tensor-core dots + near-tie recheck
       scan_parts_tc(E, i, g, E.arena + base, cnt, [&](int jj) { return warp_dot(E.r + (long long)jj * ld, xv, d, lane); },
                     lane, bp, bpos, nre);
     else if (P) scan_parts(P + i * ldp, E.col_of, E.arena + base, cnt, lane, bp, bpos);   // parts from the DMMA contraction
     else { scan_members(E, E.arena + base, 0, cnt, xv, lane, bp, bpos); vdir += cnt; }
-    const int j = bpos < cnt ? E.arena[base + bpos] : -1;
+    const int j = have_win ? (bpos < cnt ? win.id : -1) : (bpos < cnt ? E.arena[base + bpos] : -1);
     ChainLvl c = empty_level();
     c.part = bp; c.j = j; c.g = g;
     ++L;
     const bool outside = j < 0 || radd(bp, rsq) > radius;
+    int ncnt = 0, nbase = 0, npb = -1;
     if (!outside) {
-      c.w = E.w[j]; c.q = E.q[j]; c.sn = E.sn[j]; c.child = E.child[j];
+      if (have_win) { c.w = win.w; c.q = win.q; c.sn = win.sn; c.child = win.child; }
+      else { c.w = E.w[j]; c.q = E.q[j]; c.sn = E.sn[j]; c.child = E.child[j]; }
+      if (c.child >= 0) {   // next level's group, overlapping the merge-norm dot
+        ncnt = E.g_count[c.child]; nbase = E.g_base[c.child];
+        npb = E.panel_gofs ? E.panel_gofs[c.child] : -1;
+      }
       const double* sh = E.s + (long long)j * ld;
       double acc = 0.0;
       for (int e = lane; e < d; e += 32) { const double v = radd(sh[e], su[e]); acc = fma(v, v, acc); }
@@ -73,6 +81,7 @@ __global__ void k_rchain(EngDev E, const int* __restrict__ order, long long n, C
     }
     if (L >= PCY_FMAXL) { trunc = 1; break; }
     g = c.child;
+    cnt = ncnt; base = nbase; pb = npb;
     radius = rmul(radius, 0.25);
   }
   if (pred < 0) pred = L - 1;

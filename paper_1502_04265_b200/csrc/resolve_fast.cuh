@@ -92,19 +92,23 @@ __global__ void k_chain2(EngDev E, const double* __restrict__ X, const double* _
   double radius = T;
   int g = 0, L = 0, pred = -1, predj = -1, trunc = 0, nre = 0;
   long long vis = 0, vdir = 0;   // member visits (all / direct scans)
+  // the next level's group (count, base, panel column) is loaded as soon as
+  // its id is known, overlapping the <s_j, x> dot of the current level
+  int cnt = E.g_count[0], base = E.g_base[0];
+  int pb = E.panel_gofs ? E.panel_gofs[0] : -1;
   for (;;) {
-    const int cnt = E.g_count[g], base = E.g_base[g];
     double bp; int bpos;
+    LaneWinner win{-1, -1, 0, 0.0, 0.0};
+    bool have_win = false;
     // visited-groups K1 (panel mode, d <= 256): big groups from the tensor-core
     // panel, the others by direct fp64 scans; otherwise the full-set contraction
-    const int pb = E.panel_gofs ? E.panel_gofs[g] : -1;
     vis += cnt;
     if (E.panel_gofs) {
       if constexpr (WPI == 1) {
         if (E.tc_dots && pb >= 0)
           scan_parts_tc(E, i, g, E.arena + base, cnt, [&](int jj) { return xdot(E.r + (long long)jj * ld); }, lane,
                         bp, bpos, nre, pb);
-        else { scan_members_lane(E, E.arena + base, cnt, xv, lane, bp, bpos); vdir += cnt; }
+        else { scan_members_lane_w(E, E.arena + base, cnt, xv, lane, bp, bpos, win); vdir += cnt; have_win = true; }
       }
     } else if (E.tc_dots) {   // tensor-core dots + near-tie recheck
       if constexpr (WPI == 1)
@@ -116,12 +120,18 @@ __global__ void k_chain2(EngDev E, const double* __restrict__ X, const double* _
     }
     else if (P) scan_parts(P + i * ldp, E.col_of, E.arena + base, cnt, lane, bp, bpos);   // DMMA parts
     else { scan_members(E, E.arena + base, 0, cnt, xv, lane, bp, bpos); vdir += cnt; }
-    const int j = bpos < cnt ? E.arena[base + bpos] : -1;
+    const int j = have_win ? (bpos < cnt ? win.id : -1) : (bpos < cnt ? E.arena[base + bpos] : -1);
     ChainLvl c = empty_level();
     c.part = bp; c.j = j; c.g = g;
+    int ncnt = 0, nbase = 0, npb = -1;
     if (j >= 0) {
+      if (have_win) { c.w = win.w; c.q = win.q; c.sn = win.sn; c.child = win.child; }
+      else { c.w = E.w[j]; c.q = E.q[j]; c.sn = E.sn[j]; c.child = E.child[j]; }
+      if (c.child >= 0) {   // issued before the dot: both round trips overlap
+        ncnt = E.g_count[c.child]; nbase = E.g_base[c.child];
+        npb = E.panel_gofs ? E.panel_gofs[c.child] : -1;
+      }
       c.dot = xdot(E.s + (long long)j * ld);
-      c.w = E.w[j]; c.q = E.q[j]; c.sn = E.sn[j]; c.child = E.child[j];
     }
     ++L;
     const bool outside = j < 0 || radd(bp, xs) > radius;
@@ -146,6 +156,7 @@ __global__ void k_chain2(EngDev E, const double* __restrict__ X, const double* _
     }
     if (L >= PCY_FMAXL) { trunc = 1; break; }
     g = c.child;
+    cnt = ncnt; base = nbase; pb = npb;
     radius = rmul(radius, 0.25);
   }
   if (pred < 0) pred = L - 1;

@@ -12,7 +12,7 @@ for f in sys.argv[1:]:
     print(f, f"value={d['value']:.0f} e2e={d['e2e']['value']:.0f} ms={d['ms_per_step']:.1f}", km,
           "phase", d.get("phase_ms", [None])[-1], "launches", d.get("gpu_launches"))
     r = d.get("roofline") or {}
-    print("   roof", r.get("kernel", "")[:50], r.get("frac"), [(x["kernel"][:28], round(x["frac"], 3), round(x.get("ms_per_step") or 0, 1)) for x in d.get("rooflines", [])])
+    print("   roof", r.get("kernel", "")[:50], r.get("frac"), [(x["kernel"][:28], (round(x["frac"], 3) if x.get("frac") is not None else None), round(x.get("ms_per_step") or 0, 1)) for x in d.get("rooflines", [])])
     for k in ("k1_work", "parity", "engine_counters"):
         if d.get(k) is not None:
             print("   ", k, d[k])
