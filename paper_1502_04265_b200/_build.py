@@ -49,7 +49,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
         objs.append(obj)
-        cmd = [_nvcc(), *NVCC_FLAGS, "-c", src, "-o", obj]
+        extra = os.environ.get("PCY_NVCC_EXTRA", "").split()   # build-time diagnostics (e.g. -DPCY_TRACE)
+        cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))

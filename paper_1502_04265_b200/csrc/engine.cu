@@ -1759,6 +1759,14 @@ struct Engine {
                           ctl_h->err, ctl_h->stop, ctl_h->F, m);
             return PCY_ESTATE;
           }
+#ifdef PCY_TRACE
+          {   // build-time diagnostics only (PCY_NVCC_EXTRA=-DPCY_TRACE)
+            int pm[2] = {-1, 0};
+            if (k3par) cudaMemcpy(pm, parctl, sizeof(pm), cudaMemcpyDeviceToHost);
+            fprintf(stderr, "[rea] nodes %lld off %lld nb %lld status %d stop %lld mode %d P %d\n", nodes, off, nb,
+                    ctl_h->status, ctl_h->stop, pm[0], pm[1]);
+          }
+#endif
           if (ctl_h->status == ST_FULL) {
             if (ctl_h->stop == 0) { pcy_set_error("reattach made no progress"); return PCY_ESTATE; }
             off += ctl_h->stop;

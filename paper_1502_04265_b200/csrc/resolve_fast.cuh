@@ -990,9 +990,13 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
           const double xsy = xs_s[y];
           const double pnew = radd(xsy, rmul(gram[(long long)tid * gld + y], -2.0));
           if (pnew < prec + 1e-10 * (xs + xsy) + 1e-300) {
-            if (P == PLAN_ROOT) {   // the window ends before this root open
-              atomicMin(&s_c, y);
-              if (y < 64) atomicMax(&s_last, y);
+            if (P == PLAN_ROOT) {
+              // x would prefer the earlier root opener y: the window ends
+              // before x (y's open stays in the window, in the OPEN(ROOT)
+              // domain; items before x do not prefer any new root, so their
+              // root winners -- and domains -- stand)
+              atomicMin(&s_c, tid);
+              if (tid < 64) atomicMax(&s_last, tid);
             } else {
               const int v = pj[l];
               atomicOr(&act_bits[v >> 5], 1u << (v & 31));
