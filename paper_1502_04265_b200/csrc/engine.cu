@@ -1899,6 +1899,14 @@ struct Engine {
             gemm_timed = false;
           }
         }
+#ifdef PCY_TRACE
+        {   // build-time diagnostics only (PCY_NVCC_EXTRA=-DPCY_TRACE)
+          int pm[2] = {-1, 0};
+          if (k3par) cudaMemcpy(pm, parctl, sizeof(pm), cudaMemcpyDeviceToHost);
+          fprintf(stderr, "[ins] start %lld kn %lld status %d stop %lld mode %d P %d F %lld\n", off + start, kn,
+                  ctl_h->status, ctl_h->stop, pm[0], pm[1], ctl_h->F);
+        }
+#endif
         const int status = ctl_h->status;
         if (status == ST_DONE) {
           if (k3par) kbatch = kbatch * 2 > 1024 ? 1024 : kbatch * 2;

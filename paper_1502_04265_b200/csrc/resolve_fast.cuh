@@ -479,6 +479,9 @@ __global__ void __launch_bounds__(64, 1) k_resolve2(EngDev E, const double* __re
           unsigned long long t = 0;
           if (lane == 0) t = atomicAdd(&par->open_ticket, 1ULL);
           const long long tt = (long long)__shfl_sync(PCY_FULL, t, 0);
+          // k_plan's budget bound guarantees F0 + tt < m; a violation (never
+          // expected) would need a rebuild here: report it, write nothing
+          if (par->F0 + tt >= E.m) return true;
           slot = tt < par->freen0 ? (long long)E.free_ids[par->freen0 - 1 - tt] : par->Falloc0 + (tt - par->freen0);
           nid = par->nidx0 + gix(i);
           ++opened;
@@ -846,7 +849,7 @@ constexpr int PLAN_ROOT = -2;
 // dynamic shared memory of k_plan: the hash / union-find tables, per-item xs
 // and opener links, and the active-node bitmap (nwords words)
 __host__ __device__ inline size_t plan_smem_bytes(int nwords) {
-  return sizeof(int) * 4 * PLAN_HASH + sizeof(double) * PCY_PAR_MAXITEMS + sizeof(int) * PCY_PAR_MAXITEMS +
+  return sizeof(int) * 6 * PLAN_HASH + sizeof(double) * PCY_PAR_MAXITEMS + sizeof(int) * PCY_PAR_MAXITEMS +
          sizeof(unsigned) * (size_t)nwords;
 }
 __device__ __forceinline__ int ph_slot(int key) { return (int)(((unsigned)key * 2654435761u) >> 20) & (PLAN_HASH - 1); }
@@ -900,6 +903,9 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
   double* xs_s = reinterpret_cast<double*>(plan_sm + 4 * PLAN_HASH);   // per item: |x|^2 (rn of the node)
   int* onext = reinterpret_cast<int*>(xs_s + PCY_PAR_MAXITEMS);        // opener list links, by item
   unsigned* act_bits = reinterpret_cast<unsigned*>(onext + PCY_PAR_MAXITEMS);   // active nodes
+  int* tkey = reinterpret_cast<int*>(act_bits + nwords);   // budget bound: node / group keys ...
+  int* tmin = tkey + PLAN_HASH;                            // ... and the first item that may touch them
+  __shared__ unsigned char s_unc[PCY_PAR_MAXITEMS];       // item may open (or is invalid)
   __shared__ int ccnt[PCY_PAR_MAXITEMS / 32][PCY_PAR_MAXCTA];
   __shared__ int ctot[PCY_PAR_MAXCTA];
   __shared__ int wsum[32];
@@ -912,11 +918,17 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
   long long room = E.m - F0;
   if (room < 0) room = 0;
   if (order) room = n;   // rebuild reattach: merges and adds never exceed the budget
-  for (int h = tid; h < PLAN_HASH; h += blockDim.x) { hkey[h] = -1; uf[h] = h; ohead[h] = -1; hfirst[h] = 0x7fffffff; }
+  for (int h = tid; h < PLAN_HASH; h += blockDim.x) {
+    hkey[h] = -1; uf[h] = h; ohead[h] = -1; hfirst[h] = 0x7fffffff; tkey[h] = -1;
+  }
+  if (tid < PCY_PAR_MAXITEMS) s_unc[tid] = 0;
   for (int q = tid; q < (PCY_PAR_MAXITEMS / 32) * PCY_PAR_MAXCTA; q += blockDim.x) (&ccnt[0][0])[q] = 0;
   for (int q = tid; q < nwords; q += blockDim.x) act_bits[q] = 0u;
   if (tid == 0) {
-    s_c = (int)(room < nn ? room : nn);
+    // the budget cut (no item may find F == m) is placed after the predictions:
+    // weighted windows take `room` items, unit windows as many as keep the
+    // number of items that may open within `room` (see below)
+    s_c = nn;
     if (first_rem >= 0) s_c = 0;
     s_last = -1; s_heavy = 0; s_cut = 0x7fffffff; s_P = 0;
   }
@@ -955,11 +967,14 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
     } else {
       atomicMin(&s_c, tid);
       if (tid < 64) atomicMax(&s_last, tid);
+      s_unc[tid] = 1;
     }
+    if (opener) s_unc[tid] = 1;
     if (W && W[tid] > 1) s_heavy = 1;
   }
   __syncthreads();
   const bool heavy = s_heavy != 0;
+  if (tid == 0 && (heavy || order) && room < nn) atomicMin(&s_c, (int)room);
   auto open_key = [&](int P) { return NC + (P == PLAN_ROOT ? NC : P); };
   if (heavy) {
     if (tid < nn && opener && target == PLAN_ROOT) {   // root opens end the window
@@ -990,6 +1005,7 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
           const double xsy = xs_s[y];
           const double pnew = radd(xsy, rmul(gram[(long long)tid * gld + y], -2.0));
           if (pnew < prec + 1e-10 * (xs + xsy) + 1e-300) {
+            s_unc[tid] = 1;   // its decisions may change: it may open
             if (P == PLAN_ROOT) {
               // x would prefer the earlier root opener y: the window ends
               // before x (y's open stays in the window, in the OPEN(ROOT)
@@ -1008,6 +1024,80 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
     }
   }
   __syncthreads();
+  // Budget bound of unit windows (coreset.py:330-335: an open at F == m opens
+  // one copy and rebuilds, which a parallel window cannot do).  Only items that
+  // may open count against room = m - F0: predicted openers, conflicting
+  // items, and absorbers whose K1 decision may not hold -- their absorb node
+  // may be touched by an earlier item of the window, or an earlier item that
+  // may open (not predicted) could add a member to a group on their path.
+  // "May touch" is every path node of an uncertain item (it may absorb at any
+  // level of its chain) and only the absorb node of a certain one; the sets
+  // are iterated to a fixpoint (uncertainty only grows).  A certain absorber
+  // follows its K1 chain and absorbs, so the window is safe when the count of
+  // uncertain items before its end is <= room.
+  if (!heavy && !order && room < nn && s_c > 0) {
+    const int cmax = s_c;
+    const bool live = tid < cmax;
+    int gk[PCY_FMAXL];   // group key per level: OPEN(parent)
+#pragma unroll
+    for (int l = 0; l < PCY_FMAXL; ++l) gk[l] = open_key(l == 0 ? PLAN_ROOT : pj[l > 0 ? l - 1 : 0]);
+    for (int it = 0; it < 16; ++it) {
+      for (int hh = tid; hh < PLAN_HASH; hh += blockDim.x) tmin[hh] = 0x7fffffff;
+      __syncthreads();
+      const bool unc = live && s_unc[tid];
+      if (live) {
+        if (unc) {
+#pragma unroll
+          for (int l = 0; l < PCY_FMAXL; ++l)
+            if (l < h.len && pj[l] >= 0) atomicMin(&tmin[ph_insert(tkey, pj[l])], tid);
+          if (!opener && h.len > 0) atomicMin(&tmin[ph_insert(tkey, gk[h.len - 1 < PCY_FMAXL ? h.len - 1 : 0])], tid);
+        } else if (absorb >= 0) {
+          atomicMin(&tmin[ph_insert(tkey, absorb)], tid);
+        }
+      }
+      __syncthreads();
+      int changed = 0;
+      if (live && !unc) {
+        bool u = false;
+        if (absorb >= 0) { const int so = ph_find(tkey, absorb); u = so >= 0 && tmin[so] < tid; }
+#pragma unroll
+        for (int l = 0; l < PCY_FMAXL; ++l) {
+          if (l > alev) break;
+          const int so = ph_find(tkey, gk[l]);
+          if (so >= 0 && tmin[so] < tid) u = true;
+        }
+        if (u) { s_unc[tid] = 1; changed = 1; }
+      }
+      if (!__syncthreads_or(changed)) break;
+    }
+    // window end: the first item whose inclusive count of uncertain items exceeds room
+    const int u = live && s_unc[tid] ? 1 : 0;
+    int inc = u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(PCY_FULL, inc, o);
+      if (lane >= o) inc += t;
+    }
+    if (lane == 31) wsum[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+      const int v = wsum[lane];
+      int wi = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(PCY_FULL, wi, o);
+        if (lane >= o) wi += t;
+      }
+      wsum[lane] = wi - v;
+    }
+    __syncthreads();
+    const int cum = wsum[wid] + inc;
+    if (u && cum > room && cum - 1 <= room) {   // the (room+1)-th possible opener
+      atomicMin(&s_c, tid);
+      if (tid < 64) atomicMax(&s_last, tid);
+    }
+    __syncthreads();
+  }
   const int c0 = s_c;
   if (c0 < theta) {
     if (tid == 0) {

@@ -437,6 +437,7 @@ __global__ void __launch_bounds__(32, 1) k_resolve3(EngDev E, const double* __re
         unsigned long long tk = 0;
         if (lane == 0) tk = atomicAdd(&par->open_ticket, 1ULL);
         const long long tt = (long long)__shfl_sync(PCY_FULL, tk, 0);
+        if (par->F0 + tt >= E.m) return true;   // k_plan's budget bound violated (never expected): report
         slot = tt < par->freen0 ? (long long)E.free_ids[par->freen0 - 1 - tt] : par->Falloc0 + (tt - par->freen0);
         nid = par->nidx0 + gix(i);
         ++opened;
