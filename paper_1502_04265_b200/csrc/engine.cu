@@ -777,7 +777,6 @@ __global__ void k_publish(EngCtl* __restrict__ src, EngCtl* dst, long long seq, 
 // slots go to fs_list in position order, and panel_n is published with the
 // counters.  The tree does not change between this publication and the next
 // K1 launch, so the panel is that launch's snapshot.
-constexpr int PCY_PANEL_MIN = 128;
 constexpr int PCY_PANEL_MAXG = 2048;   // listed big groups (later ones are scanned directly)
 __global__ void __launch_bounds__(1024) k_publish_panel(EngDev E, EngCtl* dst, long long seq) {
   __shared__ int wsc[32], wsb[32];
@@ -854,7 +853,7 @@ __global__ void __launch_bounds__(1024) k_publish_panel(EngDev E, EngCtl* dst, l
 __global__ void k_tree_reset(EngDev E) {
   if (threadIdx.x || blockIdx.x) return;
   EngCtl* C = E.ctl;
-  C->G_alloc = 1; C->A_alloc = 0; C->F = 0;
+  C->G_alloc = 1; C->A_alloc = 0; C->F = 0; C->maxg = 0;
   E.g_count[0] = 0; E.g_cap[0] = 0; E.g_base[0] = 0;
 }
 
@@ -1109,7 +1108,7 @@ __global__ void k_rb_reset(EngDev E, long long nslots) {
   if (u == 0) {
     EngCtl* C = E.ctl;
     C->T = rmul(C->T, 2.0);
-    C->G_alloc = 1; C->A_alloc = 0; C->F = 0;
+    C->G_alloc = 1; C->A_alloc = 0; C->F = 0; C->maxg = 0;
     E.g_count[0] = 0; E.g_cap[0] = 0; E.g_base[0] = 0;
   }
 }
@@ -1408,6 +1407,12 @@ struct Engine {
     else k_publish<<<1, 32, 0, st>>>(E.ctl, ctl_map_d, want, E.g_count, E.g_base);
     pcy_count_launch();
     PCY_LAUNCH_CHECK();
+    return wait_seq(st, want);
+  }
+  // The window kernels publish themselves while no group is in the K1 panel
+  // (k_resolve2x & co.); the panel publication is a separate launch.
+  bool self_publish() const { return !panel || ctl_h->maxg < PCY_PANEL_MIN; }
+  int wait_seq(cudaStream_t st, long long want) {
     volatile long long* sp = &ctl_h->seq;
     for (long long spins = 0; *sp != want; ++spins) {
       if ((spins & 1023) == 1023) {
@@ -1502,21 +1507,21 @@ struct Engine {
       if (nnew_cap < 8) { nper = 0; use_tc = false; }
       switch (nper) {
         case 1: PCY_CUDA(cudaFuncSetAttribute(k_resolve2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
-                PCY_CUDA(cudaFuncSetAttribute(k_resolve2<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
+                PCY_CUDA(cudaFuncSetAttribute(k_resolve2x<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
                 PCY_CUDA(cudaFuncSetAttribute(k_reattach2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem));
-                PCY_CUDA(cudaFuncSetAttribute(k_reattach2<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem)); break;
+                PCY_CUDA(cudaFuncSetAttribute(k_reattach2x<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem)); break;
         case 2: PCY_CUDA(cudaFuncSetAttribute(k_resolve2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
-                PCY_CUDA(cudaFuncSetAttribute(k_resolve2<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
+                PCY_CUDA(cudaFuncSetAttribute(k_resolve2x<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
                 PCY_CUDA(cudaFuncSetAttribute(k_reattach2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem));
-                PCY_CUDA(cudaFuncSetAttribute(k_reattach2<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem)); break;
+                PCY_CUDA(cudaFuncSetAttribute(k_reattach2x<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem)); break;
         case 4: PCY_CUDA(cudaFuncSetAttribute(k_resolve2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
-                PCY_CUDA(cudaFuncSetAttribute(k_resolve2<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
+                PCY_CUDA(cudaFuncSetAttribute(k_resolve2x<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
                 PCY_CUDA(cudaFuncSetAttribute(k_reattach2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem));
-                PCY_CUDA(cudaFuncSetAttribute(k_reattach2<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem)); break;
+                PCY_CUDA(cudaFuncSetAttribute(k_reattach2x<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem)); break;
         case 8: PCY_CUDA(cudaFuncSetAttribute(k_resolve2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
-                PCY_CUDA(cudaFuncSetAttribute(k_resolve2<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
+                PCY_CUDA(cudaFuncSetAttribute(k_resolve2x<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
                 PCY_CUDA(cudaFuncSetAttribute(k_reattach2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem));
-                PCY_CUDA(cudaFuncSetAttribute(k_reattach2<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem)); break;
+                PCY_CUDA(cudaFuncSetAttribute(k_reattach2x<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem)); break;
         default: break;
       }
     }
@@ -1531,16 +1536,16 @@ struct Engine {
         rea_smem = resolve3_smem_bytes<2048>(ld, nnew_cap, true, NC, GC, 2);
         PCY_CUDA(cudaFuncSetAttribute(k_resolve3<true, 2048>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
         PCY_CUDA(cudaFuncSetAttribute(k_reattach3<true, 2048>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem));
-        PCY_CUDA(cudaFuncSetAttribute(k_resolve3<true, 2048, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
-        PCY_CUDA(cudaFuncSetAttribute(k_reattach3<true, 2048, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem));
+        PCY_CUDA(cudaFuncSetAttribute(k_resolve3x<true, 2048>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
+        PCY_CUDA(cudaFuncSetAttribute(k_reattach3x<true, 2048>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem));
       } else if (resolve3_smem_bytes<512>(ld, 0, false, NC, GC, 2) <= maxsm) {
         nper = 101; nnew_cap = PCY_NNEW_MAX;
         res_smem = resolve3_smem_bytes<512>(ld, 0, false, NC, GC, 0);
         rea_smem = resolve3_smem_bytes<512>(ld, 0, false, NC, GC, 2);
         PCY_CUDA(cudaFuncSetAttribute(k_resolve3<false, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
         PCY_CUDA(cudaFuncSetAttribute(k_reattach3<false, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem));
-        PCY_CUDA(cudaFuncSetAttribute(k_resolve3<false, 512, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
-        PCY_CUDA(cudaFuncSetAttribute(k_reattach3<false, 512, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem));
+        PCY_CUDA(cudaFuncSetAttribute(k_resolve3x<false, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
+        PCY_CUDA(cudaFuncSetAttribute(k_reattach3x<false, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rea_smem));
       }
     }
     plan_smem = plan_smem_bytes((int)(NC / 32 + 1));
@@ -1691,6 +1696,9 @@ struct Engine {
       k_rb_reset<<<(unsigned)((nslots + 255) / 256), 256, 0, st>>>(E, nslots); pcy_count_launch();
       ctl_h->root_count = 0;   // fresh roots; the mirror refreshes at the next publication
       if (panel) {   // the reattach K1 needs the panel of the emptied tree
+        // no group is listed until one reaches the panel size again (the
+        // publications in between are skipped, see self_publish)
+        PCY_CUDA(cudaMemsetAsync(E.fs_gofs, 0xff, sizeof(int) * GC, st));
         const int prc = sync_ctl(st);
         if (prc) return prc;
       }
@@ -1722,6 +1730,7 @@ struct Engine {
           }
           if (gram_early) PCY_CUDA(cudaStreamWaitEvent(st, evk3, 0));
           ParCtl* pp = nullptr;
+          bool selfp = false; long long pseq = 0;
           const double* rg = rea_gram ? gram : nullptr;   // the batch Gram exists exactly when k3par
           if (k3par) {
             if (nper != 101 && !gram_early) {   // opener rows against the batch (k_plan's conflict test)
@@ -1733,26 +1742,34 @@ struct Engine {
                                                    gram, nb);
             pcy_count_launch();
             pp = parctl;
+            // one launch serves either choice of k_plan and, while no group is
+            // in the K1 panel, publishes the counters itself
+            selfp = self_publish();
+            pseq = selfp ? ++seq : 0;
+            EngCtl* pb = selfp ? ctl_map_d : nullptr;
             switch (nper) {
-              case 1: k_reattach2<1, true><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp, rg, nb); break;
-              case 2: k_reattach2<2, true><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp, rg, nb); break;
-              case 4: k_reattach2<4, true><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp, rg, nb); break;
-              case 8: k_reattach2<8, true><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp, rg, nb); break;
-              case 100: k_reattach3<true, 2048, true><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr, nullptr, 0, 0, pp); break;
-              default: k_reattach3<false, 512, true><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr, gram, nb, 0, pp); break;
+              case 1: k_reattach2x<1><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp, rg, nb, pb, pseq); break;
+              case 2: k_reattach2x<2><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp, rg, nb, pb, pseq); break;
+              case 4: k_reattach2x<4><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp, rg, nb, pb, pseq); break;
+              case 8: k_reattach2x<8><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp, rg, nb, pb, pseq); break;
+              case 100: k_reattach3x<true, 2048><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr, nullptr, 0, 0, pp, pb, pseq); break;
+              default: k_reattach3x<false, 512><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr, gram, nb, 0, pp, pb, pseq); break;
+            }
+            pcy_count_launch();
+          } else {
+            switch (nper) {
+              case 1: k_reattach2<1><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp, rg, nb); break;
+              case 2: k_reattach2<2><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp, rg, nb); break;
+              case 4: k_reattach2<4><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp, rg, nb); break;
+              case 8: k_reattach2<8><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp, rg, nb); break;
+              case 100: k_reattach3<true, 2048><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr, nullptr, 0, 0, pp); break;
+              default: k_reattach3<false, 512><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr, gram, nb, 0, pp); break;
             }
             pcy_count_launch();
           }
-          switch (nper) {
-            case 1: k_reattach2<1><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp, rg, nb); pcy_count_launch(); break;
-            case 2: k_reattach2<2><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp, rg, nb); pcy_count_launch(); break;
-            case 4: k_reattach2<4><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp, rg, nb); pcy_count_launch(); break;
-            case 8: k_reattach2<8><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp, rg, nb); pcy_count_launch(); break;
-            case 100: k_reattach3<true, 2048><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr, nullptr, 0, 0, pp); pcy_count_launch(); break;
-            default: k_reattach3<false, 512><<<1, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr, gram, nb, 0, pp); pcy_count_launch(); break;
-          }
           PCY_LAUNCH_CHECK();
-          rc = sync_ctl(st); if (rc) return rc;
+          rc = selfp ? wait_seq(st, pseq) : sync_ctl(st); if (rc) return rc;
+          if (selfp && !self_publish()) { rc = sync_ctl(st); if (rc) return rc; }   // a group reached the panel size
           if (ctl_h->status == ST_ARENA) { pcy_set_error("member arena exhausted in rebuild"); return PCY_ESTATE; }
           if (ctl_h->status == ST_PAR_BROKEN) {
             pcy_set_error("subtree-parallel reattach met an excluded stop (inner status %d, window %lld, F %lld, m %lld)",
@@ -1849,9 +1866,9 @@ struct Engine {
         if (hi) { PCY_CUDA(cudaEventRecord(evk1, st)); PCY_CUDA(cudaStreamWaitEvent(hi, evk1, 0)); rs = hi; }
         if (prof) PCY_CUDA(cudaEventRecord(ev[1], rs));
         ParCtl* pp = nullptr;
+        bool selfp = false; long long pseq = 0;
         if (k3par) {
-          // k_plan picks a subtree-parallel window or a sequential stretch; the
-          // launch that was not chosen returns at once
+          // k_plan picks a subtree-parallel window or a sequential stretch
           if (nper != 101 && !gram_early) {   // opener rows against the batch (k_plan's conflict test)
             const int grc = pcy_launch_gram_split(Xs, nullptr, ld, (int)kn, d, gram, kn, gram_part, gram_split, rs);
             if (grc) return grc;
@@ -1860,33 +1877,41 @@ struct Engine {
                                                  (int)(NC / 32 + 1), nullptr, gram, kn);
           pcy_count_launch();
           pp = parctl;
+          // one launch serves either choice of k_plan and, while no group is
+          // in the K1 panel, publishes the counters itself
+          selfp = self_publish();
+          pseq = selfp ? ++seq : 0;
+          EngCtl* pb = selfp ? ctl_map_d : nullptr;
           switch (nper) {
-            case 1: k_resolve2<1, true><<<PCY_PAR_MAXCTA, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, pp); break;
-            case 2: k_resolve2<2, true><<<PCY_PAR_MAXCTA, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, pp); break;
-            case 4: k_resolve2<4, true><<<PCY_PAR_MAXCTA, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, pp); break;
-            case 8: k_resolve2<8, true><<<PCY_PAR_MAXCTA, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, pp); break;
-            case 100: k_resolve3<true, 2048, true><<<PCY_PAR_MAXCTA, 32, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, nullptr, 0, 0, pp); break;
-            case 101: k_resolve3<false, 512, true><<<PCY_PAR_MAXCTA, 32, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, gram, kn, 0, pp); break;
+            case 1: k_resolve2x<1><<<PCY_PAR_MAXCTA, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, pp, pb, pseq); break;
+            case 2: k_resolve2x<2><<<PCY_PAR_MAXCTA, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, pp, pb, pseq); break;
+            case 4: k_resolve2x<4><<<PCY_PAR_MAXCTA, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, pp, pb, pseq); break;
+            case 8: k_resolve2x<8><<<PCY_PAR_MAXCTA, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, pp, pb, pseq); break;
+            case 100: k_resolve3x<true, 2048><<<PCY_PAR_MAXCTA, 32, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, nullptr, 0, 0, pp, pb, pseq); break;
+            case 101: k_resolve3x<false, 512><<<PCY_PAR_MAXCTA, 32, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, gram, kn, 0, pp, pb, pseq); break;
           }
           pcy_count_launch();
-        }
-        switch (nper) {
-          case 1: k_resolve2<1><<<1, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, pp); pcy_count_launch(); break;
-          case 2: k_resolve2<2><<<1, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, pp); pcy_count_launch(); break;
-          case 4: k_resolve2<4><<<1, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, pp); pcy_count_launch(); break;
-          case 8: k_resolve2<8><<<1, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, pp); pcy_count_launch(); break;
-          case 100: k_resolve3<true, 2048><<<1, 32, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, nullptr, 0, 0, pp); pcy_count_launch(); break;
-          case 101: k_resolve3<false, 512><<<1, 32, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, gram, kn, 0, pp); pcy_count_launch(); break;
-          default:
-            k_resolve<<<1, 32, sizeof(double) * ld, rs>>>(E, Xs, XSs, Ws, Bs, kn, 0, first_rem, countw); pcy_count_launch();
+        } else {
+          switch (nper) {
+            case 1: k_resolve2<1><<<1, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, pp); pcy_count_launch(); break;
+            case 2: k_resolve2<2><<<1, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, pp); pcy_count_launch(); break;
+            case 4: k_resolve2<4><<<1, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, pp); pcy_count_launch(); break;
+            case 8: k_resolve2<8><<<1, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, pp); pcy_count_launch(); break;
+            case 100: k_resolve3<true, 2048><<<1, 32, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, nullptr, 0, 0, pp); pcy_count_launch(); break;
+            case 101: k_resolve3<false, 512><<<1, 32, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, gram, kn, 0, pp); pcy_count_launch(); break;
+            default:
+              k_resolve<<<1, 32, sizeof(double) * ld, rs>>>(E, Xs, XSs, Ws, Bs, kn, 0, first_rem, countw); pcy_count_launch();
+          }
         }
         if (prof) PCY_CUDA(cudaEventRecord(ev[2], rs));
         PCY_LAUNCH_CHECK();
-        int rc = sync_ctl(rs);
+        int rc = selfp ? wait_seq(rs, pseq) : sync_ctl(rs);
+        if (!rc && selfp && !self_publish()) rc = sync_ctl(rs);   // a group reached the panel size
         if (hi) { PCY_CUDA(cudaEventRecord(evk3, hi)); PCY_CUDA(cudaStreamWaitEvent(st, evk3, 0)); }
         if (rc) return rc;
         if (prof) {
           float t1 = 0.f, t2 = 0.f;
+          PCY_CUDA(cudaEventSynchronize(ev[2]));   // recorded after the self-publishing kernel
           PCY_CUDA(cudaEventElapsedTime(&t1, ev[0], ev[1]));
           PCY_CUDA(cudaEventElapsedTime(&t2, ev[1], ev[2]));
           const long long done = ctl_h->status == ST_DONE ? kn : ctl_h->stop + (ctl_h->status == ST_FULL ? 0 : 1);

@@ -2,6 +2,7 @@
 // kernels in engine.cu (see DESIGN.md §3 for the HBM layout).
 #pragma once
 #include "common.cuh"
+#include <cstddef>
 
 #define PCY_MAXL 24          // chain levels recorded per item by k_chain
 #define PCY_GROUP_MIN_CAP 4  // first arena extent of a group
@@ -41,8 +42,22 @@ struct EngCtl {
   // member visits of the chain walks (the reference's own dgemv work,
   // coreset.py:172) and the visits served by direct fp64 scans
   long long panel_n, cnt_vis, cnt_vis_direct;
+  // largest member count any group reached since the last tree reset: below
+  // PCY_PANEL_MIN no group is in the K1 panel, so the resolve kernels publish
+  // the counters themselves and the panel publication is skipped
+  long long maxg;
   long long seq;          // publication sequence number (mapped host mirror)
+  // k_plan's early publication (mirror only, written after `seq`'s words): the
+  // window it chose for K1 batch `plan_seq`, so the host can enqueue the next
+  // batch while the resolve kernel runs
+  long long plan_mode, plan_nwin, plan_seq;
 };
+
+// groups of at least this many members are contracted on the tensor cores
+// (the K1 panel, k_publish_panel); smaller groups are scanned directly
+constexpr int PCY_PANEL_MIN = 128;
+
+
 
 // Subtree-parallel resolve (k_plan + k_resolve2<NPER, true>, resolve_fast.cuh).
 // Between two changes of the root group, an item's decisions read and write
@@ -101,3 +116,18 @@ struct EngDev {
   int* order; int* lvl; int* stk_g; int* stk_p;
   unsigned long long* minbits;
 };
+
+// One thread copies the device counters to the mapped host mirror and then
+// writes the sequence number the host spins on (same protocol as k_publish).
+// Counters other CTAs updated with atomics are read at L2 (volatile).
+__device__ __forceinline__ void ctl_publish_thread(const EngDev& E, EngCtl* dst, long long seq) {
+  EngCtl* src = E.ctl;
+  src->root_count = *(volatile const int*)&E.g_count[0];
+  src->root_base = *(volatile const int*)&E.g_base[0];
+  const int words = (int)(offsetof(EngCtl, seq) / sizeof(long long));
+  volatile const long long* s = reinterpret_cast<volatile const long long*>(src);
+  volatile long long* t = reinterpret_cast<volatile long long*>(dst);
+  for (int k = 0; k < words; ++k) t[k] = s[k];
+  __threadfence_system();
+  t[words] = seq;
+}

@@ -96,11 +96,12 @@ __global__ void k_rchain(EngDev E, const int* __restrict__ order, long long n, C
 // PAR = true: CTA b reattaches the nodes of k_plan's subtree list b (the same
 // partition argument as the resolve: merges change only the host, adds only
 // the group of the parent); PAR = false with `par`: k_plan's sequential stretch.
-template <int NPER, bool PAR = false>
-__global__ void __launch_bounds__(32, 1) k_reattach2(EngDev E, const int* __restrict__ order, long long n,
-                                                     int nnew_cap, const ChainHdr* __restrict__ H,
-                                                     const ChainLvl* __restrict__ R, ParCtl* __restrict__ par = nullptr,
-                                                     const double* __restrict__ gram = nullptr, long long gld = 0) {
+template <int NPER, bool PAR>
+__device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __restrict__ order, long long n,
+                                               int nnew_cap, const ChainHdr* __restrict__ H,
+                                               const ChainLvl* __restrict__ R, ParCtl* __restrict__ par,
+                                               const double* __restrict__ gram, long long gld,
+                                               EngCtl* pub, long long pseq) {
   extern __shared__ __align__(16) unsigned char smraw[];
   ReattachSmem& S = *reinterpret_cast<ReattachSmem*>(smraw);
   const int lane = threadIdx.x;
@@ -419,6 +420,7 @@ __global__ void __launch_bounds__(32, 1) k_reattach2(EngDev E, const int* __rest
     if (lane == 0) {
       S.tbase[t] = nb; S.tcap[t] = ncap;
       E.g_base[g] = nb; E.g_cap[g] = ncap; E.g_count[g] = cnt + total;
+      if (cnt + total >= PCY_PANEL_MIN) atomicMax(&C->maxg, (long long)(cnt + total));
     }
     __syncwarp();
   }
@@ -445,6 +447,7 @@ __global__ void __launch_bounds__(32, 1) k_reattach2(EngDev E, const int* __rest
         C->status = fail ? fail : (par->n_win < par->n_total ? ST_FULL : ST_DONE);
         C->stop = par->n_win;
         __threadfence();
+        if (pub) ctl_publish_thread(E, pub, pseq);
       }
     }
     return;
@@ -453,5 +456,26 @@ __global__ void __launch_bounds__(32, 1) k_reattach2(EngDev E, const int* __rest
   if (lane == 0) {
     C->F = F; C->free_n = freen; C->G_alloc = Galloc; C->A_alloc = Aalloc;
     C->status = status; C->stop = stop;
+    __threadfence();
+    if (pub) ctl_publish_thread(E, pub, pseq);
   }
+}
+
+template <int NPER, bool PAR = false>
+__global__ void __launch_bounds__(32, 1) k_reattach2(EngDev E, const int* __restrict__ order, long long n,
+                                                     int nnew_cap, const ChainHdr* __restrict__ H,
+                                                     const ChainLvl* __restrict__ R, ParCtl* __restrict__ par = nullptr,
+                                                     const double* __restrict__ gram = nullptr, long long gld = 0) {
+  reattach2_body<NPER, PAR>(E, order, n, nnew_cap, H, R, par, gram, gld, nullptr, 0);
+}
+
+// One launch for either choice of k_plan (as k_resolve2x).
+template <int NPER>
+__global__ void __launch_bounds__(32, 1) k_reattach2x(EngDev E, const int* __restrict__ order, long long n,
+                                                      int nnew_cap, const ChainHdr* __restrict__ H,
+                                                      const ChainLvl* __restrict__ R, ParCtl* __restrict__ par,
+                                                      const double* __restrict__ gram, long long gld,
+                                                      EngCtl* pub, long long pseq) {
+  if (par->mode == 0) reattach2_body<NPER, true>(E, order, n, nnew_cap, H, R, par, gram, gld, pub, pseq);
+  else if (blockIdx.x == 0) reattach2_body<NPER, false>(E, order, n, nnew_cap, H, R, par, gram, gld, pub, pseq);
 }

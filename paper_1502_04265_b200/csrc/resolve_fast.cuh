@@ -287,12 +287,15 @@ constexpr int K3_SLOTS = 4, K3_BAR_FULL = 1, K3_BAR_EMPTY = 1 + K3_SLOTS;   // +
 // non-null it runs only when k_plan chose the sequential mode, for
 // par->n_win items).  PAR = true: CTA b resolves the items of root subtree
 // list b of k_plan's window (see ParCtl), allocating through the tickets.
-template <int NPER, bool PAR = false>
-__global__ void __launch_bounds__(64, 1) k_resolve2(EngDev E, const double* __restrict__ X,
-                                                    const double* __restrict__ XS, const long long* __restrict__ W,
-                                                    const int* __restrict__ BAD, long long n, long long first_rem,
-                                                    int countw, int nnew_cap, const ChainHdr* __restrict__ H,
-                                                    const ChainLvl* __restrict__ R, ParCtl* __restrict__ par = nullptr) {
+// pub / pseq (k_resolve2x only): the CTA that finishes the window copies the
+// counters to the host mirror itself (no separate publication launch).
+template <int NPER, bool PAR>
+__device__ __forceinline__ void resolve2_body(const EngDev& E, const double* __restrict__ X,
+                                              const double* __restrict__ XS, const long long* __restrict__ W,
+                                              const int* __restrict__ BAD, long long n, long long first_rem,
+                                              int countw, int nnew_cap, const ChainHdr* __restrict__ H,
+                                              const ChainLvl* __restrict__ R, ParCtl* __restrict__ par,
+                                              EngCtl* pub, long long pseq) {
   extern __shared__ __align__(16) unsigned char smraw[];
   ResolveSmem& S = *reinterpret_cast<ResolveSmem*>(smraw);
   const int lane = threadIdx.x & 31;
@@ -758,6 +761,7 @@ __global__ void __launch_bounds__(64, 1) k_resolve2(EngDev E, const double* __re
     if (lane == 0) {
       S.tbase[t] = nb; S.tcap[t] = ncap;
       E.g_base[g] = nb; E.g_cap[g] = ncap; E.g_count[g] = cnt + total;
+      if (cnt + total >= PCY_PANEL_MIN) atomicMax(&C->maxg, (long long)(cnt + total));
     }
     __syncwarp();
   }
@@ -797,6 +801,7 @@ __global__ void __launch_bounds__(64, 1) k_resolve2(EngDev E, const double* __re
         C->status = fail ? fail : (par->n_win < par->n_total ? ST_FULL : ST_DONE);
         C->err = fail ? par->pad : 0; C->stop = par->n_win; C->remaining = 0;
         __threadfence();
+        if (pub) ctl_publish_thread(E, pub, pseq);
       }
     }
     return;
@@ -808,7 +813,31 @@ __global__ void __launch_bounds__(64, 1) k_resolve2(EngDev E, const double* __re
     C->status = status; C->err = err; C->stop = stop; C->remaining = remaining;
     C->cnt_levels += c_lv; C->cnt_direct += c_dir; C->cnt_demand += c_dem; C->cnt_slow += c_slow;
     C->cnt_items += c_it; C->cnt_dem_fast += c_demf; C->cnt_touch_child += c_tch;
+    __threadfence();
+    if (pub) ctl_publish_thread(E, pub, pseq);
   }
+}
+
+template <int NPER, bool PAR = false>
+__global__ void __launch_bounds__(64, 1) k_resolve2(EngDev E, const double* __restrict__ X,
+                                                    const double* __restrict__ XS, const long long* __restrict__ W,
+                                                    const int* __restrict__ BAD, long long n, long long first_rem,
+                                                    int countw, int nnew_cap, const ChainHdr* __restrict__ H,
+                                                    const ChainLvl* __restrict__ R, ParCtl* __restrict__ par = nullptr) {
+  resolve2_body<NPER, PAR>(E, X, XS, W, BAD, n, first_rem, countw, nnew_cap, H, R, par, nullptr, 0);
+}
+
+// One launch for either choice of k_plan: the subtree-parallel window (every
+// CTA with a list) or the sequential stretch (CTA 0).
+template <int NPER>
+__global__ void __launch_bounds__(64, 1) k_resolve2x(EngDev E, const double* __restrict__ X,
+                                                     const double* __restrict__ XS, const long long* __restrict__ W,
+                                                     const int* __restrict__ BAD, long long n, long long first_rem,
+                                                     int countw, int nnew_cap, const ChainHdr* __restrict__ H,
+                                                     const ChainLvl* __restrict__ R, ParCtl* __restrict__ par,
+                                                     EngCtl* pub, long long pseq) {
+  if (par->mode == 0) resolve2_body<NPER, true>(E, X, XS, W, BAD, n, first_rem, countw, nnew_cap, H, R, par, pub, pseq);
+  else if (blockIdx.x == 0) resolve2_body<NPER, false>(E, X, XS, W, BAD, n, first_rem, countw, nnew_cap, H, R, par, pub, pseq);
 }
 
 // ------------------------------------------------------------- K3 planner

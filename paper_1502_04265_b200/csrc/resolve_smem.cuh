@@ -300,13 +300,14 @@ __device__ bool table_cleanup(const EngDev& E, ResolveSmemT<MS>& S, int nnew, lo
 constexpr int REC3_CHUNKS = PCY_FMAXL * (int)sizeof(ChainLvl) / 16;
 
 // PAR / par: as k_resolve2 (k_plan windows, one CTA per subtree list).
-template <bool TROWS, int MS, bool PAR = false>
-__global__ void __launch_bounds__(32, 1) k_resolve3(EngDev E, const double* __restrict__ X,
-                                                    const double* __restrict__ XS, const long long* __restrict__ W,
-                                                    const int* __restrict__ BAD, long long n, long long first_rem,
-                                                    int countw, int nnew_cap, const ChainHdr* __restrict__ H,
-                                                    const ChainLvl* __restrict__ R, const double* __restrict__ gram,
-                                                    long long gld, long long goff, ParCtl* __restrict__ par = nullptr) {
+template <bool TROWS, int MS, bool PAR>
+__device__ __forceinline__ void resolve3_body(const EngDev& E, const double* __restrict__ X,
+                                              const double* __restrict__ XS, const long long* __restrict__ W,
+                                              const int* __restrict__ BAD, long long n, long long first_rem,
+                                              int countw, int nnew_cap, const ChainHdr* __restrict__ H,
+                                              const ChainLvl* __restrict__ R, const double* __restrict__ gram,
+                                              long long gld, long long goff, ParCtl* __restrict__ par,
+                                              EngCtl* pub, long long pseq) {
   extern __shared__ __align__(16) unsigned char smraw[];
   ResolveSmemT<MS>& S = *reinterpret_cast<ResolveSmemT<MS>*>(smraw);
   const int lane = threadIdx.x;
@@ -676,6 +677,7 @@ __global__ void __launch_bounds__(32, 1) k_resolve3(EngDev E, const double* __re
         C->status = fail ? fail : (par->n_win < par->n_total ? ST_FULL : ST_DONE);
         C->err = fail ? par->pad : 0; C->stop = par->n_win; C->remaining = 0;
         __threadfence();
+        if (pub) ctl_publish_thread(E, pub, pseq);
       }
     }
     return;
@@ -687,15 +689,43 @@ __global__ void __launch_bounds__(32, 1) k_resolve3(EngDev E, const double* __re
     C->status = status; C->err = err; C->stop = stop; C->remaining = remaining;
     C->cnt_levels += c_lv; C->cnt_direct += c_dir; C->cnt_demand += c_dem; C->cnt_slow += c_slow;
     C->cnt_items += c_it;
+    __threadfence();
+    if (pub) ctl_publish_thread(E, pub, pseq);
   }
 }
 
-// ------------------------------------------------------------- reattach
 template <bool TROWS, int MS, bool PAR = false>
-__global__ void __launch_bounds__(32, 1) k_reattach3(EngDev E, const int* __restrict__ order, long long n,
-                                                     int nnew_cap, const ChainHdr* __restrict__ H,
+__global__ void __launch_bounds__(32, 1) k_resolve3(EngDev E, const double* __restrict__ X,
+                                                    const double* __restrict__ XS, const long long* __restrict__ W,
+                                                    const int* __restrict__ BAD, long long n, long long first_rem,
+                                                    int countw, int nnew_cap, const ChainHdr* __restrict__ H,
+                                                    const ChainLvl* __restrict__ R, const double* __restrict__ gram,
+                                                    long long gld, long long goff, ParCtl* __restrict__ par = nullptr) {
+  resolve3_body<TROWS, MS, PAR>(E, X, XS, W, BAD, n, first_rem, countw, nnew_cap, H, R, gram, gld, goff, par, nullptr, 0);
+}
+
+// One launch for either choice of k_plan (as k_resolve2x).
+template <bool TROWS, int MS>
+__global__ void __launch_bounds__(32, 1) k_resolve3x(EngDev E, const double* __restrict__ X,
+                                                     const double* __restrict__ XS, const long long* __restrict__ W,
+                                                     const int* __restrict__ BAD, long long n, long long first_rem,
+                                                     int countw, int nnew_cap, const ChainHdr* __restrict__ H,
                                                      const ChainLvl* __restrict__ R, const double* __restrict__ gram,
-                                                     long long gld, long long goff, ParCtl* __restrict__ par = nullptr) {
+                                                     long long gld, long long goff, ParCtl* __restrict__ par,
+                                                     EngCtl* pub, long long pseq) {
+  if (par->mode == 0)
+    resolve3_body<TROWS, MS, true>(E, X, XS, W, BAD, n, first_rem, countw, nnew_cap, H, R, gram, gld, goff, par, pub, pseq);
+  else if (blockIdx.x == 0)
+    resolve3_body<TROWS, MS, false>(E, X, XS, W, BAD, n, first_rem, countw, nnew_cap, H, R, gram, gld, goff, par, pub, pseq);
+}
+
+// ------------------------------------------------------------- reattach
+template <bool TROWS, int MS, bool PAR>
+__device__ __forceinline__ void reattach3_body(const EngDev& E, const int* __restrict__ order, long long n,
+                                               int nnew_cap, const ChainHdr* __restrict__ H,
+                                               const ChainLvl* __restrict__ R, const double* __restrict__ gram,
+                                               long long gld, long long goff, ParCtl* __restrict__ par,
+                                               EngCtl* pub, long long pseq) {
   extern __shared__ __align__(16) unsigned char smraw[];
   ResolveSmemT<MS>& S = *reinterpret_cast<ResolveSmemT<MS>*>(smraw);
   const int lane = threadIdx.x;
@@ -959,6 +989,7 @@ __global__ void __launch_bounds__(32, 1) k_reattach3(EngDev E, const int* __rest
         C->status = fail ? fail : (par->n_win < par->n_total ? ST_FULL : ST_DONE);
         C->stop = par->n_win;
         __threadfence();
+        if (pub) ctl_publish_thread(E, pub, pseq);
       }
     }
     return;
@@ -967,5 +998,26 @@ __global__ void __launch_bounds__(32, 1) k_reattach3(EngDev E, const int* __rest
   if (lane == 0) {
     C->F = F; C->free_n = freen; C->G_alloc = Galloc; C->A_alloc = Aalloc;
     C->status = status; C->stop = stop;
+    __threadfence();
+    if (pub) ctl_publish_thread(E, pub, pseq);
   }
+}
+
+template <bool TROWS, int MS, bool PAR = false>
+__global__ void __launch_bounds__(32, 1) k_reattach3(EngDev E, const int* __restrict__ order, long long n,
+                                                     int nnew_cap, const ChainHdr* __restrict__ H,
+                                                     const ChainLvl* __restrict__ R, const double* __restrict__ gram,
+                                                     long long gld, long long goff, ParCtl* __restrict__ par = nullptr) {
+  reattach3_body<TROWS, MS, PAR>(E, order, n, nnew_cap, H, R, gram, gld, goff, par, nullptr, 0);
+}
+
+// One launch for either choice of k_plan (as k_resolve2x).
+template <bool TROWS, int MS>
+__global__ void __launch_bounds__(32, 1) k_reattach3x(EngDev E, const int* __restrict__ order, long long n,
+                                                      int nnew_cap, const ChainHdr* __restrict__ H,
+                                                      const ChainLvl* __restrict__ R, const double* __restrict__ gram,
+                                                      long long gld, long long goff, ParCtl* __restrict__ par,
+                                                      EngCtl* pub, long long pseq) {
+  if (par->mode == 0) reattach3_body<TROWS, MS, true>(E, order, n, nnew_cap, H, R, gram, gld, goff, par, pub, pseq);
+  else if (blockIdx.x == 0) reattach3_body<TROWS, MS, false>(E, order, n, nnew_cap, H, R, gram, gld, goff, par, pub, pseq);
 }
