@@ -127,7 +127,7 @@ class BicoEngine:
     """
 
     def __init__(self, dim: int, budget: int, *, bootstrap_cap: int = 1001,
-                 device=None, block_rows: int = 4096, host_buffer: int = 8192):
+                 device=None, block_rows: int = 0, host_buffer: int = 8192):
         if dim < 1:
             raise ValueError("dim must be >= 1")
         if budget < 1:

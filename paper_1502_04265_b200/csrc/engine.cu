@@ -1326,7 +1326,7 @@ struct Engine {
   cudaEvent_t done_ev = nullptr;
   bool done_rec = false;
   EngCtl* ctl_map_d = nullptr;   // device view of the mirror
-  long long seq = 0;
+  long long seq = 0, plan_seq = 0;
   long long* aggw = nullptr;
   double* mp_nrm = nullptr;
   cudaEvent_t ev[8] = {};
@@ -1364,6 +1364,7 @@ struct Engine {
   int nper = 0;          // resolve kernel: 1..8 register rows, 100/101 shared-memory rows, 0 generic
   int nnew_cap = 0, rea_cap = 0;   // new-node table sizes of K3 and of the reattach
   int rea_cap_t = 0;               // reattach table with reference rows (no batch Gram)
+  int rea_ts_cap = 0;              // entries of the Gram-scored table whose s rows stay in shared memory
   bool rea_gram = false;           // k_reattach2 takes new-entry dots from the batch Gram
   size_t rea_smem_t = 0, rea_smem_g = 0;
   size_t res_smem = 0, rea_smem = 0;
@@ -1412,6 +1413,21 @@ struct Engine {
   // The window kernels publish themselves while no group is in the K1 panel
   // (k_resolve2x & co.); the panel publication is a separate launch.
   bool self_publish() const { return !panel || ctl_h->maxg < PCY_PANEL_MIN; }
+  // k_plan's early publication (mirror words after `seq`)
+  int wait_plan(cudaStream_t st, long long want) {
+    volatile long long* sp = &ctl_h->plan_seq;
+    for (long long spins = 0; *sp != want; ++spins) {
+      if ((spins & 1023) == 1023) {
+        const cudaError_t e = cudaStreamQuery(st);
+        if (e != cudaSuccess && e != cudaErrorNotReady) {
+          pcy_set_error("engine kernel failed: %s", cudaGetErrorString(e));
+          return PCY_ECUDA;
+        }
+      }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    return PCY_OK;
+  }
   int wait_seq(cudaStream_t st, long long want) {
     volatile long long* sp = &ctl_h->seq;
     for (long long spins = 0; *sp != want; ++spins) {
@@ -1432,7 +1448,13 @@ struct Engine {
     ld = (int)pcy_round_up(d, 4);
     sample_cap = budget + 1 < bootstrap_cap ? budget + 1 : bootstrap_cap;
     NC = m + 2; GC = NC + 2; AC = 24 * NC + 4096;
-    Bmax = block_rows > 0 ? block_rows : 4096;
+    // rows staged per block: windows run ahead of the host only inside a
+    // block, so small-d engines stage whole pieces (about 64 MB of rows)
+    if (block_rows > 0) Bmax = block_rows;
+    else {
+      const long long fit = ((long long)64 << 20) / (8LL * ld);
+      Bmax = fit < 4096 ? 4096 : fit > 16384 ? 16384 : fit / 1024 * 1024;
+    }
     PCY_CUDA(cudaSetDevice(dev));
     PCY_CUDA(cudaStreamCreateWithFlags(&own, cudaStreamNonBlocking));
     PCY_CUDA(cudaEventCreateWithFlags(&done_ev, cudaEventDisableTiming));
@@ -1502,6 +1524,11 @@ struct Engine {
       rea_cap_t = (int)rcap;
       rea_smem_t = reattach_smem_bytes(ld, rea_cap_t, NC, GC);
       rea_smem_g = reattach_smem_bytes(ld, PCY_NNEW_REA, NC, GC, false);
+      {   // s rows of the first entries in what is left of shared memory
+        const long long left = maxsm > rea_smem_g ? (long long)((maxsm - rea_smem_g) / (sizeof(double) * ld)) : 0;
+        rea_ts_cap = (int)(left > PCY_NNEW_REA ? PCY_NNEW_REA : left);
+        rea_smem_g += sizeof(double) * (size_t)ld * rea_ts_cap;
+      }
       rea_cap = rea_cap_t;
       rea_smem = rea_smem_t > rea_smem_g ? rea_smem_t : rea_smem_g;   // attribute: either variant fits
       if (nnew_cap < 8) { nper = 0; use_tc = false; }
@@ -1706,7 +1733,10 @@ struct Engine {
       if (prof) PCY_CUDA(cudaEventRecord(ev[3], st));
       int rc;
       if (nper) {
-        long long off = 0, batch = 1024;   // K1 rows per reattach launch, adapted to where launches stop
+        // K1 rows per reattach launch, adapted to where launches stop.  The
+        // first launches meet an empty tree (one domain: every node is a root
+        // or competes for one), so they stay short until roots exist.
+        long long off = 0, batch = k3par ? 64 : 1024;
         const int wpc = ld <= 512 ? 8 : (ld <= 2048 ? 4 : 2);
         while (off < nodes) {
           const long long nb = nodes - off < batch ? nodes - off : batch;
@@ -1739,7 +1769,7 @@ struct Engine {
             }
             k_plan<<<1, PCY_PAR_MAXITEMS, plan_smem, st>>>(E, nullptr, nullptr, nullptr, nb, -1, nper <= 8 ? rea_cap : nnew_cap,
                                                    16, chh, chr, parctl, (int)(NC / 32 + 1), E.order + off,
-                                                   gram, nb);
+                                                   gram, nb, nullptr, 0);
             pcy_count_launch();
             pp = parctl;
             // one launch serves either choice of k_plan and, while no group is
@@ -1748,10 +1778,10 @@ struct Engine {
             pseq = selfp ? ++seq : 0;
             EngCtl* pb = selfp ? ctl_map_d : nullptr;
             switch (nper) {
-              case 1: k_reattach2x<1><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp, rg, nb, pb, pseq); break;
-              case 2: k_reattach2x<2><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp, rg, nb, pb, pseq); break;
-              case 4: k_reattach2x<4><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp, rg, nb, pb, pseq); break;
-              case 8: k_reattach2x<8><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp, rg, nb, pb, pseq); break;
+              case 1: k_reattach2x<1><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp, rg, nb, pb, pseq, rg ? rea_ts_cap : 0); break;
+              case 2: k_reattach2x<2><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp, rg, nb, pb, pseq, rg ? rea_ts_cap : 0); break;
+              case 4: k_reattach2x<4><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp, rg, nb, pb, pseq, rg ? rea_ts_cap : 0); break;
+              case 8: k_reattach2x<8><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, rea_cap, chh, chr, pp, rg, nb, pb, pseq, rg ? rea_ts_cap : 0); break;
               case 100: k_reattach3x<true, 2048><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr, nullptr, 0, 0, pp, pb, pseq); break;
               default: k_reattach3x<false, 512><<<PCY_PAR_MAXCTA, 32, rea_smem, st>>>(E, E.order + off, nb, nnew_cap, chh, chr, gram, nb, 0, pp, pb, pseq); break;
             }
@@ -1790,7 +1820,7 @@ struct Engine {
             batch = std::min<long long>(1024, std::max<long long>(128, 2 * ctl_h->stop));
           } else {
             off += nb;
-            batch = 1024;
+            batch = batch * 4 > 1024 ? 1024 : batch * 4;
           }
         }
       } else {
@@ -1817,64 +1847,76 @@ struct Engine {
   int live(const double* X, const double* XS, const long long* W, const int* BAD, long long n,
            int countw, cudaStream_t st, long long* bad_at, int* bad_code) {
     *bad_at = -1;
+    const int wpc = ld <= 512 ? 8 : (ld <= 2048 ? 4 : 2);
+    const bool gram_early = k3par && nper <= 8 && hi;   // small d only: at large d the Gram competes with the K1 contraction
+    // K1 of rows [s0, s0 + kn): the batch Gram for k_plan's open-conflict test
+    // (it depends only on the rows: on the K3 stream, beside the chain walk),
+    // the panel contraction and the chain walk.  Nothing here needs the host
+    // to know the tree (the panel size is the last publication's).
+    auto enqueue_k1 = [&](long long s0, long long kn, bool prof) -> int {
+      const double* Xs = X + s0 * ld;
+      const double* XSs = XS + s0;
+      const long long* Ws = W ? W + s0 : nullptr;
+      if (!nper) { k_snapshot<<<64, 256, 0, st>>>(E); pcy_count_launch(); }
+      if (prof) PCY_CUDA(cudaEventRecord(ev[0], st));
+      if (gram_early) {
+        PCY_CUDA(cudaEventRecord(evk1, st)); PCY_CUDA(cudaStreamWaitEvent(hi, evk1, 0));
+        const int grc = pcy_launch_gram_split(Xs, nullptr, ld, (int)kn, d, gram, kn, gram_part, gram_split, hi);
+        if (grc) return grc;
+      }
+      if (nper) {
+        int grc;
+        const bool use_p = full_set(Xs, nullptr, kn, st, &grc);
+        if (grc) return grc;
+        if (ld > 512)   // one item per CTA, dots split over 4 warps
+          k_chain2<4><<<(unsigned)(kn), 128, sizeof(double) * (ld + 8) + sizeof(int) * (TC_CAND_MAX + 4), st>>>(
+              E, Xs, XSs, Ws, kn, chh, chr, use_p ? parts : nullptr, ctl_h->F_alloc);
+        else
+          k_chain2<1><<<(unsigned)((kn + wpc - 1) / wpc), wpc * 32, sizeof(double) * wpc * ld, st>>>(
+              E, Xs, XSs, Ws, kn, chh, chr, use_p ? parts : nullptr, ctl_h->F_alloc);
+        pcy_count_launch();
+        if (nper == 101 && !gram_early) {
+          const int grc2 = pcy_launch_gram_split(Xs, nullptr, ld, (int)(kn), d, gram, kn, gram_part, gram_split, st);
+          if (grc2) return grc2;
+        }
+      } else {
+        k_chain<<<(unsigned)((kn + wpc - 1) / wpc), wpc * 32, sizeof(double) * wpc * ld, st>>>(E, Xs, XSs, kn); pcy_count_launch();
+      }
+      PCY_LAUNCH_CHECK();
+      return PCY_OK;
+    };
     long long off = 0;
     while (off < n) {
-      const long long sub = nper ? (long long)1024 : Bmax;   // items one K3 launch can usually absorb
+      // without the subtree-parallel planner one K3 launch absorbs about 1024 items
+      const long long sub = k3par ? n : (nper ? (long long)1024 : Bmax);
       const long long nb = n - off < sub ? n - off : sub;
       long long start = 0, first_rem = -1;
+      long long k1_kn = 0;   // > 0: K1 of rows [start, start + k1_kn) is already enqueued
       while (start < nb) {
         // K1 chains kn rows; with the subtree-parallel resolve the batch follows
         // where the windows stop, so rows are not re-chained many times
-        const long long kn = k3par && nb - start > kbatch ? kbatch : nb - start;
+        const long long kn = k1_kn > 0 ? k1_kn : (k3par && nb - start > kbatch ? kbatch : nb - start);
         const double* Xs = X + (off + start) * ld;
         const double* XSs = XS + off + start;
         const bool prof = pcy_prof_enabled();
-        int rc0 = PCY_OK;
         const long long* Ws = W ? W + off + start : nullptr;
         const int* Bs = BAD ? BAD + off + start : nullptr;
-        const int wpc = ld <= 512 ? 8 : (ld <= 2048 ? 4 : 2);
-        const unsigned nblk = (unsigned)((kn + wpc - 1) / wpc);
-        if (!nper) { k_snapshot<<<64, 256, 0, st>>>(E); pcy_count_launch(); }
-        if (prof) PCY_CUDA(cudaEventRecord(ev[0], st));
-        // the batch Gram for k_plan's open-conflict test depends only on the
-        // batch rows: on the K3 stream it runs beside the K1 contraction
-        const bool gram_early = k3par && nper <= 8 && hi;   // small d only: at large d the Gram competes with the K1 contraction
-        if (gram_early) {
-          PCY_CUDA(cudaEventRecord(evk1, st)); PCY_CUDA(cudaStreamWaitEvent(hi, evk1, 0));
-          const int grc = pcy_launch_gram_split(Xs, nullptr, ld, (int)kn, d, gram, kn, gram_part, gram_split, hi);
-          if (grc) return grc;
-        }
-        if (nper) {
-          int grc;
-          const bool use_p = full_set(Xs, nullptr, kn, st, &grc);
-          if (grc) return grc;
-          if (ld > 512)   // one item per CTA, dots split over 4 warps
-            k_chain2<4><<<(unsigned)(kn), 128, sizeof(double) * (ld + 8) + sizeof(int) * (TC_CAND_MAX + 4), st>>>(
-                E, Xs, XSs, Ws, kn, chh, chr, use_p ? parts : nullptr, ctl_h->F_alloc);
-          else
-            k_chain2<1><<<nblk, wpc * 32, sizeof(double) * wpc * ld, st>>>(E, Xs, XSs, Ws, kn, chh, chr,
-                                                                          use_p ? parts : nullptr, ctl_h->F_alloc);
-          pcy_count_launch();
-          if (nper == 101 && !gram_early) {
-            rc0 = pcy_launch_gram_split(Xs, nullptr, ld, (int)(kn), d, gram, kn, gram_part, gram_split, st);
-            if (rc0) return rc0;
-          }
-        } else {
-          k_chain<<<nblk, wpc * 32, sizeof(double) * wpc * ld, st>>>(E, Xs, XSs, kn); pcy_count_launch();
-        }
+        if (k1_kn == 0) { const int rc1 = enqueue_k1(off + start, kn, prof); if (rc1) return rc1; }
+        k1_kn = 0;
         cudaStream_t rs = st;
         if (hi) { PCY_CUDA(cudaEventRecord(evk1, st)); PCY_CUDA(cudaStreamWaitEvent(hi, evk1, 0)); rs = hi; }
         if (prof) PCY_CUDA(cudaEventRecord(ev[1], rs));
         ParCtl* pp = nullptr;
-        bool selfp = false; long long pseq = 0;
+        bool selfp = false; long long pseq = 0, planseq = 0;
         if (k3par) {
           // k_plan picks a subtree-parallel window or a sequential stretch
           if (nper != 101 && !gram_early) {   // opener rows against the batch (k_plan's conflict test)
             const int grc = pcy_launch_gram_split(Xs, nullptr, ld, (int)kn, d, gram, kn, gram_part, gram_split, rs);
             if (grc) return grc;
           }
+          planseq = ++plan_seq;
           k_plan<<<1, PCY_PAR_MAXITEMS, plan_smem, rs>>>(E, XSs, Ws, Bs, kn, first_rem, nnew_cap, 16, chh, chr, parctl,
-                                                 (int)(NC / 32 + 1), nullptr, gram, kn);
+                                                 (int)(NC / 32 + 1), nullptr, gram, kn, ctl_map_d, planseq);
           pcy_count_launch();
           pp = parctl;
           // one launch serves either choice of k_plan and, while no group is
@@ -1905,9 +1947,33 @@ struct Engine {
         }
         if (prof) PCY_CUDA(cudaEventRecord(ev[2], rs));
         PCY_LAUNCH_CHECK();
+        // the next K1 (on st) starts when this window's resolve has finished
+        if (hi) { PCY_CUDA(cudaEventRecord(evk3, hi)); PCY_CUDA(cudaStreamWaitEvent(st, evk3, 0)); }
+        // Run-ahead: k_plan publishes the window it chose before the resolve
+        // kernel runs.  A parallel window of n_win items ends at start + n_win
+        // whatever the resolve does (its only other outcomes are fatal), so the
+        // next batch's K1 is enqueued now and the host round trip hides behind
+        // the resolve kernel.  Needs the self-published counters (no panel
+        // launch between the windows) and a K1 that takes nothing from the host
+        // mirror (panel mode with an empty panel).
+        long long nstart = -1, nkn = 0, nkb = kbatch;
+#ifndef PCY_TRACE
+        if (selfp && panel && hi && !prof && first_rem < 0) {
+          int rcp = wait_plan(rs, planseq); if (rcp) return rcp;
+          if (ctl_h->plan_mode == 0) {
+            const long long nwin = ctl_h->plan_nwin;
+            if (nwin == kn) nkb = kbatch * 2 > 1024 ? 1024 : kbatch * 2;
+            else { const long long b2 = 2 * nwin; nkb = b2 < 128 ? 128 : b2 > 1024 ? 1024 : b2; }
+            nstart = start + nwin;
+            if (nwin > 0 && nstart < nb) {
+              nkn = nb - nstart > nkb ? nkb : nb - nstart;
+              rcp = enqueue_k1(off + nstart, nkn, false); if (rcp) return rcp;
+            }
+          }
+        }
+#endif
         int rc = selfp ? wait_seq(rs, pseq) : sync_ctl(rs);
         if (!rc && selfp && !self_publish()) rc = sync_ctl(rs);   // a group reached the panel size
-        if (hi) { PCY_CUDA(cudaEventRecord(evk3, hi)); PCY_CUDA(cudaStreamWaitEvent(st, evk3, 0)); }
         if (rc) return rc;
         if (prof) {
           float t1 = 0.f, t2 = 0.f;
@@ -1935,7 +2001,11 @@ struct Engine {
         const int status = ctl_h->status;
         if (status == ST_DONE) {
           if (k3par) kbatch = kbatch * 2 > 1024 ? 1024 : kbatch * 2;
-          if (kn < nb - start) { start += kn; first_rem = -1; continue; }
+          if (kn < nb - start) {
+            start += kn; first_rem = -1;
+            if (nkn > 0 && nstart == start) k1_kn = nkn;
+            continue;
+          }
           break;
         }
         if (status == ST_INVALID) { *bad_at = off + start + ctl_h->stop; *bad_code = ctl_h->err; return PCY_OK; }
@@ -1949,6 +2019,7 @@ struct Engine {
           if (ctl_h->stop == 0) { pcy_set_error("resolve made no progress"); return PCY_ESTATE; }
           start += ctl_h->stop; first_rem = -1;
           if (k3par) { const long long b2 = 2 * ctl_h->stop; kbatch = b2 < 128 ? 128 : b2 > 1024 ? 1024 : b2; }
+          if (nkn > 0 && nstart == start) k1_kn = nkn;
           continue;
         }
         if (status == ST_REBUILD) {

@@ -101,7 +101,7 @@ __device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __res
                                                int nnew_cap, const ChainHdr* __restrict__ H,
                                                const ChainLvl* __restrict__ R, ParCtl* __restrict__ par,
                                                const double* __restrict__ gram, long long gld,
-                                               EngCtl* pub, long long pseq) {
+                                               EngCtl* pub, long long pseq, int ts_cap) {
   extern __shared__ __align__(16) unsigned char smraw[];
   ReattachSmem& S = *reinterpret_cast<ReattachSmem*>(smraw);
   const int lane = threadIdx.x;
@@ -129,6 +129,22 @@ __device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __res
   const int mwords = (int)(E.NC / 32 + 1);
   unsigned* gbits = mbits + mwords;
   const int gwords = (int)(E.GC / 32 + 1);
+  // batch-Gram rows of the current and the next item (lower triangle: the
+  // columns of earlier items), staged with cp.async one item ahead so the
+  // scans of same-launch entries read shared memory
+  double* growb = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(mbits) +
+                                            ((sizeof(unsigned) * (size_t)(mwords + gwords) + 15) & ~size_t(15)));
+  auto stage_grow = [&](int buf, long long it) {
+    if (!gram) return;
+    const double* src = gram + it * gld;
+    double* dst = growb + buf * PCY_PAR_MAXITEMS;
+    for (int c = lane; c < (int)it; c += 32) cp_async8(dst + c, src + c);
+    cp_async_commit();
+  };
+  // s rows of the first ts_cap entries placed in this launch: in a fresh tree
+  // most hosts are such entries, and the merge test (coreset.py:407-417) then
+  // reads and updates shared memory instead of waiting on an HBM row per level
+  double* tsr = growb + 2 * PCY_PAR_MAXITEMS;
   EngCtl* C = E.ctl;
   const double T = C->T;
   long long F = C->F, freen = C->free_n, Galloc = C->G_alloc, Aalloc = C->A_alloc;
@@ -167,6 +183,8 @@ __device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __res
     const uint4* src = reinterpret_cast<const uint4*>(R + gix(0) * PCY_FMAXL);
     uint4* dst = reinterpret_cast<uint4*>(&S.rb[0][0]);
     for (int c = lane; c < REC_CHUNKS; c += 32) dst[c] = src[c];
+    stage_grow(0, gix(0));
+    cp_async_wait_all();
   }
   __syncwarp();
   int cur = 0;
@@ -190,6 +208,7 @@ __device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __res
       for (int q = 0; q < (REC_CHUNKS + 31) / 32; ++q) { const int c = lane + 32 * q; if (c < REC_CHUNKS) rpf[q] = src[c]; }
       if (hn.predj >= 0) load_row<NPER>(pn, E.s + (long long)hn.predj * ld, d, lane);
       if (i + 2 < n) { h2 = H[gix(i + 2)]; u2 = order[gix(i + 2)]; }
+      stage_grow(cur ^ 1, gix(i + 1));
     }
     // ---- item i: node u
     const int u = u_c;
@@ -223,7 +242,7 @@ __device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __res
         double np_ = INFINITY; int nt = 0x7fffffff;
         if (gram) {
           // same-launch nodes are rows of this batch: (current, earlier) entry of the batch Gram
-          const double* grow = gram + gix(i) * gld;
+          const double* grow = growb + cur * PCY_PAR_MAXITEMS;
           for (int c0 = 0; c0 < nnew; c0 += 32) {
             const int t = c0 + lane;
             if (t < nnew && S.tgrp[t] == g) {
@@ -266,7 +285,13 @@ __device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __res
           gs = (int)(((unsigned)g * 2654435761u) >> 24) & (PCY_GMAP_SLOTS - 1);
           while (S.gkey[gs] >= 0) gs = (gs + 1) & (PCY_GMAP_SLOTS - 1);
         }
+        if (t < ts_cap) {
+          double* hs = tsr + (long long)t * ld;
+#pragma unroll
+          for (int k = 0; k < NPER; ++k) { const int e = lane + 32 * k; if (e < ld) hs[e] = su[k]; }
+        }
         if (lane == 0) {
+          S.tdirty[t] = 0;
           S.tid[t] = u; S.tgrp[t] = g; S.tchild[t] = -1; S.tnext[t] = -1; S.titem[t] = (int)gix(i);
           S.tw[t] = wu_c; S.tq[t] = qu_c; S.tsn[t] = snu_c; S.trn[t] = rsq_c;
           if (had) { S.tnext[S.gtail[gs]] = t; S.gtail[gs] = t; }
@@ -278,6 +303,7 @@ __device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __res
       }
       // merge test with the host (coreset.py:407-417)
       const bool touched = bt < 0 && ((mbits[bj >> 5] >> (bj & 31)) & 1u);
+      const bool shost = bt >= 0 && bt < ts_cap;   // the host's s row is in shared memory
       int ms = -1;
       bool merge;
       long long mw; double mq, mnorm;
@@ -290,19 +316,36 @@ __device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __res
         if (bt >= 0) { hw = S.tw[bt]; hq = S.tq[bt]; hsn = S.tsn[bt]; }
         else if (touched) { ms = map_find(S, bj); hw = S.mw[ms]; hq = S.mq[ms]; hsn = S.msn[ms]; }
         else { hw = E.w[bj]; hq = E.q[bj]; hsn = E.sn[bj]; }
-        if (bj != prnode) { load_row<NPER>(pr, E.s + (long long)bj * ld, d, lane); prnode = bj; }
         double acc = 0.0;
+        if (shost) {
+          const double* hs = tsr + (long long)bt * ld;
 #pragma unroll
-        for (int k = 0; k < NPER; ++k) { const double v = radd(pr[k], su[k]); acc = fma(v, v, acc); }
+          for (int k = 0; k < NPER; ++k) {
+            const int e = lane + 32 * k;
+            const double v = radd(e < ld ? hs[e] : 0.0, su[k]);
+            acc = fma(v, v, acc);
+          }
+        } else {
+          if (bj != prnode) { load_row<NPER>(pr, E.s + (long long)bj * ld, d, lane); prnode = bj; }
+#pragma unroll
+          for (int k = 0; k < NPER; ++k) { const double v = radd(pr[k], su[k]); acc = fma(v, v, acc); }
+        }
         mnorm = warp_sum(acc);
         mw = hw + wu_c; mq = radd(hq, qu_c);
         merge = rsub(mq, rdiv(mnorm, (double)mw)) <= T;
       }
       if (merge) {
-        if (bj != prnode) { load_row<NPER>(pr, E.s + (long long)bj * ld, d, lane); prnode = bj; }
+        if (shost) {
+          double* hs = tsr + (long long)bt * ld;
 #pragma unroll
-        for (int k = 0; k < NPER; ++k) pr[k] = radd(pr[k], su[k]);
-        store_row<NPER>(E.s + (long long)bj * ld, pr, d, lane);
+          for (int k = 0; k < NPER; ++k) { const int e = lane + 32 * k; if (e < d) hs[e] = radd(hs[e], su[k]); }
+          if (lane == 0) S.tdirty[bt] = 1;
+        } else {
+          if (bj != prnode) { load_row<NPER>(pr, E.s + (long long)bj * ld, d, lane); prnode = bj; }
+#pragma unroll
+          for (int k = 0; k < NPER; ++k) pr[k] = radd(pr[k], su[k]);
+          store_row<NPER>(E.s + (long long)bj * ld, pr, d, lane);
+        }
         if (bt >= 0) {
           if (lane == 0) { S.tw[bt] = mw; S.tq[bt] = mq; S.tsn[bt] = mnorm; }
           __syncwarp();
@@ -323,7 +366,7 @@ __device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __res
           if (lane == 0) { E.alive[u] = 0; E.free_ids[freen] = u; }
           ++freen;
         }
-        lastmod = bj;
+        lastmod = shost ? -1 : bj;   // a shared-memory host is never a K1-predicted node
         __syncwarp();
         break;
       }
@@ -371,13 +414,21 @@ __device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __res
       hc = hn; hn = h2;
       u_c = u_n; u_n = u2;
       wu_c = wu_n; qu_c = qu_n; snu_c = snu_n; rsq_c = rsq_n;
+      cp_async_wait_all();   // the next item's Gram row
       cur ^= 1;
     }
     __syncwarp();
   }
+  cp_async_wait_all();
 
   // ---- cleanup: statistics of placed nodes, memberships in position order
   __syncwarp();
+  for (int t = 0; t < nnew && t < ts_cap; ++t) {
+    if (!S.tdirty[t]) continue;
+    const double* hs = tsr + (long long)t * ld;
+    double* dst = E.s + (long long)S.tid[t] * ld;
+    for (int e = lane; e < d; e += 32) dst[e] = hs[e];
+  }
   for (int t = lane; t < nnew; t += 32) {
     const int node = S.tid[t];
     E.w[node] = S.tw[t]; E.q[node] = S.tq[t]; E.sn[node] = S.tsn[t];
@@ -466,7 +517,7 @@ __global__ void __launch_bounds__(32, 1) k_reattach2(EngDev E, const int* __rest
                                                      int nnew_cap, const ChainHdr* __restrict__ H,
                                                      const ChainLvl* __restrict__ R, ParCtl* __restrict__ par = nullptr,
                                                      const double* __restrict__ gram = nullptr, long long gld = 0) {
-  reattach2_body<NPER, PAR>(E, order, n, nnew_cap, H, R, par, gram, gld, nullptr, 0);
+  reattach2_body<NPER, PAR>(E, order, n, nnew_cap, H, R, par, gram, gld, nullptr, 0, 0);
 }
 
 // One launch for either choice of k_plan (as k_resolve2x).
@@ -475,7 +526,7 @@ __global__ void __launch_bounds__(32, 1) k_reattach2x(EngDev E, const int* __res
                                                       int nnew_cap, const ChainHdr* __restrict__ H,
                                                       const ChainLvl* __restrict__ R, ParCtl* __restrict__ par,
                                                       const double* __restrict__ gram, long long gld,
-                                                      EngCtl* pub, long long pseq) {
-  if (par->mode == 0) reattach2_body<NPER, true>(E, order, n, nnew_cap, H, R, par, gram, gld, pub, pseq);
-  else if (blockIdx.x == 0) reattach2_body<NPER, false>(E, order, n, nnew_cap, H, R, par, gram, gld, pub, pseq);
+                                                      EngCtl* pub, long long pseq, int ts_cap) {
+  if (par->mode == 0) reattach2_body<NPER, true>(E, order, n, nnew_cap, H, R, par, gram, gld, pub, pseq, ts_cap);
+  else if (blockIdx.x == 0) reattach2_body<NPER, false>(E, order, n, nnew_cap, H, R, par, gram, gld, pub, pseq, ts_cap);
 }

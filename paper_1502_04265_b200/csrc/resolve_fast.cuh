@@ -180,6 +180,7 @@ struct ResolveSmemN {
   int tk[NT], tfirst[NT], tcnt[NT], tbase[NT], tcap[NT];
   int titem[NT];   // k_reattach2: batch row of the node that placed the entry (its Gram row)
   int tgn[NT];     // k_reattach2: new entries of the group, at the group's first entry
+  int tdirty[NT];  // k_reattach2: the entry's shared-memory s row took a merge
   long long tw[NT];
   double trn[NT], tq[NT], tsn[NT];
   // item staging ring of k_resolve2 (producer warp -> decision warp), K3_SLOTS slots
@@ -203,8 +204,10 @@ __host__ __device__ inline size_t resolve_smem_bytes(int ld, int nnew, long long
 // k_reattach2 keeps only the reference rows of its new entries (no s rows),
 // and none when the batch Gram gives their dots (trows = false)
 __host__ __device__ inline size_t reattach_smem_bytes(int ld, int nnew, long long NC, long long GC, bool trows = true) {
+  // without reference rows the current and the next item's batch-Gram rows are staged instead
   return ((sizeof(ReattachSmem) + 15) & ~size_t(15)) + sizeof(double) * ((size_t)ld + (trows ? (size_t)nnew * (size_t)(ld | 1) : 0)) +
-         ((sizeof(unsigned) * (size_t)(NC / 32 + 1 + GC / 32 + 1) + 15) & ~size_t(15));
+         ((sizeof(unsigned) * (size_t)(NC / 32 + 1 + GC / 32 + 1) + 15) & ~size_t(15)) +
+         (trows ? 0 : sizeof(double) * 2 * PCY_PAR_MAXITEMS);
 }
 
 __device__ __forceinline__ int map_slot(int id) { return (int)(((unsigned)id * 2654435761u) >> 21) & (PCY_MOD_SLOTS - 1); }
@@ -923,7 +926,7 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
                                                            const ChainLvl* __restrict__ R, ParCtl* __restrict__ par,
                                                            int nwords,
                                                            const int* __restrict__ order, const double* __restrict__ gram,
-                                                           long long gld) {
+                                                           long long gld, EngCtl* pub, long long planseq) {
   extern __shared__ int plan_sm[];
   int* hkey = plan_sm;                    // domain keys: SUB(v) = v, OPEN(P) = NC + P, OPEN(ROOT) = 2 NC
   int* uf = plan_sm + PLAN_HASH;          // union-find over hash slots
@@ -1136,6 +1139,12 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
       if (first_rem < 0 && room >= theta && c0 < nn) ns = (s_last > c0 ? s_last : c0) + 1;
       if (ns > n) ns = n;
       par->n_win = ns;
+      if (pub) {   // early publication: the host may enqueue the next K1 batch now
+        volatile long long* t = &pub->plan_mode;
+        t[0] = 1; t[1] = ns;
+        __threadfence_system();
+        t[2] = planseq;
+      }
     }
     return;
   }
@@ -1237,6 +1246,12 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
     par->Aalloc0 = C->A_alloc; par->nidx0 = C->next_index;
     par->open_ticket = 0; par->g_ticket = 0; par->a_ticket = 0; par->done = 0; par->opens = 0;
     par->arena_fail = 0;
+    if (pub) {   // early publication: the host may enqueue the next K1 batch now
+      volatile long long* t = &pub->plan_mode;
+      t[0] = 0; t[1] = c;
+      __threadfence_system();
+      t[2] = planseq;
+    }
   }
   __syncthreads();
   if (tid < c) par->list[ctot[cta] + rank] = tid;

@@ -9,12 +9,6 @@
 // rows of nodes opened in the launch live in HBM at their slot.
 #pragma once
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // ld doubles (ld % 4 == 0, 32-B aligned rows) global -> shared, asynchronous
 __device__ __forceinline__ void row_fetch(double* dst, const double* src, int ld, int lane) {
