@@ -88,9 +88,25 @@ __device__ __forceinline__ double warp_scan32(double v, int lane) {
   }
   return v;
 }
+// Loads are issued ahead of the dependent scans (KS_CMAX blocks of 32 values,
+// KS_PMAX range totals per lane): one L2 round trip per draw level instead of
+// one per block.  The arithmetic and its order are unchanged.
+constexpr int KS_CMAX = 8, KS_PMAX = 16;
 __device__ double warp_range_total(const double* vals, long long p0, long long p1, int lane) {
   double tb = 0.0;
-  for (long long b0 = p0; b0 < p1; b0 += 32) {
+  double raw[KS_CMAX];
+#pragma unroll
+  for (int q = 0; q < KS_CMAX; ++q) {
+    const long long i = p0 + 32 * q + lane;
+    raw[q] = i < p1 ? __ldcg(vals + i) : 0.0;
+  }
+#pragma unroll
+  for (int q = 0; q < KS_CMAX; ++q) {
+    if (p0 + 32 * q >= p1) break;
+    const double v = warp_scan32(raw[q], lane);
+    tb = tb + __shfl_sync(PCY_FULL, v, 31);
+  }
+  for (long long b0 = p0 + 32 * KS_CMAX; b0 < p1; b0 += 32) {
     const long long i = b0 + lane;
     const double v = warp_scan32(i < p1 ? __ldcg(vals + i) : 0.0, lane);
     tb = tb + __shfl_sync(PCY_FULL, v, 31);
@@ -106,8 +122,17 @@ __device__ long long warp_draw(const double* part, int G, const double* __restri
                                int lane, double* total_out) {
   const int per = (G + 31) / 32;
   const int a = lane * per, b = min(G, a + per);
+  const bool regs = per <= KS_PMAX;
+  double pv[KS_PMAX];
+#pragma unroll
+  for (int t = 0; t < KS_PMAX; ++t) pv[t] = (regs && a + t < b) ? __ldcg(part + a + t) : 0.0;
   double loc = 0.0;
-  for (int c = a; c < b; ++c) loc += __ldcg(part + c);
+  if (regs) {
+#pragma unroll
+    for (int t = 0; t < KS_PMAX; ++t) if (a + t < b) loc += pv[t];
+  } else {
+    for (int c = a; c < b; ++c) loc += __ldcg(part + c);
+  }
   const double inc = warp_scan32(loc, lane);
   const double total = __shfl_sync(PCY_FULL, inc, 31);
   *total_out = total;
@@ -115,10 +140,21 @@ __device__ long long warp_draw(const double* part, int G, const double* __restri
   // the range holding the target: first c (lane order = range order)
   int cfound = 0x7fffffff;
   double cum = inc - loc, cstart = 0.0;
-  for (int c = a; c < b; ++c) {
-    const double pc = __ldcg(part + c);
-    if (cum + pc > target) { cfound = c; cstart = cum; break; }
-    cum += pc;
+  if (regs) {
+#pragma unroll
+    for (int t = 0; t < KS_PMAX; ++t) {
+      if (a + t < b && cfound == 0x7fffffff) {
+        const double pc = pv[t];
+        if (cum + pc > target) { cfound = a + t; cstart = cum; }
+        else cum += pc;
+      }
+    }
+  } else {
+    for (int c = a; c < b; ++c) {
+      const double pc = __ldcg(part + c);
+      if (cum + pc > target) { cfound = c; cstart = cum; break; }
+      cum += pc;
+    }
   }
   const unsigned hit = __ballot_sync(PCY_FULL, cfound != 0x7fffffff);
   if (!hit) return n - 1;
@@ -128,7 +164,23 @@ __device__ long long warp_draw(const double* part, int G, const double* __restri
   // in-range search, in the association of warp_range_total
   const long long p0 = ks_lo(n, cs, G), p1 = ks_lo(n, cs + 1, G);
   double tb = 0.0;
-  for (long long b0 = p0; b0 < p1; b0 += 32) {
+  double raw[KS_CMAX];
+#pragma unroll
+  for (int q = 0; q < KS_CMAX; ++q) {
+    const long long i = p0 + 32 * q + lane;
+    raw[q] = i < p1 ? __ldcg(vals + i) : 0.0;
+  }
+#pragma unroll
+  for (int q = 0; q < KS_CMAX; ++q) {
+    const long long b0 = p0 + 32 * q;
+    if (b0 >= p1) break;
+    const long long i = b0 + lane;
+    const double v = warp_scan32(raw[q], lane);
+    const unsigned over = __ballot_sync(PCY_FULL, i < p1 && cum + (tb + v) > target);
+    if (over) return b0 + __ffs(over) - 1;
+    tb = tb + __shfl_sync(PCY_FULL, v, 31);
+  }
+  for (long long b0 = p0 + 32 * KS_CMAX; b0 < p1; b0 += 32) {
     const long long i = b0 + lane;
     const double v = warp_scan32(i < p1 ? __ldcg(vals + i) : 0.0, lane);
     const unsigned over = __ballot_sync(PCY_FULL, i < p1 && cum + (tb + v) > target);
@@ -262,11 +314,10 @@ __global__ void __launch_bounds__(KS_THREADS) k_seed_coop(const double* __restri
       }
     }
     __syncthreads();
-    if (c == 0)
-      for (int r = 0; r < reps; ++r) {
-        double* C = centers + ((long long)r * k + j) * d;
-        for (int e = threadIdx.x; e < d; e += blockDim.x) C[e] = P[s_idx[r] * d + e];
-      }
+    for (int r = c; r < reps; r += G) {   // repetition r's centre row: CTA r mod G
+      double* C = centers + ((long long)r * k + j) * d;
+      for (int e = threadIdx.x; e < d; e += blockDim.x) C[e] = P[s_idx[r] * d + e];
+    }
     if (j == k - 1) break;
     // distances to the new centres, mass, range totals
     for (int r0 = 0; r0 < reps; r0 += rg) {
@@ -279,22 +330,31 @@ __global__ void __launch_bounds__(KS_THREADS) k_seed_coop(const double* __restri
       for (long long i = p0 + 2 * warp; i < p1; i += 2 * nwarp) {
         const long long ib = i + 1 < p1 ? i + 1 : -1;
         double acc[2][KS_RMAX];
+        // lane q keeps repetition q's running minimum of both rows: loaded
+        // before the distance pass, so the update below waits on nothing
+        double bprev[2] = {0.0, 0.0}, wrow[2] = {0.0, 0.0};
+        if (lane < rn) {
+          const long long rb = (long long)(r0 + lane) * n;
+          if (j > 0) { bprev[0] = best_all[rb + i]; if (ib >= 0) bprev[1] = best_all[rb + ib]; }
+          wrow[0] = w[i]; if (ib >= 0) wrow[1] = w[ib];
+        }
         seed_rows2(P + i * d, P + (ib >= 0 ? ib : i) * d, cs, d, rn, lane, acc);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const long long ii = h == 0 ? i : ib;
           if (ii < 0) break;
+          double mine = 0.0;   // lane q: distance to repetition q's newest centre
 #pragma unroll
           for (int q = 0; q < KS_RMAX; ++q) {
             if (q >= rn) break;
             const double a = warp_sum(acc[h][q]);
-            if (lane == 0) {
-              const int r = r0 + q;
-              double* best = best_all + (long long)r * n;
-              const double bb = j == 0 ? a : fmin(best[ii], a);
-              best[ii] = bb;
-              mass_w[(long long)r * n + ii] = rmul(w[ii], bb);
-            }
+            if (lane == q) mine = a;
+          }
+          if (lane < rn) {
+            const long long rb = (long long)(r0 + lane) * n;
+            const double bb = j == 0 ? mine : fmin(bprev[h], mine);
+            best_all[rb + ii] = bb;
+            mass_w[rb + ii] = rmul(wrow[h], bb);
           }
         }
       }

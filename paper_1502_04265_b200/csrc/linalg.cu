@@ -60,55 +60,68 @@ __global__ void k_gram_check(const double* __restrict__ G, int r, int expect_ide
 // solve.  A pivot that is not positive, not finite or at rounding level of the
 // Gram's scale (a rank-deficient sketch, where CholeskyQR amplifies noise)
 // sets status[0].
-__global__ void __launch_bounds__(256) k_chol_blk(double* __restrict__ G, int r, int k0, int kb,
-                                                  double* __restrict__ D, int* __restrict__ status) {
+__global__ void __launch_bounds__(4 * CHB) k_chol_blk(double* __restrict__ G, int r, int k0, int kb,
+                                                      double* __restrict__ D, int* __restrict__ status) {
+  // Four threads per row (factor) / per column (inverse), each taking every
+  // fourth element: two barriers per pivot column, warp shuffles in the inverse.
   extern __shared__ double blk_sm[];   // a (L11) and x (its inverse), CHB x (CHB + 1) each
   double (*a)[CHB + 1] = reinterpret_cast<double (*)[CHB + 1]>(blk_sm);
   double (*x)[CHB + 1] = reinterpret_cast<double (*)[CHB + 1]>(blk_sm + CHB * (CHB + 1));
+  __shared__ double colj[CHB];
+  __shared__ double s_piv;
   __shared__ int bad;
   if (*(volatile int*)status) return;
   const int tid = threadIdx.x;
   const double gmax = __longlong_as_double(*reinterpret_cast<const long long*>(status + 4));
   const double thr = 16.0 * 2.220446049250313e-16 * gmax;
   if (tid == 0) bad = 0;
-  for (int e = tid; e < kb * kb; e += blockDim.x) {
+  for (int e = tid; e < kb * kb; e += 4 * CHB) {
     const int i = e / kb, c = e % kb;
     a[i][c] = G[(long long)(k0 + i) * r + k0 + c];
   }
   __syncthreads();
-  for (int j = 0; j < kb; ++j) {
-    const double t = a[j][j];
-    if (!(t > 0.0) || !isfinite(t) || t <= thr) { if (tid == 0) bad = 1; break; }
-    const double piv = sqrt(t);
-    __syncthreads();
-    if (tid == 0) a[j][j] = piv;
-    for (int i = j + 1 + tid; i < kb; i += blockDim.x) a[i][j] /= piv;
-    __syncthreads();
-    // trailing lower triangle: 8 rows x 32 columns per pass (no index division)
-    const int ty = tid >> 5, tx = tid & 31;
-    for (int i = j + 1 + ty; i < kb; i += 8) {
-      const double lij = a[i][j];
-      for (int c = j + 1 + tx; c <= i; c += 32) a[i][c] = fma(-lij, a[c][j], a[i][c]);
+  {
+    const int i = tid & (CHB - 1), part = tid >> 6;   // row i, columns c = part (mod 4)
+    for (int j = 0; j < kb; ++j) {
+      if (tid == j) {
+        const double t = a[j][j];
+        if (!(t > 0.0) || !isfinite(t) || t <= thr) bad = 1;
+        else { const double piv = sqrt(t); a[j][j] = piv; s_piv = piv; }
+      }
+      __syncthreads();
+      if (bad) break;
+      if (part == 0 && i > j && i < kb) { const double l = a[i][j] / s_piv; a[i][j] = l; colj[i] = l; }
+      __syncthreads();
+      if (i > j && i < kb) {
+        const double l = colj[i];
+        double* __restrict__ row = a[i];
+        for (int c = j + 1 + part; c <= i; c += 4) row[c] = fma(-l, colj[c], row[c]);
+      }
     }
-    __syncthreads();
   }
   __syncthreads();
   if (bad) { if (tid == 0) atomicOr(status, 1); return; }
-  // D = L11^-1 by rows: x[i][j] = -(sum_{k=j}^{i-1} L[i][k] x[k][j]) / L[i][i]
-  for (int i = 0; i < kb; ++i) {
-    for (int j = tid; j <= i; j += blockDim.x) {
-      double v;
-      if (j == i) v = 1.0 / a[i][i];
-      else {
-        double acc = 0.0;
-        for (int k = j; k < i; ++k) acc = fma(a[i][k], x[k][j], acc);
-        v = -acc / a[i][i];
-      }
-      x[i][j] = v;
+  // D = L11^-1: x[i][j] = -(sum_{k=j}^{i-1} L[i][k] x[k][j]) / L[i][i].  Column j
+  // belongs to four adjacent lanes (k = j + q, j + q + 4, ...), their partial
+  // sums added in lane order.
+  {
+    const int j = tid >> 2, q = tid & 3;
+    const bool on = j < kb;
+    if (on && q == 0) x[j][j] = 1.0 / a[j][j];
+    __syncwarp();
+    for (int i = 1; i < kb; ++i) {   // uniform trip count: the shuffles need the whole warp
+      double acc = 0.0;
+      if (on && i > j)
+        for (int k = j + q; k < i; k += 4) acc = fma(a[i][k], x[k][j], acc);
+      const double a1 = __shfl_down_sync(0xffffffffu, acc, 1);
+      const double a2 = __shfl_down_sync(0xffffffffu, acc, 2);
+      const double a3 = __shfl_down_sync(0xffffffffu, acc, 3);
+      if (on && i > j && q == 0) x[i][j] = -(((acc + a1) + a2) + a3) / a[i][i];
+      __syncwarp();
     }
-    __syncthreads();
   }
-  for (int e = tid; e < kb * kb; e += blockDim.x) {
+  __syncthreads();
+  for (int e = tid; e < kb * kb; e += 4 * CHB) {
     const int i = e / kb, c = e % kb;
     G[(long long)(k0 + i) * r + k0 + c] = c <= i ? a[i][c] : 0.0;
     D[(long long)i * CHB + c] = c <= i ? x[i][c] : 0.0;
@@ -497,7 +510,7 @@ static int cholqr(cudaStream_t st, double* Y, long long rows, int r, double* Gs,
     k_gram_check<<<eb, 256, 0, st>>>(Gs, r, pass, status); pcy_count_launch();
     for (int k0 = 0; k0 < r; k0 += CHB) {
       const int kb = std::min(CHB, r - k0), rest = r - k0 - kb;
-      k_chol_blk<<<1, 256, blk_smem, st>>>(Gs, r, k0, kb, D + (long long)k0 * CHB, status); pcy_count_launch();
+      k_chol_blk<<<1, 4 * CHB, blk_smem, st>>>(Gs, r, k0, kb, D + (long long)k0 * CHB, status); pcy_count_launch();
       if (rest > 0) {
         // panel L21 = A21 L11^-T (through T), trailing A22 -= L21 L21^T
         double* A21 = Gs + (long long)(k0 + kb) * r + k0;
