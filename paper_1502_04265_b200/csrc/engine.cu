@@ -1992,10 +1992,13 @@ struct Engine {
         }
 #ifdef PCY_TRACE
         {   // build-time diagnostics only (PCY_NVCC_EXTRA=-DPCY_TRACE)
-          int pm[2] = {-1, 0};
-          if (k3par) cudaMemcpy(pm, parctl, sizeof(pm), cudaMemcpyDeviceToHost);
-          fprintf(stderr, "[ins] start %lld kn %lld status %d stop %lld mode %d P %d F %lld\n", off + start, kn,
-                  ctl_h->status, ctl_h->stop, pm[0], pm[1], ctl_h->F);
+          int pm[2] = {-1, 0}, dbg[3] = {0, 0, 0};
+          if (k3par) {
+            cudaMemcpy(pm, parctl, sizeof(pm), cudaMemcpyDeviceToHost);
+            cudaMemcpy(dbg, &parctl->dbg_sets, sizeof(dbg), cudaMemcpyDeviceToHost);
+          }
+          fprintf(stderr, "[ins] start %lld kn %lld status %d stop %lld mode %d P %d F %lld sets %d maxset %d maxcta %d\n", off + start, kn,
+                  ctl_h->status, ctl_h->stop, pm[0], pm[1], ctl_h->F, dbg[0], dbg[1], dbg[2]);
         }
 #endif
         const int status = ctl_h->status;

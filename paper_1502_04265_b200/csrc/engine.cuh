@@ -77,6 +77,7 @@ struct ParCtl {
   long long F0, Falloc0, freen0, Galloc0, Aalloc0, nidx0;   // control snapshot
   unsigned long long open_ticket, g_ticket, a_ticket, done, opens;
   int arena_fail, pad;
+  int dbg_sets, dbg_maxset, dbg_maxcta, dbg_pad;   // PCY_TRACE builds: domain sets, largest set, longest CTA list
   int off[PCY_PAR_MAXCTA + 1];
   int list[PCY_PAR_MAXITEMS];
 };

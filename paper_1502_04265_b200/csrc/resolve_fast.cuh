@@ -1178,6 +1178,19 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
   if (act) atomicMin(&hfirst[root], tid);
   __syncthreads();
   const int isfirst = act && hfirst[root] == tid;
+#ifdef PCY_TRACE
+  {   // build-time diagnostics: set sizes
+    __shared__ int s_dbg[2];
+    if (tid < 2) s_dbg[tid] = 0;
+    for (int hh = tid; hh < PLAN_HASH; hh += blockDim.x) tmin[hh] = 0;
+    __syncthreads();
+    if (act) atomicAdd(&tmin[root], 1);
+    __syncthreads();
+    if (isfirst) { atomicAdd(&s_dbg[0], 1); atomicMax(&s_dbg[1], tmin[root]); }
+    __syncthreads();
+    if (tid == 0) { par->dbg_sets = s_dbg[0]; par->dbg_maxset = s_dbg[1]; }
+  }
+#endif
   // exclusive scan of isfirst in item order: set tickets
   const unsigned bal = __ballot_sync(PCY_FULL, isfirst);
   if (lane == 0) wsum[wid] = __popc(bal);
@@ -1195,7 +1208,103 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
   __syncthreads();
   if (isfirst) ohead[root] = wsum[wid] + __popc(bal & ((1u << lane) - 1u));
   __syncthreads();
-  const int cta = act ? ohead[root] % PCY_PAR_MAXCTA : -1 - lane;
+  // Balanced CTA lists.  A window of 1024 items has ~800 domain sets, most of
+  // one or two items and a few of tens; the resolve launch lasts as long as
+  // its longest list.  Sets of >= PLAN_BIG items are dealt out largest first
+  // in snake order; the small sets then fill the CTAs, in stream order, up to
+  // a common level (water-filling over the big sets' loads).  Deterministic.
+  constexpr int PLAN_BIG = 4, PLAN_NBIG = PCY_PAR_MAXITEMS / PLAN_BIG;
+  __shared__ int s_load[PCY_PAR_MAXCTA], s_cap[PCY_PAR_MAXCTA + 1];
+  __shared__ int s_bsz[PLAN_NBIG], s_broot[PLAN_NBIG];
+  __shared__ int s_nbig;
+  int* scnt = tmin;   // items per set (by hash slot); the budget bound is done with these tables
+  int* scta = tkey;   // CTA of each set
+  for (int hh = tid; hh < PLAN_HASH; hh += blockDim.x) scnt[hh] = 0;
+  if (tid < PCY_PAR_MAXCTA) s_load[tid] = 0;
+  __syncthreads();
+  if (act) atomicAdd(&scnt[root], 1);
+  __syncthreads();
+  const int ssz = isfirst ? scnt[root] : 0;
+  const bool bigf = isfirst && ssz >= PLAN_BIG;
+  {
+    // big sets compacted in stream order; small sets' item prefix in stream order
+    const unsigned bb = __ballot_sync(PCY_FULL, bigf);
+    int sv = (isfirst && !bigf) ? ssz : 0, sinc = sv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(PCY_FULL, sinc, o);
+      if (lane >= o) sinc += t;
+    }
+    __shared__ int wbig[32], wsml[32];
+    if (lane == 31) wsml[wid] = sinc;
+    if (lane == 0) wbig[wid] = __popc(bb);
+    __syncthreads();
+    if (wid == 0) {
+      const int vb = wbig[lane], vs = wsml[lane];
+      int ib = vb, is = vs;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int tb = __shfl_up_sync(PCY_FULL, ib, o), ts2 = __shfl_up_sync(PCY_FULL, is, o);
+        if (lane >= o) { ib += tb; is += ts2; }
+      }
+      wbig[lane] = ib - vb; wsml[lane] = is - vs;
+      if (lane == 31) s_nbig = ib;
+    }
+    __syncthreads();
+    if (bigf) { const int kk = wbig[wid] + __popc(bb & ((1u << lane) - 1u)); s_bsz[kk] = ssz; s_broot[kk] = root; }
+    sinc = wsml[wid] + sinc - sv;   // exclusive prefix of small-set items before this item
+    __syncthreads();
+    const int nbig = s_nbig;
+    if (tid < nbig) {
+      const int mysz = s_bsz[tid];
+      int rk = 0;
+      for (int kk = 0; kk < nbig; ++kk) { const int o = s_bsz[kk]; rk += (o > mysz) || (o == mysz && kk < tid); }
+      const int pos = rk % (2 * PCY_PAR_MAXCTA);
+      const int cc = pos < PCY_PAR_MAXCTA ? pos : 2 * PCY_PAR_MAXCTA - 1 - pos;
+      scta[s_broot[tid]] = cc;
+      atomicAdd(&s_load[cc], mysz);
+    }
+    __syncthreads();
+    if (wid == 0) {
+      int bigsum = 0;
+      for (int q = lane; q < PCY_PAR_MAXCTA; q += 32) bigsum += s_load[q];
+      bigsum = __reduce_add_sync(PCY_FULL, bigsum);
+      const int small = c0 - bigsum;
+      int lo = 0, hi = PCY_PAR_MAXITEMS + 1;   // least level whose free room holds the small sets
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        int f = 0;
+        for (int q = lane; q < PCY_PAR_MAXCTA; q += 32) f += max(0, mid - s_load[q]);
+        f = __reduce_add_sync(PCY_FULL, f);
+        if (f >= small) hi = mid; else lo = mid + 1;
+      }
+      int carry = 0;
+      for (int base = 0; base < PCY_PAR_MAXCTA; base += 32) {
+        const int q = base + lane;
+        const int v = q < PCY_PAR_MAXCTA ? max(0, lo - s_load[q]) : 0;
+        int inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(PCY_FULL, inc, o);
+          if (lane >= o) inc += t;
+        }
+        if (q < PCY_PAR_MAXCTA) s_cap[q] = carry + inc - v;
+        carry += __shfl_sync(PCY_FULL, inc, 31);
+      }
+      if (lane == 0) s_cap[PCY_PAR_MAXCTA] = carry;
+    }
+    __syncthreads();
+    if (isfirst && !bigf) {
+      int lo = 0, hi = PCY_PAR_MAXCTA - 1;   // last CTA whose room starts at or before this set
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_cap[mid] <= sinc) lo = mid; else hi = mid - 1;
+      }
+      scta[root] = lo;
+    }
+    __syncthreads();
+  }
+  const int cta = act ? scta[root] : -1 - lane;
   // rank of each item within its CTA (stream order): per-warp chunk counts
   const unsigned grp = __match_any_sync(PCY_FULL, cta);
   const int rin = __popc(grp & ((1u << lane) - 1u));
@@ -1229,7 +1338,14 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
     }
     if (lane == 31) wsum[wid] = cinc;
     if (cv > 0) atomicMax(&s_P, tid + 1);
+#ifdef PCY_TRACE
+    if (tid == 0) par->dbg_maxcta = 0;
+#endif
   }
+#ifdef PCY_TRACE
+  __syncthreads();
+  if (tid < PCY_PAR_MAXCTA) atomicMax(&par->dbg_maxcta, cv);
+#endif
   __syncthreads();
   if (tid < SCAN_T) {
     int base = 0;
