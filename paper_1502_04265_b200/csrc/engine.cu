@@ -20,6 +20,7 @@
 #include <cstddef>
 #include <cstdlib>
 #include <vector>
+#include <algorithm>
 #include "engine.cuh"
 
 static thread_local char g_err[512];
@@ -1326,13 +1327,13 @@ struct Engine {
   cudaEvent_t done_ev = nullptr;
   bool done_rec = false;
   EngCtl* ctl_map_d = nullptr;   // device view of the mirror
-  long long seq = 0, plan_seq = 0;
+  long long seq = 0, plan_seq = 0, tl_early = 0;
   long long* aggw = nullptr;
   double* mp_nrm = nullptr;
   cudaEvent_t ev[8] = {};
-  // K3 (the critical path of an engine) runs on a highest-priority stream so
-  // that, with several engines on one GPU, it is scheduled ahead of the other
-  // engines' contraction CTAs; events order it after K1 and before the next block.
+  // Side stream (highest priority) for the batch Gram of k_plan's conflict
+  // test: it depends only on the batch rows and runs beside the chain walk;
+  // evk1 (rows / previous window done) and evk3 (Gram done) order it.
   cudaStream_t hi = nullptr;
   cudaEvent_t evk1 = nullptr, evk3 = nullptr;
   bool gemm_timed = false;           // ev[6..7] bracket the last full-set contraction
@@ -1383,6 +1384,33 @@ struct Engine {
   }
   void touch(cudaStream_t st) { if (cudaEventRecord(done_ev, st) == cudaSuccess) done_rec = true; }
   ~Engine() {
+#ifdef PCY_TIMELINE
+    {   // build-time diagnostics: mean phase durations / gaps of the insertion windows (us)
+      cudaDeviceSynchronize();
+      unsigned int cnt = 0;
+      cudaMemcpyFromSymbol(&cnt, g_tl_n, sizeof(cnt));
+      if (cnt > PCY_TL_CAP) cnt = PCY_TL_CAP;
+      std::vector<unsigned long long> h(cnt);
+      if (cnt) cudaMemcpyFromSymbol(h.data(), g_tl, sizeof(unsigned long long) * cnt);
+      const unsigned int zero = 0;
+      cudaMemcpyToSymbol(g_tl_n, &zero, sizeof(zero));
+      std::sort(h.begin(), h.end());
+      double sum[8] = {}; long long num[8] = {};
+      // transitions: 1->2 chain (+hop), 2->3 plan, 3->4 plan->resolve gap, 4->5 resolve, 5->1 resolve end -> next chain
+      for (size_t i = 1; i < h.size(); ++i) {
+        const int a = (int)(h[i - 1] & 15), b = (int)(h[i] & 15);
+        const double dt = (double)((h[i] >> 4) - (h[i - 1] >> 4)) * 1e-3;
+        int k = -1;
+        if (a == 1 && b == 2) k = 0; else if (a == 2 && b == 3) k = 1; else if (a == 3 && b == 4) k = 2;
+        else if (a == 4 && b == 5) k = 3; else if (a == 5 && b == 1) k = 4;
+        if (k >= 0 && dt < 5000.0) { sum[k] += dt; ++num[k]; }
+      }
+      const char* nm[5] = {"chain start->plan start", "plan", "plan end->resolve start", "resolve", "resolve end->next chain start"};
+      fprintf(stderr, "[timeline] %u stamps, %lld run-ahead K1 launches", cnt, tl_early);
+      for (int k = 0; k < 5; ++k) fprintf(stderr, " | %s: n %lld mean %.2f us total %.2f ms", nm[k], num[k], num[k] ? sum[k] / num[k] : 0.0, sum[k] * 1e-3);
+      fprintf(stderr, "\n");
+    }
+#endif
     if (ctl_h) {
       g_counters[0] += ctl_h->cnt_levels; g_counters[1] += ctl_h->cnt_direct; g_counters[2] += ctl_h->cnt_demand;
       g_counters[3] += ctl_h->cnt_slow; g_counters[4] += ctl_h->cnt_items;
@@ -1863,6 +1891,7 @@ struct Engine {
         PCY_CUDA(cudaEventRecord(evk1, st)); PCY_CUDA(cudaStreamWaitEvent(hi, evk1, 0));
         const int grc = pcy_launch_gram_split(Xs, nullptr, ld, (int)kn, d, gram, kn, gram_part, gram_split, hi);
         if (grc) return grc;
+        PCY_CUDA(cudaEventRecord(evk3, hi));   // k_plan waits for it
       }
       if (nper) {
         int grc;
@@ -1903,8 +1932,11 @@ struct Engine {
         const int* Bs = BAD ? BAD + off + start : nullptr;
         if (k1_kn == 0) { const int rc1 = enqueue_k1(off + start, kn, prof); if (rc1) return rc1; }
         k1_kn = 0;
+        // K1, k_plan and the resolve kernel share the caller's stream (no
+        // cross-stream hop on the window's critical path); only the batch Gram
+        // runs beside the chain walk on the side stream
         cudaStream_t rs = st;
-        if (hi) { PCY_CUDA(cudaEventRecord(evk1, st)); PCY_CUDA(cudaStreamWaitEvent(hi, evk1, 0)); rs = hi; }
+        if (gram_early) PCY_CUDA(cudaStreamWaitEvent(st, evk3, 0));
         if (prof) PCY_CUDA(cudaEventRecord(ev[1], rs));
         ParCtl* pp = nullptr;
         bool selfp = false; long long pseq = 0, planseq = 0;
@@ -1947,8 +1979,6 @@ struct Engine {
         }
         if (prof) PCY_CUDA(cudaEventRecord(ev[2], rs));
         PCY_LAUNCH_CHECK();
-        // the next K1 (on st) starts when this window's resolve has finished
-        if (hi) { PCY_CUDA(cudaEventRecord(evk3, hi)); PCY_CUDA(cudaStreamWaitEvent(st, evk3, 0)); }
         // Run-ahead: k_plan publishes the window it chose before the resolve
         // kernel runs.  A parallel window of n_win items ends at start + n_win
         // whatever the resolve does (its only other outcomes are fatal), so the
@@ -1968,6 +1998,9 @@ struct Engine {
             if (nwin > 0 && nstart < nb) {
               nkn = nb - nstart > nkb ? nkb : nb - nstart;
               rcp = enqueue_k1(off + nstart, nkn, false); if (rcp) return rcp;
+#ifdef PCY_TIMELINE
+              ++tl_early;
+#endif
             }
           }
         }

@@ -118,20 +118,43 @@ struct EngDev {
   unsigned long long* minbits;
 };
 
-// One thread copies the device counters to the mapped host mirror and then
-// writes the sequence number the host spins on (same protocol as k_publish).
-// Counters other CTAs updated with atomics are read at L2 (volatile).
-__device__ __forceinline__ void ctl_publish_thread(const EngDev& E, EngCtl* dst, long long seq) {
+// One warp copies the device counters to the mapped host mirror (a word per
+// lane: one L2 round trip, not one per word) and then writes the sequence
+// number the host spins on (same protocol as k_publish).  Counters other CTAs
+// updated with atomics are read at L2 (volatile).  Call with the whole warp.
+__device__ __forceinline__ void ctl_publish_warp(const EngDev& E, EngCtl* dst, long long seq, int lane) {
   EngCtl* src = E.ctl;
-  src->root_count = *(volatile const int*)&E.g_count[0];
-  src->root_base = *(volatile const int*)&E.g_base[0];
+  if (lane == 0) {
+    src->root_count = *(volatile const int*)&E.g_count[0];
+    src->root_base = *(volatile const int*)&E.g_base[0];
+  }
+  __syncwarp();
   const int words = (int)(offsetof(EngCtl, seq) / sizeof(long long));
   volatile const long long* s = reinterpret_cast<volatile const long long*>(src);
   volatile long long* t = reinterpret_cast<volatile long long*>(dst);
-  for (int k = 0; k < words; ++k) t[k] = s[k];
+  for (int k = lane; k < words; k += 32) t[k] = s[k];
   __threadfence_system();
-  t[words] = seq;
+  __syncwarp();
+  if (lane == 0) t[words] = seq;
 }
+
+// Build-time timeline (PCY_NVCC_EXTRA=-DPCY_TIMELINE): kernels stamp the
+// global timer at entry / exit; the engine prints the mean phase durations and
+// gaps of the insertion windows when it is destroyed.
+#ifdef PCY_TIMELINE
+#define PCY_TL_CAP (1 << 18)
+__device__ unsigned long long g_tl[PCY_TL_CAP];
+__device__ unsigned int g_tl_n;
+__device__ __forceinline__ void tl_stamp(int tag) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  const unsigned i = atomicAdd(&g_tl_n, 1u);
+  if (i < PCY_TL_CAP) g_tl[i] = (t << 4) | (unsigned long long)tag;
+}
+#define PCY_TL(tag) tl_stamp(tag)
+#else
+#define PCY_TL(tag) ((void)0)
+#endif
 
 // cp.async helpers (global -> shared without registers)
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {

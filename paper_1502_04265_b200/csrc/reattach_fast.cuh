@@ -483,6 +483,7 @@ __device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __res
   } else status = ST_ARENA;
   __syncwarp();
   if constexpr (PAR) {
+    int lastf = 0;   // this CTA finished the window: its warp publishes
     if (lane == 0) {
       using ull = unsigned long long;
       if (status != ST_DONE) { atomicExch(&par->arena_fail, status == ST_ARENA ? ST_ARENA : ST_PAR_BROKEN); par->pad = status; }
@@ -498,9 +499,11 @@ __device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __res
         C->status = fail ? fail : (par->n_win < par->n_total ? ST_FULL : ST_DONE);
         C->stop = par->n_win;
         __threadfence();
-        if (pub) ctl_publish_thread(E, pub, pseq);
+        lastf = 1;
       }
     }
+    lastf = __shfl_sync(PCY_FULL, lastf, 0);
+    if (lastf && pub) ctl_publish_warp(E, pub, pseq, lane);
     return;
   }
   if (par && status == ST_DONE && n < par->n_total) { status = ST_FULL; stop = n; }   // k_plan's sequential stretch
@@ -508,8 +511,9 @@ __device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __res
     C->F = F; C->free_n = freen; C->G_alloc = Galloc; C->A_alloc = Aalloc;
     C->status = status; C->stop = stop;
     __threadfence();
-    if (pub) ctl_publish_thread(E, pub, pseq);
   }
+  __syncwarp();
+  if (pub) ctl_publish_warp(E, pub, pseq, lane);
 }
 
 template <int NPER, bool PAR = false>

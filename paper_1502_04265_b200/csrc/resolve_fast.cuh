@@ -67,6 +67,7 @@ __global__ void k_chain2(EngDev E, const double* __restrict__ X, const double* _
   // dots are split over the warps (cta_dot), for large d.
   extern __shared__ double sm_x[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  if (blockIdx.x == 0 && threadIdx.x == 0) PCY_TL(1);
   const long long i = WPI == 1 ? (long long)blockIdx.x * (blockDim.x >> 5) + wib : (long long)blockIdx.x;
   if (i >= n) return;
   const int d = E.d, ld = E.ld;
@@ -779,6 +780,7 @@ __device__ __forceinline__ void resolve2_body(const EngDev& E, const double* __r
   __syncwarp();
   if constexpr (PAR) {
     // deltas of this subtree, then the last CTA publishes the window
+    int lastf = 0;   // this CTA finished the window: its warp publishes
     if (lane == 0) {
       using ull = unsigned long long;
       if (status != ST_DONE) { atomicExch(&par->arena_fail, status == ST_ARENA ? ST_ARENA : ST_PAR_BROKEN); par->pad = status; }
@@ -804,9 +806,12 @@ __device__ __forceinline__ void resolve2_body(const EngDev& E, const double* __r
         C->status = fail ? fail : (par->n_win < par->n_total ? ST_FULL : ST_DONE);
         C->err = fail ? par->pad : 0; C->stop = par->n_win; C->remaining = 0;
         __threadfence();
-        if (pub) ctl_publish_thread(E, pub, pseq);
+        PCY_TL(5);
+        lastf = 1;
       }
     }
+    lastf = __shfl_sync(PCY_FULL, lastf, 0);
+    if (lastf && pub) ctl_publish_warp(E, pub, pseq, lane);
     return;
   }
   if (par && status == ST_DONE && n < par->n_total) { status = ST_FULL; stop = n; }   // k_plan's sequential stretch
@@ -817,8 +822,10 @@ __device__ __forceinline__ void resolve2_body(const EngDev& E, const double* __r
     C->cnt_levels += c_lv; C->cnt_direct += c_dir; C->cnt_demand += c_dem; C->cnt_slow += c_slow;
     C->cnt_items += c_it; C->cnt_dem_fast += c_demf; C->cnt_touch_child += c_tch;
     __threadfence();
-    if (pub) ctl_publish_thread(E, pub, pseq);
+    if (pub) PCY_TL(5);
   }
+  __syncwarp();
+  if (pub) ctl_publish_warp(E, pub, pseq, lane);
 }
 
 template <int NPER, bool PAR = false>
@@ -839,6 +846,7 @@ __global__ void __launch_bounds__(64, 1) k_resolve2x(EngDev E, const double* __r
                                                      int countw, int nnew_cap, const ChainHdr* __restrict__ H,
                                                      const ChainLvl* __restrict__ R, ParCtl* __restrict__ par,
                                                      EngCtl* pub, long long pseq) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) PCY_TL(4);
   if (par->mode == 0) resolve2_body<NPER, true>(E, X, XS, W, BAD, n, first_rem, countw, nnew_cap, H, R, par, pub, pseq);
   else if (blockIdx.x == 0) resolve2_body<NPER, false>(E, X, XS, W, BAD, n, first_rem, countw, nnew_cap, H, R, par, pub, pseq);
 }
@@ -943,6 +951,7 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
   __shared__ int wsum[32];
   __shared__ int s_c, s_last, s_heavy, s_cut, s_P;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0 && !order) PCY_TL(2);
   const EngCtl* C = E.ctl;
   const long long F0 = C->F;
   const int NC = (int)E.NC;
@@ -1139,6 +1148,7 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
       if (first_rem < 0 && room >= theta && c0 < nn) ns = (s_last > c0 ? s_last : c0) + 1;
       if (ns > n) ns = n;
       par->n_win = ns;
+      if (!order) PCY_TL(3);
       if (pub) {   // early publication: the host may enqueue the next K1 batch now
         volatile long long* t = &pub->plan_mode;
         t[0] = 1; t[1] = ns;
@@ -1362,6 +1372,7 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
     par->Aalloc0 = C->A_alloc; par->nidx0 = C->next_index;
     par->open_ticket = 0; par->g_ticket = 0; par->a_ticket = 0; par->done = 0; par->opens = 0;
     par->arena_fail = 0;
+    if (!order) PCY_TL(3);
     if (pub) {   // early publication: the host may enqueue the next K1 batch now
       volatile long long* t = &pub->plan_mode;
       t[0] = 0; t[1] = c;

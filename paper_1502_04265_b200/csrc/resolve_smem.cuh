@@ -647,6 +647,7 @@ __device__ __forceinline__ void resolve3_body(const EngDev& E, const double* __r
   __syncwarp();
   if (!table_cleanup<MS>(E, S, nnew, Aalloc, lane, PAR ? par : nullptr)) status = ST_ARENA;
   if constexpr (PAR) {
+    int lastf = 0;   // this CTA finished the window: its warp publishes
     if (lane == 0) {
       using ull = unsigned long long;
       if (status != ST_DONE) { atomicExch(&par->arena_fail, status == ST_ARENA ? ST_ARENA : ST_PAR_BROKEN); par->pad = status; }
@@ -671,9 +672,11 @@ __device__ __forceinline__ void resolve3_body(const EngDev& E, const double* __r
         C->status = fail ? fail : (par->n_win < par->n_total ? ST_FULL : ST_DONE);
         C->err = fail ? par->pad : 0; C->stop = par->n_win; C->remaining = 0;
         __threadfence();
-        if (pub) ctl_publish_thread(E, pub, pseq);
+        lastf = 1;
       }
     }
+    lastf = __shfl_sync(PCY_FULL, lastf, 0);
+    if (lastf && pub) ctl_publish_warp(E, pub, pseq, lane);
     return;
   }
   if (par && status == ST_DONE && n < par->n_total) { status = ST_FULL; stop = n; }   // k_plan's sequential stretch
@@ -684,8 +687,9 @@ __device__ __forceinline__ void resolve3_body(const EngDev& E, const double* __r
     C->cnt_levels += c_lv; C->cnt_direct += c_dir; C->cnt_demand += c_dem; C->cnt_slow += c_slow;
     C->cnt_items += c_it;
     __threadfence();
-    if (pub) ctl_publish_thread(E, pub, pseq);
   }
+  __syncwarp();
+  if (pub) ctl_publish_warp(E, pub, pseq, lane);
 }
 
 template <bool TROWS, int MS, bool PAR = false>
@@ -968,6 +972,7 @@ __device__ __forceinline__ void reattach3_body(const EngDev& E, const int* __res
   __syncwarp();
   if (!table_cleanup<MS>(E, S, nnew, Aalloc, lane, PAR ? par : nullptr)) status = ST_ARENA;
   if constexpr (PAR) {
+    int lastf = 0;   // this CTA finished the window: its warp publishes
     if (lane == 0) {
       using ull = unsigned long long;
       if (status != ST_DONE) { atomicExch(&par->arena_fail, status == ST_ARENA ? ST_ARENA : ST_PAR_BROKEN); par->pad = status; }
@@ -983,9 +988,11 @@ __device__ __forceinline__ void reattach3_body(const EngDev& E, const int* __res
         C->status = fail ? fail : (par->n_win < par->n_total ? ST_FULL : ST_DONE);
         C->stop = par->n_win;
         __threadfence();
-        if (pub) ctl_publish_thread(E, pub, pseq);
+        lastf = 1;
       }
     }
+    lastf = __shfl_sync(PCY_FULL, lastf, 0);
+    if (lastf && pub) ctl_publish_warp(E, pub, pseq, lane);
     return;
   }
   if (par && status == ST_DONE && n < par->n_total) { status = ST_FULL; stop = n; }   // k_plan's sequential stretch
@@ -993,8 +1000,9 @@ __device__ __forceinline__ void reattach3_body(const EngDev& E, const int* __res
     C->F = F; C->free_n = freen; C->G_alloc = Galloc; C->A_alloc = Aalloc;
     C->status = status; C->stop = stop;
     __threadfence();
-    if (pub) ctl_publish_thread(E, pub, pseq);
   }
+  __syncwarp();
+  if (pub) ctl_publish_warp(E, pub, pseq, lane);
 }
 
 template <bool TROWS, int MS, bool PAR = false>
