@@ -1314,6 +1314,20 @@ static void ctl_pool_put(EngCtl* c) {
   g_ctl_pool.push_back(c);
 }
 
+// Launch with the programmatic-serialization attribute: the kernel may be
+// scheduled before its predecessor in the stream has finished and orders
+// itself with pdl_wait() (engine.cuh).
+template <class... KArgs, class... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid; cfg.blockDim = block; cfg.dynamicSmemBytes = smem; cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at; cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, KArgs(args)...);
+}
+
 struct Engine {
   int dev = 0, d = 0, ld = 0;
   long long m = 0, sample_cap = 0, NC = 0, GC = 0, AC = 0, Bmax = 0;
@@ -1342,6 +1356,8 @@ struct Engine {
   ChainLvl* chr = nullptr;
   double* parts = nullptr;                             // full-set parts matrix (1024 x NC)
   double* gram = nullptr;                              // block Gram (K3 with rows in HBM)
+  double* gram_b = nullptr;                            // second Gram buffer: run-ahead batches alternate
+  int gram_flip = 0;
   double* gram_part = nullptr;                         // split-K partials of the block Gram (large d)
   int gram_split = 1;
   bool use_tc = false;                                 // full-set K1 on tcgen05 (split TF32 + recheck)
@@ -1506,6 +1522,7 @@ struct Engine {
     A_(E.ch_node, Bmax * PCY_MAXL); A_(E.ch_part, Bmax * PCY_MAXL); A_(E.ch_len, Bmax);
     A_(chh, Bmax); A_(chr, Bmax * PCY_FMAXL);
     A_(gram, (long long)1024 * 1024);
+    A_(gram_b, (long long)1024 * 1024);
     gram_split = d >= 2048 ? 8 : d >= 512 ? 4 : 1;   // K slices of >= 128-512 elements
     if (gram_split > 1) A_(gram_part, (long long)gram_split * 1024 * 1024);
     E.pend_cap = m + 2;
@@ -1881,15 +1898,24 @@ struct Engine {
     // (it depends only on the rows: on the K3 stream, beside the chain walk),
     // the panel contraction and the chain walk.  Nothing here needs the host
     // to know the tree (the panel size is the last publication's).
-    auto enqueue_k1 = [&](long long s0, long long kn, bool prof) -> int {
+    // The batch Grams alternate between two buffers: with `ahead` (run-ahead
+    // batch) the side stream waits only for the event recorded before the
+    // current window's k_plan -- the buffer's last reader is the k_plan before
+    // that one -- so nothing sits between the resolve kernel and this chain
+    // walk in the stream and the walk is launched programmatically.
+    double* gram_k1 = gram;   // the buffer of the batch enqueued last
+    auto enqueue_k1 = [&](long long s0, long long kn, bool prof, bool ahead) -> int {
       const double* Xs = X + s0 * ld;
       const double* XSs = XS + s0;
       const long long* Ws = W ? W + s0 : nullptr;
       if (!nper) { k_snapshot<<<64, 256, 0, st>>>(E); pcy_count_launch(); }
       if (prof) PCY_CUDA(cudaEventRecord(ev[0], st));
       if (gram_early) {
-        PCY_CUDA(cudaEventRecord(evk1, st)); PCY_CUDA(cudaStreamWaitEvent(hi, evk1, 0));
-        const int grc = pcy_launch_gram_split(Xs, nullptr, ld, (int)kn, d, gram, kn, gram_part, gram_split, hi);
+        gram_flip ^= 1;
+        gram_k1 = gram_flip ? gram_b : gram;
+        if (!ahead) PCY_CUDA(cudaEventRecord(evk1, st));
+        PCY_CUDA(cudaStreamWaitEvent(hi, evk1, 0));
+        const int grc = pcy_launch_gram_split(Xs, nullptr, ld, (int)kn, d, gram_k1, kn, gram_part, gram_split, hi);
         if (grc) return grc;
         PCY_CUDA(cudaEventRecord(evk3, hi));   // k_plan waits for it
       }
@@ -1900,6 +1926,9 @@ struct Engine {
         if (ld > 512)   // one item per CTA, dots split over 4 warps
           k_chain2<4><<<(unsigned)(kn), 128, sizeof(double) * (ld + 8) + sizeof(int) * (TC_CAND_MAX + 4), st>>>(
               E, Xs, XSs, Ws, kn, chh, chr, use_p ? parts : nullptr, ctl_h->F_alloc);
+        else if (ahead)
+          PCY_CUDA(launch_pdl(k_chain2<1>, dim3((unsigned)((kn + wpc - 1) / wpc)), dim3(wpc * 32), sizeof(double) * wpc * ld, st,
+                              E, Xs, XSs, Ws, kn, chh, chr, (const double*)(use_p ? parts : nullptr), (long long)ctl_h->F_alloc));
         else
           k_chain2<1><<<(unsigned)((kn + wpc - 1) / wpc), wpc * 32, sizeof(double) * wpc * ld, st>>>(
               E, Xs, XSs, Ws, kn, chh, chr, use_p ? parts : nullptr, ctl_h->F_alloc);
@@ -1930,13 +1959,17 @@ struct Engine {
         const bool prof = pcy_prof_enabled();
         const long long* Ws = W ? W + off + start : nullptr;
         const int* Bs = BAD ? BAD + off + start : nullptr;
-        if (k1_kn == 0) { const int rc1 = enqueue_k1(off + start, kn, prof); if (rc1) return rc1; }
+        if (k1_kn == 0) { const int rc1 = enqueue_k1(off + start, kn, prof, false); if (rc1) return rc1; }
         k1_kn = 0;
+        double* const gram_w = gram_early ? gram_k1 : gram;   // this window's batch Gram
         // K1, k_plan and the resolve kernel share the caller's stream (no
         // cross-stream hop on the window's critical path); only the batch Gram
         // runs beside the chain walk on the side stream
         cudaStream_t rs = st;
-        if (gram_early) PCY_CUDA(cudaStreamWaitEvent(st, evk3, 0));
+        if (gram_early) {
+          PCY_CUDA(cudaStreamWaitEvent(st, evk3, 0));
+          PCY_CUDA(cudaEventRecord(evk1, st));   // a run-ahead batch's Gram may start from here (other buffer)
+        }
         if (prof) PCY_CUDA(cudaEventRecord(ev[1], rs));
         ParCtl* pp = nullptr;
         bool selfp = false; long long pseq = 0, planseq = 0;
@@ -1948,7 +1981,7 @@ struct Engine {
           }
           planseq = ++plan_seq;
           k_plan<<<1, PCY_PAR_MAXITEMS, plan_smem, rs>>>(E, XSs, Ws, Bs, kn, first_rem, nnew_cap, 16, chh, chr, parctl,
-                                                 (int)(NC / 32 + 1), nullptr, gram, kn, ctl_map_d, planseq);
+                                                 (int)(NC / 32 + 1), nullptr, gram_w, kn, ctl_map_d, planseq);
           pcy_count_launch();
           pp = parctl;
           // one launch serves either choice of k_plan and, while no group is
@@ -1957,10 +1990,10 @@ struct Engine {
           pseq = selfp ? ++seq : 0;
           EngCtl* pb = selfp ? ctl_map_d : nullptr;
           switch (nper) {
-            case 1: k_resolve2x<1><<<PCY_PAR_MAXCTA, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, pp, pb, pseq); break;
-            case 2: k_resolve2x<2><<<PCY_PAR_MAXCTA, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, pp, pb, pseq); break;
-            case 4: k_resolve2x<4><<<PCY_PAR_MAXCTA, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, pp, pb, pseq); break;
-            case 8: k_resolve2x<8><<<PCY_PAR_MAXCTA, 64, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, pp, pb, pseq); break;
+            case 1: PCY_CUDA(launch_pdl(k_resolve2x<1>, dim3(PCY_PAR_MAXCTA), dim3(64), res_smem, rs, E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, (const ChainHdr*)chh, (const ChainLvl*)chr, pp, pb, pseq)); break;
+            case 2: PCY_CUDA(launch_pdl(k_resolve2x<2>, dim3(PCY_PAR_MAXCTA), dim3(64), res_smem, rs, E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, (const ChainHdr*)chh, (const ChainLvl*)chr, pp, pb, pseq)); break;
+            case 4: PCY_CUDA(launch_pdl(k_resolve2x<4>, dim3(PCY_PAR_MAXCTA), dim3(64), res_smem, rs, E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, (const ChainHdr*)chh, (const ChainLvl*)chr, pp, pb, pseq)); break;
+            case 8: PCY_CUDA(launch_pdl(k_resolve2x<8>, dim3(PCY_PAR_MAXCTA), dim3(64), res_smem, rs, E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, (const ChainHdr*)chh, (const ChainLvl*)chr, pp, pb, pseq)); break;
             case 100: k_resolve3x<true, 2048><<<PCY_PAR_MAXCTA, 32, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, nullptr, 0, 0, pp, pb, pseq); break;
             case 101: k_resolve3x<false, 512><<<PCY_PAR_MAXCTA, 32, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, gram, kn, 0, pp, pb, pseq); break;
           }
@@ -1997,7 +2030,7 @@ struct Engine {
             nstart = start + nwin;
             if (nwin > 0 && nstart < nb) {
               nkn = nb - nstart > nkb ? nkb : nb - nstart;
-              rcp = enqueue_k1(off + nstart, nkn, false); if (rcp) return rcp;
+              rcp = enqueue_k1(off + nstart, nkn, false, true); if (rcp) return rcp;
 #ifdef PCY_TIMELINE
               ++tl_early;
 #endif

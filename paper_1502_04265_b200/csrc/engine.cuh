@@ -156,6 +156,14 @@ __device__ __forceinline__ void tl_stamp(int tag) {
 #define PCY_TL(tag) ((void)0)
 #endif
 
+// Programmatic dependent launch (sm_90+): a kernel launched with the
+// programmatic-serialization attribute may be scheduled while its predecessor
+// in the stream still runs; pdl_wait() blocks until the predecessor has
+// completed and its writes are visible (a no-op for ordinary launches), and
+// pdl_launch_dependents() lets the successor's CTAs be scheduled early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // cp.async helpers (global -> shared without registers)
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);

@@ -531,6 +531,7 @@ __global__ void __launch_bounds__(32, 1) k_reattach2x(EngDev E, const int* __res
                                                       const ChainLvl* __restrict__ R, ParCtl* __restrict__ par,
                                                       const double* __restrict__ gram, long long gld,
                                                       EngCtl* pub, long long pseq, int ts_cap) {
+  pdl_wait();   // k_plan has finished (programmatic launch)
   if (par->mode == 0) reattach2_body<NPER, true>(E, order, n, nnew_cap, H, R, par, gram, gld, pub, pseq, ts_cap);
   else if (blockIdx.x == 0) reattach2_body<NPER, false>(E, order, n, nnew_cap, H, R, par, gram, gld, pub, pseq, ts_cap);
 }

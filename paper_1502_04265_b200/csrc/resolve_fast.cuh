@@ -67,6 +67,7 @@ __global__ void k_chain2(EngDev E, const double* __restrict__ X, const double* _
   // dots are split over the warps (cta_dot), for large d.
   extern __shared__ double sm_x[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  pdl_wait();   // run-ahead launch: the previous window's resolve kernel has finished
   if (blockIdx.x == 0 && threadIdx.x == 0) PCY_TL(1);
   const long long i = WPI == 1 ? (long long)blockIdx.x * (blockDim.x >> 5) + wib : (long long)blockIdx.x;
   if (i >= n) return;
@@ -846,6 +847,8 @@ __global__ void __launch_bounds__(64, 1) k_resolve2x(EngDev E, const double* __r
                                                      int countw, int nnew_cap, const ChainHdr* __restrict__ H,
                                                      const ChainLvl* __restrict__ R, ParCtl* __restrict__ par,
                                                      EngCtl* pub, long long pseq) {
+  pdl_wait();                // k_plan has finished
+  pdl_launch_dependents();   // the next batch's chain walk may be scheduled; it waits for this grid
   if (blockIdx.x == 0 && threadIdx.x == 0) PCY_TL(4);
   if (par->mode == 0) resolve2_body<NPER, true>(E, X, XS, W, BAD, n, first_rem, countw, nnew_cap, H, R, par, pub, pseq);
   else if (blockIdx.x == 0) resolve2_body<NPER, false>(E, X, XS, W, BAD, n, first_rem, countw, nnew_cap, H, R, par, pub, pseq);
@@ -951,6 +954,7 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
   __shared__ int wsum[32];
   __shared__ int s_c, s_last, s_heavy, s_cut, s_P;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  pdl_launch_dependents();   // the resolve kernel's CTAs may be scheduled; they wait for this grid
   if (tid == 0 && !order) PCY_TL(2);
   const EngCtl* C = E.ctl;
   const long long F0 = C->F;

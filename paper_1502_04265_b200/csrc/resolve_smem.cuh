@@ -711,6 +711,7 @@ __global__ void __launch_bounds__(32, 1) k_resolve3x(EngDev E, const double* __r
                                                      const ChainLvl* __restrict__ R, const double* __restrict__ gram,
                                                      long long gld, long long goff, ParCtl* __restrict__ par,
                                                      EngCtl* pub, long long pseq) {
+  pdl_wait();   // k_plan has finished (programmatic launch)
   if (par->mode == 0)
     resolve3_body<TROWS, MS, true>(E, X, XS, W, BAD, n, first_rem, countw, nnew_cap, H, R, gram, gld, goff, par, pub, pseq);
   else if (blockIdx.x == 0)
@@ -1020,6 +1021,7 @@ __global__ void __launch_bounds__(32, 1) k_reattach3x(EngDev E, const int* __res
                                                       const ChainLvl* __restrict__ R, const double* __restrict__ gram,
                                                       long long gld, long long goff, ParCtl* __restrict__ par,
                                                       EngCtl* pub, long long pseq) {
+  pdl_wait();   // k_plan has finished (programmatic launch)
   if (par->mode == 0) reattach3_body<TROWS, MS, true>(E, order, n, nnew_cap, H, R, gram, gld, goff, par, pub, pseq);
   else if (blockIdx.x == 0) reattach3_body<TROWS, MS, false>(E, order, n, nnew_cap, H, R, gram, gld, goff, par, pub, pseq);
 }
