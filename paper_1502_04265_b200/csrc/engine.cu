@@ -1421,6 +1421,26 @@ struct Engine {
         else if (a == 4 && b == 5) k = 3; else if (a == 5 && b == 1) k = 4;
         if (k >= 0 && dt < 5000.0) { sum[k] += dt; ++num[k]; }
       }
+      {
+        unsigned int cc = 0;
+        cudaMemcpyFromSymbol(&cc, g_tlc_n, sizeof(cc));
+        if (cc > PCY_TL_CAP) cc = PCY_TL_CAP;
+        std::vector<unsigned long long> hc(cc);
+        if (cc) cudaMemcpyFromSymbol(hc.data(), g_tlc, sizeof(unsigned long long) * cc);
+        cudaMemcpyToSymbol(g_tlc_n, &zero, sizeof(zero));
+        // cycles by item-count bucket, and the slowest CTAs
+        double cs[8] = {}, it[8] = {}, sl[8] = {}, nn[8] = {}; long long cn[8] = {};
+        for (auto v : hc) {
+          const long long items = v & 0xffff, nnew = (v >> 16) & 0xfff, slow = (v >> 28) & 0xfff, cyc = v >> 40;
+          int b = items <= 2 ? 0 : items <= 4 ? 1 : items <= 8 ? 2 : items <= 12 ? 3 : items <= 16 ? 4 : items <= 24 ? 5 : items <= 48 ? 6 : 7;
+          cs[b] += (double)cyc; it[b] += (double)items; sl[b] += (double)slow; nn[b] += (double)nnew; ++cn[b];
+        }
+        const char* bn[8] = {"<=2", "<=4", "<=8", "<=12", "<=16", "<=24", "<=48", ">48"};
+        fprintf(stderr, "[timeline-cta] %u resolve CTAs:", cc);
+        for (int b = 0; b < 8; ++b)
+          if (cn[b]) fprintf(stderr, " | items %s: n %lld mean items %.1f new %.1f slow %.1f cycles %.0f", bn[b], cn[b], it[b] / cn[b], nn[b] / cn[b], sl[b] / cn[b], cs[b] / cn[b]);
+        fprintf(stderr, "\n");
+      }
       const char* nm[5] = {"chain start->plan start", "plan", "plan end->resolve start", "resolve", "resolve end->next chain start"};
       fprintf(stderr, "[timeline] %u stamps, %lld run-ahead K1 launches", cnt, tl_early);
       for (int k = 0; k < 5; ++k) fprintf(stderr, " | %s: n %lld mean %.2f us total %.2f ms", nm[k], num[k], num[k] ? sum[k] / num[k] : 0.0, sum[k] * 1e-3);

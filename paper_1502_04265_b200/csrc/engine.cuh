@@ -152,6 +152,15 @@ __device__ __forceinline__ void tl_stamp(int tag) {
   if (i < PCY_TL_CAP) g_tl[i] = (t << 4) | (unsigned long long)tag;
 }
 #define PCY_TL(tag) tl_stamp(tag)
+// per resolve CTA: items, new nodes, slow-path evaluations, cycles
+__device__ unsigned long long g_tlc[PCY_TL_CAP];
+__device__ unsigned int g_tlc_n;
+__device__ __forceinline__ void tl_cta(long long items, int nnew, long long slow, long long cyc) {
+  const unsigned i = atomicAdd(&g_tlc_n, 1u);
+  if (i < PCY_TL_CAP)
+    g_tlc[i] = ((unsigned long long)(cyc & 0xffffff) << 40) | ((unsigned long long)(slow & 0xfff) << 28) |
+               ((unsigned long long)(nnew & 0xfff) << 16) | (unsigned long long)(items & 0xffff);
+}
 #else
 #define PCY_TL(tag) ((void)0)
 #endif

@@ -385,6 +385,9 @@ __device__ __forceinline__ void resolve2_body(const EngDev& E, const double* __r
     return;
   }
 
+#ifdef PCY_TIMELINE
+  const long long tl_t0 = clock64();
+#endif
   EngCtl* C = E.ctl;
   const long long m = E.m;
   const double T = C->T;
@@ -782,6 +785,9 @@ __device__ __forceinline__ void resolve2_body(const EngDev& E, const double* __r
   if constexpr (PAR) {
     // deltas of this subtree, then the last CTA publishes the window
     int lastf = 0;   // this CTA finished the window: its warp publishes
+#ifdef PCY_TIMELINE
+    if (lane == 0) tl_cta(n, nnew, c_slow, clock64() - tl_t0);
+#endif
     if (lane == 0) {
       using ull = unsigned long long;
       if (status != ST_DONE) { atomicExch(&par->arena_fail, status == ST_ARENA ? ST_ARENA : ST_PAR_BROKEN); par->pad = status; }
