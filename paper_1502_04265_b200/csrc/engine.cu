@@ -1440,6 +1440,45 @@ struct Engine {
         for (int b = 0; b < 8; ++b)
           if (cn[b]) fprintf(stderr, " | items %s: n %lld mean items %.1f new %.1f slow %.1f cycles %.0f", bn[b], cn[b], it[b] / cn[b], nn[b] / cn[b], sl[b] / cn[b], cs[b] / cn[b]);
         fprintf(stderr, "\n");
+        unsigned long long ts[8][8];
+        cudaMemcpyFromSymbol(ts, g_tls, sizeof(ts));
+        unsigned long long tz[8][8] = {};
+        cudaMemcpyToSymbol(g_tls, tz, sizeof(tz));
+        fprintf(stderr, "[timeline-split]");
+        for (int b = 0; b < 8; ++b)
+          if (ts[b][0]) fprintf(stderr, " | items %s: wait %.0f slow %.0f start %.0f clean %.0f demand %.0f fast %.0f", bn[b], (double)ts[b][1] / ts[b][0], (double)ts[b][2] / ts[b][0],
+                                (double)ts[b][3] / ts[b][0], (double)ts[b][4] / ts[b][0], (double)ts[b][5] / ts[b][0], (double)ts[b][6] / ts[b][0]);
+        fprintf(stderr, "\n");
+        unsigned long long t2[8][8];
+        cudaMemcpyFromSymbol(t2, g_tls2, sizeof(t2));
+        cudaMemcpyToSymbol(g_tls2, tz, sizeof(tz));
+        fprintf(stderr, "[timeline-split2]");
+        for (int b = 0; b < 8; ++b)
+          if (ts[b][0]) fprintf(stderr, " | items %s: direct-scan %.0f (n %.1f) new-members %.0f (n %.1f) capacity %.0f levels %.1f", bn[b], (double)t2[b][1] / ts[b][0], (double)t2[b][4] / ts[b][0],
+                                (double)t2[b][2] / ts[b][0], (double)t2[b][5] / ts[b][0], (double)t2[b][3] / ts[b][0], (double)t2[b][6] / ts[b][0]);
+        fprintf(stderr, "\n");
+      }
+      {
+        unsigned long long tr[8][8], tz2[8][8] = {};
+        cudaMemcpyFromSymbol(tr, g_tlr, sizeof(tr));
+        cudaMemcpyToSymbol(g_tlr, tz2, sizeof(tz2));
+        const char* rb[8] = {"<=8", "<=16", "<=32", "<=64", "<=128", "<=256", "<=512", ">512"};
+        fprintf(stderr, "[timeline-rea]");
+        for (int b = 0; b < 8; ++b)
+          if (tr[b][0]) fprintf(stderr, " | items %s: n %llu mean items %.1f cycles %.0f stage-wait %.0f adds %.1f levels %.1f scan %.0f", rb[b], tr[b][0], (double)tr[b][2] / tr[b][0],
+                                (double)tr[b][1] / tr[b][0], (double)tr[b][3] / tr[b][0], (double)tr[b][4] / tr[b][0], (double)tr[b][5] / tr[b][0], (double)tr[b][6] / tr[b][0]);
+        fprintf(stderr, "\n");
+        unsigned long long t2[8][12], tz3[8][12] = {};
+        cudaMemcpyFromSymbol(t2, g_tlr2, sizeof(t2));
+        cudaMemcpyToSymbol(g_tlr2, tz3, sizeof(tz3));
+        fprintf(stderr, "[timeline-rea2]");
+        for (int b = 0; b < 8; ++b)
+          if (tr[b][0]) {
+            const double c = (double)tr[b][0];
+            fprintf(stderr, " | items %s: dirscan n %.1f cyc %.0f newscan n %.1f cyc %.0f merge rec %.1f glob %.1f smem %.1f cyc %.0f tail cyc %.0f", rb[b], t2[b][0] / c, t2[b][1] / c,
+                    t2[b][2] / c, t2[b][3] / c, t2[b][4] / c, t2[b][5] / c, t2[b][6] / c, t2[b][7] / c, t2[b][8] / c);
+          }
+        fprintf(stderr, "\n");
       }
       const char* nm[5] = {"chain start->plan start", "plan", "plan end->resolve start", "resolve", "resolve end->next chain start"};
       fprintf(stderr, "[timeline] %u stamps, %lld run-ahead K1 launches", cnt, tl_early);
@@ -1557,6 +1596,7 @@ struct Engine {
     A_(bs.flags, Bmax + 1); A_(bs.spos, Bmax); A_(bs.ppos, Bmax); A_(bs.dpos, Bmax); A_(bs.skey, bs.scap); A_(bs.sfirst, bs.scap);
     A_(parctl, 1);
 #undef A_
+    PCY_CUDA(cudaMemsetAsync(parctl, 0, sizeof(ParCtl), own));   // ParCtl::ready starts below every launch number
     for (auto& e : ev) PCY_CUDA(cudaEventCreate(&e));
     {
       int least = 0, greatest = 0;
@@ -1924,7 +1964,7 @@ struct Engine {
     // that one -- so nothing sits between the resolve kernel and this chain
     // walk in the stream and the walk is launched programmatically.
     double* gram_k1 = gram;   // the buffer of the batch enqueued last
-    auto enqueue_k1 = [&](long long s0, long long kn, bool prof, bool ahead) -> int {
+    auto enqueue_k1 = [&](long long s0, long long kn, bool prof, bool ahead, long long wait_seq) -> int {
       const double* Xs = X + s0 * ld;
       const double* XSs = XS + s0;
       const long long* Ws = W ? W + s0 : nullptr;
@@ -1948,7 +1988,7 @@ struct Engine {
               E, Xs, XSs, Ws, kn, chh, chr, use_p ? parts : nullptr, ctl_h->F_alloc);
         else if (ahead)
           PCY_CUDA(launch_pdl(k_chain2<1>, dim3((unsigned)((kn + wpc - 1) / wpc)), dim3(wpc * 32), sizeof(double) * wpc * ld, st,
-                              E, Xs, XSs, Ws, kn, chh, chr, (const double*)(use_p ? parts : nullptr), (long long)ctl_h->F_alloc));
+                              E, Xs, XSs, Ws, kn, chh, chr, (const double*)(use_p ? parts : nullptr), (long long)ctl_h->F_alloc, wait_seq));
         else
           k_chain2<1><<<(unsigned)((kn + wpc - 1) / wpc), wpc * 32, sizeof(double) * wpc * ld, st>>>(
               E, Xs, XSs, Ws, kn, chh, chr, use_p ? parts : nullptr, ctl_h->F_alloc);
@@ -1979,7 +2019,7 @@ struct Engine {
         const bool prof = pcy_prof_enabled();
         const long long* Ws = W ? W + off + start : nullptr;
         const int* Bs = BAD ? BAD + off + start : nullptr;
-        if (k1_kn == 0) { const int rc1 = enqueue_k1(off + start, kn, prof, false); if (rc1) return rc1; }
+        if (k1_kn == 0) { const int rc1 = enqueue_k1(off + start, kn, prof, false, 0); if (rc1) return rc1; }
         k1_kn = 0;
         double* const gram_w = gram_early ? gram_k1 : gram;   // this window's batch Gram
         // K1, k_plan and the resolve kernel share the caller's stream (no
@@ -2010,10 +2050,10 @@ struct Engine {
           pseq = selfp ? ++seq : 0;
           EngCtl* pb = selfp ? ctl_map_d : nullptr;
           switch (nper) {
-            case 1: PCY_CUDA(launch_pdl(k_resolve2x<1>, dim3(PCY_PAR_MAXCTA), dim3(64), res_smem, rs, E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, (const ChainHdr*)chh, (const ChainLvl*)chr, pp, pb, pseq)); break;
-            case 2: PCY_CUDA(launch_pdl(k_resolve2x<2>, dim3(PCY_PAR_MAXCTA), dim3(64), res_smem, rs, E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, (const ChainHdr*)chh, (const ChainLvl*)chr, pp, pb, pseq)); break;
-            case 4: PCY_CUDA(launch_pdl(k_resolve2x<4>, dim3(PCY_PAR_MAXCTA), dim3(64), res_smem, rs, E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, (const ChainHdr*)chh, (const ChainLvl*)chr, pp, pb, pseq)); break;
-            case 8: PCY_CUDA(launch_pdl(k_resolve2x<8>, dim3(PCY_PAR_MAXCTA), dim3(64), res_smem, rs, E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, (const ChainHdr*)chh, (const ChainLvl*)chr, pp, pb, pseq)); break;
+            case 1: PCY_CUDA(launch_pdl(k_resolve2x<1>, dim3(PCY_PAR_MAXCTA), dim3(64), res_smem, rs, E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, (const ChainHdr*)chh, (const ChainLvl*)chr, pp, pb, pseq, planseq)); break;
+            case 2: PCY_CUDA(launch_pdl(k_resolve2x<2>, dim3(PCY_PAR_MAXCTA), dim3(64), res_smem, rs, E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, (const ChainHdr*)chh, (const ChainLvl*)chr, pp, pb, pseq, planseq)); break;
+            case 4: PCY_CUDA(launch_pdl(k_resolve2x<4>, dim3(PCY_PAR_MAXCTA), dim3(64), res_smem, rs, E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, (const ChainHdr*)chh, (const ChainLvl*)chr, pp, pb, pseq, planseq)); break;
+            case 8: PCY_CUDA(launch_pdl(k_resolve2x<8>, dim3(PCY_PAR_MAXCTA), dim3(64), res_smem, rs, E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, (const ChainHdr*)chh, (const ChainLvl*)chr, pp, pb, pseq, planseq)); break;
             case 100: k_resolve3x<true, 2048><<<PCY_PAR_MAXCTA, 32, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, nullptr, 0, 0, pp, pb, pseq); break;
             case 101: k_resolve3x<false, 512><<<PCY_PAR_MAXCTA, 32, res_smem, rs>>>(E, Xs, XSs, Ws, Bs, kn, first_rem, countw, nnew_cap, chh, chr, gram, kn, 0, pp, pb, pseq); break;
           }
@@ -2050,7 +2090,7 @@ struct Engine {
             nstart = start + nwin;
             if (nwin > 0 && nstart < nb) {
               nkn = nb - nstart > nkb ? nkb : nb - nstart;
-              rcp = enqueue_k1(off + nstart, nkn, false, true); if (rcp) return rcp;
+              rcp = enqueue_k1(off + nstart, nkn, false, true, pseq); if (rcp) return rcp;
 #ifdef PCY_TIMELINE
               ++tl_early;
 #endif

@@ -51,6 +51,10 @@ struct EngCtl {
   // window it chose for K1 batch `plan_seq`, so the host can enqueue the next
   // batch while the resolve kernel runs
   long long plan_mode, plan_nwin, plan_seq;
+  // device only: publication number of the last window whose tree writes are
+  // complete (set by the finishing resolve CTA before it copies the counters
+  // to the host mirror); the run-ahead chain walk waits on it (flag_wait)
+  long long win_done;
 };
 
 // groups of at least this many members are contracted on the tensor cores
@@ -77,6 +81,7 @@ struct ParCtl {
   long long F0, Falloc0, freen0, Galloc0, Aalloc0, nidx0;   // control snapshot
   unsigned long long open_ticket, g_ticket, a_ticket, done, opens;
   int arena_fail, pad;
+  long long ready;     // k_plan's launch number once every field above/below is written (flag_wait)
   int dbg_sets, dbg_maxset, dbg_maxcta, dbg_pad;   // PCY_TRACE builds: domain sets, largest set, longest CTA list
   int off[PCY_PAR_MAXCTA + 1];
   int list[PCY_PAR_MAXITEMS];
@@ -161,6 +166,36 @@ __device__ __forceinline__ void tl_cta(long long items, int nnew, long long slow
     g_tlc[i] = ((unsigned long long)(cyc & 0xffffff) << 40) | ((unsigned long long)(slow & 0xfff) << 28) |
                ((unsigned long long)(nnew & 0xfff) << 16) | (unsigned long long)(items & 0xffff);
 }
+// decision-warp cycle split per list-length bucket: count, wait-for-staging,
+// slow-path, start-up, clean-up, demand-load cycles
+__device__ unsigned long long g_tls[8][8];
+__device__ __forceinline__ void tl_split(long long items, long long wait, long long slow, long long start, long long clean, long long dem, long long fast) {
+  const int b = items <= 2 ? 0 : items <= 4 ? 1 : items <= 8 ? 2 : items <= 12 ? 3 : items <= 16 ? 4 : items <= 24 ? 5 : items <= 48 ? 6 : 7;
+  atomicAdd(&g_tls[b][0], 1ULL); atomicAdd(&g_tls[b][1], (unsigned long long)wait); atomicAdd(&g_tls[b][2], (unsigned long long)slow);
+  atomicAdd(&g_tls[b][3], (unsigned long long)start); atomicAdd(&g_tls[b][4], (unsigned long long)clean); atomicAdd(&g_tls[b][5], (unsigned long long)dem);
+  atomicAdd(&g_tls[b][6], (unsigned long long)fast);
+}
+__device__ unsigned long long g_tls2[8][8];
+__device__ __forceinline__ void tl_split2(long long items, long long dir, long long nw, long long cap, long long ndir, long long nnew, long long nlev) {
+  const int b = items <= 2 ? 0 : items <= 4 ? 1 : items <= 8 ? 2 : items <= 12 ? 3 : items <= 16 ? 4 : items <= 24 ? 5 : items <= 48 ? 6 : 7;
+  atomicAdd(&g_tls2[b][1], (unsigned long long)dir); atomicAdd(&g_tls2[b][2], (unsigned long long)nw);
+  atomicAdd(&g_tls2[b][3], (unsigned long long)cap); atomicAdd(&g_tls2[b][4], (unsigned long long)ndir); atomicAdd(&g_tls2[b][5], (unsigned long long)nnew);
+  atomicAdd(&g_tls2[b][6], (unsigned long long)nlev);
+}
+// reattach CTAs by list length: count, cycles, items, stage-wait cycles, adds, levels, new-member scan cycles
+__device__ unsigned long long g_tlr[8][8];
+__device__ __forceinline__ void tl_rea(long long items, long long cyc, long long wait, long long adds, long long lev, long long scan) {
+  const int b = items <= 8 ? 0 : items <= 16 ? 1 : items <= 32 ? 2 : items <= 64 ? 3 : items <= 128 ? 4 : items <= 256 ? 5 : items <= 512 ? 6 : 7;
+  atomicAdd(&g_tlr[b][0], 1ULL); atomicAdd(&g_tlr[b][1], (unsigned long long)cyc); atomicAdd(&g_tlr[b][2], (unsigned long long)items);
+  atomicAdd(&g_tlr[b][3], (unsigned long long)wait); atomicAdd(&g_tlr[b][4], (unsigned long long)adds); atomicAdd(&g_tlr[b][5], (unsigned long long)lev);
+  atomicAdd(&g_tlr[b][6], (unsigned long long)scan);
+}
+__device__ unsigned long long g_tlr2[8][12];
+__device__ __forceinline__ void tl_rea2(long long items, long long a0, long long a1, long long a2, long long a3, long long a4, long long a5, long long a6, long long a7, long long a8) {
+  const int b = items <= 8 ? 0 : items <= 16 ? 1 : items <= 32 ? 2 : items <= 64 ? 3 : items <= 128 ? 4 : items <= 256 ? 5 : items <= 512 ? 6 : 7;
+  const long long v[9] = {a0, a1, a2, a3, a4, a5, a6, a7, a8};
+  for (int k = 0; k < 9; ++k) atomicAdd(&g_tlr2[b][k], (unsigned long long)v[k]);
+}
 #else
 #define PCY_TL(tag) ((void)0)
 #endif
@@ -171,6 +206,31 @@ __device__ __forceinline__ void tl_cta(long long items, int nnew, long long slow
 // completed and its writes are visible (a no-op for ordinary launches), and
 // pdl_launch_dependents() lets the successor's CTAs be scheduled early.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Flag hand-off between two kernels of one stream where the second was
+// launched programmatically and is already resident: thread 0 of the CTA polls
+// a device word the producer stores after a __threadfence() (relaxed loads at
+// L2, then an acquire fence at GPU scope: later loads of this SM do not hit
+// stale L1 lines), the CTA then
+// meets at a barrier.  The wait for full grid completion (drain, flush, the
+// producer's host-mirror writes) is skipped.  After `spins` unsuccessful polls
+// the CTA falls back to griddepcontrol.wait, which is always sufficient.
+__device__ __forceinline__ long long ld_relaxed_gpu(const long long* p) {
+  long long v;
+  asm volatile("ld.relaxed.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void flag_wait(const long long* flag, long long want, int spins = 4096) {
+  if (threadIdx.x == 0) {
+    bool ok = false;
+    for (int it = 0; it < spins; ++it) {
+      if (ld_relaxed_gpu(flag) >= want) { ok = true; break; }   // polls at L2; the fence below acquires
+      __nanosleep(40);
+    }
+    if (!ok) asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  }
+  __syncthreads();
+}
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // cp.async helpers (global -> shared without registers)

@@ -160,6 +160,10 @@ __device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __res
     }
   };
   int status = ST_DONE; long long stop = n;
+#ifdef PCY_TIMELINE
+  const long long tl_t0 = clock64();
+  long long tl_wait = 0, tl_lev = 0, tl_scan = 0, tl_nd = 0, tl_cd = 0, tl_nn = 0, tl_cn = 0, tl_nrec = 0, tl_nglob = 0, tl_cm = 0, tl_nsm = 0, tl_ctail = 0;
+#endif
 
   for (int s2 = lane; s2 < PCY_MOD_SLOTS; s2 += 32) S.mkey[s2] = -1;
   for (int s2 = lane; s2 < PCY_GMAP_SLOTS; s2 += 32) S.gkey[s2] = -1;
@@ -223,6 +227,10 @@ __device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __res
     for (;;) {
       int bj = -1, li = -1;
       double bp = INFINITY;
+#ifdef PCY_TIMELINE
+      ++tl_lev;
+      const long long tl_s0 = clock64();
+#endif
       if (!direct) {
         if (L < len) { li = L; bj = S.rb[cur][L].j; bp = S.rb[cur][L].part; }
         else direct = true;
@@ -235,8 +243,15 @@ __device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __res
           scan_members(E, mem, 0, cnt, xsm, lane, p, ps);
           if (ps < cnt) { bj = mem[ps]; bp = p; }
         }
+#ifdef PCY_TIMELINE
+        ++tl_nd; tl_cd += clock64() - tl_s0;
+#endif
       }
       int bt = -1;
+#ifdef PCY_TIMELINE
+      const long long tl_s1 = clock64();
+      if ((gbits[g >> 5] >> (g & 31)) & 1u) ++tl_nn;
+#endif
       if ((gbits[g >> 5] >> (g & 31)) & 1u) {
         // one new member per lane: sequential dot over the padded smem row
         double np_ = INFINITY; int nt = 0x7fffffff;
@@ -270,6 +285,11 @@ __device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __res
         warp_argmin(np_, nt);
         if (nt != 0x7fffffff && (np_ < bp || bj < 0)) { bp = np_; bt = nt; bj = S.tid[nt]; }
       }
+#ifdef PCY_TIMELINE
+      const long long tl_s2 = clock64();
+      tl_scan += tl_s2 - tl_s0;
+      tl_cn += tl_s2 - tl_s1;
+#endif
       if (bj < 0 || radd(bp, rsq_c) > radius) {
         // group.add(node): u keeps its statistics (coreset.py:403-406)
         const int t = nnew++;
@@ -312,7 +332,13 @@ __device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __res
         const ChainLvl& rc = S.rb[cur][li];
         hw = rc.w; hq = rc.q; hsn = rc.sn;
         merge = rc.take != 0; mw = rc.w + wu_c; mq = rc.nq; mnorm = rc.nsn;
+#ifdef PCY_TIMELINE
+        ++tl_nrec;
+#endif
       } else {
+#ifdef PCY_TIMELINE
+        if (shost) ++tl_nsm; else if (bj != prnode) ++tl_nglob;
+#endif
         if (bt >= 0) { hw = S.tw[bt]; hq = S.tq[bt]; hsn = S.tsn[bt]; }
         else if (touched) { ms = map_find(S, bj); hw = S.mw[ms]; hq = S.mq[ms]; hsn = S.msn[ms]; }
         else { hw = E.w[bj]; hq = E.q[bj]; hsn = E.sn[bj]; }
@@ -334,6 +360,10 @@ __device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __res
         mw = hw + wu_c; mq = radd(hq, qu_c);
         merge = rsub(mq, rdiv(mnorm, (double)mw)) <= T;
       }
+#ifdef PCY_TIMELINE
+      const long long tl_s3 = clock64();
+      tl_cm += tl_s3 - tl_s2;
+#endif
       if (merge) {
         if (shost) {
           double* hs = tsr + (long long)bt * ld;
@@ -393,8 +423,14 @@ __device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __res
       g = c;
       radius = rmul(radius, 0.25);
       ++L;
+#ifdef PCY_TIMELINE
+      tl_ctail += clock64() - tl_s3;
+#endif
     }
     __syncwarp();
+#ifdef PCY_TIMELINE
+    const long long tl_w0 = clock64();
+#endif
     if (has_next) {
       uint4* dst = reinterpret_cast<uint4*>(&S.rb[cur ^ 1][0]);
 #pragma unroll
@@ -418,6 +454,10 @@ __device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __res
       cur ^= 1;
     }
     __syncwarp();
+#ifdef PCY_TIMELINE
+    if (__shfl_sync(PCY_FULL, xr[0] + su[0] + (double)wu_c, 0) == 1.2345e-300) ++tl_lev;   // wait for the prefetched rows
+    tl_wait += clock64() - tl_w0;
+#endif
   }
   cp_async_wait_all();
 
@@ -484,6 +524,9 @@ __device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __res
   __syncwarp();
   if constexpr (PAR) {
     int lastf = 0;   // this CTA finished the window: its warp publishes
+#ifdef PCY_TIMELINE
+    if (lane == 0) { tl_rea(n, clock64() - tl_t0, tl_wait, nnew, tl_lev, tl_scan); tl_rea2(n, tl_nd, tl_cd, tl_nn, tl_cn, tl_nrec, tl_nglob, tl_nsm, tl_cm, tl_ctail); }
+#endif
     if (lane == 0) {
       using ull = unsigned long long;
       if (status != ST_DONE) { atomicExch(&par->arena_fail, status == ST_ARENA ? ST_ARENA : ST_PAR_BROKEN); par->pad = status; }

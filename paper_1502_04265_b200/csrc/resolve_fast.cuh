@@ -61,13 +61,17 @@ __device__ __forceinline__ long long capacity(long long nn, double qv, double sn
 template <int WPI>
 __global__ void k_chain2(EngDev E, const double* __restrict__ X, const double* __restrict__ XS,
                          const long long* __restrict__ W, long long n, ChainHdr* __restrict__ H,
-                         ChainLvl* __restrict__ R, const double* __restrict__ P, long long ldp) {
+                         ChainLvl* __restrict__ R, const double* __restrict__ P, long long ldp,
+                         long long wait_seq = 0) {
   // WPI == 1: one warp per item, several items per CTA.  WPI > 1: one item per
   // CTA; every warp walks the same chain (identical decisions) and the fp64
   // dots are split over the warps (cta_dot), for large d.
   extern __shared__ double sm_x[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  pdl_wait();   // run-ahead launch: the previous window's resolve kernel has finished
+  // run-ahead launch: the previous window's resolve kernel has finished its
+  // tree writes (wait_seq: its publication number) / has completed
+  if (wait_seq > 0) flag_wait(&E.ctl->win_done, wait_seq);
+  else pdl_wait();
   if (blockIdx.x == 0 && threadIdx.x == 0) PCY_TL(1);
   const long long i = WPI == 1 ? (long long)blockIdx.x * (blockDim.x >> 5) + wib : (long long)blockIdx.x;
   if (i >= n) return;
@@ -387,6 +391,7 @@ __device__ __forceinline__ void resolve2_body(const EngDev& E, const double* __r
 
 #ifdef PCY_TIMELINE
   const long long tl_t0 = clock64();
+  long long tl_wait = 0, tl_slow = 0, tl_start = 0, tl_clean = 0, tl_dem = 0, tl_fast = 0, tl_dir = 0, tl_new = 0, tl_cap = 0, tl_ndir = 0, tl_nnew = 0, tl_nlev = 0;
 #endif
   EngCtl* C = E.ctl;
   const long long m = E.m;
@@ -436,7 +441,14 @@ __device__ __forceinline__ void resolve2_body(const EngDev& E, const double* __r
   for (long long i = 0; i < n; ++i) {
     const int sl = (int)(i & (K3_SLOTS - 1));
     const int cur = sl;
+#ifdef PCY_TIMELINE
+    const long long tl_w0 = clock64();
+    if (i == 0) tl_start = tl_w0 - tl_t0;
+#endif
     nbar_sync(K3_BAR_FULL + sl, 64);
+#ifdef PCY_TIMELINE
+    tl_wait += clock64() - tl_w0;
+#endif
     const ChainHdr hc = S.shdr[sl];
     const int bad_c = S.sbad[sl];
     const long long w_c = S.sw[sl];
@@ -475,7 +487,14 @@ __device__ __forceinline__ void resolve2_body(const EngDev& E, const double* __r
     // current row of snapshot node bj into pr (HBM unless it is the held row)
     auto fetch_row = [&](int bj) {
       if (bj == prnode) return;
+#ifdef PCY_TIMELINE
+      const long long tl_d0 = clock64();
+#endif
       load_row<NPER>(pr, E.s + (long long)bj * ld, d, lane);
+#ifdef PCY_TIMELINE
+      if (__shfl_sync(PCY_FULL, pr[0], 0) == 1.2345e-300) ++c_dem;   // wait for the row
+      tl_dem += clock64() - tl_d0;
+#endif
       ++c_dem;
       prnode = bj;
     };
@@ -532,6 +551,9 @@ __device__ __forceinline__ void resolve2_body(const EngDev& E, const double* __r
     // ---- verified fast path: nothing on K1's path changed in this launch, so
     // every decision along it is K1's (same statistics, dots, members).
     bool done_fast = false;
+#ifdef PCY_TIMELINE
+    const long long tl_f0 = clock64();
+#endif
     if (!resume && len > 0 && !hc.trunc) {
       const int pl = hc.pred;
       bool ok = pl >= 0 && pl < len;
@@ -578,6 +600,10 @@ __device__ __forceinline__ void resolve2_body(const EngDev& E, const double* __r
         }
       }
     }
+#ifdef PCY_TIMELINE
+    const long long tl_s0 = clock64();
+    tl_fast += tl_s0 - tl_f0;
+#endif
     if (!done_fast) for (;;) {
       int bj = -1, li = -1;
       double bp = INFINITY;
@@ -586,7 +612,14 @@ __device__ __forceinline__ void resolve2_body(const EngDev& E, const double* __r
         else direct = true;   // truncated chain
       }
       ++c_lv;
+#ifdef PCY_TIMELINE
+      const long long tl_l0 = clock64();
+      ++tl_nlev;
+#endif
       if (direct && g < G0) {
+#ifdef PCY_TIMELINE
+        ++tl_ndir;
+#endif
         // members present at launch start, scanned directly (truncated chains only)
         ++c_dir;
         const int cnt = E.g_count[g];
@@ -599,6 +632,11 @@ __device__ __forceinline__ void resolve2_body(const EngDev& E, const double* __r
       }
       // members opened in this launch, in position order
       int bt = -1;
+#ifdef PCY_TIMELINE
+      const long long tl_l1 = clock64();
+      tl_dir += tl_l1 - tl_l0;
+      if ((gbits[g >> 5] >> (g & 31)) & 1u) ++tl_nnew;
+#endif
       if ((gbits[g >> 5] >> (g & 31)) & 1u) {
         // one new member per lane: sequential dot over the padded smem row
         double np_ = INFINITY; int nt = 0x7fffffff;
@@ -621,6 +659,10 @@ __device__ __forceinline__ void resolve2_body(const EngDev& E, const double* __r
         warp_argmin(np_, nt);
         if (nt != 0x7fffffff && (np_ < bp || bj < 0)) { bp = np_; bt = nt; bj = S.tid[nt]; }
       }
+#ifdef PCY_TIMELINE
+      const long long tl_l2 = clock64();
+      tl_new += tl_l2 - tl_l1;
+#endif
       // admission radius (coreset.py:329)
       if (bj < 0 || radd(bp, xs) > radius) {
         if (do_open(g, L)) { status = ST_REBUILD; stop = i; remaining = rem; }
@@ -660,6 +702,9 @@ __device__ __forceinline__ void resolve2_body(const EngDev& E, const double* __r
           nsn = radd(snv, radd(rmul(rmul(2.0, ft), dt), rmul((double)(take * take), xs)));
         }
       }
+#ifdef PCY_TIMELINE
+      tl_cap += clock64() - tl_l2;
+#endif
       if (take > 0) {
         const double ft = (double)take;
         if (bt >= 0) {
@@ -714,6 +759,9 @@ __device__ __forceinline__ void resolve2_body(const EngDev& E, const double* __r
       ++L;
     }
     __syncwarp();
+#ifdef PCY_TIMELINE
+    if (!done_fast) tl_slow += clock64() - tl_s0;
+#endif
     ++c_it;
 #pragma unroll
     for (int q = K3_SLOTS - 1; q > 0; --q) rec_mod[q] = rec_mod[q - 1];
@@ -726,6 +774,9 @@ __device__ __forceinline__ void resolve2_body(const EngDev& E, const double* __r
 
   // ---- cleanup: new nodes and their memberships to HBM (position order per group)
   __syncwarp();
+#ifdef PCY_TIMELINE
+  tl_clean = clock64();
+#endif
   for (int t = 0; t < nnew; ++t) {
     const int node = S.tid[t];
     const double* rr = tref + (long long)t * lds;
@@ -786,7 +837,7 @@ __device__ __forceinline__ void resolve2_body(const EngDev& E, const double* __r
     // deltas of this subtree, then the last CTA publishes the window
     int lastf = 0;   // this CTA finished the window: its warp publishes
 #ifdef PCY_TIMELINE
-    if (lane == 0) tl_cta(n, nnew, c_slow, clock64() - tl_t0);
+    if (lane == 0) { tl_cta(n, nnew, c_slow, clock64() - tl_t0); tl_split(n, tl_wait, tl_slow, tl_start, clock64() - tl_clean, tl_dem, tl_fast); tl_split2(n, tl_dir, tl_new, tl_cap, tl_ndir, tl_nnew, tl_nlev); }
 #endif
     if (lane == 0) {
       using ull = unsigned long long;
@@ -813,6 +864,7 @@ __device__ __forceinline__ void resolve2_body(const EngDev& E, const double* __r
         C->status = fail ? fail : (par->n_win < par->n_total ? ST_FULL : ST_DONE);
         C->err = fail ? par->pad : 0; C->stop = par->n_win; C->remaining = 0;
         __threadfence();
+        if (pub) *(volatile long long*)&C->win_done = pseq;   // the run-ahead chain walk may start
         PCY_TL(5);
         lastf = 1;
       }
@@ -829,7 +881,7 @@ __device__ __forceinline__ void resolve2_body(const EngDev& E, const double* __r
     C->cnt_levels += c_lv; C->cnt_direct += c_dir; C->cnt_demand += c_dem; C->cnt_slow += c_slow;
     C->cnt_items += c_it; C->cnt_dem_fast += c_demf; C->cnt_touch_child += c_tch;
     __threadfence();
-    if (pub) PCY_TL(5);
+    if (pub) { *(volatile long long*)&C->win_done = pseq; PCY_TL(5); }
   }
   __syncwarp();
   if (pub) ctl_publish_warp(E, pub, pseq, lane);
@@ -852,8 +904,8 @@ __global__ void __launch_bounds__(64, 1) k_resolve2x(EngDev E, const double* __r
                                                      const int* __restrict__ BAD, long long n, long long first_rem,
                                                      int countw, int nnew_cap, const ChainHdr* __restrict__ H,
                                                      const ChainLvl* __restrict__ R, ParCtl* __restrict__ par,
-                                                     EngCtl* pub, long long pseq) {
-  pdl_wait();                // k_plan has finished
+                                                     EngCtl* pub, long long pseq, long long planseq) {
+  flag_wait(&par->ready, planseq);   // k_plan has written its window
   pdl_launch_dependents();   // the next batch's chain walk may be scheduled; it waits for this grid
   if (blockIdx.x == 0 && threadIdx.x == 0) PCY_TL(4);
   if (par->mode == 0) resolve2_body<NPER, true>(E, X, XS, W, BAD, n, first_rem, countw, nnew_cap, H, R, par, pub, pseq);
@@ -1159,6 +1211,8 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
       if (ns > n) ns = n;
       par->n_win = ns;
       if (!order) PCY_TL(3);
+      __threadfence();
+      *(volatile long long*)&par->ready = planseq;   // the resolve CTAs may go (flag_wait)
       if (pub) {   // early publication: the host may enqueue the next K1 batch now
         volatile long long* t = &pub->plan_mode;
         t[0] = 1; t[1] = ns;
@@ -1375,6 +1429,8 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
     if (tid <= PCY_PAR_MAXCTA) par->off[tid] = ex;   // off[P] = window size
   }
   __syncthreads();
+  if (tid < c) { par->list[ctot[cta] + rank] = tid; __threadfence(); }
+  __syncthreads();
   if (tid == 0) {
     const int P = s_P;
     par->mode = 0; par->P = P; par->n_win = c; par->n_total = n;
@@ -1382,6 +1438,8 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
     par->Aalloc0 = C->A_alloc; par->nidx0 = C->next_index;
     par->open_ticket = 0; par->g_ticket = 0; par->a_ticket = 0; par->done = 0; par->opens = 0;
     par->arena_fail = 0;
+    __threadfence();
+    *(volatile long long*)&par->ready = planseq;   // the resolve CTAs may go (flag_wait)
     if (!order) PCY_TL(3);
     if (pub) {   // early publication: the host may enqueue the next K1 batch now
       volatile long long* t = &pub->plan_mode;
@@ -1390,6 +1448,4 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
       t[2] = planseq;
     }
   }
-  __syncthreads();
-  if (tid < c) par->list[ctot[cta] + rank] = tid;
 }
