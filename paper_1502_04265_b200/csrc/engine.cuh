@@ -190,6 +190,7 @@ __device__ __forceinline__ void tl_rea(long long items, long long cyc, long long
   atomicAdd(&g_tlr[b][3], (unsigned long long)wait); atomicAdd(&g_tlr[b][4], (unsigned long long)adds); atomicAdd(&g_tlr[b][5], (unsigned long long)lev);
   atomicAdd(&g_tlr[b][6], (unsigned long long)scan);
 }
+__device__ unsigned long long g_tlp[10];   // k_plan phase cycles (thread 0)
 __device__ unsigned long long g_tlr2[8][12];
 __device__ __forceinline__ void tl_rea2(long long items, long long a0, long long a1, long long a2, long long a3, long long a4, long long a5, long long a6, long long a7, long long a8) {
   const int b = items <= 8 ? 0 : items <= 16 ? 1 : items <= 32 ? 2 : items <= 64 ? 3 : items <= 128 ? 4 : items <= 256 ? 5 : items <= 512 ? 6 : 7;

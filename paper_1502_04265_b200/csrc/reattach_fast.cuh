@@ -174,20 +174,23 @@ __device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __res
 
   // ---- prologue: item 0
   double xr[NPER], su[NPER], pr[NPER];
-  int u_c = n > 0 ? order[gix(0)] : 0;
-  int u_n = n > 1 ? order[gix(1)] : 0;
-  ChainHdr hc = n > 0 ? H[gix(0)] : ChainHdr{0, 0, -1, 0};
-  ChainHdr hn = n > 1 ? H[gix(1)] : ChainHdr{0, 0, -1, 0};
+  // window positions of items i .. i+2 in registers (list entries are read
+  // three items ahead: no list load sits on an item's critical path)
+  long long gq0 = n > 0 ? gix(0) : 0, gq1 = n > 1 ? gix(1) : 0, gq2 = n > 2 ? gix(2) : 0;
+  int u_c = n > 0 ? order[gq0] : 0;
+  int u_n = n > 1 ? order[gq1] : 0;
+  ChainHdr hc = n > 0 ? H[gq0] : ChainHdr{0, 0, -1, 0};
+  ChainHdr hn = n > 1 ? H[gq1] : ChainHdr{0, 0, -1, 0};
   long long wu_c = 0; double qu_c = 0.0, snu_c = 0.0, rsq_c = 0.0;
   if (n > 0) {
     load_row<NPER>(xr, E.r + (long long)u_c * ld, d, lane);
     load_row<NPER>(su, E.s + (long long)u_c * ld, d, lane);
     if (hc.predj >= 0) load_row<NPER>(pr, E.s + (long long)hc.predj * ld, d, lane);
     wu_c = E.w[u_c]; qu_c = E.q[u_c]; snu_c = E.sn[u_c]; rsq_c = E.rn[u_c];
-    const uint4* src = reinterpret_cast<const uint4*>(R + gix(0) * PCY_FMAXL);
+    const uint4* src = reinterpret_cast<const uint4*>(R + gq0 * PCY_FMAXL);
     uint4* dst = reinterpret_cast<uint4*>(&S.rb[0][0]);
     for (int c = lane; c < REC_CHUNKS; c += 32) dst[c] = src[c];
-    stage_grow(0, gix(0));
+    stage_grow(0, gq0);
     cp_async_wait_all();
   }
   __syncwarp();
@@ -203,16 +206,17 @@ __device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __res
     ChainHdr h2 = ChainHdr{0, 0, -1, 0};
     int u2 = 0;
     long long wu_n = 0; double qu_n = 0.0, snu_n = 0.0, rsq_n = 0.0;
+    const long long gq3 = i + 3 < n ? gix(i + 3) : 0;
     if (has_next) {
       load_row<NPER>(xn, E.r + (long long)u_n * ld, d, lane);
       load_row<NPER>(sun, E.s + (long long)u_n * ld, d, lane);
       wu_n = E.w[u_n]; qu_n = E.q[u_n]; snu_n = E.sn[u_n]; rsq_n = E.rn[u_n];
-      const uint4* src = reinterpret_cast<const uint4*>(R + gix(i + 1) * PCY_FMAXL);
+      const uint4* src = reinterpret_cast<const uint4*>(R + gq1 * PCY_FMAXL);
 #pragma unroll
       for (int q = 0; q < (REC_CHUNKS + 31) / 32; ++q) { const int c = lane + 32 * q; if (c < REC_CHUNKS) rpf[q] = src[c]; }
       if (hn.predj >= 0) load_row<NPER>(pn, E.s + (long long)hn.predj * ld, d, lane);
-      if (i + 2 < n) { h2 = H[gix(i + 2)]; u2 = order[gix(i + 2)]; }
-      stage_grow(cur ^ 1, gix(i + 1));
+      if (i + 2 < n) { h2 = H[gq2]; u2 = order[gq2]; }
+      stage_grow(cur ^ 1, gq1);
     }
     // ---- item i: node u
     const int u = u_c;
@@ -312,7 +316,7 @@ __device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __res
         }
         if (lane == 0) {
           S.tdirty[t] = 0;
-          S.tid[t] = u; S.tgrp[t] = g; S.tchild[t] = -1; S.tnext[t] = -1; S.titem[t] = (int)gix(i);
+          S.tid[t] = u; S.tgrp[t] = g; S.tchild[t] = -1; S.tnext[t] = -1; S.titem[t] = (int)gq0;
           S.tw[t] = wu_c; S.tq[t] = qu_c; S.tsn[t] = snu_c; S.trn[t] = rsq_c;
           if (had) { S.tnext[S.gtail[gs]] = t; S.gtail[gs] = t; }
           else { S.gkey[gs] = g; S.ghead[gs] = t; S.gtail[gs] = t; gbits[g >> 5] |= 1u << (g & 31); }
@@ -453,6 +457,7 @@ __device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __res
       cp_async_wait_all();   // the next item's Gram row
       cur ^= 1;
     }
+    gq0 = gq1; gq1 = gq2; gq2 = gq3;
     __syncwarp();
 #ifdef PCY_TIMELINE
     if (__shfl_sync(PCY_FULL, xr[0] + su[0] + (double)wu_c, 0) == 1.2345e-300) ++tl_lev;   // wait for the prefetched rows

@@ -1012,6 +1012,13 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
   __shared__ int wsum[32];
   __shared__ int s_c, s_last, s_heavy, s_cut, s_P;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+#ifdef PCY_TIMELINE
+  long long plan_t[10];
+  plan_t[0] = clock64();
+#define PLAN_T(k) plan_t[k] = clock64()
+#else
+#define PLAN_T(k) ((void)0)
+#endif
   pdl_launch_dependents();   // the resolve kernel's CTAs may be scheduled; they wait for this grid
   if (tid == 0 && !order) PCY_TL(2);
   const EngCtl* C = E.ctl;
@@ -1036,6 +1043,7 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
     s_last = -1; s_heavy = 0; s_cut = 0x7fffffff; s_P = 0;
   }
   __syncthreads();
+  PLAN_T(1);
   // pass 1: invalid rows, weighted items, predicted actions
   ChainHdr h = ChainHdr{0, 0, -1, 0};
   const ChainLvl* rec = R + (long long)tid * PCY_FMAXL;
@@ -1076,6 +1084,7 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
     if (W && W[tid] > 1) s_heavy = 1;
   }
   __syncthreads();
+  PLAN_T(2);
   const bool heavy = s_heavy != 0;
   if (tid == 0 && (heavy || order) && room < nn) atomicMin(&s_c, (int)room);
   auto open_key = [&](int P) { return NC + (P == PLAN_ROOT ? NC : P); };
@@ -1127,6 +1136,7 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
     }
   }
   __syncthreads();
+  PLAN_T(3);
   // Budget bound of unit windows (coreset.py:330-335: an open at F == m opens
   // one copy and rebuilds, which a parallel window cannot do).  Only items that
   // may open count against room = m - F0: predicted openers, conflicting
@@ -1144,19 +1154,22 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
     int gk[PCY_FMAXL];   // group key per level: OPEN(parent)
 #pragma unroll
     for (int l = 0; l < PCY_FMAXL; ++l) gk[l] = open_key(l == 0 ? PLAN_ROOT : pj[l > 0 ? l - 1 : 0]);
+    // The may-touch minima only decrease as items turn uncertain, so the table
+    // is filled incrementally: certain absorbers enter their absorb node once,
+    // an item enters its whole path when it turns uncertain (same tables and
+    // decisions as recomputing them every round).
+    for (int hh = tid; hh < PLAN_HASH; hh += blockDim.x) tmin[hh] = 0x7fffffff;
+    __syncthreads();
+    bool unc = live && s_unc[tid];
+    bool pending = unc;   // uncertain, path not entered yet
+    if (live && !unc && absorb >= 0) atomicMin(&tmin[ph_insert(tkey, absorb)], tid);
     for (int it = 0; it < 16; ++it) {
-      for (int hh = tid; hh < PLAN_HASH; hh += blockDim.x) tmin[hh] = 0x7fffffff;
-      __syncthreads();
-      const bool unc = live && s_unc[tid];
-      if (live) {
-        if (unc) {
+      if (pending) {
 #pragma unroll
-          for (int l = 0; l < PCY_FMAXL; ++l)
-            if (l < h.len && pj[l] >= 0) atomicMin(&tmin[ph_insert(tkey, pj[l])], tid);
-          if (!opener && h.len > 0) atomicMin(&tmin[ph_insert(tkey, gk[h.len - 1 < PCY_FMAXL ? h.len - 1 : 0])], tid);
-        } else if (absorb >= 0) {
-          atomicMin(&tmin[ph_insert(tkey, absorb)], tid);
-        }
+        for (int l = 0; l < PCY_FMAXL; ++l)
+          if (l < h.len && pj[l] >= 0) atomicMin(&tmin[ph_insert(tkey, pj[l])], tid);
+        if (!opener && h.len > 0) atomicMin(&tmin[ph_insert(tkey, gk[h.len - 1 < PCY_FMAXL ? h.len - 1 : 0])], tid);
+        pending = false;
       }
       __syncthreads();
       int changed = 0;
@@ -1169,7 +1182,7 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
           const int so = ph_find(tkey, gk[l]);
           if (so >= 0 && tmin[so] < tid) u = true;
         }
-        if (u) { s_unc[tid] = 1; changed = 1; }
+        if (u) { s_unc[tid] = 1; unc = true; pending = true; changed = 1; }
       }
       if (!__syncthreads_or(changed)) break;
     }
@@ -1202,6 +1215,7 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
     __syncthreads();
   }
   const int c0 = s_c;
+  PLAN_T(4);
   if (c0 < theta) {
     if (tid == 0) {
       par->mode = 1; par->P = 0; par->n_total = n;
@@ -1248,6 +1262,7 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
     }
   }
   __syncthreads();
+  PLAN_T(5);
   const int root = act ? uf_find(uf, k1) : -1;
   if (act) atomicMin(&hfirst[root], tid);
   __syncthreads();
@@ -1282,6 +1297,7 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
   __syncthreads();
   if (isfirst) ohead[root] = wsum[wid] + __popc(bal & ((1u << lane) - 1u));
   __syncthreads();
+  PLAN_T(6);
   // Balanced CTA lists.  A window of 1024 items has ~800 domain sets, most of
   // one or two items and a few of tens; the resolve launch lasts as long as
   // its longest list.  Sets of >= PLAN_BIG items are dealt out largest first
@@ -1377,6 +1393,7 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
       scta[root] = lo;
     }
     __syncthreads();
+  PLAN_T(7);
   }
   const int cta = act ? scta[root] : -1 - lane;
   // rank of each item within its CTA (stream order): per-warp chunk counts
@@ -1399,6 +1416,7 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
   const int c = c0 < s_cut ? c0 : s_cut;
   if (tid < c) atomicMax(&ctot[cta], rank + 1);
   __syncthreads();
+  PLAN_T(8);
   // list offsets: exclusive scan of the CTA counts (warps 0..4), P = last CTA with items + 1
   constexpr int SCAN_T = (PCY_PAR_MAXCTA + 1 + 31) / 32 * 32;
   int cv = 0, cinc = 0;
@@ -1440,6 +1458,10 @@ __global__ void __launch_bounds__(PCY_PAR_MAXITEMS) k_plan(EngDev E, const doubl
     par->arena_fail = 0;
     __threadfence();
     *(volatile long long*)&par->ready = planseq;   // the resolve CTAs may go (flag_wait)
+#ifdef PCY_TIMELINE
+    plan_t[9] = clock64();
+    if (!order) { for (int k = 1; k < 10; ++k) atomicAdd(&g_tlp[k], (unsigned long long)(plan_t[k] - plan_t[k - 1])); atomicAdd(&g_tlp[0], 1ULL); }
+#endif
     if (!order) PCY_TL(3);
     if (pub) {   // early publication: the host may enqueue the next K1 batch now
       volatile long long* t = &pub->plan_mode;
