@@ -132,10 +132,7 @@ __device__ bool grp_append(const EngDev& E, int g, int node, long long& A_alloc,
 // Nearest among members [lo, hi) of the arena segment `mem`, against vector xv
 // (shared memory).  Lane-per-member transposed dots.  Returns the part
 // |r|^2 - 2 r.x and the position (lowest position wins ties), on all lanes.
-// Not inlined: the unrolled 32-member body is about half of every kernel that
-// would inline it, and the resolve / reattach kernels reach it only for
-// truncated chains; out of line the hot loops stay compact in the I-cache.
-__device__ __noinline__ void scan_members(const EngDev& E, const int* __restrict__ mem,
+__device__ __forceinline__ void scan_members(const EngDev& E, const int* __restrict__ mem,
                                              int lo, int hi, const double* __restrict__ xv,
                                              int lane, double& bp, int& bpos) {
   const int d = E.d, ld = E.ld;
@@ -1478,7 +1475,7 @@ struct Engine {
         for (int b = 0; b < 8; ++b)
           if (tr[b][0]) {
             const double c = (double)tr[b][0];
-            fprintf(stderr, " | items %s: dirscan n %.1f cyc %.0f newscan n %.1f cyc %.0f merge rec %.1f glob %.1f smem %.1f cyc %.0f tail cyc %.0f", rb[b], t2[b][0] / c, t2[b][1] / c,
+            fprintf(stderr, " | items %s: dirscan n %.1f head cyc %.0f newscan n %.1f cyc %.0f merge rec %.1f glob %.1f smem %.1f cyc %.0f tail cyc %.0f", rb[b], t2[b][0] / c, t2[b][1] / c,
                     t2[b][2] / c, t2[b][3] / c, t2[b][4] / c, t2[b][5] / c, t2[b][6] / c, t2[b][7] / c, t2[b][8] / c);
           }
         fprintf(stderr, "\n");

@@ -134,11 +134,16 @@ __device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __res
   // scans of same-launch entries read shared memory
   double* growb = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(mbits) +
                                             ((sizeof(unsigned) * (size_t)(mwords + gwords) + 15) & ~size_t(15)));
-  auto stage_grow = [&](int buf, long long it) {
+  // Only the columns the scans read are staged, by entry: the batch rows of the
+  // entries placed so far (nn of them) and of the item being processed while
+  // this copy is in flight (it may place entry nn).  Entries come from earlier
+  // items of this list, so their columns are in the row's lower triangle.
+  auto stage_grow = [&](int buf, long long it, int nn, long long placing) {
     if (!gram) return;
     const double* src = gram + it * gld;
     double* dst = growb + buf * PCY_PAR_MAXITEMS;
-    for (int c = lane; c < (int)it; c += 32) cp_async8(dst + c, src + c);
+    for (int t = lane; t < nn; t += 32) cp_async8(dst + t, src + S.titem[t]);
+    if (lane == 0 && placing >= 0) cp_async8(dst + nn, src + placing);
     cp_async_commit();
   };
   // s rows of the first ts_cap entries placed in this launch: in a fresh tree
@@ -162,7 +167,7 @@ __device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __res
   int status = ST_DONE; long long stop = n;
 #ifdef PCY_TIMELINE
   const long long tl_t0 = clock64();
-  long long tl_wait = 0, tl_lev = 0, tl_scan = 0, tl_nd = 0, tl_cd = 0, tl_nn = 0, tl_cn = 0, tl_nrec = 0, tl_nglob = 0, tl_cm = 0, tl_nsm = 0, tl_ctail = 0;
+  long long tl_wait = 0, tl_lev = 0, tl_scan = 0, tl_nd = 0, tl_cd = 0, tl_nn = 0, tl_cn = 0, tl_nrec = 0, tl_nglob = 0, tl_cm = 0, tl_nsm = 0, tl_ctail = 0, tl_head = 0;
 #endif
 
   for (int s2 = lane; s2 < PCY_MOD_SLOTS; s2 += 32) S.mkey[s2] = -1;
@@ -190,7 +195,7 @@ __device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __res
     const uint4* src = reinterpret_cast<const uint4*>(R + gq0 * PCY_FMAXL);
     uint4* dst = reinterpret_cast<uint4*>(&S.rb[0][0]);
     for (int c = lane; c < REC_CHUNKS; c += 32) dst[c] = src[c];
-    stage_grow(0, gq0);
+    stage_grow(0, gq0, 0, -1);
     cp_async_wait_all();
   }
   __syncwarp();
@@ -198,6 +203,9 @@ __device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __res
   int prnode = hc.predj;
 
   for (long long i = 0; i < n; ++i) {
+#ifdef PCY_TIMELINE
+    const long long tl_h0 = clock64();
+#endif
     if (nnew >= nnew_cap || S.modcount >= PCY_MOD_SLOTS / 2) { status = ST_FULL; stop = i; break; }
     // ---- prefetch item i+1
     double xn[NPER], sun[NPER], pn[NPER];
@@ -216,7 +224,7 @@ __device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __res
       for (int q = 0; q < (REC_CHUNKS + 31) / 32; ++q) { const int c = lane + 32 * q; if (c < REC_CHUNKS) rpf[q] = src[c]; }
       if (hn.predj >= 0) load_row<NPER>(pn, E.s + (long long)hn.predj * ld, d, lane);
       if (i + 2 < n) { h2 = H[gq2]; u2 = order[gq2]; }
-      stage_grow(cur ^ 1, gq1);
+      stage_grow(cur ^ 1, gq1, nnew, gq0);
     }
     // ---- item i: node u
     const int u = u_c;
@@ -228,6 +236,9 @@ __device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __res
     for (int k = 0; k < NPER; ++k) { const int e = lane + 32 * k; if (e < ld) xsm[e] = xr[k]; }
     __syncwarp();
     int lastmod = -1;
+#ifdef PCY_TIMELINE
+    tl_head += clock64() - tl_h0;
+#endif
     for (;;) {
       int bj = -1, li = -1;
       double bp = INFINITY;
@@ -262,12 +273,13 @@ __device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __res
         if (gram) {
           // same-launch nodes are rows of this batch: (current, earlier) entry of the batch Gram
           const double* grow = growb + cur * PCY_PAR_MAXITEMS;
-          for (int c0 = 0; c0 < nnew; c0 += 32) {
-            const int t = c0 + lane;
-            if (t < nnew && S.tgrp[t] == g) {
-              const double part = radd(S.trn[t], rmul(grow[S.titem[t]], -2.0));
-              if (part < np_) { np_ = part; nt = t; }
-            }
+          for (int c0 = 0; c0 < nnew; c0 += 64) {   // two independent entries per lane and pass
+            const int t0 = c0 + lane, t1 = t0 + 32;
+            const bool v0 = t0 < nnew && S.tgrp[t0] == g, v1 = t1 < nnew && S.tgrp[t1] == g;
+            const double p0 = v0 ? radd(S.trn[t0], rmul(grow[t0], -2.0)) : INFINITY;
+            const double p1 = v1 ? radd(S.trn[t1], rmul(grow[t1], -2.0)) : INFINITY;
+            if (p0 < np_) { np_ = p0; nt = t0; }
+            if (p1 < np_) { np_ = p1; nt = t1; }
           }
         } else
         for (int c0 = 0; c0 < nnew; c0 += 32) {
@@ -530,7 +542,7 @@ __device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __res
   if constexpr (PAR) {
     int lastf = 0;   // this CTA finished the window: its warp publishes
 #ifdef PCY_TIMELINE
-    if (lane == 0) { tl_rea(n, clock64() - tl_t0, tl_wait, nnew, tl_lev, tl_scan); tl_rea2(n, tl_nd, tl_cd, tl_nn, tl_cn, tl_nrec, tl_nglob, tl_nsm, tl_cm, tl_ctail); }
+    if (lane == 0) { tl_rea(n, clock64() - tl_t0, tl_wait, nnew, tl_lev, tl_scan); tl_rea2(n, tl_nd, tl_head, tl_nn, tl_cn, tl_nrec, tl_nglob, tl_nsm, tl_cm, tl_ctail); }
 #endif
     if (lane == 0) {
       using ull = unsigned long long;
