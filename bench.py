@@ -620,8 +620,8 @@ def main():
         achieved = (r_units * bytes_per_pt) / (r_ms / 1e3) / 1e9 if r_ms > 0 else 0.0
         rooflines.append({"kernel": "k_plan + k_resolve2/3 (K3 subtree-parallel resolve + CF update)", "bound": "hbm",
                           "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                          "traffic": traffic(lambda k: k.startswith("k_resolve") and k.endswith("1>")),
-                          "traffic_unit": "bytes per launch (ncu dram read+write, subtree-parallel launch)",
+                          "traffic": traffic(lambda k: k.startswith("k_resolve") and ("x<" in k or k.endswith("1>"))),
+                          "traffic_unit": "bytes per launch (ncu dram read+write of the window's resolve launch; ncu replays start cold, in the bench the tree is L2-resident)",
                           "bytes_per_launch": (r_units * bytes_per_pt / r_cnt) if r_cnt else None,
                           "peak_source": peak_src,
                           "note": "latency-bound: one CTA per k_plan domain walks its items in stream order; "
