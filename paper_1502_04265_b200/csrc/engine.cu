@@ -1454,8 +1454,8 @@ struct Engine {
         cudaMemcpyToSymbol(g_tls2, tz, sizeof(tz));
         fprintf(stderr, "[timeline-split2]");
         for (int b = 0; b < 8; ++b)
-          if (ts[b][0]) fprintf(stderr, " | items %s: direct-scan %.0f (n %.1f) new-members %.0f (n %.1f) capacity %.0f levels %.1f", bn[b], (double)t2[b][1] / ts[b][0], (double)t2[b][4] / ts[b][0],
-                                (double)t2[b][2] / ts[b][0], (double)t2[b][5] / ts[b][0], (double)t2[b][3] / ts[b][0], (double)t2[b][6] / ts[b][0]);
+          if (ts[b][0]) fprintf(stderr, " | items %s: direct-scan %.0f (n %.1f) new-members %.0f (n %.1f) capacity %.0f levels %.1f clean %.1f", bn[b], (double)t2[b][1] / ts[b][0], (double)t2[b][4] / ts[b][0],
+                                (double)t2[b][2] / ts[b][0], (double)t2[b][5] / ts[b][0], (double)t2[b][3] / ts[b][0], (double)t2[b][6] / ts[b][0], (double)t2[b][7] / ts[b][0]);
         fprintf(stderr, "\n");
       }
       {

@@ -176,11 +176,11 @@ __device__ __forceinline__ void tl_split(long long items, long long wait, long l
   atomicAdd(&g_tls[b][6], (unsigned long long)fast);
 }
 __device__ unsigned long long g_tls2[8][8];
-__device__ __forceinline__ void tl_split2(long long items, long long dir, long long nw, long long cap, long long ndir, long long nnew, long long nlev) {
+__device__ __forceinline__ void tl_split2(long long items, long long dir, long long nw, long long cap, long long ndir, long long nnew, long long nlev, long long ncl) {
   const int b = items <= 2 ? 0 : items <= 4 ? 1 : items <= 8 ? 2 : items <= 12 ? 3 : items <= 16 ? 4 : items <= 24 ? 5 : items <= 48 ? 6 : 7;
   atomicAdd(&g_tls2[b][1], (unsigned long long)dir); atomicAdd(&g_tls2[b][2], (unsigned long long)nw);
   atomicAdd(&g_tls2[b][3], (unsigned long long)cap); atomicAdd(&g_tls2[b][4], (unsigned long long)ndir); atomicAdd(&g_tls2[b][5], (unsigned long long)nnew);
-  atomicAdd(&g_tls2[b][6], (unsigned long long)nlev);
+  atomicAdd(&g_tls2[b][6], (unsigned long long)nlev); atomicAdd(&g_tls2[b][7], (unsigned long long)ncl);
 }
 // reattach CTAs by list length: count, cycles, items, stage-wait cycles, adds, levels, new-member scan cycles
 __device__ unsigned long long g_tlr[8][8];

@@ -236,10 +236,29 @@ __device__ __forceinline__ void reattach2_body(const EngDev& E, const int* __res
     for (int k = 0; k < NPER; ++k) { const int e = lane + 32 * k; if (e < ld) xsm[e] = xr[k]; }
     __syncwarp();
     int lastmod = -1;
+    // levels above K1's action level where nothing changed in this launch and
+    // K1 descended (no merge) into an existing child group are stepped over
+    unsigned cleanmask = 0u;
+    if (!hc.trunc && hc.pred > 0 && hc.pred < len) {
+      bool cl = false;
+      if (lane < hc.pred) {
+        const ChainLvl& rl = S.rb[cur][lane];
+        const int g2 = rl.g, j2 = rl.j;
+        const bool bad = (g2 >= 0 && ((gbits[g2 >> 5] >> (g2 & 31)) & 1u)) || (j2 >= 0 && ((mbits[j2 >> 5] >> (j2 & 31)) & 1u));
+        cl = !bad && g2 >= 0 && j2 >= 0 && rl.child >= 0 && rl.take == 0;
+      }
+      cleanmask = __ballot_sync(PCY_FULL, cl);
+    }
 #ifdef PCY_TIMELINE
     tl_head += clock64() - tl_h0;
 #endif
     for (;;) {
+      if (!direct && ((cleanmask >> L) & 1u)) {   // unchanged level: K1's descent stands
+        g = S.rb[cur][L].child;
+        radius = rmul(radius, 0.25);
+        ++L;
+        continue;
+      }
       int bj = -1, li = -1;
       double bp = INFINITY;
 #ifdef PCY_TIMELINE

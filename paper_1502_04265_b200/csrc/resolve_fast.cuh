@@ -391,7 +391,7 @@ __device__ __forceinline__ void resolve2_body(const EngDev& E, const double* __r
 
 #ifdef PCY_TIMELINE
   const long long tl_t0 = clock64();
-  long long tl_wait = 0, tl_slow = 0, tl_start = 0, tl_clean = 0, tl_dem = 0, tl_fast = 0, tl_dir = 0, tl_new = 0, tl_cap = 0, tl_ndir = 0, tl_nnew = 0, tl_nlev = 0;
+  long long tl_wait = 0, tl_slow = 0, tl_start = 0, tl_clean = 0, tl_dem = 0, tl_fast = 0, tl_dir = 0, tl_new = 0, tl_cap = 0, tl_ndir = 0, tl_nnew = 0, tl_nlev = 0, tl_ncl = 0;
 #endif
   EngCtl* C = E.ctl;
   const long long m = E.m;
@@ -551,6 +551,10 @@ __device__ __forceinline__ void resolve2_body(const EngDev& E, const double* __r
     // ---- verified fast path: nothing on K1's path changed in this launch, so
     // every decision along it is K1's (same statistics, dots, members).
     bool done_fast = false;
+    // levels above K1's action level where nothing changed in this launch and
+    // K1 descended (no take) into an existing child group: the slow path below
+    // steps over them, as K1 did
+    unsigned cleanmask = 0u;
 #ifdef PCY_TIMELINE
     const long long tl_f0 = clock64();
 #endif
@@ -559,12 +563,15 @@ __device__ __forceinline__ void resolve2_body(const EngDev& E, const double* __r
       bool ok = pl >= 0 && pl < len;
       if (ok) {
         // one level per lane: a group that gained a member or a touched node fails
-        bool bad = false;
+        bool bad = false, cl = false;
         if (lane <= pl) {
-          const int g2 = S.rb[cur][lane].g, j2 = S.rb[cur][lane].j;
+          const ChainLvl& rl = S.rb[cur][lane];
+          const int g2 = rl.g, j2 = rl.j;
           bad = (g2 >= 0 && ((gbits[g2 >> 5] >> (g2 & 31)) & 1u)) || (j2 >= 0 && ((mbits[j2 >> 5] >> (j2 & 31)) & 1u));
+          cl = !bad && lane < pl && j2 >= 0 && rl.child >= 0 && rl.take == 0;
         }
         ok = !__any_sync(PCY_FULL, bad);
+        cleanmask = __ballot_sync(PCY_FULL, cl);
       }
       if (ok) {
         const ChainLvl& rp = S.rb[cur][pl];
@@ -605,6 +612,12 @@ __device__ __forceinline__ void resolve2_body(const EngDev& E, const double* __r
     tl_fast += tl_s0 - tl_f0;
 #endif
     if (!done_fast) for (;;) {
+      if (!direct && rem == wi && ((cleanmask >> L) & 1u)) {   // unchanged level: K1's descent stands
+        g = S.rb[cur][L].child;
+        radius = rmul(radius, 0.25);
+        ++L; ++c_lv;
+        continue;
+      }
       int bj = -1, li = -1;
       double bp = INFINITY;
       if (!direct) {
@@ -675,6 +688,9 @@ __device__ __forceinline__ void resolve2_body(const EngDev& E, const double* __r
       const bool touched = bt < 0 && ((mbits[bj >> 5] >> (bj & 31)) & 1u);
       if (bt < 0 && li >= 0 && !touched && rem == wi && !resume) {
         // untouched snapshot node on the first descent: K1's decision is exact
+#ifdef PCY_TIMELINE
+        if (!((gbits[g >> 5] >> (g & 31)) & 1u)) ++tl_ncl;
+#endif
         const ChainLvl& rc = S.rb[cur][li];
         nn = rc.w; qv = rc.q; snv = rc.sn; take = rc.take;
         if (take > 0) { nw2 = nn + take; nq = rc.nq; nsn = rc.nsn; }
@@ -837,7 +853,7 @@ __device__ __forceinline__ void resolve2_body(const EngDev& E, const double* __r
     // deltas of this subtree, then the last CTA publishes the window
     int lastf = 0;   // this CTA finished the window: its warp publishes
 #ifdef PCY_TIMELINE
-    if (lane == 0) { tl_cta(n, nnew, c_slow, clock64() - tl_t0); tl_split(n, tl_wait, tl_slow, tl_start, clock64() - tl_clean, tl_dem, tl_fast); tl_split2(n, tl_dir, tl_new, tl_cap, tl_ndir, tl_nnew, tl_nlev); }
+    if (lane == 0) { tl_cta(n, nnew, c_slow, clock64() - tl_t0); tl_split(n, tl_wait, tl_slow, tl_start, clock64() - tl_clean, tl_dem, tl_fast); tl_split2(n, tl_dir, tl_new, tl_cap, tl_ndir, tl_nnew, tl_nlev, tl_ncl); }
 #endif
     if (lane == 0) {
       using ull = unsigned long long;
