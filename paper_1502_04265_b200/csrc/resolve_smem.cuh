@@ -474,9 +474,20 @@ __device__ __forceinline__ void resolve3_body(const EngDev& E, const double* __r
 
     // ---- verified fast path (see k_resolve2)
     bool done_fast = false;
+    unsigned cleanmask = 0u;   // unchanged levels above K1's action level (see k_resolve2)
     if (!resume && len > 0 && !hc.trunc) {
       const int pl = hc.pred;
       bool ok = pl >= 0 && pl < len;
+      if (ok) {
+        bool cl = false;
+        if (lane < pl) {
+          const ChainLvl& rl = S.rb[cur][lane];
+          const int g2 = rl.g, j2 = rl.j;
+          const bool bad = (g2 >= 0 && ((gbits[g2 >> 5] >> (g2 & 31)) & 1u)) || (j2 >= 0 && ((mbits[j2 >> 5] >> (j2 & 31)) & 1u));
+          cl = !bad && g2 >= 0 && j2 >= 0 && rl.child >= 0 && rl.take == 0;
+        }
+        cleanmask = __ballot_sync(PCY_FULL, cl);
+      }
       for (int L2 = 0; ok && L2 <= pl; ++L2) {
         const int g2 = S.rb[cur][L2].g, j2 = S.rb[cur][L2].j;
         if (g2 >= 0 && ((gbits[g2 >> 5] >> (g2 & 31)) & 1u)) ok = false;
@@ -505,6 +516,12 @@ __device__ __forceinline__ void resolve3_body(const EngDev& E, const double* __r
       }
     }
     if (!done_fast) for (;;) {
+      if (!direct && rem == wi && ((cleanmask >> L) & 1u)) {   // unchanged level: K1's descent stands
+        g = S.rb[cur][L].child;
+        radius = rmul(radius, 0.25);
+        ++L; ++c_lv;
+        continue;
+      }
       int bj = -1, li = -1;
       double bp = INFINITY;
       if (!direct) {
@@ -826,7 +843,24 @@ __device__ __forceinline__ void reattach3_body(const EngDev& E, const int* __res
     double radius = T;
     bool direct = false;
     int lastmod = -1;
+    unsigned cleanmask = 0u;   // unchanged levels above K1's action level (see k_reattach2)
+    if (!hc.trunc && hc.pred > 0 && hc.pred < len) {
+      bool cl = false;
+      if (lane < hc.pred) {
+        const ChainLvl& rl = S.rb[cur][lane];
+        const int g2 = rl.g, j2 = rl.j;
+        const bool bad = (g2 >= 0 && ((gbits[g2 >> 5] >> (g2 & 31)) & 1u)) || (j2 >= 0 && ((mbits[j2 >> 5] >> (j2 & 31)) & 1u));
+        cl = !bad && g2 >= 0 && j2 >= 0 && rl.child >= 0 && rl.take == 0;
+      }
+      cleanmask = __ballot_sync(PCY_FULL, cl);
+    }
     for (;;) {
+      if (!direct && ((cleanmask >> L) & 1u)) {   // unchanged level: K1's descent stands
+        g = S.rb[cur][L].child;
+        radius = rmul(radius, 0.25);
+        ++L;
+        continue;
+      }
       int bj = -1, li = -1;
       double bp = INFINITY;
       if (!direct) {
