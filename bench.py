@@ -74,6 +74,7 @@ class ClockSampler:
         self.index = index
         self.proc = None
         self.lines = []
+        self.first = 0
 
     def start(self):
         try:
@@ -89,6 +90,16 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def wait_first(self, timeout: float = 3.0):
+        """Block until nvidia-smi printed its first sample (its start-up is over)."""
+        t0 = time.perf_counter()
+        while self.proc is not None and not self.lines and time.perf_counter() - t0 < timeout:
+            time.sleep(0.01)
+
+    def mark(self):
+        """Start of the timed region: earlier samples are dropped (unless no later one arrives)."""
+        self.first = len(self.lines)
+
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -99,7 +110,8 @@ class ClockSampler:
             self.proc.kill()
         sm, smax, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        timed = self.lines[self.first:] or self.lines
+        for ln in timed:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 9:
                 continue
@@ -419,14 +431,19 @@ def main():
         torch.cuda.synchronize()
         return 0
 
+    # nvidia-smi is started before the warm-up: its start-up (NVML initialisation
+    # holds driver locks for several hundred ms and stalled the launches of whatever
+    # steps it overlapped: 97 / 99 / 97 / 112 / 125 ms) then lands in untimed
+    # steps.  Only the samples taken inside the timed region are reported.
+    clocks = ClockSampler(local)
+    clocks.start()
+    clocks.wait_first()
     for _ in range(args.warmup):
         step_device()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-
-    clocks = ClockSampler(local)
-    clocks.start()
+    clocks.mark()
     l0 = nat.launch_count()
     st = torch.cuda.current_stream()
     evs = []
